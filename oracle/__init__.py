@@ -1,0 +1,277 @@
+"""CPU oracle for the dense CG / BiCGSTAB hot path (arXiv 1511.07174).
+
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this module.
+The product package ``paper_1511_07174_b200`` never imports it, and this module
+never imports the product.  The arithmetic lives in ``ks_oracle.c`` (plain C,
+sequential FP64 sums, ``-ffp-contract=off``); this file only marshals arguments
+through ctypes and builds the shared object with gcc when it is missing/stale.
+
+Parity status per function: every function below is
+pinned by a ``-m "not gpu"`` test in ``tests/test_oracle_*.py``; none is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ks_oracle.c")
+_HDR = os.path.join(_HERE, "ks_oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
+          "-std=c11", "-Wall"]
+
+OK, EARG, EDIM, ENOTSPD, EMAXIT, EBREAKDOWN, ESINGULAR = 0, 1, 2, 3, 4, 5, 6
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C, no CUDA)."""
+    stale = (not os.path.exists(_LIB)) or any(
+        os.path.getmtime(p) > os.path.getmtime(_LIB) for p in (_SRC, _HDR))
+    if force or stale:
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Report(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("matvecs", C.c_int64),
+                ("converged", C.c_int32), ("breakdown", C.c_int32),
+                ("half_step_exit", C.c_int32), ("status", C.c_int32),
+                ("relres", C.c_double)]
+
+
+class _Gen(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int64), ("seed", C.c_uint64),
+                ("kd", C.c_int32), ("table", C.POINTER(C.c_double))]
+
+
+class _Op(C.Structure):
+    _fields_ = [("n", C.c_int64), ("A", C.POINTER(C.c_double)), ("lda", C.c_int64),
+                ("gen", C.POINTER(_Gen)), ("threads", C.c_int32)]
+
+
+_lib = None
+_D = C.POINTER(C.c_double)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        i64, i32, u64, dbl = C.c_int64, C.c_int32, C.c_uint64, C.c_double
+        L.or_dot.restype = dbl
+        L.or_dot.argtypes = [i64, _D, _D]
+        L.or_nrm2.restype = dbl
+        L.or_nrm2.argtypes = [i64, _D]
+        L.or_axpy.argtypes = [i64, dbl, _D, _D]
+        L.or_gemv.argtypes = [i64, i64, _D, i64, _D, _D, i32]
+        L.or_op_rows.argtypes = [C.POINTER(_Op), i64, i64, _D, _D]
+        L.or_cg.restype = C.c_int
+        L.or_cg.argtypes = [C.POINTER(_Op), _D, _D, dbl, i64, _D, _D, i64, C.POINTER(_Report),
+                            _D, _D, _D, i64]
+        L.or_bicgstab.restype = C.c_int
+        L.or_bicgstab.argtypes = [C.POINTER(_Op), _D, _D, dbl, i64, _D, _D, i64,
+                                  C.POINTER(_Report), _D, _D, i64]
+        L.or_ge_solve_ld.restype = C.c_int
+        L.or_ge_solve_ld.argtypes = [i64, _D, i64, _D, _D]
+        L.or_spd_exact_solve_ld.argtypes = [i64, _D, u64, _D, _D]
+        L.or_true_relres_ld.restype = dbl
+        L.or_true_relres_ld.argtypes = [C.POINTER(_Op), _D, _D]
+        L.or_hash.restype = u64
+        L.or_hash.argtypes = [u64, u64, u64]
+        L.or_gen_rows.argtypes = [C.POINTER(_Gen), i64, i64, _D, i64]
+        L.or_gen_rhs.argtypes = [i64, u64, _D]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_D)
+
+
+def _vec(a, n=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if n is not None and a.shape != (n,):
+        raise ValueError(f"expected shape ({n},), got {a.shape}")
+    return a
+
+
+@dataclass
+class Report:
+    iterations: int
+    matvecs: int
+    converged: bool
+    breakdown: bool
+    half_step_exit: bool
+    status: int
+    relres: float
+
+
+class Operator:
+    """A stored row-major matrix, or a generator spec expanded row by row."""
+
+    def __init__(self, A=None, *, gen: dict | None = None, threads: int = 1):
+        self._keep = []
+        if A is not None:
+            A = np.ascontiguousarray(A, dtype=np.float64)
+            if A.ndim != 2 or A.shape[0] != A.shape[1]:
+                raise ValueError("A must be square")
+            self.n = A.shape[0]
+            self._keep.append(A)
+            self._op = _Op(self.n, _p(A), A.shape[1], None, threads)
+        else:
+            g = gen
+            self.n = int(g["n"])
+            table = g.get("table")
+            if table is not None:
+                table = _vec(table, self.n)
+                self._keep.append(table)
+            self._gen = _Gen(int(g["kind"]), self.n, int(g["seed"]), int(g.get("kd", 1)),
+                             _p(table))
+            self._op = _Op(self.n, None, 0, C.pointer(self._gen), threads)
+
+    @property
+    def ref(self):
+        return C.byref(self._op)
+
+    def rows(self, r0: int, nrows: int, x) -> np.ndarray:
+        """y[r] = sum_j a_{r0+r, j} x_j, sequential per row."""
+        x = _vec(x, self.n)
+        y = np.empty(nrows)
+        lib().or_op_rows(self.ref, r0, nrows, _p(x), _p(y))
+        return y
+
+    def apply(self, x) -> np.ndarray:
+        return self.rows(0, self.n, x)
+
+
+def _as_op(A) -> Operator:
+    return A if isinstance(A, Operator) else Operator(A)
+
+
+def dot(x, y) -> float:
+    x, y = _vec(x), _vec(y)
+    return lib().or_dot(x.size, _p(x), _p(y))
+
+
+def nrm2(x) -> float:
+    x = _vec(x)
+    return lib().or_nrm2(x.size, _p(x))
+
+
+def axpy(alpha, x, y) -> np.ndarray:
+    x, y = _vec(x), _vec(y).copy()
+    lib().or_axpy(x.size, float(alpha), _p(x), _p(y))
+    return y
+
+
+def gemv(A, x, threads: int = 1) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    x = _vec(x, A.shape[1])
+    y = np.empty(A.shape[0])
+    lib().or_gemv(A.shape[0], A.shape[1], _p(A), A.shape[1], _p(x), _p(y), threads)
+    return y
+
+
+def _rep(r: _Report) -> Report:
+    return Report(int(r.iterations), int(r.matvecs), bool(r.converged), bool(r.breakdown),
+                  bool(r.half_step_exit), int(r.status), float(r.relres))
+
+
+def cg(A, b, x0=None, tol=1e-8, maxit=None, trace: int = 0):
+    """SURVEY.md sec.8(c).3.  Returns (x, hist, report[, trace dict])."""
+    op = _as_op(A)
+    n = op.n
+    b = _vec(b, n)
+    x0 = None if x0 is None else _vec(x0, n)
+    maxit = 10 * n if maxit is None else int(maxit)
+    x = np.empty(n)
+    hist = np.zeros(max(maxit, 1))
+    rep = _Report()
+    tx = tr = tp = None
+    if trace:
+        tx, tr, tp = (np.zeros((trace, n)) for _ in range(3))
+    lib().or_cg(op.ref, _p(b), _p(x0), float(tol), maxit, _p(x), _p(hist), maxit,
+                C.byref(rep), _p(tx), _p(tr), _p(tp), trace)
+    R = _rep(rep)
+    out = (x, hist[:min(R.iterations, maxit)].copy(), R)
+    if trace:
+        return out + ({"x": tx, "r": tr, "p": tp},)
+    return out
+
+
+def bicgstab(A, b, x0=None, tol=1e-8, maxit=None, trace: int = 0):
+    """SURVEY.md sec.8(c).4.  Returns (x, hist, report[, trace dict])."""
+    op = _as_op(A)
+    n = op.n
+    b = _vec(b, n)
+    x0 = None if x0 is None else _vec(x0, n)
+    maxit = 10 * n if maxit is None else int(maxit)
+    x = np.empty(n)
+    hist = np.zeros(max(maxit, 1))
+    rep = _Report()
+    ts = tr = None
+    if trace:
+        ts, tr = np.zeros((trace, n)), np.zeros((trace, n))
+    lib().or_bicgstab(op.ref, _p(b), _p(x0), float(tol), maxit, _p(x), _p(hist), maxit,
+                      C.byref(rep), _p(ts), _p(tr), trace)
+    R = _rep(rep)
+    out = (x, hist[:min(R.iterations, maxit)].copy(), R)
+    if trace:
+        return out + ({"s": ts, "r": tr},)
+    return out
+
+
+def ge_solve_ld(A, b) -> np.ndarray:
+    """Long-double Gaussian elimination with partial pivoting (pin P5)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    b = _vec(b, n)
+    x = np.empty(n)
+    st = lib().or_ge_solve_ld(n, _p(A), n, _p(b), _p(x))
+    if st != OK:
+        raise np.linalg.LinAlgError(f"or_ge_solve_ld status {st}")
+    return x
+
+
+def spd_exact_solve_ld(table, seed: int, b) -> np.ndarray:
+    """Closed-form solution of the G-SPD system (pin P6)."""
+    table = _vec(table)
+    n = table.size
+    b = _vec(b, n)
+    x = np.empty(n)
+    lib().or_spd_exact_solve_ld(n, _p(table), int(seed), _p(b), _p(x))
+    return x
+
+
+def true_relres_ld(A, b, x) -> float:
+    op = _as_op(A)
+    b, x = _vec(b, op.n), _vec(x, op.n)
+    return lib().or_true_relres_ld(op.ref, _p(b), _p(x))
+
+
+def hash64(seed: int, stream: int, key: int) -> int:
+    return int(lib().or_hash(seed, stream, key))
+
+
+def gen_rows(gen: dict, r0: int, nrows: int) -> np.ndarray:
+    n = int(gen["n"])
+    op = Operator(gen=gen)
+    A = np.empty((nrows, n))
+    lib().or_gen_rows(op._op.gen, r0, nrows, _p(A), n)
+    return A
+
+
+def gen_rhs(n: int, seed: int) -> np.ndarray:
+    b = np.empty(n)
+    lib().or_gen_rhs(n, int(seed), _p(b))
+    return b
