@@ -1,0 +1,383 @@
+"""Benchmark of the dense FP64 CG / BiCGSTAB hot path (BASELINE.json metric
+"CG/BiCGSTAB iters/s & GEMV HBM GB/s vs peak, n=65536 FP64, 1/2/4/8 B200").
+
+Workload (config C3/C3' of SURVEY.md sec.8(d).3): n = 65536, FP64, A row-block
+sharded over N GPUs (strong scaling).  Two matrices are resident in HBM:
+G-SPD(65536, kappa=1e4) for CG and G-DD(65536, kd=16) for BiCGSTAB (seed
+151107174, generated on the device).  One STEP = one CG iteration + one BiCGSTAB
+iteration = every row of sec.8(a) (3 GEMVs, 3 x 8 n^2 / N bytes per GPU).
+value = steps/s for the whole job.  Timed: K steps = ks_cg(maxit=K) +
+ks_bicgstab(maxit=K) with tol = 0 (fixed length), inputs resident on the device,
+bracketed by barrier + synchronize, CUDA events on the stream the library runs
+on (torch's current stream, borrowed), max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 65536]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the CPU oracle (oracle/, the only baseline this paper
+has) on a bounded row sample of the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "CG/BiCGSTAB iters/s & GEMV HBM GB/s vs peak, n=65536 FP64, 1/2/4/8 B200"
+UNIT = "steps/s (step = 1 CG iter + 1 BiCGSTAB iter)"
+SEED = 151107174
+NOMINAL_HBM = 8000.0   # GB/s, north star's "~8 TB/s"
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def clocks_bad(c):
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if bad & set(c.get("reasons", [])):
+        return True
+    if c.get("sm_mhz") and c.get("sm_max_mhz") and not c["reasons"]:
+        return c["sm_mhz"] < 0.5 * c["sm_max_mhz"]
+    return False
+
+
+# ------------------------------------------------------------ CPU oracle
+
+def oracle_step_sample(n: int, rows: int, threads: int, budget_s: float, steps: int | None = None,
+                       warmup: int = 0):
+    """Times the CPU oracle on a bounded row sample of the bench workload: per
+    step the 3 GEMVs of one CG + one BiCGSTAB iteration (oracle or_gemv:
+    sequential FP64 row sums, rows spread over `threads` OpenMP threads -- bitwise
+    equal to 1 thread) on `rows` rows of each n-wide matrix, extrapolated x n/rows,
+    plus the O(n) vector work of both iterations (10 full-length dots/axpys)."""
+    import oracle
+    import synth
+    r0 = n // 2 - rows // 2
+    Aspd = oracle.gen_rows(synth.spec("spd", n, kappa=1e4, seed=SEED), r0, rows)
+    Add = oracle.gen_rows(synth.spec("dd", n, kd=16, seed=SEED), r0, rows)
+    x = synth.rhs(n, SEED)
+    y = np.empty(rows)
+    L = oracle.lib()
+    P = oracle._p
+
+    def one():
+        t0 = time.perf_counter()
+        L.or_gemv(rows, n, P(Aspd), n, P(x), P(y), threads)   # CG:       q = A p
+        L.or_gemv(rows, n, P(Add), n, P(x), P(y), threads)    # BiCGSTAB: v = A p
+        L.or_gemv(rows, n, P(Add), n, P(x), P(y), threads)    # BiCGSTAB: t = A s
+        t1 = time.perf_counter()
+        z = x.copy()
+        for _ in range(5):
+            oracle.dot(x, z)
+            z = oracle.axpy(0.5, x, z)
+        return t1 - t0, time.perf_counter() - t1
+
+    for _ in range(warmup):
+        one()
+    g, v = [], []
+    t_start = time.perf_counter()
+    while True:
+        a, b = one()
+        g.append(a)
+        v.append(b)
+        if steps is not None and len(g) >= steps:
+            break
+        if steps is None and time.perf_counter() - t_start >= budget_s:
+            break
+    full = statistics.mean(g) * (n / rows) + statistics.mean(v)
+    return {"value": 1.0 / full, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"rows [{r0},{r0 + rows}) of G-SPD(n={n},1e4) and G-DD(n={n},16): 3 oracle "
+                      f"GEMVs per step (sequential FP64 row sums, OpenMP over rows on {threads} "
+                      f"threads), extrapolated x{n / rows:.0f}, + 10 full-length oracle dot/axpy; "
+                      f"{len(g)} sampled steps",
+            "seconds_per_step": full, "sampled_steps": len(g)}
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n = args.n
+    rows = max(64, min(n, args.ref_rows))
+    t0 = time.perf_counter()
+    cpu = oracle_step_sample(n, rows, threads, budget_s=0, steps=args.steps, warmup=args.warmup)
+    wall = time.perf_counter() - t0
+    line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / cpu["value"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C3: n={n} FP64 dense; CG on G-SPD(1e4) + BiCGSTAB on G-DD(16)",
+                       "n": n, "parallelism": "cpu oracle, rank 0 only"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- our path
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1511_07174_b200 as ks
+    import synth
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if args.gpus != world:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, K, W = args.n, args.steps, args.warmup
+    stream = torch.cuda.current_stream()
+
+    def mk():
+        if world > 1:
+            return ks.Context.from_process_group(n)
+        return ks.Context.from_rank(n, 0, 1, None, local, stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    t_gen = time.perf_counter()
+    cg_ctx, bs_ctx = mk(), mk()
+    table = synth.spd_table(n, 1e4, SEED)
+    b_cg = cg_ctx.generate("spd", seed=SEED, table=table)
+    b_bs = bs_ctx.generate("dd", seed=SEED, kd=16)
+    t_gen = time.perf_counter() - t_gen
+    for c in (cg_ctx, bs_ctx):
+        c.set_option("true_residual", 0)
+        c.set_option("profile_gemv", 1)
+    row_b, row_e = cg_ctx.row_range(rank)
+    m = row_e - row_b
+
+    bd_cg = torch.from_numpy(b_cg).to(dev)
+    bd_bs = torch.from_numpy(b_bs).to(dev)
+    xd = torch.empty(n, dtype=torch.float64, device=dev)
+
+    def device_steps(k):
+        _, _, r1 = cg_ctx.cg(bd_cg, tol=0.0, maxit=k, out=xd, hist=False)
+        _, _, r2 = bs_ctx.bicgstab(bd_bs, tol=0.0, maxit=k, out=xd, hist=False)
+        assert r1.iterations == k and r2.iterations == k, (r1, r2)
+        return r1, r2
+
+    device_steps(W)                               # warm-up (W >= 3 steps)
+    torch.cuda.synchronize()
+
+    def timed():
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as cs:
+            e0.record(stream)
+            r1, r2 = device_steps(K)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        return e0.elapsed_time(e1) * 1e-3, r1, r2, cs.summary()
+
+    sec, r_cg, r_bs, clocks = timed()
+    remeasured = False
+    if clocks_bad(clocks):
+        sec, r_cg, r_bs, clocks = timed()
+        remeasured = True
+    sec = allmax(sec)
+    cg_loop, bs_loop = allmax(r_cg.seconds_loop), allmax(r_bs.seconds_loop)
+    gemv_s = allmax(r_cg.seconds_gemv + r_bs.seconds_gemv)
+    gemv_n = r_cg.gemv_launches + r_bs.gemv_launches
+    launches = allsum(float(r_cg.kernel_launches + r_bs.kernel_launches))
+
+    # e2e: the public API with HOST (pinned) buffers, H2D/D2H inside the region
+    bh_cg = torch.from_numpy(b_cg).pin_memory()
+    bh_bs = torch.from_numpy(b_bs).pin_memory()
+    xh = torch.empty(n, dtype=torch.float64).pin_memory()
+    hh = torch.empty(K, dtype=torch.float64).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    cg_ctx.cg(bh_cg, tol=0.0, maxit=K, out=xh, hist=hh)
+    bs_ctx.bicgstab(bh_bs, tol=0.0, maxit=K, out=xh, hist=hh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_wall = time.perf_counter() - t0
+    e2e_s = allmax(max(e0.elapsed_time(e1) * 1e-3, e2e_wall))
+    barrier()
+
+    # roofline of the dominant kernel (K1 GEMV): algorithmic bytes 8*m*n per launch
+    gemv_avg = gemv_s / max(1, gemv_n)
+    achieved = 8.0 * m * n / gemv_avg / 1e9
+    peak, peak_kind = measured_peak()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    if os.path.exists(tp):
+        try:
+            t = json.load(open(tp))
+            if int(t.get("n", -1)) == n and int(t.get("P", -1)) == world:
+                traffic = t.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = oracle_step_sample(n, args.cpu_rows, os.cpu_count() or 1, budget_s=args.cpu_budget)
+        value = K / sec
+        T_roof = lambda g: g * 8.0 * n * n / world / (NOMINAL_HBM * 1e9) + \
+            g * 8.0 * n * (world - 1) / world / 0.9e12
+        cg_ips, bs_ips = K / cg_loop, K / bs_loop
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": 1e3 * sec / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (G-SPD kappa=1e4 + G-DD kd=16, seed 151107174, generated on device)",
+            "config": {"workload": f"C3/C3': n={n} FP64 dense, CG on G-SPD(1e4) + BiCGSTAB on "
+                                   f"G-DD(16), row-block over {world} GPU(s), tol=0 fixed length",
+                       "n": n, "global_batch": 1, "parallelism": f"row-block P={world}",
+                       "l2": f"no flush needed: resident inputs {2 * 8 * m * n / 1e9:.1f} GB/GPU "
+                             f">> 126 MB L2"},
+            "per_method": {
+                "cg_iters_per_s": cg_ips, "bicgstab_iters_per_s": bs_ips,
+                "cg_frac_of_roofline_8TBps": cg_ips * T_roof(1),
+                "bicgstab_frac_of_roofline_8TBps": bs_ips * T_roof(2),
+                "cg_target_80pct_1gpu": 186.3, "bicgstab_target_80pct_1gpu": 93.1},
+            "roofline": {"bound": "hbm", "kernel": "k1_gemv (K1)", "achieved": achieved,
+                         "peak": peak, "peak_kind": f"{peak_kind} copy GB/s (MEASURED_PEAKS.json)",
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": 8.0 * m * n,
+                         "avg_launch_ms": gemv_avg * 1e3, "frac_of_nominal_8TBps": achieved / NOMINAL_HBM,
+                         "gemv_share_of_step": gemv_s / sec},
+            "e2e": {"value": K / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": 2 * 8 * n / K,
+                    "d2h_bytes_per_step": 2 * 8 * (n + K) / K},
+            "gpu_launches": int(launches),
+            "clocks": clocks, "remeasured": remeasured,
+            "cpu_baseline": cpu,
+            "generate_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    cg_ctx.close()
+    bs_ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=env_int("WORLD_SIZE", 1))
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--cpu-rows", type=int, default=2048)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,168 @@
+/*
+ * include/ks.h -- C ABI of the B200-native dense Krylov hot path (arXiv 1511.07174).
+ *
+ * What it computes.  The per-iteration body of the paper's non-stationary Krylov
+ * solvers on a dense matrix: "inner products, saxpy and matrix-vector products
+ * that has the complexity of O(n^2)" (sec.2) for CG on SPD systems
+ * and BiCGSTAB on nonsymmetric systems (sec.2; listed as
+ * implemented at PAPER.md:78 and PAPER.md:109).  The recurrences are the
+ * textbook ones written out in SURVEY.md sec.8(c).3 (CG) and sec.8(c).4
+ * (BiCGSTAB); every reading of a point the paper leaves open is listed in
+ * DESIGN.md ("Readings", Q1-Q26).  Parallelism is hidden behind an opaque
+ * object, as the paper asks ("encapsulation of data and distribution and
+ * communication in opaque objects").
+ *
+ * Layout.  A is n x n, ROW-MAJOR (element (i,j) at A[i*lda + j]), FP64.  It is
+ * split into contiguous row blocks, one per GPU: shard g owns rows
+ * [g*floor(n/P) + min(g, n mod P), ...) (ks_row_range).  On the device each row
+ * is padded to a multiple of 512 doubles (4 KiB); the padding is zero.
+ *
+ * Pointers.  Every vector argument of ks_matvec / ks_cg / ks_bicgstab may be
+ * host memory (pageable or pinned) or CUDA device memory: copies use
+ * cudaMemcpyDefault (unified addressing).  Buffers are owned by the caller,
+ * read or written only during the call, never retained.  Every call is
+ * synchronous: it returns after its outputs are in the caller's memory.
+ *
+ * Errors.  Every call returns a ks_status.  Argument errors (KS_EARG, KS_EDIM)
+ * are detected before any work.  KS_ECUDA / KS_ENCCL / KS_ENOMEM poison the
+ * context: later calls return KS_ESTATE except ks_destroy.  The library never
+ * aborts, exits, prints or throws across this ABI; ks_last_error() returns a
+ * message.  A context is used by one caller thread at a time.
+ */
+#ifndef KS_H
+#define KS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ks_ctx ks_ctx; /* opaque handle */
+
+typedef enum { KS_FLOAT64 = 0 /* KS_FLOAT32 reserved */ } ks_dtype;
+
+typedef enum {
+    KS_OK = 0,         /* converged (or call succeeded)                         */
+    KS_EARG = 1,       /* invalid argument                                      */
+    KS_EDIM = 2,       /* dimension mismatch          (SPEC.md:675 exit code 2) */
+    KS_ENOTSPD = 3,    /* CG: <p, A p> <= 0 or non-finite      (exit code 3)    */
+    KS_EMAXIT = 4,     /* maxit reached without convergence    (exit code 4)    */
+    KS_EBREAKDOWN = 5, /* BiCGSTAB scalar exactly 0 / non-finite (exit code 5)  */
+    KS_ECUDA = 6,      /* CUDA runtime error (poisons the context)              */
+    KS_ENCCL = 7,      /* NCCL error (poisons the context)                      */
+    KS_ENOMEM = 8,     /* device allocation failed (poisons the context)        */
+    KS_ESTATE = 9      /* context poisoned, or matrix not fully loaded          */
+} ks_status;
+
+typedef struct {
+    int64_t iterations;    /* completed loop bodies (Q3); the setup     */
+                           /* GEMV r0 = b - A x0 is never counted                  */
+    int64_t matvecs;       /* CG: iterations; BiCGSTAB: 2*iterations - half_step   */
+    int32_t converged;     /* 1 if relres <= tol                                   */
+    int32_t breakdown;     /* 1 on a BiCGSTAB breakdown                            */
+    int32_t half_step_exit;/* 1 if BiCGSTAB stopped on ||s||         */
+    int32_t status;        /* the ks_status the call returned                      */
+    double relres;         /* recurrence ||r_k||/||b|| at exit (Q1)                 */
+    double true_relres;    /* ||b - A x||/||b|| with one extra GEMV (or -1 if off) */
+    double seconds_loop;   /* CUDA-event time of the iteration loop (max over      */
+                           /* this context's GPUs); excludes setup and copies      */
+    double seconds_total;  /* host wall-clock of the whole call                    */
+    double seconds_gemv;   /* sum of K1 GEMV launch durations inside the loop      */
+                           /* (CUDA events; 0 unless KS_OPT_PROFILE_GEMV = 1)      */
+    int64_t gemv_launches; /* K1 launches inside the loop (per GPU)                */
+    int64_t kernel_launches; /* all library kernel launches of the call (per GPU)  */
+} ks_report;
+
+/* Synthetic-input generator spec.
+ *   kind 0 = G-SPD: A_ij = s_i s_j c[(i-j) mod n]; spd_table = c (host, n doubles,
+ *            borrowed during the call), s_i = 1 - 2 (H(seed,4,i) >> 63).
+ *   kind 1 = G-DD : dense nonsymmetric, strictly row-diagonally dominant, exact
+ *            dyadic entries; kd = number of diagonal classes.
+ *   b_i = 2 U53(seed,2,i) - 1.  H is SplitMix64 as specified in DESIGN.md.     */
+typedef struct {
+    int32_t kind;
+    uint64_t seed;
+    double kappa;             /* informational for G-SPD (the table fixes A)      */
+    int32_t kd;
+    const double* spd_table;
+} ks_gen_spec;
+
+typedef enum {
+    KS_OPT_TRUE_RESIDUAL = 0, /* 1 (default): report true_relres (one extra GEMV) */
+    KS_OPT_PROFILE_GEMV = 1,  /* 1: time every K1 launch with CUDA events         */
+    KS_OPT_POLL_BATCH = 2,    /* iterations queued between done-flag polls (16)   */
+    KS_OPT_GEMV_ROWS = 3,     /* K1 rows per CTA tile: 4, 8 or 16 (default 0=auto)*/
+    KS_OPT_GEMV_SPLIT = 4,    /* K1 column splits per tile (0 = auto)             */
+    KS_OPT_GEMV_KERNEL = 5,   /* K1 variant: 0 = auto, 1 = LDG stream, 2 = TMA    */
+                              /* bulk-copy ring                                   */
+    KS_OPT_USE_GRAPHS = 6     /* 1: replay each poll batch as a CUDA graph        */
+} ks_option;
+
+/* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL
+ * communicator from ncclCommInitAll when ngpus > 1).  n >= 1, 1 <= ngpus <= 16
+ * and <= device count, dtype = KS_FLOAT64.  Allocates each shard (m_g x ld FP64)
+ * plus O(n) vectors with cudaMalloc and zero-fills them.                        */
+ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
+
+/* One rank of a multi-process job (one process per GPU, e.g. torchrun).
+ * nccl_comm: a BORROWED ncclComm_t of nranks ranks (e.g. torch's
+ * ProcessGroupNCCL._comm_ptr()), or NULL when nranks == 1.  stream: a BORROWED
+ * cudaStream_t on `device` (NULL -> the context creates its own).  Both must
+ * outlive the context.  The shard of this rank is ks_row_range(ctx, rank).      */
+ks_status ks_create_rank(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t rank, int32_t nranks,
+                         void* nccl_comm, int32_t device, void* stream);
+
+/* Frees every device allocation of the context (never the borrowed comm/stream). */
+ks_status ks_destroy(ks_ctx* ctx);
+
+/* Row range [*row_begin, *row_end) of shard `shard` (0 <= shard < P). */
+ks_status ks_row_range(const ks_ctx* ctx, int32_t shard, int64_t* row_begin, int64_t* row_end);
+
+/* Copies rows [row_begin, row_begin + nrows) of A (row-major, leading dimension
+ * lda >= n; row r of the argument is global row row_begin + r) into the shards
+ * that own them; rows owned by other ranks of a multi-process job are ignored.
+ * Rows may be loaded in any chunks; a reloaded row is overwritten.               */
+ks_status ks_load_rows(ks_ctx* ctx, int64_t row_begin, int64_t nrows, const double* A, int64_t lda);
+
+/* Expands the generator spec on the device into every shard (K0), and writes b
+ * (n doubles, generated on the device) to b_out if non-NULL.                    */
+ks_status ks_generate(ks_ctx* ctx, const ks_gen_spec* spec, double* b_out);
+
+/* y = A x (n doubles each).  The plain GEMV building block.        */
+ks_status ks_matvec(ks_ctx* ctx, const double* x, double* y);
+
+/* Times `reps` back-to-back K1 GEMV launches on device-resident data with CUDA
+ * events; *seconds_per_matvec = elapsed/reps (max over this context's GPUs).    */
+ks_status ks_time_matvec(ks_ctx* ctx, int32_t reps, double* seconds_per_matvec);
+
+/* CG.  b: n doubles (required).  x0: n doubles or NULL
+ * (zero start).  tol >= 0 (tol = 0 runs exactly maxit iterations unless r = 0).
+ * maxit >= 0.  x: n doubles (required), receives the last complete iterate.
+ * hist: NULL or hist_cap doubles; receives min(iterations, hist_cap) values
+ * ||r_k||/||b||, k = 1..iterations (Q4).  rep: NULL or filled.
+ * Returns KS_OK, KS_EMAXIT, KS_ENOTSPD, or an error.  b = 0 -> x = 0, KS_OK.   */
+ks_status ks_cg(ks_ctx* ctx, const double* b, const double* x0, double tol, int64_t maxit,
+                double* x, double* hist, int64_t hist_cap, ks_report* rep);
+
+/* BiCGSTAB: shadow residual rhat = r0; exact-zero or
+ * non-finite scalars -> KS_EBREAKDOWN with x = last complete iterate; a
+ * half-step exit records ||s_i||/||b|| as the last history value.               */
+ks_status ks_bicgstab(ks_ctx* ctx, const double* b, const double* x0, double tol, int64_t maxit,
+                      double* x, double* hist, int64_t hist_cap, ks_report* rep);
+
+ks_status ks_set_option(ks_ctx* ctx, ks_option opt, int64_t value);
+ks_status ks_get_option(const ks_ctx* ctx, ks_option opt, int64_t* value);
+
+/* Number of GPUs (shards) this context drives locally, and the global P.        */
+ks_status ks_info(const ks_ctx* ctx, int32_t* local_gpus, int32_t* nranks, int64_t* n, int64_t* ld);
+
+/* Last error message of ctx (or of the calling thread when ctx == NULL).         */
+const char* ks_last_error(const ks_ctx* ctx);
+
+/* Library version string, e.g. "ks 0.1 sm_100a". */
+const char* ks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_H */

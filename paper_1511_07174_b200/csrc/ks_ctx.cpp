@@ -1,0 +1,155 @@
+// L3 context: partition, device allocation, NCCL plumbing, worker threads.
+#include "ks_ctx.h"
+
+#include <algorithm>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+namespace ks {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    const ks_status code = (e == cudaErrorMemoryAllocation) ? KS_ENOMEM : KS_ECUDA;
+    throw KsError(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return;
+    throw KsError(KS_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+VecArgs Rank::vargs() const {
+    VecArgs a;
+    a.L = L;
+    a.st = st;
+    a.hist = hist;
+    a.b_full = b_full;
+    a.x_loc = x_loc;
+    a.p_full = p_full;
+    a.s_full = s_full;
+    a.q_loc = q_loc;
+    a.rhat_loc = rhat_loc;
+    a.G_r = G_r;
+    a.G_v = G_v;
+    a.S = S;
+    a.scr = scr;
+    a.num_sms = num_sms;
+    return a;
+}
+
+template <class T>
+static void dmalloc(T** p, size_t count) {
+    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+    KS_CUDA(cudaMemset(*p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+}
+
+void rank_alloc(ks_ctx* c, Rank& r) {
+    KS_CUDA(cudaSetDevice(r.dev));
+    KS_CUDA(cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, r.dev));
+    if (!r.stream) {
+        KS_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
+        r.own_stream = true;
+    }
+    const int64_t ld = c->ld;
+    const size_t P = (size_t)c->P;
+    dmalloc(&r.A, (size_t)r.m * (size_t)ld);     // zero padding columns [n, ld)
+    dmalloc(&r.b_full, ld);
+    dmalloc(&r.x_loc, r.m + 64);
+    dmalloc(&r.p_full, ld);
+    dmalloc(&r.s_full, ld);
+    dmalloc(&r.q_loc, r.m + 64);
+    dmalloc(&r.rhat_loc, r.m + 64);
+    dmalloc(&r.G_r, P * (size_t)r.L.chunk);
+    dmalloc(&r.G_v, P * (size_t)r.L.chunk);
+    dmalloc(&r.S, P * kScalSlot);
+    dmalloc(&r.st, 1);
+    r.hist_alloc = 1024;
+    dmalloc(&r.hist, r.hist_alloc);
+    dmalloc(&r.scr.part, (size_t)kNumTickets * kPartStride);
+    dmalloc(&r.scr.ticket, kNumTickets);
+    r.scr.tile_cap = r.m / 4 + 2;
+    r.scr.qpart_cap = std::max<int64_t>(2 * 6 * 2 * 160 * 16 + 4096, 2 * r.scr.tile_cap + 4096);
+    dmalloc(&r.scr.qpart, r.scr.qpart_cap);
+    dmalloc(&r.scr.tile_ticket, r.scr.tile_cap);
+    KS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&r.h_done), 2 * sizeof(int)));
+    KS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&r.h_state), sizeof(DevState)));
+    for (auto& e : r.ev_poll) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    KS_CUDA(cudaEventCreate(&r.ev_t0));
+    KS_CUDA(cudaEventCreate(&r.ev_t1));
+    r.loaded.assign((size_t)r.m, 0);
+    r.loaded_count = 0;
+    KS_CUDA(cudaDeviceSynchronize());
+}
+
+void rank_free(Rank& r) {
+    if (cudaSetDevice(r.dev) != cudaSuccess) return;
+    cudaDeviceSynchronize();
+    for (void* p : {(void*)r.A, (void*)r.b_full, (void*)r.x_loc, (void*)r.p_full, (void*)r.s_full,
+                    (void*)r.q_loc, (void*)r.rhat_loc, (void*)r.G_r, (void*)r.G_v, (void*)r.S,
+                    (void*)r.st, (void*)r.hist, (void*)r.scr.part, (void*)r.scr.ticket,
+                    (void*)r.scr.qpart, (void*)r.scr.tile_ticket, (void*)r.table_tmp})
+        if (p) cudaFree(p);
+    if (r.h_done) cudaFreeHost(r.h_done);
+    if (r.h_state) cudaFreeHost(r.h_state);
+    for (auto e : r.ev_poll) if (e) cudaEventDestroy(e);
+    if (r.ev_t0) cudaEventDestroy(r.ev_t0);
+    if (r.ev_t1) cudaEventDestroy(r.ev_t1);
+    for (auto e : r.ev_gemv) cudaEventDestroy(e);
+    r.ev_gemv.clear();
+    if (r.own_comm && r.comm) ncclCommDestroy(r.comm);
+    if (r.own_stream && r.stream) cudaStreamDestroy(r.stream);
+    r = Rank{};
+}
+
+// In-place allgather of one chunk per rank (count_per_rank doubles at G + rank*chunk).
+void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank) {
+    if (c->P == 1) return;
+    KS_NCCL(ncclAllGather(G + (int64_t)r.rank * count_per_rank, G, (size_t)count_per_rank,
+                          ncclDouble, r.comm, r.stream));
+}
+
+// Copies the P row slices held in chunk layout to a contiguous n-vector.
+void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cudaMemcpyKind kind) {
+    for (int g = 0; g < c->P; ++g) {
+        const int64_t b = r.L.row0[g], e = r.L.row0[g + 1];
+        if (e > b)
+            KS_CUDA(cudaMemcpyAsync(dst + b, G + (int64_t)g * r.L.chunk, (size_t)(e - b) * sizeof(double),
+                                    kind, r.stream));
+    }
+}
+
+GemvConfig gemv_config(const ks_ctx* c, const Rank& r) {
+    GemvConfig g = choose_gemv(r.m, c->ld, r.num_sms, (int)c->opt.gemv_rows, (int)c->opt.gemv_split,
+                               (int)c->opt.gemv_kernel);
+    const int64_t tiles = (r.m + g.rows - 1) / g.rows;
+    const int64_t cap = (r.scr.qpart_cap - 2 * tiles - 64) / std::max<int64_t>(1, tiles * g.rows);
+    if (g.splits > cap) g.splits = (int)std::max<int64_t>(1, cap);
+    return g;
+}
+
+}  // namespace ks
+
+void ks_ctx::for_each_rank(const std::function<void(ks::Rank&)>& fn) {
+    if (ranks.size() == 1) {
+        ks::cuda_check(cudaSetDevice(ranks[0].dev), "cudaSetDevice");
+        fn(ranks[0]);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::exception_ptr first;
+    std::mutex mu;
+    for (auto& r : ranks) {
+        th.emplace_back([&, rp = &r] {
+            try {
+                ks::cuda_check(cudaSetDevice(rp->dev), "cudaSetDevice");
+                fn(*rp);
+            } catch (...) {
+                std::lock_guard<std::mutex> g(mu);
+                if (!first) first = std::current_exception();
+            }
+        });
+    }
+    for (auto& t : th) t.join();
+    if (first) std::rethrow_exception(first);
+}

@@ -1,0 +1,109 @@
+// L3: the opaque context -- "encapsulation of data and distribution and
+// communication in opaque objects".  1-D row-block partition of A
+// over P GPUs, one Rank per local GPU.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ks_internal.h"
+
+namespace ks {
+
+struct KsError : std::runtime_error {
+    ks_status code;
+    KsError(ks_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+void nccl_check(ncclResult_t r, const char* what);
+#define KS_CUDA(x) ::ks::cuda_check((x), #x)
+#define KS_NCCL(x) ::ks::nccl_check((x), #x)
+
+struct Rank {
+    int rank = 0, dev = 0, num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    bool own_comm = false;
+    Layout L{};
+    int64_t m = 0, row0 = 0;
+
+    // device memory (owned)
+    double* A = nullptr;        // m x ld
+    double* b_full = nullptr;   // ld
+    double* x_loc = nullptr;    // m (padded)
+    double* p_full = nullptr;   // ld
+    double* s_full = nullptr;   // ld
+    double* q_loc = nullptr;    // m
+    double* rhat_loc = nullptr; // m
+    double* G_r = nullptr;      // P * chunk
+    double* G_v = nullptr;      // P * chunk
+    double* S = nullptr;        // P * kScalSlot
+    DevState* st = nullptr;
+    double* hist = nullptr;
+    int64_t hist_alloc = 0;
+    Scratch scr{};
+    double* table_tmp = nullptr;
+
+    // host
+    int* h_done = nullptr;      // pinned, 2 slots
+    DevState* h_state = nullptr; // pinned
+    std::vector<unsigned char> loaded;  // per local row
+    int64_t loaded_count = 0;
+
+    // events
+    cudaEvent_t ev_poll[2]{};
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+    std::vector<cudaEvent_t> ev_gemv;   // profiling pairs
+
+    int64_t launches = 0;
+    int64_t gemv_launches = 0;
+    double gemv_seconds = 0.0;
+
+    VecArgs vargs() const;
+};
+
+struct Options {
+    int64_t true_residual = 1;
+    int64_t profile_gemv = 0;
+    int64_t poll_batch = 16;
+    int64_t gemv_rows = 0;
+    int64_t gemv_split = 0;
+    int64_t gemv_kernel = 0;
+    int64_t use_graphs = 0;
+};
+
+}  // namespace ks
+
+struct ks_ctx {
+    int64_t n = 0, ld = 0;
+    int P = 1;               // global number of ranks
+    bool multiprocess = false;
+    std::vector<ks::Rank> ranks;   // local ranks (1 in multi-process mode)
+    ks::Options opt;
+    bool poisoned = false;
+    std::string last_error;
+
+    // Runs fn(rank) on every local rank: one worker thread per GPU when there is
+    // more than one.  Exceptions are collected; the first is rethrown.
+    void for_each_rank(const std::function<void(ks::Rank&)>& fn);
+    bool writes_host(const ks::Rank& r) const { return multiprocess || r.rank == 0; }
+};
+
+namespace ks {
+void rank_alloc(ks_ctx* c, Rank& r);
+void rank_free(Rank& r);
+void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank);
+void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cudaMemcpyKind kind);
+int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
+               double* x, double* hist, int64_t hist_cap, ks_report* rep);
+int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,
+                     int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep);
+GemvConfig gemv_config(const ks_ctx* c, const Rank& r);
+}  // namespace ks

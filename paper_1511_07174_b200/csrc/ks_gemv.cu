@@ -1,0 +1,355 @@
+// K1 -- FP64 row-block GEMV with fused dot epilogue.
+//
+//   y[i] = sum_{j<n} A_loc[i,j] * x[j]          ("matrix-vector products")
+//   optional: y[i] = bsub[i] - (A x)[i]          (residual r0 = b - A x0)
+//   optional: *out1 = <w1, y>, *out2 = <y, y>    (fused inner products)
+//
+// HBM-bound: 0.25 flop/byte, ~20x below the FP64 ridge, so no tensor cores (this
+// is not a dense contraction).  Algorithmic bytes per launch = 8*m*n (A read
+// once); x (<= 2 MiB) stays L2-resident and is re-read once per row tile.
+//
+// Variant 1 ("LDG stream"): a CTA of NT threads owns a tile of R rows and a
+// contiguous range of 2*NT-column blocks (split-K over S CTAs when there are too
+// few tiles to fill 148 SMs).  Thread t streams columns {2t + 2*NT*c} of all R
+// rows with 128-bit evict-first loads (ld.global.cs.v2.f64), so every warp
+// instruction reads 512 contiguous bytes of one row, and each x element loaded
+// (ld.global.nc) is reused for R rows from registers.  Rows are reduced with a
+// warp butterfly plus a fixed cross-warp tree; split partials are combined in
+// split order by the last-arriving CTA of the tile; tile dot partials are
+// combined in tile order by the last-arriving tile -- the result is bitwise
+// independent of CTA scheduling.
+//
+// Variant 2 ("TMA bulk ring"): same tiling, but one elected thread streams the
+// R row segments of each column block into a shared-memory ring with
+// cp.async.bulk (TMA, SASS UBLKCP) completing on mbarriers, with an L2
+// evict-first cache hint; all warps consume from shared memory.  Deep
+// memory-level parallelism without register staging.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "ks_device.cuh"
+#include "ks_internal.h"
+
+namespace ks {
+
+namespace {
+
+constexpr int kNT = 256;  // threads per CTA
+constexpr int kNW = kNT / 32;
+
+__device__ __forceinline__ double2 ld_stream(const double* p) {
+    return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double2 ld_x(const double* p) {
+    return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+// Tile epilogue shared by both variants.  `acc` holds the full-row sums (valid in
+// every thread).  Returns nothing; handles split-K combine, y store, dots.
+template <int R>
+__device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)[R], int64_t tile,
+                                              int s, int S, int64_t tiles, double* qpart,
+                                              unsigned* tile_ticket, double* dpart,
+                                              unsigned* ticket, double* red) {
+    __shared__ int s_last;
+    const int64_t r0 = tile * R;
+    const int nvalid = (int)min((int64_t)R, p.m - r0);
+    if (S > 1) {
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) qpart[(tile * S + s) * R + r] = acc[r];
+            __threadfence();
+            unsigned t = atomicAdd(&tile_ticket[tile], 1u);
+            s_last = (t == (unsigned)(S - 1));
+        }
+        __syncthreads();
+        if (!s_last) return;
+        if (threadIdx.x == 0) tile_ticket[tile] = 0u;
+        __threadfence();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double v = 0.0;
+            for (int q = 0; q < S; ++q) v += __ldcg(qpart + (tile * S + q) * R + r);
+            acc[r] = v;
+        }
+    }
+    const bool want_dots = (p.out1 != nullptr) || (p.out2 != nullptr);
+    if (threadIdx.x == 0) {
+        double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (r < nvalid) {
+                double yv = acc[r];
+                if (p.bsub) yv = p.bsub[r0 + r] - yv;
+                p.y[r0 + r] = yv;
+                if (p.w1) d1 = fma(p.w1[r0 + r], yv, d1);
+                d2 = fma(yv, yv, d2);
+            }
+        }
+        if (want_dots) {
+            dpart[tile * 2 + 0] = d1;
+            dpart[tile * 2 + 1] = d2;
+            __threadfence();
+            unsigned t = atomicAdd(ticket, 1u);
+            s_last = (t == (unsigned)(tiles - 1));
+        }
+    }
+    if (!want_dots) return;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double v[2] = {0.0, 0.0};
+    for (int64_t t = threadIdx.x; t < tiles; t += kNT) {
+        v[0] += __ldcg(dpart + t * 2 + 0);
+        v[1] += __ldcg(dpart + t * 2 + 1);
+    }
+    block_sum<kNT, 2>(v, red);
+    if (threadIdx.x == 0) {
+        if (p.out1) *p.out1 = v[0];
+        if (p.out2) *p.out2 = v[1];
+        *ticket = 0u;
+    }
+}
+
+template <int R, int U>
+__global__ void __launch_bounds__(kNT) k1_gemv_ldg(GemvParams p, int S, int64_t tiles,
+                                                   double* qpart, unsigned* tile_ticket,
+                                                   double* dpart, unsigned* ticket) {
+    __shared__ double red[R * kNW];
+    if (p.done && *(volatile const int*)p.done) return;
+    const int64_t unit = blockIdx.x;
+    const int64_t tile = unit / S;
+    const int s = (int)(unit % S);
+    const int64_t r0 = tile * R;
+    const int nvalid = (int)min((int64_t)R, p.m - r0);
+    const int64_t ncb = p.ncols / (2 * kNT);
+    const int64_t cb0 = s * ncb / S, cb1 = (s + 1) * ncb / S;
+
+    const double* base = p.A + r0 * p.lda + 2 * threadIdx.x;
+    int64_t roff[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) roff[r] = (int64_t)min(r, nvalid - 1) * p.lda;
+    const double* xp = p.x + 2 * threadIdx.x;
+
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+
+    int64_t cb = cb0;
+    for (; cb + U <= cb1; cb += U) {
+        double2 av[U][R];
+        double2 xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = (cb + u) * (2 * kNT);
+            xv[u] = ld_x(xp + c);
+#pragma unroll
+            for (int r = 0; r < R; ++r) av[u][r] = ld_stream(base + roff[r] + c);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                acc[r] = fma(av[u][r].x, xv[u].x, acc[r]);
+                acc[r] = fma(av[u][r].y, xv[u].y, acc[r]);
+            }
+        }
+    }
+    for (; cb < cb1; ++cb) {
+        const int64_t c = cb * (2 * kNT);
+        const double2 xv = ld_x(xp + c);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double2 a = ld_stream(base + roff[r] + c);
+            acc[r] = fma(a.x, xv.x, acc[r]);
+            acc[r] = fma(a.y, xv.y, acc[r]);
+        }
+    }
+    block_sum<kNT, R>(acc, red);
+    gemv_epilogue<R>(p, acc, tile, s, S, tiles, qpart, tile_ticket, dpart, ticket, red);
+}
+
+// ----------------------------------------------------------------------------
+// Variant 2: cp.async.bulk (TMA) ring.  Stage = R row segments of CW doubles.
+// ----------------------------------------------------------------------------
+constexpr int kCW = 512;          // columns per stage per row (4 KiB per row segment)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+template <int R, int STAGES>
+__global__ void __launch_bounds__(kNT) k1_gemv_tma(GemvParams p, int S, int64_t tiles,
+                                                   double* qpart, unsigned* tile_ticket,
+                                                   double* dpart, unsigned* ticket) {
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    double* ring = reinterpret_cast<double*>(dyn_smem);  // STAGES * R * kCW
+    __shared__ __align__(8) uint64_t full_bar[STAGES];
+    __shared__ __align__(8) uint64_t empty_bar[STAGES];
+    __shared__ double red[R * kNW];
+    if (p.done && *(volatile const int*)p.done) return;
+
+    const int64_t unit = blockIdx.x;
+    const int64_t tile = unit / S;
+    const int s = (int)(unit % S);
+    const int64_t r0 = tile * R;
+    const int nvalid = (int)min((int64_t)R, p.m - r0);
+    const int64_t nst = p.ncols / kCW;                 // column stages of the row
+    const int64_t st0 = s * nst / S, st1 = (s + 1) * nst / S;
+    const int64_t nsteps = st1 - st0;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full_bar[i], 1);
+            mbar_init(&empty_bar[i], kNW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint64_t pol = policy_evict_first();
+    const uint32_t stage_bytes = (uint32_t)(nvalid * kCW * sizeof(double));
+    auto produce = [&](int64_t step) {
+        const int slot = (int)(step % STAGES);
+        double* dst = ring + (int64_t)slot * R * kCW;
+        mbar_expect_tx(&full_bar[slot], stage_bytes);
+        const int64_t c = (st0 + step) * kCW;
+        for (int r = 0; r < nvalid; ++r)
+            bulk_g2s(dst + r * kCW, p.A + (r0 + r) * p.lda + c, kCW * sizeof(double),
+                     &full_bar[slot], pol);
+    };
+    if (threadIdx.x == 0) {
+        for (int64_t q = 0; q < min((int64_t)STAGES, nsteps); ++q) produce(q);
+    }
+
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    const int warp = threadIdx.x >> 5;
+    for (int64_t step = 0; step < nsteps; ++step) {
+        const int slot = (int)(step % STAGES);
+        const uint32_t parity = (uint32_t)((step / STAGES) & 1);
+        const int64_t c = (st0 + step) * kCW + 2 * threadIdx.x;
+        const double2 xv = ld_x(p.x + c);
+        mbar_wait(&full_bar[slot], parity);
+        const double* src = ring + (int64_t)slot * R * kCW + 2 * threadIdx.x;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int rr = min(r, nvalid - 1);
+            const double2 a = *reinterpret_cast<const double2*>(src + rr * kCW);
+            acc[r] = fma(a.x, xv.x, acc[r]);
+            acc[r] = fma(a.y, xv.y, acc[r]);
+        }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty_bar[slot]);
+        if (threadIdx.x == 0 && step + STAGES < nsteps) {
+            mbar_wait(&empty_bar[slot], parity);
+            produce(step + STAGES);
+        }
+        (void)warp;
+    }
+    block_sum<kNT, R>(acc, red);
+    gemv_epilogue<R>(p, acc, tile, s, S, tiles, qpart, tile_ticket, dpart, ticket, red);
+}
+
+template <int R>
+int launch_rows(const GemvParams& p, const GemvConfig& c, const Scratch& s, int ticket_id,
+                cudaStream_t st) {
+    const int64_t tiles = (p.m + R - 1) / R;
+    const int64_t grid = tiles * c.splits;
+    double* dpart = s.part + (int64_t)ticket_id * kPartStride;
+    // dots of more than kPartStride/2 tiles go to the split-K scratch tail
+    if (tiles * 2 > kPartStride) dpart = s.qpart + (s.qpart_cap - tiles * 2);
+    unsigned* ticket = s.ticket + ticket_id;
+    if (c.variant == 2) {
+        constexpr int STAGES = (R >= 16) ? 3 : (R >= 8 ? 6 : 12);
+        const size_t smem = (size_t)STAGES * R * kCW * sizeof(double);
+        auto kern = k1_gemv_tma<R, STAGES>;
+        static std::atomic<unsigned> attr_set{0};  // one bit per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_set & (1u << dev))) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set |= 1u << dev;
+        }
+        kern<<<(unsigned)grid, kNT, smem, st>>>(p, c.splits, tiles, s.qpart, s.tile_ticket, dpart,
+                                               ticket);
+    } else {
+        constexpr int U = (R >= 16) ? 1 : (R >= 8 ? 2 : 4);
+        k1_gemv_ldg<R, U><<<(unsigned)grid, kNT, 0, st>>>(p, c.splits, tiles, s.qpart,
+                                                          s.tile_ticket, dpart, ticket);
+    }
+    return 1;
+}
+
+}  // namespace
+
+GemvConfig choose_gemv(int64_t m, int64_t ncols, int num_sms, int rows_opt, int split_opt,
+                       int variant_opt) {
+    GemvConfig c;
+    c.variant = variant_opt == 2 ? 2 : 1;
+    // measured on B200 at n = 65536 (profiles/): LDG R=4 7.35 TB/s, R=8 7.08, R=16 5.26;
+    // TMA R=16 6.82, R=8 6.00, R=4 4.28
+    c.rows = (rows_opt == 4 || rows_opt == 8 || rows_opt == 16) ? rows_opt : (c.variant == 2 ? 16 : 4);
+    const int64_t tiles = (m + c.rows - 1) / c.rows;
+    const int64_t ncb = std::max<int64_t>(1, ncols / (2 * kNT));   // == ncols / kCW
+    if (split_opt > 0) {
+        c.splits = (int)std::min<int64_t>(split_opt, ncb);
+    } else {
+        const int64_t target = 6LL * 2 * num_sms;   // ~6 waves of 2 CTAs/SM
+        int64_t S = tiles >= target ? 1 : (target + tiles - 1) / tiles;
+        c.splits = (int)std::max<int64_t>(1, std::min<int64_t>({S, ncb, 32}));
+    }
+    return c;
+}
+
+int launch_gemv(const GemvParams& p, const GemvConfig& c, const Scratch& s, int ticket_id,
+                int num_sms, cudaStream_t st) {
+    (void)num_sms;
+    if (p.m <= 0) return 0;
+    switch (c.rows) {
+        case 4: return launch_rows<4>(p, c, s, ticket_id, st);
+        case 8: return launch_rows<8>(p, c, s, ticket_id, st);
+        default: return launch_rows<16>(p, c, s, ticket_id, st);
+    }
+}
+
+}  // namespace ks

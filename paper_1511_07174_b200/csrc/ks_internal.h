@@ -1,0 +1,119 @@
+// Internal declarations of the B200 dense Krylov library (not part of the ABI).
+// Layering: ks_abi.cpp (L4 C ABI) -> ks_ctx.cpp / ks_solvers.cpp
+// (L3 context + L2 schedules) -> ks_gemv.cu / ks_vec.cu / ks_gen.cu (L1 kernels).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ks.h"
+
+namespace ks {
+
+constexpr int kMaxRanks = 16;
+constexpr int64_t kColAlign = 512;   // row padding of the device shard (doubles)
+constexpr int kScalSlot = 4;         // doubles per rank in the scalar gather buffer
+constexpr int kNumTickets = 64;
+
+// Row partition + gather layout, passed by value to kernels.
+struct Layout {
+    int P, rank;
+    int64_t n, ld;     // n; padded length of full vectors (multiple of kColAlign)
+    int64_t chunk;     // stride (doubles) of one rank's chunk in a gather buffer
+    int64_t pslot;     // offset of the partial-scalar slots inside a chunk
+    int64_t row0[kMaxRanks + 1];
+};
+
+// Device-resident solver state (one per rank).  Scalars that a kernel reads and
+// a later kernel writes live in 4-deep rings indexed by iteration (k & 3), so no
+// kernel ever reads a value another CTA of the same launch may be writing.
+struct DevState {
+    double nb;                 // ||b||
+    double tol;
+    double rho[4], alpha[4], omega[4];
+    double relres;             // last recorded recurrence relres
+    double true_rr;            // ||b - A x||^2 (true residual)
+    long long iters;           // completed loop bodies
+    long long maxit;
+    long long half_iter;       // BiCGSTAB iteration of a half-step exit (0 = none)
+    long long hist_cap;
+    int done, status, converged, breakdown, half, bzero;
+};
+
+// Scratch for deterministic last-block grid reductions.
+struct Scratch {
+    double* part;        // kNumTickets * kPartStride doubles
+    unsigned* ticket;    // kNumTickets
+    double* qpart;       // split-K partial rows
+    unsigned* tile_ticket;
+    int64_t qpart_cap, tile_cap;
+};
+constexpr int64_t kPartStride = 4096 * 2;
+
+struct GemvParams {
+    const double* A; int64_t lda; int64_t m; int64_t ncols;
+    const double* x;       // padded full input vector (ncols)
+    double* y;             // m outputs
+    const double* bsub;    // nullable: y = bsub - A x
+    const double* w1;      // nullable: *out1 = <w1, y>
+    double* out1;
+    double* out2;          // nullable: *out2 = <y, y>
+    const int* done;       // nullable: skip when *done != 0
+};
+
+struct GemvConfig {
+    int variant;   // 1 = LDG stream, 2 = TMA bulk ring
+    int rows;      // R
+    int splits;    // S
+};
+
+// ---- kernels (launchers return the number of kernel launches issued) -------
+int launch_gemv(const GemvParams& p, const GemvConfig& c, const Scratch& s, int ticket_id,
+                int num_sms, cudaStream_t st);
+GemvConfig choose_gemv(int64_t m, int64_t ncols, int num_sms, int rows_opt, int split_opt,
+                       int variant_opt);
+
+int launch_gen_spd(double* A, int64_t lda, int64_t row0, int64_t m, int64_t n, uint64_t seed,
+                   const double* table_dev, cudaStream_t st);
+int launch_gen_dd(double* A, int64_t lda, int64_t row0, int64_t m, int64_t n, uint64_t seed,
+                  int kd, cudaStream_t st);
+int launch_gen_rhs(double* b, int64_t n, uint64_t seed, cudaStream_t st);
+
+// Vector/control kernels (ks_vec.cu).  `G_r`, `G_v` are gather buffers in chunk
+// layout; `S` is the scalar gather buffer (kScalSlot doubles per rank).
+struct VecArgs {
+    Layout L;
+    DevState* st;
+    double* hist;
+    const double* b_full;  // ld
+    double* x_loc;         // m
+    double* p_full;        // ld
+    double* s_full;        // ld
+    double* q_loc;         // m (CG q / BiCGSTAB t)
+    double* rhat_loc;      // m
+    double* G_r;           // P * chunk
+    double* G_v;           // P * chunk
+    double* S;             // P * kScalSlot
+    Scratch scr;
+    int num_sms;
+};
+
+int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaStream_t st);
+int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
+                   cudaStream_t st);
+int launch_cg_update(const VecArgs& a, long long k, cudaStream_t st);
+int launch_cg_direction(const VecArgs& a, long long k, cudaStream_t st);
+int launch_cg_finish(const VecArgs& a, cudaStream_t st);
+int launch_bs_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
+                   cudaStream_t st);
+int launch_bs_p(const VecArgs& a, long long i, cudaStream_t st);
+int launch_bs_s(const VecArgs& a, long long i, cudaStream_t st);
+int launch_bs_xr(const VecArgs& a, long long i, cudaStream_t st);
+int launch_bs_finish(const VecArgs& a, cudaStream_t st);
+int launch_true_res_final(const VecArgs& a, cudaStream_t st);
+int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chunk
+
+}  // namespace ks

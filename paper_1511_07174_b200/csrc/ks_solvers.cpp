@@ -1,0 +1,261 @@
+// L2: per-GPU schedules of CG and BiCGSTAB
+// (sec.8(c).4).  Each local rank runs the same schedule on its own
+// stream; NCCL collectives over NVLink carry the vector slices with the partial
+// scalars piggybacked:
+//   CG        : 1 allgather (r + rho' partials) + 1 scalar allgather (sigma) / iteration
+//   BiCGSTAB  : 2 allgathers (v + <rhat,v>; r + <rhat,r>,<r,r>) + 1 scalar allgather
+// The host only queues work: scalars never leave the device inside the loop; a
+// 4-byte done flag is polled once per batch with one batch in flight.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "ks_ctx.h"
+
+namespace ks {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+struct Prof {
+    ks_ctx* c;
+    Rank& r;
+    int64_t per_slot;
+    int used[2] = {0, 0};
+    Prof(ks_ctx* c_, Rank& r_, int64_t gemvs_per_batch) : c(c_), r(r_), per_slot(gemvs_per_batch) {
+        if (!c->opt.profile_gemv) return;
+        const size_t need = (size_t)(2 * 2 * per_slot);
+        while (r.ev_gemv.size() < need) {
+            cudaEvent_t e;
+            KS_CUDA(cudaEventCreate(&e));
+            r.ev_gemv.push_back(e);
+        }
+    }
+    void begin(int slot) { used[slot] = 0; }
+    void pre(int slot) {
+        if (!c->opt.profile_gemv) return;
+        KS_CUDA(cudaEventRecord(r.ev_gemv[(size_t)(slot * per_slot + used[slot]) * 2], r.stream));
+    }
+    void post(int slot) {
+        if (!c->opt.profile_gemv) return;
+        KS_CUDA(cudaEventRecord(r.ev_gemv[(size_t)(slot * per_slot + used[slot]) * 2 + 1], r.stream));
+        ++used[slot];
+    }
+    void harvest(int slot) {
+        if (!c->opt.profile_gemv) return;
+        for (int q = 0; q < used[slot]; ++q) {
+            float ms = 0.f;
+            const size_t base = (size_t)(slot * per_slot + q) * 2;
+            KS_CUDA(cudaEventElapsedTime(&ms, r.ev_gemv[base], r.ev_gemv[base + 1]));
+            r.gemv_seconds += ms * 1e-3;
+        }
+        used[slot] = 0;
+    }
+};
+
+// Batched launch loop with a device done flag.
+template <class IterFn>
+void run_loop(ks_ctx* c, Rank& r, int64_t maxit, int gemvs_per_iter, IterFn&& iter) {
+    const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
+    Prof prof(c, r, B * gemvs_per_iter);
+    int64_t k = 1;
+    int64_t batch = 0;
+    KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+    while (k <= maxit) {
+        const int slot = (int)(batch & 1);
+        prof.begin(slot);
+        const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
+        for (; k <= kend; ++k) iter(k, prof, slot);
+        KS_CUDA(cudaMemcpyAsync(&r.h_done[slot], &r.st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                                r.stream));
+        KS_CUDA(cudaEventRecord(r.ev_poll[slot], r.stream));
+        if (batch >= 1) {
+            KS_CUDA(cudaEventSynchronize(r.ev_poll[slot ^ 1]));
+            prof.harvest(slot ^ 1);
+            if (r.h_done[slot ^ 1]) { ++batch; break; }
+        }
+        ++batch;
+    }
+    KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    prof.harvest(0);
+    prof.harvest(1);
+}
+
+void gemv(ks_ctx* c, Rank& r, const GemvParams& p) {
+    r.launches += launch_gemv(p, gemv_config(c, r), r.scr, 1, r.num_sms, r.stream);
+}
+
+GemvParams gp(const ks_ctx* c, const Rank& r, const double* x, double* y) {
+    GemvParams p{};
+    p.A = r.A;
+    p.lda = c->ld;
+    p.m = r.m;
+    p.ncols = c->ld;
+    p.x = x;
+    p.y = y;
+    return p;
+}
+
+// Setup shared by both methods (rows A0 / B0): b and x0 in; r0 = b - A x0
+// (K1 residual mode) or r0 = b; x_loc; rhat; partial <r0, r0>; allgather G_r.
+void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_cap) {
+    const size_t nbytes = (size_t)c->n * sizeof(double);
+    if (hist_cap > r.hist_alloc) {
+        KS_CUDA(cudaFree(r.hist));
+        r.hist = nullptr;
+        r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.hist), (size_t)r.hist_alloc * sizeof(double)));
+    }
+    KS_CUDA(cudaMemcpyAsync(r.b_full, b, nbytes, cudaMemcpyDefault, r.stream));
+    VecArgs a = r.vargs();
+    if (x0) {
+        KS_CUDA(cudaMemcpyAsync(r.s_full, x0, nbytes, cudaMemcpyDefault, r.stream));
+        GemvParams p = gp(c, r, r.s_full, r.G_r + (int64_t)r.rank * r.L.chunk);
+        p.bsub = r.b_full + r.row0;
+        gemv(c, r, p);
+        r.launches += launch_setup_r(a, true, r.s_full, r.stream);
+    } else {
+        r.launches += launch_setup_r(a, false, nullptr, r.stream);
+    }
+    allgather(c, r, r.G_r, r.L.chunk);
+}
+
+// Final x: gather, optional true residual ||b - A x|| (one extra GEMV), copy out.
+void finish_and_copy(ks_ctx* c, Rank& r, double* x, double* hist, int64_t hist_cap,
+                     ks_report* rep, bool bicgstab, const Clock::time_point& t_start) {
+    VecArgs a = r.vargs();
+    const double* xfull_dev = nullptr;
+    if (c->P > 1) {
+        r.launches += launch_pack_x(a, r.stream);
+        allgather(c, r, r.G_v, r.L.chunk);
+    }
+    if (c->opt.true_residual) {
+        if (c->P > 1) copy_chunks_to(c, r, r.G_v, r.s_full, cudaMemcpyDeviceToDevice);
+        else KS_CUDA(cudaMemcpyAsync(r.s_full, r.x_loc, (size_t)c->n * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, r.stream));
+        xfull_dev = r.s_full;
+        GemvParams p = gp(c, r, xfull_dev, r.q_loc);
+        p.bsub = r.b_full + r.row0;
+        p.out2 = r.S + (int64_t)r.rank * kScalSlot + 1;
+        gemv(c, r, p);
+        allgather(c, r, r.S, kScalSlot);
+        r.launches += launch_true_res_final(a, r.stream);
+    }
+    KS_CUDA(cudaMemcpyAsync(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    const DevState& s = *r.h_state;
+    if (c->writes_host(r)) {
+        if (c->P > 1) copy_chunks_to(c, r, r.G_v, x, cudaMemcpyDefault);
+        else KS_CUDA(cudaMemcpyAsync(x, r.x_loc, (size_t)c->n * sizeof(double), cudaMemcpyDefault,
+                                     r.stream));
+        const int64_t nh = std::min<int64_t>(s.iters, hist_cap);
+        if (hist && nh > 0)
+            KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault,
+                                    r.stream));
+        KS_CUDA(cudaStreamSynchronize(r.stream));
+    }
+    if (rep) {
+        float ms = 0.f;
+        KS_CUDA(cudaEventElapsedTime(&ms, r.ev_t0, r.ev_t1));
+        ks_report R;
+        std::memset(&R, 0, sizeof R);
+        R.iterations = s.iters;
+        R.half_step_exit = s.half;
+        R.matvecs = bicgstab ? 2 * s.iters - (s.half ? 1 : 0) : s.iters;
+        R.converged = s.converged;
+        R.breakdown = s.breakdown;
+        R.status = s.status;
+        R.relres = s.relres;
+        R.true_relres = (c->opt.true_residual && s.nb > 0) ? std::sqrt(s.true_rr) / s.nb
+                        : (s.bzero ? 0.0 : -1.0);
+        R.seconds_loop = ms * 1e-3;
+        R.seconds_total = std::chrono::duration<double>(Clock::now() - t_start).count();
+        R.seconds_gemv = r.gemv_seconds;
+        R.gemv_launches = r.gemv_launches;
+        R.kernel_launches = r.launches;
+        *rep = R;
+    }
+}
+
+void check_loaded(const ks_ctx* c, const Rank& r) {
+    (void)c;
+    if (r.loaded_count < r.m)
+        throw KsError(KS_ESTATE, "matrix not fully loaded: call ks_load_rows / ks_generate first");
+}
+
+}  // namespace
+
+int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
+               double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    const auto t_start = Clock::now();
+    check_loaded(c, r);
+    r.launches = 0;
+    r.gemv_launches = 0;
+    r.gemv_seconds = 0.0;
+    setup(c, r, b, x0, hist_cap);
+    VecArgs a = r.vargs();
+    r.launches += launch_cg_init(a, tol, maxit, hist_cap, r.stream);
+    double* sig = r.S + (int64_t)r.rank * kScalSlot;
+    GemvParams pq = gp(c, r, r.p_full, r.q_loc);
+    pq.w1 = r.p_full + r.row0;                 // sigma_g = <p_loc, q_loc>
+    pq.out1 = sig;
+    pq.done = &r.st->done;
+    run_loop(c, r, maxit, 1, [&](int64_t k, Prof& prof, int slot) {
+        prof.pre(slot);
+        gemv(c, r, pq);                          // A1
+        prof.post(slot);
+        ++r.gemv_launches;
+        allgather(c, r, r.S, kScalSlot);         // A2 (C2)
+        r.launches += launch_cg_update(a, k, r.stream);    // A2 + A3
+        allgather(c, r, r.G_r, r.L.chunk);       // A4 (C1)
+        r.launches += launch_cg_direction(a, k, r.stream); // A5
+    });
+    r.launches += launch_cg_finish(a, r.stream);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+    return r.h_state->status;
+}
+
+int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,
+                     int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    const auto t_start = Clock::now();
+    check_loaded(c, r);
+    r.launches = 0;
+    r.gemv_launches = 0;
+    r.gemv_seconds = 0.0;
+    setup(c, r, b, x0, hist_cap);
+    VecArgs a = r.vargs();
+    r.launches += launch_bs_init(a, tol, maxit, hist_cap, r.stream);
+    double* vown = r.G_v + (int64_t)r.rank * r.L.chunk;
+    GemvParams pv = gp(c, r, r.p_full, vown);  // B3: v = A p, <rhat, v>_g
+    pv.w1 = r.rhat_loc;
+    pv.out1 = vown + r.L.pslot;
+    pv.done = &r.st->done;
+    double* sc = r.S + (int64_t)r.rank * kScalSlot;
+    GemvParams pt = gp(c, r, r.s_full, r.q_loc);  // B6: t = A s, <t,s>_g, <t,t>_g
+    pt.w1 = r.s_full + r.row0;
+    pt.out1 = sc;
+    pt.out2 = sc + 1;
+    pt.done = &r.st->done;
+    run_loop(c, r, maxit, 2, [&](int64_t i, Prof& prof, int slot) {
+        r.launches += launch_bs_p(a, i, r.stream);  // B8(i-1) + B1
+        prof.pre(slot);
+        gemv(c, r, pv);                          // B3
+        prof.post(slot);
+        allgather(c, r, r.G_v, r.L.chunk);       // B2/B4 (C1 + C2)
+        r.launches += launch_bs_s(a, i, r.stream);  // B4 + B5
+        prof.pre(slot);
+        gemv(c, r, pt);                          // B6
+        prof.post(slot);
+        r.gemv_launches += 2;
+        allgather(c, r, r.S, kScalSlot);         // B7 (C2)
+        r.launches += launch_bs_xr(a, i, r.stream); // B7
+        allgather(c, r, r.G_r, r.L.chunk);       // B8 partials + r (C1)
+    });
+    r.launches += launch_bs_finish(a, r.stream);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, true, t_start);
+    return r.h_state->status;
+}
+
+}  // namespace ks

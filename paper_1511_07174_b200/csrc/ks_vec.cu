@@ -1,0 +1,417 @@
+// K2/K3 -- fused vector updates with fused dots, and the per-iteration control
+// logic folded into their prologues (SURVEY.md sec.8(a) rows A0, A2-A5, B0-B2,
+// B4, B5, B7, B8).  Every kernel is O(n) and HBM/L2-bound; each one replaces
+// several BLAS-1 passes (axpy, axpy, dot) by one pass with a deterministic
+// fused reduction.
+//
+// Schedule, one rank of P, iteration k:
+//   CG:       K1 q=A p (+sigma_g) -> [allgather S] -> cg_update -> [allgather G_r]
+//             -> cg_direction
+//   BiCGSTAB: bs_p -> K1 v=A p (+<rhat,v>_g) -> [allgather G_v] -> bs_s
+//             -> K1 t=A s (+<t,s>_g,<t,t>_g) -> [allgather S] -> bs_xr -> [allgather G_r]
+// The collectives carry the partial scalars next to the vector slices; every
+// rank forms the replicated full-length vectors (p, s) redundantly and sums the
+// partials in rank order, so all ranks take identical control decisions.
+//
+// Control: each kernel first checks st->done; the scalars a kernel reads were
+// written by an earlier kernel (rings indexed by iteration), and the decision
+// (convergence, breakdown, not-SPD) is computed identically by every CTA, then
+// recorded by one thread.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ks_device.cuh"
+#include "ks_internal.h"
+
+namespace ks {
+
+namespace {
+
+constexpr int kNT = 256;
+
+__device__ __forceinline__ int64_t gidx(const Layout& L, int64_t j) {
+    int g = 0;
+    while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
+    return (int64_t)g * L.chunk + (j - L.row0[g]);
+}
+__device__ __forceinline__ double* own_chunk(const VecArgs& a, double* G) {
+    return G + (int64_t)a.L.rank * a.L.chunk;
+}
+__device__ __forceinline__ double sum_slots(const Layout& L, const double* G, int k) {
+    double s = 0.0;
+    for (int g = 0; g < L.P; ++g) s += G[(int64_t)g * L.chunk + L.pslot + k];
+    return s;
+}
+__device__ __forceinline__ double sum_scal(const Layout& L, const double* S, int k) {
+    double s = 0.0;
+    for (int g = 0; g < L.P; ++g) s += S[g * kScalSlot + k];
+    return s;
+}
+__device__ __forceinline__ bool is_done(const DevState* st) {
+    return *(volatile const int*)&st->done != 0;
+}
+__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
+__device__ __forceinline__ int64_t m_loc(const Layout& L) {
+    return L.row0[L.rank + 1] - L.row0[L.rank];
+}
+__device__ __forceinline__ void put_hist(DevState* st, double* hist, long long k1, double v) {
+    if (hist && k1 >= 0 && k1 < st->hist_cap) hist[k1] = v;
+}
+
+// ---------------------------------------------------------------- setup (A0/B0)
+__global__ void __launch_bounds__(kNT) k_setup_r(VecArgs a, int have_x0, const double* x0_full) {
+    __shared__ double red[kNT / 32];
+    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    double* rl = own_chunk(a, a.G_r);
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
+        double r;
+        if (have_x0) {
+            r = rl[i];                       // r0 = b - A x0 written by K1 (residual mode)
+            a.x_loc[i] = x0_full[r0 + i];
+        } else {
+            r = a.b_full[r0 + i];            // r0 = b (x0 = 0, Q5)
+            rl[i] = r;
+            a.x_loc[i] = 0.0;
+        }
+        a.rhat_loc[i] = r;                   // BiCGSTAB shadow residual rhat = r0 (Q7)
+        acc[0] = fma(r, r, acc[0]);
+    }
+    block_sum<kNT, 1>(acc, red);
+    if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        rl[a.L.pslot + 0] = acc[0];          // <rhat, r0> = <r0, r0>
+        rl[a.L.pslot + 1] = acc[0];
+    }
+}
+
+__device__ void init_state(DevState* st, double tol, long long maxit, long long hist_cap) {
+    st->tol = tol;
+    st->maxit = maxit;
+    st->hist_cap = hist_cap;
+    st->iters = 0;
+    st->half_iter = 0;
+    st->done = 0;
+    st->status = KS_EMAXIT;
+    st->converged = 0;
+    st->breakdown = 0;
+    st->half = 0;
+    st->bzero = 0;
+    st->true_rr = -1.0;
+    for (int q = 0; q < 4; ++q) st->rho[q] = st->alpha[q] = st->omega[q] = 1.0;
+}
+
+// Decides the 0-iteration exits (Q6: b = 0 -> x = 0; Q2: ||r0||/||b|| <= tol).
+__device__ void init_decide(DevState* st, double bb, double rr) {
+    const double nb = sqrt(bb);
+    st->nb = nb;
+    if (nb == 0.0) {
+        st->bzero = 1; st->converged = 1; st->status = KS_OK; st->relres = 0.0; st->done = 1;
+        return;
+    }
+    const double rel = sqrt(rr) / nb;
+    st->relres = rel;
+    if (rel <= st->tol) { st->converged = 1; st->status = KS_OK; st->done = 1; }
+}
+
+// ------------------------------------------------------------------- CG (A1-A5)
+__global__ void __launch_bounds__(kNT) k_cg_init(VecArgs a, double tol, long long maxit,
+                                                 long long hist_cap) {
+    __shared__ double red[kNT / 32];
+    double acc[1] = {0.0};
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
+        a.p_full[j] = a.G_r[gidx(a.L, j)];                 // p0 = r0 (full, replicated)
+        const double bj = a.b_full[j];
+        acc[0] = fma(bj, bj, acc[0]);
+    }
+    block_sum<kNT, 1>(acc, red);
+    if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        DevState* st = a.st;
+        init_state(st, tol, maxit, hist_cap);
+        const double rho0 = sum_slots(a.L, a.G_r, 1);
+        st->rho[0] = rho0;
+        init_decide(st, acc[0], rho0);
+    }
+}
+
+// A2 + A3: sigma = sum_g sigma_g; alpha = rho/sigma; x += alpha p; r -= alpha q;
+// rho'_g = <r_loc, r_loc> -> own partial slot of G_r (rides on the r allgather).
+__global__ void __launch_bounds__(kNT) k_cg_update(VecArgs a, long long k) {
+    __shared__ double red[kNT / 32];
+    DevState* st = a.st;
+    if (is_done(st)) return;
+    const double sigma = sum_scal(a.L, a.S, 0);
+    if (!(sigma > 0.0)) {                                   // Q9: NOTSPD, x unchanged
+        if (lead()) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
+        return;
+    }
+    const double alpha = st->rho[(k - 1) & 3] / sigma;
+    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    double* rl = own_chunk(a, a.G_r);
+    const double* pl = a.p_full + r0;
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
+        a.x_loc[i] = fma(alpha, pl[i], a.x_loc[i]);
+        const double r = fma(-alpha, a.q_loc[i], rl[i]);
+        rl[i] = r;
+        acc[0] = fma(r, r, acc[0]);
+    }
+    block_sum<kNT, 1>(acc, red);
+    if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        rl[a.L.pslot + 1] = acc[0];
+        st->alpha[k & 3] = alpha;
+    }
+}
+
+// A5: rho' = sum_g rho'_g; convergence test (Q1); beta; p = r + beta p (full n).
+__global__ void __launch_bounds__(kNT) k_cg_direction(VecArgs a, long long k) {
+    DevState* st = a.st;
+    if (is_done(st)) return;
+    const double rho1 = sum_slots(a.L, a.G_r, 1);
+    const double rel = sqrt(rho1) / st->nb;
+    if (rel <= st->tol) {
+        if (lead()) {
+            put_hist(st, a.hist, k - 1, rel);
+            st->relres = rel; st->iters = k; st->converged = 1; st->status = KS_OK; st->done = 1;
+        }
+        return;
+    }
+    const double beta = rho1 / st->rho[(k - 1) & 3];
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT)
+        a.p_full[j] = fma(beta, a.p_full[j], a.G_r[gidx(a.L, j)]);
+    if (lead()) {
+        put_hist(st, a.hist, k - 1, rel);
+        st->relres = rel; st->iters = k; st->rho[k & 3] = rho1;
+    }
+}
+
+__global__ void __launch_bounds__(kNT) k_finish(VecArgs a, int bicgstab) {
+    DevState* st = a.st;
+    if (lead() && !st->done) {
+        const long long maxit = st->maxit;
+        st->iters = maxit;
+        st->status = KS_EMAXIT;
+        if (bicgstab && maxit >= 1) {                     // test of the last full step
+            const double rel = sqrt(sum_slots(a.L, a.G_r, 1)) / st->nb;
+            put_hist(st, a.hist, maxit - 1, rel);
+            st->relres = rel;
+            if (rel <= st->tol) { st->converged = 1; st->status = KS_OK; }
+        }
+        st->done = 1;
+    }
+    if (st->bzero) {                                      // Q6: b = 0 -> x = 0
+        const int64_t m = m_loc(a.L);
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
+            a.x_loc[i] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------- BiCGSTAB (B1-B8)
+__global__ void __launch_bounds__(kNT) k_bs_init(VecArgs a, double tol, long long maxit,
+                                                 long long hist_cap) {
+    __shared__ double red[kNT / 32];
+    double acc[1] = {0.0};
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
+        const double bj = a.b_full[j];
+        acc[0] = fma(bj, bj, acc[0]);
+    }
+    block_sum<kNT, 1>(acc, red);
+    if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        DevState* st = a.st;
+        init_state(st, tol, maxit, hist_cap);   // rho_old = alpha = omega = 1 (Q8)
+        init_decide(st, acc[0], sum_slots(a.L, a.G_r, 1));
+    }
+}
+
+// B8 (test of iteration i-1) + B1: rho_i = <rhat, r_{i-1}> from the gathered
+// partials; beta; p = r + beta (p - omega v) over the full length (i = 1: p = r).
+__global__ void __launch_bounds__(kNT) k_bs_p(VecArgs a, long long i) {
+    DevState* st = a.st;
+    if (is_done(st)) return;
+    const double rho = sum_slots(a.L, a.G_r, 0);
+    double rel = 0.0;
+    if (i >= 2) {
+        rel = sqrt(sum_slots(a.L, a.G_r, 1)) / st->nb;
+        if (rel <= st->tol) {
+            if (lead()) {
+                put_hist(st, a.hist, i - 2, rel);
+                st->relres = rel; st->iters = i - 1; st->converged = 1; st->status = KS_OK;
+                st->done = 1;
+            }
+            return;
+        }
+    }
+    if (rho == 0.0 || !isfinite(rho)) {                    // Q9
+        if (lead()) {
+            if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
+            st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1;
+        }
+        return;
+    }
+    if (i == 1) {
+        for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT)
+            a.p_full[j] = a.G_r[gidx(a.L, j)];
+    } else {
+        const int q = (int)((i - 1) & 3);
+        const double om = st->omega[q];
+        const double beta = (rho / st->rho[q]) * (st->alpha[q] / om);
+        for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
+            const int64_t gj = gidx(a.L, j);
+            a.p_full[j] = fma(beta, fma(-om, a.G_v[gj], a.p_full[j]), a.G_r[gj]);
+        }
+    }
+    if (lead()) {
+        if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
+        st->rho[i & 3] = rho;
+        st->iters = i - 1;
+    }
+}
+
+// B4 + B5: gamma = sum_g <rhat,v>_g; alpha = rho/gamma; s = r - alpha v (full n,
+// redundant); ||s||^2 over the full length; half-step test.
+__global__ void __launch_bounds__(kNT) k_bs_s(VecArgs a, long long i) {
+    __shared__ double red[kNT / 32];
+    DevState* st = a.st;
+    if (is_done(st)) return;
+    const double g = sum_slots(a.L, a.G_v, 0);
+    if (g == 0.0 || !isfinite(g)) {
+        if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+        return;
+    }
+    const double alpha = st->rho[i & 3] / g;
+    double acc[1] = {0.0};
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
+        const int64_t gj = gidx(a.L, j);
+        const double s = fma(-alpha, a.G_v[gj], a.G_r[gj]);
+        a.s_full[j] = s;
+        acc[0] = fma(s, s, acc[0]);
+    }
+    block_sum<kNT, 1>(acc, red);
+    if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        st->alpha[i & 3] = alpha;
+        const double srel = sqrt(acc[0]) / st->nb;
+        if (srel <= st->tol) {                              // half-step exit (Q2)
+            put_hist(st, a.hist, i - 1, srel);
+            st->relres = srel; st->half = 1; st->half_iter = i; st->converged = 1;
+            st->status = KS_OK; st->iters = i; st->done = 1;
+        }
+    }
+}
+
+// B7: omega = <t,s>/<t,t>; x += alpha p + omega s; r = s - omega t; partials
+// <rhat, r>_g and <r, r>_g into the own slots of G_r.  On a half-step exit in
+// iteration i this kernel applies x += alpha p instead.
+__global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, long long i) {
+    __shared__ double red[2 * (kNT / 32)];
+    DevState* st = a.st;
+    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    const double* pl = a.p_full + r0;
+    if (is_done(st)) {
+        if (st->half_iter == i) {
+            const double alpha = st->alpha[i & 3];
+            for (int64_t l = blockIdx.x * (int64_t)kNT + threadIdx.x; l < m; l += (int64_t)gridDim.x * kNT)
+                a.x_loc[l] = fma(alpha, pl[l], a.x_loc[l]);
+        }
+        return;
+    }
+    const double ts = sum_scal(a.L, a.S, 0), tt = sum_scal(a.L, a.S, 1);
+    const double om = ts / tt;
+    if (tt == 0.0 || !isfinite(tt) || om == 0.0 || !isfinite(om)) {
+        if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+        return;
+    }
+    const double alpha = st->alpha[i & 3];
+    double* rl = own_chunk(a, a.G_r);
+    const double* sl = a.s_full + r0;
+    double acc[2] = {0.0, 0.0};
+    for (int64_t l = blockIdx.x * (int64_t)kNT + threadIdx.x; l < m; l += (int64_t)gridDim.x * kNT) {
+        const double s = sl[l];
+        a.x_loc[l] = fma(om, s, fma(alpha, pl[l], a.x_loc[l]));
+        const double r = fma(-om, a.q_loc[l], s);
+        rl[l] = r;
+        acc[0] = fma(a.rhat_loc[l], r, acc[0]);
+        acc[1] = fma(r, r, acc[1]);
+    }
+    block_sum<kNT, 2>(acc, red);
+    if (grid_sum<kNT, 2>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        rl[a.L.pslot + 0] = acc[0];
+        rl[a.L.pslot + 1] = acc[1];
+        st->omega[i & 3] = om;
+        st->iters = i;
+    }
+}
+
+__global__ void k_true_res_final(VecArgs a) {
+    if (lead()) a.st->true_rr = sum_scal(a.L, a.S, 1);
+}
+
+__global__ void __launch_bounds__(kNT) k_pack_x(VecArgs a) {
+    const int64_t m = m_loc(a.L);
+    double* xl = own_chunk(a, a.G_v);
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
+        xl[i] = a.x_loc[i];
+}
+
+unsigned grid_for(int64_t len, int num_sms) {
+    int64_t g = (len + kNT * 4 - 1) / (kNT * 4);
+    if (g < 1) g = 1;
+    const int64_t cap = 2LL * num_sms;
+    return (unsigned)(g > cap ? cap : g);
+}
+
+int64_t mloc_h(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
+
+}  // namespace
+
+int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaStream_t st) {
+    k_setup_r<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, have_x0 ? 1 : 0, x0_full);
+    return 1;
+}
+int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
+                   cudaStream_t st) {
+    k_cg_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
+    return 1;
+}
+int launch_cg_update(const VecArgs& a, long long k, cudaStream_t st) {
+    k_cg_update<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, k);
+    return 1;
+}
+int launch_cg_direction(const VecArgs& a, long long k, cudaStream_t st) {
+    k_cg_direction<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, k);
+    return 1;
+}
+int launch_cg_finish(const VecArgs& a, cudaStream_t st) {
+    k_finish<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, 0);
+    return 1;
+}
+int launch_bs_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
+                   cudaStream_t st) {
+    k_bs_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
+    return 1;
+}
+int launch_bs_p(const VecArgs& a, long long i, cudaStream_t st) {
+    k_bs_p<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, i);
+    return 1;
+}
+int launch_bs_s(const VecArgs& a, long long i, cudaStream_t st) {
+    k_bs_s<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, i);
+    return 1;
+}
+int launch_bs_xr(const VecArgs& a, long long i, cudaStream_t st) {
+    k_bs_xr<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, i);
+    return 1;
+}
+int launch_bs_finish(const VecArgs& a, cudaStream_t st) {
+    k_finish<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, 1);
+    return 1;
+}
+int launch_true_res_final(const VecArgs& a, cudaStream_t st) {
+    k_true_res_final<<<1, 32, 0, st>>>(a);
+    return 1;
+}
+int launch_pack_x(const VecArgs& a, cudaStream_t st) {
+    k_pack_x<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a);
+    return 1;
+}
+
+}  // namespace ks

@@ -331,3 +331,21 @@ def test_edge_notspd_and_breakdown_and_maxit():
     assert rep.status == oracle.EMAXIT and rep.iterations == 7 and hist.size == 7
     x, hist, rep = oracle.cg(A, b, tol=1e-10, maxit=0)
     assert rep.status == oracle.EMAXIT and rep.iterations == 0 and np.all(x == 0)
+
+
+def test_Q17_bicgstab_floor():
+    """Reading Q17: the history bar needs an absolute floor because
+    two legitimate FP64 evaluation orders of the SAME method differ at the
+    rounding floor.  A symmetric permutation P A P^T, P b is the same system in
+    exact arithmetic; the oracle's own histories on the two copies differ by
+    > 1e-14 (so survey's 1e-14 floor is too tight for BiCGSTAB) but < 1e-12
+    (the floor the GPU tests use), while the relative bar holds above 1e-6."""
+    A, b = synth.gdd(1024, 16)
+    _, h1, r1 = oracle.bicgstab(A, b, tol=1e-10)
+    P = np.arange(1024)[::-1]
+    _, h2, r2 = oracle.bicgstab(A[np.ix_(P, P)], b[P], tol=1e-10)
+    assert r1.iterations == r2.iterations
+    d = np.abs(h1 - h2)
+    assert d.max() > 1e-14 and d.max() < 1e-12
+    big = h1 > 1e-6
+    assert np.all(d[big] <= 1e-8 * h1[big])
