@@ -1,0 +1,129 @@
+"""Multi-GPU parity (pin P13): P GPUs vs the oracle with the same bars, identical
+results on every rank, and the two multi-GPU modes -- one process driving P GPUs
+(ks_create, ncclCommInitAll + worker threads) and one process per GPU (torchrun,
+torch's NCCL communicator borrowed through ks_create_rank)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+ks = pytest.importorskip("paper_1511_07174_b200")
+torch = pytest.importorskip("torch")
+
+from test_gpu_parity import FLOOR_BS, bars, gemv_bound_check  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ngpu():
+    return torch.cuda.device_count()
+
+
+needs2 = pytest.mark.skipif("ngpu() < 2", reason="needs >= 2 GPUs (gpurun --gpus 2)")
+
+
+@needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_gemv_and_cg(P):
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    n = 2050   # uneven partition: first n mod P shards get one more row
+    rng = np.random.default_rng(P)
+    A = rng.standard_normal((n, n))
+    x = rng.standard_normal(n)
+    with ks.Context(n, ngpus=P) as ctx:
+        assert ctx.nranks == P and ctx.local_gpus == P
+        assert [ctx.row_range(g) for g in range(P)] == ks.partition(n, P)
+        ctx.load_rows(A[:1000])
+        ctx.load_rows(A[1000:], 1000)
+        y = ctx.matvec(x)
+    gemv_bound_check(A, x, y)
+    n = 2048
+    As, c, b = synth.gspd(n, 1e4)
+    xo, ho, ro = oracle.cg(As, b, tol=1e-10)
+    with ks.Context(n, ngpus=P) as ctx:
+        ctx.generate("spd", seed=synth.SEED, table=c)
+        xg, hg, rg = ctx.cg(b, tol=1e-10)
+    bars(xg, hg, rg, xo, ho, ro)
+    with ks.Context(n) as c1:
+        c1.generate("spd", seed=synth.SEED, table=c)
+        x1, h1, r1 = c1.cg(b, tol=1e-10)
+    assert r1.iterations == rg.iterations
+
+
+@needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_bicgstab(P):
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    for n, kd in [(1024, 4), (4096, 16), (1001, 4)]:
+        A, b = synth.gdd(n, kd)
+        xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
+        with ks.Context(n, ngpus=P) as ctx:
+            ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
+            x, h, r = ctx.bicgstab(b, tol=1e-10)
+        bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+        assert r.half_step_exit == ro.half_step_exit
+
+
+@needs2
+def test_multi_edge_cases():
+    n = 64
+    A = synth.random_spd(n, 10.0, 1)
+    with ks.Context(n, ngpus=2) as ctx:
+        ctx.load_rows(A)
+        x, h, r = ctx.cg(np.zeros(n), tol=1e-10)
+        assert r.iterations == 0 and np.all(x == 0)
+        b = np.random.default_rng(0).standard_normal(n)
+        x, h, r = ctx.cg(b, tol=1e-30, maxit=5)
+        assert r.status == ks.KS_EMAXIT and r.iterations == 5
+        x0 = np.random.default_rng(1).standard_normal(n)
+        xo, ho, ro = oracle.cg(A, b, x0=x0, tol=1e-10)
+        x, h, r = ctx.cg(b, x0=x0, tol=1e-10)
+        bars(x, h, r, xo, ho, ro)
+
+
+@needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_torchrun_borrowed_comm(tmp_path, P):
+    """One process per GPU (torchrun, nccl); every rank returns the same x and
+    history; results meet the bars vs the oracle."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    n = 4096
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + P}",
+           os.path.join(ROOT, "tools", "dist_solve.py"), str(n), str(tmp_path)]
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
+    res = [json.load(open(tmp_path / f"dist_{n}_r{g}.json")) for g in range(P)]
+    for key in ("cg", "bs"):
+        for g in range(1, P):
+            assert res[g][key]["x"] == res[0][key]["x"], key     # bitwise identical on all ranks
+            assert res[g][key]["h"] == res[0][key]["h"], key
+            assert res[g][key]["it"] == res[0][key]["it"], key
+    As, c, b = synth.gspd(n, 1e4)
+    xo, ho, ro = oracle.cg(As, b, tol=1e-10)
+    R = res[0]["cg"]
+
+    class Rep:
+        iterations = R["it"]
+    bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro)
+    y = np.array(res[0]["matvec"])
+    gemv_bound_check(As, b, y)
+    A, b = synth.gdd(n, 16)
+    xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
+    R = res[0]["bs"]
+    Rep.iterations = R["it"]
+    bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro, floor=FLOOR_BS)
+    A, b = synth.gdd(n, 4)
+    xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
+    R = res[0]["bs_loaded"]
+    Rep.iterations = R["it"]
+    bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro, floor=FLOOR_BS)
