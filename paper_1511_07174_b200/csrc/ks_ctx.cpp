@@ -64,6 +64,7 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     dmalloc(&r.G_v, P * (size_t)r.L.chunk);
     dmalloc(&r.S, P * kScalSlot);
     dmalloc(&r.st, 1);
+    dmalloc(&r.kdev, 1);
     r.hist_alloc = 1024;
     dmalloc(&r.hist, r.hist_alloc);
     dmalloc(&r.scr.part, (size_t)kNumTickets * kPartStride);
@@ -88,7 +89,8 @@ void rank_free(Rank& r) {
     for (void* p : {(void*)r.A, (void*)r.b_full, (void*)r.x_loc, (void*)r.p_full, (void*)r.s_full,
                     (void*)r.q_loc, (void*)r.rhat_loc, (void*)r.G_r, (void*)r.G_v, (void*)r.S,
                     (void*)r.st, (void*)r.hist, (void*)r.scr.part, (void*)r.scr.ticket,
-                    (void*)r.scr.qpart, (void*)r.scr.tile_ticket, (void*)r.table_tmp})
+                    (void*)r.scr.qpart, (void*)r.scr.tile_ticket, (void*)r.table_tmp,
+                    (void*)r.kdev})
         if (p) cudaFree(p);
     if (r.h_done) cudaFreeHost(r.h_done);
     if (r.h_state) cudaFreeHost(r.h_state);
@@ -96,6 +98,7 @@ void rank_free(Rank& r) {
     if (r.ev_t0) cudaEventDestroy(r.ev_t0);
     if (r.ev_t1) cudaEventDestroy(r.ev_t1);
     for (auto e : r.ev_gemv) cudaEventDestroy(e);
+    for (auto& g : r.graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
     r.ev_gemv.clear();
     if (r.own_comm && r.comm) ncclCommDestroy(r.comm);
     if (r.own_stream && r.stream) cudaStreamDestroy(r.stream);

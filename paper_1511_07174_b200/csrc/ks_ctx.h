@@ -62,6 +62,16 @@ struct Rank {
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
     std::vector<cudaEvent_t> ev_gemv;   // profiling pairs
 
+    // CUDA-graph replay of one poll batch (KS_OPT_USE_GRAPHS)
+    long long* kdev = nullptr;            // iteration base read by the captured kernels
+    struct GraphCache {
+        cudaGraphExec_t exec = nullptr;
+        int kind = -1;
+        int64_t B = 0, launches = 0;
+        const void* hist = nullptr;
+        int variant = 0, rows = 0, splits = 0;
+    } graphs[2];
+
     int64_t launches = 0;
     int64_t gemv_launches = 0;
     double gemv_seconds = 0.0;

@@ -104,16 +104,19 @@ struct VecArgs {
 int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaStream_t st);
 int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
                    cudaStream_t st);
-int launch_cg_update(const VecArgs& a, long long k, cudaStream_t st);
-int launch_cg_direction(const VecArgs& a, long long k, cudaStream_t st);
+int launch_cg_update(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st);
+int launch_cg_direction(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st);
 int launch_cg_finish(const VecArgs& a, cudaStream_t st);
 int launch_bs_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
                    cudaStream_t st);
-int launch_bs_p(const VecArgs& a, long long i, cudaStream_t st);
-int launch_bs_s(const VecArgs& a, long long i, cudaStream_t st);
-int launch_bs_xr(const VecArgs& a, long long i, cudaStream_t st);
+int launch_bs_p(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st);
+int launch_bs_s(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st);
+int launch_bs_xr(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st);
 int launch_bs_finish(const VecArgs& a, cudaStream_t st);
 int launch_true_res_final(const VecArgs& a, cudaStream_t st);
 int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chunk
+// Iteration kernels use k = koff + (kdev ? *kdev : 0): a captured batch of
+// iterations (CUDA graph) is replayed with *kdev advanced by k_advance.
+int launch_advance(long long* kdev, long long by, cudaStream_t st);
 
 }  // namespace ks

@@ -54,19 +54,52 @@ struct Prof {
     }
 };
 
-// Batched launch loop with a device done flag.
+// Batched launch loop with a device done flag.  With
+// KS_OPT_USE_GRAPHS a full batch of B iterations is captured once into a CUDA
+// graph (kernels + NCCL calls) and replayed; the captured kernels read the
+// iteration base from r.kdev, which the graph's last node advances by B.
 template <class IterFn>
-void run_loop(ks_ctx* c, Rank& r, int64_t maxit, int gemvs_per_iter, IterFn&& iter) {
+void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, IterFn&& iter) {
     const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
     Prof prof(c, r, B * gemvs_per_iter);
+    const bool use_graph = c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
+    Rank::GraphCache* g = nullptr;
+    if (use_graph) {
+        g = &r.graphs[kind];
+        const GemvConfig cfg = gemv_config(c, r);
+        if (!(g->exec && g->kind == kind && g->B == B && g->hist == r.hist && g->variant == cfg.variant &&
+              g->rows == cfg.rows && g->splits == cfg.splits)) {
+            if (g->exec) { KS_CUDA(cudaGraphExecDestroy(g->exec)); g->exec = nullptr; }
+            const int64_t before = r.launches;
+            cudaGraph_t graph;
+            KS_CUDA(cudaStreamBeginCapture(r.stream, cudaStreamCaptureModeThreadLocal));
+            for (int64_t j = 1; j <= B; ++j) iter(r.kdev, j, prof, 0);
+            r.launches += launch_advance(r.kdev, B, r.stream);
+            KS_CUDA(cudaStreamEndCapture(r.stream, &graph));
+            KS_CUDA(cudaGraphInstantiate(&g->exec, graph, 0));
+            KS_CUDA(cudaGraphDestroy(graph));
+            g->kind = kind; g->B = B; g->hist = r.hist;
+            g->variant = cfg.variant; g->rows = cfg.rows; g->splits = cfg.splits;
+            g->launches = r.launches - before;
+            r.launches = before;
+        }
+        KS_CUDA(cudaMemsetAsync(r.kdev, 0, sizeof(long long), r.stream));
+    }
     int64_t k = 1;
     int64_t batch = 0;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
     while (k <= maxit) {
         const int slot = (int)(batch & 1);
         prof.begin(slot);
-        const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
-        for (; k <= kend; ++k) iter(k, prof, slot);
+        if (use_graph && k + B - 1 <= maxit) {
+            KS_CUDA(cudaGraphLaunch(g->exec, r.stream));   // iterations k .. k+B-1
+            r.launches += g->launches;
+            r.gemv_launches += B * gemvs_per_iter;
+            k += B;
+        } else {
+            const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
+            for (; k <= kend; ++k) iter(nullptr, k, prof, slot);
+        }
         KS_CUDA(cudaMemcpyAsync(&r.h_done[slot], &r.st->done, sizeof(int), cudaMemcpyDeviceToHost,
                                 r.stream));
         KS_CUDA(cudaEventRecord(r.ev_poll[slot], r.stream));
@@ -202,15 +235,15 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
     pq.w1 = r.p_full + r.row0;                 // sigma_g = <p_loc, q_loc>
     pq.out1 = sig;
     pq.done = &r.st->done;
-    run_loop(c, r, maxit, 1, [&](int64_t k, Prof& prof, int slot) {
+    run_loop(c, r, 0, maxit, 1, [&](const long long* kdev, int64_t k, Prof& prof, int slot) {
         prof.pre(slot);
         gemv(c, r, pq);                          // A1
         prof.post(slot);
-        ++r.gemv_launches;
+        if (!kdev) ++r.gemv_launches;
         allgather(c, r, r.S, kScalSlot);         // A2 (C2)
-        r.launches += launch_cg_update(a, k, r.stream);    // A2 + A3
+        r.launches += launch_cg_update(a, kdev, k, r.stream);    // A2 + A3
         allgather(c, r, r.G_r, r.L.chunk);       // A4 (C1)
-        r.launches += launch_cg_direction(a, k, r.stream); // A5
+        r.launches += launch_cg_direction(a, kdev, k, r.stream); // A5
     });
     r.launches += launch_cg_finish(a, r.stream);
     finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
@@ -238,19 +271,19 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     pt.out1 = sc;
     pt.out2 = sc + 1;
     pt.done = &r.st->done;
-    run_loop(c, r, maxit, 2, [&](int64_t i, Prof& prof, int slot) {
-        r.launches += launch_bs_p(a, i, r.stream);  // B8(i-1) + B1
+    run_loop(c, r, 1, maxit, 2, [&](const long long* kdev, int64_t i, Prof& prof, int slot) {
+        r.launches += launch_bs_p(a, kdev, i, r.stream);  // B8(i-1) + B1
         prof.pre(slot);
         gemv(c, r, pv);                          // B3
         prof.post(slot);
         allgather(c, r, r.G_v, r.L.chunk);       // B2/B4 (C1 + C2)
-        r.launches += launch_bs_s(a, i, r.stream);  // B4 + B5
+        r.launches += launch_bs_s(a, kdev, i, r.stream);  // B4 + B5
         prof.pre(slot);
         gemv(c, r, pt);                          // B6
         prof.post(slot);
-        r.gemv_launches += 2;
+        if (!kdev) r.gemv_launches += 2;
         allgather(c, r, r.S, kScalSlot);         // B7 (C2)
-        r.launches += launch_bs_xr(a, i, r.stream); // B7
+        r.launches += launch_bs_xr(a, kdev, i, r.stream); // B7
         allgather(c, r, r.G_r, r.L.chunk);       // B8 partials + r (C1)
     });
     r.launches += launch_bs_finish(a, r.stream);

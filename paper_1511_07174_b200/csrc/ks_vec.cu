@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(kNT) k_cg_init(VecArgs a, double tol, long lon
 
 // A2 + A3: sigma = sum_g sigma_g; alpha = rho/sigma; x += alpha p; r -= alpha q;
 // rho'_g = <r_loc, r_loc> -> own partial slot of G_r (rides on the r allgather).
-__global__ void __launch_bounds__(kNT) k_cg_update(VecArgs a, long long k) {
+__global__ void __launch_bounds__(kNT) k_cg_update(VecArgs a, const long long* kdev, long long koff) {
+    const long long k = koff + (kdev ? *kdev : 0);
     __shared__ double red[kNT / 32];
     DevState* st = a.st;
     if (is_done(st)) return;
@@ -164,7 +165,8 @@ __global__ void __launch_bounds__(kNT) k_cg_update(VecArgs a, long long k) {
 }
 
 // A5: rho' = sum_g rho'_g; convergence test (Q1); beta; p = r + beta p (full n).
-__global__ void __launch_bounds__(kNT) k_cg_direction(VecArgs a, long long k) {
+__global__ void __launch_bounds__(kNT) k_cg_direction(VecArgs a, const long long* kdev, long long koff) {
+    const long long k = koff + (kdev ? *kdev : 0);
     DevState* st = a.st;
     if (is_done(st)) return;
     const double rho1 = sum_slots(a.L, a.G_r, 1);
@@ -225,7 +227,8 @@ __global__ void __launch_bounds__(kNT) k_bs_init(VecArgs a, double tol, long lon
 
 // B8 (test of iteration i-1) + B1: rho_i = <rhat, r_{i-1}> from the gathered
 // partials; beta; p = r + beta (p - omega v) over the full length (i = 1: p = r).
-__global__ void __launch_bounds__(kNT) k_bs_p(VecArgs a, long long i) {
+__global__ void __launch_bounds__(kNT) k_bs_p(VecArgs a, const long long* kdev, long long koff) {
+    const long long i = koff + (kdev ? *kdev : 0);
     DevState* st = a.st;
     if (is_done(st)) return;
     const double rho = sum_slots(a.L, a.G_r, 0);
@@ -269,7 +272,8 @@ __global__ void __launch_bounds__(kNT) k_bs_p(VecArgs a, long long i) {
 
 // B4 + B5: gamma = sum_g <rhat,v>_g; alpha = rho/gamma; s = r - alpha v (full n,
 // redundant); ||s||^2 over the full length; half-step test.
-__global__ void __launch_bounds__(kNT) k_bs_s(VecArgs a, long long i) {
+__global__ void __launch_bounds__(kNT) k_bs_s(VecArgs a, const long long* kdev, long long koff) {
+    const long long i = koff + (kdev ? *kdev : 0);
     __shared__ double red[kNT / 32];
     DevState* st = a.st;
     if (is_done(st)) return;
@@ -301,7 +305,8 @@ __global__ void __launch_bounds__(kNT) k_bs_s(VecArgs a, long long i) {
 // B7: omega = <t,s>/<t,t>; x += alpha p + omega s; r = s - omega t; partials
 // <rhat, r>_g and <r, r>_g into the own slots of G_r.  On a half-step exit in
 // iteration i this kernel applies x += alpha p instead.
-__global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, long long i) {
+__global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, const long long* kdev, long long koff) {
+    const long long i = koff + (kdev ? *kdev : 0);
     __shared__ double red[2 * (kNT / 32)];
     DevState* st = a.st;
     const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
@@ -341,6 +346,10 @@ __global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, long long i) {
     }
 }
 
+__global__ void k_advance(long long* kdev, long long by) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *kdev += by;
+}
+
 __global__ void k_true_res_final(VecArgs a) {
     if (lead()) a.st->true_rr = sum_scal(a.L, a.S, 1);
 }
@@ -372,12 +381,12 @@ int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist
     k_cg_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
     return 1;
 }
-int launch_cg_update(const VecArgs& a, long long k, cudaStream_t st) {
-    k_cg_update<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, k);
+int launch_cg_update(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st) {
+    k_cg_update<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, kdev, k);
     return 1;
 }
-int launch_cg_direction(const VecArgs& a, long long k, cudaStream_t st) {
-    k_cg_direction<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, k);
+int launch_cg_direction(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st) {
+    k_cg_direction<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, kdev, k);
     return 1;
 }
 int launch_cg_finish(const VecArgs& a, cudaStream_t st) {
@@ -389,20 +398,24 @@ int launch_bs_init(const VecArgs& a, double tol, long long maxit, long long hist
     k_bs_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
     return 1;
 }
-int launch_bs_p(const VecArgs& a, long long i, cudaStream_t st) {
-    k_bs_p<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, i);
+int launch_bs_p(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st) {
+    k_bs_p<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, kdev, i);
     return 1;
 }
-int launch_bs_s(const VecArgs& a, long long i, cudaStream_t st) {
-    k_bs_s<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, i);
+int launch_bs_s(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st) {
+    k_bs_s<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, kdev, i);
     return 1;
 }
-int launch_bs_xr(const VecArgs& a, long long i, cudaStream_t st) {
-    k_bs_xr<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, i);
+int launch_bs_xr(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st) {
+    k_bs_xr<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, kdev, i);
     return 1;
 }
 int launch_bs_finish(const VecArgs& a, cudaStream_t st) {
     k_finish<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, 1);
+    return 1;
+}
+int launch_advance(long long* kdev, long long by, cudaStream_t st) {
+    k_advance<<<1, 32, 0, st>>>(kdev, by);
     return 1;
 }
 int launch_true_res_final(const VecArgs& a, cudaStream_t st) {

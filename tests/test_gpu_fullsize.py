@@ -1,0 +1,84 @@
+"""Full-size parity at BASELINE.json's headline size n = 65536 (configs C3/C3'),
+in the launch configuration bench.py times (auto K1 config, one GPU, generated
+inputs).  The oracle cannot run whole solves at this size in seconds, so this file
+checks what it can compute one by one, and properties that hold at any size:
+  * sampled GEMV rows vs the oracle's on-the-fly generated rows (P9 bound),
+  * CG x vs the long-double closed-form solution (P6), survey App. A.8 counts (P14),
+  * BiCGSTAB true residual by the oracle with on-the-fly rows (P11),
+  * the first BiCGSTAB iterations vs the oracle itself (north-star bars).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+ks = pytest.importorskip("paper_1511_07174_b200")
+
+from test_gpu_parity import FLOOR_BS, bars, gamma  # noqa: E402
+
+N = 65536
+THREADS = os.cpu_count() or 1
+SAMPLE = [0, 1, 511, 512, 4095, 32767, 32768, 65534, 65535] + \
+    list(np.random.default_rng(65536).integers(0, N, 23))
+
+
+def _rows_check(spec, x, y):
+    op = oracle.Operator(gen=spec, threads=min(THREADS, 8))
+    for i in SAMPLE:
+        yo = op.rows(int(i), 1, x)[0]
+        a = oracle.gen_rows(spec, int(i), 1)[0]
+        bound = 2 * gamma(N) * float(np.abs(a) @ np.abs(x))
+        assert abs(y[i] - yo) <= bound, (i, y[i], yo, bound)
+
+
+def test_fullsize_gemv_sampled_rows():
+    x = synth.rhs(N, synth.SEED2)
+    for kind in ("dd", "spd"):
+        spec = synth.spec(kind, N, kappa=1e4, kd=16)
+        with ks.Context(N) as ctx:
+            ctx.generate(kind, seed=synth.SEED, table=spec["table"], kd=16, want_b=False)
+            y = ctx.matvec(x)
+        _rows_check(spec, x, y)
+
+
+def test_fullsize_cg_closed_form():
+    """C3': G-SPD(65536, 1e4), tol 1e-10: x vs the closed form, counts/histories vs
+    the survey's independent spec implementation (reference values)."""
+    c = synth.spd_table(N, 1e4)
+    with ks.Context(N) as ctx:
+        b = ctx.generate("spd", seed=synth.SEED, table=c)
+        x, h, r = ctx.cg(b, tol=1e-10)
+    assert r.converged and abs(r.iterations - 840) <= 2, r
+    assert np.allclose(h[:3], [0.5745285, 0.4442545, 0.3710058], rtol=5e-7, atol=0)
+    xcf = oracle.spd_exact_solve_ld(c, synth.SEED, b)
+    assert np.linalg.norm(x - xcf) <= 1e4 * 1e-10 * np.linalg.norm(xcf)
+    assert r.true_relres <= 10 * 1e-10
+    # sampled true residual entries by the oracle (on-the-fly rows)
+    spec = synth.spec("spd", N, kappa=1e4)
+    op = oracle.Operator(gen=spec, threads=min(THREADS, 8))
+    nb = float(np.linalg.norm(b))
+    for i in SAMPLE[:12]:
+        ri = b[i] - op.rows(int(i), 1, x)[0]
+        assert abs(ri) <= 10 * 1e-10 * nb
+
+
+def test_fullsize_bicgstab_true_residual_and_first_iterations():
+    """C3: G-DD(65536, 16), tol 1e-10."""
+    spec = synth.spec("dd", N, kd=16)
+    with ks.Context(N) as ctx:
+        b = ctx.generate("dd", seed=synth.SEED, kd=16)
+        x, h, r = ctx.bicgstab(b, tol=1e-10)
+        x2, h2, r2 = ctx.bicgstab(b, tol=0.0, maxit=2)       # bench mode, fixed length
+    assert r.converged and abs(r.iterations - 23) <= 2, r
+    assert np.allclose(h[:3], [0.3187527, 0.1602609, 0.08888871], rtol=5e-7, atol=0)
+    op = oracle.Operator(gen=spec, threads=THREADS)
+    tr = oracle.true_relres_ld(op, b, x)
+    assert tr <= 10 * 1e-10
+    assert abs(tr - r.true_relres) <= 1e-3 * tr + 1e-15
+    # the oracle itself, 2 iterations (4 GEMVs with on-the-fly rows)
+    xo, ho, ro = oracle.bicgstab(op, b, tol=0.0, maxit=2)
+    bars(x2, h2, r2, xo, ho, ro, iters_tol=0, floor=FLOOR_BS)

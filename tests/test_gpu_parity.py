@@ -279,3 +279,28 @@ def test_device_pointer_buffers():
         _, _, r = ctx.cg(bd, tol=1e-10, out=xd, hist=hd)
         torch.cuda.synchronize()
         bars(xd.cpu().numpy(), hd[: r.iterations].cpu().numpy(), r, xo, ho, ro)
+
+
+@pytest.mark.parametrize("method", ["cg", "bicgstab"])
+def test_graph_replay_bitwise_equal(method):
+    """KS_OPT_USE_GRAPHS replays captured poll batches (kernels read the iteration
+    base from device memory); results must equal direct launches bit for bit,
+    including a tail batch shorter than the poll batch and an early exit."""
+    n = 1024
+    if method == "cg":
+        A, c, b = synth.gspd(n, 1e3)
+    else:
+        A, b = synth.gdd(n, 16)
+    outs = []
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        for graphs, batch, tol, maxit in [(0, 16, 1e-10, None), (1, 16, 1e-10, None),
+                                          (1, 7, 1e-10, None), (0, 16, 0.0, 45), (1, 16, 0.0, 45)]:
+            ctx.set_option("use_graphs", graphs)
+            ctx.set_option("poll_batch", batch)
+            x, h, r = getattr(ctx, method)(b, tol=tol, maxit=maxit)
+            outs.append((x, h, r.iterations, tol))
+    ref = {0.0: outs[3], 1e-10: outs[0]}
+    for x, h, it, tol in outs:
+        rx, rh, rit, _ = ref[tol]
+        assert it == rit and np.array_equal(x, rx) and np.array_equal(h, rh)
