@@ -194,6 +194,9 @@ def run_reference(args):
 # ------------------------------------------------------------- our path
 
 def run_ours(args):
+    # stdout carries exactly one JSON line: C-level prints (NCCL banner, ...) go to stderr
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     import torch
     import torch.distributed as dist
 
@@ -244,6 +247,9 @@ def run_ours(args):
     for c in (cg_ctx, bs_ctx):
         c.set_option("true_residual", 0)
         c.set_option("profile_gemv", 1)
+        c.set_option("fused_comm", 1 if args.comm == "fused" else 0)
+    comm_mode = "fused NVLink peer stores" if cg_ctx.get_option("fused_comm") else \
+        ("none (P=1)" if world == 1 else "NCCL allgather")
     row_b, row_e = cg_ctx.row_range(rank)
     m = row_e - row_b
 
@@ -331,6 +337,7 @@ def run_ours(args):
             "config": {"workload": f"C3/C3': n={n} FP64 dense, CG on G-SPD(1e4) + BiCGSTAB on "
                                    f"G-DD(16), row-block over {world} GPU(s), tol=0 fixed length",
                        "n": n, "global_batch": 1, "parallelism": f"row-block P={world}",
+                       "collectives": comm_mode,
                        "l2": f"no flush needed: resident inputs {2 * 8 * m * n / 1e9:.1f} GB/GPU "
                              f">> 126 MB L2"},
             "per_method": {
@@ -352,7 +359,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "generate_s": t_gen,
         }
-        print(json.dumps(line), flush=True)
+        json_out.write(json.dumps(line) + "\n")
+        json_out.flush()
     cg_ctx.close()
     bs_ctx.close()
     if world > 1:
@@ -371,6 +379,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", choices=["fused", "nccl"], default="fused")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -95,7 +95,14 @@ typedef enum {
     KS_OPT_GEMV_SPLIT = 4,    /* K1 column splits per tile (0 = auto)             */
     KS_OPT_GEMV_KERNEL = 5,   /* K1 variant: 0 = auto, 1 = LDG stream, 2 = TMA    */
                               /* bulk-copy ring                                   */
-    KS_OPT_USE_GRAPHS = 6     /* 1: replay each poll batch as a CUDA graph        */
+    KS_OPT_USE_GRAPHS = 6,    /* 1: replay each poll batch as a CUDA graph        */
+    KS_OPT_FUSED_COMM = 7     /* 1 (default): when P > 1 and every GPU pair has   */
+                              /* peer access, the producing kernels store their   */
+                              /* slices/partials straight into every rank's       */
+                              /* exchange buffer over NVLink and release an epoch */
+                              /* flag (no NCCL call in the loop); 0: NCCL         */
+                              /* allgathers.  ks_get_option returns the effective */
+                              /* mode.                                            */
 } ks_option;
 
 /* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL

@@ -92,6 +92,7 @@ ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus) {
             for (int g = 0; g < ngpus; ++g) { c->ranks[g].comm = comms[g]; c->ranks[g].own_comm = true; }
         }
         c->for_each_rank([&](Rank& r) { ks::rank_alloc(c, r); });
+        ks::setup_peers(c);
         return KS_OK;
     });
     if (st != KS_OK) {
@@ -138,6 +139,7 @@ ks_status ks_create_rank(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t rank, 
                 throw KsError(KS_EARG, "nccl_comm size/rank do not match (nranks, rank)");
         }
         c->for_each_rank([&](Rank& rr) { ks::rank_alloc(c, rr); });
+        ks::setup_peers(c);
         return KS_OK;
     });
     if (st != KS_OK) {
@@ -303,6 +305,7 @@ static ks_status solve(ks_ctx* c, bool bicg, const double* b, const double* x0, 
     }
     if (rep) *rep = R;
     const ks_status s = status_of(stat[0]);
+    if (s == KS_ENCCL) return fail(c, KS_ENCCL, "fused collective wait timed out (peer rank lost)");
     if (s != KS_OK) {
         const char* what = s == KS_EMAXIT ? "maximum iterations reached"
                          : s == KS_ENOTSPD ? "CG: <p, A p> <= 0 (matrix not SPD)"
@@ -343,6 +346,7 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             if (v < 0 || v > 2) return fail(c, KS_EARG, "kernel must be 0, 1 or 2");
             o.gemv_kernel = v; break;
         case KS_OPT_USE_GRAPHS: o.use_graphs = v ? 1 : 0; break;
+        case KS_OPT_FUSED_COMM: o.fused_comm = v ? 1 : 0; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -359,6 +363,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_GEMV_SPLIT: *v = o.gemv_split; break;
         case KS_OPT_GEMV_KERNEL: *v = o.gemv_kernel; break;
         case KS_OPT_USE_GRAPHS: *v = o.use_graphs; break;
+        case KS_OPT_FUSED_COMM: *v = c->fused() ? 1 : 0; break;   // effective value
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

@@ -19,8 +19,13 @@ void nccl_check(ncclResult_t r, const char* what) {
     throw KsError(KS_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
 }
 
-VecArgs Rank::vargs() const {
+VecArgs Rank::vargs(bool fused) const {
     VecArgs a;
+    a.gpar = fused ? (int64_t)L.P * L.chunk : 0;
+    a.spar = fused ? (int64_t)L.P * kScalSlot : 0;
+    a.peer = fused ? 1 : 0;
+    a.pp = pp;
+    a.flags = flags;
     a.L = L;
     a.st = st;
     a.hist = hist;
@@ -28,6 +33,7 @@ VecArgs Rank::vargs() const {
     a.x_loc = x_loc;
     a.p_full = p_full;
     a.s_full = s_full;
+    a.v_full = v_full;
     a.q_loc = q_loc;
     a.rhat_loc = rhat_loc;
     a.G_r = G_r;
@@ -58,11 +64,29 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     dmalloc(&r.x_loc, r.m + 64);
     dmalloc(&r.p_full, ld);
     dmalloc(&r.s_full, ld);
+    dmalloc(&r.v_full, ld);
     dmalloc(&r.q_loc, r.m + 64);
     dmalloc(&r.rhat_loc, r.m + 64);
-    dmalloc(&r.G_r, P * (size_t)r.L.chunk);
-    dmalloc(&r.G_v, P * (size_t)r.L.chunk);
-    dmalloc(&r.S, P * kScalSlot);
+    {
+        const size_t g = 2 * P * (size_t)r.L.chunk;
+        const size_t sdoubles = (2 * P * kScalSlot + 63) / 64 * 64;
+        const size_t fwords = (kNumPhases * kMaxRanks + 63) / 64 * 64;
+        const size_t total = 2 * g + sdoubles + fwords;
+        dmalloc(&r.xbuf, total);
+        r.xbuf_bytes = total * sizeof(double);
+        r.G_r = r.xbuf;
+        r.G_v = r.xbuf + g;
+        r.S = r.xbuf + 2 * g;
+        r.flags = reinterpret_cast<unsigned long long*>(r.xbuf + 2 * g + sdoubles);
+        for (int q = 0; q < kMaxRanks; ++q) {
+            r.pp.G_r[q] = r.pp.G_v[q] = r.pp.S[q] = nullptr;
+            r.pp.flags[q] = nullptr;
+        }
+        r.pp.G_r[r.rank] = r.G_r;
+        r.pp.G_v[r.rank] = r.G_v;
+        r.pp.S[r.rank] = r.S;
+        r.pp.flags[r.rank] = r.flags;
+    }
     dmalloc(&r.st, 1);
     dmalloc(&r.kdev, 1);
     r.hist_alloc = 1024;
@@ -86,8 +110,10 @@ void rank_alloc(ks_ctx* c, Rank& r) {
 void rank_free(Rank& r) {
     if (cudaSetDevice(r.dev) != cudaSuccess) return;
     cudaDeviceSynchronize();
-    for (void* p : {(void*)r.A, (void*)r.b_full, (void*)r.x_loc, (void*)r.p_full, (void*)r.s_full,
-                    (void*)r.q_loc, (void*)r.rhat_loc, (void*)r.G_r, (void*)r.G_v, (void*)r.S,
+    for (void* p : r.ipc_opened) cudaIpcCloseMemHandle(p);
+    r.ipc_opened.clear();
+    for (void* p : {(void*)r.A, (void*)r.b_full, (void*)r.x_loc, (void*)r.p_full, (void*)r.s_full, (void*)r.v_full,
+                    (void*)r.q_loc, (void*)r.rhat_loc, (void*)r.xbuf,
                     (void*)r.st, (void*)r.hist, (void*)r.scr.part, (void*)r.scr.ticket,
                     (void*)r.scr.qpart, (void*)r.scr.tile_ticket, (void*)r.table_tmp,
                     (void*)r.kdev})
@@ -120,6 +146,79 @@ void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cuda
             KS_CUDA(cudaMemcpyAsync(dst + b, G + (int64_t)g * r.L.chunk, (size_t)(e - b) * sizeof(double),
                                     kind, r.stream));
     }
+}
+
+// Makes every rank's exchange buffers addressable from every other rank:
+// - one process, several GPUs: cudaDeviceEnablePeerAccess, raw pointers;
+// - one process per GPU: CUDA IPC handles of the exchange allocation, exchanged
+//   over the (borrowed) NCCL communicator itself, opened with lazy peer access.
+// Peer access is required for the fused collectives; without it the context
+// keeps the NCCL collectives (opt.fused_comm is then ineffective).
+void setup_peers(ks_ctx* c) {
+    if (c->P == 1) return;
+    const size_t offGv = (size_t)(c->ranks[0].G_v - c->ranks[0].xbuf);
+    const size_t offS = (size_t)(c->ranks[0].S - c->ranks[0].xbuf);
+    const size_t offF = (size_t)(reinterpret_cast<double*>(c->ranks[0].flags) - c->ranks[0].xbuf);
+    if (!c->multiprocess) {
+        bool ok = true;
+        for (auto& a : c->ranks)
+            for (auto& b : c->ranks) {
+                if (a.dev == b.dev) continue;
+                int can = 0;
+                KS_CUDA(cudaDeviceCanAccessPeer(&can, a.dev, b.dev));
+                if (!can) { ok = false; continue; }
+                KS_CUDA(cudaSetDevice(a.dev));
+                cudaError_t e = cudaDeviceEnablePeerAccess(b.dev, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else KS_CUDA(e);
+            }
+        for (auto& a : c->ranks) {
+            for (auto& b : c->ranks) {
+                a.pp.G_r[b.rank] = b.G_r;
+                a.pp.G_v[b.rank] = b.G_v;
+                a.pp.S[b.rank] = b.S;
+                a.pp.flags[b.rank] = b.flags;
+            }
+            a.peer_ok = ok;
+        }
+        return;
+    }
+    Rank& r = c->ranks[0];
+    KS_CUDA(cudaSetDevice(r.dev));
+    cudaIpcMemHandle_t mine;
+    KS_CUDA(cudaIpcGetMemHandle(&mine, r.xbuf));
+    const size_t hs = sizeof(cudaIpcMemHandle_t);
+    char* dbuf = nullptr;
+    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&dbuf), hs * (size_t)c->P));
+    KS_CUDA(cudaMemcpy(dbuf + hs * (size_t)r.rank, &mine, hs, cudaMemcpyHostToDevice));
+    KS_NCCL(ncclAllGather(dbuf + hs * (size_t)r.rank, dbuf, hs, ncclChar, r.comm, r.stream));
+    std::vector<cudaIpcMemHandle_t> all((size_t)c->P);
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    KS_CUDA(cudaMemcpy(all.data(), dbuf, hs * (size_t)c->P, cudaMemcpyDeviceToHost));
+    KS_CUDA(cudaFree(dbuf));
+    bool ok = true;
+    for (int g = 0; g < c->P; ++g) {
+        if (g == r.rank) continue;
+        void* base = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&base, all[(size_t)g], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) { cudaGetLastError(); ok = false; continue; }
+        r.ipc_opened.push_back(base);
+        double* d = static_cast<double*>(base);
+        r.pp.G_r[g] = d;
+        r.pp.G_v[g] = d + offGv;
+        r.pp.S[g] = d + offS;
+        r.pp.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
+    }
+    // every rank must agree, or none uses the fused path (collectives must match)
+    int* dok = nullptr;
+    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&dok), sizeof(int)));
+    int hok = ok ? 1 : 0;
+    KS_CUDA(cudaMemcpy(dok, &hok, sizeof(int), cudaMemcpyHostToDevice));
+    KS_NCCL(ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, r.comm, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    KS_CUDA(cudaMemcpy(&hok, dok, sizeof(int), cudaMemcpyDeviceToHost));
+    KS_CUDA(cudaFree(dok));
+    r.peer_ok = hok != 0;
 }
 
 GemvConfig gemv_config(const ks_ctx* c, const Rank& r) {

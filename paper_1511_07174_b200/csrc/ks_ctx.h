@@ -40,11 +40,21 @@ struct Rank {
     double* x_loc = nullptr;    // m (padded)
     double* p_full = nullptr;   // ld
     double* s_full = nullptr;   // ld
+    double* v_full = nullptr;   // ld
     double* q_loc = nullptr;    // m
     double* rhat_loc = nullptr; // m
-    double* G_r = nullptr;      // P * chunk
-    double* G_v = nullptr;      // P * chunk
-    double* S = nullptr;        // P * kScalSlot
+    // exchange buffers, one allocation (one CUDA IPC handle): G_r, G_v (2 parities
+    // x P chunks each), S (2 parities x P x kScalSlot), epoch flags
+    double* xbuf = nullptr;
+    size_t xbuf_bytes = 0;
+    double* G_r = nullptr;      // 2 * P * chunk
+    double* G_v = nullptr;      // 2 * P * chunk
+    double* S = nullptr;        // 2 * P * kScalSlot
+    unsigned long long* flags = nullptr;   // [kNumPhases][kMaxRanks]
+    PeerPtrs pp{};
+    bool peer_ok = false;       // every rank's exchange buffers are load/store reachable
+    std::vector<void*> ipc_opened;
+    unsigned long long epoch_next = 1;
     DevState* st = nullptr;
     double* hist = nullptr;
     int64_t hist_alloc = 0;
@@ -69,14 +79,14 @@ struct Rank {
         int kind = -1;
         int64_t B = 0, launches = 0;
         const void* hist = nullptr;
-        int variant = 0, rows = 0, splits = 0;
+        int variant = 0, rows = 0, splits = 0, fused = 0;
     } graphs[2];
 
     int64_t launches = 0;
     int64_t gemv_launches = 0;
     double gemv_seconds = 0.0;
 
-    VecArgs vargs() const;
+    VecArgs vargs(bool fused) const;
 };
 
 struct Options {
@@ -87,6 +97,7 @@ struct Options {
     int64_t gemv_split = 0;
     int64_t gemv_kernel = 0;
     int64_t use_graphs = 0;
+    int64_t fused_comm = 1;   // fused NVLink peer-store collectives when available
 };
 
 }  // namespace ks
@@ -104,11 +115,13 @@ struct ks_ctx {
     // more than one.  Exceptions are collected; the first is rethrown.
     void for_each_rank(const std::function<void(ks::Rank&)>& fn);
     bool writes_host(const ks::Rank& r) const { return multiprocess || r.rank == 0; }
+    bool fused() const { return P > 1 && opt.fused_comm && !ranks.empty() && ranks[0].peer_ok; }
 };
 
 namespace ks {
 void rank_alloc(ks_ctx* c, Rank& r);
 void rank_free(Rank& r);
+void setup_peers(ks_ctx* c);   // peer access / CUDA IPC of the exchange buffers
 void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank);
 void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cudaMemcpyKind kind);
 int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,

@@ -68,4 +68,55 @@ __device__ __forceinline__ bool grid_sum(double (&v)[K], double* part, unsigned*
     return true;
 }
 
+// ---- fused NVLink collectives: epoch flags ---------------------------------
+__device__ __forceinline__ void flag_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void flag_store_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long flag_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Block-wide wait until flags[src] >= epoch for every source rank (thread 0
+// spins with acquire loads; the barrier then orders every thread's later loads).
+// Bounded: after kWaitTimeoutNs the wait gives up and returns false, so a broken
+// peer can never hang the GPU.
+constexpr unsigned long long kWaitTimeoutNs = 10ULL * 1000 * 1000 * 1000;
+__device__ __forceinline__ bool wait_flags(const unsigned long long* flags, int P,
+                                           unsigned long long epoch) {
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        const unsigned long long t0 = globaltimer_ns();
+        for (int g = 0; g < P && ok; ++g) {
+            while (flag_acquire_sys(flags + g) < epoch) {
+                if (globaltimer_ns() - t0 > kWaitTimeoutNs) { ok = 0; break; }
+                __nanosleep(20);
+            }
+        }
+        s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+// Releases `epoch` into flag slot f_peer[g] of every rank g: ONE fence.sc.sys
+// (orders every store this thread performed or observed before it) followed by
+// relaxed system-scope stores -- a release pattern whose P flag stores are posted
+// back to back (P st.release.sys would each wait for the previous remote store).
+__device__ __forceinline__ void publish_flags(unsigned long long* const* f_peer, int P,
+                                              unsigned long long epoch) {
+    __threadfence_system();
+    for (int g = 0; g < P; ++g) flag_store_relaxed_sys(f_peer[g], epoch);
+}
+
 }  // namespace ks

@@ -77,6 +77,10 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
         }
     }
     const bool want_dots = (p.out1 != nullptr) || (p.out2 != nullptr);
+    // fused publish: iteration parity and epoch (graph-safe: read from device)
+    long long k = 0;
+    if (p.pub_P) k = p.koff + (p.kdev ? *p.kdev : 0);
+    const int64_t par = k & 1;
     if (threadIdx.x == 0) {
         double d1 = 0.0, d2 = 0.0;
 #pragma unroll
@@ -84,7 +88,11 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
             if (r < nvalid) {
                 double yv = acc[r];
                 if (p.bsub) yv = p.bsub[r0 + r] - yv;
-                p.y[r0 + r] = yv;
+                if (p.pub_P && p.y_peer[0]) {
+                    for (int g = 0; g < p.pub_P; ++g) p.y_peer[g][par * p.ypar + r0 + r] = yv;
+                } else {
+                    p.y[par * p.y_par + r0 + r] = yv;
+                }
                 if (p.w1) d1 = fma(p.w1[r0 + r], yv, d1);
                 d2 = fma(yv, yv, d2);
             }
@@ -92,7 +100,10 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
         if (want_dots) {
             dpart[tile * 2 + 0] = d1;
             dpart[tile * 2 + 1] = d2;
-            __threadfence();
+            // rows stored to peers must be visible system-wide before the flag;
+            // tiles that only produced dot partials need the GPU-scope fence of the
+            // ticket pattern (the last block releases at system scope)
+            if (p.pub_P && p.y_peer[0]) __threadfence_system(); else __threadfence();
             unsigned t = atomicAdd(ticket, 1u);
             s_last = (t == (unsigned)(tiles - 1));
         }
@@ -108,8 +119,16 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
     }
     block_sum<kNT, 2>(v, red);
     if (threadIdx.x == 0) {
-        if (p.out1) *p.out1 = v[0];
-        if (p.out2) *p.out2 = v[1];
+        if (p.pub_P) {                     // fused C2: partials -> every rank, then the flag
+            for (int g = 0; g < p.pub_P; ++g) {
+                if (p.out1) p.d_peer[g][par * p.dpar + 0] = v[0];
+                if (p.out2) p.d_peer[g][par * p.dpar + 1] = v[1];
+            }
+            publish_flags(p.f_peer, p.pub_P, *(volatile const unsigned long long*)p.ebase + k);
+        } else {
+            if (p.out1) *p.out1 = v[0];
+            if (p.out2) *p.out2 = v[1];
+        }
         *ticket = 0u;
     }
 }

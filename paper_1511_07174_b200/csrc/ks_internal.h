@@ -17,6 +17,20 @@ constexpr int kMaxRanks = 16;
 constexpr int64_t kColAlign = 512;   // row padding of the device shard (doubles)
 constexpr int kScalSlot = 4;         // doubles per rank in the scalar gather buffer
 constexpr int kNumTickets = 64;
+// Fused-collective phases (one epoch flag per phase and source rank).
+constexpr int kPhaseS = 0;   // scalar partials  (CG sigma; BiCGSTAB <t,s>, <t,t>)
+constexpr int kPhaseR = 1;   // r slice + <rhat,r>, <r,r> / rho' partials
+constexpr int kPhaseV = 2;   // BiCGSTAB v slice + <rhat,v>
+constexpr int kNumPhases = 3;
+
+// Peer (NVLink, unified-address) pointers to every rank's exchange buffers,
+// parity-0 bases; rank g's own entries point at its local memory.
+struct PeerPtrs {
+    double* G_r[kMaxRanks];
+    double* G_v[kMaxRanks];
+    double* S[kMaxRanks];
+    unsigned long long* flags[kMaxRanks];   // [kNumPhases][kMaxRanks] epochs
+};
 
 // Row partition + gather layout, passed by value to kernels.
 struct Layout {
@@ -40,7 +54,9 @@ struct DevState {
     long long maxit;
     long long half_iter;       // BiCGSTAB iteration of a half-step exit (0 = none)
     long long hist_cap;
+    unsigned long long ebase;  // epoch of iteration k is ebase + k (fused collectives)
     int done, status, converged, breakdown, half, bzero;
+    int peer_timeout;          // a fused-collective wait timed out (error)
 };
 
 // Scratch for deterministic last-block grid reductions.
@@ -62,6 +78,18 @@ struct GemvParams {
     double* out1;
     double* out2;          // nullable: *out2 = <y, y>
     const int* done;       // nullable: skip when *done != 0
+    // Fused publish (peer mode): y rows and/or dot partials stored straight into
+    // every rank's exchange buffer, then the phase flag released with the epoch.
+    int pub_P = 0, pub_rank = 0;           // 0: no peer publishing
+    double* y_peer[kMaxRanks];             // parity-0 address of row 0 of this rank's slice at rank g
+    int64_t ypar = 0;                      // parity stride of y_peer
+    int64_t y_par = 0;                     // parity stride applied to the local y
+    double* d_peer[kMaxRanks];             // parity-0 address of this rank's dot slots at rank g
+    int64_t dpar = 0;
+    unsigned long long* f_peer[kMaxRanks]; // flag [phase][this rank] at rank g
+    const unsigned long long* ebase = nullptr;
+    const long long* kdev = nullptr;       // epoch = *ebase + koff + (kdev ? *kdev : 0)
+    long long koff = 0;
 };
 
 struct GemvConfig {
@@ -92,6 +120,7 @@ struct VecArgs {
     double* x_loc;         // m
     double* p_full;        // ld
     double* s_full;        // ld
+    double* v_full;        // ld (BiCGSTAB: local copy of the gathered v)
     double* q_loc;         // m (CG q / BiCGSTAB t)
     double* rhat_loc;      // m
     double* G_r;           // P * chunk
@@ -99,16 +128,21 @@ struct VecArgs {
     double* S;             // P * kScalSlot
     Scratch scr;
     int num_sms;
+    // iteration-parity double buffering of G_r / G_v / S (0 in NCCL mode)
+    int64_t gpar, spar;
+    int peer;              // 1: fused NVLink peer-store collectives
+    PeerPtrs pp;
+    unsigned long long* flags;   // own [kNumPhases][kMaxRanks]
 };
 
 int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaStream_t st);
 int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
-                   cudaStream_t st);
+                   unsigned long long ebase, cudaStream_t st);
 int launch_cg_update(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st);
 int launch_cg_direction(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st);
 int launch_cg_finish(const VecArgs& a, cudaStream_t st);
 int launch_bs_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
-                   cudaStream_t st);
+                   unsigned long long ebase, cudaStream_t st);
 int launch_bs_p(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st);
 int launch_bs_s(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st);
 int launch_bs_xr(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st);

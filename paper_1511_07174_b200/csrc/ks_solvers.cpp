@@ -68,7 +68,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
         g = &r.graphs[kind];
         const GemvConfig cfg = gemv_config(c, r);
         if (!(g->exec && g->kind == kind && g->B == B && g->hist == r.hist && g->variant == cfg.variant &&
-              g->rows == cfg.rows && g->splits == cfg.splits)) {
+              g->rows == cfg.rows && g->splits == cfg.splits && g->fused == (c->fused() ? 1 : 0))) {
             if (g->exec) { KS_CUDA(cudaGraphExecDestroy(g->exec)); g->exec = nullptr; }
             const int64_t before = r.launches;
             cudaGraph_t graph;
@@ -80,6 +80,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
             KS_CUDA(cudaGraphDestroy(graph));
             g->kind = kind; g->B = B; g->hist = r.hist;
             g->variant = cfg.variant; g->rows = cfg.rows; g->splits = cfg.splits;
+            g->fused = c->fused() ? 1 : 0;
             g->launches = r.launches - before;
             r.launches = before;
         }
@@ -142,7 +143,7 @@ void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_c
         KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.hist), (size_t)r.hist_alloc * sizeof(double)));
     }
     KS_CUDA(cudaMemcpyAsync(r.b_full, b, nbytes, cudaMemcpyDefault, r.stream));
-    VecArgs a = r.vargs();
+    VecArgs a = r.vargs(false);   // setup gathers r0 with NCCL into parity 0
     if (x0) {
         KS_CUDA(cudaMemcpyAsync(r.s_full, x0, nbytes, cudaMemcpyDefault, r.stream));
         GemvParams p = gp(c, r, r.s_full, r.G_r + (int64_t)r.rank * r.L.chunk);
@@ -158,7 +159,7 @@ void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_c
 // Final x: gather, optional true residual ||b - A x|| (one extra GEMV), copy out.
 void finish_and_copy(ks_ctx* c, Rank& r, double* x, double* hist, int64_t hist_cap,
                      ks_report* rep, bool bicgstab, const Clock::time_point& t_start) {
-    VecArgs a = r.vargs();
+    VecArgs a = r.vargs(false);   // final x gather / true residual: NCCL, parity 0
     const double* xfull_dev = nullptr;
     if (c->P > 1) {
         r.launches += launch_pack_x(a, r.stream);
@@ -220,6 +221,24 @@ void check_loaded(const ks_ctx* c, const Rank& r) {
 
 }  // namespace
 
+// Fused-publish parameters of a K1 launch (peer mode): the y rows of this rank
+// (y_base: parity-0 chunk base in the G buffer of every rank, or none) and the dot
+// partials (slot base in G or S of every rank) go straight to every rank, then
+// the flag of `phase` is released with the iteration's epoch.
+void fuse_gemv(const ks_ctx* c, const Rank& r, GemvParams& p, int phase, double* const* ybase,
+               int64_t ypar, double* const* dbase, int64_t doff, int64_t dpar) {
+    p.pub_P = c->P;
+    p.pub_rank = r.rank;
+    for (int g = 0; g < c->P; ++g) {
+        p.y_peer[g] = ybase ? ybase[g] + (int64_t)r.rank * r.L.chunk : nullptr;
+        p.d_peer[g] = dbase[g] + doff;
+        p.f_peer[g] = r.pp.flags[g] + phase * kMaxRanks + r.rank;
+    }
+    p.ypar = ypar;
+    p.dpar = dpar;
+    p.ebase = &r.st->ebase;
+}
+
 int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
                double* x, double* hist, int64_t hist_cap, ks_report* rep) {
     const auto t_start = Clock::now();
@@ -228,26 +247,32 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
     setup(c, r, b, x0, hist_cap);
-    VecArgs a = r.vargs();
-    r.launches += launch_cg_init(a, tol, maxit, hist_cap, r.stream);
+    const bool fused = c->fused();
+    VecArgs a = r.vargs(fused);
+    const unsigned long long ebase = r.epoch_next;
+    r.epoch_next += (unsigned long long)maxit + 2;
+    r.launches += launch_cg_init(a, tol, maxit, hist_cap, ebase, r.stream);
     double* sig = r.S + (int64_t)r.rank * kScalSlot;
     GemvParams pq = gp(c, r, r.p_full, r.q_loc);
     pq.w1 = r.p_full + r.row0;                 // sigma_g = <p_loc, q_loc>
     pq.out1 = sig;
     pq.done = &r.st->done;
+    if (fused) fuse_gemv(c, r, pq, kPhaseS, nullptr, 0, r.pp.S, (int64_t)r.rank * kScalSlot, a.spar);
     run_loop(c, r, 0, maxit, 1, [&](const long long* kdev, int64_t k, Prof& prof, int slot) {
+        pq.kdev = kdev;
+        pq.koff = k;
         prof.pre(slot);
-        gemv(c, r, pq);                          // A1
+        gemv(c, r, pq);                          // A1 (+ fused C2 publish)
         prof.post(slot);
         if (!kdev) ++r.gemv_launches;
-        allgather(c, r, r.S, kScalSlot);         // A2 (C2)
-        r.launches += launch_cg_update(a, kdev, k, r.stream);    // A2 + A3
-        allgather(c, r, r.G_r, r.L.chunk);       // A4 (C1)
+        if (!fused) allgather(c, r, r.S, kScalSlot);   // A2 (C2)
+        r.launches += launch_cg_update(a, kdev, k, r.stream);    // A2 + A3 (+ fused C1)
+        if (!fused) allgather(c, r, r.G_r, r.L.chunk); // A4 (C1)
         r.launches += launch_cg_direction(a, kdev, k, r.stream); // A5
     });
     r.launches += launch_cg_finish(a, r.stream);
     finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
-    return r.h_state->status;
+    return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
 }
 
 int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,
@@ -258,37 +283,48 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
     setup(c, r, b, x0, hist_cap);
-    VecArgs a = r.vargs();
-    r.launches += launch_bs_init(a, tol, maxit, hist_cap, r.stream);
+    const bool fused = c->fused();
+    VecArgs a = r.vargs(fused);
+    const unsigned long long ebase = r.epoch_next;
+    r.epoch_next += (unsigned long long)maxit + 2;
+    r.launches += launch_bs_init(a, tol, maxit, hist_cap, ebase, r.stream);
     double* vown = r.G_v + (int64_t)r.rank * r.L.chunk;
     GemvParams pv = gp(c, r, r.p_full, vown);  // B3: v = A p, <rhat, v>_g
     pv.w1 = r.rhat_loc;
     pv.out1 = vown + r.L.pslot;
     pv.done = &r.st->done;
+    if (fused) {   // v rows stay local (pulled by bs_s); the partial is pushed
+        fuse_gemv(c, r, pv, kPhaseV, nullptr, 0, r.pp.G_v, (int64_t)r.rank * r.L.chunk + r.L.pslot,
+                  a.gpar);
+        pv.y_par = a.gpar;
+    }
     double* sc = r.S + (int64_t)r.rank * kScalSlot;
     GemvParams pt = gp(c, r, r.s_full, r.q_loc);  // B6: t = A s, <t,s>_g, <t,t>_g
     pt.w1 = r.s_full + r.row0;
     pt.out1 = sc;
     pt.out2 = sc + 1;
     pt.done = &r.st->done;
+    if (fused) fuse_gemv(c, r, pt, kPhaseS, nullptr, 0, r.pp.S, (int64_t)r.rank * kScalSlot, a.spar);
     run_loop(c, r, 1, maxit, 2, [&](const long long* kdev, int64_t i, Prof& prof, int slot) {
+        pv.kdev = pt.kdev = kdev;
+        pv.koff = pt.koff = i;
         r.launches += launch_bs_p(a, kdev, i, r.stream);  // B8(i-1) + B1
         prof.pre(slot);
-        gemv(c, r, pv);                          // B3
+        gemv(c, r, pv);                          // B3 (+ fused C1/C2 publish)
         prof.post(slot);
-        allgather(c, r, r.G_v, r.L.chunk);       // B2/B4 (C1 + C2)
+        if (!fused) allgather(c, r, r.G_v, r.L.chunk);   // B2/B4 (C1 + C2)
         r.launches += launch_bs_s(a, kdev, i, r.stream);  // B4 + B5
         prof.pre(slot);
-        gemv(c, r, pt);                          // B6
+        gemv(c, r, pt);                          // B6 (+ fused C2 publish)
         prof.post(slot);
         if (!kdev) r.gemv_launches += 2;
-        allgather(c, r, r.S, kScalSlot);         // B7 (C2)
-        r.launches += launch_bs_xr(a, kdev, i, r.stream); // B7
-        allgather(c, r, r.G_r, r.L.chunk);       // B8 partials + r (C1)
+        if (!fused) allgather(c, r, r.S, kScalSlot);     // B7 (C2)
+        r.launches += launch_bs_xr(a, kdev, i, r.stream); // B7 (+ fused C1)
+        if (!fused) allgather(c, r, r.G_r, r.L.chunk);   // B8 partials + r (C1)
     });
     r.launches += launch_bs_finish(a, r.stream);
     finish_and_copy(c, r, x, hist, hist_cap, rep, true, t_start);
-    return r.h_state->status;
+    return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
 }
 
 }  // namespace ks

@@ -35,6 +35,14 @@ __device__ __forceinline__ int64_t gidx(const Layout& L, int64_t j) {
     while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
     return (int64_t)g * L.chunk + (j - L.row0[g]);
 }
+// Gather buffers are double-buffered by iteration parity in the fused mode
+// (gpar/spar = 0 in NCCL mode: one buffer, gathered in place).
+__device__ __forceinline__ double* Gpar(const VecArgs& a, double* G, long long k) {
+    return G + (k & 1) * a.gpar;
+}
+__device__ __forceinline__ double* Spar(const VecArgs& a, long long k) {
+    return a.S + (k & 1) * a.spar;
+}
 __device__ __forceinline__ double* own_chunk(const VecArgs& a, double* G) {
     return G + (int64_t)a.L.rank * a.L.chunk;
 }
@@ -57,6 +65,36 @@ __device__ __forceinline__ int64_t m_loc(const Layout& L) {
 }
 __device__ __forceinline__ void put_hist(DevState* st, double* hist, long long k1, double v) {
     if (hist && k1 >= 0 && k1 < st->hist_cap) hist[k1] = v;
+}
+__device__ __forceinline__ unsigned long long epoch_of(const DevState* st, long long k) {
+    return *(volatile const unsigned long long*)&st->ebase + (unsigned long long)k;
+}
+// Fused mode: wait for phase `ph` of iteration k from every rank.  A timeout
+// marks the solve failed (KS_ENCCL) instead of hanging.
+__device__ __forceinline__ bool wait_phase(const VecArgs& a, int ph, long long k) {
+    if (!a.peer) return true;
+    const bool ok = wait_flags(a.flags + ph * kMaxRanks, a.L.P, epoch_of(a.st, k));
+    if (!ok && threadIdx.x == 0) {
+        a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1;
+    }
+    return ok;
+}
+// Stores v at offset `off` of this rank's chunk in G (parity-0 base per rank) at
+// every rank (fused allgather), or only locally in NCCL mode.
+__device__ __forceinline__ void publish(const VecArgs& a, double* const* Gpeer, double* G_own,
+                                        long long k, int64_t off, double v) {
+    const int64_t o = (k & 1) * a.gpar + (int64_t)a.L.rank * a.L.chunk + off;
+    if (a.peer) {
+        for (int g = 0; g < a.L.P; ++g) Gpeer[g][o] = v;
+    } else {
+        G_own[o] = v;
+    }
+}
+__device__ __forceinline__ void publish_phase(const VecArgs& a, int ph, long long k) {
+    if (!a.peer) return;
+    unsigned long long* f[kMaxRanks];
+    for (int g = 0; g < a.L.P; ++g) f[g] = a.pp.flags[g] + ph * kMaxRanks + a.L.rank;
+    publish_flags(f, a.L.P, epoch_of(a.st, k));
 }
 
 // ---------------------------------------------------------------- setup (A0/B0)
@@ -85,8 +123,11 @@ __global__ void __launch_bounds__(kNT) k_setup_r(VecArgs a, int have_x0, const d
     }
 }
 
-__device__ void init_state(DevState* st, double tol, long long maxit, long long hist_cap) {
+__device__ void init_state(DevState* st, double tol, long long maxit, long long hist_cap,
+                           unsigned long long ebase) {
     st->tol = tol;
+    st->ebase = ebase;
+    st->peer_timeout = 0;
     st->maxit = maxit;
     st->hist_cap = hist_cap;
     st->iters = 0;
@@ -116,7 +157,7 @@ __device__ void init_decide(DevState* st, double bb, double rr) {
 
 // ------------------------------------------------------------------- CG (A1-A5)
 __global__ void __launch_bounds__(kNT) k_cg_init(VecArgs a, double tol, long long maxit,
-                                                 long long hist_cap) {
+                                                 long long hist_cap, unsigned long long ebase) {
     __shared__ double red[kNT / 32];
     double acc[1] = {0.0};
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
@@ -127,7 +168,7 @@ __global__ void __launch_bounds__(kNT) k_cg_init(VecArgs a, double tol, long lon
     block_sum<kNT, 1>(acc, red);
     if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
         DevState* st = a.st;
-        init_state(st, tol, maxit, hist_cap);
+        init_state(st, tol, maxit, hist_cap, ebase);
         const double rho0 = sum_slots(a.L, a.G_r, 1);
         st->rho[0] = rho0;
         init_decide(st, acc[0], rho0);
@@ -141,26 +182,29 @@ __global__ void __launch_bounds__(kNT) k_cg_update(VecArgs a, const long long* k
     __shared__ double red[kNT / 32];
     DevState* st = a.st;
     if (is_done(st)) return;
-    const double sigma = sum_scal(a.L, a.S, 0);
+    if (!wait_phase(a, kPhaseS, k)) return;                   // sigma partials of iteration k
+    const double sigma = sum_scal(a.L, Spar(a, k), 0);
     if (!(sigma > 0.0)) {                                   // Q9: NOTSPD, x unchanged
         if (lead()) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
         return;
     }
     const double alpha = st->rho[(k - 1) & 3] / sigma;
     const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
-    double* rl = own_chunk(a, a.G_r);
+    const double* rin = own_chunk(a, Gpar(a, a.G_r, k - 1));   // r_{k-1}
     const double* pl = a.p_full + r0;
     double acc[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
         a.x_loc[i] = fma(alpha, pl[i], a.x_loc[i]);
-        const double r = fma(-alpha, a.q_loc[i], rl[i]);
-        rl[i] = r;
+        const double r = fma(-alpha, a.q_loc[i], rin[i]);
+        publish(a, a.pp.G_r, a.G_r, k, i, r);                // r_k -> every rank (fused C1)
         acc[0] = fma(r, r, acc[0]);
     }
+    if (a.peer) __threadfence_system();
     block_sum<kNT, 1>(acc, red);
     if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
-        rl[a.L.pslot + 1] = acc[0];
+        publish(a, a.pp.G_r, a.G_r, k, a.L.pslot + 1, acc[0]);
         st->alpha[k & 3] = alpha;
+        publish_phase(a, kPhaseR, k);
     }
 }
 
@@ -169,7 +213,9 @@ __global__ void __launch_bounds__(kNT) k_cg_direction(VecArgs a, const long long
     const long long k = koff + (kdev ? *kdev : 0);
     DevState* st = a.st;
     if (is_done(st)) return;
-    const double rho1 = sum_slots(a.L, a.G_r, 1);
+    if (!wait_phase(a, kPhaseR, k)) return;
+    const double* Gr = Gpar(a, a.G_r, k);
+    const double rho1 = sum_slots(a.L, Gr, 1);
     const double rel = sqrt(rho1) / st->nb;
     if (rel <= st->tol) {
         if (lead()) {
@@ -180,7 +226,7 @@ __global__ void __launch_bounds__(kNT) k_cg_direction(VecArgs a, const long long
     }
     const double beta = rho1 / st->rho[(k - 1) & 3];
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT)
-        a.p_full[j] = fma(beta, a.p_full[j], a.G_r[gidx(a.L, j)]);
+        a.p_full[j] = fma(beta, a.p_full[j], Gr[gidx(a.L, j)]);
     if (lead()) {
         put_hist(st, a.hist, k - 1, rel);
         st->relres = rel; st->iters = k; st->rho[k & 3] = rho1;
@@ -189,12 +235,13 @@ __global__ void __launch_bounds__(kNT) k_cg_direction(VecArgs a, const long long
 
 __global__ void __launch_bounds__(kNT) k_finish(VecArgs a, int bicgstab) {
     DevState* st = a.st;
+    if (bicgstab && !is_done(st) && st->maxit >= 1 && !wait_phase(a, kPhaseR, st->maxit)) return;
     if (lead() && !st->done) {
         const long long maxit = st->maxit;
         st->iters = maxit;
         st->status = KS_EMAXIT;
         if (bicgstab && maxit >= 1) {                     // test of the last full step
-            const double rel = sqrt(sum_slots(a.L, a.G_r, 1)) / st->nb;
+            const double rel = sqrt(sum_slots(a.L, Gpar(a, a.G_r, maxit), 1)) / st->nb;
             put_hist(st, a.hist, maxit - 1, rel);
             st->relres = rel;
             if (rel <= st->tol) { st->converged = 1; st->status = KS_OK; }
@@ -210,7 +257,7 @@ __global__ void __launch_bounds__(kNT) k_finish(VecArgs a, int bicgstab) {
 
 // ------------------------------------------------------------- BiCGSTAB (B1-B8)
 __global__ void __launch_bounds__(kNT) k_bs_init(VecArgs a, double tol, long long maxit,
-                                                 long long hist_cap) {
+                                                 long long hist_cap, unsigned long long ebase) {
     __shared__ double red[kNT / 32];
     double acc[1] = {0.0};
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
@@ -220,7 +267,7 @@ __global__ void __launch_bounds__(kNT) k_bs_init(VecArgs a, double tol, long lon
     block_sum<kNT, 1>(acc, red);
     if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
         DevState* st = a.st;
-        init_state(st, tol, maxit, hist_cap);   // rho_old = alpha = omega = 1 (Q8)
+        init_state(st, tol, maxit, hist_cap, ebase);   // rho_old = alpha = omega = 1 (Q8)
         init_decide(st, acc[0], sum_slots(a.L, a.G_r, 1));
     }
 }
@@ -231,10 +278,12 @@ __global__ void __launch_bounds__(kNT) k_bs_p(VecArgs a, const long long* kdev, 
     const long long i = koff + (kdev ? *kdev : 0);
     DevState* st = a.st;
     if (is_done(st)) return;
-    const double rho = sum_slots(a.L, a.G_r, 0);
+    if (i >= 2 && !wait_phase(a, kPhaseR, i - 1)) return;
+    const double* Gr = Gpar(a, a.G_r, i - 1);              // r_{i-1} (+ partials)
+    const double rho = sum_slots(a.L, Gr, 0);
     double rel = 0.0;
     if (i >= 2) {
-        rel = sqrt(sum_slots(a.L, a.G_r, 1)) / st->nb;
+        rel = sqrt(sum_slots(a.L, Gr, 1)) / st->nb;
         if (rel <= st->tol) {
             if (lead()) {
                 put_hist(st, a.hist, i - 2, rel);
@@ -253,14 +302,13 @@ __global__ void __launch_bounds__(kNT) k_bs_p(VecArgs a, const long long* kdev, 
     }
     if (i == 1) {
         for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT)
-            a.p_full[j] = a.G_r[gidx(a.L, j)];
+            a.p_full[j] = Gr[gidx(a.L, j)];
     } else {
         const int q = (int)((i - 1) & 3);
         const double om = st->omega[q];
         const double beta = (rho / st->rho[q]) * (st->alpha[q] / om);
         for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
-            const int64_t gj = gidx(a.L, j);
-            a.p_full[j] = fma(beta, fma(-om, a.G_v[gj], a.p_full[j]), a.G_r[gj]);
+            a.p_full[j] = fma(beta, fma(-om, a.v_full[j], a.p_full[j]), Gr[gidx(a.L, j)]);
         }
     }
     if (lead()) {
@@ -277,16 +325,28 @@ __global__ void __launch_bounds__(kNT) k_bs_s(VecArgs a, const long long* kdev, 
     __shared__ double red[kNT / 32];
     DevState* st = a.st;
     if (is_done(st)) return;
-    const double g = sum_slots(a.L, a.G_v, 0);
+    if (!wait_phase(a, kPhaseV, i)) return;                   // v_i slices + <rhat,v> partials
+    // the <rhat,v> partials were pushed into the local buffer; the v slices are
+    // PULLED from their owners over NVLink in the fused mode (K1 wrote them
+    // locally; its last block released the flag), or read from the NCCL-gathered
+    // local buffer.  A full local copy is kept for the next bs_p.
+    const double* Gv = Gpar(a, a.G_v, i);
+    const double* Gr = Gpar(a, a.G_r, i - 1);
+    const double g = sum_slots(a.L, Gv, 0);
     if (g == 0.0 || !isfinite(g)) {
         if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
         return;
     }
     const double alpha = st->rho[i & 3] / g;
+    const int64_t vpar = (i & 1) * a.gpar;
     double acc[1] = {0.0};
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
-        const int64_t gj = gidx(a.L, j);
-        const double s = fma(-alpha, a.G_v[gj], a.G_r[gj]);
+        int o = 0;
+        while (o + 1 < a.L.P && j >= a.L.row0[o + 1]) ++o;
+        const int64_t gj = (int64_t)o * a.L.chunk + (j - a.L.row0[o]);
+        const double v = a.peer ? __ldcg(a.pp.G_v[o] + vpar + gj) : Gv[gj];
+        a.v_full[j] = v;
+        const double s = fma(-alpha, v, Gr[gj]);
         a.s_full[j] = s;
         acc[0] = fma(s, s, acc[0]);
     }
@@ -319,30 +379,33 @@ __global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, const long long* kdev,
         }
         return;
     }
-    const double ts = sum_scal(a.L, a.S, 0), tt = sum_scal(a.L, a.S, 1);
+    if (!wait_phase(a, kPhaseS, i)) return;                   // <t,s>, <t,t> partials
+    const double* Si = Spar(a, i);
+    const double ts = sum_scal(a.L, Si, 0), tt = sum_scal(a.L, Si, 1);
     const double om = ts / tt;
     if (tt == 0.0 || !isfinite(tt) || om == 0.0 || !isfinite(om)) {
         if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
         return;
     }
     const double alpha = st->alpha[i & 3];
-    double* rl = own_chunk(a, a.G_r);
     const double* sl = a.s_full + r0;
     double acc[2] = {0.0, 0.0};
     for (int64_t l = blockIdx.x * (int64_t)kNT + threadIdx.x; l < m; l += (int64_t)gridDim.x * kNT) {
         const double s = sl[l];
         a.x_loc[l] = fma(om, s, fma(alpha, pl[l], a.x_loc[l]));
         const double r = fma(-om, a.q_loc[l], s);
-        rl[l] = r;
+        publish(a, a.pp.G_r, a.G_r, i, l, r);                // r_i -> every rank (fused C1)
         acc[0] = fma(a.rhat_loc[l], r, acc[0]);
         acc[1] = fma(r, r, acc[1]);
     }
+    if (a.peer) __threadfence_system();
     block_sum<kNT, 2>(acc, red);
     if (grid_sum<kNT, 2>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
-        rl[a.L.pslot + 0] = acc[0];
-        rl[a.L.pslot + 1] = acc[1];
+        publish(a, a.pp.G_r, a.G_r, i, a.L.pslot + 0, acc[0]);
+        publish(a, a.pp.G_r, a.G_r, i, a.L.pslot + 1, acc[1]);
         st->omega[i & 3] = om;
         st->iters = i;
+        publish_phase(a, kPhaseR, i);
     }
 }
 
@@ -377,8 +440,8 @@ int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaSt
     return 1;
 }
 int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
-                   cudaStream_t st) {
-    k_cg_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
+                   unsigned long long ebase, cudaStream_t st) {
+    k_cg_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap, ebase);
     return 1;
 }
 int launch_cg_update(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st) {
@@ -394,8 +457,8 @@ int launch_cg_finish(const VecArgs& a, cudaStream_t st) {
     return 1;
 }
 int launch_bs_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
-                   cudaStream_t st) {
-    k_bs_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
+                   unsigned long long ebase, cudaStream_t st) {
+    k_bs_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap, ebase);
     return 1;
 }
 int launch_bs_p(const VecArgs& a, const long long* kdev, long long i, cudaStream_t st) {

@@ -74,6 +74,41 @@ def test_multi_bicgstab(P):
 
 
 @needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_fused_collectives_bitwise_equal_nccl(P):
+    """NEXT-1: the fused NVLink peer-store collectives carry the same partials and
+    sum them in the same rank order as the NCCL allgathers, so x, the history and
+    the iteration count must be bitwise identical in both modes (and with graphs)."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    n = 4100
+    D, bd = synth.gdd(n, 16)
+    Cs, cs, bs = synth.gspd(4096, 1e4)
+    with ks.Context(n, ngpus=P) as ctx, ks.Context(4096, ngpus=P) as cc:
+        ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
+        assert ctx.get_option("fused_comm") == 1, "peer access expected on NVSwitch B200s"
+        res = {}
+        for fused, graphs in [(0, 0), (1, 0), (1, 1)]:
+            for cx in (ctx, cc):
+                cx.set_option("fused_comm", fused)
+                cx.set_option("use_graphs", graphs)
+            res[(fused, graphs)] = (ctx.bicgstab(bd, tol=1e-10), cc.cg(bs, tol=1e-10),
+                                    ctx.bicgstab(bd, tol=0.0, maxit=37))
+        ref = res[(0, 0)]
+        for key, val in res.items():
+            for (x, h, r), (xr, hr, rr) in zip(val, ref):
+                assert r.iterations == rr.iterations, key
+                assert np.array_equal(x, xr) and np.array_equal(h, hr), key
+    xo, ho, ro = oracle.bicgstab(D, bd, tol=1e-10)
+    x, h, r = ref[0]
+    bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+    xo, ho, ro = oracle.cg(Cs, bs, tol=1e-10)
+    x, h, r = ref[1]
+    bars(x, h, r, xo, ho, ro)
+
+
+@needs2
 def test_multi_edge_cases():
     n = 64
     A = synth.random_spd(n, 10.0, 1)
@@ -115,6 +150,8 @@ def test_torchrun_borrowed_comm(tmp_path, P):
     class Rep:
         iterations = R["it"]
     bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro)
+    assert res[0]["fused_effective"] == 1
+    assert res[0]["bs_mode1"] == res[0]["bs_mode0"]           # fused == NCCL, bitwise
     y = np.array(res[0]["matvec"])
     gemv_bound_check(As, b, y)
     A, b = synth.gdd(n, 16)

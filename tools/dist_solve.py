@@ -33,5 +33,13 @@ with ks.Context.from_process_group(n) as ctx:
             c2.load_rows(A[r0:r1], r0)
             x2, h2, rr = c2.bicgstab(bb, tol=1e-10)
             res["bs_loaded"] = {"x": x2.tolist(), "h": h2.tolist(), "it": rr.iterations}
+# fused NVLink collectives (default) vs NCCL allgathers: bitwise identical
+with ks.Context.from_process_group(n) as ctx:
+    b = ctx.generate("dd", seed=synth.SEED, kd=16)
+    res["fused_effective"] = ctx.get_option("fused_comm")
+    for mode in (1, 0):
+        ctx.set_option("fused_comm", mode)
+        x, h, r = ctx.bicgstab(b, tol=1e-10)
+        res[f"bs_mode{mode}"] = {"x": x.tolist(), "h": h.tolist(), "it": r.iterations}
 json.dump(res, open(os.path.join(outdir, f"dist_{n}_r{rank}.json"), "w"))
 dist.destroy_process_group()
