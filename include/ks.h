@@ -67,9 +67,11 @@ typedef struct {
     double seconds_loop;   /* CUDA-event time of the iteration loop (max over      */
                            /* this context's GPUs); excludes setup and copies      */
     double seconds_total;  /* host wall-clock of the whole call                    */
-    double seconds_gemv;   /* sum of K1 GEMV launch durations inside the loop      */
-                           /* (CUDA events; 0 unless KS_OPT_PROFILE_GEMV = 1)      */
-    int64_t gemv_launches; /* K1 launches inside the loop (per GPU)                */
+    double seconds_gemv;   /* CUDA-event time of the kernels that ran the loop's    */
+                           /* GEMVs: the K1 launches, or (persistent mode) the     */
+                           /* whole-iteration kernels, which also run the vector   */
+                           /* phases; 0 unless KS_OPT_PROFILE_GEMV = 1             */
+    int64_t gemv_launches; /* GEMVs executed inside the loop (per GPU)             */
     int64_t kernel_launches; /* all library kernel launches of the call (per GPU)  */
 } ks_report;
 
@@ -96,12 +98,18 @@ typedef enum {
     KS_OPT_GEMV_KERNEL = 5,   /* K1 variant: 0 = auto, 1 = LDG stream, 2 = TMA    */
                               /* bulk-copy ring                                   */
     KS_OPT_USE_GRAPHS = 6,    /* 1: replay each poll batch as a CUDA graph        */
-    KS_OPT_FUSED_COMM = 7     /* 1 (default): when P > 1 and every GPU pair has   */
+    KS_OPT_FUSED_COMM = 7,    /* 1 (default): when P > 1 and every GPU pair has   */
                               /* peer access, the producing kernels store their   */
                               /* slices/partials straight into every rank's       */
                               /* exchange buffer over NVLink and release an epoch */
                               /* flag (no NCCL call in the loop); 0: NCCL         */
                               /* allgathers.  ks_get_option returns the effective */
+                              /* mode.                                            */
+    KS_OPT_PERSISTENT = 8     /* 0: one kernel per step; 1: one persistent        */
+                              /* cooperative kernel per poll batch (grid barriers */
+                              /* instead of kernel boundaries; needs P == 1 or    */
+                              /* the fused exchange); 2 (default): auto (on when  */
+                              /* eligible).  ks_get_option returns the effective  */
                               /* mode.                                            */
 } ks_option;
 

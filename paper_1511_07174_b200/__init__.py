@@ -27,7 +27,8 @@ KS_ECUDA, KS_ENCCL, KS_ENOMEM, KS_ESTATE = 6, 7, 8, 9
 STATUS_NAMES = {0: "OK", 1: "EARG", 2: "EDIM", 3: "ENOTSPD", 4: "EMAXIT", 5: "EBREAKDOWN",
                 6: "ECUDA", 7: "ENCCL", 8: "ENOMEM", 9: "ESTATE"}
 OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 3,
-           "gemv_split": 4, "gemv_kernel": 5, "use_graphs": 6, "fused_comm": 7}
+           "gemv_split": 4, "gemv_kernel": 5, "use_graphs": 6, "fused_comm": 7,
+           "persistent": 8}
 EXPORTS = ["ks_create", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
            "ks_generate", "ks_matvec", "ks_time_matvec", "ks_cg", "ks_bicgstab",
            "ks_set_option", "ks_get_option", "ks_info", "ks_last_error", "ks_version"]

@@ -347,6 +347,9 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             o.gemv_kernel = v; break;
         case KS_OPT_USE_GRAPHS: o.use_graphs = v ? 1 : 0; break;
         case KS_OPT_FUSED_COMM: o.fused_comm = v ? 1 : 0; break;
+        case KS_OPT_PERSISTENT:
+            if (v < 0 || v > 2) return fail(c, KS_EARG, "persistent must be 0, 1 or 2");
+            o.persistent = v; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -364,6 +367,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_GEMV_KERNEL: *v = o.gemv_kernel; break;
         case KS_OPT_USE_GRAPHS: *v = o.use_graphs; break;
         case KS_OPT_FUSED_COMM: *v = c->fused() ? 1 : 0; break;   // effective value
+        case KS_OPT_PERSISTENT: *v = c->persistent() ? 1 : 0; break;  // effective value
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

@@ -98,6 +98,7 @@ struct Options {
     int64_t gemv_kernel = 0;
     int64_t use_graphs = 0;
     int64_t fused_comm = 1;   // fused NVLink peer-store collectives when available
+    int64_t persistent = 2;   // 0 off, 1 on, 2 auto: persistent cooperative kernels
 };
 
 }  // namespace ks
@@ -116,6 +117,13 @@ struct ks_ctx {
     void for_each_rank(const std::function<void(ks::Rank&)>& fn);
     bool writes_host(const ks::Rank& r) const { return multiprocess || r.rank == 0; }
     bool fused() const { return P > 1 && opt.fused_comm && !ranks.empty() && ranks[0].peer_ok; }
+    // persistent kernels need P == 1 or the fused exchange (no NCCL inside a kernel)
+    bool persistent() const {
+        if (opt.persistent == 0) return false;
+        if (!(P == 1 || fused())) return false;
+        return opt.persistent == 1 || n <= kPersistAutoMaxN;
+    }
+    static constexpr int64_t kPersistAutoMaxN = 1LL << 62;   // tuned from measurements
 };
 
 namespace ks {

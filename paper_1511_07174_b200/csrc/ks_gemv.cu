@@ -31,6 +31,7 @@
 #include <atomic>
 
 #include "ks_device.cuh"
+#include "ks_tile.cuh"
 #include "ks_internal.h"
 
 namespace ks {
@@ -40,12 +41,6 @@ namespace {
 constexpr int kNT = 256;  // threads per CTA
 constexpr int kNW = kNT / 32;
 
-__device__ __forceinline__ double2 ld_stream(const double* p) {
-    return __ldcs(reinterpret_cast<const double2*>(p));
-}
-__device__ __forceinline__ double2 ld_x(const double* p) {
-    return __ldg(reinterpret_cast<const double2*>(p));
-}
 
 // Tile epilogue shared by both variants.  `acc` holds the full-row sums (valid in
 // every thread).  Returns nothing; handles split-K combine, y store, dots.
@@ -147,46 +142,8 @@ __global__ void __launch_bounds__(kNT) k1_gemv_ldg(GemvParams p, int S, int64_t 
     const int64_t ncb = p.ncols / (2 * kNT);
     const int64_t cb0 = s * ncb / S, cb1 = (s + 1) * ncb / S;
 
-    const double* base = p.A + r0 * p.lda + 2 * threadIdx.x;
-    int64_t roff[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) roff[r] = (int64_t)min(r, nvalid - 1) * p.lda;
-    const double* xp = p.x + 2 * threadIdx.x;
-
     double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-
-    int64_t cb = cb0;
-    for (; cb + U <= cb1; cb += U) {
-        double2 av[U][R];
-        double2 xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t c = (cb + u) * (2 * kNT);
-            xv[u] = ld_x(xp + c);
-#pragma unroll
-            for (int r = 0; r < R; ++r) av[u][r] = ld_stream(base + roff[r] + c);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                acc[r] = fma(av[u][r].x, xv[u].x, acc[r]);
-                acc[r] = fma(av[u][r].y, xv[u].y, acc[r]);
-            }
-        }
-    }
-    for (; cb < cb1; ++cb) {
-        const int64_t c = cb * (2 * kNT);
-        const double2 xv = ld_x(xp + c);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const double2 a = ld_stream(base + roff[r] + c);
-            acc[r] = fma(a.x, xv.x, acc[r]);
-            acc[r] = fma(a.y, xv.y, acc[r]);
-        }
-    }
+    stream_rows<R, U, kNT>(p.A, p.lda, r0, nvalid, p.x, cb0, cb1, acc);
     block_sum<kNT, R>(acc, red);
     gemv_epilogue<R>(p, acc, tile, s, S, tiles, qpart, tile_ticket, dpart, ticket, red);
 }

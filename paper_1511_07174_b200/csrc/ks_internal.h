@@ -153,4 +153,9 @@ int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chun
 // iterations (CUDA graph) is replayed with *kdev advanced by k_advance.
 int launch_advance(long long* kdev, long long by, cudaStream_t st);
 
+// Persistent cooperative whole-iteration kernels (ks_persist.cu, NEXT-2).
+int persist_grid(int bicgstab, int num_sms, int64_t mmax);
+int launch_persist(int bicgstab, const VecArgs& a, const double* A, int64_t lda, int64_t ncols,
+                   double* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st);
+
 }  // namespace ks

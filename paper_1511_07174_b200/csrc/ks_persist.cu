@@ -1,0 +1,459 @@
+// NEXT-2: persistent cooperative whole-iteration kernels.
+//
+// One cooperative launch runs a batch of CG / BiCGSTAB iterations (the same
+// rows A1-A5 / B1-B8 as the multi-kernel path), with grid-wide barriers where
+// the multi-kernel path has kernel boundaries.  This removes the per-kernel
+// launch gaps and last-block reductions that dominate small systems (C1: the
+// 8 MiB matrix is L2-resident and a GEMV is ~1 us) and the ~30 us/iteration of
+// vector-kernel overhead at large n.  The GEMV phase streams A with the same
+// inner loop as K1 (ks_tile.cuh) over tiles assigned round-robin to the
+// resident CTAs.  All reductions are fixed-order (tile order within a CTA, CTA
+// order across the grid), so results are deterministic and identical on every
+// rank; the grid size depends only on (n, P) so every rank uses the same one.
+// For P > 1 it requires the fused NVLink exchange (no host-launched NCCL call
+// can run inside a persistent kernel): partial scalars and r slices are pushed
+// to every rank and flagged; v is pulled.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ks_device.cuh"
+#include "ks_internal.h"
+#include "ks_tile.cuh"
+
+namespace ks {
+
+namespace {
+
+constexpr int kNT = 256;
+constexpr int kNW = kNT / 32;
+constexpr int kR = 4;
+constexpr int kU = 4;
+
+// -- small helpers (the same conventions as ks_vec.cu) ------------------------
+__device__ __forceinline__ int64_t m_of(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
+__device__ __forceinline__ int64_t gidx_p(const Layout& L, int64_t j, int* owner) {
+    int g = 0;
+    while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
+    *owner = g;
+    return (int64_t)g * L.chunk + (j - L.row0[g]);
+}
+__device__ __forceinline__ double* par_ptr(double* G, int64_t par, long long k) { return G + (k & 1) * par; }
+__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
+__device__ __forceinline__ bool done_flag(const DevState* st) { return *(volatile const int*)&st->done != 0; }
+__device__ __forceinline__ unsigned long long epoch(const DevState* st, long long k) {
+    return *(volatile const unsigned long long*)&st->ebase + (unsigned long long)k;
+}
+__device__ __forceinline__ double slots_sum(const Layout& L, const double* G, int q) {
+    double s = 0.0;
+    for (int g = 0; g < L.P; ++g) s += G[(int64_t)g * L.chunk + L.pslot + q];
+    return s;
+}
+__device__ __forceinline__ double scal_sum(const Layout& L, const double* S, int q) {
+    double s = 0.0;
+    for (int g = 0; g < L.P; ++g) s += S[g * kScalSlot + q];
+    return s;
+}
+__device__ __forceinline__ void hist_put(DevState* st, double* hist, long long k1, double v) {
+    if (hist && k1 >= 0 && k1 < st->hist_cap) hist[k1] = v;
+}
+
+// Grid-wide barrier (all CTAs co-resident: cooperative launch).  Generation
+// counter: the last arriver resets the count and releases the next generation.
+// Bounded spin: a timeout marks the solve failed instead of hanging.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ bool grid_sync(unsigned* bar, DevState* st) {
+    __shared__ int s_ok;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        unsigned* cnt = bar;
+        unsigned* gen = bar + 1;
+        const unsigned g0 = ld_acquire_gpu(gen);
+        __threadfence();
+        const unsigned arrived = atomicAdd(cnt, 1u) + 1u;
+        if (arrived == gridDim.x) {
+            atomicExch(cnt, 0u);
+            __threadfence();
+            st_release_gpu(gen, g0 + 1u);
+        } else {
+            const unsigned long long t0 = globaltimer_ns();
+            while (ld_acquire_gpu(gen) == g0) {
+                if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                    ok = 0;
+                    st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1;
+                    break;
+                }
+            }
+        }
+        s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+// Sum over CTAs (in CTA order, fixed tree) of slot q of the per-CTA partials;
+// every CTA computes the same value.
+template <int K>
+__device__ __forceinline__ void grid_total(const double* bpart, int q0, double (&out)[K], double* red) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double acc = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kNT) acc += __ldcg(bpart + (int64_t)b * 4 + q0 + k);
+        out[k] = acc;
+    }
+    block_sum<kNT, K>(out, red);
+}
+
+// Fused-mode wait for phase ph of iteration k from every rank (all CTAs).
+__device__ __forceinline__ bool wait_ph(const VecArgs& a, int ph, long long k) {
+    const bool ok = wait_flags(a.flags + ph * kMaxRanks, a.L.P, epoch(a.st, k));
+    if (!ok && threadIdx.x == 0) { a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1; }
+    return ok;
+}
+__device__ __forceinline__ void flags_out(const VecArgs& a, int ph, long long k) {
+    unsigned long long* f[kMaxRanks];
+    for (int g = 0; g < a.L.P; ++g) f[g] = a.pp.flags[g] + ph * kMaxRanks + a.L.rank;
+    publish_flags(f, a.L.P, epoch(a.st, k));
+}
+
+struct PersistArgs {
+    VecArgs a;
+    const double* A;
+    int64_t lda, ncols;
+    double* bpart;      // gridDim.x * 4
+    unsigned* bar;      // {count, generation}
+    long long k0, k1;   // iteration range of this launch (inclusive)
+};
+
+// GEMV phase: y = A_loc x over the tiles of this CTA (round-robin); thread 0
+// returns the CTA's partials <w1, y> and <y, y> accumulated in tile order.
+__device__ void gemv_phase(const PersistArgs& P, const double* x, double* y, const double* w1,
+                           double& d1, double& d2, double* red) {
+    const int64_t m = m_of(P.a.L);
+    const int64_t tiles = (m + kR - 1) / kR;
+    const int64_t ncb = P.ncols / (2 * kNT);
+    d1 = 0.0;
+    d2 = 0.0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t r0 = tile * kR;
+        const int nvalid = (int)min((int64_t)kR, m - r0);
+        double acc[kR];
+        stream_rows<kR, kU, kNT>(P.A, P.lda, r0, nvalid, x, 0, ncb, acc);
+        block_sum<kNT, kR>(acc, red);
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                if (r < nvalid) {
+                    const double yv = acc[r];
+                    y[r0 + r] = yv;
+                    if (w1) d1 = fma(w1[r0 + r], yv, d1);
+                    d2 = fma(yv, yv, d2);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- CG (A1-A5)
+__global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs P) {
+    __shared__ double red[kR * kNW];
+    const VecArgs& a = P.a;
+    const Layout& L = a.L;
+    DevState* st = a.st;
+    const int64_t m = m_of(L), r0 = L.row0[L.rank];
+    const int64_t gstride = (int64_t)gridDim.x * kNT;
+    const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
+    for (long long k = P.k0; k <= P.k1; ++k) {
+        if (done_flag(st)) break;
+        // A1: q = A p, sigma_g = <p_loc, q>
+        double d1, d2;
+        gemv_phase(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
+        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
+        if (!grid_sync(P.bar, st)) return;
+        double sig[1];
+        grid_total<1>(P.bpart, 0, sig, red);
+        double sigma = sig[0];
+        if (a.peer) {                                   // A2 fused C2
+            if (lead()) {
+                for (int g = 0; g < L.P; ++g) a.pp.S[g][(k & 1) * a.spar + L.rank * kScalSlot] = sigma;
+                flags_out(a, kPhaseS, k);
+            }
+            if (!wait_ph(a, kPhaseS, k)) return;
+            sigma = scal_sum(L, par_ptr(a.S, a.spar, k), 0);
+        }
+        if (!(sigma > 0.0)) {                           // Q9
+            if (lead()) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
+            break;
+        }
+        const double alpha = st->rho[(k - 1) & 3] / sigma;
+        // A3: x += alpha p, r -= alpha q, rho'_g
+        const double* rin = par_ptr(a.G_r, a.gpar, k - 1) + (int64_t)L.rank * L.chunk;
+        const int64_t ro = (k & 1) * a.gpar + (int64_t)L.rank * L.chunk;
+        double acc[1] = {0.0};
+        for (int64_t i = tid0; i < m; i += gstride) {
+            a.x_loc[i] = fma(alpha, a.p_full[r0 + i], a.x_loc[i]);
+            const double r = fma(-alpha, a.q_loc[i], rin[i]);
+            if (a.peer) {
+                for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + i] = r;
+            } else {
+                a.G_r[ro + i] = r;
+            }
+            acc[0] = fma(r, r, acc[0]);
+        }
+        if (a.peer) __threadfence_system();
+        block_sum<kNT, 1>(acc, red);
+        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = acc[0];
+        if (!grid_sync(P.bar, st)) return;
+        double rr[1];
+        grid_total<1>(P.bpart, 1, rr, red);
+        double rho1 = rr[0];
+        if (a.peer) {                                   // A4 fused C1 (+ partials)
+            if (lead()) {
+                for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + L.pslot + 1] = rho1;
+                flags_out(a, kPhaseR, k);
+            }
+            if (!wait_ph(a, kPhaseR, k)) return;
+            rho1 = slots_sum(L, par_ptr(a.G_r, a.gpar, k), 1);
+        }
+        // A5: test, beta, p = r + beta p (full, replicated)
+        const double rel = sqrt(rho1) / st->nb;
+        if (rel <= st->tol) {
+            if (lead()) {
+                hist_put(st, a.hist, k - 1, rel);
+                st->relres = rel; st->iters = k; st->converged = 1; st->status = KS_OK; st->done = 1;
+            }
+            break;
+        }
+        const double beta = rho1 / st->rho[(k - 1) & 3];
+        const double* Gr = par_ptr(a.G_r, a.gpar, k);
+        for (int64_t j = tid0; j < L.n; j += gstride) {
+            int o;
+            const int64_t gj = gidx_p(L, j, &o);
+            a.p_full[j] = fma(beta, a.p_full[j], Gr[gj]);
+        }
+        if (lead()) {
+            hist_put(st, a.hist, k - 1, rel);
+            st->relres = rel; st->iters = k; st->rho[k & 3] = rho1; st->alpha[k & 3] = alpha;
+            if (!a.peer) a.G_r[ro + L.pslot + 1] = rho1;    // for the multi-kernel path / finish
+        }
+        if (!grid_sync(P.bar, st)) return;
+    }
+}
+
+// ---------------------------------------------------------- BiCGSTAB (B1-B8)
+__global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
+    __shared__ double red[kR * kNW];
+    const VecArgs& a = P.a;
+    const Layout& L = a.L;
+    DevState* st = a.st;
+    const int64_t m = m_of(L), r0 = L.row0[L.rank];
+    const int64_t gstride = (int64_t)gridDim.x * kNT;
+    const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
+    // scalars of the previous iteration (written by the previous launch / init)
+    double rho_prev = st->rho[(P.k0 - 1) & 3], alpha_prev = st->alpha[(P.k0 - 1) & 3];
+    double omega_prev = st->omega[(P.k0 - 1) & 3];
+    for (long long i = P.k0; i <= P.k1; ++i) {
+        if (done_flag(st)) break;
+        // B8 (test of i-1) + B1
+        if (a.peer && i >= 2 && !wait_ph(a, kPhaseR, i - 1)) return;
+        const double* Gr = par_ptr(a.G_r, a.gpar, i - 1);
+        const double rho = slots_sum(L, Gr, 0);
+        double rel = 0.0;
+        if (i >= 2) {
+            rel = sqrt(slots_sum(L, Gr, 1)) / st->nb;
+            if (rel <= st->tol) {
+                if (lead()) {
+                    hist_put(st, a.hist, i - 2, rel);
+                    st->relres = rel; st->iters = i - 1; st->converged = 1; st->status = KS_OK; st->done = 1;
+                }
+                break;
+            }
+        }
+        if (rho == 0.0 || !isfinite(rho)) {
+            if (lead()) {
+                if (i >= 2) { hist_put(st, a.hist, i - 2, rel); st->relres = rel; }
+                st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1;
+            }
+            break;
+        }
+        if (i == 1) {
+            for (int64_t j = tid0; j < L.n; j += gstride) {
+                int o;
+                a.p_full[j] = Gr[gidx_p(L, j, &o)];
+            }
+        } else {
+            const double beta = (rho / rho_prev) * (alpha_prev / omega_prev);
+            for (int64_t j = tid0; j < L.n; j += gstride) {
+                int o;
+                const int64_t gj = gidx_p(L, j, &o);
+                a.p_full[j] = fma(beta, fma(-omega_prev, a.v_full[j], a.p_full[j]), Gr[gj]);
+            }
+        }
+        if (lead()) {
+            if (i >= 2) { hist_put(st, a.hist, i - 2, rel); st->relres = rel; }
+            st->rho[i & 3] = rho;
+            st->iters = i - 1;
+        }
+        if (!grid_sync(P.bar, st)) return;
+        // B3: v = A p (own chunk of G_v[i&1]), <rhat, v>_g
+        const int64_t vo = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
+        double d1, d2;
+        gemv_phase(P, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red);
+        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
+        if (!grid_sync(P.bar, st)) return;
+        double gm[1];
+        grid_total<1>(P.bpart, 0, gm, red);
+        double gam = gm[0];
+        if (a.peer) {                                   // B2/B4: v pulled, partial pushed
+            if (lead()) {
+                for (int g = 0; g < L.P; ++g) a.pp.G_v[g][vo + L.pslot] = gam;
+                flags_out(a, kPhaseV, i);
+            }
+            if (!wait_ph(a, kPhaseV, i)) return;
+            gam = slots_sum(L, par_ptr(a.G_v, a.gpar, i), 0);
+        }
+        if (gam == 0.0 || !isfinite(gam)) {
+            if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+            break;
+        }
+        const double alpha = rho / gam;
+        // B4/B5: s = r - alpha v (full n, redundant), ||s||^2
+        double sacc[1] = {0.0};
+        for (int64_t j = tid0; j < L.n; j += gstride) {
+            int o;
+            const int64_t gj = gidx_p(L, j, &o);
+            const double v = a.peer ? __ldcg(a.pp.G_v[o] + (i & 1) * a.gpar + gj)
+                                    : a.G_v[(i & 1) * a.gpar + gj];
+            a.v_full[j] = v;
+            const double s = fma(-alpha, v, Gr[gj]);
+            a.s_full[j] = s;
+            sacc[0] = fma(s, s, sacc[0]);
+        }
+        block_sum<kNT, 1>(sacc, red);
+        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = sacc[0];
+        if (!grid_sync(P.bar, st)) return;
+        double ssv[1];
+        grid_total<1>(P.bpart, 1, ssv, red);
+        const double srel = sqrt(ssv[0]) / st->nb;
+        if (srel <= st->tol) {                          // half-step exit
+            for (int64_t l = tid0; l < m; l += gstride) a.x_loc[l] = fma(alpha, a.p_full[r0 + l], a.x_loc[l]);
+            if (lead()) {
+                hist_put(st, a.hist, i - 1, srel);
+                st->alpha[i & 3] = alpha;
+                st->relres = srel; st->half = 1; st->half_iter = i; st->converged = 1;
+                st->status = KS_OK; st->iters = i; st->done = 1;
+            }
+            break;
+        }
+        // B6: t = A s (q_loc), <t, s_loc>_g, <t, t>_g
+        gemv_phase(P, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red);
+        if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 2] = d1; P.bpart[blockIdx.x * 4 + 3] = d2; }
+        if (!grid_sync(P.bar, st)) return;
+        double tv[2];
+        grid_total<2>(P.bpart, 2, tv, red);
+        double ts = tv[0], tt = tv[1];
+        if (a.peer) {                                   // B7 fused C2
+            if (lead()) {
+                for (int g = 0; g < L.P; ++g) {
+                    a.pp.S[g][(i & 1) * a.spar + L.rank * kScalSlot + 0] = ts;
+                    a.pp.S[g][(i & 1) * a.spar + L.rank * kScalSlot + 1] = tt;
+                }
+                flags_out(a, kPhaseS, i);
+            }
+            if (!wait_ph(a, kPhaseS, i)) return;
+            ts = scal_sum(L, par_ptr(a.S, a.spar, i), 0);
+            tt = scal_sum(L, par_ptr(a.S, a.spar, i), 1);
+        }
+        const double om = ts / tt;
+        if (tt == 0.0 || !isfinite(tt) || om == 0.0 || !isfinite(om)) {
+            if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+            break;
+        }
+        // B7: x += alpha p + omega s; r = s - omega t; <rhat, r>_g, <r, r>_g
+        const int64_t ro = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
+        double acc[2] = {0.0, 0.0};
+        for (int64_t l = tid0; l < m; l += gstride) {
+            const double s = a.s_full[r0 + l];
+            a.x_loc[l] = fma(om, s, fma(alpha, a.p_full[r0 + l], a.x_loc[l]));
+            const double r = fma(-om, a.q_loc[l], s);
+            if (a.peer) {
+                for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + l] = r;
+            } else {
+                a.G_r[ro + l] = r;
+            }
+            acc[0] = fma(a.rhat_loc[l], r, acc[0]);
+            acc[1] = fma(r, r, acc[1]);
+        }
+        if (a.peer) __threadfence_system();
+        block_sum<kNT, 2>(acc, red);
+        if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 0] = acc[0]; P.bpart[blockIdx.x * 4 + 1] = acc[1]; }
+        if (!grid_sync(P.bar, st)) return;
+        double rv[2];
+        grid_total<2>(P.bpart, 0, rv, red);
+        if (lead()) {
+            if (a.peer) {
+                for (int g = 0; g < L.P; ++g) {
+                    a.pp.G_r[g][ro + L.pslot + 0] = rv[0];
+                    a.pp.G_r[g][ro + L.pslot + 1] = rv[1];
+                }
+                flags_out(a, kPhaseR, i);
+            } else {
+                a.G_r[ro + L.pslot + 0] = rv[0];
+                a.G_r[ro + L.pslot + 1] = rv[1];
+            }
+            st->alpha[i & 3] = alpha;
+            st->omega[i & 3] = om;
+            st->iters = i;
+        }
+        rho_prev = rho;
+        alpha_prev = alpha;
+        omega_prev = om;
+        // the slots written by the lead are read at the top of the next
+        // iteration: one more barrier (P == 1) or the R flags (fused)
+        if (!a.peer && !grid_sync(P.bar, st)) return;
+    }
+}
+
+int coop_grid(const void* kern, int num_sms, int64_t mmax) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t cap = (int64_t)per_sm * num_sms;
+    const int64_t tiles = (mmax + kR - 1) / kR;
+    int64_t g = tiles < num_sms ? num_sms : tiles;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+}  // namespace
+
+int persist_grid(int bicgstab, int num_sms, int64_t mmax) {
+    return coop_grid(bicgstab ? (const void*)k_bs_persist : (const void*)k_cg_persist, num_sms, mmax);
+}
+
+int launch_persist(int bicgstab, const VecArgs& a, const double* A, int64_t lda, int64_t ncols,
+                   double* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st) {
+    PersistArgs P;
+    P.a = a;
+    P.A = A;
+    P.lda = lda;
+    P.ncols = ncols;
+    P.bpart = bpart;
+    P.bar = bar;
+    P.k0 = k0;
+    P.k1 = k1;
+    void* args[] = {&P};
+    const void* kern = bicgstab ? (const void*)k_bs_persist : (const void*)k_cg_persist;
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kNT), args, 0, st);
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+}  // namespace ks

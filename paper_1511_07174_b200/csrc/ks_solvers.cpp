@@ -61,8 +61,11 @@ struct Prof {
 template <class IterFn>
 void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, IterFn&& iter) {
     const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
-    Prof prof(c, r, B * gemvs_per_iter);
-    const bool use_graph = c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
+    const bool persist = c->persistent();
+    Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
+    int pgrid = 0;
+    if (persist) pgrid = persist_grid(kind, r.num_sms, r.L.pslot);
+    const bool use_graph = !persist && c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
     Rank::GraphCache* g = nullptr;
     if (use_graph) {
         g = &r.graphs[kind];
@@ -92,7 +95,18 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     while (k <= maxit) {
         const int slot = (int)(batch & 1);
         prof.begin(slot);
-        if (use_graph && k + B - 1 <= maxit) {
+        if (persist) {                                    // one cooperative launch per batch
+            const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
+            prof.pre(slot);
+            const int rc = launch_persist(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
+                                          r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
+                                          r.stream);
+            prof.post(slot);
+            if (rc < 0) KS_CUDA((cudaError_t)(-rc));
+            r.launches += 1;
+            r.gemv_launches += (kend - k + 1) * gemvs_per_iter;
+            k = kend + 1;
+        } else if (use_graph && k + B - 1 <= maxit) {
             KS_CUDA(cudaGraphLaunch(g->exec, r.stream));   // iterations k .. k+B-1
             r.launches += g->launches;
             r.gemv_launches += B * gemvs_per_iter;

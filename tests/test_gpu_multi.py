@@ -93,6 +93,7 @@ def test_fused_collectives_bitwise_equal_nccl(P):
             for cx in (ctx, cc):
                 cx.set_option("fused_comm", fused)
                 cx.set_option("use_graphs", graphs)
+                cx.set_option("persistent", 0)
             res[(fused, graphs)] = (ctx.bicgstab(bd, tol=1e-10), cc.cg(bs, tol=1e-10),
                                     ctx.bicgstab(bd, tol=0.0, maxit=37))
         ref = res[(0, 0)]
@@ -106,6 +107,31 @@ def test_fused_collectives_bitwise_equal_nccl(P):
     xo, ho, ro = oracle.cg(Cs, bs, tol=1e-10)
     x, h, r = ref[1]
     bars(x, h, r, xo, ho, ro)
+
+
+@needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_persistent_fused(P):
+    """NEXT-1 + NEXT-2 together: persistent cooperative kernels on every GPU with
+    the fused NVLink exchange; bars vs the oracle; identical on repeat."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    D, bd = synth.gdd(4096, 16)
+    Cs, cs, bs = synth.gspd(4096, 1e4)
+    with ks.Context(4096, ngpus=P) as ctx, ks.Context(4096, ngpus=P) as cc:
+        ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
+        for cx in (ctx, cc):
+            cx.set_option("persistent", 1)
+            assert cx.get_option("persistent") == 1
+        x, h, r = ctx.bicgstab(bd, tol=1e-10)
+        x2, h2, r2 = ctx.bicgstab(bd, tol=1e-10)
+        xc, hc, rc = cc.cg(bs, tol=1e-10)
+    assert np.array_equal(x, x2) and np.array_equal(h, h2)
+    xo, ho, ro = oracle.bicgstab(D, bd, tol=1e-10)
+    bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+    xo, ho, ro = oracle.cg(Cs, bs, tol=1e-10)
+    bars(xc, hc, rc, xo, ho, ro)
 
 
 @needs2
@@ -150,13 +176,18 @@ def test_torchrun_borrowed_comm(tmp_path, P):
     class Rep:
         iterations = R["it"]
     bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro)
-    assert res[0]["fused_effective"] == 1
+    assert res[0]["fused_effective"] == 1 and res[0]["persistent_effective"] == 1
     assert res[0]["bs_mode1"] == res[0]["bs_mode0"]           # fused == NCCL, bitwise
+    for g in range(1, P):
+        assert res[g]["bs_persistent"] == res[0]["bs_persistent"]
     y = np.array(res[0]["matvec"])
     gemv_bound_check(As, b, y)
     A, b = synth.gdd(n, 16)
     xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
     R = res[0]["bs"]
+    Rep.iterations = R["it"]
+    bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro, floor=FLOOR_BS)
+    R = res[0]["bs_persistent"]
     Rep.iterations = R["it"]
     bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro, floor=FLOOR_BS)
     A, b = synth.gdd(n, 4)

@@ -304,3 +304,69 @@ def test_graph_replay_bitwise_equal(method):
     for x, h, it, tol in outs:
         rx, rh, rit, _ = ref[tol]
         assert it == rit and np.array_equal(x, rx) and np.array_equal(h, rh)
+
+
+@pytest.mark.parametrize("persistent", [0, 1])
+def test_persistent_vs_multikernel_parity(persistent):
+    """NEXT-2: the persistent cooperative kernels (grid barriers instead of kernel
+    boundaries) meet the same bars vs the oracle as the multi-kernel path, on CG
+    (C1, G-SPD 4096) and BiCGSTAB (G-DD 1024/4096), and are deterministic."""
+    cases = [("cg", *synth.gspd(1024, 1e3)[::2]), ("cg", *synth.gspd(4096, 1e4)[::2]),
+             ("bicgstab", *synth.gdd(1024, 4)), ("bicgstab", *synth.gdd(4096, 16))]
+    for method, A, b in cases:
+        n = A.shape[0]
+        xo, ho, ro = getattr(oracle, method)(A, b, tol=1e-10)
+        with ks.Context(n) as ctx:
+            ctx.load_rows(A)
+            ctx.set_option("persistent", persistent)
+            assert ctx.get_option("persistent") == persistent
+            x, h, r = getattr(ctx, method)(b, tol=1e-10)
+            x2, h2, r2 = getattr(ctx, method)(b, tol=1e-10)
+            ctx.set_option("poll_batch", 7)
+            x3, h3, r3 = getattr(ctx, method)(b, tol=1e-10)
+        bars(x, h, r, xo, ho, ro, floor=FLOOR_CG if method == "cg" else FLOOR_BS)
+        assert r.half_step_exit == ro.half_step_exit
+        for xx, hh, rr in ((x2, h2, r2), (x3, h3, r3)):
+            assert rr.iterations == r.iterations and np.array_equal(xx, x) and np.array_equal(hh, h)
+
+
+def test_persistent_edge_cases():
+    n = 64
+    A = synth.random_spd(n, 10.0, 1)
+    b = np.random.default_rng(0).standard_normal(n)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        ctx.set_option("persistent", 1)
+        x, h, r = ctx.cg(np.zeros(n), x0=np.ones(n), tol=1e-10)
+        assert r.converged and r.iterations == 0 and np.all(x == 0)
+        xo, ho, ro = oracle.cg(A, b, tol=1e-30, maxit=7)
+        x, h, r = ctx.cg(b, tol=1e-30, maxit=7)
+        assert r.status == ks.KS_EMAXIT and r.iterations == 7 and len(h) == 7
+        bars(x, h, r, xo, ho, ro, iters_tol=0)
+        for q in (1, 3, 64):
+            ctx.set_option("poll_batch", q)
+            x2, h2, r2 = ctx.cg(b, tol=1e-10)
+            x3, h3, r3 = ctx.bicgstab(b, tol=1e-10)
+            if q == 1:
+                ref = (x2, h2, r2.iterations, x3, h3, r3.iterations)
+            assert r2.iterations == ref[2] and np.array_equal(x2, ref[0]) and np.array_equal(h2, ref[1])
+            assert r3.iterations == ref[5] and np.array_equal(x3, ref[3]) and np.array_equal(h3, ref[4])
+        D, bd = synth.gdd(300, 4, seed=synth.SEED2)
+    with ks.Context(300) as ctx:
+        ctx.load_rows(D)
+        ctx.set_option("persistent", 1)
+        xo, ho, ro = oracle.bicgstab(D, bd, tol=1e-30, maxit=3)
+        x, h, r = ctx.bicgstab(bd, tol=1e-30, maxit=3)
+        assert r.status == ks.KS_EMAXIT and r.iterations == 3
+        bars(x, h, r, xo, ho, ro, iters_tol=0, floor=FLOOR_BS)
+    with ks.Context(2) as ctx:
+        ctx.set_option("persistent", 1)
+        ctx.load_rows(np.diag([1.0, -1.0]))
+        x, h, r = ctx.cg(np.array([1.0, 1.0]), tol=1e-12)
+        assert r.status == ks.KS_ENOTSPD and r.iterations == 0
+        ctx.load_rows(np.array([[0.0, 1.0], [-1.0, 0.0]]))
+        x, h, r = ctx.bicgstab(np.array([1.0, 0.0]), tol=1e-12)
+        assert r.status == ks.KS_EBREAKDOWN and r.iterations == 0
+        ctx.load_rows(np.array([[2.0, 1.0], [0.0, 3.0]]))
+        x, h, r = ctx.bicgstab(np.array([3.0, 3.0]), tol=1e-12)
+        assert r.half_step_exit and r.iterations == 1 and np.allclose(x, [1.0, 1.0], rtol=1e-12)

@@ -37,6 +37,10 @@ with ks.Context.from_process_group(n) as ctx:
 with ks.Context.from_process_group(n) as ctx:
     b = ctx.generate("dd", seed=synth.SEED, kd=16)
     res["fused_effective"] = ctx.get_option("fused_comm")
+    res["persistent_effective"] = ctx.get_option("persistent")
+    x, h, r = ctx.bicgstab(b, tol=1e-10)          # default: persistent + fused
+    res["bs_persistent"] = {"x": x.tolist(), "h": h.tolist(), "it": r.iterations}
+    ctx.set_option("persistent", 0)                # multi-kernel: fused vs NCCL bitwise
     for mode in (1, 0):
         ctx.set_option("fused_comm", mode)
         x, h, r = ctx.bicgstab(b, tol=1e-10)

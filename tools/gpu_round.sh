@@ -1,15 +1,15 @@
 #!/bin/bash
-# One GPU call: tests, bench, ncu launch list, ncu full capture of K1.
+# One single-GPU call: tests, smoke, bench (+ multi-kernel variant), ncu launch list, ncu full.
 set -u
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt
-timeout 900 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json
-CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
+timeout 600 python bench.py --kernels multi --no-cpu-baseline > gpurun_out/bench_multi.json 2> gpurun_out/bench_multi.err; echo "bench multi rc=$?"
+CMD="python bench.py --steps 16 --warmup 3 --no-cpu-baseline"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
 timeout 300 $CMD > gpurun_out/plain2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_gemv -s 3 -c 2 -o gpurun_out/prof_k1 $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
-ls -la gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:persist -s 2 -c 2 -o gpurun_out/prof_persist $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"

@@ -55,7 +55,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "lts__t_sector_hit_rate.pct"]
 
 
-def full(path, out, traffic=None, n=None, P=None):
+def full(path, out, traffic=None, n=None, P=None, gemvs=None, persistent=False):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -81,14 +81,20 @@ def full(path, out, traffic=None, n=None, P=None):
     if traffic:
         def to_bytes(s):
             v, u = s.split()
-            v = float(v.replace(",", ""))
+            v = float(v.replace(",", "")) if v not in ("-nan", "nan") else float("nan")
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[u]
-        rd = [to_bytes(r["dram__bytes_read.sum"]) for r in recs]
-        wr = [to_bytes(r["dram__bytes_write.sum"]) for r in recs]
-        per = sum(a + b for a, b in zip(rd, wr)) / len(recs)
-        json.dump({"kernel": recs[0]["kernel"], "n": n, "P": P, "dram_bytes_per_launch": per,
-                   "dram_read_per_launch": sum(rd) / len(rd), "dram_write_per_launch": sum(wr) / len(wr),
-                   "algorithmic_bytes": 8.0 * n * n / P, "source": path},
+        import math
+        g_all = gemvs or [1] * len(recs)
+        ok = [i for i, r in enumerate(recs) if not math.isnan(to_bytes(r["dram__bytes_read.sum"]))]
+        rd = [to_bytes(recs[i]["dram__bytes_read.sum"]) for i in ok]
+        wr = [to_bytes(recs[i]["dram__bytes_write.sum"]) for i in ok]
+        g = [g_all[i] for i in ok]
+        per = sum(a + b for a, b in zip(rd, wr)) / sum(g)
+        json.dump({"kernels": [recs[i]["kernel"] for i in ok], "n": n, "P": P, "persistent": persistent,
+                   "gemvs_per_launch": g,
+                   "dram_bytes_per_launch": per,   # per GEMV when gemvs are given
+                   "dram_read_per_gemv": sum(rd) / sum(g), "dram_write_per_gemv": sum(wr) / sum(g),
+                   "algorithmic_bytes_per_gemv": 8.0 * n * n / P, "source": path},
                   open(traffic, "w"), indent=1)
 
 
@@ -100,4 +106,5 @@ if __name__ == "__main__":
         tr = a[a.index("--traffic") + 1] if "--traffic" in a else None
         n = int(a[a.index("--n") + 1]) if "--n" in a else None
         P = int(a[a.index("--P") + 1]) if "--P" in a else None
-        full(a[2], a[3], tr, n, P)
+        gm = [int(v) for v in a[a.index("--gemvs") + 1].split(",")] if "--gemvs" in a else None
+        full(a[2], a[3], tr, n, P, gm, "--persistent" in a)
