@@ -86,6 +86,12 @@ def lib():
         L.or_spd_exact_solve_ld.argtypes = [i64, _D, u64, _D, _D]
         L.or_true_relres_ld.restype = dbl
         L.or_true_relres_ld.argtypes = [C.POINTER(_Op), _D, _D]
+        L.or_gemv_t.argtypes = [i64, i64, _D, i64, _D, _D]
+        L.or_bicg.restype = C.c_int
+        L.or_bicg.argtypes = [i64, _D, i64, _D, _D, dbl, i64, _D, _D, i64, C.POINTER(_Report),
+                              _D, _D, _D, _D, i64]
+        L.or_gmres.restype = C.c_int
+        L.or_gmres.argtypes = [i64, _D, i64, _D, _D, dbl, i64, i64, _D, _D, i64, C.POINTER(_Report)]
         L.or_hash.restype = u64
         L.or_hash.argtypes = [u64, u64, u64]
         L.or_gen_rows.argtypes = [C.POINTER(_Gen), i64, i64, _D, i64]
@@ -229,6 +235,53 @@ def bicgstab(A, b, x0=None, tol=1e-8, maxit=None, trace: int = 0):
     if trace:
         return out + ({"s": ts, "r": tr},)
     return out
+
+
+def gemv_t(A, x) -> np.ndarray:
+    """y = A^T x for row-major A (sequential sums over rows)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    x = _vec(x, A.shape[0])
+    y = np.empty(A.shape[1])
+    lib().or_gemv_t(A.shape[0], A.shape[1], _p(A), A.shape[1], _p(x), _p(y))
+    return y
+
+
+def bicg(A, b, x0=None, tol=1e-8, maxit=None, trace: int = 0):
+    """BiCG.  Returns (x, hist, report[, trace dict r, rt, p, pt])."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    b = _vec(b, n)
+    x0 = None if x0 is None else _vec(x0, n)
+    maxit = 10 * n if maxit is None else int(maxit)
+    x = np.empty(n)
+    hist = np.zeros(max(maxit, 1))
+    rep = _Report()
+    tr = [None] * 4
+    if trace:
+        tr = [np.zeros((trace, n)) for _ in range(4)]
+    lib().or_bicg(n, _p(A), n, _p(b), _p(x0), float(tol), maxit, _p(x), _p(hist), maxit,
+                  C.byref(rep), *(_p(t) for t in tr), trace)
+    R = _rep(rep)
+    out = (x, hist[:min(R.iterations, maxit)].copy(), R)
+    if trace:
+        return out + (dict(zip(("r", "rt", "p", "pt"), tr)),)
+    return out
+
+
+def gmres(A, b, x0=None, tol=1e-8, restart=30, maxit=None):
+    """Restarted GMRES(m) with MGS Arnoldi.  hist = implicit residuals."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    b = _vec(b, n)
+    x0 = None if x0 is None else _vec(x0, n)
+    maxit = 10 * n if maxit is None else int(maxit)
+    x = np.empty(n)
+    hist = np.zeros(max(maxit, 1))
+    rep = _Report()
+    lib().or_gmres(n, _p(A), n, _p(b), _p(x0), float(tol), int(restart), maxit, _p(x), _p(hist),
+                   maxit, C.byref(rep))
+    R = _rep(rep)
+    return x, hist[:min(R.iterations, maxit)].copy(), R
 
 
 def ge_solve_ld(A, b) -> np.ndarray:

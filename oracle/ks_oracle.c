@@ -316,6 +316,205 @@ done:
 }
 
 /* ------------------------------------------------------------------------- */
+/* Transposed GEMV: y_j = sum_{i<m} a_ij x_i, A row-major m x n (sequential   */
+/* in i for every j).  BiCG's "system's matrix and its transpose" */
+/* ------------------------------------------------------------------------- */
+void or_gemv_t(int64_t m, int64_t n, const double* A, int64_t lda, const double* x, double* y) {
+    for (int64_t j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int64_t i = 0; i < m; ++i) s += A[i * lda + j] * x[i];
+        y[j] = s;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* BiCG -- PAPER.md:33 sec.2: "BiCG generates two mutually orthogonal       */
+/* sequences of residual vectors and A-orthogonal sequences of direction     */
+/* vectors.  The updates for residuals and for the direction vectors are     */
+/* similar to those of the CG method, but are performed using system's       */
+/* matrix and its transpose."  Listing (Fletcher 1976; ext: Barrett et al.,  */
+/* Templates sec.2.3.5), shadow residual rt0 = r0 (Q7), exact-zero or         */
+/* non-finite rho / <pt, A p> -> BREAKDOWN (Q9), test on ||r_k||/||b|| (Q1):   */
+/*   r = b - A x0; rt = r; rho = <rt, r>; p = r; pt = rt                     */
+/*   for k = 1..maxit:                                                        */
+/*     q = A p; qt = A^T pt; sigma = <pt, q>; alpha = rho / sigma             */
+/*     x += alpha p; r -= alpha q; rt -= alpha qt                             */
+/*     hist[k-1] = ||r||/||b||; converged -> stop                              */
+/*     rho1 = <rt, r>; beta = rho1 / rho; p = r + beta p; pt = rt + beta pt    */
+/* trace_* (nullable) receive r_k, rt_k, p_k, pt_k for k = 0..trace_cap-1.    */
+/* ------------------------------------------------------------------------- */
+int or_bicg(int64_t n, const double* A, int64_t lda, const double* b, const double* x0, double tol,
+            int64_t maxit, double* x, double* hist, int64_t hist_cap, or_report* rep,
+            double* trace_r, double* trace_rt, double* trace_p, double* trace_pt, int64_t trace_cap) {
+    or_report R;
+    memset(&R, 0, sizeof R);
+    if (n < 1 || tol < 0 || maxit < 0) { R.status = OR_EARG; if (rep) *rep = R; return OR_EARG; }
+    double* r = (double*)malloc((size_t)n * sizeof(double));
+    double* rt = (double*)malloc((size_t)n * sizeof(double));
+    double* p = (double*)malloc((size_t)n * sizeof(double));
+    double* pt = (double*)malloc((size_t)n * sizeof(double));
+    double* q = (double*)malloc((size_t)n * sizeof(double));
+    double* qt = (double*)malloc((size_t)n * sizeof(double));
+    double nb = or_nrm2(n, b);
+    if (nb == 0.0) {
+        for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
+        R.converged = 1; R.status = OR_OK;
+        goto done;
+    }
+    if (x0) {
+        for (int64_t i = 0; i < n; ++i) x[i] = x0[i];
+        or_gemv(n, n, A, lda, x, q, 1);
+        for (int64_t i = 0; i < n; ++i) r[i] = b[i] - q[i];
+    } else {
+        for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; }
+    }
+    for (int64_t i = 0; i < n; ++i) { rt[i] = r[i]; p[i] = r[i]; pt[i] = r[i]; }
+    double rho = or_dot(n, rt, r);
+    trace_store(trace_r, trace_cap, 0, n, r);
+    trace_store(trace_rt, trace_cap, 0, n, rt);
+    trace_store(trace_p, trace_cap, 0, n, p);
+    trace_store(trace_pt, trace_cap, 0, n, pt);
+    R.relres = or_nrm2(n, r) / nb;
+    if (R.relres <= tol) { R.converged = 1; R.status = OR_OK; goto done; }
+    R.status = OR_EMAXIT;
+    for (int64_t k = 1; k <= maxit; ++k) {
+        if (rho == 0.0 || !finite(rho)) { R.status = OR_EBREAKDOWN; R.breakdown = 1; R.iterations = k - 1; break; }
+        or_gemv(n, n, A, lda, p, q, 1);                     /* q = A p     */
+        or_gemv_t(n, n, A, lda, pt, qt);                    /* qt = A^T pt */
+        double sigma = or_dot(n, pt, q);
+        if (sigma == 0.0 || !finite(sigma)) { R.status = OR_EBREAKDOWN; R.breakdown = 1; R.iterations = k - 1; break; }
+        double alpha = rho / sigma;
+        or_axpy(n, alpha, p, x);
+        or_axpy(n, -alpha, q, r);
+        or_axpy(n, -alpha, qt, rt);
+        double rel = or_nrm2(n, r) / nb;
+        if (hist && k - 1 < hist_cap) hist[k - 1] = rel;
+        R.relres = rel;
+        R.iterations = k;
+        trace_store(trace_r, trace_cap, k, n, r);
+        trace_store(trace_rt, trace_cap, k, n, rt);
+        if (rel <= tol) { R.converged = 1; R.status = OR_OK; break; }
+        double rho1 = or_dot(n, rt, r);
+        double beta = rho1 / rho;
+        for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+        for (int64_t i = 0; i < n; ++i) pt[i] = rt[i] + beta * pt[i];
+        trace_store(trace_p, trace_cap, k, n, p);
+        trace_store(trace_pt, trace_cap, k, n, pt);
+        rho = rho1;
+    }
+    if (R.status == OR_EMAXIT) R.iterations = maxit;
+done:
+    R.matvecs = 2 * R.iterations;
+    free(r); free(rt); free(p); free(pt); free(q); free(qt);
+    if (rep) *rep = R;
+    return R.status;
+}
+
+/* ------------------------------------------------------------------------- */
+/* GMRES(m) -- PAPER.md:31 sec.2: "GMRES uses a Gram-Schmidt                 */
+/* orthogonalization process and requires the storage and computation of an  */
+/* increasing amount of information at each iteration.  These difficulties   */
+/* can be alleviated by restarting the computations after a fixed number of  */
+/* iterations.  The intermediate results are then used as a new initial      */
+/* point."  Listing (Saad & Schultz 1986, the paper's ref [20]): Arnoldi with */
+/* modified Gram-Schmidt (SPEC.md design decision), Givens rotations for the  */
+/* least-squares residual, restart from the current x.                        */
+/*   cycle: r = b - A x; beta = ||r||; v_1 = r / beta; g = beta e_1           */
+/*     for j = 1..m:  w = A v_j                                               */
+/*        for i = 1..j: h_ij = <w, v_i>; w -= h_ij v_i          (MGS)         */
+/*        h_{j+1,j} = ||w||; v_{j+1} = w / h_{j+1,j} (unless 0: exact)        */
+/*        apply rotations 1..j-1 to column j; new rotation zeroes h_{j+1,j};  */
+/*        g_{j+1} = -s_j g_j; g_j = c_j g_j                                    */
+/*        hist[k-1] = |g_{j+1}| / ||b||  (k = total inner steps)               */
+/*        stop the cycle if hist <= tol, h_{j+1,j} == 0 or k == maxit          */
+/*     solve H y = g (upper triangular, back substitution); x += V y           */
+/* iterations = total inner steps; converged when the implicit residual       */
+/* |g_{j+1}|/||b|| <= tol (Q1 analogue).                                       */
+/* ------------------------------------------------------------------------- */
+int or_gmres(int64_t n, const double* A, int64_t lda, const double* b, const double* x0, double tol,
+             int64_t restart, int64_t maxit, double* x, double* hist, int64_t hist_cap, or_report* rep) {
+    or_report R;
+    memset(&R, 0, sizeof R);
+    if (n < 1 || tol < 0 || maxit < 0 || restart < 1) { R.status = OR_EARG; if (rep) *rep = R; return OR_EARG; }
+    const int64_t m = restart;
+    double* V = (double*)malloc((size_t)(m + 1) * (size_t)n * sizeof(double));
+    double* H = (double*)calloc((size_t)(m + 1) * (size_t)m, sizeof(double));   /* H[i*m + j] */
+    double* cs = (double*)malloc((size_t)m * sizeof(double));
+    double* sn = (double*)malloc((size_t)m * sizeof(double));
+    double* g = (double*)malloc((size_t)(m + 1) * sizeof(double));
+    double* y = (double*)malloc((size_t)m * sizeof(double));
+    double* w = (double*)malloc((size_t)n * sizeof(double));
+    double nb = or_nrm2(n, b);
+    int64_t k = 0;
+    if (nb == 0.0) {
+        for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
+        R.converged = 1; R.status = OR_OK;
+        goto done;
+    }
+    for (int64_t i = 0; i < n; ++i) x[i] = x0 ? x0[i] : 0.0;
+    R.status = OR_EMAXIT;
+    for (;;) {
+        or_gemv(n, n, A, lda, x, w, 1);                       /* r = b - A x */
+        for (int64_t i = 0; i < n; ++i) w[i] = b[i] - w[i];
+        double beta = or_nrm2(n, w);
+        R.relres = beta / nb;
+        if (R.relres <= tol) { R.converged = 1; R.status = OR_OK; break; }
+        if (k >= maxit) break;
+        for (int64_t i = 0; i < n; ++i) V[i] = w[i] / beta;
+        for (int64_t i = 0; i <= m; ++i) g[i] = 0.0;
+        g[0] = beta;
+        int64_t j = 0, jdone = 0;
+        int stop = 0;
+        for (j = 0; j < m && k < maxit; ++j) {
+            const double* vj = V + j * n;
+            or_gemv(n, n, A, lda, vj, w, 1);                   /* w = A v_j */
+            for (int64_t i = 0; i <= j; ++i) {                 /* MGS */
+                double h = or_dot(n, w, V + i * n);
+                H[i * m + j] = h;
+                or_axpy(n, -h, V + i * n, w);
+            }
+            double hn = or_nrm2(n, w);
+            H[(j + 1) * m + j] = hn;
+            if (hn != 0.0)
+                for (int64_t i = 0; i < n; ++i) V[(j + 1) * n + i] = w[i] / hn;
+            for (int64_t i = 0; i < j; ++i) {                  /* previous rotations */
+                double a = H[i * m + j], c = H[(i + 1) * m + j];
+                H[i * m + j] = cs[i] * a + sn[i] * c;
+                H[(i + 1) * m + j] = -sn[i] * a + cs[i] * c;
+            }
+            double a = H[j * m + j], c = H[(j + 1) * m + j];
+            double den = sqrt(a * a + c * c);
+            cs[j] = a / den;
+            sn[j] = c / den;
+            H[j * m + j] = den;
+            H[(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++k;
+            double rel = fabs(g[j + 1]) / nb;
+            if (hist && k - 1 < hist_cap) hist[k - 1] = rel;
+            R.relres = rel;
+            jdone = j + 1;
+            if (rel <= tol || hn == 0.0) { stop = 1; break; }
+        }
+        for (int64_t i = jdone - 1; i >= 0; --i) {             /* back substitution */
+            double s = g[i];
+            for (int64_t l = i + 1; l < jdone; ++l) s -= H[i * m + l] * y[l];
+            y[i] = s / H[i * m + i];
+        }
+        for (int64_t i = 0; i < jdone; ++i) or_axpy(n, y[i], V + i * n, x);
+        if (stop) { R.converged = 1; R.status = OR_OK; break; }
+        if (k >= maxit) break;
+    }
+    R.iterations = k;
+done:
+    R.matvecs = R.iterations;
+    free(V); free(H); free(cs); free(sn); free(g); free(y); free(w);
+    if (rep) *rep = R;
+    return R.status;
+}
+
+/* ------------------------------------------------------------------------- */
 /* Reference solutions -- SURVEY.md sec.8(c).5                               */
 /* ------------------------------------------------------------------------- */
 

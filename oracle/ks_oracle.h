@@ -68,6 +68,14 @@ int or_bicgstab(const or_op* op, const double* b, const double* x0, double tol, 
                 double* x, double* hist, int64_t hist_cap, or_report* rep,
                 double* trace_s, double* trace_r, int64_t trace_cap);
 
+/* --- the paper's other Krylov methods --- */
+void or_gemv_t(int64_t m, int64_t n, const double* A, int64_t lda, const double* x, double* y);
+int or_bicg(int64_t n, const double* A, int64_t lda, const double* b, const double* x0, double tol,
+            int64_t maxit, double* x, double* hist, int64_t hist_cap, or_report* rep,
+            double* trace_r, double* trace_rt, double* trace_p, double* trace_pt, int64_t trace_cap);
+int or_gmres(int64_t n, const double* A, int64_t lda, const double* b, const double* x0, double tol,
+             int64_t restart, int64_t maxit, double* x, double* hist, int64_t hist_cap, or_report* rep);
+
 /* --- reference solutions --- */
 int    or_ge_solve_ld(int64_t n, const double* A, int64_t lda, const double* b, double* x);
 void   or_spd_exact_solve_ld(int64_t n, const double* table, uint64_t seed, const double* b,
