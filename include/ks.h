@@ -165,6 +165,17 @@ ks_status ks_cg(ks_ctx* ctx, const double* b, const double* x0, double tol, int6
 ks_status ks_bicgstab(ks_ctx* ctx, const double* b, const double* x0, double tol, int64_t maxit,
                       double* x, double* hist, int64_t hist_cap, ks_report* rep);
 
+/* BiCG (NEXT-3; "performed using system's matrix and its transpose";
+ * listed as implemented at PAPER.md:78, 109).  Fletcher's recurrence with shadow
+ * residual rt0 = r0 (oracle or_bicg); arguments and returns as ks_cg; an exactly
+ * zero or non-finite <rt, r> or <pt, A p> -> KS_EBREAKDOWN.  Two GEMVs per
+ * iteration: A p (K1) and A^T pt (K1T, row-block partials reduce-scattered).    */
+ks_status ks_bicg(ks_ctx* ctx, const double* b, const double* x0, double tol, int64_t maxit,
+                  double* x, double* hist, int64_t hist_cap, ks_report* rep);
+
+/* y = A^T x (n doubles each): the transposed GEMV building block of BiCG (K1T). */
+ks_status ks_matvec_t(ks_ctx* ctx, const double* x, double* y);
+
 ks_status ks_set_option(ks_ctx* ctx, ks_option opt, int64_t value);
 ks_status ks_get_option(const ks_ctx* ctx, ks_option opt, int64_t* value);
 

@@ -30,7 +30,8 @@ OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 
            "gemv_split": 4, "gemv_kernel": 5, "use_graphs": 6, "fused_comm": 7,
            "persistent": 8}
 EXPORTS = ["ks_create", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
-           "ks_generate", "ks_matvec", "ks_time_matvec", "ks_cg", "ks_bicgstab",
+           "ks_generate", "ks_matvec", "ks_matvec_t", "ks_time_matvec", "ks_cg", "ks_bicgstab",
+           "ks_bicg",
            "ks_set_option", "ks_get_option", "ks_info", "ks_last_error", "ks_version"]
 
 
@@ -95,6 +96,8 @@ def lib():
             "ks_load_rows": [vp, i64, i64, vp, i64],
             "ks_generate": [vp, C.POINTER(_GenSpec), vp],
             "ks_matvec": [vp, vp, vp],
+            "ks_matvec_t": [vp, vp, vp],
+            "ks_bicg": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
             "ks_time_matvec": [vp, i32, C.POINTER(dbl)],
             "ks_cg": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
             "ks_bicgstab": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
@@ -256,6 +259,13 @@ class Context:
         self._check(lib().ks_matvec(self._h, _ptr(x), _ptr(y)))
         return y
 
+    def matvec_t(self, x, out=None):
+        """y = A^T x (the transposed GEMV of BiCG)."""
+        x = _f64(x, self.n, "x")
+        y = np.empty(self.n) if out is None else _f64(out, self.n, "out")
+        self._check(lib().ks_matvec_t(self._h, _ptr(x), _ptr(y)))
+        return y
+
     def time_matvec(self, reps: int = 20) -> float:
         s = C.c_double()
         self._check(lib().ks_time_matvec(self._h, int(reps), C.byref(s)))
@@ -287,6 +297,11 @@ class Context:
            hist=True, hist_cap: int = 1 << 20):
         """CG.  Returns (x, hist, Report)."""
         return self._solve(lib().ks_cg, b, x0, tol, maxit, out, hist, hist_cap)
+
+    def bicg(self, b, x0=None, tol: float = 1e-8, maxit: int | None = None, *, out=None,
+             hist=True, hist_cap: int = 1 << 20):
+        """BiCG (PAPER.md:33, NEXT-3).  Returns (x, hist, Report)."""
+        return self._solve(lib().ks_bicg, b, x0, tol, maxit, out, hist, hist_cap)
 
     def bicgstab(self, b, x0=None, tol: float = 1e-8, maxit: int | None = None, *, out=None,
                  hist=True, hist_cap: int = 1 << 20):

@@ -277,7 +277,7 @@ ks_status ks_time_matvec(ks_ctx* c, int32_t reps, double* seconds) {
     return st;
 }
 
-static ks_status solve(ks_ctx* c, bool bicg, const double* b, const double* x0, double tol,
+static ks_status solve(ks_ctx* c, int method, const double* b, const double* x0, double tol,
                        int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep) {
     if (!c) return fail(nullptr, KS_EARG, "ctx is NULL");
     if (!b || !x) return fail(c, KS_EARG, "b and x are required");
@@ -290,8 +290,9 @@ static ks_status solve(ks_ctx* c, bool bicg, const double* b, const double* x0, 
     ks_status st = guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
             const size_t i = (size_t)(&r - c->ranks.data());
-            stat[i] = bicg ? ks::run_bicgstab(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i])
-                           : ks::run_cg(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i]);
+            stat[i] = method == 1 ? ks::run_bicgstab(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i])
+                    : method == 2 ? ks::run_bicg(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i])
+                                  : ks::run_cg(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i]);
             KS_CUDA(cudaGetLastError());
         });
         return KS_OK;
@@ -319,12 +320,40 @@ static ks_status solve(ks_ctx* c, bool bicg, const double* b, const double* x0, 
 
 ks_status ks_cg(ks_ctx* c, const double* b, const double* x0, double tol, int64_t maxit, double* x,
                 double* hist, int64_t hist_cap, ks_report* rep) {
-    return solve(c, false, b, x0, tol, maxit, x, hist, hist_cap, rep);
+    return solve(c, 0, b, x0, tol, maxit, x, hist, hist_cap, rep);
+}
+
+ks_status ks_bicg(ks_ctx* c, const double* b, const double* x0, double tol, int64_t maxit, double* x,
+                  double* hist, int64_t hist_cap, ks_report* rep) {
+    return solve(c, 2, b, x0, tol, maxit, x, hist, hist_cap, rep);
+}
+
+ks_status ks_matvec_t(ks_ctx* c, const double* x, double* y) {
+    if (!c || !x || !y) return fail(c, KS_EARG, "NULL argument");
+    return guarded(c, [&] {
+        c->for_each_rank([&](Rank& r) {
+            if (r.loaded_count < r.m) throw KsError(KS_ESTATE, "matrix not fully loaded");
+            KS_CUDA(cudaMemcpyAsync(r.q_loc, x + r.row0, (size_t)r.m * sizeof(double), cudaMemcpyDefault,
+                                    r.stream));
+            const double* mine = ks::gemv_t(c, r, r.q_loc, nullptr);
+            // gather every rank's rows of A^T x (chunk layout) and copy out
+            if (c->P > 1) {
+                KS_CUDA(cudaMemcpyAsync(r.G_v + (int64_t)r.rank * r.L.chunk, mine,
+                                        (size_t)r.m * sizeof(double), cudaMemcpyDeviceToDevice, r.stream));
+                ks::allgather(c, r, r.G_v, r.L.chunk);
+                if (c->writes_host(r)) ks::copy_chunks_to(c, r, r.G_v, y, cudaMemcpyDefault);
+            } else {
+                KS_CUDA(cudaMemcpyAsync(y, mine, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+            }
+            KS_CUDA(cudaStreamSynchronize(r.stream));
+        });
+        return KS_OK;
+    });
 }
 
 ks_status ks_bicgstab(ks_ctx* c, const double* b, const double* x0, double tol, int64_t maxit,
                       double* x, double* hist, int64_t hist_cap, ks_report* rep) {
-    return solve(c, true, b, x0, tol, maxit, x, hist, hist_cap, rep);
+    return solve(c, 1, b, x0, tol, maxit, x, hist, hist_cap, rep);
 }
 
 ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {

@@ -36,6 +36,8 @@ VecArgs Rank::vargs(bool fused) const {
     a.v_full = v_full;
     a.q_loc = q_loc;
     a.rhat_loc = rhat_loc;
+    a.pt_loc = pt_loc;
+    a.qt_loc = (L.P > 1) ? qt_loc : U;
     a.G_r = G_r;
     a.G_v = G_v;
     a.S = S;
@@ -67,6 +69,9 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     dmalloc(&r.v_full, ld);
     dmalloc(&r.q_loc, r.m + 64);
     dmalloc(&r.rhat_loc, r.m + 64);
+    dmalloc(&r.pt_loc, r.m + 64);
+    dmalloc(&r.U, P * (size_t)r.L.chunk);
+    dmalloc(&r.qt_loc, (size_t)r.L.chunk);
     {
         const size_t g = 2 * P * (size_t)r.L.chunk;
         const size_t sdoubles = (2 * P * kScalSlot + 63) / 64 * 64;
@@ -116,7 +121,8 @@ void rank_free(Rank& r) {
                     (void*)r.q_loc, (void*)r.rhat_loc, (void*)r.xbuf,
                     (void*)r.st, (void*)r.hist, (void*)r.scr.part, (void*)r.scr.ticket,
                     (void*)r.scr.qpart, (void*)r.scr.tile_ticket, (void*)r.table_tmp,
-                    (void*)r.kdev})
+                    (void*)r.kdev, (void*)r.pt_loc, (void*)r.U, (void*)r.qt_loc,
+                    (void*)r.upart, (void*)r.col_ticket})
         if (p) cudaFree(p);
     if (r.h_done) cudaFreeHost(r.h_done);
     if (r.h_state) cudaFreeHost(r.h_state);
@@ -219,6 +225,27 @@ void setup_peers(ks_ctx* c) {
     KS_CUDA(cudaMemcpy(&hok, dok, sizeof(int), cudaMemcpyDeviceToHost));
     KS_CUDA(cudaFree(dok));
     r.peer_ok = hok != 0;
+}
+
+const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done) {
+    const int64_t rc = gemv_t_chunk_rows(r.m, c->ld, r.num_sms);
+    const int64_t nrc = (r.m + rc - 1) / rc;
+    const int64_t need = nrc * c->ld;
+    if (need > r.upart_cap) {
+        if (r.upart) KS_CUDA(cudaFree(r.upart));
+        if (r.col_ticket) KS_CUDA(cudaFree(r.col_ticket));
+        r.upart = nullptr;
+        r.col_ticket = nullptr;
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.upart), (size_t)need * sizeof(double)));
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.col_ticket), (size_t)(c->ld / 512 + 1) * sizeof(unsigned)));
+        KS_CUDA(cudaMemset(r.col_ticket, 0, (size_t)(c->ld / 512 + 1) * sizeof(unsigned)));
+        r.upart_cap = need;
+    }
+    r.launches += launch_gemv_t(r.A, c->ld, r.m, c->n, x_loc, rc, r.upart, r.col_ticket, r.U, r.L, done,
+                                r.stream);
+    if (c->P == 1) return r.U;
+    KS_NCCL(ncclReduceScatter(r.U, r.qt_loc, (size_t)r.L.chunk, ncclDouble, ncclSum, r.comm, r.stream));
+    return r.qt_loc;
 }
 
 GemvConfig gemv_config(const ks_ctx* c, const Rank& r) {

@@ -43,6 +43,12 @@ struct Rank {
     double* v_full = nullptr;   // ld
     double* q_loc = nullptr;    // m
     double* rhat_loc = nullptr; // m
+    double* pt_loc = nullptr;   // m (BiCG)
+    double* U = nullptr;        // P * chunk: K1T output (chunk layout)
+    double* qt_loc = nullptr;   // chunk: reduce-scattered qt (P > 1)
+    double* upart = nullptr;    // K1T row-chunk partials (lazily sized)
+    unsigned* col_ticket = nullptr;
+    int64_t upart_cap = 0;
     // exchange buffers, one allocation (one CUDA IPC handle): G_r, G_v (2 parities
     // x P chunks each), S (2 parities x P x kScalSlot), epoch flags
     double* xbuf = nullptr;
@@ -136,5 +142,10 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
                double* x, double* hist, int64_t hist_cap, ks_report* rep);
 int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,
                      int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep);
+int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
+                 double* x, double* hist, int64_t hist_cap, ks_report* rep);
+// K1T into r.U (chunk layout); for P > 1 reduce-scattered into r.qt_loc.  Returns the
+// pointer holding this rank's rows of A^T x.
+const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done);
 GemvConfig gemv_config(const ks_ctx* c, const Rank& r);
 }  // namespace ks

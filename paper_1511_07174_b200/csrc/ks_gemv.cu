@@ -328,4 +328,105 @@ int launch_gemv(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
     }
 }
 
+
+// ============================================================================
+// K1T -- transposed GEMV u = A_loc^T x_loc (length n) for BiCG (
+// PAPER.md:33 "performed using system's matrix and its transpose").  Row-major
+// A has no contiguous columns, so a CTA owns a block of 512 columns (2 per
+// thread, 128-bit evict-first loads, 4 KiB contiguous per row) and a chunk of
+// RC rows; it accumulates x_i * A[i, cols] over its rows with UT rows in
+// flight.  Row-chunk partials are combined per column block in chunk order by
+// the last-arriving CTA (deterministic).  Same 8*m*n algorithmic bytes as K1.
+// Output in chunk layout (out[g*chunk + (j - row0[g])]) so P > 1 can
+// reduce-scatter it; for P = 1 it is the plain vector.
+// ============================================================================
+namespace {
+
+constexpr int kUT = 8;
+
+__global__ void __launch_bounds__(kNT) k1t_gemv(const double* A, int64_t lda, int64_t m, int64_t n,
+                                               const double* x, int64_t rc_rows, int64_t nrc,
+                                               double* upart, unsigned* col_ticket, double* out,
+                                               Layout L, const int* done) {
+    __shared__ int s_last;
+    if (done && *(volatile const int*)done) return;
+    const int64_t cb = blockIdx.x % (lda / (2 * kNT));
+    const int64_t rc = blockIdx.x / (lda / (2 * kNT));
+    const int64_t col = cb * (2 * kNT) + 2 * threadIdx.x;
+    const int64_t i0 = rc * rc_rows;
+    const int64_t i1 = min(m, i0 + rc_rows);
+    const double* a = A + col;
+    double2 acc = make_double2(0.0, 0.0);
+    int64_t i = i0;
+    for (; i + kUT <= i1; i += kUT) {
+        double2 v[kUT];
+        double xi[kUT];
+#pragma unroll
+        for (int u = 0; u < kUT; ++u) {
+            v[u] = ld_stream(a + (i + u) * lda);
+            xi[u] = __ldg(x + i + u);
+        }
+#pragma unroll
+        for (int u = 0; u < kUT; ++u) {
+            acc.x = fma(v[u].x, xi[u], acc.x);
+            acc.y = fma(v[u].y, xi[u], acc.y);
+        }
+    }
+    for (; i < i1; ++i) {
+        const double2 v = ld_stream(a + i * lda);
+        const double xi = __ldg(x + i);
+        acc.x = fma(v.x, xi, acc.x);
+        acc.y = fma(v.y, xi, acc.y);
+    }
+    if (nrc > 1) {
+        *reinterpret_cast<double2*>(upart + rc * lda + col) = acc;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned t = atomicAdd(&col_ticket[cb], 1u);
+            s_last = (t == (unsigned)(nrc - 1));
+        }
+        __syncthreads();
+        if (!s_last) return;
+        if (threadIdx.x == 0) col_ticket[cb] = 0u;
+        __threadfence();
+        acc = make_double2(0.0, 0.0);
+        for (int64_t q = 0; q < nrc; ++q) {
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(upart + q * lda + col));
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+    }
+    for (int e = 0; e < 2; ++e) {
+        const int64_t j = col + e;
+        if (j >= n) break;
+        int g = 0;
+        while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
+        out[(int64_t)g * L.chunk + (j - L.row0[g])] = e ? acc.y : acc.x;
+    }
+}
+
+}  // namespace
+
+int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms) {
+    const int64_t ncb = lda / (2 * kNT);
+    const int64_t target = 6LL * 4 * num_sms;            // ~6 waves of 4 CTAs/SM
+    int64_t nrc = (target + ncb - 1) / ncb;
+    if (nrc < 1) nrc = 1;
+    int64_t rc = (m + nrc - 1) / nrc;
+    rc = std::max<int64_t>(8, (rc + 7) / 8 * 8);
+    return rc;
+}
+
+int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
+                  int64_t rc_rows, double* upart, unsigned* col_ticket, double* out, const Layout& L,
+                  const int* done, cudaStream_t st) {
+    if (m <= 0) return 0;
+    const int64_t ncb = lda / (2 * kNT);
+    const int64_t nrc = (m + rc_rows - 1) / rc_rows;
+    k1t_gemv<<<(unsigned)(ncb * nrc), kNT, 0, st>>>(A, lda, m, n, x, rc_rows, nrc, upart, col_ticket,
+                                                    out, L, done);
+    return 1;
+}
+
 }  // namespace ks

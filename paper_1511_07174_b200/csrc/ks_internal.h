@@ -104,6 +104,13 @@ int launch_gemv(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
 GemvConfig choose_gemv(int64_t m, int64_t ncols, int num_sms, int rows_opt, int split_opt,
                        int variant_opt);
 
+// K1T: u = A_loc^T x_loc (BiCG), chunk-layout output; upart holds
+// ceil(m / rc_rows) x lda partials, col_ticket lda / 512 counters.
+int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms);
+int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
+                  int64_t rc_rows, double* upart, unsigned* col_ticket, double* out, const Layout& L,
+                  const int* done, cudaStream_t st);
+
 int launch_gen_spd(double* A, int64_t lda, int64_t row0, int64_t m, int64_t n, uint64_t seed,
                    const double* table_dev, cudaStream_t st);
 int launch_gen_dd(double* A, int64_t lda, int64_t row0, int64_t m, int64_t n, uint64_t seed,
@@ -122,7 +129,9 @@ struct VecArgs {
     double* s_full;        // ld
     double* v_full;        // ld (BiCGSTAB: local copy of the gathered v)
     double* q_loc;         // m (CG q / BiCGSTAB t)
-    double* rhat_loc;      // m
+    double* rhat_loc;      // m (BiCGSTAB rhat; BiCG's shadow residual rt)
+    double* pt_loc;        // m (BiCG shadow direction pt)
+    const double* qt_loc;  // m (BiCG qt = (A^T pt) rows of this rank)
     double* G_r;           // P * chunk
     double* G_v;           // P * chunk
     double* S;             // P * kScalSlot
@@ -152,6 +161,11 @@ int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chun
 // Iteration kernels use k = koff + (kdev ? *kdev : 0): a captured batch of
 // iterations (CUDA graph) is replayed with *kdev advanced by k_advance.
 int launch_advance(long long* kdev, long long by, cudaStream_t st);
+// BiCG (NEXT-3)
+int launch_bicg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
+                     cudaStream_t st);
+int launch_bicg_update(const VecArgs& a, long long k, cudaStream_t st);
+int launch_bicg_direction(const VecArgs& a, long long k, cudaStream_t st);
 
 // Persistent cooperative whole-iteration kernels (ks_persist.cu, NEXT-2).
 int persist_grid(int bicgstab, int num_sms, int64_t mmax);

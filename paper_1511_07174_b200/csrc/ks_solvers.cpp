@@ -341,4 +341,60 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
 }
 
+// BiCG (NEXT-3): multi-kernel schedule; NCCL for P > 1 (allgather of
+// [r | <rt,r>, <r,r>], scalar allgather of <pt, A p>, reduce-scatter of A^T pt).
+int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
+                 double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    const auto t_start = Clock::now();
+    check_loaded(c, r);
+    r.launches = 0;
+    r.gemv_launches = 0;
+    r.gemv_seconds = 0.0;
+    setup(c, r, b, x0, hist_cap);                  // r0, x, rt0 = r0, slots <r0,r0>
+    VecArgs a = r.vargs(false);
+    r.launches += launch_bicg_init(a, tol, maxit, hist_cap, r.stream);
+    GemvParams pq = gp(c, r, r.p_full, r.q_loc);   // q = A p, sigma_g = <pt_loc, q>
+    pq.w1 = r.pt_loc;
+    pq.out1 = r.S + (int64_t)r.rank * kScalSlot;
+    pq.done = &r.st->done;
+    const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
+    Prof prof(c, r, 2 * B);
+    int64_t k = 1, batch = 0;
+    KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+    while (k <= maxit) {
+        const int slot = (int)(batch & 1);
+        prof.begin(slot);
+        const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
+        for (; k <= kend; ++k) {
+            prof.pre(slot);
+            gemv(c, r, pq);                                    // q = A p
+            prof.post(slot);
+            prof.pre(slot);
+            gemv_t(c, r, r.pt_loc, &r.st->done);               // qt = A^T pt (+ reduce-scatter)
+            prof.post(slot);
+            r.gemv_launches += 2;
+            allgather(c, r, r.S, kScalSlot);
+            r.launches += launch_bicg_update(a, k, r.stream);
+            allgather(c, r, r.G_r, r.L.chunk);
+            r.launches += launch_bicg_direction(a, k, r.stream);
+        }
+        KS_CUDA(cudaMemcpyAsync(&r.h_done[slot], &r.st->done, sizeof(int), cudaMemcpyDeviceToHost, r.stream));
+        KS_CUDA(cudaEventRecord(r.ev_poll[slot], r.stream));
+        if (batch >= 1) {
+            KS_CUDA(cudaEventSynchronize(r.ev_poll[slot ^ 1]));
+            prof.harvest(slot ^ 1);
+            if (r.h_done[slot ^ 1]) { ++batch; break; }
+        }
+        ++batch;
+    }
+    KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    prof.harvest(0);
+    prof.harvest(1);
+    r.launches += launch_cg_finish(a, r.stream);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+    if (rep) rep->matvecs = 2 * rep->iterations;
+    return r.h_state->status;
+}
+
 }  // namespace ks

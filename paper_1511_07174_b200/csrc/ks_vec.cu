@@ -409,6 +409,94 @@ __global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, const long long* kdev,
     }
 }
 
+// ---------------------------------------------------------------- BiCG (NEXT-3)
+// Fletcher's BiCG (oracle or_bicg): p = r + beta p (full, replicated like CG),
+// the shadow pair (rt, pt) stays sharded: qt rows come from K1T + reduce-scatter.
+__global__ void __launch_bounds__(kNT) k_bicg_init(VecArgs a, double tol, long long maxit,
+                                                   long long hist_cap) {
+    __shared__ double red[kNT / 32];
+    const int64_t m = m_loc(a.L);
+    double acc[1] = {0.0};
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
+        a.p_full[j] = a.G_r[gidx(a.L, j)];                  // p0 = r0
+        const double bj = a.b_full[j];
+        acc[0] = fma(bj, bj, acc[0]);
+    }
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
+        a.pt_loc[i] = a.rhat_loc[i];                        // pt0 = rt0 = r0 (Q7)
+    block_sum<kNT, 1>(acc, red);
+    if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        DevState* st = a.st;
+        init_state(st, tol, maxit, hist_cap, 0);
+        st->rho[0] = sum_slots(a.L, a.G_r, 0);              // <rt0, r0>
+        init_decide(st, acc[0], sum_slots(a.L, a.G_r, 1));
+    }
+}
+
+// sigma = <pt, A p> (K1 partials); alpha; x += alpha p; r -= alpha q; rt -= alpha qt;
+// partials <rt, r>, <r, r> into the own slots of G_r.
+__global__ void __launch_bounds__(kNT) k_bicg_update(VecArgs a, long long k) {
+    __shared__ double red[2 * (kNT / 32)];
+    DevState* st = a.st;
+    if (is_done(st)) return;
+    const double sigma = sum_scal(a.L, a.S, 0);
+    if (sigma == 0.0 || !isfinite(sigma)) {
+        if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = k - 1; st->done = 1; }
+        return;
+    }
+    const double alpha = st->rho[(k - 1) & 3] / sigma;
+    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    double* rl = own_chunk(a, a.G_r);
+    double acc[2] = {0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
+        a.x_loc[i] = fma(alpha, a.p_full[r0 + i], a.x_loc[i]);
+        const double r = fma(-alpha, a.q_loc[i], rl[i]);
+        rl[i] = r;
+        const double rt = fma(-alpha, a.qt_loc[i], a.rhat_loc[i]);
+        a.rhat_loc[i] = rt;
+        acc[0] = fma(rt, r, acc[0]);
+        acc[1] = fma(r, r, acc[1]);
+    }
+    block_sum<kNT, 2>(acc, red);
+    if (grid_sum<kNT, 2>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        rl[a.L.pslot + 0] = acc[0];
+        rl[a.L.pslot + 1] = acc[1];
+        st->alpha[k & 3] = alpha;
+    }
+}
+
+// test (Q1), rho' breakdown (Q9), beta, p = r + beta p (full), pt = rt + beta pt.
+__global__ void __launch_bounds__(kNT) k_bicg_direction(VecArgs a, long long k) {
+    DevState* st = a.st;
+    if (is_done(st)) return;
+    const double rho1 = sum_slots(a.L, a.G_r, 0);
+    const double rel = sqrt(sum_slots(a.L, a.G_r, 1)) / st->nb;
+    if (rel <= st->tol) {
+        if (lead()) {
+            put_hist(st, a.hist, k - 1, rel);
+            st->relres = rel; st->iters = k; st->converged = 1; st->status = KS_OK; st->done = 1;
+        }
+        return;
+    }
+    if (rho1 == 0.0 || !isfinite(rho1)) {
+        if (lead()) {
+            put_hist(st, a.hist, k - 1, rel);
+            st->relres = rel; st->iters = k; st->status = KS_EBREAKDOWN; st->breakdown = 1; st->done = 1;
+        }
+        return;
+    }
+    const double beta = rho1 / st->rho[(k - 1) & 3];
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT)
+        a.p_full[j] = fma(beta, a.p_full[j], a.G_r[gidx(a.L, j)]);
+    const int64_t m = m_loc(a.L);
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
+        a.pt_loc[i] = fma(beta, a.pt_loc[i], a.rhat_loc[i]);
+    if (lead()) {
+        put_hist(st, a.hist, k - 1, rel);
+        st->relres = rel; st->iters = k; st->rho[k & 3] = rho1;
+    }
+}
+
 __global__ void k_advance(long long* kdev, long long by) {
     if (threadIdx.x == 0 && blockIdx.x == 0) *kdev += by;
 }
@@ -479,6 +567,19 @@ int launch_bs_finish(const VecArgs& a, cudaStream_t st) {
 }
 int launch_advance(long long* kdev, long long by, cudaStream_t st) {
     k_advance<<<1, 32, 0, st>>>(kdev, by);
+    return 1;
+}
+int launch_bicg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
+                     cudaStream_t st) {
+    k_bicg_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
+    return 1;
+}
+int launch_bicg_update(const VecArgs& a, long long k, cudaStream_t st) {
+    k_bicg_update<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, k);
+    return 1;
+}
+int launch_bicg_direction(const VecArgs& a, long long k, cudaStream_t st) {
+    k_bicg_direction<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, k);
     return 1;
 }
 int launch_true_res_final(const VecArgs& a, cudaStream_t st) {

@@ -135,6 +135,24 @@ def test_multi_persistent_fused(P):
 
 
 @needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_bicg(P):
+    """NEXT-3 BiCG at P GPUs: K1T partials reduce-scattered over NCCL."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    for n, kd in [(1024, 4), (4099, 16)]:
+        A, b = synth.gdd(n, kd)
+        xo, ho, ro = oracle.bicg(A, b, tol=1e-10)
+        with ks.Context(n, ngpus=P) as ctx:
+            ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
+            x, h, r = ctx.bicg(b, tol=1e-10)
+            xt = np.random.default_rng(3).standard_normal(n)
+            yt = ctx.matvec_t(xt)
+        bars(x, h, r, xo, ho, ro)
+        gemv_bound_check(np.ascontiguousarray(A.T), xt, yt)
+
+
+@needs2
 def test_multi_edge_cases():
     n = 64
     A = synth.random_spd(n, 10.0, 1)

@@ -370,3 +370,57 @@ def test_persistent_edge_cases():
         ctx.load_rows(np.array([[2.0, 1.0], [0.0, 3.0]]))
         x, h, r = ctx.bicgstab(np.array([3.0, 3.0]), tol=1e-12)
         assert r.half_step_exit and r.iterations == 1 and np.allclose(x, [1.0, 1.0], rtol=1e-12)
+
+
+# ------------------------------------------------------------- NEXT-3: BiCG (K1T)
+
+@pytest.mark.parametrize("n", [1, 3, 100, 513, 1000, 3000])
+def test_gemv_t_parity_ragged(n):
+    """K1T: y = A^T x vs a long-double column sum, forward-error bound of any
+    summation order (the transposed GEMV BiCG needs)."""
+    rng = np.random.default_rng(n + 7)
+    A = rng.standard_normal((n, n))
+    x = rng.standard_normal(n)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        y = ctx.matvec_t(x)
+        y2 = ctx.matvec_t(x)
+    gemv_bound_check(np.ascontiguousarray(A.T), x, y)
+    assert np.array_equal(y, y2)
+    assert np.allclose(y, oracle.gemv_t(A, x), rtol=0, atol=gamma(n) * float(np.max(np.abs(A.T) @ np.abs(x))))
+
+
+@pytest.mark.parametrize("n,kd", [(1024, 4), (1024, 16), (4096, 16)])
+def test_bicg_parity(n, kd):
+    A, b = synth.gdd(n, kd)
+    xo, ho, ro = oracle.bicg(A, b, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
+        x, h, r = ctx.bicg(b, tol=1e-10)
+    assert r.converged and r.matvecs == 2 * r.iterations
+    bars(x, h, r, xo, ho, ro)
+    assert r.true_relres <= 10 * 1e-10
+
+
+def test_bicg_edges_and_spd_equivalence():
+    n = 256
+    A, c, b = synth.gspd(n, 100.0)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        xb, hb, rb = ctx.bicg(b, tol=1e-10)
+        xc, hc, rc = ctx.cg(b, tol=1e-10)
+        assert abs(rb.iterations - rc.iterations) <= 1                  # SPEC.md:550
+        assert np.linalg.norm(xb - xc) <= 1e-9 * np.linalg.norm(xc)
+        x, h, r = ctx.bicg(np.zeros(n), tol=1e-10)
+        assert r.converged and r.iterations == 0 and np.all(x == 0)
+        xo, ho, ro = oracle.bicg(A, b, tol=1e-30, maxit=6)
+        x, h, r = ctx.bicg(b, tol=1e-30, maxit=6)
+        assert r.status == ks.KS_EMAXIT and r.iterations == 6
+        bars(x, h, r, xo, ho, ro, iters_tol=0)
+    with ks.Context(2) as ctx:
+        ctx.load_rows(np.array([[0.0, 1.0], [1.0, 0.0]]))
+        x, h, r = ctx.bicg(np.array([1.0, 0.0]), tol=1e-12)
+        assert r.status == ks.KS_EBREAKDOWN and r.iterations == 0
+        ctx.load_rows(np.array([[2.0, 1.0], [0.0, 3.0]]))
+        x, h, r = ctx.bicg(np.array([3.0, 3.0]), tol=1e-12)
+        assert r.converged and np.allclose(x, [1.0, 1.0], rtol=1e-12)
