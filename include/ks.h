@@ -173,6 +173,16 @@ ks_status ks_bicgstab(ks_ctx* ctx, const double* b, const double* x0, double tol
 ks_status ks_bicg(ks_ctx* ctx, const double* b, const double* x0, double tol, int64_t maxit,
                   double* x, double* hist, int64_t hist_cap, ks_report* rep);
 
+/* Restarted GMRES(m) (NEXT-3; "Gram-Schmidt orthogonalization ...
+ * restarting the computations after a fixed number of iterations", listed as
+ * implemented at PAPER.md:78, 109).  Arnoldi with classical Gram-Schmidt applied
+ * twice, Givens rotations, restart from the current x.  1 <= restart <= 63.
+ * iterations = total inner (Arnoldi) steps; hist receives the implicit residual
+ * |g_{j+1}|/||b|| of every inner step; converged when it is <= tol (or on a
+ * lucky breakdown).  Returns KS_OK or KS_EMAXIT (x = the last update).           */
+ks_status ks_gmres(ks_ctx* ctx, const double* b, const double* x0, double tol, int32_t restart,
+                   int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep);
+
 /* y = A^T x (n doubles each): the transposed GEMV building block of BiCG (K1T). */
 ks_status ks_matvec_t(ks_ctx* ctx, const double* x, double* y);
 

@@ -31,7 +31,7 @@ OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 
            "persistent": 8}
 EXPORTS = ["ks_create", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
            "ks_generate", "ks_matvec", "ks_matvec_t", "ks_time_matvec", "ks_cg", "ks_bicgstab",
-           "ks_bicg",
+           "ks_bicg", "ks_gmres",
            "ks_set_option", "ks_get_option", "ks_info", "ks_last_error", "ks_version"]
 
 
@@ -98,6 +98,7 @@ def lib():
             "ks_matvec": [vp, vp, vp],
             "ks_matvec_t": [vp, vp, vp],
             "ks_bicg": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
+            "ks_gmres": [vp, vp, vp, dbl, i32, i64, vp, vp, i64, C.POINTER(_Report)],
             "ks_time_matvec": [vp, i32, C.POINTER(dbl)],
             "ks_cg": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
             "ks_bicgstab": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
@@ -302,6 +303,13 @@ class Context:
              hist=True, hist_cap: int = 1 << 20):
         """BiCG (PAPER.md:33, NEXT-3).  Returns (x, hist, Report)."""
         return self._solve(lib().ks_bicg, b, x0, tol, maxit, out, hist, hist_cap)
+
+    def gmres(self, b, x0=None, tol: float = 1e-8, restart: int = 30, maxit: int | None = None, *,
+              out=None, hist=True, hist_cap: int = 1 << 20):
+        """Restarted GMRES(m) (NEXT-3).  Returns (x, hist, Report)."""
+        r = int(restart)
+        fn = lambda h, b_, x0_, tol_, mx, x_, hi, cap, rep: lib().ks_gmres(h, b_, x0_, tol_, r, mx, x_, hi, cap, rep)
+        return self._solve(fn, b, x0, tol, maxit, out, hist, hist_cap)
 
     def bicgstab(self, b, x0=None, tol: float = 1e-8, maxit: int | None = None, *, out=None,
                  hist=True, hist_cap: int = 1 << 20):

@@ -328,6 +328,38 @@ ks_status ks_bicg(ks_ctx* c, const double* b, const double* x0, double tol, int6
     return solve(c, 2, b, x0, tol, maxit, x, hist, hist_cap, rep);
 }
 
+ks_status ks_gmres(ks_ctx* c, const double* b, const double* x0, double tol, int32_t restart,
+                   int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    if (!c) return fail(nullptr, KS_EARG, "ctx is NULL");
+    if (!b || !x) return fail(c, KS_EARG, "b and x are required");
+    if (!(tol >= 0.0)) return fail(c, KS_EARG, "tol must be >= 0");
+    if (maxit < 0) return fail(c, KS_EARG, "maxit must be >= 0");
+    if (restart < 1 || restart >= ks::kMaxBasis) return fail(c, KS_EARG, "restart must be in [1, 63]");
+    if (hist_cap < 0 || (hist_cap > 0 && !hist)) return fail(c, KS_EARG, "bad hist/hist_cap");
+    if (!hist) hist_cap = 0;
+    std::vector<ks_report> reps(c->ranks.size());
+    std::vector<int64_t> stat(c->ranks.size(), 0);
+    ks_status st = guarded(c, [&] {
+        c->for_each_rank([&](Rank& r) {
+            const size_t i = (size_t)(&r - c->ranks.data());
+            stat[i] = ks::run_gmres(c, r, b, x0, tol, restart, maxit, x, hist, hist_cap, &reps[i]);
+            KS_CUDA(cudaGetLastError());
+        });
+        return KS_OK;
+    });
+    if (st != KS_OK) return st;
+    ks_report R = reps[0];
+    for (auto& q : reps) {
+        R.seconds_loop = std::max(R.seconds_loop, q.seconds_loop);
+        R.seconds_total = std::max(R.seconds_total, q.seconds_total);
+        R.seconds_gemv = std::max(R.seconds_gemv, q.seconds_gemv);
+    }
+    if (rep) *rep = R;
+    const ks_status s = (ks_status)stat[0];
+    if (s == KS_EMAXIT) { c->last_error = "maximum iterations reached"; g_tls_error = c->last_error; }
+    return s;
+}
+
 ks_status ks_matvec_t(ks_ctx* c, const double* x, double* y) {
     if (!c || !x || !y) return fail(c, KS_EARG, "NULL argument");
     return guarded(c, [&] {

@@ -46,6 +46,13 @@ struct Rank {
     double* pt_loc = nullptr;   // m (BiCG)
     double* U = nullptr;        // P * chunk: K1T output (chunk layout)
     double* qt_loc = nullptr;   // chunk: reduce-scattered qt (P > 1)
+    // GMRES(m) workspace (lazily sized by the restart length)
+    double* gmV = nullptr;
+    int64_t gm_ldv = 0;
+    int gm_m = 0;
+    double* gmH = nullptr;      // (m+1) x m + cs, sn (m) + g (m+1)
+    double* gm_hx = nullptr;    // P x kMaxBasis
+    GmresState* gm_state = nullptr;
     double* upart = nullptr;    // K1T row-chunk partials (lazily sized)
     unsigned* col_ticket = nullptr;
     int64_t upart_cap = 0;
@@ -142,6 +149,8 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
                double* x, double* hist, int64_t hist_cap, ks_report* rep);
 int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,
                      int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep);
+int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int restart,
+                  int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep);
 int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
                  double* x, double* hist, int64_t hist_cap, ks_report* rep);
 // K1T into r.U (chunk layout); for P > 1 reduce-scattered into r.qt_loc.  Returns the

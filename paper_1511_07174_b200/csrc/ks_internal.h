@@ -161,6 +161,36 @@ int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chun
 // Iteration kernels use k = koff + (kdev ? *kdev : 0): a captured batch of
 // iterations (CUDA graph) is replayed with *kdev advanced by k_advance.
 int launch_advance(long long* kdev, long long by, cudaStream_t st);
+// GMRES(m) (NEXT-3, ks_gmres.cu)
+constexpr int kMaxBasis = 64;          // restart length m <= kMaxBasis - 1
+struct GmresState {
+    long long jdone;    // Arnoldi steps completed in the current cycle
+    int cycle_end;      // the current cycle ended (convergence, m steps, maxit)
+    int converged;
+    int skip;           // done || cycle_end: K1 launches of the cycle exit early
+};
+struct GmresArgs {
+    VecArgs a;
+    double* V;          // (m+1) basis slices, V_i at V + i * ldv (own rows)
+    int64_t ldv;
+    int mres;           // m
+    double* H;          // (m+1) x m, row-major H[i * m + j]
+    double* cs;
+    double* sn;
+    double* g;          // m+1
+    double* hx;         // P x kMaxBasis: partial dots, gathered in place
+    GmresState* gs;
+    double* part;       // gridDim.x x kMaxBasis CTA partials
+    unsigned* ticket;
+};
+int launch_gm_init(const GmresArgs& g, double tol, long long maxit, long long hist_cap, cudaStream_t st);
+int launch_gm_start(const GmresArgs& g, cudaStream_t st);
+int launch_gm_dots(const GmresArgs& g, int j, cudaStream_t st);
+int launch_gm_orth(const GmresArgs& g, int j, int pass, cudaStream_t st);
+int launch_gm_step_end(const GmresArgs& g, int j, long long k, cudaStream_t st);
+int launch_gm_vfull(const GmresArgs& g, cudaStream_t st);
+int launch_gm_cycle_end(const GmresArgs& g, long long k_enqueued, cudaStream_t st);
+
 // BiCG (NEXT-3)
 int launch_bicg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
                      cudaStream_t st);

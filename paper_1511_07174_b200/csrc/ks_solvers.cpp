@@ -341,6 +341,115 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
 }
 
+// GMRES(m) (NEXT-3): host-orchestrated cycles (their structure is
+// deterministic; an early exit inside a cycle makes the remaining launches of the
+// cycle no-ops through GmresState::skip).  NCCL for P > 1.
+int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int restart,
+                  int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    const auto t_start = Clock::now();
+    check_loaded(c, r);
+    r.launches = 0;
+    r.gemv_launches = 0;
+    r.gemv_seconds = 0.0;
+    const size_t nbytes = (size_t)c->n * sizeof(double);
+    if (hist_cap > r.hist_alloc) {
+        KS_CUDA(cudaFree(r.hist));
+        r.hist = nullptr;
+        r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.hist), (size_t)r.hist_alloc * sizeof(double)));
+    }
+    if (r.gm_m < restart || !r.gmV) {
+        for (void* p : {(void*)r.gmV, (void*)r.gmH, (void*)r.gm_hx, (void*)r.gm_state})
+            if (p) KS_CUDA(cudaFree(p));
+        r.gm_ldv = (r.m + 31) / 32 * 32;
+        r.gm_m = restart;
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gmV), (size_t)(restart + 1) * r.gm_ldv * sizeof(double)));
+        const size_t hsz = (size_t)(restart + 1) * restart + 3 * (size_t)(restart + 1);
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gmH), hsz * sizeof(double)));
+        KS_CUDA(cudaMemset(r.gmH, 0, hsz * sizeof(double)));
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gm_hx), (size_t)c->P * kMaxBasis * sizeof(double)));
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gm_state), sizeof(GmresState)));
+        KS_CUDA(cudaMemset(r.gm_state, 0, sizeof(GmresState)));
+    }
+    VecArgs a = r.vargs(false);
+    GmresArgs g;
+    g.a = a;
+    g.V = r.gmV;
+    g.ldv = r.gm_ldv;
+    g.mres = restart;
+    g.H = r.gmH;
+    g.cs = r.gmH + (size_t)(restart + 1) * restart;
+    g.sn = g.cs + (restart + 1);
+    g.g = g.sn + (restart + 1);
+    g.hx = r.gm_hx;
+    g.gs = r.gm_state;
+    g.part = r.scr.part + 3 * kPartStride;     // 296 CTAs x 64 <= kPartStride
+    g.ticket = r.scr.ticket + 12;
+    KS_CUDA(cudaMemcpyAsync(r.b_full, b, nbytes, cudaMemcpyDefault, r.stream));
+    if (x0) KS_CUDA(cudaMemcpyAsync(r.x_loc, x0 + r.row0, (size_t)r.m * sizeof(double), cudaMemcpyDefault, r.stream));
+    else KS_CUDA(cudaMemsetAsync(r.x_loc, 0, (size_t)r.m * sizeof(double), r.stream));
+    r.launches += launch_gm_init(g, tol, maxit, hist_cap, r.stream);
+    GemvParams pres = gp(c, r, r.s_full, r.q_loc);   // r = b - A x, ||r||^2 partial
+    pres.bsub = r.b_full + r.row0;
+    pres.out2 = r.S + (int64_t)r.rank * kScalSlot + 1;
+    pres.done = &r.st->done;
+    GemvParams pw = gp(c, r, r.p_full, r.q_loc);     // w = A v_j
+    pw.done = &r.gm_state->skip;
+    Prof prof(c, r, restart + 1);
+    int64_t k = 0, cycle = 0;
+    KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+    while (true) {
+        const int slot = (int)(cycle & 1);
+        prof.begin(slot);
+        // x (gathered, full length) -> residual of the cycle start
+        if (c->P > 1) {
+            r.launches += launch_pack_x(a, r.stream);
+            allgather(c, r, r.G_v, r.L.chunk);
+            copy_chunks_to(c, r, r.G_v, r.s_full, cudaMemcpyDeviceToDevice);
+        } else {
+            KS_CUDA(cudaMemcpyAsync(r.s_full, r.x_loc, nbytes, cudaMemcpyDeviceToDevice, r.stream));
+        }
+        gemv(c, r, pres);
+        allgather(c, r, r.S, kScalSlot);
+        r.launches += launch_gm_start(g, r.stream);
+        allgather(c, r, r.G_r, r.L.chunk);
+        r.launches += launch_gm_vfull(g, r.stream);
+        for (int j = 0; j < restart && k < maxit; ++j) {
+            ++k;
+            prof.pre(slot);
+            gemv(c, r, pw);                                    // w = A v_j
+            prof.post(slot);
+            ++r.gemv_launches;
+            r.launches += launch_gm_dots(g, j, r.stream);      // CGS pass 1
+            allgather(c, r, g.hx, kMaxBasis);
+            r.launches += launch_gm_orth(g, j, 1, r.stream);   // update + pass-2 dots
+            allgather(c, r, g.hx, kMaxBasis);
+            r.launches += launch_gm_orth(g, j, 2, r.stream);   // update + ||w||^2
+            allgather(c, r, g.hx, kMaxBasis);
+            r.launches += launch_gm_step_end(g, j, k, r.stream);
+            allgather(c, r, r.G_r, r.L.chunk);
+            r.launches += launch_gm_vfull(g, r.stream);
+        }
+        r.launches += launch_gm_cycle_end(g, k, r.stream);
+        KS_CUDA(cudaMemcpyAsync(&r.h_done[slot], &r.st->done, sizeof(int), cudaMemcpyDeviceToHost, r.stream));
+        KS_CUDA(cudaEventRecord(r.ev_poll[slot], r.stream));
+        if (cycle >= 1) {
+            KS_CUDA(cudaEventSynchronize(r.ev_poll[slot ^ 1]));
+            prof.harvest(slot ^ 1);
+            if (r.h_done[slot ^ 1]) break;
+        }
+        ++cycle;
+        if (k >= maxit) break;
+    }
+    KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    prof.harvest(0);
+    prof.harvest(1);
+    r.launches += launch_cg_finish(a, r.stream);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+    return r.h_state->status;
+}
+
 // BiCG (NEXT-3): multi-kernel schedule; NCCL for P > 1 (allgather of
 // [r | <rt,r>, <r,r>], scalar allgather of <pt, A p>, reduce-scatter of A^T pt).
 int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,

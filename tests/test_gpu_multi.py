@@ -153,6 +153,21 @@ def test_multi_bicg(P):
 
 
 @needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_gmres(P):
+    """NEXT-3 GMRES(m) at P GPUs (NCCL exchanges of the CGS2 partial dots)."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    for n, kd, m in [(1024, 16, 30), (4099, 16, 8)]:
+        A, b = synth.gdd(n, kd)
+        xo, ho, ro = oracle.gmres(A, b, tol=1e-10, restart=m)
+        with ks.Context(n, ngpus=P) as ctx:
+            ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
+            x, h, r = ctx.gmres(b, tol=1e-10, restart=m)
+        bars(x, h, r, xo, ho, ro)
+
+
+@needs2
 def test_multi_edge_cases():
     n = 64
     A = synth.random_spd(n, 10.0, 1)

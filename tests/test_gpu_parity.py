@@ -6,7 +6,9 @@ seeded inputs.  Bars (BASELINE.json north_star, readings Q17-Q19 in DESIGN.md):
   * GEMV:  |y_gpu,i - y_ld,i| <= gamma_n sum_j |a_ij||x_j| (Higham sec.3.1), vs a
            long-double row sum -- pin P9.
 """
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -424,3 +426,49 @@ def test_bicg_edges_and_spd_equivalence():
         ctx.load_rows(np.array([[2.0, 1.0], [0.0, 3.0]]))
         x, h, r = ctx.bicg(np.array([3.0, 3.0]), tol=1e-12)
         assert r.converged and np.allclose(x, [1.0, 1.0], rtol=1e-12)
+
+
+# -------------------------------------------------------------- NEXT-3: GMRES(m)
+
+@pytest.mark.parametrize("n,kd,m", [(1024, 4, 30), (1024, 16, 30), (1024, 16, 5), (4096, 16, 30),
+                                    (300, 4, 63)])
+def test_gmres_parity(n, kd, m):
+    """GPU GMRES(m) (CGS2 Arnoldi) vs the oracle (MGS Arnoldi): same Krylov basis in
+    exact arithmetic; north-star bars on x, the implicit-residual history and the
+    inner-step count; restarts included (m = 5)."""
+    A, b = synth.gdd(n, kd)
+    xo, ho, ro = oracle.gmres(A, b, tol=1e-10, restart=m)
+    with ks.Context(n) as ctx:
+        ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
+        x, h, r = ctx.gmres(b, tol=1e-10, restart=m)
+        x2, h2, r2 = ctx.gmres(b, tol=1e-10, restart=m)
+    assert r.converged and r.status == ks.KS_OK
+    bars(x, h, r, xo, ho, ro)
+    assert r.true_relres <= 10 * 1e-10
+    assert r2.iterations == r.iterations and np.array_equal(x, x2) and np.array_equal(h, h2)
+
+
+def test_gmres_edges():
+    n = 200
+    A, b = synth.gdd(n, 4, seed=synth.SEED2)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        x, h, r = ctx.gmres(np.zeros(n), tol=1e-10)
+        assert r.converged and r.iterations == 0 and np.all(x == 0)
+        xo, ho, ro = oracle.gmres(A, b, tol=1e-30, restart=5, maxit=12)
+        x, h, r = ctx.gmres(b, tol=1e-30, restart=5, maxit=12)
+        assert r.status == ks.KS_EMAXIT and r.iterations == 12 and len(h) == 12
+        bars(x, h, r, xo, ho, ro, iters_tol=0)
+        x0 = np.random.default_rng(2).standard_normal(n)
+        xo, ho, ro = oracle.gmres(A, b, x0=x0, tol=1e-10, restart=7)
+        x, h, r = ctx.gmres(b, x0=x0, tol=1e-10, restart=7)
+        bars(x, h, r, xo, ho, ro)
+        with pytest.raises(ks.KsError):
+            ctx.gmres(b, restart=64)
+    for e in json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))["gmres"]:
+        A = np.array(e["A"], float)
+        with ks.Context(A.shape[0]) as ctx:
+            ctx.load_rows(A)
+            x, h, r = ctx.gmres(np.array(e["b"], float), tol=1e-12, restart=e["restart"])
+        assert r.converged and r.iterations <= e["max_iterations"], e["cite"]
+        assert np.allclose(x, e["x"], rtol=1e-12, atol=1e-15), e["cite"]

@@ -24,6 +24,8 @@ CONFIGS = {
     "C5bs": ("bicgstab", 262144, dict(kd=16), 4),
     "C3bicg": ("bicg", 65536, dict(kd=16), 30),       # NEXT-3: BiCG (A p and A^T pt)
     "C1bicg": ("bicg", 1024, dict(kd=16), 200),
+    "C3gmres": ("gmres", 65536, dict(kd=16), 30),     # NEXT-3: GMRES(30)
+    "C1gmres": ("gmres", 1024, dict(kd=16), 200),
 }
 NOMINAL = 8000e9
 
@@ -62,7 +64,7 @@ def main():
         solve(b, tol=0.0, maxit=2, hist=False)                     # warm-up
         _, _, r = solve(b, tol=0.0, maxit=K, hist=False)
         ips = K / r.seconds_loop
-        g = 1 if method == "cg" else 2           # GEMVs per iteration
+        g = 1 if method in ("cg", "gmres") else 2   # GEMVs per iteration
         m = ctx.row_range(rank)[1] - ctx.row_range(rank)[0]
         gemv_bw = 8.0 * m * n * r.gemv_launches / max(r.seconds_gemv, 1e-12)
         t_roof = g * 8.0 * n * n / world / NOMINAL + g * 8.0 * n * (world - 1) / world / 0.9e12
