@@ -92,6 +92,12 @@ def lib():
                               _D, _D, _D, _D, i64]
         L.or_gmres.restype = C.c_int
         L.or_gmres.argtypes = [i64, _D, i64, _D, _D, dbl, i64, i64, _D, _D, i64, C.POINTER(_Report)]
+        _F = C.POINTER(C.c_float)
+        flt = C.c_float
+        L.or_cg_f32.restype = C.c_int
+        L.or_cg_f32.argtypes = [i64, _F, i64, _F, flt, i64, _F, _F, i64, C.POINTER(_Report)]
+        L.or_bicgstab_f32.restype = C.c_int
+        L.or_bicgstab_f32.argtypes = [i64, _F, i64, _F, flt, i64, _F, _F, i64, C.POINTER(_Report)]
         L.or_hash.restype = u64
         L.or_hash.argtypes = [u64, u64, u64]
         L.or_gen_rows.argtypes = [C.POINTER(_Gen), i64, i64, _D, i64]
@@ -282,6 +288,31 @@ def gmres(A, b, x0=None, tol=1e-8, restart=30, maxit=None):
                    maxit, C.byref(rep))
     R = _rep(rep)
     return x, hist[:min(R.iterations, maxit)].copy(), R
+
+
+def _solve_f32(fn, A, b, tol, maxit):
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    n = A.shape[0]
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    maxit = 10 * n if maxit is None else int(maxit)
+    x = np.empty(n, dtype=np.float32)
+    hist = np.zeros(max(maxit, 1), dtype=np.float32)
+    rep = _Report()
+    F = C.POINTER(C.c_float)
+    fn(n, A.ctypes.data_as(F), n, b.ctypes.data_as(F), C.c_float(tol), maxit, x.ctypes.data_as(F),
+       hist.ctypes.data_as(F), maxit, C.byref(rep))
+    R = _rep(rep)
+    return x, hist[:min(R.iterations, maxit)].copy(), R
+
+
+def cg_f32(A, b, tol=1e-5, maxit=None):
+    """NEXT-4: CG in binary32 (A, b rounded to float by the caller or here)."""
+    return _solve_f32(lib().or_cg_f32, A, b, tol, maxit)
+
+
+def bicgstab_f32(A, b, tol=1e-5, maxit=None):
+    """NEXT-4: BiCGSTAB in binary32."""
+    return _solve_f32(lib().or_bicgstab_f32, A, b, tol, maxit)
 
 
 def ge_solve_ld(A, b) -> np.ndarray:

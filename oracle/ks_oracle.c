@@ -515,6 +515,120 @@ done:
 }
 
 /* ------------------------------------------------------------------------- */
+/* Single precision CG / BiCGSTAB -- NEXT-4.  Line-for-line the listings of   */
+/* sec.8(c).3 / .4 (and or_cg / or_bicgstab above) in binary32; x0 = 0.      */
+/* ------------------------------------------------------------------------- */
+static float dot_f(int64_t n, const float* x, const float* y) {
+    float s = 0.0f;
+    for (int64_t i = 0; i < n; ++i) s += x[i] * y[i];
+    return s;
+}
+static void gemv_f(int64_t n, const float* A, int64_t lda, const float* x, float* y) {
+    for (int64_t i = 0; i < n; ++i) {
+        const float* a = A + i * lda;
+        float s = 0.0f;
+        for (int64_t j = 0; j < n; ++j) s += a[j] * x[j];
+        y[i] = s;
+    }
+}
+
+int or_cg_f32(int64_t n, const float* A, int64_t lda, const float* b, float tol, int64_t maxit,
+              float* x, float* hist, int64_t hist_cap, or_report* rep) {
+    or_report R;
+    memset(&R, 0, sizeof R);
+    float* r = (float*)malloc((size_t)n * sizeof(float));
+    float* p = (float*)malloc((size_t)n * sizeof(float));
+    float* q = (float*)malloc((size_t)n * sizeof(float));
+    const float nb = sqrtf(dot_f(n, b, b));
+    for (int64_t i = 0; i < n; ++i) { x[i] = 0.0f; r[i] = b[i]; p[i] = b[i]; }
+    if (nb == 0.0f) { R.converged = 1; R.status = OR_OK; goto done; }
+    float rho = dot_f(n, r, r);
+    R.relres = sqrtf(rho) / nb;
+    if (R.relres <= tol) { R.converged = 1; R.status = OR_OK; goto done; }
+    R.status = OR_EMAXIT;
+    for (int64_t k = 1; k <= maxit; ++k) {
+        gemv_f(n, A, lda, p, q);
+        const float sigma = dot_f(n, p, q);
+        if (!(sigma > 0.0f)) { R.status = OR_ENOTSPD; R.iterations = k - 1; break; }
+        const float alpha = rho / sigma;
+        for (int64_t i = 0; i < n; ++i) x[i] = alpha * p[i] + x[i];
+        for (int64_t i = 0; i < n; ++i) r[i] = -alpha * q[i] + r[i];
+        const float rho1 = dot_f(n, r, r);
+        const float rel = sqrtf(rho1) / nb;
+        if (hist && k - 1 < hist_cap) hist[k - 1] = rel;
+        R.relres = rel;
+        R.iterations = k;
+        if (rel <= tol) { R.converged = 1; R.status = OR_OK; break; }
+        const float beta = rho1 / rho;
+        for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+        rho = rho1;
+    }
+    if (R.status == OR_EMAXIT) R.iterations = maxit;
+done:
+    R.matvecs = R.iterations;
+    free(r); free(p); free(q);
+    if (rep) *rep = R;
+    return R.status;
+}
+
+int or_bicgstab_f32(int64_t n, const float* A, int64_t lda, const float* b, float tol, int64_t maxit,
+                    float* x, float* hist, int64_t hist_cap, or_report* rep) {
+    or_report R;
+    memset(&R, 0, sizeof R);
+    float* r = (float*)malloc((size_t)n * sizeof(float));
+    float* rhat = (float*)malloc((size_t)n * sizeof(float));
+    float* p = (float*)calloc((size_t)n, sizeof(float));
+    float* v = (float*)calloc((size_t)n, sizeof(float));
+    float* s = (float*)malloc((size_t)n * sizeof(float));
+    float* t = (float*)malloc((size_t)n * sizeof(float));
+    const float nb = sqrtf(dot_f(n, b, b));
+    float rho_old = 1.0f, alpha = 1.0f, omega = 1.0f;
+    for (int64_t i = 0; i < n; ++i) { x[i] = 0.0f; r[i] = b[i]; rhat[i] = b[i]; }
+    if (nb == 0.0f) { R.converged = 1; R.status = OR_OK; goto done; }
+    R.relres = sqrtf(dot_f(n, r, r)) / nb;
+    if (R.relres <= tol) { R.converged = 1; R.status = OR_OK; goto done; }
+    R.status = OR_EMAXIT;
+    for (int64_t i = 1; i <= maxit; ++i) {
+        const float rho = dot_f(n, rhat, r);
+        if (rho == 0.0f || !isfinite(rho)) { R.status = OR_EBREAKDOWN; R.breakdown = 1; R.iterations = i - 1; break; }
+        const float beta = (rho / rho_old) * (alpha / omega);
+        for (int64_t j = 0; j < n; ++j) p[j] = r[j] + beta * (p[j] - omega * v[j]);
+        gemv_f(n, A, lda, p, v);
+        const float g = dot_f(n, rhat, v);
+        if (g == 0.0f || !isfinite(g)) { R.status = OR_EBREAKDOWN; R.breakdown = 1; R.iterations = i - 1; break; }
+        alpha = rho / g;
+        for (int64_t j = 0; j < n; ++j) s[j] = r[j] - alpha * v[j];
+        const float srel = sqrtf(dot_f(n, s, s)) / nb;
+        if (srel <= tol) {
+            for (int64_t j = 0; j < n; ++j) x[j] = alpha * p[j] + x[j];
+            if (hist && i - 1 < hist_cap) hist[i - 1] = srel;
+            R.relres = srel; R.half_step_exit = 1; R.converged = 1; R.status = OR_OK; R.iterations = i;
+            break;
+        }
+        gemv_f(n, A, lda, s, t);
+        const float tt = dot_f(n, t, t);
+        if (tt == 0.0f || !isfinite(tt)) { R.status = OR_EBREAKDOWN; R.breakdown = 1; R.iterations = i - 1; break; }
+        const float om = dot_f(n, t, s) / tt;
+        if (om == 0.0f || !isfinite(om)) { R.status = OR_EBREAKDOWN; R.breakdown = 1; R.iterations = i - 1; break; }
+        omega = om;
+        for (int64_t j = 0; j < n; ++j) x[j] = (x[j] + alpha * p[j]) + omega * s[j];
+        for (int64_t j = 0; j < n; ++j) r[j] = s[j] - omega * t[j];
+        const float rel = sqrtf(dot_f(n, r, r)) / nb;
+        if (hist && i - 1 < hist_cap) hist[i - 1] = rel;
+        R.relres = rel;
+        R.iterations = i;
+        if (rel <= tol) { R.converged = 1; R.status = OR_OK; break; }
+        rho_old = rho;
+    }
+    if (R.status == OR_EMAXIT) R.iterations = maxit;
+done:
+    R.matvecs = 2 * R.iterations - (R.half_step_exit ? 1 : 0);
+    free(r); free(rhat); free(p); free(v); free(s); free(t);
+    if (rep) *rep = R;
+    return R.status;
+}
+
+/* ------------------------------------------------------------------------- */
 /* Reference solutions -- SURVEY.md sec.8(c).5                               */
 /* ------------------------------------------------------------------------- */
 

@@ -76,6 +76,14 @@ int or_bicg(int64_t n, const double* A, int64_t lda, const double* b, const doub
 int or_gmres(int64_t n, const double* A, int64_t lda, const double* b, const double* x0, double tol,
              int64_t restart, int64_t maxit, double* x, double* hist, int64_t hist_cap, or_report* rep);
 
+/* --- single precision ---
+ * The same listings evaluated in IEEE binary32: float storage, float products,
+ * float sequential sums (no FMA), float scalars.  A is row-major float.        */
+int or_cg_f32(int64_t n, const float* A, int64_t lda, const float* b, float tol, int64_t maxit,
+              float* x, float* hist, int64_t hist_cap, or_report* rep);
+int or_bicgstab_f32(int64_t n, const float* A, int64_t lda, const float* b, float tol, int64_t maxit,
+                    float* x, float* hist, int64_t hist_cap, or_report* rep);
+
 /* --- reference solutions --- */
 int    or_ge_solve_ld(int64_t n, const double* A, int64_t lda, const double* b, double* x);
 void   or_spd_exact_solve_ld(int64_t n, const double* table, uint64_t seed, const double* b,
