@@ -39,7 +39,13 @@ extern "C" {
 
 typedef struct ks_ctx ks_ctx; /* opaque handle */
 
-typedef enum { KS_FLOAT64 = 0 /* KS_FLOAT32 reserved */ } ks_dtype;
+/* Storage and arithmetic precision of the device path.  KS_FLOAT32 (SURVEY.md
+ * NEXT-4; the paper's experiments are single precision): A and every
+ * device vector in binary32, half the HBM bytes per GEMV.  The ABI stays FP64
+ * (host/device double buffers, converted on the device).  FP32 supports ks_cg and
+ * ks_bicgstab with x0 = NULL on the persistent path (P == 1, or P > 1 with peer
+ * access); ks_bicg, ks_gmres, ks_matvec_t and x0 != NULL return KS_EARG.        */
+typedef enum { KS_FLOAT64 = 0, KS_FLOAT32 = 1 } ks_dtype;
 
 typedef enum {
     KS_OK = 0,         /* converged (or call succeeded)                         */

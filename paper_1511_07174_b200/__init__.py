@@ -24,6 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libks.so")
 
 KS_OK, KS_EARG, KS_EDIM, KS_ENOTSPD, KS_EMAXIT, KS_EBREAKDOWN = 0, 1, 2, 3, 4, 5
 KS_ECUDA, KS_ENCCL, KS_ENOMEM, KS_ESTATE = 6, 7, 8, 9
+DTYPES = {"f64": 0, "float64": 0, "f32": 1, "float32": 1}
 STATUS_NAMES = {0: "OK", 1: "EARG", 2: "EDIM", 3: "ENOTSPD", 4: "EMAXIT", 5: "EBREAKDOWN",
                 6: "ECUDA", 7: "ENCCL", 8: "ENOMEM", 9: "ESTATE"}
 OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 3,
@@ -152,28 +153,29 @@ def _f64(a, n: int, name: str):
 class Context:
     """Opaque solver context: A resident in HBM, row-block sharded."""
 
-    def __init__(self, n: int, ngpus: int = 1, *, _handle=None):
+    def __init__(self, n: int, ngpus: int = 1, *, dtype: str = "f64", _handle=None):
         self._h = C.c_void_p()
+        self.dtype = "f32" if DTYPES[dtype] == 1 else "f64"
         if _handle is not None:
             self._h = _handle
         else:
-            self._check(lib().ks_create(C.byref(self._h), int(n), 0, int(ngpus)))
+            self._check(lib().ks_create(C.byref(self._h), int(n), DTYPES[dtype], int(ngpus)))
         lg, nr, nn, ld = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
         self._check(lib().ks_info(self._h, C.byref(lg), C.byref(nr), C.byref(nn), C.byref(ld)))
         self.n, self.nranks, self.local_gpus, self.ld = nn.value, nr.value, lg.value, ld.value
 
     @classmethod
     def from_rank(cls, n: int, rank: int, nranks: int, nccl_comm: int | None, device: int,
-                  stream: int | None = None) -> "Context":
+                  stream: int | None = None, dtype: str = "f64") -> "Context":
         h = C.c_void_p()
-        st = lib().ks_create_rank(C.byref(h), int(n), 0, int(rank), int(nranks), nccl_comm,
+        st = lib().ks_create_rank(C.byref(h), int(n), DTYPES[dtype], int(rank), int(nranks), nccl_comm,
                                   int(device), stream)
         if st != KS_OK:
             raise KsError(st, lib().ks_last_error(None).decode())
-        return cls(n, _handle=h)
+        return cls(n, dtype=dtype, _handle=h)
 
     @classmethod
-    def from_process_group(cls, n: int, group=None, stream=None) -> "Context":
+    def from_process_group(cls, n: int, group=None, stream=None, dtype: str = "f64") -> "Context":
         """One rank per process (torchrun): borrows torch's NCCL communicator and
         the current CUDA stream.  torch is only the plumbing here."""
         import torch
@@ -188,7 +190,7 @@ class Context:
             dist.all_reduce(t, group=pg)           # makes sure the communicator exists
             torch.cuda.synchronize()
             comm = pg._get_backend(torch.device("cuda"))._comm_ptr()
-        return cls.from_rank(n, rank, world, comm, dev, s.cuda_stream)
+        return cls.from_rank(n, rank, world, comm, dev, s.cuda_stream, dtype=dtype)
 
     # -- plumbing ---------------------------------------------------------------
     def _check(self, st: int, ok=(KS_OK,)):

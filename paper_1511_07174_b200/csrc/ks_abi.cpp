@@ -40,7 +40,8 @@ ks_status guarded(ks_ctx* c, F&& f) {
 void make_layout(ks_ctx* c) {
     const int64_t n = c->n;
     const int P = c->P;
-    c->ld = (n + ks::kColAlign - 1) / ks::kColAlign * ks::kColAlign;
+    const int64_t align = (int64_t)(4096 / c->esz);   // 4 KiB rows: 512 doubles / 1024 floats
+    c->ld = (n + align - 1) / align * align;
     ks::Layout L{};
     L.P = P;
     L.n = n;
@@ -70,7 +71,7 @@ extern "C" {
 ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus) {
     if (!out) return fail(nullptr, KS_EARG, "out is NULL");
     *out = nullptr;
-    if (dtype != KS_FLOAT64) return fail(nullptr, KS_EARG, "only KS_FLOAT64 is supported");
+    if (dtype != KS_FLOAT64 && dtype != KS_FLOAT32) return fail(nullptr, KS_EARG, "dtype must be KS_FLOAT64 or KS_FLOAT32");
     if (n < 1) return fail(nullptr, KS_EDIM, "n must be >= 1");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
@@ -80,6 +81,8 @@ ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus) {
     ks_ctx* c = new ks_ctx();
     c->n = n;
     c->P = ngpus;
+    c->dtype = dtype;
+    c->esz = dtype == KS_FLOAT32 ? sizeof(float) : sizeof(double);
     c->ranks.resize((size_t)ngpus);
     for (int g = 0; g < ngpus; ++g) { c->ranks[g].rank = g; c->ranks[g].dev = g; }
     make_layout(c);
@@ -108,7 +111,7 @@ ks_status ks_create_rank(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t rank, 
                          void* nccl_comm, int32_t device, void* stream) {
     if (!out) return fail(nullptr, KS_EARG, "out is NULL");
     *out = nullptr;
-    if (dtype != KS_FLOAT64) return fail(nullptr, KS_EARG, "only KS_FLOAT64 is supported");
+    if (dtype != KS_FLOAT64 && dtype != KS_FLOAT32) return fail(nullptr, KS_EARG, "dtype must be KS_FLOAT64 or KS_FLOAT32");
     if (n < 1) return fail(nullptr, KS_EDIM, "n must be >= 1");
     if (nranks < 1 || nranks > ks::kMaxRanks || rank < 0 || rank >= nranks)
         return fail(nullptr, KS_EARG, "need 0 <= rank < nranks <= 16");
@@ -120,6 +123,8 @@ ks_status ks_create_rank(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t rank, 
     ks_ctx* c = new ks_ctx();
     c->n = n;
     c->P = nranks;
+    c->dtype = dtype;
+    c->esz = dtype == KS_FLOAT32 ? sizeof(float) : sizeof(double);
     c->multiprocess = true;
     c->ranks.resize(1);
     Rank& r = c->ranks[0];
@@ -178,6 +183,26 @@ ks_status ks_load_rows(ks_ctx* c, int64_t row_begin, int64_t nrows, const double
             const int64_t b = std::max(row_begin, r.row0);
             const int64_t e = std::min(row_begin + nrows, r.row0 + r.m);
             if (e <= b) return;
+            if (c->dtype == KS_FLOAT32) {                 // FP64 rows -> device staging -> FP32
+                const int64_t chunk = std::max<int64_t>(1, (int64_t)(8 << 20) / c->n);
+                double* stage = nullptr;
+                KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&stage), (size_t)std::min(chunk, e - b) * c->n * sizeof(double)));
+                for (int64_t i = b; i < e; i += chunk) {
+                    const int64_t cnt = std::min(chunk, e - i);
+                    KS_CUDA(cudaMemcpy2DAsync(stage, (size_t)c->n * sizeof(double), A + (i - row_begin) * lda,
+                                              (size_t)lda * sizeof(double), (size_t)c->n * sizeof(double),
+                                              (size_t)cnt, cudaMemcpyDefault, r.stream));
+                    ks::launch_rows_d2f(stage, c->n, reinterpret_cast<float*>(r.A) + (i - r.row0) * c->ld, c->ld,
+                                        cnt, c->n, r.stream);
+                }
+                KS_CUDA(cudaStreamSynchronize(r.stream));
+                KS_CUDA(cudaFree(stage));
+                for (int64_t i = b; i < e; ++i) {
+                    auto& f = r.loaded[(size_t)(i - r.row0)];
+                    if (!f) { f = 1; ++r.loaded_count; }
+                }
+                return;
+            }
             KS_CUDA(cudaMemcpy2DAsync(r.A + (b - r.row0) * c->ld, (size_t)c->ld * sizeof(double),
                                       A + (b - row_begin) * lda, (size_t)lda * sizeof(double),
                                       (size_t)c->n * sizeof(double), (size_t)(e - b), cudaMemcpyDefault,
@@ -204,17 +229,26 @@ ks_status ks_generate(ks_ctx* c, const ks_gen_spec* spec, double* b_out) {
                 KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&tab), (size_t)c->n * sizeof(double)));
                 KS_CUDA(cudaMemcpyAsync(tab, spec->spd_table, (size_t)c->n * sizeof(double),
                                         cudaMemcpyDefault, r.stream));
-                ks::launch_gen_spd(r.A, c->ld, r.row0, r.m, c->n, spec->seed, tab, r.stream);
+                if (c->dtype == KS_FLOAT32)
+                    ks::launch_gen_spd_f32(reinterpret_cast<float*>(r.A), c->ld, r.row0, r.m, c->n, spec->seed, tab, r.stream);
+                else
+                    ks::launch_gen_spd(r.A, c->ld, r.row0, r.m, c->n, spec->seed, tab, r.stream);
                 KS_CUDA(cudaStreamSynchronize(r.stream));
                 KS_CUDA(cudaFree(tab));
             } else {
-                ks::launch_gen_dd(r.A, c->ld, r.row0, r.m, c->n, spec->seed, spec->kd, r.stream);
+                if (c->dtype == KS_FLOAT32)
+                    ks::launch_gen_dd_f32(reinterpret_cast<float*>(r.A), c->ld, r.row0, r.m, c->n, spec->seed, spec->kd, r.stream);
+                else
+                    ks::launch_gen_dd(r.A, c->ld, r.row0, r.m, c->n, spec->seed, spec->kd, r.stream);
             }
             KS_CUDA(cudaGetLastError());
             if (b_out && c->writes_host(r)) {
-                ks::launch_gen_rhs(r.b_full, c->n, spec->seed, r.stream);
-                KS_CUDA(cudaMemcpyAsync(b_out, r.b_full, (size_t)c->n * sizeof(double),
-                                        cudaMemcpyDefault, r.stream));
+                double* bd = nullptr;                     // b is FP64 at the ABI
+                KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&bd), (size_t)c->n * sizeof(double)));
+                ks::launch_gen_rhs(bd, c->n, spec->seed, r.stream);
+                KS_CUDA(cudaMemcpyAsync(b_out, bd, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+                KS_CUDA(cudaStreamSynchronize(r.stream));
+                KS_CUDA(cudaFree(bd));
             }
             KS_CUDA(cudaStreamSynchronize(r.stream));
             std::fill(r.loaded.begin(), r.loaded.end(), 1);
@@ -229,6 +263,26 @@ ks_status ks_matvec(ks_ctx* c, const double* x, double* y) {
     return guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
             if (r.loaded_count < r.m) throw KsError(KS_ESTATE, "matrix not fully loaded");
+            if (c->dtype == KS_FLOAT32) {
+                double* tmp = nullptr;
+                KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&tmp), (size_t)c->n * sizeof(double)));
+                KS_CUDA(cudaMemcpyAsync(tmp, x, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+                ks::launch_d2f(tmp, reinterpret_cast<float*>(r.s_full), c->n, r.stream);
+                ks::GemvParamsT<float> p{};
+                p.A = reinterpret_cast<const float*>(r.A); p.lda = c->ld; p.m = r.m; p.ncols = c->ld;
+                p.x = reinterpret_cast<const float*>(r.s_full);
+                p.y = reinterpret_cast<float*>(r.G_v) + (int64_t)r.rank * r.L.chunk;
+                ks::launch_gemv_f32(p, r.scr, 1, r.stream);
+                ks::allgather(c, r, r.G_v, r.L.chunk);
+                ks::copy_chunks_to(c, r, r.G_v, r.p_full, cudaMemcpyDeviceToDevice);
+                ks::launch_f2d(reinterpret_cast<const float*>(r.p_full), tmp, c->n, r.stream);
+                if (c->writes_host(r))
+                    KS_CUDA(cudaMemcpyAsync(y, tmp, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+                KS_CUDA(cudaStreamSynchronize(r.stream));
+                KS_CUDA(cudaGetLastError());
+                KS_CUDA(cudaFree(tmp));
+                return;
+            }
             KS_CUDA(cudaMemcpyAsync(r.s_full, x, (size_t)c->n * sizeof(double), cudaMemcpyDefault,
                                     r.stream));
             ks::GemvParams p{};
@@ -250,6 +304,22 @@ ks_status ks_time_matvec(ks_ctx* c, int32_t reps, double* seconds) {
     std::vector<double> per(c->ranks.size(), 0.0);
     ks_status st = guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
+            if (c->dtype == KS_FLOAT32) {
+                ks::GemvParamsT<float> p{};
+                p.A = reinterpret_cast<const float*>(r.A); p.lda = c->ld; p.m = r.m; p.ncols = c->ld;
+                p.x = reinterpret_cast<const float*>(r.p_full);
+                p.y = reinterpret_cast<float*>(r.q_loc);
+                ks::launch_gemv_f32(p, r.scr, 1, r.stream);
+                KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+                for (int q = 0; q < reps; ++q) ks::launch_gemv_f32(p, r.scr, 1, r.stream);
+                KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+                KS_CUDA(cudaStreamSynchronize(r.stream));
+                KS_CUDA(cudaGetLastError());
+                float ms = 0.f;
+                KS_CUDA(cudaEventElapsedTime(&ms, r.ev_t0, r.ev_t1));
+                per[(size_t)(&r - c->ranks.data())] = ms * 1e-3 / reps;
+                return;
+            }
             ks::GemvParams p{};
             p.A = r.A; p.lda = c->ld; p.m = r.m; p.ncols = c->ld;
             p.x = r.p_full;
@@ -285,11 +355,21 @@ static ks_status solve(ks_ctx* c, int method, const double* b, const double* x0,
     if (maxit < 0) return fail(c, KS_EARG, "maxit must be >= 0");
     if (hist_cap < 0 || (hist_cap > 0 && !hist)) return fail(c, KS_EARG, "bad hist/hist_cap");
     if (!hist) hist_cap = 0;
+    if (c->dtype == KS_FLOAT32) {
+        if (method == 2) return fail(c, KS_EARG, "BiCG is FP64-only");
+        if (x0) return fail(c, KS_EARG, "FP32 path: x0 must be NULL (zero start)");
+        if (!(c->P == 1 || c->fused())) return fail(c, KS_EARG, "FP32 path needs P == 1 or peer access");
+    }
     std::vector<ks_report> reps(c->ranks.size());
     std::vector<int64_t> stat(c->ranks.size(), 0);
     ks_status st = guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
             const size_t i = (size_t)(&r - c->ranks.data());
+            if (c->dtype == KS_FLOAT32) {
+                stat[i] = ks::run_f32(c, r, method == 1, b, tol, maxit, x, hist, hist_cap, &reps[i]);
+                KS_CUDA(cudaGetLastError());
+                return;
+            }
             stat[i] = method == 1 ? ks::run_bicgstab(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i])
                     : method == 2 ? ks::run_bicg(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i])
                                   : ks::run_cg(c, r, b, x0, tol, maxit, x, hist, hist_cap, &reps[i]);
@@ -331,6 +411,7 @@ ks_status ks_bicg(ks_ctx* c, const double* b, const double* x0, double tol, int6
 ks_status ks_gmres(ks_ctx* c, const double* b, const double* x0, double tol, int32_t restart,
                    int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep) {
     if (!c) return fail(nullptr, KS_EARG, "ctx is NULL");
+    if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "GMRES is FP64-only");
     if (!b || !x) return fail(c, KS_EARG, "b and x are required");
     if (!(tol >= 0.0)) return fail(c, KS_EARG, "tol must be >= 0");
     if (maxit < 0) return fail(c, KS_EARG, "maxit must be >= 0");
@@ -362,6 +443,7 @@ ks_status ks_gmres(ks_ctx* c, const double* b, const double* x0, double tol, int
 
 ks_status ks_matvec_t(ks_ctx* c, const double* x, double* y) {
     if (!c || !x || !y) return fail(c, KS_EARG, "NULL argument");
+    if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "ks_matvec_t is FP64-only");
     return guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
             if (r.loaded_count < r.m) throw KsError(KS_ESTATE, "matrix not fully loaded");

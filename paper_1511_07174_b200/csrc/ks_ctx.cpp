@@ -51,6 +51,14 @@ static void dmalloc(T** p, size_t count) {
     KS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
     KS_CUDA(cudaMemset(*p, 0, std::max<size_t>(count, 1) * sizeof(T)));
 }
+// element buffers of the context's dtype (double* members hold floats in FP32 contexts)
+static void emalloc(double** p, size_t count, size_t esz) {
+    const size_t bytes = std::max<size_t>(count, 1) * esz;
+    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+    KS_CUDA(cudaMemset(*p, 0, bytes));
+}
+template <class T>
+static T* as(double* p) { return reinterpret_cast<T*>(p); }
 
 void rank_alloc(ks_ctx* c, Rank& r) {
     KS_CUDA(cudaSetDevice(r.dev));
@@ -61,28 +69,33 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     }
     const int64_t ld = c->ld;
     const size_t P = (size_t)c->P;
-    dmalloc(&r.A, (size_t)r.m * (size_t)ld);     // zero padding columns [n, ld)
-    dmalloc(&r.b_full, ld);
-    dmalloc(&r.x_loc, r.m + 64);
-    dmalloc(&r.p_full, ld);
-    dmalloc(&r.s_full, ld);
-    dmalloc(&r.v_full, ld);
-    dmalloc(&r.q_loc, r.m + 64);
-    dmalloc(&r.rhat_loc, r.m + 64);
-    dmalloc(&r.pt_loc, r.m + 64);
-    dmalloc(&r.U, P * (size_t)r.L.chunk);
-    dmalloc(&r.qt_loc, (size_t)r.L.chunk);
+    const size_t e = c->esz;
+    emalloc(&r.A, (size_t)r.m * (size_t)ld, e);     // zero padding columns [n, ld)
+    emalloc(&r.b_full, ld, e);
+    emalloc(&r.x_loc, r.m + 64, e);
+    emalloc(&r.p_full, ld, e);
+    emalloc(&r.s_full, ld, e);
+    emalloc(&r.v_full, ld, e);
+    emalloc(&r.q_loc, r.m + 64, e);
+    emalloc(&r.rhat_loc, r.m + 64, e);
+    emalloc(&r.pt_loc, r.m + 64, e);
+    emalloc(&r.U, P * (size_t)r.L.chunk, e);
+    emalloc(&r.qt_loc, (size_t)r.L.chunk, e);
     {
-        const size_t g = 2 * P * (size_t)r.L.chunk;
-        const size_t sdoubles = (2 * P * kScalSlot + 63) / 64 * 64;
-        const size_t fwords = (kNumPhases * kMaxRanks + 63) / 64 * 64;
-        const size_t total = 2 * g + sdoubles + fwords;
-        dmalloc(&r.xbuf, total);
-        r.xbuf_bytes = total * sizeof(double);
-        r.G_r = r.xbuf;
-        r.G_v = r.xbuf + g;
-        r.S = r.xbuf + 2 * g;
-        r.flags = reinterpret_cast<unsigned long long*>(r.xbuf + 2 * g + sdoubles);
+        // exchange buffers (one allocation -> one CUDA IPC handle), byte layout
+        const size_t g = 2 * P * (size_t)r.L.chunk * e;
+        const size_t sb = (2 * P * kScalSlot * e + 511) / 512 * 512;
+        const size_t fb = (kNumPhases * kMaxRanks * sizeof(unsigned long long) + 511) / 512 * 512;
+        const size_t total = 2 * g + sb + fb;
+        char* base = nullptr;
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total));
+        KS_CUDA(cudaMemset(base, 0, total));
+        r.xbuf = reinterpret_cast<double*>(base);
+        r.xbuf_bytes = total;
+        r.G_r = reinterpret_cast<double*>(base);
+        r.G_v = reinterpret_cast<double*>(base + g);
+        r.S = reinterpret_cast<double*>(base + 2 * g);
+        r.flags = reinterpret_cast<unsigned long long*>(base + 2 * g + sb);
         for (int q = 0; q < kMaxRanks; ++q) {
             r.pp.G_r[q] = r.pp.G_v[q] = r.pp.S[q] = nullptr;
             r.pp.flags[q] = nullptr;
@@ -141,17 +154,55 @@ void rank_free(Rank& r) {
 // In-place allgather of one chunk per rank (count_per_rank doubles at G + rank*chunk).
 void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank) {
     if (c->P == 1) return;
-    KS_NCCL(ncclAllGather(G + (int64_t)r.rank * count_per_rank, G, (size_t)count_per_rank,
-                          ncclDouble, r.comm, r.stream));
+    char* base = reinterpret_cast<char*>(G);
+    KS_NCCL(ncclAllGather(base + (size_t)r.rank * (size_t)count_per_rank * c->esz, base,
+                          (size_t)count_per_rank, c->dtype == KS_FLOAT32 ? ncclFloat : ncclDouble,
+                          r.comm, r.stream));
 }
 
 // Copies the P row slices held in chunk layout to a contiguous n-vector.
+VecArgsT<float> Rank::vargs_f32(bool fused) const {
+    VecArgsT<float> a;
+    a.L = L;
+    a.st = st;
+    a.hist = hist;
+    a.b_full = as<float>(b_full);
+    a.x_loc = as<float>(x_loc);
+    a.p_full = as<float>(p_full);
+    a.s_full = as<float>(s_full);
+    a.v_full = as<float>(v_full);
+    a.q_loc = as<float>(q_loc);
+    a.rhat_loc = as<float>(rhat_loc);
+    a.pt_loc = as<float>(pt_loc);
+    a.qt_loc = as<float>(qt_loc);
+    a.G_r = as<float>(G_r);
+    a.G_v = as<float>(G_v);
+    a.S = as<float>(S);
+    a.scr = scr;
+    a.num_sms = num_sms;
+    a.gpar = fused ? (int64_t)L.P * L.chunk : 0;
+    a.spar = fused ? (int64_t)L.P * kScalSlot : 0;
+    a.peer = fused ? 1 : 0;
+    for (int g = 0; g < kMaxRanks; ++g) {
+        a.pp.G_r[g] = as<float>(pp.G_r[g]);
+        a.pp.G_v[g] = as<float>(pp.G_v[g]);
+        a.pp.S[g] = as<float>(pp.S[g]);
+        a.pp.flags[g] = pp.flags[g];
+    }
+    a.flags = flags;
+    return a;
+}
+
+// Elements are of the context's dtype (G and dst both).
 void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cudaMemcpyKind kind) {
+    const size_t e = c->esz;
+    const char* src = reinterpret_cast<const char*>(G);
+    char* out = reinterpret_cast<char*>(dst);
     for (int g = 0; g < c->P; ++g) {
-        const int64_t b = r.L.row0[g], e = r.L.row0[g + 1];
-        if (e > b)
-            KS_CUDA(cudaMemcpyAsync(dst + b, G + (int64_t)g * r.L.chunk, (size_t)(e - b) * sizeof(double),
-                                    kind, r.stream));
+        const int64_t b = r.L.row0[g], en = r.L.row0[g + 1];
+        if (en > b)
+            KS_CUDA(cudaMemcpyAsync(out + (size_t)b * e, src + (size_t)g * (size_t)r.L.chunk * e,
+                                    (size_t)(en - b) * e, kind, r.stream));
     }
 }
 
@@ -163,9 +214,10 @@ void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cuda
 // keeps the NCCL collectives (opt.fused_comm is then ineffective).
 void setup_peers(ks_ctx* c) {
     if (c->P == 1) return;
-    const size_t offGv = (size_t)(c->ranks[0].G_v - c->ranks[0].xbuf);
-    const size_t offS = (size_t)(c->ranks[0].S - c->ranks[0].xbuf);
-    const size_t offF = (size_t)(reinterpret_cast<double*>(c->ranks[0].flags) - c->ranks[0].xbuf);
+    auto boff = [&](const void* p) {
+        return (size_t)(static_cast<const char*>(p) - reinterpret_cast<const char*>(c->ranks[0].xbuf));
+    };
+    const size_t offGv = boff(c->ranks[0].G_v), offS = boff(c->ranks[0].S), offF = boff(c->ranks[0].flags);
     if (!c->multiprocess) {
         bool ok = true;
         for (auto& a : c->ranks)
@@ -210,10 +262,10 @@ void setup_peers(ks_ctx* c) {
         cudaError_t e = cudaIpcOpenMemHandle(&base, all[(size_t)g], cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) { cudaGetLastError(); ok = false; continue; }
         r.ipc_opened.push_back(base);
-        double* d = static_cast<double*>(base);
-        r.pp.G_r[g] = d;
-        r.pp.G_v[g] = d + offGv;
-        r.pp.S[g] = d + offS;
+        char* d = static_cast<char*>(base);
+        r.pp.G_r[g] = reinterpret_cast<double*>(d);
+        r.pp.G_v[g] = reinterpret_cast<double*>(d + offGv);
+        r.pp.S[g] = reinterpret_cast<double*>(d + offS);
         r.pp.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
     }
     // every rank must agree, or none uses the fused path (collectives must match)

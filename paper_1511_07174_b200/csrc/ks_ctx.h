@@ -100,6 +100,7 @@ struct Rank {
     double gemv_seconds = 0.0;
 
     VecArgs vargs(bool fused) const;
+    VecArgsT<float> vargs_f32(bool fused) const;   // FP32 contexts: buffers hold floats
 };
 
 struct Options {
@@ -118,6 +119,8 @@ struct Options {
 
 struct ks_ctx {
     int64_t n = 0, ld = 0;
+    ks_dtype dtype = KS_FLOAT64;
+    size_t esz = sizeof(double);   // bytes per element of A and the device vectors
     int P = 1;               // global number of ranks
     bool multiprocess = false;
     std::vector<ks::Rank> ranks;   // local ranks (1 in multi-process mode)
@@ -143,8 +146,10 @@ namespace ks {
 void rank_alloc(ks_ctx* c, Rank& r);
 void rank_free(Rank& r);
 void setup_peers(ks_ctx* c);   // peer access / CUDA IPC of the exchange buffers
-void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank);
+void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank);   // dtype-aware
 void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cudaMemcpyKind kind);
+int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, int64_t maxit,
+                double* x, double* hist, int64_t hist_cap, ks_report* rep);
 int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
                double* x, double* hist, int64_t hist_cap, ks_report* rep);
 int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,

@@ -9,7 +9,8 @@
 
 namespace ks {
 
-__device__ __forceinline__ double warp_sum(double v) {
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
     // xor butterfly: a+b == b+a in IEEE, so all lanes end with the same bits.
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -19,8 +20,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Block sum of K values per thread; result valid in every thread.  `red` must
 // hold K * (NT/32) doubles.  Fixed tree: warp butterfly, then warp sums added in
 // warp order by a butterfly over the first NT/32 lanes of every warp.
-template <int NT, int K>
-__device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
+template <int NT, int K, class T>
+__device__ __forceinline__ void block_sum(T (&v)[K], T* red) {
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -33,7 +34,7 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        double t = lane < NW ? red[k * NW + lane] : 0.0;
+        T t = lane < NW ? red[k * NW + lane] : T(0);
         v[k] = warp_sum(t);
     }
 }
@@ -42,9 +43,8 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
 // Returns true in the last-arriving block, whose threads then hold the grid
 // totals in v (blocks summed in blockIdx order by a fixed tree).  The ticket is
 // reset by the last block so the slot can be reused by the next launch.
-template <int NT, int K>
-__device__ __forceinline__ bool grid_sum(double (&v)[K], double* part, unsigned* ticket,
-                                         double* red) {
+template <int NT, int K, class T>
+__device__ __forceinline__ bool grid_sum(T (&v)[K], T* part, unsigned* ticket, T* red) {
     __shared__ int s_last;
     const int nb = gridDim.x;
     if (threadIdx.x == 0) {
@@ -59,7 +59,7 @@ __device__ __forceinline__ bool grid_sum(double (&v)[K], double* part, unsigned*
     __threadfence();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        double acc = 0.0;
+        T acc = T(0);
         for (int b = threadIdx.x; b < nb; b += NT) acc += __ldcg(part + (int64_t)b * K + k);
         v[k] = acc;
     }

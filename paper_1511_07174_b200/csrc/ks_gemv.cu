@@ -44,11 +44,11 @@ constexpr int kNW = kNT / 32;
 
 // Tile epilogue shared by both variants.  `acc` holds the full-row sums (valid in
 // every thread).  Returns nothing; handles split-K combine, y store, dots.
-template <int R>
-__device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)[R], int64_t tile,
-                                              int s, int S, int64_t tiles, double* qpart,
-                                              unsigned* tile_ticket, double* dpart,
-                                              unsigned* ticket, double* red) {
+template <int R, class T>
+__device__ __forceinline__ void gemv_epilogue(const GemvParamsT<T>& p, T (&acc)[R], int64_t tile,
+                                              int s, int S, int64_t tiles, T* qpart,
+                                              unsigned* tile_ticket, T* dpart,
+                                              unsigned* ticket, T* red) {
     __shared__ int s_last;
     const int64_t r0 = tile * R;
     const int nvalid = (int)min((int64_t)R, p.m - r0);
@@ -66,7 +66,7 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
         __threadfence();
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            double v = 0.0;
+            T v = T(0);
             for (int q = 0; q < S; ++q) v += __ldcg(qpart + (tile * S + q) * R + r);
             acc[r] = v;
         }
@@ -77,11 +77,11 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
     if (p.pub_P) k = p.koff + (p.kdev ? *p.kdev : 0);
     const int64_t par = k & 1;
     if (threadIdx.x == 0) {
-        double d1 = 0.0, d2 = 0.0;
+        T d1 = T(0), d2 = T(0);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (r < nvalid) {
-                double yv = acc[r];
+                T yv = acc[r];
                 if (p.bsub) yv = p.bsub[r0 + r] - yv;
                 if (p.pub_P && p.y_peer[0]) {
                     for (int g = 0; g < p.pub_P; ++g) p.y_peer[g][par * p.ypar + r0 + r] = yv;
@@ -107,7 +107,7 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    double v[2] = {0.0, 0.0};
+    T v[2] = {T(0), T(0)};
     for (int64_t t = threadIdx.x; t < tiles; t += kNT) {
         v[0] += __ldcg(dpart + t * 2 + 0);
         v[1] += __ldcg(dpart + t * 2 + 1);
@@ -128,21 +128,21 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, double (&acc)
     }
 }
 
-template <int R, int U>
-__global__ void __launch_bounds__(kNT) k1_gemv_ldg(GemvParams p, int S, int64_t tiles,
-                                                   double* qpart, unsigned* tile_ticket,
-                                                   double* dpart, unsigned* ticket) {
-    __shared__ double red[R * kNW];
+template <int R, int U, class T>
+__global__ void __launch_bounds__(kNT) k1_gemv_ldg(GemvParamsT<T> p, int S, int64_t tiles,
+                                                   T* qpart, unsigned* tile_ticket,
+                                                   T* dpart, unsigned* ticket) {
+    __shared__ T red[R * kNW];
     if (p.done && *(volatile const int*)p.done) return;
     const int64_t unit = blockIdx.x;
     const int64_t tile = unit / S;
     const int s = (int)(unit % S);
     const int64_t r0 = tile * R;
     const int nvalid = (int)min((int64_t)R, p.m - r0);
-    const int64_t ncb = p.ncols / (2 * kNT);
+    const int64_t ncb = p.ncols / (Vec16<T>::W * kNT);
     const int64_t cb0 = s * ncb / S, cb1 = (s + 1) * ncb / S;
 
-    double acc[R];
+    T acc[R];
     stream_rows<R, U, kNT>(p.A, p.lda, r0, nvalid, p.x, cb0, cb1, acc);
     block_sum<kNT, R>(acc, red);
     gemv_epilogue<R>(p, acc, tile, s, S, tiles, qpart, tile_ticket, dpart, ticket, red);
@@ -290,8 +290,8 @@ int launch_rows(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
                                                ticket);
     } else {
         constexpr int U = (R >= 16) ? 1 : (R >= 8 ? 2 : 4);
-        k1_gemv_ldg<R, U><<<(unsigned)grid, kNT, 0, st>>>(p, c.splits, tiles, s.qpart,
-                                                          s.tile_ticket, dpart, ticket);
+        k1_gemv_ldg<R, U, double><<<(unsigned)grid, kNT, 0, st>>>(p, c.splits, tiles, s.qpart,
+                                                                  s.tile_ticket, dpart, ticket);
     }
     return 1;
 }
@@ -328,6 +328,19 @@ int launch_gemv(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
     }
 }
 
+
+// NEXT-4: K1 in FP32 (R = 4 rows x 1024-column blocks of float4 loads; no split-K:
+// the FP32 path serves the configs whose row count fills the GPU).
+int launch_gemv_f32(const GemvParamsT<float>& p, const Scratch& s, int ticket_id, cudaStream_t st) {
+    if (p.m <= 0) return 0;
+    constexpr int R = 4;
+    const int64_t tiles = (p.m + R - 1) / R;
+    float* dpart = reinterpret_cast<float*>(s.part + (int64_t)ticket_id * kPartStride);
+    if (tiles * 2 > 2 * kPartStride) dpart = reinterpret_cast<float*>(s.qpart);
+    k1_gemv_ldg<R, 4, float><<<(unsigned)tiles, kNT, 0, st>>>(p, 1, tiles, reinterpret_cast<float*>(s.qpart),
+                                                              s.tile_ticket, dpart, s.ticket + ticket_id);
+    return 1;
+}
 
 // ============================================================================
 // K1T -- transposed GEMV u = A_loc^T x_loc (length n) for BiCG (

@@ -25,12 +25,14 @@ constexpr int kNumPhases = 3;
 
 // Peer (NVLink, unified-address) pointers to every rank's exchange buffers,
 // parity-0 bases; rank g's own entries point at its local memory.
-struct PeerPtrs {
-    double* G_r[kMaxRanks];
-    double* G_v[kMaxRanks];
-    double* S[kMaxRanks];
+template <class T>
+struct PeerPtrsT {
+    T* G_r[kMaxRanks];
+    T* G_v[kMaxRanks];
+    T* S[kMaxRanks];
     unsigned long long* flags[kMaxRanks];   // [kNumPhases][kMaxRanks] epochs
 };
+using PeerPtrs = PeerPtrsT<double>;
 
 // Row partition + gather layout, passed by value to kernels.
 struct Layout {
@@ -69,28 +71,30 @@ struct Scratch {
 };
 constexpr int64_t kPartStride = 4096 * 2;
 
-struct GemvParams {
-    const double* A; int64_t lda; int64_t m; int64_t ncols;
-    const double* x;       // padded full input vector (ncols)
-    double* y;             // m outputs
-    const double* bsub;    // nullable: y = bsub - A x
-    const double* w1;      // nullable: *out1 = <w1, y>
-    double* out1;
-    double* out2;          // nullable: *out2 = <y, y>
+template <class T>
+struct GemvParamsT {
+    const T* A; int64_t lda; int64_t m; int64_t ncols;
+    const T* x;            // padded full input vector (ncols)
+    T* y;                  // m outputs
+    const T* bsub;         // nullable: y = bsub - A x
+    const T* w1;           // nullable: *out1 = <w1, y>
+    T* out1;
+    T* out2;               // nullable: *out2 = <y, y>
     const int* done;       // nullable: skip when *done != 0
     // Fused publish (peer mode): y rows and/or dot partials stored straight into
     // every rank's exchange buffer, then the phase flag released with the epoch.
     int pub_P = 0, pub_rank = 0;           // 0: no peer publishing
-    double* y_peer[kMaxRanks];             // parity-0 address of row 0 of this rank's slice at rank g
+    T* y_peer[kMaxRanks];                  // parity-0 address of row 0 of this rank's slice at rank g
     int64_t ypar = 0;                      // parity stride of y_peer
     int64_t y_par = 0;                     // parity stride applied to the local y
-    double* d_peer[kMaxRanks];             // parity-0 address of this rank's dot slots at rank g
+    T* d_peer[kMaxRanks];                  // parity-0 address of this rank's dot slots at rank g
     int64_t dpar = 0;
     unsigned long long* f_peer[kMaxRanks]; // flag [phase][this rank] at rank g
     const unsigned long long* ebase = nullptr;
     const long long* kdev = nullptr;       // epoch = *ebase + koff + (kdev ? *kdev : 0)
     long long koff = 0;
 };
+using GemvParams = GemvParamsT<double>;
 
 struct GemvConfig {
     int variant;   // 1 = LDG stream, 2 = TMA bulk ring
@@ -119,30 +123,33 @@ int launch_gen_rhs(double* b, int64_t n, uint64_t seed, cudaStream_t st);
 
 // Vector/control kernels (ks_vec.cu).  `G_r`, `G_v` are gather buffers in chunk
 // layout; `S` is the scalar gather buffer (kScalSlot doubles per rank).
-struct VecArgs {
+template <class T>
+struct VecArgsT {
     Layout L;
     DevState* st;
-    double* hist;
-    const double* b_full;  // ld
-    double* x_loc;         // m
-    double* p_full;        // ld
-    double* s_full;        // ld
-    double* v_full;        // ld (BiCGSTAB: local copy of the gathered v)
-    double* q_loc;         // m (CG q / BiCGSTAB t)
-    double* rhat_loc;      // m (BiCGSTAB rhat; BiCG's shadow residual rt)
-    double* pt_loc;        // m (BiCG shadow direction pt)
-    const double* qt_loc;  // m (BiCG qt = (A^T pt) rows of this rank)
-    double* G_r;           // P * chunk
-    double* G_v;           // P * chunk
-    double* S;             // P * kScalSlot
+    double* hist;          // always FP64 (relres values)
+    const T* b_full;       // ld
+    T* x_loc;              // m
+    T* p_full;             // ld
+    T* s_full;             // ld
+    T* v_full;             // ld (BiCGSTAB: local copy of the gathered v)
+    T* q_loc;              // m (CG q / BiCGSTAB t)
+    T* rhat_loc;           // m (BiCGSTAB rhat; BiCG's shadow residual rt)
+    T* pt_loc;             // m (BiCG shadow direction pt)
+    const T* qt_loc;       // m (BiCG qt = (A^T pt) rows of this rank)
+    T* G_r;                // P * chunk
+    T* G_v;                // P * chunk
+    T* S;                  // P * kScalSlot
     Scratch scr;
     int num_sms;
     // iteration-parity double buffering of G_r / G_v / S (0 in NCCL mode)
     int64_t gpar, spar;
     int peer;              // 1: fused NVLink peer-store collectives
-    PeerPtrs pp;
+    PeerPtrsT<T> pp;
     unsigned long long* flags;   // own [kNumPhases][kMaxRanks]
+    T* b_full_mut() const { return const_cast<T*>(b_full); }
 };
+using VecArgs = VecArgsT<double>;
 
 int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaStream_t st);
 int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
@@ -197,9 +204,30 @@ int launch_bicg_init(const VecArgs& a, double tol, long long maxit, long long hi
 int launch_bicg_update(const VecArgs& a, long long k, cudaStream_t st);
 int launch_bicg_direction(const VecArgs& a, long long k, cudaStream_t st);
 
-// Persistent cooperative whole-iteration kernels (ks_persist.cu, NEXT-2).
+// Persistent cooperative whole-iteration kernels (ks_persist.cu, NEXT-2); the
+// FP32 instantiation is the NEXT-4 path.
+template <class T>
 int persist_grid(int bicgstab, int num_sms, int64_t mmax);
-int launch_persist(int bicgstab, const VecArgs& a, const double* A, int64_t lda, int64_t ncols,
-                   double* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st);
+template <class T>
+int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
+                   T* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st);
+
+// NEXT-4 (FP32) support kernels (ks_f32.cu): K1 in FP32, setup/init/finish in
+// FP32, conversions at the FP64 ABI boundary, FP32 generators.
+int launch_gemv_f32(const GemvParamsT<float>& p, const Scratch& s, int ticket_id, cudaStream_t st);
+int launch_setup_r_f32(const VecArgsT<float>& a, cudaStream_t st);           // x0 = 0
+int launch_init_f32(const VecArgsT<float>& a, int bicgstab, double tol, long long maxit,
+                    long long hist_cap, unsigned long long ebase, cudaStream_t st);
+int launch_finish_f32(const VecArgsT<float>& a, int bicgstab, cudaStream_t st);
+int launch_pack_x_f32(const VecArgsT<float>& a, cudaStream_t st);
+int launch_true_res_final_f32(const VecArgsT<float>& a, cudaStream_t st);
+int launch_d2f(const double* src, float* dst, int64_t n, cudaStream_t st);
+int launch_f2d(const float* src, double* dst, int64_t n, cudaStream_t st);
+int launch_rows_d2f(const double* src, int64_t lds, float* dst, int64_t ldd, int64_t rows,
+                    int64_t cols, cudaStream_t st);
+int launch_gen_spd_f32(float* A, int64_t lda, int64_t row0, int64_t m, int64_t n, uint64_t seed,
+                       const double* table_dev, cudaStream_t st);
+int launch_gen_dd_f32(float* A, int64_t lda, int64_t row0, int64_t m, int64_t n, uint64_t seed,
+                      int kd, cudaStream_t st);
 
 }  // namespace ks

@@ -38,19 +38,22 @@ __device__ __forceinline__ int64_t gidx_p(const Layout& L, int64_t j, int* owner
     *owner = g;
     return (int64_t)g * L.chunk + (j - L.row0[g]);
 }
-__device__ __forceinline__ double* par_ptr(double* G, int64_t par, long long k) { return G + (k & 1) * par; }
+template <class T>
+__device__ __forceinline__ T* par_ptr(T* G, int64_t par, long long k) { return G + (k & 1) * par; }
 __device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
 __device__ __forceinline__ bool done_flag(const DevState* st) { return *(volatile const int*)&st->done != 0; }
 __device__ __forceinline__ unsigned long long epoch(const DevState* st, long long k) {
     return *(volatile const unsigned long long*)&st->ebase + (unsigned long long)k;
 }
-__device__ __forceinline__ double slots_sum(const Layout& L, const double* G, int q) {
-    double s = 0.0;
+template <class T>
+__device__ __forceinline__ T slots_sum(const Layout& L, const T* G, int q) {
+    T s = T(0);
     for (int g = 0; g < L.P; ++g) s += G[(int64_t)g * L.chunk + L.pslot + q];
     return s;
 }
-__device__ __forceinline__ double scal_sum(const Layout& L, const double* S, int q) {
-    double s = 0.0;
+template <class T>
+__device__ __forceinline__ T scal_sum(const Layout& L, const T* S, int q) {
+    T s = T(0);
     for (int g = 0; g < L.P; ++g) s += S[g * kScalSlot + q];
     return s;
 }
@@ -101,11 +104,11 @@ __device__ bool grid_sync(unsigned* bar, DevState* st) {
 
 // Sum over CTAs (in CTA order, fixed tree) of slot q of the per-CTA partials;
 // every CTA computes the same value.
-template <int K>
-__device__ __forceinline__ void grid_total(const double* bpart, int q0, double (&out)[K], double* red) {
+template <int K, class T>
+__device__ __forceinline__ void grid_total(const T* bpart, int q0, T (&out)[K], T* red) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        double acc = 0.0;
+        T acc = T(0);
         for (int b = threadIdx.x; b < (int)gridDim.x; b += kNT) acc += __ldcg(bpart + (int64_t)b * 4 + q0 + k);
         out[k] = acc;
     }
@@ -113,46 +116,50 @@ __device__ __forceinline__ void grid_total(const double* bpart, int q0, double (
 }
 
 // Fused-mode wait for phase ph of iteration k from every rank (all CTAs).
-__device__ __forceinline__ bool wait_ph(const VecArgs& a, int ph, long long k) {
+template <class T>
+__device__ __forceinline__ bool wait_ph(const VecArgsT<T>& a, int ph, long long k) {
     const bool ok = wait_flags(a.flags + ph * kMaxRanks, a.L.P, epoch(a.st, k));
     if (!ok && threadIdx.x == 0) { a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1; }
     return ok;
 }
-__device__ __forceinline__ void flags_out(const VecArgs& a, int ph, long long k) {
+template <class T>
+__device__ __forceinline__ void flags_out(const VecArgsT<T>& a, int ph, long long k) {
     unsigned long long* f[kMaxRanks];
     for (int g = 0; g < a.L.P; ++g) f[g] = a.pp.flags[g] + ph * kMaxRanks + a.L.rank;
     publish_flags(f, a.L.P, epoch(a.st, k));
 }
 
+template <class T>
 struct PersistArgs {
-    VecArgs a;
-    const double* A;
+    VecArgsT<T> a;
+    const T* A;
     int64_t lda, ncols;
-    double* bpart;      // gridDim.x * 4
+    T* bpart;           // gridDim.x * 4
     unsigned* bar;      // {count, generation}
     long long k0, k1;   // iteration range of this launch (inclusive)
 };
 
 // GEMV phase: y = A_loc x over the tiles of this CTA (round-robin); thread 0
 // returns the CTA's partials <w1, y> and <y, y> accumulated in tile order.
-__device__ void gemv_phase(const PersistArgs& P, const double* x, double* y, const double* w1,
-                           double& d1, double& d2, double* red) {
+template <class T>
+__device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w1, T& d1, T& d2,
+                           T* red) {
     const int64_t m = m_of(P.a.L);
     const int64_t tiles = (m + kR - 1) / kR;
-    const int64_t ncb = P.ncols / (2 * kNT);
-    d1 = 0.0;
-    d2 = 0.0;
+    const int64_t ncb = P.ncols / (Vec16<T>::W * kNT);
+    d1 = T(0);
+    d2 = T(0);
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int64_t r0 = tile * kR;
         const int nvalid = (int)min((int64_t)kR, m - r0);
-        double acc[kR];
+        T acc[kR];
         stream_rows<kR, kU, kNT>(P.A, P.lda, r0, nvalid, x, 0, ncb, acc);
         block_sum<kNT, kR>(acc, red);
         if (threadIdx.x == 0) {
 #pragma unroll
             for (int r = 0; r < kR; ++r) {
                 if (r < nvalid) {
-                    const double yv = acc[r];
+                    const T yv = acc[r];
                     y[r0 + r] = yv;
                     if (w1) d1 = fma(w1[r0 + r], yv, d1);
                     d2 = fma(yv, yv, d2);
@@ -163,9 +170,10 @@ __device__ void gemv_phase(const PersistArgs& P, const double* x, double* y, con
 }
 
 // ---------------------------------------------------------------- CG (A1-A5)
-__global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs P) {
-    __shared__ double red[kR * kNW];
-    const VecArgs& a = P.a;
+template <class T>
+__global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
+    __shared__ T red[kR * kNW];
+    const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
     const int64_t m = m_of(L), r0 = L.row0[L.rank];
@@ -174,13 +182,13 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs P) {
     for (long long k = P.k0; k <= P.k1; ++k) {
         if (done_flag(st)) break;
         // A1: q = A p, sigma_g = <p_loc, q>
-        double d1, d2;
+        T d1, d2;
         gemv_phase(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
         if (!grid_sync(P.bar, st)) return;
-        double sig[1];
+        T sig[1];
         grid_total<1>(P.bpart, 0, sig, red);
-        double sigma = sig[0];
+        T sigma = sig[0];
         if (a.peer) {                                   // A2 fused C2
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) a.pp.S[g][(k & 1) * a.spar + L.rank * kScalSlot] = sigma;
@@ -189,18 +197,18 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs P) {
             if (!wait_ph(a, kPhaseS, k)) return;
             sigma = scal_sum(L, par_ptr(a.S, a.spar, k), 0);
         }
-        if (!(sigma > 0.0)) {                           // Q9
+        if (!(sigma > T(0))) {                           // Q9
             if (lead()) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
             break;
         }
-        const double alpha = st->rho[(k - 1) & 3] / sigma;
+        const T alpha = (T)st->rho[(k - 1) & 3] / sigma;
         // A3: x += alpha p, r -= alpha q, rho'_g
-        const double* rin = par_ptr(a.G_r, a.gpar, k - 1) + (int64_t)L.rank * L.chunk;
+        const T* rin = par_ptr(a.G_r, a.gpar, k - 1) + (int64_t)L.rank * L.chunk;
         const int64_t ro = (k & 1) * a.gpar + (int64_t)L.rank * L.chunk;
-        double acc[1] = {0.0};
+        T acc[1] = {T(0)};
         for (int64_t i = tid0; i < m; i += gstride) {
             a.x_loc[i] = fma(alpha, a.p_full[r0 + i], a.x_loc[i]);
-            const double r = fma(-alpha, a.q_loc[i], rin[i]);
+            const T r = fma(-alpha, a.q_loc[i], rin[i]);
             if (a.peer) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + i] = r;
             } else {
@@ -212,9 +220,9 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs P) {
         block_sum<kNT, 1>(acc, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = acc[0];
         if (!grid_sync(P.bar, st)) return;
-        double rr[1];
+        T rr[1];
         grid_total<1>(P.bpart, 1, rr, red);
-        double rho1 = rr[0];
+        T rho1 = rr[0];
         if (a.peer) {                                   // A4 fused C1 (+ partials)
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + L.pslot + 1] = rho1;
@@ -224,16 +232,16 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs P) {
             rho1 = slots_sum(L, par_ptr(a.G_r, a.gpar, k), 1);
         }
         // A5: test, beta, p = r + beta p (full, replicated)
-        const double rel = sqrt(rho1) / st->nb;
-        if (rel <= st->tol) {
+        const T rel = sqrt(rho1) / (T)st->nb;
+        if (rel <= (T)st->tol) {
             if (lead()) {
                 hist_put(st, a.hist, k - 1, rel);
                 st->relres = rel; st->iters = k; st->converged = 1; st->status = KS_OK; st->done = 1;
             }
             break;
         }
-        const double beta = rho1 / st->rho[(k - 1) & 3];
-        const double* Gr = par_ptr(a.G_r, a.gpar, k);
+        const T beta = rho1 / (T)st->rho[(k - 1) & 3];
+        const T* Gr = par_ptr(a.G_r, a.gpar, k);
         for (int64_t j = tid0; j < L.n; j += gstride) {
             int o;
             const int64_t gj = gidx_p(L, j, &o);
@@ -249,27 +257,28 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs P) {
 }
 
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
-__global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
-    __shared__ double red[kR * kNW];
-    const VecArgs& a = P.a;
+template <class T>
+__global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
+    __shared__ T red[kR * kNW];
+    const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
     const int64_t m = m_of(L), r0 = L.row0[L.rank];
     const int64_t gstride = (int64_t)gridDim.x * kNT;
     const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
     // scalars of the previous iteration (written by the previous launch / init)
-    double rho_prev = st->rho[(P.k0 - 1) & 3], alpha_prev = st->alpha[(P.k0 - 1) & 3];
-    double omega_prev = st->omega[(P.k0 - 1) & 3];
+    T rho_prev = (T)st->rho[(P.k0 - 1) & 3], alpha_prev = (T)st->alpha[(P.k0 - 1) & 3];
+    T omega_prev = (T)st->omega[(P.k0 - 1) & 3];
     for (long long i = P.k0; i <= P.k1; ++i) {
         if (done_flag(st)) break;
         // B8 (test of i-1) + B1
         if (a.peer && i >= 2 && !wait_ph(a, kPhaseR, i - 1)) return;
-        const double* Gr = par_ptr(a.G_r, a.gpar, i - 1);
-        const double rho = slots_sum(L, Gr, 0);
-        double rel = 0.0;
+        const T* Gr = par_ptr(a.G_r, a.gpar, i - 1);
+        const T rho = slots_sum(L, Gr, 0);
+        T rel = T(0);
         if (i >= 2) {
-            rel = sqrt(slots_sum(L, Gr, 1)) / st->nb;
-            if (rel <= st->tol) {
+            rel = sqrt(slots_sum(L, Gr, 1)) / (T)st->nb;
+            if (rel <= (T)st->tol) {
                 if (lead()) {
                     hist_put(st, a.hist, i - 2, rel);
                     st->relres = rel; st->iters = i - 1; st->converged = 1; st->status = KS_OK; st->done = 1;
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
                 break;
             }
         }
-        if (rho == 0.0 || !isfinite(rho)) {
+        if (rho == T(0) || !isfinite(rho)) {
             if (lead()) {
                 if (i >= 2) { hist_put(st, a.hist, i - 2, rel); st->relres = rel; }
                 st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1;
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
                 a.p_full[j] = Gr[gidx_p(L, j, &o)];
             }
         } else {
-            const double beta = (rho / rho_prev) * (alpha_prev / omega_prev);
+            const T beta = (rho / rho_prev) * (alpha_prev / omega_prev);
             for (int64_t j = tid0; j < L.n; j += gstride) {
                 int o;
                 const int64_t gj = gidx_p(L, j, &o);
@@ -305,13 +314,13 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
         if (!grid_sync(P.bar, st)) return;
         // B3: v = A p (own chunk of G_v[i&1]), <rhat, v>_g
         const int64_t vo = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
-        double d1, d2;
+        T d1, d2;
         gemv_phase(P, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
         if (!grid_sync(P.bar, st)) return;
-        double gm[1];
+        T gm[1];
         grid_total<1>(P.bpart, 0, gm, red);
-        double gam = gm[0];
+        T gam = gm[0];
         if (a.peer) {                                   // B2/B4: v pulled, partial pushed
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_v[g][vo + L.pslot] = gam;
@@ -320,30 +329,30 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
             if (!wait_ph(a, kPhaseV, i)) return;
             gam = slots_sum(L, par_ptr(a.G_v, a.gpar, i), 0);
         }
-        if (gam == 0.0 || !isfinite(gam)) {
+        if (gam == T(0) || !isfinite(gam)) {
             if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
             break;
         }
-        const double alpha = rho / gam;
+        const T alpha = rho / gam;
         // B4/B5: s = r - alpha v (full n, redundant), ||s||^2
-        double sacc[1] = {0.0};
+        T sacc[1] = {T(0)};
         for (int64_t j = tid0; j < L.n; j += gstride) {
             int o;
             const int64_t gj = gidx_p(L, j, &o);
-            const double v = a.peer ? __ldcg(a.pp.G_v[o] + (i & 1) * a.gpar + gj)
+            const T v = a.peer ? __ldcg(a.pp.G_v[o] + (i & 1) * a.gpar + gj)
                                     : a.G_v[(i & 1) * a.gpar + gj];
             a.v_full[j] = v;
-            const double s = fma(-alpha, v, Gr[gj]);
+            const T s = fma(-alpha, v, Gr[gj]);
             a.s_full[j] = s;
             sacc[0] = fma(s, s, sacc[0]);
         }
         block_sum<kNT, 1>(sacc, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = sacc[0];
         if (!grid_sync(P.bar, st)) return;
-        double ssv[1];
+        T ssv[1];
         grid_total<1>(P.bpart, 1, ssv, red);
-        const double srel = sqrt(ssv[0]) / st->nb;
-        if (srel <= st->tol) {                          // half-step exit
+        const T srel = sqrt(ssv[0]) / (T)st->nb;
+        if (srel <= (T)st->tol) {                          // half-step exit
             for (int64_t l = tid0; l < m; l += gstride) a.x_loc[l] = fma(alpha, a.p_full[r0 + l], a.x_loc[l]);
             if (lead()) {
                 hist_put(st, a.hist, i - 1, srel);
@@ -357,9 +366,9 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
         gemv_phase(P, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red);
         if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 2] = d1; P.bpart[blockIdx.x * 4 + 3] = d2; }
         if (!grid_sync(P.bar, st)) return;
-        double tv[2];
+        T tv[2];
         grid_total<2>(P.bpart, 2, tv, red);
-        double ts = tv[0], tt = tv[1];
+        T ts = tv[0], tt = tv[1];
         if (a.peer) {                                   // B7 fused C2
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) {
@@ -372,18 +381,18 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
             ts = scal_sum(L, par_ptr(a.S, a.spar, i), 0);
             tt = scal_sum(L, par_ptr(a.S, a.spar, i), 1);
         }
-        const double om = ts / tt;
-        if (tt == 0.0 || !isfinite(tt) || om == 0.0 || !isfinite(om)) {
+        const T om = ts / tt;
+        if (tt == T(0) || !isfinite(tt) || om == T(0) || !isfinite(om)) {
             if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
             break;
         }
         // B7: x += alpha p + omega s; r = s - omega t; <rhat, r>_g, <r, r>_g
         const int64_t ro = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
-        double acc[2] = {0.0, 0.0};
+        T acc[2] = {T(0), T(0)};
         for (int64_t l = tid0; l < m; l += gstride) {
-            const double s = a.s_full[r0 + l];
+            const T s = a.s_full[r0 + l];
             a.x_loc[l] = fma(om, s, fma(alpha, a.p_full[r0 + l], a.x_loc[l]));
-            const double r = fma(-om, a.q_loc[l], s);
+            const T r = fma(-om, a.q_loc[l], s);
             if (a.peer) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + l] = r;
             } else {
@@ -396,7 +405,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
         block_sum<kNT, 2>(acc, red);
         if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 0] = acc[0]; P.bpart[blockIdx.x * 4 + 1] = acc[1]; }
         if (!grid_sync(P.bar, st)) return;
-        double rv[2];
+        T rv[2];
         grid_total<2>(P.bpart, 0, rv, red);
         if (lead()) {
             if (a.peer) {
@@ -422,6 +431,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs P) {
     }
 }
 
+template <class T>
 int coop_grid(const void* kern, int num_sms, int64_t mmax) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, 0);
@@ -435,13 +445,16 @@ int coop_grid(const void* kern, int num_sms, int64_t mmax) {
 
 }  // namespace
 
+template <class T>
 int persist_grid(int bicgstab, int num_sms, int64_t mmax) {
-    return coop_grid(bicgstab ? (const void*)k_bs_persist : (const void*)k_cg_persist, num_sms, mmax);
+    return coop_grid<T>(bicgstab ? (const void*)k_bs_persist<T> : (const void*)k_cg_persist<T>, num_sms,
+                        mmax);
 }
 
-int launch_persist(int bicgstab, const VecArgs& a, const double* A, int64_t lda, int64_t ncols,
-                   double* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st) {
-    PersistArgs P;
+template <class T>
+int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
+                   T* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st) {
+    PersistArgs<T> P;
     P.a = a;
     P.A = A;
     P.lda = lda;
@@ -451,9 +464,16 @@ int launch_persist(int bicgstab, const VecArgs& a, const double* A, int64_t lda,
     P.k0 = k0;
     P.k1 = k1;
     void* args[] = {&P};
-    const void* kern = bicgstab ? (const void*)k_bs_persist : (const void*)k_cg_persist;
+    const void* kern = bicgstab ? (const void*)k_bs_persist<T> : (const void*)k_cg_persist<T>;
     cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kNT), args, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
+
+template int persist_grid<double>(int, int, int64_t);
+template int persist_grid<float>(int, int, int64_t);
+template int launch_persist<double>(int, const VecArgsT<double>&, const double*, int64_t, int64_t, double*,
+                                    unsigned*, long long, long long, int, cudaStream_t);
+template int launch_persist<float>(int, const VecArgsT<float>&, const float*, int64_t, int64_t, float*,
+                                   unsigned*, long long, long long, int, cudaStream_t);
 
 }  // namespace ks

@@ -64,7 +64,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     const bool persist = c->persistent();
     Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
     int pgrid = 0;
-    if (persist) pgrid = persist_grid(kind, r.num_sms, r.L.pslot);
+    if (persist) pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot);
     const bool use_graph = !persist && c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
     Rank::GraphCache* g = nullptr;
     if (use_graph) {
@@ -98,7 +98,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
         if (persist) {                                    // one cooperative launch per batch
             const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
             prof.pre(slot);
-            const int rc = launch_persist(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
+            const int rc = launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
                                           r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
                                           r.stream);
             prof.post(slot);
@@ -339,6 +339,123 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     r.launches += launch_bs_finish(a, r.stream);
     finish_and_copy(c, r, x, hist, hist_cap, rep, true, t_start);
     return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
+}
+
+// NEXT-4: CG / BiCGSTAB in FP32 (persistent path; P == 1 or the fused exchange).
+// The ABI is FP64: b is converted on the device, x converted back; x0 = 0.
+int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, int64_t maxit,
+                double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    const auto t_start = Clock::now();
+    check_loaded(c, r);
+    r.launches = 0;
+    r.gemv_launches = 0;
+    r.gemv_seconds = 0.0;
+    if (hist_cap > r.hist_alloc) {
+        KS_CUDA(cudaFree(r.hist));
+        r.hist = nullptr;
+        r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.hist), (size_t)r.hist_alloc * sizeof(double)));
+    }
+    const bool fused = c->fused();
+    VecArgsT<float> a0 = r.vargs_f32(false), a = r.vargs_f32(fused);
+    double* tmp = nullptr;                              // FP64 staging of b / x
+    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&tmp), (size_t)c->n * sizeof(double)));
+    KS_CUDA(cudaMemcpyAsync(tmp, b, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+    r.launches += launch_d2f(tmp, a.b_full_mut(), c->n, r.stream);
+    r.launches += launch_setup_r_f32(a0, r.stream);
+    allgather(c, r, r.G_r, r.L.chunk);
+    const unsigned long long ebase = r.epoch_next;
+    r.epoch_next += (unsigned long long)maxit + 2;
+    r.launches += launch_init_f32(a, bicgstab, tol, maxit, hist_cap, ebase, r.stream);
+    const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
+    const int gemvs = bicgstab ? 2 : 1;
+    Prof prof(c, r, 1);
+    const int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot);
+    float* bpart = reinterpret_cast<float*>(r.scr.part + 2 * kPartStride);
+    int64_t k = 1, batch = 0;
+    KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+    while (k <= maxit) {
+        const int slot = (int)(batch & 1);
+        prof.begin(slot);
+        const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
+        prof.pre(slot);
+        const int rc = launch_persist<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld,
+                                             bpart, r.scr.ticket + 8, k, kend, pgrid, r.stream);
+        prof.post(slot);
+        if (rc < 0) KS_CUDA((cudaError_t)(-rc));
+        r.launches += 1;
+        r.gemv_launches += (kend - k + 1) * gemvs;
+        k = kend + 1;
+        KS_CUDA(cudaMemcpyAsync(&r.h_done[slot], &r.st->done, sizeof(int), cudaMemcpyDeviceToHost, r.stream));
+        KS_CUDA(cudaEventRecord(r.ev_poll[slot], r.stream));
+        if (batch >= 1) {
+            KS_CUDA(cudaEventSynchronize(r.ev_poll[slot ^ 1]));
+            prof.harvest(slot ^ 1);
+            if (r.h_done[slot ^ 1]) { ++batch; break; }
+        }
+        ++batch;
+    }
+    KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    prof.harvest(0);
+    prof.harvest(1);
+    r.launches += launch_finish_f32(a, bicgstab, r.stream);
+    // x (full length, FP32) -> true residual (K1 FP32, residual mode) -> FP64 out
+    float* xfull = a.s_full;
+    if (c->P > 1) {
+        r.launches += launch_pack_x_f32(a0, r.stream);
+        allgather(c, r, r.G_v, r.L.chunk);
+        copy_chunks_to(c, r, r.G_v, r.s_full, cudaMemcpyDeviceToDevice);
+    } else {
+        KS_CUDA(cudaMemcpyAsync(xfull, a.x_loc, (size_t)c->n * sizeof(float), cudaMemcpyDeviceToDevice, r.stream));
+    }
+    if (c->opt.true_residual) {
+        GemvParamsT<float> p{};
+        p.A = reinterpret_cast<const float*>(r.A);
+        p.lda = c->ld;
+        p.m = r.m;
+        p.ncols = c->ld;
+        p.x = xfull;
+        p.y = a.q_loc;
+        p.bsub = a.b_full + r.row0;
+        p.out2 = a0.S + (int64_t)r.rank * kScalSlot + 1;
+        r.launches += launch_gemv_f32(p, r.scr, 1, r.stream);
+        allgather(c, r, r.S, kScalSlot);
+        r.launches += launch_true_res_final_f32(a0, r.stream);
+    }
+    r.launches += launch_f2d(xfull, tmp, c->n, r.stream);
+    KS_CUDA(cudaMemcpyAsync(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    const DevState& s = *r.h_state;
+    if (c->writes_host(r)) {
+        KS_CUDA(cudaMemcpyAsync(x, tmp, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+        const int64_t nh = std::min<int64_t>(s.iters, hist_cap);
+        if (hist && nh > 0)
+            KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault, r.stream));
+        KS_CUDA(cudaStreamSynchronize(r.stream));
+    }
+    KS_CUDA(cudaFree(tmp));
+    if (rep) {
+        float ms = 0.f;
+        KS_CUDA(cudaEventElapsedTime(&ms, r.ev_t0, r.ev_t1));
+        ks_report R;
+        std::memset(&R, 0, sizeof R);
+        R.iterations = s.iters;
+        R.half_step_exit = s.half;
+        R.matvecs = bicgstab ? 2 * s.iters - (s.half ? 1 : 0) : s.iters;
+        R.converged = s.converged;
+        R.breakdown = s.breakdown;
+        R.status = s.status;
+        R.relres = s.relres;
+        R.true_relres = (c->opt.true_residual && s.nb > 0) ? std::sqrt(s.true_rr) / s.nb : (s.bzero ? 0.0 : -1.0);
+        R.seconds_loop = ms * 1e-3;
+        R.seconds_total = std::chrono::duration<double>(Clock::now() - t_start).count();
+        R.seconds_gemv = r.gemv_seconds;
+        R.gemv_launches = r.gemv_launches;
+        R.kernel_launches = r.launches;
+        *rep = R;
+    }
+    return s.peer_timeout ? (int64_t)KS_ENCCL : s.status;
 }
 
 // GMRES(m) (NEXT-3): host-orchestrated cycles (their structure is

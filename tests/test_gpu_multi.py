@@ -168,6 +168,27 @@ def test_multi_gmres(P):
 
 
 @needs2
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_f32(P):
+    """NEXT-4 at P GPUs: FP32 persistent kernels with the fused NVLink exchange."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    from test_gpu_parity import bars_f32
+    n = 4096
+    A, b = synth.gdd(n, 16)
+    xo, ho, ro = oracle.bicgstab_f32(A, b, tol=1e-5)
+    Cs, cs, bs = synth.gspd(n, 1e2)
+    xc, hc, rc = oracle.cg_f32(Cs, bs, tol=1e-5)
+    with ks.Context(n, ngpus=P, dtype="f32") as ctx, ks.Context(n, ngpus=P, dtype="f32") as cc:
+        ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
+        x, h, r = ctx.bicgstab(b.astype(np.float32).astype(np.float64), tol=1e-5)
+        x2, h2, r2 = cc.cg(bs.astype(np.float32).astype(np.float64), tol=1e-5)
+    bars_f32(x, h, r, xo, ho, ro)
+    bars_f32(x2, h2, r2, xc, hc, rc)
+
+
+@needs2
 def test_multi_edge_cases():
     n = 64
     A = synth.random_spd(n, 10.0, 1)

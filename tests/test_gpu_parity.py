@@ -472,3 +472,82 @@ def test_gmres_edges():
             x, h, r = ctx.gmres(np.array(e["b"], float), tol=1e-12, restart=e["restart"])
         assert r.converged and r.iterations <= e["max_iterations"], e["cite"]
         assert np.allclose(x, e["x"], rtol=1e-12, atol=1e-15), e["cite"]
+
+
+# ----------------------------------------------------------------- NEXT-4: FP32
+
+# FP32 bars (reading Q27): the FP32 oracle's own spread on a permuted
+# system is <= 8e-7 (history, absolute) and <= 5.8e-6 (x); bars keep a >= 12x margin.
+F32_X, F32_REL, F32_FLOOR = 1e-4, 1e-3, 1e-5
+
+
+def bars_f32(x, h, r, xo, ho, ro):
+    assert abs(r.iterations - ro.iterations) <= 2, (r.iterations, ro.iterations)
+    k = min(50, len(h), len(ho))
+    d = np.abs(h[:k] - ho[:k].astype(np.float64))
+    assert np.all(d <= F32_REL * ho[:k] + F32_FLOOR), float(np.max(d))
+    xo = xo.astype(np.float64)
+    assert np.linalg.norm(x - xo) <= F32_X * np.linalg.norm(xo)
+
+
+def test_f32_generate_and_matvec():
+    n = 1024
+    A, c, b = synth.gspd(n, 1e3)
+    D, bd = synth.gdd(n, 16)
+    with ks.Context(n, dtype="f32") as g1, ks.Context(n, dtype="f32") as g2, \
+            ks.Context(n, dtype="f32") as l1:
+        g1.generate("spd", seed=synth.SEED, table=c, want_b=False)
+        g2.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        l1.load_rows(D)
+        for j in (0, 513, 1023):
+            e = np.zeros(n)
+            e[j] = 1.0
+            assert np.array_equal(g1.matvec(e), A[:, j].astype(np.float32).astype(np.float64))
+            assert np.array_equal(g2.matvec(e), D[:, j].astype(np.float32).astype(np.float64))
+        x = np.random.default_rng(1).standard_normal(n).astype(np.float32).astype(np.float64)
+        y = l1.matvec(x)
+        assert np.array_equal(y, g2.matvec(x))
+        A32 = D.astype(np.float32).astype(np.float64)
+        ref = A32 @ x
+        bound = 2 * n * 2.0 ** -24 * (np.abs(A32) @ np.abs(x))
+        assert np.all(np.abs(y - ref) <= bound)
+
+
+@pytest.mark.parametrize("method,case", [("cg", (1024, 1e3)), ("cg", (4096, 1e2)),
+                                         ("bicgstab", (1024, 4)), ("bicgstab", (1024, 16)),
+                                         ("bicgstab", (4096, 16))])
+def test_f32_parity(method, case):
+    """NEXT-4: FP32 CG / BiCGSTAB on the GPU vs the FP32 oracle listings, tol 1e-5."""
+    n = case[0]
+    if method == "cg":
+        A, c, b = synth.gspd(n, case[1])
+        xo, ho, ro = oracle.cg_f32(A, b, tol=1e-5)
+    else:
+        A, b = synth.gdd(n, case[1])
+        xo, ho, ro = oracle.bicgstab_f32(A, b, tol=1e-5)
+    bb = b.astype(np.float32).astype(np.float64)
+    with ks.Context(n, dtype="f32") as ctx:
+        if method == "cg":
+            ctx.generate("spd", seed=synth.SEED, table=c, want_b=False)
+        else:
+            ctx.generate("dd", seed=synth.SEED, kd=case[1], want_b=False)
+        x, h, r = getattr(ctx, method)(bb, tol=1e-5)
+        x2, h2, r2 = getattr(ctx, method)(bb, tol=1e-5)
+    assert r.converged
+    bars_f32(x, h, r, xo, ho, ro)
+    assert np.array_equal(x, x2) and np.array_equal(h, h2)
+    assert r.true_relres <= 10 * 1e-5
+
+
+def test_f32_unsupported_calls():
+    n = 64
+    with ks.Context(n, dtype="f32") as ctx:
+        ctx.load_rows(synth.random_spd(n, 10.0, 1))
+        b = np.ones(n)
+        for call in (lambda: ctx.cg(b, x0=np.ones(n)), lambda: ctx.bicg(b), lambda: ctx.gmres(b),
+                     lambda: ctx.matvec_t(b)):
+            with pytest.raises(ks.KsError) as e:
+                call()
+            assert e.value.status == ks.KS_EARG
+        x, h, r = ctx.cg(np.zeros(n), tol=1e-5)
+        assert r.iterations == 0 and np.all(x == 0)

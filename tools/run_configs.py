@@ -45,11 +45,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     out = []
     for name in sys.argv[1:]:
+        dtype = "f64"
+        if name.endswith(":f32"):
+            name, dtype = name[:-4], "f32"
         method, n, gp, K = CONFIGS[name]
         if world > 1:
-            ctx = ks.Context.from_process_group(n)
+            ctx = ks.Context.from_process_group(n, dtype=dtype)
         else:
-            ctx = ks.Context.from_rank(n, 0, 1, None, local, torch.cuda.current_stream().cuda_stream)
+            ctx = ks.Context.from_rank(n, 0, 1, None, local, torch.cuda.current_stream().cuda_stream,
+                                       dtype=dtype)
         t0 = time.perf_counter()
         table = None
         if method == "cg":
@@ -66,17 +70,18 @@ def main():
         ips = K / r.seconds_loop
         g = 1 if method in ("cg", "gmres") else 2   # GEMVs per iteration
         m = ctx.row_range(rank)[1] - ctx.row_range(rank)[0]
-        gemv_bw = 8.0 * m * n * r.gemv_launches / max(r.seconds_gemv, 1e-12)
-        t_roof = g * 8.0 * n * n / world / NOMINAL + g * 8.0 * n * (world - 1) / world / 0.9e12
+        esz = 4.0 if dtype == "f32" else 8.0
+        gemv_bw = esz * m * n * r.gemv_launches / max(r.seconds_gemv, 1e-12)
+        t_roof = g * esz * n * n / world / NOMINAL + g * esz * n * (world - 1) / world / 0.9e12
         ctx.set_option("profile_gemv", 0)
         ctx.set_option("true_residual", 1)
-        x, h, rt = solve(b, tol=1e-10)
-        rec = {"config": name, "method": method, "n": n, "P": world, "gen_s": tgen,
+        x, h, rt = solve(b, tol=1e-5 if dtype == "f32" else 1e-10)
+        rec = {"config": name, "dtype": dtype, "method": method, "n": n, "P": world, "gen_s": tgen,
                "fixed_iters": K, "iters_per_s": ips, "frac_roofline_8TBps": ips * t_roof,
                "gemv_GBps_per_gpu": gemv_bw / 1e9, "iters_to_tol": rt.iterations,
                "converged": rt.converged, "half_step_exit": rt.half_step_exit,
                "true_relres": rt.true_relres, "solve_s": rt.seconds_total, "hist0": h[:3].tolist()}
-        if method == "cg" and rank == 0:
+        if method == "cg" and rank == 0 and dtype == "f64":
             import oracle
             xcf = oracle.spd_exact_solve_ld(table, synth.SEED, b)
             rec["x_vs_closed_form"] = float(np.linalg.norm(x - xcf) / np.linalg.norm(xcf))
