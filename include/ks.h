@@ -99,7 +99,7 @@ typedef enum {
     KS_OPT_TRUE_RESIDUAL = 0, /* 1 (default): report true_relres (one extra GEMV) */
     KS_OPT_PROFILE_GEMV = 1,  /* 1: time every K1 launch with CUDA events         */
     KS_OPT_POLL_BATCH = 2,    /* iterations queued between done-flag polls (16)   */
-    KS_OPT_GEMV_ROWS = 3,     /* K1 rows per CTA tile: 4, 8 or 16 (default 0=auto)*/
+    KS_OPT_GEMV_ROWS = 3,     /* K1 rows per CTA tile: 2, 4, 8, 16 (0 = auto)     */
     KS_OPT_GEMV_SPLIT = 4,    /* K1 column splits per tile (0 = auto)             */
     KS_OPT_GEMV_KERNEL = 5,   /* K1 variant: 0 = auto, 1 = LDG stream, 2 = TMA    */
                               /* bulk-copy ring                                   */
@@ -111,17 +111,19 @@ typedef enum {
                               /* flag (no NCCL call in the loop); 0: NCCL         */
                               /* allgathers.  ks_get_option returns the effective */
                               /* mode.                                            */
-    KS_OPT_PERSISTENT = 8     /* 0: one kernel per step; 1: one persistent        */
+    KS_OPT_PERSISTENT = 8,    /* 0: one kernel per step; 1: one persistent        */
                               /* cooperative kernel per poll batch (grid barriers */
                               /* instead of kernel boundaries; needs P == 1 or    */
                               /* the fused exchange); 2 (default): auto (on when  */
                               /* eligible).  ks_get_option returns the effective  */
                               /* mode.                                            */
+    KS_OPT_GEMV_UNROLL = 9    /* tuning: K1 LDG column-block unroll 1/2/4/8 (0 =  */
+                              /* the default for the row count)                   */
 } ks_option;
 
 /* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL
  * communicator from ncclCommInitAll when ngpus > 1).  n >= 1, 1 <= ngpus <= 16
- * and <= device count, dtype = KS_FLOAT64.  Allocates each shard (m_g x ld FP64)
+ * and <= device count, dtype = KS_FLOAT64 or KS_FLOAT32.  Allocates each shard (m_g x ld)
  * plus O(n) vectors with cudaMalloc and zero-fills them.                        */
 ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
 

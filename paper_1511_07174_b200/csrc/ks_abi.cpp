@@ -480,7 +480,7 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             if (v < 1 || v > 4096) return fail(c, KS_EARG, "poll batch must be in [1, 4096]");
             o.poll_batch = v; break;
         case KS_OPT_GEMV_ROWS:
-            if (v != 0 && v != 4 && v != 8 && v != 16) return fail(c, KS_EARG, "rows must be 0, 4, 8 or 16");
+            if (v != 0 && v != 2 && v != 4 && v != 8 && v != 16) return fail(c, KS_EARG, "rows must be 0, 2, 4, 8 or 16");
             o.gemv_rows = v; break;
         case KS_OPT_GEMV_SPLIT:
             if (v < 0 || v > 64) return fail(c, KS_EARG, "split must be in [0, 64]");
@@ -493,6 +493,9 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
         case KS_OPT_PERSISTENT:
             if (v < 0 || v > 2) return fail(c, KS_EARG, "persistent must be 0, 1 or 2");
             o.persistent = v; break;
+        case KS_OPT_GEMV_UNROLL:
+            if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8) return fail(c, KS_EARG, "unroll must be 0, 1, 2, 4 or 8");
+            o.gemv_unroll = v; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -511,6 +514,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_USE_GRAPHS: *v = o.use_graphs; break;
         case KS_OPT_FUSED_COMM: *v = c->fused() ? 1 : 0; break;   // effective value
         case KS_OPT_PERSISTENT: *v = c->persistent() ? 1 : 0; break;  // effective value
+        case KS_OPT_GEMV_UNROLL: *v = o.gemv_unroll; break;
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

@@ -111,7 +111,7 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     dmalloc(&r.hist, r.hist_alloc);
     dmalloc(&r.scr.part, (size_t)kNumTickets * kPartStride);
     dmalloc(&r.scr.ticket, kNumTickets);
-    r.scr.tile_cap = r.m / 4 + 2;
+    r.scr.tile_cap = r.m / 2 + 2;                  // tiles of the smallest row count (R = 2)
     r.scr.qpart_cap = std::max<int64_t>(2 * 6 * 2 * 160 * 16 + 4096, 2 * r.scr.tile_cap + 4096);
     dmalloc(&r.scr.qpart, r.scr.qpart_cap);
     dmalloc(&r.scr.tile_ticket, r.scr.tile_cap);
@@ -304,6 +304,7 @@ const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done) {
 GemvConfig gemv_config(const ks_ctx* c, const Rank& r) {
     GemvConfig g = choose_gemv(r.m, c->ld, r.num_sms, (int)c->opt.gemv_rows, (int)c->opt.gemv_split,
                                (int)c->opt.gemv_kernel);
+    g.unroll = (int)c->opt.gemv_unroll;
     const int64_t tiles = (r.m + g.rows - 1) / g.rows;
     const int64_t cap = (r.scr.qpart_cap - 2 * tiles - 64) / std::max<int64_t>(1, tiles * g.rows);
     if (g.splits > cap) g.splits = (int)std::max<int64_t>(1, cap);

@@ -113,6 +113,7 @@ struct Options {
     int64_t use_graphs = 0;
     int64_t fused_comm = 1;   // fused NVLink peer-store collectives when available
     int64_t persistent = 2;   // 0 off, 1 on, 2 auto: persistent cooperative kernels
+    int64_t gemv_unroll = 0;  // tuning: K1 LDG unroll (0 = default)
 };
 
 }  // namespace ks

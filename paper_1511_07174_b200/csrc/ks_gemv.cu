@@ -266,6 +266,16 @@ __global__ void __launch_bounds__(kNT) k1_gemv_tma(GemvParams p, int S, int64_t 
     gemv_epilogue<R>(p, acc, tile, s, S, tiles, qpart, tile_ticket, dpart, ticket, red);
 }
 
+template <int R, int U>
+void launch_ldg(const GemvParams& p, const GemvConfig& c, const Scratch& s, int ticket_id, cudaStream_t st) {
+    const int64_t tiles = (p.m + R - 1) / R;
+    const int64_t grid = tiles * c.splits;
+    double* dpart = s.part + (int64_t)ticket_id * kPartStride;
+    if (tiles * 2 > kPartStride) dpart = s.qpart + (s.qpart_cap - tiles * 2);
+    k1_gemv_ldg<R, U, double><<<(unsigned)grid, kNT, 0, st>>>(p, c.splits, tiles, s.qpart, s.tile_ticket,
+                                                              dpart, s.ticket + ticket_id);
+}
+
 template <int R>
 int launch_rows(const GemvParams& p, const GemvConfig& c, const Scratch& s, int ticket_id,
                 cudaStream_t st) {
@@ -288,10 +298,15 @@ int launch_rows(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
         }
         kern<<<(unsigned)grid, kNT, smem, st>>>(p, c.splits, tiles, s.qpart, s.tile_ticket, dpart,
                                                ticket);
-    } else {
-        constexpr int U = (R >= 16) ? 1 : (R >= 8 ? 2 : 4);
-        k1_gemv_ldg<R, U, double><<<(unsigned)grid, kNT, 0, st>>>(p, c.splits, tiles, s.qpart,
-                                                                  s.tile_ticket, dpart, ticket);
+        return 1;
+    }
+    // LDG stream: unroll U (tuning sweep; default 16 loads in flight per thread)
+    const int U = c.unroll > 0 ? c.unroll : (R >= 16 ? 1 : (R >= 8 ? 2 : 4));
+    switch (U) {
+        case 1: launch_ldg<R, 1>(p, c, s, ticket_id, st); break;
+        case 2: launch_ldg<R, 2>(p, c, s, ticket_id, st); break;
+        case 8: launch_ldg<R, 8>(p, c, s, ticket_id, st); break;
+        default: launch_ldg<R, 4>(p, c, s, ticket_id, st); break;
     }
     return 1;
 }
@@ -302,9 +317,12 @@ GemvConfig choose_gemv(int64_t m, int64_t ncols, int num_sms, int rows_opt, int 
                        int variant_opt) {
     GemvConfig c;
     c.variant = variant_opt == 2 ? 2 : 1;
-    // measured on B200 at n = 65536 (profiles/): LDG R=4 7.35 TB/s, R=8 7.08, R=16 5.26;
+    // measured on B200 at n = 65536 (profiles/r01_gemv_sweep*.json): LDG R=2/U=4
+    // 7.41 TB/s, R=4/U=2 7.40, R=4/U=4 6.84-7.43 (box dependent), R=8 <= 7.18;
     // TMA R=16 6.82, R=8 6.00, R=4 4.28
-    c.rows = (rows_opt == 4 || rows_opt == 8 || rows_opt == 16) ? rows_opt : (c.variant == 2 ? 16 : 4);
+    c.rows = (rows_opt == 2 || rows_opt == 4 || rows_opt == 8 || rows_opt == 16) ? rows_opt
+                                                                                  : (c.variant == 2 ? 16 : 2);
+    c.unroll = 0;
     const int64_t tiles = (m + c.rows - 1) / c.rows;
     const int64_t ncb = std::max<int64_t>(1, ncols / (2 * kNT));   // == ncols / kCW
     if (split_opt > 0) {
@@ -322,6 +340,7 @@ int launch_gemv(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
     (void)num_sms;
     if (p.m <= 0) return 0;
     switch (c.rows) {
+        case 2: return launch_rows<2>(p, c, s, ticket_id, st);
         case 4: return launch_rows<4>(p, c, s, ticket_id, st);
         case 8: return launch_rows<8>(p, c, s, ticket_id, st);
         default: return launch_rows<16>(p, c, s, ticket_id, st);
@@ -329,11 +348,11 @@ int launch_gemv(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
 }
 
 
-// NEXT-4: K1 in FP32 (R = 4 rows x 1024-column blocks of float4 loads; no split-K:
+// NEXT-4: K1 in FP32 (R = 2 rows x 1024-column blocks of float4 loads; no split-K:
 // the FP32 path serves the configs whose row count fills the GPU).
 int launch_gemv_f32(const GemvParamsT<float>& p, const Scratch& s, int ticket_id, cudaStream_t st) {
     if (p.m <= 0) return 0;
-    constexpr int R = 4;
+    constexpr int R = 2;
     const int64_t tiles = (p.m + R - 1) / R;
     float* dpart = reinterpret_cast<float*>(s.part + (int64_t)ticket_id * kPartStride);
     if (tiles * 2 > 2 * kPartStride) dpart = reinterpret_cast<float*>(s.qpart);

@@ -100,6 +100,7 @@ struct GemvConfig {
     int variant;   // 1 = LDG stream, 2 = TMA bulk ring
     int rows;      // R
     int splits;    // S
+    int unroll;    // LDG unroll U (0 = default for R)
 };
 
 // ---- kernels (launchers return the number of kernel launches issued) -------
@@ -206,11 +207,13 @@ int launch_bicg_direction(const VecArgs& a, long long k, cudaStream_t st);
 
 // Persistent cooperative whole-iteration kernels (ks_persist.cu, NEXT-2); the
 // FP32 instantiation is the NEXT-4 path.
+// rows/unroll: the GEMV tile shape (0, 0 = default R=2, U=4; (4,2) and (4,4) selectable).
 template <class T>
-int persist_grid(int bicgstab, int num_sms, int64_t mmax);
+int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll);
 template <class T>
 int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
-                   T* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st);
+                   T* bpart, unsigned* bar, long long k0, long long k1, int grid, int rows, int unroll,
+                   cudaStream_t st);
 
 // NEXT-4 (FP32) support kernels (ks_f32.cu): K1 in FP32, setup/init/finish in
 // FP32, conversions at the FP64 ABI boundary, FP32 generators.

@@ -27,8 +27,8 @@ namespace {
 
 constexpr int kNT = 256;
 constexpr int kNW = kNT / 32;
-constexpr int kR = 4;
-constexpr int kU = 4;
+// GEMV tile shape of the persistent kernels (rows R x unrolled column blocks U);
+// instantiated for the shapes the tuning sweep found at the streaming ceiling.
 
 // -- small helpers (the same conventions as ks_vec.cu) ------------------------
 __device__ __forceinline__ int64_t m_of(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
@@ -141,7 +141,7 @@ struct PersistArgs {
 
 // GEMV phase: y = A_loc x over the tiles of this CTA (round-robin); thread 0
 // returns the CTA's partials <w1, y> and <y, y> accumulated in tile order.
-template <class T>
+template <int kR, int kU, class T>
 __device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w1, T& d1, T& d2,
                            T* red) {
     const int64_t m = m_of(P.a.L);
@@ -170,9 +170,9 @@ __device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w
 }
 
 // ---------------------------------------------------------------- CG (A1-A5)
-template <class T>
+template <class T, int kR, int kU>
 __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
-    __shared__ T red[kR * kNW];
+    __shared__ T red[(kR > 2 ? kR : 2) * kNW];
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
         if (done_flag(st)) break;
         // A1: q = A p, sigma_g = <p_loc, q>
         T d1, d2;
-        gemv_phase(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
+        gemv_phase<kR, kU>(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
         if (!grid_sync(P.bar, st)) return;
         T sig[1];
@@ -257,9 +257,9 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
 }
 
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
-template <class T>
+template <class T, int kR, int kU>
 __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
-    __shared__ T red[kR * kNW];
+    __shared__ T red[(kR > 2 ? kR : 2) * kNW];
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
         // B3: v = A p (own chunk of G_v[i&1]), <rhat, v>_g
         const int64_t vo = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
         T d1, d2;
-        gemv_phase(P, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red);
+        gemv_phase<kR, kU>(P, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
         if (!grid_sync(P.bar, st)) return;
         T gm[1];
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
             break;
         }
         // B6: t = A s (q_loc), <t, s_loc>_g, <t, t>_g
-        gemv_phase(P, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red);
+        gemv_phase<kR, kU>(P, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red);
         if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 2] = d1; P.bpart[blockIdx.x * 4 + 3] = d2; }
         if (!grid_sync(P.bar, st)) return;
         T tv[2];
@@ -431,13 +431,27 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
     }
 }
 
+// Persistent GEMV shape: default R=2, U=4 (the sweep's best: CG 211.5 / BiCGSTAB
+// 105.3 it/s at n = 65536 vs 206.6 / 103.4 for R=4/U=2, profiles/r01_persist_sweep.json);
+// (4,2) and (4,4) selectable through KS_OPT_GEMV_ROWS / KS_OPT_GEMV_UNROLL.
 template <class T>
-int coop_grid(const void* kern, int num_sms, int64_t mmax) {
+const void* pick(int bicgstab, int rows, int unroll) {
+    const int shape = (rows == 4 && unroll == 2) ? 1 : (rows == 4 && unroll == 4) ? 2 : 0;
+    if (bicgstab) {
+        return shape == 1 ? (const void*)k_bs_persist<T, 4, 2>
+             : shape == 2 ? (const void*)k_bs_persist<T, 4, 4> : (const void*)k_bs_persist<T, 2, 4>;
+    }
+    return shape == 1 ? (const void*)k_cg_persist<T, 4, 2>
+         : shape == 2 ? (const void*)k_cg_persist<T, 4, 4> : (const void*)k_cg_persist<T, 2, 4>;
+}
+int rows_of(int rows, int unroll) { return (rows == 4 && (unroll == 2 || unroll == 4)) ? 4 : 2; }
+
+int coop_grid(const void* kern, int num_sms, int64_t mmax, int R) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, 0);
     if (per_sm < 1) per_sm = 1;
     const int64_t cap = (int64_t)per_sm * num_sms;
-    const int64_t tiles = (mmax + kR - 1) / kR;
+    const int64_t tiles = (mmax + R - 1) / R;
     int64_t g = tiles < num_sms ? num_sms : tiles;
     if (g > cap) g = cap;
     return (int)g;
@@ -446,14 +460,14 @@ int coop_grid(const void* kern, int num_sms, int64_t mmax) {
 }  // namespace
 
 template <class T>
-int persist_grid(int bicgstab, int num_sms, int64_t mmax) {
-    return coop_grid<T>(bicgstab ? (const void*)k_bs_persist<T> : (const void*)k_cg_persist<T>, num_sms,
-                        mmax);
+int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll) {
+    return coop_grid(pick<T>(bicgstab, rows, unroll), num_sms, mmax, rows_of(rows, unroll));
 }
 
 template <class T>
 int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
-                   T* bpart, unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st) {
+                   T* bpart, unsigned* bar, long long k0, long long k1, int grid, int rows, int unroll,
+                   cudaStream_t st) {
     PersistArgs<T> P;
     P.a = a;
     P.A = A;
@@ -464,16 +478,16 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
     P.k0 = k0;
     P.k1 = k1;
     void* args[] = {&P};
-    const void* kern = bicgstab ? (const void*)k_bs_persist<T> : (const void*)k_cg_persist<T>;
-    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kNT), args, 0, st);
+    cudaError_t e = cudaLaunchCooperativeKernel(pick<T>(bicgstab, rows, unroll), dim3((unsigned)grid),
+                                                dim3(kNT), args, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
-template int persist_grid<double>(int, int, int64_t);
-template int persist_grid<float>(int, int, int64_t);
+template int persist_grid<double>(int, int, int64_t, int, int);
+template int persist_grid<float>(int, int, int64_t, int, int);
 template int launch_persist<double>(int, const VecArgsT<double>&, const double*, int64_t, int64_t, double*,
-                                    unsigned*, long long, long long, int, cudaStream_t);
+                                    unsigned*, long long, long long, int, int, int, cudaStream_t);
 template int launch_persist<float>(int, const VecArgsT<float>&, const float*, int64_t, int64_t, float*,
-                                   unsigned*, long long, long long, int, cudaStream_t);
+                                   unsigned*, long long, long long, int, int, int, cudaStream_t);
 
 }  // namespace ks

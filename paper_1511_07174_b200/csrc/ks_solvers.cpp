@@ -64,7 +64,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     const bool persist = c->persistent();
     Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
     int pgrid = 0;
-    if (persist) pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot);
+    if (persist) pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, (int)c->opt.gemv_rows, (int)c->opt.gemv_unroll);
     const bool use_graph = !persist && c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
     Rank::GraphCache* g = nullptr;
     if (use_graph) {
@@ -100,7 +100,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
             prof.pre(slot);
             const int rc = launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
                                           r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
-                                          r.stream);
+                                          (int)c->opt.gemv_rows, (int)c->opt.gemv_unroll, r.stream);
             prof.post(slot);
             if (rc < 0) KS_CUDA((cudaError_t)(-rc));
             r.launches += 1;
@@ -370,7 +370,8 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
     const int gemvs = bicgstab ? 2 : 1;
     Prof prof(c, r, 1);
-    const int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot);
+    const int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, (int)c->opt.gemv_rows,
+                                          (int)c->opt.gemv_unroll);
     float* bpart = reinterpret_cast<float*>(r.scr.part + 2 * kPartStride);
     int64_t k = 1, batch = 0;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
@@ -380,7 +381,8 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
         const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
         prof.pre(slot);
         const int rc = launch_persist<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld,
-                                             bpart, r.scr.ticket + 8, k, kend, pgrid, r.stream);
+                                             bpart, r.scr.ticket + 8, k, kend, pgrid, (int)c->opt.gemv_rows,
+                                             (int)c->opt.gemv_unroll, r.stream);
         prof.post(slot);
         if (rc < 0) KS_CUDA((cudaError_t)(-rc));
         r.launches += 1;
