@@ -117,8 +117,10 @@ typedef enum {
                               /* the fused exchange); 2 (default): auto (on when  */
                               /* eligible).  ks_get_option returns the effective  */
                               /* mode.                                            */
-    KS_OPT_GEMV_UNROLL = 9    /* tuning: K1 LDG column-block unroll 1/2/4/8 (0 =  */
+    KS_OPT_GEMV_UNROLL = 9,   /* tuning: K1 LDG column-block unroll 1/2/4/8 (0 =  */
                               /* the default for the row count)                   */
+    KS_OPT_PERSIST_GRID = 10  /* tuning: cap on the persistent kernels' CTA count */
+                              /* (0 = auto; the grid must be equal on all ranks)  */
 } ks_option;
 
 /* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL

@@ -496,6 +496,9 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
         case KS_OPT_GEMV_UNROLL:
             if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8) return fail(c, KS_EARG, "unroll must be 0, 1, 2, 4 or 8");
             o.gemv_unroll = v; break;
+        case KS_OPT_PERSIST_GRID:
+            if (v < 0 || v > 1 << 20) return fail(c, KS_EARG, "bad persistent grid");
+            o.persist_grid = v; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -515,6 +518,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_FUSED_COMM: *v = c->fused() ? 1 : 0; break;   // effective value
         case KS_OPT_PERSISTENT: *v = c->persistent() ? 1 : 0; break;  // effective value
         case KS_OPT_GEMV_UNROLL: *v = o.gemv_unroll; break;
+        case KS_OPT_PERSIST_GRID: *v = o.persist_grid; break;
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

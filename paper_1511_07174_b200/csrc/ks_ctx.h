@@ -114,6 +114,7 @@ struct Options {
     int64_t fused_comm = 1;   // fused NVLink peer-store collectives when available
     int64_t persistent = 2;   // 0 off, 1 on, 2 auto: persistent cooperative kernels
     int64_t gemv_unroll = 0;  // tuning: K1 LDG unroll (0 = default)
+    int64_t persist_grid = 0; // tuning: persistent CTAs (0 = auto)
 };
 
 }  // namespace ks

@@ -64,7 +64,10 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     const bool persist = c->persistent();
     Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
     int pgrid = 0;
-    if (persist) pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, (int)c->opt.gemv_rows, (int)c->opt.gemv_unroll);
+    if (persist) {
+        pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, (int)c->opt.gemv_rows, (int)c->opt.gemv_unroll);
+        if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
+    }
     const bool use_graph = !persist && c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
     Rank::GraphCache* g = nullptr;
     if (use_graph) {
