@@ -119,8 +119,11 @@ typedef enum {
                               /* mode.                                            */
     KS_OPT_GEMV_UNROLL = 9,   /* tuning: K1 LDG column-block unroll 1/2/4/8 (0 =  */
                               /* the default for the row count)                   */
-    KS_OPT_PERSIST_GRID = 10  /* tuning: cap on the persistent kernels' CTA count */
+    KS_OPT_PERSIST_GRID = 10, /* tuning: cap on the persistent kernels' CTA count */
                               /* (0 = auto; the grid must be equal on all ranks)  */
+    KS_OPT_GEMVT_SHAPE = 11   /* tuning (process-wide): K1T 16-byte vectors per   */
+                              /* thread per row (1/2/4) * 100 + rows in flight    */
+                              /* (4/8/16); default 204 (profiles/r01_gemvt_sweep) */
 } ks_option;
 
 /* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL

@@ -115,6 +115,7 @@ struct Options {
     int64_t persistent = 2;   // 0 off, 1 on, 2 auto: persistent cooperative kernels
     int64_t gemv_unroll = 0;  // tuning: K1 LDG unroll (0 = default)
     int64_t persist_grid = 0; // tuning: persistent CTAs (0 = auto)
+    int64_t gemvt_shape = 204; // tuning: K1T vectors/thread/row * 100 + rows in flight
 };
 
 }  // namespace ks

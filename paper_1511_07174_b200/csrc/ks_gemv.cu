@@ -374,44 +374,56 @@ int launch_gemv_f32(const GemvParamsT<float>& p, const Scratch& s, int ticket_id
 // ============================================================================
 namespace {
 
-constexpr int kUT = 8;
-
+// VPT: 16-byte vectors per thread per row (column block = 2 * VPT * NT doubles);
+// UT: rows in flight per thread.
+template <int VPT, int UT>
 __global__ void __launch_bounds__(kNT) k1t_gemv(const double* A, int64_t lda, int64_t m, int64_t n,
                                                const double* x, int64_t rc_rows, int64_t nrc,
                                                double* upart, unsigned* col_ticket, double* out,
                                                Layout L, const int* done) {
+    constexpr int CB = 2 * VPT * kNT;
     __shared__ int s_last;
     if (done && *(volatile const int*)done) return;
-    const int64_t cb = blockIdx.x % (lda / (2 * kNT));
-    const int64_t rc = blockIdx.x / (lda / (2 * kNT));
-    const int64_t col = cb * (2 * kNT) + 2 * threadIdx.x;
+    const int64_t ncb = lda / CB;
+    const int64_t cb = blockIdx.x % ncb;
+    const int64_t rc = blockIdx.x / ncb;
+    const int64_t col0 = cb * CB + 2 * threadIdx.x;     // + v * 2 * kNT
     const int64_t i0 = rc * rc_rows;
     const int64_t i1 = min(m, i0 + rc_rows);
-    const double* a = A + col;
-    double2 acc = make_double2(0.0, 0.0);
+    double2 acc[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) acc[v] = make_double2(0.0, 0.0);
     int64_t i = i0;
-    for (; i + kUT <= i1; i += kUT) {
-        double2 v[kUT];
-        double xi[kUT];
+    for (; i + UT <= i1; i += UT) {
+        double2 a[UT][VPT];
+        double xi[UT];
 #pragma unroll
-        for (int u = 0; u < kUT; ++u) {
-            v[u] = ld_stream(a + (i + u) * lda);
+        for (int u = 0; u < UT; ++u) {
             xi[u] = __ldg(x + i + u);
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) a[u][v] = ld_stream(A + (i + u) * lda + col0 + v * 2 * kNT);
         }
 #pragma unroll
-        for (int u = 0; u < kUT; ++u) {
-            acc.x = fma(v[u].x, xi[u], acc.x);
-            acc.y = fma(v[u].y, xi[u], acc.y);
-        }
+        for (int u = 0; u < UT; ++u)
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) {
+                acc[v].x = fma(a[u][v].x, xi[u], acc[v].x);
+                acc[v].y = fma(a[u][v].y, xi[u], acc[v].y);
+            }
     }
     for (; i < i1; ++i) {
-        const double2 v = ld_stream(a + i * lda);
         const double xi = __ldg(x + i);
-        acc.x = fma(v.x, xi, acc.x);
-        acc.y = fma(v.y, xi, acc.y);
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            const double2 a = ld_stream(A + i * lda + col0 + v * 2 * kNT);
+            acc[v].x = fma(a.x, xi, acc[v].x);
+            acc[v].y = fma(a.y, xi, acc[v].y);
+        }
     }
     if (nrc > 1) {
-        *reinterpret_cast<double2*>(upart + rc * lda + col) = acc;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v)
+            *reinterpret_cast<double2*>(upart + rc * lda + col0 + v * 2 * kNT) = acc[v];
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -422,31 +434,45 @@ __global__ void __launch_bounds__(kNT) k1t_gemv(const double* A, int64_t lda, in
         if (!s_last) return;
         if (threadIdx.x == 0) col_ticket[cb] = 0u;
         __threadfence();
-        acc = make_double2(0.0, 0.0);
-        for (int64_t q = 0; q < nrc; ++q) {
-            const double2 v = __ldcg(reinterpret_cast<const double2*>(upart + q * lda + col));
-            acc.x += v.x;
-            acc.y += v.y;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            double2 sum = make_double2(0.0, 0.0);
+            for (int64_t q = 0; q < nrc; ++q) {
+                const double2 w = __ldcg(reinterpret_cast<const double2*>(upart + q * lda + col0 + v * 2 * kNT));
+                sum.x += w.x;
+                sum.y += w.y;
+            }
+            acc[v] = sum;
         }
     }
-    for (int e = 0; e < 2; ++e) {
-        const int64_t j = col + e;
-        if (j >= n) break;
-        int g = 0;
-        while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
-        out[(int64_t)g * L.chunk + (j - L.row0[g])] = e ? acc.y : acc.x;
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) {
+        for (int e = 0; e < 2; ++e) {
+            const int64_t j = col0 + v * 2 * kNT + e;
+            if (j >= n) break;
+            int g = 0;
+            while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
+            out[(int64_t)g * L.chunk + (j - L.row0[g])] = e ? acc[v].y : acc[v].x;
+        }
     }
 }
 
+int g_k1t_vpt = 2, g_k1t_ut = 4;   // tuning knobs (KS_OPT_GEMVT_SHAPE); sweep best 204
+
 }  // namespace
 
+void set_gemv_t_shape(int vpt, int ut) {
+    g_k1t_vpt = (vpt == 1 || vpt == 2 || vpt == 4) ? vpt : 2;
+    g_k1t_ut = (ut == 4 || ut == 8 || ut == 16) ? ut : 4;
+}
+
 int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms) {
-    const int64_t ncb = lda / (2 * kNT);
+    const int64_t ncb = std::max<int64_t>(1, lda / (2 * g_k1t_vpt * kNT));
     const int64_t target = 6LL * 4 * num_sms;            // ~6 waves of 4 CTAs/SM
     int64_t nrc = (target + ncb - 1) / ncb;
     if (nrc < 1) nrc = 1;
     int64_t rc = (m + nrc - 1) / nrc;
-    rc = std::max<int64_t>(8, (rc + 7) / 8 * 8);
+    rc = std::max<int64_t>(16, (rc + 15) / 16 * 16);
     return rc;
 }
 
@@ -454,11 +480,21 @@ int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const doub
                   int64_t rc_rows, double* upart, unsigned* col_ticket, double* out, const Layout& L,
                   const int* done, cudaStream_t st) {
     if (m <= 0) return 0;
-    const int64_t ncb = lda / (2 * kNT);
+    const int vpt = (lda % (2 * g_k1t_vpt * kNT) == 0) ? g_k1t_vpt : 1;
+    const int64_t ncb = lda / (2 * vpt * kNT);
     const int64_t nrc = (m + rc_rows - 1) / rc_rows;
-    k1t_gemv<<<(unsigned)(ncb * nrc), kNT, 0, st>>>(A, lda, m, n, x, rc_rows, nrc, upart, col_ticket,
-                                                    out, L, done);
-    return 1;
+    const unsigned grid = (unsigned)(ncb * nrc);
+#define K1T_CASE(V, U)                                                                       \
+    if (vpt == V && g_k1t_ut == U) {                                                          \
+        k1t_gemv<V, U><<<grid, kNT, 0, st>>>(A, lda, m, n, x, rc_rows, nrc, upart, col_ticket,  \
+                                            out, L, done);                                     \
+        return 1;                                                                              \
+    }
+    K1T_CASE(1, 4) K1T_CASE(1, 8) K1T_CASE(1, 16)
+    K1T_CASE(2, 4) K1T_CASE(2, 8) K1T_CASE(2, 16)
+    K1T_CASE(4, 4) K1T_CASE(4, 8) K1T_CASE(4, 16)
+#undef K1T_CASE
+    return 0;
 }
 
 }  // namespace ks

@@ -112,6 +112,7 @@ GemvConfig choose_gemv(int64_t m, int64_t ncols, int num_sms, int rows_opt, int 
 // K1T: u = A_loc^T x_loc (BiCG), chunk-layout output; upart holds
 // ceil(m / rc_rows) x lda partials, col_ticket lda / 512 counters.
 int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms);
+void set_gemv_t_shape(int vpt, int ut);   // tuning (process-wide): vectors/thread/row, rows in flight
 int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
                   int64_t rc_rows, double* upart, unsigned* col_ticket, double* out, const Layout& L,
                   const int* done, cudaStream_t st);

@@ -18,6 +18,15 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
+// Persistent GEMV shape: the tuning options if set, else R=4/U=2 for small shards
+// (<= 4096 rows: fewer, fuller tiles; C1 CG 13.4 vs 15.8 us/iteration,
+// profiles/r01_small_sweep.json) and the kernels' default R=2/U=4 above.
+void persist_shape(const ks_ctx* c, const Rank& r, int* rows, int* unroll) {
+    *rows = (int)c->opt.gemv_rows;
+    *unroll = (int)c->opt.gemv_unroll;
+    if (*rows == 0 && *unroll == 0 && r.L.pslot <= 4096) { *rows = 4; *unroll = 2; }
+}
+
 struct Prof {
     ks_ctx* c;
     Rank& r;
@@ -64,8 +73,10 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     const bool persist = c->persistent();
     Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
     int pgrid = 0;
+    int prows = 0, punroll = 0;
     if (persist) {
-        pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, (int)c->opt.gemv_rows, (int)c->opt.gemv_unroll);
+        persist_shape(c, r, &prows, &punroll);
+        pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, prows, punroll);
         if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
     }
     const bool use_graph = !persist && c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
@@ -103,7 +114,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
             prof.pre(slot);
             const int rc = launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
                                           r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
-                                          (int)c->opt.gemv_rows, (int)c->opt.gemv_unroll, r.stream);
+                                          prows, punroll, r.stream);
             prof.post(slot);
             if (rc < 0) KS_CUDA((cudaError_t)(-rc));
             r.launches += 1;
@@ -373,8 +384,10 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
     const int gemvs = bicgstab ? 2 : 1;
     Prof prof(c, r, 1);
-    const int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, (int)c->opt.gemv_rows,
-                                          (int)c->opt.gemv_unroll);
+    int prows = 0, punroll = 0;
+    persist_shape(c, r, &prows, &punroll);
+    int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, prows, punroll);
+    if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
     float* bpart = reinterpret_cast<float*>(r.scr.part + 2 * kPartStride);
     int64_t k = 1, batch = 0;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
@@ -384,8 +397,8 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
         const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
         prof.pre(slot);
         const int rc = launch_persist<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld,
-                                             bpart, r.scr.ticket + 8, k, kend, pgrid, (int)c->opt.gemv_rows,
-                                             (int)c->opt.gemv_unroll, r.stream);
+                                             bpart, r.scr.ticket + 8, k, kend, pgrid, prows, punroll,
+                                             r.stream);
         prof.post(slot);
         if (rc < 0) KS_CUDA((cudaError_t)(-rc));
         r.launches += 1;
