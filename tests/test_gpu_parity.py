@@ -553,3 +553,47 @@ def test_f32_unsupported_calls():
             assert e.value.status == ks.KS_EARG
         x, h, r = ctx.cg(np.zeros(n), tol=1e-5)
         assert r.iterations == 0 and np.all(x == 0)
+
+
+def test_strided_rows_and_tiny_systems():
+    """ks_load_rows with lda > n (strided host rows); n = 1 and n = 2 solves on the
+    default (persistent) path and the multi-kernel path."""
+    n = 300
+    rng = np.random.default_rng(9)
+    big = rng.standard_normal((n, n + 37))
+    A = big[:, :n]
+    x = rng.standard_normal(n)
+    with ks.Context(n) as ctx:
+        L = ks.lib()
+        import ctypes as C
+        assert L.ks_load_rows(ctx._h, 0, n, big.ctypes.data, n + 37) == ks.KS_OK
+        y = ctx.matvec(x)
+    gemv_bound_check(np.ascontiguousarray(A), x, y)
+    for persistent in (0, 1):
+        with ks.Context(1) as ctx:
+            ctx.set_option("persistent", persistent)
+            ctx.load_rows(np.array([[4.0]]))
+            xs, h, r = ctx.cg(np.array([2.0]), tol=1e-12)
+            assert r.converged and r.iterations == 1 and xs[0] == 0.5
+            xs, h, r = ctx.bicgstab(np.array([2.0]), tol=1e-12)
+            assert r.converged and abs(xs[0] - 0.5) <= 1e-15
+        with ks.Context(2) as ctx:
+            ctx.set_option("persistent", persistent)
+            ctx.load_rows(np.array([[2.0, 1.0], [1.0, 3.0]]))
+            xs, h, r = ctx.cg(np.array([1.0, 2.0]), tol=1e-14)
+            assert r.converged and r.iterations <= 2
+            assert np.allclose(xs, [0.2, 0.6], rtol=1e-14)
+
+
+def test_f32_device_buffers():
+    import torch
+    n = 1024
+    A, b = synth.gdd(n, 4)
+    xo, ho, ro = oracle.bicgstab_f32(A, b, tol=1e-5)
+    with ks.Context(n, dtype="f32") as ctx:
+        ctx.load_rows(A)
+        bd = torch.tensor(b.astype(np.float32).astype(np.float64), device="cuda:0")
+        xd = torch.empty(n, dtype=torch.float64, device="cuda:0")
+        _, h, r = ctx.bicgstab(bd, tol=1e-5, out=xd)
+        torch.cuda.synchronize()
+    bars_f32(xd.cpu().numpy(), h, r, xo, ho, ro)
