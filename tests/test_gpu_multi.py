@@ -249,3 +249,50 @@ def test_torchrun_borrowed_comm(tmp_path, P):
     R = res[0]["bs_loaded"]
     Rep.iterations = R["it"]
     bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro, floor=FLOOR_BS)
+
+
+@needs2
+def test_multi_fullsize_65536():
+    """C3/C3' at P = all GPUs (<= 4), default path (persistent + fused): CG vs the
+    closed form and the survey's counts; BiCGSTAB counts/histories and the true
+    residual by the oracle with on-the-fly rows (pins P6, P11, P14 at scale)."""
+    P = min(4, ngpu())
+    n = 65536
+    c = synth.spd_table(n, 1e4)
+    with ks.Context(n, ngpus=P) as ctx:
+        b = ctx.generate("spd", seed=synth.SEED, table=c)
+        x, h, r = ctx.cg(b, tol=1e-10)
+    assert r.converged and abs(r.iterations - 840) <= 2
+    assert np.allclose(h[:3], [0.5745285, 0.4442545, 0.3710058], rtol=5e-7, atol=0)
+    xcf = oracle.spd_exact_solve_ld(c, synth.SEED, b)
+    assert np.linalg.norm(x - xcf) <= 1e4 * 1e-10 * np.linalg.norm(xcf)
+    with ks.Context(n, ngpus=P) as ctx:
+        b = ctx.generate("dd", seed=synth.SEED, kd=16)
+        x, h, r = ctx.bicgstab(b, tol=1e-10)
+    assert r.converged and abs(r.iterations - 23) <= 2
+    assert np.allclose(h[:3], [0.3187527, 0.1602609, 0.08888871], rtol=5e-7, atol=0)
+    op = oracle.Operator(gen=synth.spec("dd", n, kd=16), threads=os.cpu_count() or 1)
+    assert oracle.true_relres_ld(op, b, x) <= 10 * 1e-10
+
+
+@pytest.mark.skipif("ngpu() < 4", reason="needs 4 GPUs (137 GB per GPU)")
+def test_c5_262144_p4():
+    """C5: n = 262144 (550 GB in total, 137 GB per GPU) at P = 4: CG vs the closed
+    form (survey: 1070 iterations); BiCGSTAB converges with a small true residual
+    checked by the oracle on sampled rows (on-the-fly generation)."""
+    n = 262144
+    c = synth.spd_table(n, 1e4)
+    with ks.Context(n, ngpus=4) as ctx:
+        b = ctx.generate("spd", seed=synth.SEED, table=c)
+        x, h, r = ctx.cg(b, tol=1e-10)
+        assert r.converged and abs(r.iterations - 1070) <= 2
+        xcf = oracle.spd_exact_solve_ld(c, synth.SEED, b)
+        assert np.linalg.norm(x - xcf) <= 1e4 * 1e-10 * np.linalg.norm(xcf)
+    with ks.Context(n, ngpus=4) as ctx:
+        b = ctx.generate("dd", seed=synth.SEED, kd=16)
+        x, h, r = ctx.bicgstab(b, tol=1e-10)
+    assert r.converged and r.iterations <= 30 and r.true_relres <= 10 * 1e-10
+    op = oracle.Operator(gen=synth.spec("dd", n, kd=16), threads=min(8, os.cpu_count() or 1))
+    nb = float(np.linalg.norm(b))
+    for i in (0, 1, 131071, 131072, 262143):
+        assert abs(b[i] - op.rows(i, 1, x)[0]) <= 10 * 1e-10 * nb
