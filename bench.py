@@ -343,7 +343,7 @@ def run_ours(args):
             "data": "synthetic (G-SPD kappa=1e4 + G-DD kd=16, seed 151107174, generated on device)",
             "config": {"workload": f"C3/C3': n={n} FP64 dense, CG on G-SPD(1e4) + BiCGSTAB on "
                                    f"G-DD(16), row-block over {world} GPU(s), tol=0 fixed length",
-                       "n": n, "global_batch": 1, "parallelism": f"row-block P={world}",
+                       "n": n, "parallelism": f"row-block P={world}",
                        "collectives": comm_mode,
                        "kernels": "persistent cooperative" if persistent else "one kernel per step",
                        "l2": f"no flush needed: resident inputs {2 * 8 * m * n / 1e9:.1f} GB/GPU "

@@ -269,15 +269,19 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
     // scalars of the previous iteration (written by the previous launch / init)
     T rho_prev = (T)st->rho[(P.k0 - 1) & 3], alpha_prev = (T)st->alpha[(P.k0 - 1) & 3];
     T omega_prev = (T)st->omega[(P.k0 - 1) & 3];
+    T rho_next = T(0), rr_next = T(0);
     for (long long i = P.k0; i <= P.k1; ++i) {
         if (done_flag(st)) break;
         // B8 (test of i-1) + B1
         if (a.peer && i >= 2 && !wait_ph(a, kPhaseR, i - 1)) return;
         const T* Gr = par_ptr(a.G_r, a.gpar, i - 1);
-        const T rho = slots_sum(L, Gr, 0);
+        // P == 1: after the first iteration of a launch the partials are in registers
+        // (every CTA computed them), so no barrier is needed to read the lead's slots
+        const bool carried = !a.peer && i > P.k0;
+        const T rho = carried ? rho_next : slots_sum(L, Gr, 0);
         T rel = T(0);
         if (i >= 2) {
-            rel = sqrt(slots_sum(L, Gr, 1)) / (T)st->nb;
+            rel = sqrt(carried ? rr_next : slots_sum(L, Gr, 1)) / (T)st->nb;
             if (rel <= (T)st->tol) {
                 if (lead()) {
                     hist_put(st, a.hist, i - 2, rel);
@@ -425,9 +429,10 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
         rho_prev = rho;
         alpha_prev = alpha;
         omega_prev = om;
-        // the slots written by the lead are read at the top of the next
-        // iteration: one more barrier (P == 1) or the R flags (fused)
-        if (!a.peer && !grid_sync(P.bar, st)) return;
+        rho_next = rv[0];
+        rr_next = rv[1];
+        // fused: the next iteration waits on the R flags; P == 1: the values are
+        // carried in registers and the lead's slots are read only by the next launch
     }
 }
 
