@@ -2,6 +2,7 @@
 // before any work, converts internal exceptions to ks_status + message, and
 // poisons the context on CUDA/NCCL/allocation errors.
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
