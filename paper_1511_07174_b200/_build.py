@@ -87,5 +87,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_example() -> str:
+    """examples/ks_example: a plain C program against include/ks.h + libks.so."""
+    src = os.path.join(ROOT, "examples", "ks_example.c")
+    exe = os.path.join(ROOT, "examples", "ks_example")
+    if not os.path.exists(src):
+        return ""
+    subprocess.run(["gcc", "-O2", "-std=c11", "-Wall", "-I", os.path.join(ROOT, "include"), src, "-o", exe,
+                    "-L", HERE, "-lks", f"-Wl,-rpath,{HERE}", "-lm"], check=True)
+    return exe
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -76,3 +76,10 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(root, f)).read()
                 assert "import oracle" not in txt and "ks_oracle" not in txt, f
                 assert "from oracle" not in txt, f
+
+
+def test_c_example_links_against_the_abi():
+    """examples/ks_example.c builds against include/ks.h + libks.so with plain gcc."""
+    from paper_1511_07174_b200 import _build
+    exe = _build.build_example()
+    assert os.path.exists(exe)

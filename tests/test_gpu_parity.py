@@ -597,3 +597,15 @@ def test_f32_device_buffers():
         _, h, r = ctx.bicgstab(bd, tol=1e-5, out=xd)
         torch.cuda.synchronize()
     bars_f32(xd.cpu().numpy(), h, r, xo, ho, ro)
+
+
+def test_c_example_runs():
+    """The ABI from C (no Python in the solve path): examples/ks_example."""
+    import subprocess
+    from paper_1511_07174_b200 import _build
+    exe = _build.build_example()
+    out = subprocess.run([exe, "4096"], capture_output=True, text=True, check=True, timeout=120).stdout
+    d = json.loads(out.strip().splitlines()[-1])
+    assert d["bicgstab"]["converged"] == 1 and abs(d["bicgstab"]["iterations"] - 30) <= 2   # App. A.8
+    assert d["bicgstab"]["true_relres"] <= 1e-9
+    assert d["cg"]["converged"] == 1 and d["cg"]["true_relres"] <= 1e-10
