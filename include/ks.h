@@ -199,6 +199,9 @@ ks_status ks_gmres(ks_ctx* ctx, const double* b, const double* x0, double tol, i
 /* y = A^T x (n doubles each): the transposed GEMV building block of BiCG (K1T). */
 ks_status ks_matvec_t(ks_ctx* ctx, const double* x, double* y);
 
+/* Options select kernels / schedules.  In a multi-process job (ks_create_rank)
+ * every rank must set the same options before the same calls: the ranks run one
+ * schedule in lockstep (collectives, epoch flags, persistent grid sizes).        */
 ks_status ks_set_option(ks_ctx* ctx, ks_option opt, int64_t value);
 ks_status ks_get_option(const ks_ctx* ctx, ks_option opt, int64_t* value);
 

@@ -1,0 +1,232 @@
+// NEXT-3 + NEXT-2: one restart cycle of GMRES(m) as one persistent
+// cooperative kernel (P = 1).  Same arithmetic as the multi-kernel path
+// (ks_gmres.cu): CGS2 Arnoldi, Givens rotations, x += V y at the cycle end; grid
+// barriers replace the ~6 kernel boundaries of every Arnoldi step.  Every CTA
+// keeps the running least-squares entry g_j and the convergence decision in
+// registers (identical everywhere: computed from the same totals), the lead CTA
+// records H, cs, sn, g and the history for the back substitution and the host.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ks_persist.cuh"
+
+namespace ks {
+
+namespace {
+
+using namespace pk;
+
+struct GPArgs {
+    PersistArgs<double> P;   // a, A, lda, ncols, bpart (grid x 4), bar
+    GmresArgs g;             // V, ldv, mres, H, cs, sn, g, hx (totals), part (grid x kMaxBasis)
+};
+
+__device__ __forceinline__ double* Vc(const GmresArgs& g, int i) { return g.V + (int64_t)i * g.ldv; }
+
+// CTA partials of <V_i, w>, i < nv -> part[blockIdx * kMaxBasis + i] (8 vectors per pass).
+__device__ void cta_dots(const GmresArgs& g, const double* w, int64_t m, int nv, double* red) {
+    for (int i0 = 0; i0 < nv; i0 += 8) {
+        double acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+        for (int64_t e = blockIdx.x * (int64_t)kNT + threadIdx.x; e < m; e += (int64_t)gridDim.x * kNT) {
+            const double we = w[e];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (i0 + q < nv) acc[q] = fma(Vc(g, i0 + q)[e], we, acc[q]);
+        }
+        block_sum<kNT, 8>(acc, red);
+        if (threadIdx.x == 0)
+            for (int q = 0; q < 8 && i0 + q < nv; ++q) g.part[(int64_t)blockIdx.x * kMaxBasis + i0 + q] = acc[q];
+    }
+}
+
+// CTA i (< nv) sums part[*][i] over CTAs in CTA order -> tot[i].
+__device__ void reduce_dots(const GmresArgs& g, int nv, double* red) {
+    if ((int)blockIdx.x >= nv) return;
+    double acc[1] = {0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kNT)
+        acc[0] += __ldcg(g.part + (int64_t)b * kMaxBasis + blockIdx.x);
+    block_sum<kNT, 1>(acc, red);
+    if (threadIdx.x == 0) g.hx[blockIdx.x] = acc[0];
+}
+
+template <int kR, int kU>
+__global__ void __launch_bounds__(kNT, 4) k_gm_cycle(GPArgs A) {
+    __shared__ double red[8 * kNW];
+    __shared__ double h1[kMaxBasis], h2[kMaxBasis];
+    __shared__ double s_rel, s_hn;
+    const VecArgs& a = A.P.a;
+    const GmresArgs& g = A.g;
+    const Layout& L = a.L;
+    DevState* st = a.st;
+    if (done_flag(st)) return;
+    const int64_t m = m_of(L);
+    const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x, gstride = (int64_t)gridDim.x * kNT;
+    long long k = *(volatile const long long*)&st->iters;   // inner steps completed so far
+    const long long maxit = st->maxit;
+    const double nb = st->nb, tol = st->tol;
+    // ---- cycle start: r = b - A x, beta, v_0 = r / beta, g = beta e_1
+    for (int64_t i = tid0; i < m; i += gstride) a.s_full[i] = a.x_loc[i];
+    if (!grid_sync(A.P.bar, st)) return;
+    double d1, d2;
+    gemv_phase<kR, kU>(A.P, a.s_full, a.q_loc, (const double*)nullptr, d1, d2, red, a.b_full);
+    if (threadIdx.x == 0) A.P.bpart[blockIdx.x * 4 + 1] = d2;
+    if (!grid_sync(A.P.bar, st)) return;
+    double bt[1];
+    grid_total<1>(A.P.bpart, 1, bt, red);
+    const double beta = sqrt(bt[0]);
+    if (beta / nb <= tol || k >= maxit) {
+        if (lead()) {
+            st->relres = beta / nb;
+            if (beta / nb <= tol) { st->converged = 1; st->status = KS_OK; }
+            else st->status = KS_EMAXIT;
+            st->done = 1;
+        }
+        return;
+    }
+    for (int64_t i = tid0; i < m; i += gstride) {
+        const double v = a.q_loc[i] / beta;
+        Vc(g, 0)[i] = v;
+        a.p_full[i] = v;
+    }
+    double gcur = beta;                      // running g_j (same in every CTA)
+    int jd = 0;
+    bool conv = false;
+    if (!grid_sync(A.P.bar, st)) return;
+    for (int j = 0; j < g.mres && k < maxit; ++j) {
+        const int nv = j + 1;
+        gemv_phase<kR, kU>(A.P, a.p_full, a.q_loc, (const double*)nullptr, d1, d2, red);   // w = A v_j
+        if (!grid_sync(A.P.bar, st)) return;
+        cta_dots(g, a.q_loc, m, nv, red);                                 // CGS pass 1
+        if (!grid_sync(A.P.bar, st)) return;
+        reduce_dots(g, nv, red);
+        if (!grid_sync(A.P.bar, st)) return;
+        if (threadIdx.x < nv) h1[threadIdx.x] = __ldcg(g.hx + threadIdx.x);
+        __syncthreads();
+        for (int64_t e = tid0; e < m; e += gstride) {                     // w -= V h1
+            double we = a.q_loc[e];
+            for (int i = 0; i < nv; ++i) we = fma(-h1[i], Vc(g, i)[e], we);
+            a.q_loc[e] = we;
+        }
+        cta_dots(g, a.q_loc, m, nv, red);                                 // CGS pass 2 (same elements,
+        if (!grid_sync(A.P.bar, st)) return;                              //  same thread: no race)
+        reduce_dots(g, nv, red);
+        if (!grid_sync(A.P.bar, st)) return;
+        if (threadIdx.x < nv) h2[threadIdx.x] = __ldcg(g.hx + threadIdx.x);
+        __syncthreads();
+        double nacc[1] = {0.0};
+        for (int64_t e = tid0; e < m; e += gstride) {                     // w -= V h2, ||w||^2
+            double we = a.q_loc[e];
+            for (int i = 0; i < nv; ++i) we = fma(-h2[i], Vc(g, i)[e], we);
+            a.q_loc[e] = we;
+            nacc[0] = fma(we, we, nacc[0]);
+        }
+        block_sum<kNT, 1>(nacc, red);
+        if (threadIdx.x == 0) A.P.bpart[blockIdx.x * 4 + 0] = nacc[0];
+        if (!grid_sync(A.P.bar, st)) return;
+        double nt[1];
+        grid_total<1>(A.P.bpart, 0, nt, red);
+        const double hn = sqrt(nt[0]);
+        if (hn != 0.0) {
+            for (int64_t e = tid0; e < m; e += gstride) {
+                const double v = a.q_loc[e] / hn;
+                Vc(g, j + 1)[e] = v;
+                a.p_full[e] = v;
+            }
+        }
+        if (threadIdx.x == 0) {            // Givens on column j (every CTA, identical)
+            const int mr = g.mres;
+            double col[kMaxBasis];
+            for (int i = 0; i < nv; ++i) col[i] = h1[i] + h2[i];
+            for (int i = 0; i < j; ++i) {
+                const double c = __ldcg(g.cs + i), s = __ldcg(g.sn + i);
+                const double x0 = col[i], x1 = col[i + 1];
+                col[i] = c * x0 + s * x1;
+                col[i + 1] = -s * x0 + c * x1;
+            }
+            const double den = sqrt(col[j] * col[j] + hn * hn);
+            const double cj = col[j] / den, sj = hn / den;
+            const double gj1 = -sj * gcur;
+            const double gj = cj * gcur;
+            s_rel = fabs(gj1) / nb;
+            s_hn = hn;
+            if (blockIdx.x == 0) {
+                for (int i = 0; i < j; ++i) g.H[(int64_t)i * mr + j] = col[i];
+                g.H[(int64_t)j * mr + j] = den;
+                g.H[(int64_t)(j + 1) * mr + j] = 0.0;
+                g.cs[j] = cj;
+                g.sn[j] = sj;
+                g.g[j] = gj;
+                g.g[j + 1] = gj1;
+                if (a.hist && k < st->hist_cap) a.hist[k] = s_rel;
+                st->relres = s_rel;
+                st->iters = k + 1;
+            }
+            red[0] = gj1;
+        }
+        __syncthreads();
+        gcur = red[0];
+        ++k;
+        jd = j + 1;
+        conv = s_rel <= tol || s_hn == 0.0;
+        if (conv || j + 1 == g.mres || k >= maxit) break;
+        if (!grid_sync(A.P.bar, st)) return;
+    }
+    if (!grid_sync(A.P.bar, st)) return;   // H, g complete
+    // ---- cycle end: y = H^{-1} g (every CTA), x += V y
+    __shared__ double y[kMaxBasis];
+    if (threadIdx.x == 0) {
+        const int mr = g.mres;
+        for (int i = jd - 1; i >= 0; --i) {
+            double s = __ldcg(g.g + i);
+            for (int l = i + 1; l < jd; ++l) s -= __ldcg(g.H + (int64_t)i * mr + l) * y[l];
+            y[i] = s / __ldcg(g.H + (int64_t)i * mr + i);
+        }
+    }
+    __syncthreads();
+    for (int64_t e = tid0; e < m; e += gstride) {
+        double xe = a.x_loc[e];
+        for (int i = 0; i < jd; ++i) xe = fma(y[i], Vc(g, i)[e], xe);
+        a.x_loc[e] = xe;
+    }
+    if (lead()) {
+        if (conv) { st->converged = 1; st->status = KS_OK; st->done = 1; }
+        else if (k >= maxit) { st->status = KS_EMAXIT; st->done = 1; }
+    }
+}
+
+}  // namespace
+
+int launch_gm_cycle_persist(const GmresArgs& g, const double* A, int64_t lda, int64_t ncols, double* bpart,
+                            unsigned* bar, int grid, cudaStream_t st) {
+    GPArgs args;
+    args.P.a = g.a;
+    args.P.A = A;
+    args.P.lda = lda;
+    args.P.ncols = ncols;
+    args.P.bpart = bpart;
+    args.P.bar = bar;
+    args.P.k0 = 0;
+    args.P.k1 = 0;
+    args.g = g;
+    void* params[] = {&args};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_gm_cycle<2, 4>, dim3((unsigned)grid), dim3(kNT),
+                                                params, 0, st);
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+int gm_persist_grid(int num_sms, int64_t m) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_gm_cycle<2, 4>, kNT, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t cap = (int64_t)per_sm * num_sms;
+    const int64_t tiles = (m + 1) / 2;
+    int64_t gsz = tiles < num_sms ? num_sms : tiles;
+    if (gsz > cap) gsz = cap;
+    if (gsz < kMaxBasis) gsz = kMaxBasis;      // one CTA per basis vector in reduce_dots
+    return (int)gsz;
+}
+
+}  // namespace ks

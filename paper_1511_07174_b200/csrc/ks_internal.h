@@ -199,6 +199,10 @@ int launch_gm_orth(const GmresArgs& g, int j, int pass, cudaStream_t st);
 int launch_gm_step_end(const GmresArgs& g, int j, long long k, cudaStream_t st);
 int launch_gm_vfull(const GmresArgs& g, cudaStream_t st);
 int launch_gm_cycle_end(const GmresArgs& g, long long k_enqueued, cudaStream_t st);
+// one restart cycle as one persistent cooperative kernel (P = 1; ks_gmres_persist.cu)
+int launch_gm_cycle_persist(const GmresArgs& g, const double* A, int64_t lda, int64_t ncols, double* bpart,
+                            unsigned* bar, int grid, cudaStream_t st);
+int gm_persist_grid(int num_sms, int64_t m);
 
 // BiCG (NEXT-3)
 int launch_bicg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,

@@ -1,0 +1,167 @@
+// Building blocks of the persistent cooperative kernels (ks_persist.cu for CG /
+// BiCGSTAB, ks_gmres_persist.cu for GMRES): grid barrier, CTA-order totals,
+// fused-exchange flag helpers, and the GEMV phase (K1's streaming loop over
+// round-robin tiles).  Everything is deterministic: fixed tile -> CTA
+// assignment, CTA partials summed in CTA order by a fixed tree.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ks_device.cuh"
+#include "ks_internal.h"
+#include "ks_tile.cuh"
+
+namespace ks {
+namespace pk {
+namespace {
+
+constexpr int kNT = 256;
+constexpr int kNW = kNT / 32;
+// GEMV tile shape of the persistent kernels (rows R x unrolled column blocks U);
+// instantiated for the shapes the tuning sweep found at the streaming ceiling.
+
+// -- small helpers (the same conventions as ks_vec.cu) ------------------------
+__device__ __forceinline__ int64_t m_of(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
+__device__ __forceinline__ int64_t gidx_p(const Layout& L, int64_t j, int* owner) {
+    int g = 0;
+    while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
+    *owner = g;
+    return (int64_t)g * L.chunk + (j - L.row0[g]);
+}
+template <class T>
+__device__ __forceinline__ T* par_ptr(T* G, int64_t par, long long k) { return G + (k & 1) * par; }
+__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
+__device__ __forceinline__ bool done_flag(const DevState* st) { return *(volatile const int*)&st->done != 0; }
+__device__ __forceinline__ unsigned long long epoch(const DevState* st, long long k) {
+    return *(volatile const unsigned long long*)&st->ebase + (unsigned long long)k;
+}
+template <class T>
+__device__ __forceinline__ T slots_sum(const Layout& L, const T* G, int q) {
+    T s = T(0);
+    for (int g = 0; g < L.P; ++g) s += G[(int64_t)g * L.chunk + L.pslot + q];
+    return s;
+}
+template <class T>
+__device__ __forceinline__ T scal_sum(const Layout& L, const T* S, int q) {
+    T s = T(0);
+    for (int g = 0; g < L.P; ++g) s += S[g * kScalSlot + q];
+    return s;
+}
+__device__ __forceinline__ void hist_put(DevState* st, double* hist, long long k1, double v) {
+    if (hist && k1 >= 0 && k1 < st->hist_cap) hist[k1] = v;
+}
+
+// Grid-wide barrier (all CTAs co-resident: cooperative launch).  Generation
+// counter: the last arriver resets the count and releases the next generation.
+// Bounded spin: a timeout marks the solve failed instead of hanging.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ bool grid_sync(unsigned* bar, DevState* st) {
+    __shared__ int s_ok;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        unsigned* cnt = bar;
+        unsigned* gen = bar + 1;
+        const unsigned g0 = ld_acquire_gpu(gen);
+        __threadfence();
+        const unsigned arrived = atomicAdd(cnt, 1u) + 1u;
+        if (arrived == gridDim.x) {
+            atomicExch(cnt, 0u);
+            __threadfence();
+            st_release_gpu(gen, g0 + 1u);
+        } else {
+            const unsigned long long t0 = globaltimer_ns();
+            while (ld_acquire_gpu(gen) == g0) {
+                if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                    ok = 0;
+                    st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1;
+                    break;
+                }
+            }
+        }
+        s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+// Sum over CTAs (in CTA order, fixed tree) of slot q of the per-CTA partials;
+// every CTA computes the same value.
+template <int K, class T>
+__device__ __forceinline__ void grid_total(const T* bpart, int q0, T (&out)[K], T* red) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        T acc = T(0);
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kNT) acc += __ldcg(bpart + (int64_t)b * 4 + q0 + k);
+        out[k] = acc;
+    }
+    block_sum<kNT, K>(out, red);
+}
+
+// Fused-mode wait for phase ph of iteration k from every rank (all CTAs).
+template <class T>
+__device__ __forceinline__ bool wait_ph(const VecArgsT<T>& a, int ph, long long k) {
+    const bool ok = wait_flags(a.flags + ph * kMaxRanks, a.L.P, epoch(a.st, k));
+    if (!ok && threadIdx.x == 0) { a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1; }
+    return ok;
+}
+template <class T>
+__device__ __forceinline__ void flags_out(const VecArgsT<T>& a, int ph, long long k) {
+    unsigned long long* f[kMaxRanks];
+    for (int g = 0; g < a.L.P; ++g) f[g] = a.pp.flags[g] + ph * kMaxRanks + a.L.rank;
+    publish_flags(f, a.L.P, epoch(a.st, k));
+}
+
+template <class T>
+struct PersistArgs {
+    VecArgsT<T> a;
+    const T* A;
+    int64_t lda, ncols;
+    T* bpart;           // gridDim.x * 4
+    unsigned* bar;      // {count, generation}
+    long long k0, k1;   // iteration range of this launch (inclusive)
+};
+
+// GEMV phase: y = A_loc x (or bsub - A_loc x) over the tiles of this CTA
+// (round-robin); thread 0 returns the CTA's partials <w1, y> and <y, y>
+// accumulated in tile order.
+template <int kR, int kU, class T>
+__device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w1, T& d1, T& d2,
+                           T* red, const T* bsub = nullptr) {
+    const int64_t m = m_of(P.a.L);
+    const int64_t tiles = (m + kR - 1) / kR;
+    const int64_t ncb = P.ncols / (Vec16<T>::W * kNT);
+    d1 = T(0);
+    d2 = T(0);
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t r0 = tile * kR;
+        const int nvalid = (int)min((int64_t)kR, m - r0);
+        T acc[kR];
+        stream_rows<kR, kU, kNT>(P.A, P.lda, r0, nvalid, x, 0, ncb, acc);
+        block_sum<kNT, kR>(acc, red);
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                if (r < nvalid) {
+                    const T yv = bsub ? bsub[r0 + r] - acc[r] : acc[r];
+                    y[r0 + r] = yv;
+                    if (w1) d1 = fma(w1[r0 + r], yv, d1);
+                    d2 = fma(yv, yv, d2);
+                }
+            }
+        }
+    }
+}
+
+
+}  // namespace
+}  // namespace pk
+}  // namespace ks

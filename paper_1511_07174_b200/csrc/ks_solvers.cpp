@@ -533,6 +533,37 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
     Prof prof(c, r, restart + 1);
     int64_t k = 0, cycle = 0;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+    if (c->P == 1 && c->opt.persistent != 0) {
+        // NEXT-2 for GMRES: one persistent cooperative kernel per restart cycle
+        const int grid = gm_persist_grid(r.num_sms, r.m);
+        const int64_t max_cycles = maxit / restart + 2;
+        for (cycle = 0; cycle < max_cycles; ++cycle) {
+            const int slot = (int)(cycle & 1);
+            prof.begin(slot);
+            prof.pre(slot);
+            const int rc = launch_gm_cycle_persist(g, r.A, c->ld, c->ld, r.scr.part + 2 * kPartStride,
+                                                   r.scr.ticket + 8, grid, r.stream);
+            prof.post(slot);
+            if (rc < 0) KS_CUDA((cudaError_t)(-rc));
+            r.launches += 1;
+            KS_CUDA(cudaMemcpyAsync(&r.h_done[slot], &r.st->done, sizeof(int), cudaMemcpyDeviceToHost, r.stream));
+            KS_CUDA(cudaEventRecord(r.ev_poll[slot], r.stream));
+            if (cycle >= 1) {
+                KS_CUDA(cudaEventSynchronize(r.ev_poll[slot ^ 1]));
+                prof.harvest(slot ^ 1);
+                if (r.h_done[slot ^ 1]) break;
+            }
+        }
+        KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+        KS_CUDA(cudaStreamSynchronize(r.stream));
+        prof.harvest(0);
+        prof.harvest(1);
+        KS_CUDA(cudaMemcpy(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost));
+        r.gemv_launches = r.h_state->iters;
+        r.launches += launch_cg_finish(a, r.stream);
+        finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+        return r.h_state->status;
+    }
     while (true) {
         const int slot = (int)(cycle & 1);
         prof.begin(slot);

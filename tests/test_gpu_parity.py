@@ -432,15 +432,17 @@ def test_bicg_edges_and_spd_equivalence():
 
 # -------------------------------------------------------------- NEXT-3: GMRES(m)
 
+@pytest.mark.parametrize("persistent", [0, 1])
 @pytest.mark.parametrize("n,kd,m", [(1024, 4, 30), (1024, 16, 30), (1024, 16, 5), (4096, 16, 30),
                                     (300, 4, 63)])
-def test_gmres_parity(n, kd, m):
+def test_gmres_parity(n, kd, m, persistent):
     """GPU GMRES(m) (CGS2 Arnoldi) vs the oracle (MGS Arnoldi): same Krylov basis in
     exact arithmetic; north-star bars on x, the implicit-residual history and the
     inner-step count; restarts included (m = 5)."""
     A, b = synth.gdd(n, kd)
     xo, ho, ro = oracle.gmres(A, b, tol=1e-10, restart=m)
     with ks.Context(n) as ctx:
+        ctx.set_option("persistent", persistent)
         ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
         x, h, r = ctx.gmres(b, tol=1e-10, restart=m)
         x2, h2, r2 = ctx.gmres(b, tol=1e-10, restart=m)
@@ -450,10 +452,12 @@ def test_gmres_parity(n, kd, m):
     assert r2.iterations == r.iterations and np.array_equal(x, x2) and np.array_equal(h, h2)
 
 
-def test_gmres_edges():
+@pytest.mark.parametrize("persistent", [0, 1])
+def test_gmres_edges(persistent):
     n = 200
     A, b = synth.gdd(n, 4, seed=synth.SEED2)
     with ks.Context(n) as ctx:
+        ctx.set_option("persistent", persistent)
         ctx.load_rows(A)
         x, h, r = ctx.gmres(np.zeros(n), tol=1e-10)
         assert r.converged and r.iterations == 0 and np.all(x == 0)
