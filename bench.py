@@ -38,6 +38,12 @@ SEED = 151107174
 NOMINAL_HBM = 8000.0   # GB/s, north star's "~8 TB/s"
 
 
+def workload(n: int) -> str:
+    """The measured problem, identical in both arms (ours and --impl reference)."""
+    return (f"C3/C3': n={n} FP64 dense, CG on G-SPD(kappa=1e4) + BiCGSTAB on G-DD(kd=16), "
+            f"seed 151107174, tol=0 fixed length, 1 step = 1 CG + 1 BiCGSTAB iteration")
+
+
 def env_int(k, d):
     return int(os.environ.get(k, d))
 
@@ -181,8 +187,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / cpu["value"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C3: n={n} FP64 dense; CG on G-SPD(1e4) + BiCGSTAB on G-DD(16)",
-                       "n": n, "parallelism": "cpu oracle, rank 0 only"},
+            "config": {"workload": workload(n), "n": n,
+                       "parallelism": "CPU oracle on the host cores, rank 0 only"},
             "cpu_baseline": cpu,
             "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -341,9 +347,8 @@ def run_ours(args):
             "warmup": W, "ms_per_step": 1e3 * sec / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (G-SPD kappa=1e4 + G-DD kd=16, seed 151107174, generated on device)",
-            "config": {"workload": f"C3/C3': n={n} FP64 dense, CG on G-SPD(1e4) + BiCGSTAB on "
-                                   f"G-DD(16), row-block over {world} GPU(s), tol=0 fixed length",
-                       "n": n, "parallelism": f"row-block P={world}",
+            "config": {"workload": workload(n), "n": n,
+                       "parallelism": f"row-block over {world} GPU(s) (P={world})",
                        "collectives": comm_mode,
                        "kernels": "persistent cooperative" if persistent else "one kernel per step",
                        "l2": f"no flush needed: resident inputs {2 * 8 * m * n / 1e9:.1f} GB/GPU "
