@@ -15,5 +15,4 @@ CMD="python bench.py --steps 16 --warmup 3 --no-cpu-baseline"
 export CUDA_VISIBLE_DEVICES=0
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-timeout 300 $CMD > gpurun_out/plain2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:persist -s 2 -c 1 -o gpurun_out/prof_persist $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+# (one ncu per call: the --set full capture runs in its own call)
