@@ -1,4 +1,4 @@
-"""Multi-rank host logic on CPU (world size 2, gloo, 127.0.0.1).
+"""Multi-rank host logic on CPU (world sizes 2 and 8, gloo, 127.0.0.1).
 
 The CUDA path's N > 1 schedule is: row-block partition
 (`ks.partition` == ks_row_range), gather buffers in chunk layout whose tail slots
@@ -11,6 +11,7 @@ numpy; the collectives by torch.distributed over gloo) and checks
   * row-sharded generation reassembles the full matrix bitwise.
 """
 import os
+import queue
 import socket
 
 import numpy as np
@@ -153,24 +154,33 @@ def _worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [256, 1000])
-def test_two_rank_schedule_gloo(n):
+@pytest.mark.parametrize("world,n", [(2, 256), (2, 1000), (8, 1002)])
+def test_multi_rank_schedule_gloo(world, n):
+    """world = 8 is the driver's largest scaling run; n = 1002 gives ragged shards."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    res = []
+    while len(res) < world:                     # fail fast if a worker dies
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"worker exited with {dead}"
+    res.sort(key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    r0, r1 = res
-    for a, b in zip(r0[1:], r1[1:]):          # identical decisions and results on both ranks
-        if isinstance(a, np.ndarray):
-            assert np.array_equal(a, b)
-        else:
-            assert a == b
+    r0 = res[0]
+    for rr in res[1:]:                          # identical decisions and results on every rank
+        for a, b in zip(r0[1:], rr[1:]):
+            if isinstance(a, np.ndarray):
+                assert np.array_equal(a, b)
+            else:
+                assert a == b
     A, c, b = synth.gspd(n, 1e3)
     xo, ho, ro = oracle.cg(A, b, tol=1e-10)
     _, x, h, k = r0[0], r0[1], r0[2], r0[3]
