@@ -121,9 +121,16 @@ typedef enum {
                               /* the default for the row count)                   */
     KS_OPT_PERSIST_GRID = 10, /* tuning: cap on the persistent kernels' CTA count */
                               /* (0 = auto; the grid must be equal on all ranks)  */
-    KS_OPT_GEMVT_SHAPE = 11   /* tuning (process-wide): K1T 16-byte vectors per   */
+    KS_OPT_GEMVT_SHAPE = 11,  /* tuning (process-wide): K1T 16-byte vectors per   */
                               /* thread per row (1/2/4) * 100 + rows in flight    */
                               /* (4/8/16); default 204 (profiles/r01_gemvt_sweep) */
+    KS_OPT_SMALL = 12         /* CG / BiCGSTAB on one GPU with the persistent     */
+                              /* path: 1 = small-n kernels that keep the full     */
+                              /* vectors in every CTA's shared memory (1 grid     */
+                              /* barrier per CG iteration, 2 per BiCGSTAB one)    */
+                              /* when they fit; 0 = off; 2 (default) = auto (on   */
+                              /* when a vector is <= 32 KiB: FP64 n <= 4096, FP32 */
+                              /* n <= 8192)                                       */
 } ks_option;
 
 /* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL

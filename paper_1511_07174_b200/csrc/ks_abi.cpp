@@ -503,6 +503,9 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
         case KS_OPT_GEMVT_SHAPE:
             ks::set_gemv_t_shape((int)(v / 100), (int)(v % 100));
             o.gemvt_shape = v; break;
+        case KS_OPT_SMALL:
+            if (v < 0 || v > 2) return fail(c, KS_EARG, "small must be 0, 1 or 2");
+            o.small = v; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -524,6 +527,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_GEMV_UNROLL: *v = o.gemv_unroll; break;
         case KS_OPT_PERSIST_GRID: *v = o.persist_grid; break;
         case KS_OPT_GEMVT_SHAPE: *v = o.gemvt_shape; break;
+        case KS_OPT_SMALL: *v = o.small; break;
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

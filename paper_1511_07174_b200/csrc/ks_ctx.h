@@ -116,6 +116,7 @@ struct Options {
     int64_t gemv_unroll = 0;  // tuning: K1 LDG unroll (0 = default)
     int64_t persist_grid = 0; // tuning: persistent CTAs (0 = auto)
     int64_t gemvt_shape = 204; // tuning: K1T vectors/thread/row * 100 + rows in flight
+    int64_t small = 2;        // 0 off, 1 on, 2 auto: small-n shared-memory kernels (P == 1)
 };
 
 }  // namespace ks
@@ -143,6 +144,9 @@ struct ks_ctx {
         return opt.persistent == 1 || n <= kPersistAutoMaxN;
     }
     static constexpr int64_t kPersistAutoMaxN = 1LL << 62;   // tuned from measurements
+    // small-n kernels on when a full vector is <= 32 KiB (FP64 n <= 4096, FP32 n <= 8192):
+    // the crossover measured in profiles/r01_small_path.json
+    static constexpr int64_t kSmallAutoMaxBytes = 32768;
 };
 
 namespace ks {

@@ -27,6 +27,16 @@ void persist_shape(const ks_ctx* c, const Rank& r, int* rows, int* unroll) {
     if (*rows == 0 && *unroll == 0 && r.L.pslot <= 4096) { *rows = 4; *unroll = 2; }
 }
 
+// Grid of the small-n shared-memory kernels (ks_small.cu), 0 = not used.
+template <class T>
+int small_path_grid(const ks_ctx* c, const Rank& r, int bicgstab) {
+    if (c->P != 1 || c->opt.small == 0) return 0;
+    if (c->opt.small == 2 && c->n * (int64_t)c->esz > ks_ctx::kSmallAutoMaxBytes) return 0;
+    int g = small_grid<T>(bicgstab, r.num_sms, c->n, c->ld);
+    if (g > 0 && c->opt.persist_grid > 0) g = (int)std::min<int64_t>(g, c->opt.persist_grid);
+    return g;
+}
+
 struct Prof {
     ks_ctx* c;
     Rank& r;
@@ -72,9 +82,10 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
     const bool persist = c->persistent();
     Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
-    int pgrid = 0;
+    int pgrid = 0, sgrid = 0;
     int prows = 0, punroll = 0;
-    if (persist) {
+    if (persist) sgrid = small_path_grid<double>(c, r, kind);
+    if (persist && sgrid == 0) {
         persist_shape(c, r, &prows, &punroll);
         pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, prows, punroll);
         if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
@@ -112,9 +123,12 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
         if (persist) {                                    // one cooperative launch per batch
             const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
             prof.pre(slot);
-            const int rc = launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
-                                          r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
-                                          prows, punroll, r.stream);
+            const int rc = sgrid > 0
+                ? launch_small<double>(kind, r.vargs(false), r.A, c->ld, c->ld, r.scr.part + 2 * kPartStride,
+                                       r.scr.ticket + 8, k, kend, sgrid, r.stream)
+                : launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
+                                         r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
+                                         prows, punroll, r.stream);
             prof.post(slot);
             if (rc < 0) KS_CUDA((cudaError_t)(-rc));
             r.launches += 1;
@@ -388,6 +402,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     persist_shape(c, r, &prows, &punroll);
     int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, prows, punroll);
     if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
+    const int sgrid = small_path_grid<float>(c, r, bicgstab);
     float* bpart = reinterpret_cast<float*>(r.scr.part + 2 * kPartStride);
     int64_t k = 1, batch = 0;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
@@ -396,9 +411,11 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
         prof.begin(slot);
         const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
         prof.pre(slot);
-        const int rc = launch_persist<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld,
-                                             bpart, r.scr.ticket + 8, k, kend, pgrid, prows, punroll,
-                                             r.stream);
+        const int rc = sgrid > 0
+            ? launch_small<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld, bpart,
+                                  r.scr.ticket + 8, k, kend, sgrid, r.stream)
+            : launch_persist<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld,
+                                    bpart, r.scr.ticket + 8, k, kend, pgrid, prows, punroll, r.stream);
         prof.post(slot);
         if (rc < 0) KS_CUDA((cudaError_t)(-rc));
         r.launches += 1;

@@ -39,8 +39,9 @@ template <> struct Vec16<float> { using type = float4; static constexpr int W = 
 // thread t owns columns 2t + 2*NT*cb (128-bit loads, 512 contiguous bytes of one
 // row per warp instruction).  U column blocks are unrolled so U*R independent
 // 16-byte loads are in flight per thread.  Rows >= nvalid re-read the last valid
-// row (tail tile) and are discarded by the caller.
-template <int R, int U, int NT, class T>
+// row (tail tile) and are discarded by the caller.  kXS: x lives in shared memory
+// (the small-n kernels, ks_small.cu) instead of global memory.
+template <int R, int U, int NT, class T, bool kXS = false>
 __device__ __forceinline__ void stream_rows(const T* A, int64_t lda, int64_t r0, int nvalid,
                                             const T* x, int64_t cb0, int64_t cb1, T (&acc)[R]) {
     using V = typename Vec16<T>::type;
@@ -59,7 +60,7 @@ __device__ __forceinline__ void stream_rows(const T* A, int64_t lda, int64_t r0,
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t c = (cb + u) * (W * NT);
-            xv[u] = ld_x(xp + c);
+            xv[u] = kXS ? *reinterpret_cast<const V*>(xp + c) : ld_x(xp + c);
 #pragma unroll
             for (int r = 0; r < R; ++r) av[u][r] = ld_stream(base + roff[r] + c);
         }
@@ -71,7 +72,7 @@ __device__ __forceinline__ void stream_rows(const T* A, int64_t lda, int64_t r0,
     }
     for (; cb < cb1; ++cb) {
         const int64_t c = cb * (W * NT);
-        const V xv = ld_x(xp + c);
+        const V xv = kXS ? *reinterpret_cast<const V*>(xp + c) : ld_x(xp + c);
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = fma16(ld_stream(base + roff[r] + c), xv, acc[r]);
     }

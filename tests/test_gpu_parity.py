@@ -310,11 +310,12 @@ def test_graph_replay_bitwise_equal(method):
         assert it == rit and np.array_equal(x, rx) and np.array_equal(h, rh)
 
 
-@pytest.mark.parametrize("persistent", [0, 1])
-def test_persistent_vs_multikernel_parity(persistent):
+@pytest.mark.parametrize("persistent,small", [(0, 0), (1, 0), (1, 1)])
+def test_persistent_vs_multikernel_parity(persistent, small):
     """NEXT-2: the persistent cooperative kernels (grid barriers instead of kernel
-    boundaries) meet the same bars vs the oracle as the multi-kernel path, on CG
-    (C1, G-SPD 4096) and BiCGSTAB (G-DD 1024/4096), and are deterministic."""
+    boundaries) and the small-n shared-memory kernels (small = 1) meet the same bars
+    vs the oracle as the multi-kernel path, on CG (C1, G-SPD 4096) and BiCGSTAB
+    (G-DD 1024/4096), and are deterministic across poll batches."""
     cases = [("cg", *synth.gspd(1024, 1e3)[::2]), ("cg", *synth.gspd(4096, 1e4)[::2]),
              ("bicgstab", *synth.gdd(1024, 4)), ("bicgstab", *synth.gdd(4096, 16))]
     for method, A, b in cases:
@@ -323,6 +324,7 @@ def test_persistent_vs_multikernel_parity(persistent):
         with ks.Context(n) as ctx:
             ctx.load_rows(A)
             ctx.set_option("persistent", persistent)
+            ctx.set_option("small", small)
             assert ctx.get_option("persistent") == persistent
             x, h, r = getattr(ctx, method)(b, tol=1e-10)
             x2, h2, r2 = getattr(ctx, method)(b, tol=1e-10)
@@ -334,13 +336,15 @@ def test_persistent_vs_multikernel_parity(persistent):
             assert rr.iterations == r.iterations and np.array_equal(xx, x) and np.array_equal(hh, h)
 
 
-def test_persistent_edge_cases():
+@pytest.mark.parametrize("small", [0, 1])
+def test_persistent_edge_cases(small):
     n = 64
     A = synth.random_spd(n, 10.0, 1)
     b = np.random.default_rng(0).standard_normal(n)
     with ks.Context(n) as ctx:
         ctx.load_rows(A)
         ctx.set_option("persistent", 1)
+        ctx.set_option("small", small)
         x, h, r = ctx.cg(np.zeros(n), x0=np.ones(n), tol=1e-10)
         assert r.converged and r.iterations == 0 and np.all(x == 0)
         xo, ho, ro = oracle.cg(A, b, tol=1e-30, maxit=7)
@@ -359,12 +363,14 @@ def test_persistent_edge_cases():
     with ks.Context(300) as ctx:
         ctx.load_rows(D)
         ctx.set_option("persistent", 1)
+        ctx.set_option("small", small)
         xo, ho, ro = oracle.bicgstab(D, bd, tol=1e-30, maxit=3)
         x, h, r = ctx.bicgstab(bd, tol=1e-30, maxit=3)
         assert r.status == ks.KS_EMAXIT and r.iterations == 3
         bars(x, h, r, xo, ho, ro, iters_tol=0, floor=FLOOR_BS)
     with ks.Context(2) as ctx:
         ctx.set_option("persistent", 1)
+        ctx.set_option("small", small)
         ctx.load_rows(np.diag([1.0, -1.0]))
         x, h, r = ctx.cg(np.array([1.0, 1.0]), tol=1e-12)
         assert r.status == ks.KS_ENOTSPD and r.iterations == 0
@@ -374,6 +380,44 @@ def test_persistent_edge_cases():
         ctx.load_rows(np.array([[2.0, 1.0], [0.0, 3.0]]))
         x, h, r = ctx.bicgstab(np.array([3.0, 3.0]), tol=1e-12)
         assert r.half_step_exit and r.iterations == 1 and np.allclose(x, [1.0, 1.0], rtol=1e-12)
+
+
+@pytest.mark.parametrize("n", [1000, 2050])
+def test_small_path_ragged_n(n):
+    """Small-n kernels (full vectors in shared memory, zero-padded to the row
+    stride): ragged n, x0 != 0, CG and BiCGSTAB vs the oracle, and the same
+    results as the general persistent kernels within the bars."""
+    A = synth.random_spd(n, 100.0, 5)
+    rng = np.random.default_rng(11)
+    b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+    D, bd = synth.gdd(n, 4, seed=synth.SEED2)
+    xo, ho, ro = oracle.cg(A, b, x0=x0, tol=1e-10)
+    yo, hyo, ryo = oracle.bicgstab(D, bd, tol=1e-10)
+    for small in (1, 0):
+        with ks.Context(n) as ctx, ks.Context(n) as dtx:
+            ctx.set_option("small", small)
+            dtx.set_option("small", small)
+            ctx.load_rows(A)
+            dtx.load_rows(D)
+            x, h, r = ctx.cg(b, x0=x0, tol=1e-10)
+            bars(x, h, r, xo, ho, ro)
+            y, hy, ry = dtx.bicgstab(bd, tol=1e-10)
+            bars(y, hy, ry, yo, hyo, ryo, floor=FLOOR_BS)
+            assert ry.half_step_exit == ryo.half_step_exit
+
+
+def test_small_path_falls_back_when_too_large():
+    """small = 1 with vectors larger than shared memory (3 x 16384 doubles for
+    BiCGSTAB) runs the general persistent kernels: identical bits to small = 0."""
+    n = 16384
+    out = []
+    for small in (1, 0):
+        with ks.Context(n) as ctx:
+            ctx.set_option("small", small)
+            bd = ctx.generate("dd", seed=synth.SEED, kd=16)
+            x, h, r = ctx.bicgstab(bd, tol=1e-10)
+            out.append((x, h, r.iterations))
+    assert out[0][2] == out[1][2] and np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
 
 
 # ------------------------------------------------------------- NEXT-3: BiCG (K1T)
@@ -522,7 +566,8 @@ def test_f32_generate_and_matvec():
 @pytest.mark.parametrize("method,case", [("cg", (1024, 1e3)), ("cg", (4096, 1e2)),
                                          ("bicgstab", (1024, 4)), ("bicgstab", (1024, 16)),
                                          ("bicgstab", (4096, 16))])
-def test_f32_parity(method, case):
+@pytest.mark.parametrize("small", [0, 1])
+def test_f32_parity(method, case, small):
     """NEXT-4: FP32 CG / BiCGSTAB on the GPU vs the FP32 oracle listings, tol 1e-5."""
     n = case[0]
     if method == "cg":
@@ -533,6 +578,7 @@ def test_f32_parity(method, case):
         xo, ho, ro = oracle.bicgstab_f32(A, b, tol=1e-5)
     bb = b.astype(np.float32).astype(np.float64)
     with ks.Context(n, dtype="f32") as ctx:
+        ctx.set_option("small", small)
         if method == "cg":
             ctx.generate("spd", seed=synth.SEED, table=c, want_b=False)
         else:
