@@ -260,7 +260,9 @@ def run_ours(args):
         for c in (cg_ctx, bs_ctx):
             c.set_option("persistent", 0)
     persistent = bool(cg_ctx.get_option("persistent"))
-    dominant = ("k_cg_persist + k_bs_persist (persistent cooperative whole-iteration kernels: "
+    small = persistent and world == 1 and 8 * n <= 32768      # KS_OPT_SMALL auto bound
+    dominant = ("k_cg_small + k_bs_small (small-n persistent kernels, vectors in shared memory)" if small
+                else "k_cg_persist + k_bs_persist (persistent cooperative whole-iteration kernels: "
                 "3 GEMVs + fused vector phases per step)" if persistent else "k1_gemv_ldg (K1 GEMV)")
     row_b, row_e = cg_ctx.row_range(rank)
     m = row_e - row_b
