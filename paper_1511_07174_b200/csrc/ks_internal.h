@@ -199,9 +199,14 @@ int launch_gm_orth(const GmresArgs& g, int j, int pass, cudaStream_t st);
 int launch_gm_step_end(const GmresArgs& g, int j, long long k, cudaStream_t st);
 int launch_gm_vfull(const GmresArgs& g, cudaStream_t st);
 int launch_gm_cycle_end(const GmresArgs& g, long long k_enqueued, cudaStream_t st);
-// one restart cycle as one persistent cooperative kernel (P = 1; ks_gmres_persist.cu)
+// one restart cycle as one persistent cooperative kernel (ks_gmres_persist.cu; P = 1,
+// or P > 1 with the fused exchange: g.a from vargs(true), exchange s has epoch ebase + s)
 int launch_gm_cycle_persist(const GmresArgs& g, const double* A, int64_t lda, int64_t ncols, double* bpart,
-                            unsigned* bar, int grid, cudaStream_t st);
+                            unsigned* bar, int grid, unsigned long long ebase, cudaStream_t st);
+// epochs one solve of GMRES(restart) with maxit steps may use
+inline unsigned long long gm_epochs(long long maxit, int restart) {
+    return (unsigned long long)(maxit / restart + 2) * (3ull + 4ull * (unsigned long long)restart) + 4ull;
+}
 int gm_persist_grid(int num_sms, int64_t m);
 
 // BiCG (NEXT-3)

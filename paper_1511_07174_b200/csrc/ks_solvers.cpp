@@ -550,16 +550,21 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
     Prof prof(c, r, restart + 1);
     int64_t k = 0, cycle = 0;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
-    if (c->P == 1 && c->opt.persistent != 0) {
-        // NEXT-2 for GMRES: one persistent cooperative kernel per restart cycle
+    if ((c->P == 1 || c->fused()) && c->opt.persistent != 0) {
+        // NEXT-2 for GMRES: one persistent cooperative kernel per restart cycle;
+        // P > 1: the Arnoldi collectives run inside it over NVLink (NEXT-1)
         const int grid = gm_persist_grid(r.num_sms, r.m);
         const int64_t max_cycles = maxit / restart + 2;
+        GmresArgs gf = g;
+        gf.a = r.vargs(c->fused());
+        const unsigned long long ebase = r.epoch_next;
+        r.epoch_next += gm_epochs(maxit, restart);
         for (cycle = 0; cycle < max_cycles; ++cycle) {
             const int slot = (int)(cycle & 1);
             prof.begin(slot);
             prof.pre(slot);
-            const int rc = launch_gm_cycle_persist(g, r.A, c->ld, c->ld, r.scr.part + 2 * kPartStride,
-                                                   r.scr.ticket + 8, grid, r.stream);
+            const int rc = launch_gm_cycle_persist(gf, r.A, c->ld, c->ld, r.scr.part + 2 * kPartStride,
+                                                   r.scr.ticket + 8, grid, ebase, r.stream);
             prof.post(slot);
             if (rc < 0) KS_CUDA((cudaError_t)(-rc));
             r.launches += 1;

@@ -154,17 +154,28 @@ def test_multi_bicg(P):
 
 @needs2
 @pytest.mark.parametrize("P", [2, 4])
-def test_multi_gmres(P):
-    """NEXT-3 GMRES(m) at P GPUs (NCCL exchanges of the CGS2 partial dots)."""
+@pytest.mark.parametrize("persistent", [0, 1])
+def test_multi_gmres(P, persistent):
+    """NEXT-3 GMRES(m) at P GPUs: multi-kernel path with NCCL exchanges of the CGS2
+    partial dots (persistent = 0), or one persistent kernel per restart cycle with
+    the exchanges fused over NVLink (persistent = 1); x0, maxit and a restart
+    length that does not divide maxit included."""
     if ngpu() < P:
         pytest.skip(f"needs {P} GPUs")
-    for n, kd, m in [(1024, 16, 30), (4099, 16, 8)]:
+    for n, kd, m in [(1024, 16, 30), (4099, 16, 8), (2050, 4, 3)]:
         A, b = synth.gdd(n, kd)
-        xo, ho, ro = oracle.gmres(A, b, tol=1e-10, restart=m)
+        x0 = np.random.default_rng(n).standard_normal(n) if n == 2050 else None
+        xo, ho, ro = oracle.gmres(A, b, x0=x0, tol=1e-10, restart=m)
         with ks.Context(n, ngpus=P) as ctx:
+            ctx.set_option("persistent", persistent)
             ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
-            x, h, r = ctx.gmres(b, tol=1e-10, restart=m)
-        bars(x, h, r, xo, ho, ro)
+            assert ctx.get_option("persistent") == persistent and ctx.get_option("fused_comm") == 1
+            x, h, r = ctx.gmres(b, x0=x0, tol=1e-10, restart=m)
+            bars(x, h, r, xo, ho, ro)
+            xo7, ho7, ro7 = oracle.gmres(A, b, x0=x0, tol=1e-30, restart=m, maxit=7)
+            x7, h7, r7 = ctx.gmres(b, x0=x0, tol=1e-30, restart=m, maxit=7)
+            assert r7.status == ks.KS_EMAXIT and r7.iterations == 7
+            bars(x7, h7, r7, xo7, ho7, ro7, iters_tol=0)
 
 
 @needs2

@@ -65,6 +65,8 @@ def main():
         solve = getattr(ctx, method)
         ctx.set_option("true_residual", 0)
         ctx.set_option("profile_gemv", 1)
+        if "KS_PERSISTENT" in os.environ:                # comparisons: force the kernel mode
+            ctx.set_option("persistent", int(os.environ["KS_PERSISTENT"]))
         solve(b, tol=0.0, maxit=2, hist=False)                     # warm-up
         _, _, r = solve(b, tol=0.0, maxit=K, hist=False)
         ips = K / r.seconds_loop
