@@ -280,7 +280,8 @@ void setup_peers(ks_ctx* c) {
     r.peer_ok = hok != 0;
 }
 
-const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done) {
+const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done, long long k,
+                     unsigned long long ebase) {
     const int64_t rc = gemv_t_chunk_rows(r.m, c->ld, r.num_sms);
     const int64_t nrc = (r.m + rc - 1) / rc;
     const int64_t need = nrc * c->ld;
@@ -290,9 +291,23 @@ const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done) {
         r.upart = nullptr;
         r.col_ticket = nullptr;
         KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.upart), (size_t)need * sizeof(double)));
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.col_ticket), (size_t)(c->ld / 512 + 1) * sizeof(unsigned)));
-        KS_CUDA(cudaMemset(r.col_ticket, 0, (size_t)(c->ld / 512 + 1) * sizeof(unsigned)));
+        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.col_ticket), (size_t)(c->ld / 512 + 2) * sizeof(unsigned)));
+        KS_CUDA(cudaMemset(r.col_ticket, 0, (size_t)(c->ld / 512 + 2) * sizeof(unsigned)));
         r.upart_cap = need;
+    }
+    if (k > 0 && c->fused()) {            // BiCG loop: reduce-scatter fused into K1T (NEXT-1)
+        GemvTPub pub;
+        pub.P = c->P;
+        const int64_t par = (k & 1) * (int64_t)r.L.P * r.L.chunk;
+        for (int g = 0; g < c->P; ++g) {
+            pub.dst[g] = r.pp.G_v[g] + par + (int64_t)r.rank * r.L.chunk;
+            pub.f_peer[g] = r.pp.flags[g] + kPhaseV * kMaxRanks + r.rank;
+        }
+        pub.epoch = ebase + (unsigned long long)k;
+        pub.ticket = r.col_ticket + c->ld / 512 + 1;
+        r.launches += launch_gemv_t(r.A, c->ld, r.m, c->n, x_loc, rc, r.upart, r.col_ticket, r.U, r.L, done,
+                                    r.stream, &pub);
+        return nullptr;                   // the consumer sums the P slots (k_bicg_update)
     }
     r.launches += launch_gemv_t(r.A, c->ld, r.m, c->n, x_loc, rc, r.upart, r.col_ticket, r.U, r.L, done,
                                 r.stream);

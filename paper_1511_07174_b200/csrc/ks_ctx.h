@@ -167,6 +167,9 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
                  double* x, double* hist, int64_t hist_cap, ks_report* rep);
 // K1T into r.U (chunk layout); for P > 1 reduce-scattered into r.qt_loc.  Returns the
 // pointer holding this rank's rows of A^T x.
-const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done);
+// k > 0 with the fused exchange (BiCG loop): the reduce-scatter is fused into K1T
+// (slots G_v[parity k][rank g's chunk], flag kPhaseV with epoch ebase + k); returns nullptr.
+const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done, long long k = 0,
+                     unsigned long long ebase = 0);
 GemvConfig gemv_config(const ks_ctx* c, const Rank& r);
 }  // namespace ks

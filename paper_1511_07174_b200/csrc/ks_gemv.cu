@@ -380,9 +380,9 @@ template <int VPT, int UT>
 __global__ void __launch_bounds__(kNT) k1t_gemv(const double* A, int64_t lda, int64_t m, int64_t n,
                                                const double* x, int64_t rc_rows, int64_t nrc,
                                                double* upart, unsigned* col_ticket, double* out,
-                                               Layout L, const int* done) {
+                                               Layout L, const int* done, GemvTPub pub) {
     constexpr int CB = 2 * VPT * kNT;
-    __shared__ int s_last;
+    __shared__ int s_last, s_all;
     if (done && *(volatile const int*)done) return;
     const int64_t ncb = lda / CB;
     const int64_t cb = blockIdx.x % ncb;
@@ -452,7 +452,21 @@ __global__ void __launch_bounds__(kNT) k1t_gemv(const double* A, int64_t lda, in
             if (j >= n) break;
             int g = 0;
             while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
-            out[(int64_t)g * L.chunk + (j - L.row0[g])] = e ? acc[v].y : acc[v].x;
+            if (pub.P) pub.dst[g][j - L.row0[g]] = e ? acc[v].y : acc[v].x;   // fused reduce-scatter
+            else out[(int64_t)g * L.chunk + (j - L.row0[g])] = e ? acc[v].y : acc[v].x;
+        }
+    }
+    if (pub.P) {
+        // the last column block to finish releases this rank's slices to every owner
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned t = atomicAdd(pub.ticket, 1u);
+            s_all = (t == (unsigned)(ncb - 1));
+            if (s_all) {
+                *pub.ticket = 0u;
+                publish_flags(pub.f_peer, pub.P, pub.epoch);
+            }
         }
     }
 }
@@ -478,8 +492,9 @@ int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms) {
 
 int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
                   int64_t rc_rows, double* upart, unsigned* col_ticket, double* out, const Layout& L,
-                  const int* done, cudaStream_t st) {
+                  const int* done, cudaStream_t st, const GemvTPub* pub) {
     if (m <= 0) return 0;
+    const GemvTPub pb = pub ? *pub : GemvTPub{};
     const int vpt = (lda % (2 * g_k1t_vpt * kNT) == 0) ? g_k1t_vpt : 1;
     const int64_t ncb = lda / (2 * vpt * kNT);
     const int64_t nrc = (m + rc_rows - 1) / rc_rows;
@@ -487,7 +502,7 @@ int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const doub
 #define K1T_CASE(V, U)                                                                       \
     if (vpt == V && g_k1t_ut == U) {                                                          \
         k1t_gemv<V, U><<<grid, kNT, 0, st>>>(A, lda, m, n, x, rc_rows, nrc, upart, col_ticket,  \
-                                            out, L, done);                                     \
+                                            out, L, done, pb);                                 \
         return 1;                                                                              \
     }
     K1T_CASE(1, 4) K1T_CASE(1, 8) K1T_CASE(1, 16)

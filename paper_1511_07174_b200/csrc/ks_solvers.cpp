@@ -648,12 +648,19 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
     setup(c, r, b, x0, hist_cap);                  // r0, x, rt0 = r0, slots <r0,r0>
-    VecArgs a = r.vargs(false);
-    r.launches += launch_bicg_init(a, tol, maxit, hist_cap, r.stream);
+    // fused (P > 1, NEXT-1): sigma partials pushed by K1's epilogue, the A^T pt
+    // reduce-scatter fused into K1T, r slices pushed by k_bicg_update -- no NCCL
+    // call in the loop
+    const bool fused = c->fused();
+    VecArgs a = r.vargs(fused);
+    const unsigned long long ebase = r.epoch_next;
+    r.epoch_next += (unsigned long long)maxit + 2;
+    r.launches += launch_bicg_init(a, tol, maxit, hist_cap, ebase, r.stream);
     GemvParams pq = gp(c, r, r.p_full, r.q_loc);   // q = A p, sigma_g = <pt_loc, q>
     pq.w1 = r.pt_loc;
     pq.out1 = r.S + (int64_t)r.rank * kScalSlot;
     pq.done = &r.st->done;
+    if (fused) fuse_gemv(c, r, pq, kPhaseS, nullptr, 0, r.pp.S, (int64_t)r.rank * kScalSlot, a.spar);
     const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
     Prof prof(c, r, 2 * B);
     int64_t k = 1, batch = 0;
@@ -663,16 +670,17 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
         prof.begin(slot);
         const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
         for (; k <= kend; ++k) {
+            pq.koff = k;
             prof.pre(slot);
-            gemv(c, r, pq);                                    // q = A p
+            gemv(c, r, pq);                                    // q = A p (+ fused sigma publish)
             prof.post(slot);
             prof.pre(slot);
-            gemv_t(c, r, r.pt_loc, &r.st->done);               // qt = A^T pt (+ reduce-scatter)
+            gemv_t(c, r, r.pt_loc, &r.st->done, fused ? k : 0, ebase);   // qt = A^T pt (+ reduce-scatter)
             prof.post(slot);
             r.gemv_launches += 2;
-            allgather(c, r, r.S, kScalSlot);
+            if (!fused) allgather(c, r, r.S, kScalSlot);
             r.launches += launch_bicg_update(a, k, r.stream);
-            allgather(c, r, r.G_r, r.L.chunk);
+            if (!fused) allgather(c, r, r.G_r, r.L.chunk);
             r.launches += launch_bicg_direction(a, k, r.stream);
         }
         KS_CUDA(cudaMemcpyAsync(&r.h_done[slot], &r.st->done, sizeof(int), cudaMemcpyDeviceToHost, r.stream));

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, const long long* kdev,
 // Fletcher's BiCG (oracle or_bicg): p = r + beta p (full, replicated like CG),
 // the shadow pair (rt, pt) stays sharded: qt rows come from K1T + reduce-scatter.
 __global__ void __launch_bounds__(kNT) k_bicg_init(VecArgs a, double tol, long long maxit,
-                                                   long long hist_cap) {
+                                                   long long hist_cap, unsigned long long ebase) {
     __shared__ double red[kNT / 32];
     const int64_t m = m_loc(a.L);
     double acc[1] = {0.0};
@@ -427,41 +427,54 @@ __global__ void __launch_bounds__(kNT) k_bicg_init(VecArgs a, double tol, long l
     block_sum<kNT, 1>(acc, red);
     if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
         DevState* st = a.st;
-        init_state(st, tol, maxit, hist_cap, 0);
+        init_state(st, tol, maxit, hist_cap, ebase);
         st->rho[0] = sum_slots(a.L, a.G_r, 0);              // <rt0, r0>
         init_decide(st, acc[0], sum_slots(a.L, a.G_r, 1));
     }
 }
 
 // sigma = <pt, A p> (K1 partials); alpha; x += alpha p; r -= alpha q; rt -= alpha qt;
-// partials <rt, r>, <r, r> into the own slots of G_r.
+// partials <rt, r>, <r, r> into the own slots of G_r.  Fused mode: sigma partials
+// and the K1T column-sum slices (G_v, one slot per source rank, summed in rank
+// order) arrive over NVLink; r_k and the partials are pushed to every rank.
 __global__ void __launch_bounds__(kNT) k_bicg_update(VecArgs a, long long k) {
     __shared__ double red[2 * (kNT / 32)];
     DevState* st = a.st;
     if (is_done(st)) return;
-    const double sigma = sum_scal(a.L, a.S, 0);
+    if (!wait_phase(a, kPhaseS, k) || !wait_phase(a, kPhaseV, k)) return;
+    const double sigma = sum_scal(a.L, Spar(a, k), 0);
     if (sigma == 0.0 || !isfinite(sigma)) {
         if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = k - 1; st->done = 1; }
         return;
     }
     const double alpha = st->rho[(k - 1) & 3] / sigma;
     const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
-    double* rl = own_chunk(a, a.G_r);
+    const double* rin = own_chunk(a, Gpar(a, a.G_r, k - 1));   // r_{k-1}
+    const double* qslots = Gpar(a, a.G_v, k);                   // fused: P slots of qt rows
     double acc[2] = {0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
         a.x_loc[i] = fma(alpha, a.p_full[r0 + i], a.x_loc[i]);
-        const double r = fma(-alpha, a.q_loc[i], rl[i]);
-        rl[i] = r;
-        const double rt = fma(-alpha, a.qt_loc[i], a.rhat_loc[i]);
+        const double r = fma(-alpha, a.q_loc[i], rin[i]);
+        publish(a, a.pp.G_r, a.G_r, k, i, r);
+        double qt;
+        if (a.peer) {
+            qt = 0.0;
+            for (int g = 0; g < a.L.P; ++g) qt += qslots[(int64_t)g * a.L.chunk + i];
+        } else {
+            qt = a.qt_loc[i];
+        }
+        const double rt = fma(-alpha, qt, a.rhat_loc[i]);
         a.rhat_loc[i] = rt;
         acc[0] = fma(rt, r, acc[0]);
         acc[1] = fma(r, r, acc[1]);
     }
+    if (a.peer) __threadfence_system();
     block_sum<kNT, 2>(acc, red);
     if (grid_sum<kNT, 2>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
-        rl[a.L.pslot + 0] = acc[0];
-        rl[a.L.pslot + 1] = acc[1];
+        publish(a, a.pp.G_r, a.G_r, k, a.L.pslot + 0, acc[0]);
+        publish(a, a.pp.G_r, a.G_r, k, a.L.pslot + 1, acc[1]);
         st->alpha[k & 3] = alpha;
+        publish_phase(a, kPhaseR, k);
     }
 }
 
@@ -469,8 +482,10 @@ __global__ void __launch_bounds__(kNT) k_bicg_update(VecArgs a, long long k) {
 __global__ void __launch_bounds__(kNT) k_bicg_direction(VecArgs a, long long k) {
     DevState* st = a.st;
     if (is_done(st)) return;
-    const double rho1 = sum_slots(a.L, a.G_r, 0);
-    const double rel = sqrt(sum_slots(a.L, a.G_r, 1)) / st->nb;
+    if (!wait_phase(a, kPhaseR, k)) return;
+    const double* Gr = Gpar(a, a.G_r, k);
+    const double rho1 = sum_slots(a.L, Gr, 0);
+    const double rel = sqrt(sum_slots(a.L, Gr, 1)) / st->nb;
     if (rel <= st->tol) {
         if (lead()) {
             put_hist(st, a.hist, k - 1, rel);
@@ -487,7 +502,7 @@ __global__ void __launch_bounds__(kNT) k_bicg_direction(VecArgs a, long long k) 
     }
     const double beta = rho1 / st->rho[(k - 1) & 3];
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT)
-        a.p_full[j] = fma(beta, a.p_full[j], a.G_r[gidx(a.L, j)]);
+        a.p_full[j] = fma(beta, a.p_full[j], Gr[gidx(a.L, j)]);
     const int64_t m = m_loc(a.L);
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
         a.pt_loc[i] = fma(beta, a.pt_loc[i], a.rhat_loc[i]);
@@ -570,8 +585,8 @@ int launch_advance(long long* kdev, long long by, cudaStream_t st) {
     return 1;
 }
 int launch_bicg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
-                     cudaStream_t st) {
-    k_bicg_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap);
+                     unsigned long long ebase, cudaStream_t st) {
+    k_bicg_init<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, tol, maxit, hist_cap, ebase);
     return 1;
 }
 int launch_bicg_update(const VecArgs& a, long long k, cudaStream_t st) {

@@ -136,18 +136,28 @@ def test_multi_persistent_fused(P):
 
 @needs2
 @pytest.mark.parametrize("P", [2, 4])
-def test_multi_bicg(P):
-    """NEXT-3 BiCG at P GPUs: K1T partials reduce-scattered over NCCL."""
+@pytest.mark.parametrize("fused", [1, 0])
+def test_multi_bicg(P, fused):
+    """NEXT-3 BiCG at P GPUs: K1T partials reduce-scattered either inside K1T over
+    NVLink peer stores (fused = 1, default) or by ncclReduceScatter (fused = 0);
+    x0 and maxit included."""
     if ngpu() < P:
         pytest.skip(f"needs {P} GPUs")
     for n, kd in [(1024, 4), (4099, 16)]:
         A, b = synth.gdd(n, kd)
         xo, ho, ro = oracle.bicg(A, b, tol=1e-10)
         with ks.Context(n, ngpus=P) as ctx:
+            ctx.set_option("fused_comm", fused)
+            assert ctx.get_option("fused_comm") == fused
             ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
             x, h, r = ctx.bicg(b, tol=1e-10)
             xt = np.random.default_rng(3).standard_normal(n)
             yt = ctx.matvec_t(xt)
+            x0 = np.random.default_rng(5).standard_normal(n)
+            xo5, ho5, ro5 = oracle.bicg(A, b, x0=x0, tol=1e-30, maxit=5)
+            x5, h5, r5 = ctx.bicg(b, x0=x0, tol=1e-30, maxit=5)
+            assert r5.status == ks.KS_EMAXIT and r5.iterations == 5
+            bars(x5, h5, r5, xo5, ho5, ro5, iters_tol=0)
         bars(x, h, r, xo, ho, ro)
         gemv_bound_check(np.ascontiguousarray(A.T), xt, yt)
 
@@ -255,6 +265,12 @@ def test_torchrun_borrowed_comm(tmp_path, P):
     R = res[0]["bs_persistent"]
     Rep.iterations = R["it"]
     bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro, floor=FLOOR_BS)
+    xo, ho, ro = oracle.gmres(A, b, tol=1e-10, restart=20)
+    R = res[0]["gmres"]
+    Rep.iterations = R["it"]
+    bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro)
+    for g in range(1, P):
+        assert res[g]["gmres"] == res[0]["gmres"]
     A, b = synth.gdd(n, 4)
     xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
     R = res[0]["bs_loaded"]

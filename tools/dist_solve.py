@@ -45,5 +45,10 @@ with ks.Context.from_process_group(n) as ctx:
         ctx.set_option("fused_comm", mode)
         x, h, r = ctx.bicgstab(b, tol=1e-10)
         res[f"bs_mode{mode}"] = {"x": x.tolist(), "h": h.tolist(), "it": r.iterations}
+    # GMRES(20): persistent cycle kernel with fused exchanges (default) in this mode
+    ctx.set_option("persistent", 2)
+    ctx.set_option("fused_comm", 1)
+    x, h, r = ctx.gmres(b, tol=1e-10, restart=20)
+    res["gmres"] = {"x": x.tolist(), "h": h.tolist(), "it": r.iterations}
 json.dump(res, open(os.path.join(outdir, f"dist_{n}_r{rank}.json"), "w"))
 dist.destroy_process_group()

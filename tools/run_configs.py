@@ -67,6 +67,8 @@ def main():
         ctx.set_option("profile_gemv", 1)
         if "KS_PERSISTENT" in os.environ:                # comparisons: force the kernel mode
             ctx.set_option("persistent", int(os.environ["KS_PERSISTENT"]))
+        if "KS_FUSED" in os.environ:                     # comparisons: fused vs NCCL exchange
+            ctx.set_option("fused_comm", int(os.environ["KS_FUSED"]))
         solve(b, tol=0.0, maxit=2, hist=False)                     # warm-up
         _, _, r = solve(b, tol=0.0, maxit=K, hist=False)
         ips = K / r.seconds_loop
