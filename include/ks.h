@@ -121,7 +121,7 @@ typedef enum {
                               /* the default for the row count)                   */
     KS_OPT_PERSIST_GRID = 10, /* tuning: cap on the persistent kernels' CTA count */
                               /* (0 = auto; the grid must be equal on all ranks)  */
-    KS_OPT_GEMVT_SHAPE = 11,  /* tuning (process-wide): K1T 16-byte vectors per   */
+    KS_OPT_GEMVT_SHAPE = 11,  /* tuning: K1T 16-byte vectors per                  */
                               /* thread per row (1/2/4) * 100 + rows in flight    */
                               /* (4/8/16); default 204 (profiles/r01_gemvt_sweep) */
     KS_OPT_SMALL = 12         /* CG / BiCGSTAB on one GPU with the persistent     */

@@ -501,7 +501,7 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             if (v < 0 || v > 1 << 20) return fail(c, KS_EARG, "bad persistent grid");
             o.persist_grid = v; break;
         case KS_OPT_GEMVT_SHAPE:
-            ks::set_gemv_t_shape((int)(v / 100), (int)(v % 100));
+            if (!ks::gemv_t_shape_ok(v)) return fail(c, KS_EARG, "gemvt shape must be (1|2|4) * 100 + (4|8|16)");
             o.gemvt_shape = v; break;
         case KS_OPT_SMALL:
             if (v < 0 || v > 2) return fail(c, KS_EARG, "small must be 0, 1 or 2");

@@ -282,7 +282,8 @@ void setup_peers(ks_ctx* c) {
 
 const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done, long long k,
                      unsigned long long ebase) {
-    const int64_t rc = gemv_t_chunk_rows(r.m, c->ld, r.num_sms);
+    const int shape = (int)c->opt.gemvt_shape;
+    const int64_t rc = gemv_t_chunk_rows(r.m, c->ld, r.num_sms, shape);
     const int64_t nrc = (r.m + rc - 1) / rc;
     const int64_t need = nrc * c->ld;
     if (need > r.upart_cap) {
@@ -306,11 +307,11 @@ const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done, l
         pub.epoch = ebase + (unsigned long long)k;
         pub.ticket = r.col_ticket + c->ld / 512 + 1;
         r.launches += launch_gemv_t(r.A, c->ld, r.m, c->n, x_loc, rc, r.upart, r.col_ticket, r.U, r.L, done,
-                                    r.stream, &pub);
+                                    shape, r.stream, &pub);
         return nullptr;                   // the consumer sums the P slots (k_bicg_update)
     }
     r.launches += launch_gemv_t(r.A, c->ld, r.m, c->n, x_loc, rc, r.upart, r.col_ticket, r.U, r.L, done,
-                                r.stream);
+                                shape, r.stream);
     if (c->P == 1) return r.U;
     KS_NCCL(ncclReduceScatter(r.U, r.qt_loc, (size_t)r.L.chunk, ncclDouble, ncclSum, r.comm, r.stream));
     return r.qt_loc;

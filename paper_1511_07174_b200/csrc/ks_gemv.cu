@@ -471,17 +471,20 @@ __global__ void __launch_bounds__(kNT) k1t_gemv(const double* A, int64_t lda, in
     }
 }
 
-int g_k1t_vpt = 2, g_k1t_ut = 4;   // tuning knobs (KS_OPT_GEMVT_SHAPE); sweep best 204
+// K1T shape from KS_OPT_GEMVT_SHAPE (vectors per thread per row * 100 + rows in
+// flight; validated by ks_set_option, default 204 = the sweep's best).
+int shape_vpt(int shape) { const int v = shape / 100; return (v == 1 || v == 2 || v == 4) ? v : 2; }
+int shape_ut(int shape) { const int u = shape % 100; return (u == 4 || u == 8 || u == 16) ? u : 4; }
 
 }  // namespace
 
-void set_gemv_t_shape(int vpt, int ut) {
-    g_k1t_vpt = (vpt == 1 || vpt == 2 || vpt == 4) ? vpt : 2;
-    g_k1t_ut = (ut == 4 || ut == 8 || ut == 16) ? ut : 4;
+bool gemv_t_shape_ok(int64_t shape) {
+    const int64_t v = shape / 100, u = shape % 100;
+    return (v == 1 || v == 2 || v == 4) && (u == 4 || u == 8 || u == 16);
 }
 
-int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms) {
-    const int64_t ncb = std::max<int64_t>(1, lda / (2 * g_k1t_vpt * kNT));
+int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms, int shape) {
+    const int64_t ncb = std::max<int64_t>(1, lda / (2 * shape_vpt(shape) * kNT));
     const int64_t target = 6LL * 4 * num_sms;            // ~6 waves of 4 CTAs/SM
     int64_t nrc = (target + ncb - 1) / ncb;
     if (nrc < 1) nrc = 1;
@@ -492,15 +495,16 @@ int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms) {
 
 int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
                   int64_t rc_rows, double* upart, unsigned* col_ticket, double* out, const Layout& L,
-                  const int* done, cudaStream_t st, const GemvTPub* pub) {
+                  const int* done, int shape, cudaStream_t st, const GemvTPub* pub) {
     if (m <= 0) return 0;
     const GemvTPub pb = pub ? *pub : GemvTPub{};
-    const int vpt = (lda % (2 * g_k1t_vpt * kNT) == 0) ? g_k1t_vpt : 1;
+    const int ut = shape_ut(shape);
+    const int vpt = (lda % (2 * shape_vpt(shape) * kNT) == 0) ? shape_vpt(shape) : 1;
     const int64_t ncb = lda / (2 * vpt * kNT);
     const int64_t nrc = (m + rc_rows - 1) / rc_rows;
     const unsigned grid = (unsigned)(ncb * nrc);
 #define K1T_CASE(V, U)                                                                       \
-    if (vpt == V && g_k1t_ut == U) {                                                          \
+    if (vpt == V && ut == U) {                                                          \
         k1t_gemv<V, U><<<grid, kNT, 0, st>>>(A, lda, m, n, x, rc_rows, nrc, upart, col_ticket,  \
                                             out, L, done, pb);                                 \
         return 1;                                                                              \

@@ -111,7 +111,8 @@ GemvConfig choose_gemv(int64_t m, int64_t ncols, int num_sms, int rows_opt, int 
 
 // K1T: u = A_loc^T x_loc (BiCG), chunk-layout output; upart holds
 // ceil(m / rc_rows) x lda partials, col_ticket lda / 512 counters.
-int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms);
+int64_t gemv_t_chunk_rows(int64_t m, int64_t lda, int num_sms, int shape);
+bool gemv_t_shape_ok(int64_t shape);   // KS_OPT_GEMVT_SHAPE value check
 // Fused reduce-scatter of K1T (BiCG, P > 1, NEXT-1): each column sum is stored
 // straight into its owner rank's exchange slot for this rank, and the last column
 // block to finish releases `epoch` into every rank's flag slot.
@@ -122,10 +123,9 @@ struct GemvTPub {
     unsigned long long epoch = 0;
     unsigned* ticket = nullptr;               // column blocks finished (self-resetting)
 };
-void set_gemv_t_shape(int vpt, int ut);   // tuning (process-wide): vectors/thread/row, rows in flight
 int launch_gemv_t(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
                   int64_t rc_rows, double* upart, unsigned* col_ticket, double* out, const Layout& L,
-                  const int* done, cudaStream_t st, const GemvTPub* pub = nullptr);
+                  const int* done, int shape, cudaStream_t st, const GemvTPub* pub = nullptr);
 
 int launch_gen_spd(double* A, int64_t lda, int64_t row0, int64_t m, int64_t n, uint64_t seed,
                    const double* table_dev, cudaStream_t st);

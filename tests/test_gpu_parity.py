@@ -659,3 +659,26 @@ def test_c_example_runs():
     assert d["bicgstab"]["converged"] == 1 and abs(d["bicgstab"]["iterations"] - 30) <= 2   # App. A.8
     assert d["bicgstab"]["true_relres"] <= 1e-9
     assert d["cg"]["converged"] == 1 and d["cg"]["true_relres"] <= 1e-10
+
+
+def test_option_validation_and_roundtrip():
+    """ks_set_option rejects out-of-range values with KS_EARG and keeps the old
+    value; accepted values read back (effective values for fused_comm/persistent)."""
+    bad = {"poll_batch": [0, 5000], "gemv_rows": [3, 32], "gemv_split": [-1, 65], "gemv_kernel": [3],
+           "persistent": [3, -1], "gemv_unroll": [3, 16], "persist_grid": [-1], "gemvt_shape": [203, 304, 4],
+           "small": [3, -1]}
+    good = {"poll_batch": 7, "gemv_rows": 4, "gemv_split": 2, "gemv_kernel": 1, "gemv_unroll": 2,
+            "persist_grid": 64, "gemvt_shape": 108, "small": 0, "true_residual": 0, "use_graphs": 1}
+    with ks.Context(64) as ctx:
+        for name, vals in bad.items():
+            before = ctx.get_option(name)
+            for v in vals:
+                with pytest.raises(ks.KsError) as e:
+                    ctx.set_option(name, v)
+                assert e.value.status == ks.KS_EARG, (name, v)
+                assert ctx.get_option(name) == before
+        for name, v in good.items():
+            ctx.set_option(name, v)
+            assert ctx.get_option(name) == v
+        assert ctx.get_option("fused_comm") == 0          # P = 1: effective value
+        assert ks.lib().ks_set_option(ctx._h, 99, 1) == ks.KS_EARG      # unknown option
