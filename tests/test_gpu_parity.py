@@ -682,3 +682,15 @@ def test_option_validation_and_roundtrip():
             assert ctx.get_option(name) == v
         assert ctx.get_option("fused_comm") == 0          # P = 1: effective value
         assert ks.lib().ks_set_option(ctx._h, 99, 1) == ks.KS_EARG      # unknown option
+
+
+def test_out_of_memory_is_reported_and_recoverable():
+    """A system too large for HBM (n = 2^21: 32 TiB) fails ks_create with KS_ENOMEM,
+    frees what it allocated, and the next context works."""
+    with pytest.raises(ks.KsError) as e:
+        ks.Context(1 << 21)
+    assert e.value.status == ks.KS_ENOMEM
+    with ks.Context(64) as ctx:
+        ctx.load_rows(np.eye(64) * 2.0)
+        x, h, r = ctx.cg(np.ones(64), tol=1e-12)
+        assert r.converged and np.allclose(x, 0.5)
