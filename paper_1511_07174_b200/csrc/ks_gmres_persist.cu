@@ -316,7 +316,9 @@ int launch_gm_cycle_persist(const GmresArgs& g, const double* A, int64_t lda, in
     args.P.k1 = 0;
     args.g = g;
     void* params[] = {&args};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_gm_cycle<2, 4>, dim3((unsigned)grid), dim3(kNT),
+    cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
+    if (e != cudaSuccess) return -(int)e;
+    e = cudaLaunchCooperativeKernel((const void*)k_gm_cycle<2, 4>, dim3((unsigned)grid), dim3(kNT),
                                                 params, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
 }

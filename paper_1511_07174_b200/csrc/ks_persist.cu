@@ -342,7 +342,9 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
     P.k0 = k0;
     P.k1 = k1;
     void* args[] = {&P};
-    cudaError_t e = cudaLaunchCooperativeKernel(pick<T>(bicgstab, rows, unroll), dim3((unsigned)grid),
+    cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
+    if (e != cudaSuccess) return -(int)e;
+    e = cudaLaunchCooperativeKernel(pick<T>(bicgstab, rows, unroll), dim3((unsigned)grid),
                                                 dim3(kNT), args, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
 }

@@ -52,40 +52,39 @@ __device__ __forceinline__ void hist_put(DevState* st, double* hist, long long k
     if (hist && k1 >= 0 && k1 < st->hist_cap) hist[k1] = v;
 }
 
-// Grid-wide barrier (all CTAs co-resident: cooperative launch).  Generation
-// counter: the last arriver resets the count and releases the next generation.
-// Bounded spin: a timeout marks the solve failed instead of hanging.
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+// Grid-wide barrier (all CTAs co-resident: cooperative launch).  One 64-bit
+// arrival counter, zeroed by the launcher before every launch and never reset
+// inside it: barrier b of the launch completes when the counter reaches
+// (b + 1) * gridDim.x, and each CTA learns b from the value its own arrival
+// returned.  Waiters observe the last arrival directly (no second round trip
+// through a generation word).  Arrival = fence (release, cumulative over the
+// CTA's bar.sync) + relaxed atomicAdd; wait = ld.acquire.gpu.  Bounded spin: a
+// timeout marks the solve failed instead of hanging.
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
-}
-__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ bool grid_sync(unsigned* bar, DevState* st) {
     __shared__ int s_ok;
     __syncthreads();
     if (threadIdx.x == 0) {
         int ok = 1;
-        unsigned* cnt = bar;
-        unsigned* gen = bar + 1;
-        const unsigned g0 = ld_acquire_gpu(gen);
+        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(bar);
         __threadfence();
-        const unsigned arrived = atomicAdd(cnt, 1u) + 1u;
-        if (arrived == gridDim.x) {
-            atomicExch(cnt, 0u);
-            __threadfence();
-            st_release_gpu(gen, g0 + 1u);
-        } else {
+        const unsigned long long old = atomicAdd(cnt, 1ull);
+        const unsigned long long target = (old / gridDim.x + 1ull) * gridDim.x;
+        if (old + 1ull != target) {
             const unsigned long long t0 = globaltimer_ns();
-            while (ld_acquire_gpu(gen) == g0) {
+            while (ld_acquire_gpu_u64(cnt) < target) {
                 if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
                     ok = 0;
                     st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1;
                     break;
                 }
             }
+        } else {
+            __threadfence();   // last arrival: acquire the other CTAs' writes
         }
         s_ok = ok;
     }

@@ -347,7 +347,9 @@ int launch_small(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, in
     P.k0 = k0;
     P.k1 = k1;
     void* args[] = {&P};
-    cudaError_t e = cudaLaunchCooperativeKernel(kern<T>(bicgstab), dim3((unsigned)grid), dim3(kNT), args,
+    cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
+    if (e != cudaSuccess) return -(int)e;
+    e = cudaLaunchCooperativeKernel(kern<T>(bicgstab), dim3((unsigned)grid), dim3(kNT), args,
                                                 smem_bytes<T>(bicgstab, ncols), st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
