@@ -26,6 +26,9 @@ CONFIGS = {
     "C1bicg": ("bicg", 1024, dict(kd=16), 200),
     "C3gmres": ("gmres", 65536, dict(kd=16), 30),     # NEXT-3: GMRES(30)
     "C1gmres": ("gmres", 1024, dict(kd=16), 200),
+    "C2bs": ("bicgstab", 32768, dict(kd=16), 50),       # per-rank size of n = 65536 at P = 8 (P = 2)
+    "C16cg": ("cg", 16384, dict(kappa=1e4), 200),
+    "C16bs": ("bicgstab", 16384, dict(kd=16), 100),
 }
 NOMINAL = 8000e9
 
