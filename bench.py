@@ -59,6 +59,26 @@ def measured_peak():
 
 # ----------------------------------------------------------------- clocks
 
+def environment(local: int) -> dict:
+    """GPU / driver / NCCL / torch versions and memory clock."""
+    import torch
+    env = {"gpu": torch.cuda.get_device_name(local), "torch": torch.__version__,
+           "cuda_runtime": torch.version.cuda}
+    try:
+        v = torch.cuda.nccl.version()
+        env["nccl"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception:
+        pass
+    try:
+        out = subprocess.run(["nvidia-smi", f"--id={local}", "--query-gpu=driver_version,clocks.max.mem,clocks.mem",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10).stdout
+        drv, mmax, mem = [x.strip() for x in out.strip().split(",")]
+        env.update(driver=drv, mem_max_mhz=float(mmax), mem_mhz=float(mem))
+    except Exception:
+        pass
+    return env
+
+
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -389,6 +409,7 @@ def run_ours(args):
             "clocks": clocks, "remeasured": remeasured,
             "cpu_baseline": cpu,
             "generate_s": t_gen,
+            "env": environment(local),
         }
         json_out.write(json.dumps(line) + "\n")
         json_out.flush()
