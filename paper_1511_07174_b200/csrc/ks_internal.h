@@ -164,6 +164,7 @@ struct VecArgsT {
 using VecArgs = VecArgsT<double>;
 
 int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaStream_t st);
+int launch_setup_local(const VecArgs& a, cudaStream_t st);   // P > 1, x0 = 0: no gather
 int launch_cg_init(const VecArgs& a, double tol, long long maxit, long long hist_cap,
                    unsigned long long ebase, cudaStream_t st);
 int launch_cg_update(const VecArgs& a, const long long* kdev, long long k, cudaStream_t st);

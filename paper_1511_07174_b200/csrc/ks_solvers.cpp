@@ -154,9 +154,11 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
         ++batch;
     }
     KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
-    KS_CUDA(cudaStreamSynchronize(r.stream));
-    prof.harvest(0);
-    prof.harvest(1);
+    if (c->opt.profile_gemv) {            // otherwise finish_and_copy's synchronisation covers it
+        KS_CUDA(cudaStreamSynchronize(r.stream));
+        prof.harvest(0);
+        prof.harvest(1);
+    }
 }
 
 void gemv(ks_ctx* c, Rank& r, const GemvParams& p) {
@@ -192,6 +194,9 @@ void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_c
         p.bsub = r.b_full + r.row0;
         gemv(c, r, p);
         r.launches += launch_setup_r(a, true, r.s_full, r.stream);
+    } else if (c->P > 1) {
+        r.launches += launch_setup_local(a, r.stream);   // r0 = b: every rank has all of b
+        return;
     } else {
         r.launches += launch_setup_r(a, false, nullptr, r.stream);
     }
@@ -220,17 +225,20 @@ void finish_and_copy(ks_ctx* c, Rank& r, double* x, double* hist, int64_t hist_c
         r.launches += launch_true_res_final(a, r.stream);
     }
     KS_CUDA(cudaMemcpyAsync(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost, r.stream));
-    KS_CUDA(cudaStreamSynchronize(r.stream));
-    const DevState& s = *r.h_state;
-    if (c->writes_host(r)) {
+    if (c->writes_host(r)) {              // x does not depend on the state: same synchronisation
         if (c->P > 1) copy_chunks_to(c, r, r.G_v, x, cudaMemcpyDefault);
         else KS_CUDA(cudaMemcpyAsync(x, r.x_loc, (size_t)c->n * sizeof(double), cudaMemcpyDefault,
                                      r.stream));
+    }
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    const DevState& s = *r.h_state;
+    if (c->writes_host(r)) {
         const int64_t nh = std::min<int64_t>(s.iters, hist_cap);
-        if (hist && nh > 0)
+        if (hist && nh > 0) {
             KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault,
                                     r.stream));
-        KS_CUDA(cudaStreamSynchronize(r.stream));
+            KS_CUDA(cudaStreamSynchronize(r.stream));
+        }
     }
     if (rep) {
         float ms = 0.f;

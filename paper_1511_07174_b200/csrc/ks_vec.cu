@@ -123,6 +123,34 @@ __global__ void __launch_bounds__(kNT) k_setup_r(VecArgs a, int have_x0, const d
     }
 }
 
+// Setup for P > 1 with x0 = 0: every rank already holds the full b, so r0 = b needs
+// no gather.  Every rank fills all chunks of G_r (parity 0) from b; <r0, r0> =
+// <rhat, r0> = ||b||^2 is one full-length reduction (fixed order, identical on
+// every rank), stored in chunk 0's partial slots with the other chunks' slots 0, so
+// the consumers' rank-ordered slot sums read it unchanged.
+__global__ void __launch_bounds__(kNT) k_setup_local(VecArgs a) {
+    __shared__ double red[kNT / 32];
+    const Layout& L = a.L;
+    const int64_t m = m_loc(L), r0 = L.row0[L.rank];
+    double acc[1] = {0.0};
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < L.n; j += (int64_t)gridDim.x * kNT) {
+        const double bj = a.b_full[j];
+        a.G_r[gidx(L, j)] = bj;
+        acc[0] = fma(bj, bj, acc[0]);
+    }
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
+        a.x_loc[i] = 0.0;
+        a.rhat_loc[i] = a.b_full[r0 + i];
+    }
+    block_sum<kNT, 1>(acc, red);
+    if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
+        for (int g = 0; g < L.P; ++g) {
+            a.G_r[(int64_t)g * L.chunk + L.pslot + 0] = g == 0 ? acc[0] : 0.0;
+            a.G_r[(int64_t)g * L.chunk + L.pslot + 1] = g == 0 ? acc[0] : 0.0;
+        }
+    }
+}
+
 __device__ void init_state(DevState* st, double tol, long long maxit, long long hist_cap,
                            unsigned long long ebase) {
     st->tol = tol;
@@ -538,6 +566,10 @@ int64_t mloc_h(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
 
 }  // namespace
 
+int launch_setup_local(const VecArgs& a, cudaStream_t st) {
+    k_setup_local<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a);
+    return 1;
+}
 int launch_setup_r(const VecArgs& a, bool have_x0, const double* x0_full, cudaStream_t st) {
     k_setup_r<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, have_x0 ? 1 : 0, x0_full);
     return 1;
