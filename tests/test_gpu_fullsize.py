@@ -82,3 +82,44 @@ def test_fullsize_bicgstab_true_residual_and_first_iterations():
     # the oracle itself, 2 iterations (4 GEMVs with on-the-fly rows)
     xo, ho, ro = oracle.bicgstab(op, b, tol=0.0, maxit=2)
     bars(x2, h2, r2, xo, ho, ro, iters_tol=0, floor=FLOOR_BS)
+
+
+def _first50(h, ho, floor):
+    k = min(50, len(h), len(ho))
+    assert k == 50
+    d = np.abs(h[:k] - ho[:k])
+    assert np.all(d <= 1e-8 * ho[:k] + floor), float(np.max(d / ho[:k]))
+
+
+@pytest.mark.parametrize("n,iters", [(32768, 623), (65536, 840)])
+def test_cg_first_50_history_vs_oracle(n, iters):
+    """C2 / C3': the GPU's first 50 CG residuals at tol 1e-10
+    vs the oracle's own first 50 iterations (on-the-fly rows, all host cores), and
+    the expected iteration count."""
+    c = synth.spd_table(n, 1e4)
+    with ks.Context(n) as ctx:
+        b = ctx.generate("spd", seed=synth.SEED, table=c)
+        x, h, r = ctx.cg(b, tol=1e-10)
+    assert r.converged and abs(r.iterations - iters) <= 2, r
+    op = oracle.Operator(gen=synth.spec("spd", n, kappa=1e4), threads=THREADS)
+    xo, ho, ro = oracle.cg(op, b, tol=0.0, maxit=50)
+    _first50(h, ho, 1e-14)
+
+
+def test_c4_131072_one_gpu():
+    """C4 at P = 1, the largest single-GPU config (137.4 GB of A in one B200's HBM):
+    CG to tol 1e-10 vs the closed-form solution (P6), the survey's count (P14) and
+    sampled true-residual entries by the oracle (P11)."""
+    n = 131072
+    c = synth.spd_table(n, 1e4)
+    with ks.Context(n) as ctx:
+        b = ctx.generate("spd", seed=synth.SEED, table=c)
+        x, h, r = ctx.cg(b, tol=1e-10)
+    assert r.converged and abs(r.iterations - 979) <= 2, r
+    xcf = oracle.spd_exact_solve_ld(c, synth.SEED, b)
+    assert np.linalg.norm(x - xcf) <= 1e4 * 1e-10 * np.linalg.norm(xcf)
+    assert r.true_relres <= 10 * 1e-10
+    op = oracle.Operator(gen=synth.spec("spd", n, kappa=1e4), threads=min(THREADS, 8))
+    nb = float(np.linalg.norm(b))
+    for i in [0, 1, 65535, 65536, 131071]:
+        assert abs(b[i] - op.rows(i, 1, x)[0]) <= 10 * 1e-10 * nb
