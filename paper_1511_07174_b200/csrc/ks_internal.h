@@ -228,14 +228,13 @@ int launch_bicg_direction(const VecArgs& a, long long k, cudaStream_t st);
 
 // Persistent cooperative whole-iteration kernels (ks_persist.cu, NEXT-2); the
 // FP32 instantiation is the NEXT-4 path.
-// rows/unroll: the GEMV tile shape (0, 0 = default R=2, U=4; (4,2) and (4,4) selectable);
-// tma = 1: the GEMV phase streams A through a TMA bulk-copy ring (R = 2).
+// rows/unroll: the GEMV tile shape (0, 0 = default R=2, U=4; (4,2) and (4,4) selectable).
 template <class T>
-int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll, int tma);
+int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll);
 template <class T>
 int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
                    T* bpart, unsigned* bar, long long k0, long long k1, int grid, int rows, int unroll,
-                   int tma, cudaStream_t st);
+                   cudaStream_t st);
 
 // Small-n single-GPU kernels (ks_small.cu, NEXT-2): full-length vectors in every
 // CTA's shared memory, 1 (CG) / 2 (BiCGSTAB) grid barriers per iteration.

@@ -28,22 +28,10 @@ namespace {
 
 using namespace pk;
 
-// GEMV phase by streaming variant: kT = 0 LDG stream (ks_tile.cuh), 1 TMA ring.
-template <int kR, int kU, int kT, class T>
-__device__ __forceinline__ void gemv_any(const PersistArgs<T>& P, TmaRing& tr, const T* x, T* y, const T* w1,
-                                         T& d1, T& d2, T* red) {
-    if constexpr (kT == 1) gemv_phase_tma<kR>(P, tr, x, y, w1, d1, d2, red);
-    else gemv_phase<kR, kU>(P, x, y, w1, d1, d2, red);
-}
-
 // ---------------------------------------------------------------- CG (A1-A5)
-template <class T, int kR, int kU, int kT>
+template <class T, int kR, int kU>
 __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
     __shared__ T red[(kR > 2 ? kR : 2) * kNW];
-    extern __shared__ __align__(128) unsigned char ring[];
-    __shared__ __align__(8) uint64_t s_full[kTS], s_empty[kTS];
-    TmaRing tr;
-    if constexpr (kT == 1) tma_ring_init<kR>(tr, s_full, s_empty, ring);
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
@@ -54,7 +42,7 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
         if (done_flag(st)) break;
         // A1: q = A p, sigma_g = <p_loc, q>
         T d1, d2;
-        gemv_any<kR, kU, kT>(P, tr, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
+        gemv_phase<kR, kU>(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
         if (!grid_sync(P.bar, st)) return;
         T sig[1];
@@ -128,13 +116,9 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
 }
 
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
-template <class T, int kR, int kU, int kT>
+template <class T, int kR, int kU>
 __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
     __shared__ T red[(kR > 2 ? kR : 2) * kNW];
-    extern __shared__ __align__(128) unsigned char ring[];
-    __shared__ __align__(8) uint64_t s_full[kTS], s_empty[kTS];
-    TmaRing tr;
-    if constexpr (kT == 1) tma_ring_init<kR>(tr, s_full, s_empty, ring);
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
@@ -194,7 +178,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
         // B3: v = A p (own chunk of G_v[i&1]), <rhat, v>_g
         const int64_t vo = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
         T d1, d2;
-        gemv_any<kR, kU, kT>(P, tr, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red);
+        gemv_phase<kR, kU>(P, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
         if (!grid_sync(P.bar, st)) return;
         T gm[1];
@@ -242,7 +226,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
             break;
         }
         // B6: t = A s (q_loc), <t, s_loc>_g, <t, t>_g
-        gemv_any<kR, kU, kT>(P, tr, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red);
+        gemv_phase<kR, kU>(P, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red);
         if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 2] = d1; P.bpart[blockIdx.x * 4 + 3] = d2; }
         if (!grid_sync(P.bar, st)) return;
         T tv[2];
@@ -314,27 +298,21 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
 // Persistent GEMV shape: default R=2, U=4 (the sweep's best: CG 211.5 / BiCGSTAB
 // 105.3 it/s at n = 65536 vs 206.6 / 103.4 for R=4/U=2, profiles/r01_persist_sweep.json);
 // (4,2) and (4,4) selectable through KS_OPT_GEMV_ROWS / KS_OPT_GEMV_UNROLL.
-// tma = 1: the GEMV phase streams A through the TMA ring (R = 2, kTS stages).
 template <class T>
-const void* pick(int bicgstab, int rows, int unroll, int tma) {
-    if (tma) return bicgstab ? (const void*)k_bs_persist<T, 2, 4, 1> : (const void*)k_cg_persist<T, 2, 4, 1>;
+const void* pick(int bicgstab, int rows, int unroll) {
     const int shape = (rows == 4 && unroll == 2) ? 1 : (rows == 4 && unroll == 4) ? 2 : 0;
     if (bicgstab) {
-        return shape == 1 ? (const void*)k_bs_persist<T, 4, 2, 0>
-             : shape == 2 ? (const void*)k_bs_persist<T, 4, 4, 0> : (const void*)k_bs_persist<T, 2, 4, 0>;
+        return shape == 1 ? (const void*)k_bs_persist<T, 4, 2>
+             : shape == 2 ? (const void*)k_bs_persist<T, 4, 4> : (const void*)k_bs_persist<T, 2, 4>;
     }
-    return shape == 1 ? (const void*)k_cg_persist<T, 4, 2, 0>
-         : shape == 2 ? (const void*)k_cg_persist<T, 4, 4, 0> : (const void*)k_cg_persist<T, 2, 4, 0>;
+    return shape == 1 ? (const void*)k_cg_persist<T, 4, 2>
+         : shape == 2 ? (const void*)k_cg_persist<T, 4, 4> : (const void*)k_cg_persist<T, 2, 4>;
 }
-int rows_of(int rows, int unroll, int tma) {
-    return tma ? 2 : (rows == 4 && (unroll == 2 || unroll == 4)) ? 4 : 2;
-}
-size_t ring_bytes(int tma) { return tma ? (size_t)kTS * 2 * 4096 : 0; }
+int rows_of(int rows, int unroll) { return (rows == 4 && (unroll == 2 || unroll == 4)) ? 4 : 2; }
 
-int coop_grid(const void* kern, int num_sms, int64_t mmax, int R, size_t smem) {
+int coop_grid(const void* kern, int num_sms, int64_t mmax, int R) {
     int per_sm = 0;
-    if (smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, 0);
     if (per_sm < 1) per_sm = 1;
     const int64_t cap = (int64_t)per_sm * num_sms;
     const int64_t tiles = (mmax + R - 1) / R;
@@ -346,15 +324,14 @@ int coop_grid(const void* kern, int num_sms, int64_t mmax, int R, size_t smem) {
 }  // namespace
 
 template <class T>
-int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll, int tma) {
-    return coop_grid(pick<T>(bicgstab, rows, unroll, tma), num_sms, mmax, rows_of(rows, unroll, tma),
-                     ring_bytes(tma));
+int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll) {
+    return coop_grid(pick<T>(bicgstab, rows, unroll), num_sms, mmax, rows_of(rows, unroll));
 }
 
 template <class T>
 int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
                    T* bpart, unsigned* bar, long long k0, long long k1, int grid, int rows, int unroll,
-                   int tma, cudaStream_t st) {
+                   cudaStream_t st) {
     PersistArgs<T> P;
     P.a = a;
     P.A = A;
@@ -367,16 +344,16 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
     void* args[] = {&P};
     cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
     if (e != cudaSuccess) return -(int)e;
-    e = cudaLaunchCooperativeKernel(pick<T>(bicgstab, rows, unroll, tma), dim3((unsigned)grid),
-                                    dim3(kNT), args, ring_bytes(tma), st);
+    e = cudaLaunchCooperativeKernel(pick<T>(bicgstab, rows, unroll), dim3((unsigned)grid),
+                                                dim3(kNT), args, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
-template int persist_grid<double>(int, int, int64_t, int, int, int);
-template int persist_grid<float>(int, int, int64_t, int, int, int);
+template int persist_grid<double>(int, int, int64_t, int, int);
+template int persist_grid<float>(int, int, int64_t, int, int);
 template int launch_persist<double>(int, const VecArgsT<double>&, const double*, int64_t, int64_t, double*,
-                                    unsigned*, long long, long long, int, int, int, int, cudaStream_t);
+                                    unsigned*, long long, long long, int, int, int, cudaStream_t);
 template int launch_persist<float>(int, const VecArgsT<float>&, const float*, int64_t, int64_t, float*,
-                                   unsigned*, long long, long long, int, int, int, int, cudaStream_t);
+                                   unsigned*, long long, long long, int, int, int, cudaStream_t);
 
 }  // namespace ks

@@ -11,7 +11,6 @@
 #include "ks_device.cuh"
 #include "ks_internal.h"
 #include "ks_tile.cuh"
-#include "ks_tma.cuh"
 
 namespace ks {
 namespace pk {
@@ -161,114 +160,6 @@ __device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w
     }
 }
 
-
-// ---- TMA-fed GEMV phase (KS_OPT_GEMV_KERNEL = 2 in persistent mode) -----------
-// Same tiles and arithmetic order as gemv_phase, but A arrives through a per-CTA
-// shared-memory ring of kTS stages, each kR row segments of 4 KiB brought in by
-// cp.async.bulk (L2 evict-first) and completed on an mbarrier; all 8 warps
-// consume every stage (thread t: 16 bytes of each row segment) and release it on
-// a second mbarrier.  Thread 0 also produces: after consuming global step G it
-// refills up to step G + kTS - kTD, i.e. into slots released kTD steps earlier,
-// so it rarely waits on a slow warp.  The ring (and its global step counter)
-// persists across the phases of one launch; each phase drains it completely.
-constexpr int kTS = 6;   // stages in the ring
-constexpr int kTD = 2;   // refill distance (slots released kTD steps ago)
-
-struct TmaRing {
-    uint64_t* full;        // [kTS] data landed (tx count)
-    uint64_t* empty;       // [kTS] 8 warps released the slot
-    unsigned char* buf;    // kTS * kR * 4 KiB
-    unsigned long long q;  // global steps consumed so far (all threads)
-    unsigned long long next;   // next step to issue (thread 0)
-};
-
-template <int kR>
-__device__ __forceinline__ void tma_ring_init(TmaRing& tr, uint64_t* full, uint64_t* empty, unsigned char* buf) {
-    tr.full = full;
-    tr.empty = empty;
-    tr.buf = buf;
-    tr.q = 0;
-    tr.next = 0;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kTS; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kNW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-}
-
-template <int kR, class T>
-__device__ void gemv_phase_tma(const PersistArgs<T>& P, TmaRing& tr, const T* x, T* y, const T* w1, T& d1,
-                               T& d2, T* red, const T* bsub = nullptr) {
-    using V = typename Vec16<T>::type;
-    constexpr int W = Vec16<T>::W;
-    constexpr int CW = W * kNT;                       // elements per 4 KiB row segment
-    constexpr uint32_t kSeg = CW * sizeof(T);         // 4096 bytes
-    const int64_t m = m_of(P.a.L);
-    const int64_t tiles = (m + kR - 1) / kR;
-    const int64_t nst = P.ncols / CW;
-    const int64_t my_tiles = tiles > (int64_t)blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const unsigned long long G0 = tr.q, Q = (unsigned long long)(my_tiles * nst);
-    d1 = T(0);
-    d2 = T(0);
-    auto issue = [&](unsigned long long G) {          // thread 0
-        const unsigned long long l = G - G0;
-        const int64_t tile = blockIdx.x + (int64_t)(l / nst) * gridDim.x, c = (int64_t)(l % nst);
-        const int64_t r0 = tile * kR;
-        const int nvalid = (int)min((int64_t)kR, m - r0);
-        const int slot = (int)(G % kTS);
-        if (G >= (unsigned long long)kTS) mbar_wait(&tr.empty[slot], (uint32_t)(((G / kTS) - 1) & 1));
-        mbar_expect_tx(&tr.full[slot], (uint32_t)nvalid * kSeg);
-        unsigned char* dst = tr.buf + (size_t)slot * kR * kSeg;
-        for (int r = 0; r < nvalid; ++r)
-            bulk_g2s(dst + (size_t)r * kSeg, P.A + (r0 + r) * P.lda + c * CW, kSeg, &tr.full[slot],
-                     policy_evict_first());
-    };
-    if (threadIdx.x == 0) {
-        tr.next = G0;
-        while (tr.next < G0 + Q && tr.next < G0 + kTS) issue(tr.next++);
-    }
-    const T* xp = x + W * threadIdx.x;
-    for (int64_t ti = 0; ti < my_tiles; ++ti) {
-        const int64_t tile = blockIdx.x + ti * gridDim.x;
-        const int64_t r0 = tile * kR;
-        const int nvalid = (int)min((int64_t)kR, m - r0);
-        T acc[kR];
-#pragma unroll
-        for (int r = 0; r < kR; ++r) acc[r] = T(0);
-        for (int64_t c = 0; c < nst; ++c) {
-            const unsigned long long G = G0 + (unsigned long long)(ti * nst + c);
-            const int slot = (int)(G % kTS);
-            const V xv = ld_x(xp + c * CW);
-            mbar_wait(&tr.full[slot], (uint32_t)((G / kTS) & 1));
-            const unsigned char* src = tr.buf + (size_t)slot * kR * kSeg + 16 * threadIdx.x;
-#pragma unroll
-            for (int r = 0; r < kR; ++r) {
-                const V av = *reinterpret_cast<const V*>(src + (size_t)min(r, nvalid - 1) * kSeg);
-                acc[r] = fma16(av, xv, acc[r]);
-            }
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&tr.empty[slot]);
-            if (threadIdx.x == 0)
-                while (tr.next < G0 + Q && tr.next + kTD <= G + kTS) issue(tr.next++);
-        }
-        block_sum<kNT, kR>(acc, red);
-        if (threadIdx.x == 0) {
-#pragma unroll
-            for (int r = 0; r < kR; ++r) {
-                if (r < nvalid) {
-                    const T yv = bsub ? bsub[r0 + r] - acc[r] : acc[r];
-                    y[r0 + r] = yv;
-                    if (w1) d1 = fma(w1[r0 + r], yv, d1);
-                    d2 = fma(yv, yv, d2);
-                }
-            }
-        }
-    }
-    tr.q = G0 + Q;
-}
 
 }  // namespace
 }  // namespace pk

@@ -37,10 +37,6 @@ int small_path_grid(const ks_ctx* c, const Rank& r, int bicgstab) {
     return g;
 }
 
-// GEMV streaming variant of the persistent kernels: KS_OPT_GEMV_KERNEL = 2 selects
-// the TMA ring, anything else the LDG stream.
-int persist_tma(const ks_ctx* c) { return c->opt.gemv_kernel == 2 ? 1 : 0; }
-
 struct Prof {
     ks_ctx* c;
     Rank& r;
@@ -91,7 +87,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     if (persist) sgrid = small_path_grid<double>(c, r, kind);
     if (persist && sgrid == 0) {
         persist_shape(c, r, &prows, &punroll);
-        pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, prows, punroll, persist_tma(c));
+        pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, prows, punroll);
         if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
     }
     const bool use_graph = !persist && c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
@@ -132,7 +128,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
                                        r.scr.ticket + 8, k, kend, sgrid, r.stream)
                 : launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
                                          r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
-                                         prows, punroll, persist_tma(c), r.stream);
+                                         prows, punroll, r.stream);
             prof.post(slot);
             if (rc < 0) KS_CUDA((cudaError_t)(-rc));
             r.launches += 1;
@@ -412,7 +408,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     Prof prof(c, r, 1);
     int prows = 0, punroll = 0;
     persist_shape(c, r, &prows, &punroll);
-    int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, prows, punroll, persist_tma(c));
+    int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, prows, punroll);
     if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
     const int sgrid = small_path_grid<float>(c, r, bicgstab);
     float* bpart = reinterpret_cast<float*>(r.scr.part + 2 * kPartStride);
@@ -427,8 +423,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
             ? launch_small<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld, bpart,
                                   r.scr.ticket + 8, k, kend, sgrid, r.stream)
             : launch_persist<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld,
-                                    bpart, r.scr.ticket + 8, k, kend, pgrid, prows, punroll, persist_tma(c),
-                                    r.stream);
+                                    bpart, r.scr.ticket + 8, k, kend, pgrid, prows, punroll, r.stream);
         prof.post(slot);
         if (rc < 0) KS_CUDA((cudaError_t)(-rc));
         r.launches += 1;

@@ -190,28 +190,6 @@ def test_multi_gmres(P, persistent):
 
 @needs2
 @pytest.mark.parametrize("P", [2, 4])
-def test_multi_persistent_tma_ring(P):
-    """P GPUs, persistent + fused: the TMA-fed GEMV phase gives the same bits as the
-    LDG stream (same tiles, same order), and meets the bars vs the oracle."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
-    n = 8191
-    A, b = synth.gdd(n, 16)
-    xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
-    outs = []
-    for variant in (1, 2):
-        with ks.Context(n, ngpus=P) as ctx:
-            ctx.set_option("gemv_kernel", variant)
-            ctx.load_rows(A)
-            assert ctx.get_option("persistent") == 1 and ctx.get_option("fused_comm") == 1
-            outs.append(ctx.bicgstab(b, tol=1e-10))
-    (x1, h1, r1), (x2, h2, r2) = outs
-    assert r1.iterations == r2.iterations and np.array_equal(x1, x2) and np.array_equal(h1, h2)
-    bars(x2, h2, r2, xo, ho, ro, floor=FLOOR_BS)
-
-
-@needs2
-@pytest.mark.parametrize("P", [2, 4])
 def test_multi_f32(P):
     """NEXT-4 at P GPUs: FP32 persistent kernels with the fused NVLink exchange."""
     if ngpu() < P:

@@ -694,31 +694,3 @@ def test_out_of_memory_is_reported_and_recoverable():
         ctx.load_rows(np.eye(64) * 2.0)
         x, h, r = ctx.cg(np.ones(64), tol=1e-12)
         assert r.converged and np.allclose(x, 0.5)
-
-
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_persistent_tma_ring_bitwise_equal_ldg(dtype):
-    """Persistent kernels with the TMA-fed GEMV phase (KS_OPT_GEMV_KERNEL = 2) run
-    the same tiles in the same arithmetic order as the LDG stream: bitwise-equal x
-    and history, on ragged n (tail tile, partial ring) and multi-batch runs."""
-    for n, method in [(3001, "cg"), (4096, "bicgstab"), (6000, "cg")]:
-        if method == "cg":
-            A = synth.random_spd(n, 100.0, 7)
-            b = np.random.default_rng(n).standard_normal(n)
-        else:
-            A, b = synth.gdd(n, 16)
-        tol = 1e-10 if dtype == "f64" else 1e-5
-        outs = []
-        for variant in (1, 2):
-            with ks.Context(n, dtype=dtype) as ctx:
-                ctx.set_option("small", 0)
-                ctx.set_option("persistent", 1)
-                ctx.set_option("gemv_kernel", variant)
-                ctx.set_option("poll_batch", 5)
-                ctx.load_rows(A)
-                outs.append(getattr(ctx, method)(b, tol=tol))
-        (x1, h1, r1), (x2, h2, r2) = outs
-        assert r1.iterations == r2.iterations and np.array_equal(x1, x2) and np.array_equal(h1, h2), (n, method)
-        if dtype == "f64":
-            xo, ho, ro = getattr(oracle, method)(A, b, tol=tol)
-            bars(x2, h2, r2, xo, ho, ro, floor=FLOOR_CG if method == "cg" else FLOOR_BS)
