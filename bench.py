@@ -11,7 +11,7 @@ ks_bicgstab(maxit=K) with tol = 0 (fixed length), inputs resident on the device,
 bracketed by barrier + synchronize, CUDA events on the stream the library runs
 on (torch's current stream, borrowed), max over ranks.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 65536]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--size 65536]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 --impl reference times the CPU oracle (oracle/, the only baseline this paper
@@ -426,7 +426,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--size", dest="n", type=int, default=65536)   # not "--n": torchrun would take it as an abbreviation of its own options
     ap.add_argument("--cpu-rows", type=int, default=2048)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=512)

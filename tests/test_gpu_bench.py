@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("n", [4096, 8192])
 def test_bench_json_contract(n):
-    out = subprocess.run([sys.executable, "bench.py", "--n", str(n), "--steps", "5", "--warmup", "3",
+    out = subprocess.run([sys.executable, "bench.py", "--size", str(n), "--steps", "5", "--warmup", "3",
                           "--cpu-rows", "64", "--cpu-budget", "2"], cwd=ROOT, capture_output=True,
                          text=True, timeout=600, check=True).stdout
     lines = out.strip().splitlines()
