@@ -80,7 +80,7 @@ __device__ bool xch_vec(const PersistArgs<double>& P, const double* src, unsigne
         const double v = src[i];
         for (int g = 0; g < L.P; ++g) a.pp.G_r[g][off + (int64_t)L.rank * L.chunk + i] = v;
     }
-    __threadfence_system();
+    if (tid0 < m) __threadfence_system();   // only threads that stored remotely
     if (!grid_sync(P.bar, st)) return false;
     if (lead()) xflag(a, kPhaseR, e);
     if (!xwait(a, kPhaseR, e)) return false;

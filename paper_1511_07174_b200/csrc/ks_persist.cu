@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
             }
             acc[0] = fma(r, r, acc[0]);
         }
-        if (a.peer) __threadfence_system();
+        if (a.peer && tid0 < m) __threadfence_system();   // only threads that stored remotely
         block_sum<kNT, 1>(acc, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = acc[0];
         if (!grid_sync(P.bar, st)) return;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
             acc[0] = fma(a.rhat_loc[l], r, acc[0]);
             acc[1] = fma(r, r, acc[1]);
         }
-        if (a.peer) __threadfence_system();
+        if (a.peer && tid0 < m) __threadfence_system();   // only threads that stored remotely
         block_sum<kNT, 2>(acc, red);
         if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 0] = acc[0]; P.bpart[blockIdx.x * 4 + 1] = acc[1]; }
         if (!grid_sync(P.bar, st)) return;
