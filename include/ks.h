@@ -8,7 +8,7 @@
  * implemented at PAPER.md:78 and PAPER.md:109).  The recurrences are the
  * textbook ones written out in SURVEY.md sec.8(c).3 (CG) and sec.8(c).4
  * (BiCGSTAB); every reading of a point the paper leaves open is listed in
- * DESIGN.md ("Readings", Q1-Q26).  Parallelism is hidden behind an opaque
+ * DESIGN.md ("Readings", Q1-Q27).  Parallelism is hidden behind an opaque
  * object, as the paper asks ("encapsulation of data and distribution and
  * communication in opaque objects").
  *
