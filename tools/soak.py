@@ -1,0 +1,51 @@
+"""Soak test of the fused multi-GPU protocols: many back-to-back solves of random
+size / method / maxit / tolerance on P GPUs (one context per (n, method) kept alive
+and reused, so epochs, parities and the barrier counter roll over many solves).
+Every result is checked: converged solves by the true residual, fixed-length runs by
+bitwise repeatability.  Prints one summary JSON line."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_1511_07174_b200 as ks
+import synth
+
+P = min(int(sys.argv[1]) if len(sys.argv) > 1 else 4, torch.cuda.device_count())
+rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+rng = np.random.default_rng(2024)
+ctxs, fails, stats = {}, [], {"solves": 0, "iters": 0}
+t0 = time.time()
+for it in range(rounds):
+    n = int(rng.choice([1000, 2049, 4096, 5003]))
+    method = str(rng.choice(["cg", "bicgstab", "bicg", "gmres"]))
+    if method == "cg" and n % 2:
+        n += 1                                   # G-SPD needs an even n
+    key = (n, method)
+    if key not in ctxs:
+        c = ks.Context(n, ngpus=P)
+        if method == "cg":
+            c.generate("spd", seed=synth.SEED, table=synth.spd_table(n, 1e3), want_b=False)
+        else:
+            c.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        c.set_option("poll_batch", int(rng.choice([1, 3, 16])))
+        ctxs[key] = c
+    c = ctxs[key]
+    b = synth.rhs(n, synth.SEED + it)
+    kw = {"restart": int(rng.choice([5, 20]))} if method == "gmres" else {}
+    fixed = rng.random() < 0.3
+    if fixed:
+        mx = int(rng.integers(1, 12))
+        x1, h1, r1 = getattr(c, method)(b, tol=0.0, maxit=mx, **kw)
+        x2, h2, r2 = getattr(c, method)(b, tol=0.0, maxit=mx, **kw)
+        if not (r1.iterations == r2.iterations and np.array_equal(x1, x2) and np.array_equal(h1, h2)):
+            fails.append({"round": it, "n": n, "method": method, "why": "not repeatable"})
+    else:
+        x, h, r = getattr(c, method)(b, tol=1e-10, **kw)
+        if not (r.converged and r.true_relres <= 1e-8):
+            fails.append({"round": it, "n": n, "method": method, "why": f"status {r.status} true {r.true_relres}"})
+        stats["iters"] += r.iterations
+    stats["solves"] += 1
+for c in ctxs.values():
+    c.close()
+print(json.dumps({"P": P, "rounds": rounds, "contexts": len(ctxs), "fails": fails, **stats,
+                  "seconds": time.time() - t0}))
