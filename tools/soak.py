@@ -10,7 +10,15 @@ import torch
 import paper_1511_07174_b200 as ks
 import synth
 
-P = min(int(sys.argv[1]) if len(sys.argv) > 1 else 4, torch.cuda.device_count())
+WORLD = int(os.environ.get("WORLD_SIZE", 1))          # torchrun: one process per GPU
+if WORLD > 1:
+    import torch.distributed as dist
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = WORLD
+else:
+    P = min(int(sys.argv[1]) if len(sys.argv) > 1 else 4, torch.cuda.device_count())
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 rng = np.random.default_rng(2024)
 ctxs, fails, stats = {}, [], {"solves": 0, "iters": 0}
@@ -22,7 +30,7 @@ for it in range(rounds):
         n += 1                                   # G-SPD needs an even n
     key = (n, method)
     if key not in ctxs:
-        c = ks.Context(n, ngpus=P)
+        c = ks.Context.from_process_group(n) if WORLD > 1 else ks.Context(n, ngpus=P)
         if method == "cg":
             c.generate("spd", seed=synth.SEED, table=synth.spd_table(n, 1e3), want_b=False)
         else:
@@ -47,5 +55,8 @@ for it in range(rounds):
     stats["solves"] += 1
 for c in ctxs.values():
     c.close()
-print(json.dumps({"P": P, "rounds": rounds, "contexts": len(ctxs), "fails": fails, **stats,
-                  "seconds": time.time() - t0}))
+if WORLD == 1 or dist.get_rank() == 0:
+    print(json.dumps({"P": P, "mode": "torchrun" if WORLD > 1 else "single-process", "rounds": rounds,
+                      "contexts": len(ctxs), "fails": fails, **stats, "seconds": time.time() - t0}))
+if WORLD > 1:
+    dist.destroy_process_group()
