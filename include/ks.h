@@ -98,7 +98,9 @@ typedef struct {
 typedef enum {
     KS_OPT_TRUE_RESIDUAL = 0, /* 1 (default): report true_relres (one extra GEMV) */
     KS_OPT_PROFILE_GEMV = 1,  /* 1: time every K1 launch with CUDA events         */
-    KS_OPT_POLL_BATCH = 2,    /* iterations queued between done-flag polls (16)   */
+    KS_OPT_POLL_BATCH = 2,    /* iterations per done-flag poll; 0 (default) =     */
+                              /* auto: the whole solve in one persistent launch,  */
+                              /* 16 on the multi-kernel path                      */
     KS_OPT_GEMV_ROWS = 3,     /* K1 rows per CTA tile: 2, 4, 8, 16 (0 = auto)     */
     KS_OPT_GEMV_SPLIT = 4,    /* K1 column splits per tile (0 = auto)             */
     KS_OPT_GEMV_KERNEL = 5,   /* K1 variant: 0 = auto, 1 = LDG stream, 2 = TMA    */

@@ -478,7 +478,7 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
         case KS_OPT_TRUE_RESIDUAL: o.true_residual = v ? 1 : 0; break;
         case KS_OPT_PROFILE_GEMV: o.profile_gemv = v ? 1 : 0; break;
         case KS_OPT_POLL_BATCH:
-            if (v < 1 || v > 4096) return fail(c, KS_EARG, "poll batch must be in [1, 4096]");
+            if (v < 0 || v > 4096) return fail(c, KS_EARG, "poll batch must be in [0, 4096]");
             o.poll_batch = v; break;
         case KS_OPT_GEMV_ROWS:
             if (v != 0 && v != 2 && v != 4 && v != 8 && v != 16) return fail(c, KS_EARG, "rows must be 0, 2, 4, 8 or 16");

@@ -106,7 +106,7 @@ struct Rank {
 struct Options {
     int64_t true_residual = 1;
     int64_t profile_gemv = 0;
-    int64_t poll_batch = 16;
+    int64_t poll_batch = 0;   // 0 = auto: whole solve per persistent launch, else 16
     int64_t gemv_rows = 0;
     int64_t gemv_split = 0;
     int64_t gemv_kernel = 0;

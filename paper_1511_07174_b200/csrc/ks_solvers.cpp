@@ -37,6 +37,14 @@ int small_path_grid(const ks_ctx* c, const Rank& r, int bicgstab) {
     return g;
 }
 
+// Iterations per host poll.  KS_OPT_POLL_BATCH = 0 (auto): a persistent kernel runs
+// the whole solve in one launch (it stops itself on convergence, so nothing is
+// wasted and no launch gap remains); the multi-kernel path queues 16 iterations.
+int64_t poll_batch(const ks_ctx* c, bool persist, int64_t maxit) {
+    if (c->opt.poll_batch > 0) return c->opt.poll_batch;
+    return persist ? std::max<int64_t>(1, maxit) : 16;
+}
+
 struct Prof {
     ks_ctx* c;
     Rank& r;
@@ -79,8 +87,8 @@ struct Prof {
 // iteration base from r.kdev, which the graph's last node advances by B.
 template <class IterFn>
 void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, IterFn&& iter) {
-    const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
     const bool persist = c->persistent();
+    const int64_t B = poll_batch(c, persist, maxit);
     Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
     int pgrid = 0, sgrid = 0;
     int prows = 0, punroll = 0;
@@ -403,7 +411,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
     r.launches += launch_init_f32(a, bicgstab, tol, maxit, hist_cap, ebase, r.stream);
-    const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
+    const int64_t B = poll_batch(c, true, maxit);
     const int gemvs = bicgstab ? 2 : 1;
     Prof prof(c, r, 1);
     int prows = 0, punroll = 0;
@@ -669,7 +677,7 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
     pq.out1 = r.S + (int64_t)r.rank * kScalSlot;
     pq.done = &r.st->done;
     if (fused) fuse_gemv(c, r, pq, kPhaseS, nullptr, 0, r.pp.S, (int64_t)r.rank * kScalSlot, a.spar);
-    const int64_t B = std::max<int64_t>(1, c->opt.poll_batch);
+    const int64_t B = poll_batch(c, false, maxit);
     Prof prof(c, r, 2 * B);
     int64_t k = 1, batch = 0;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));

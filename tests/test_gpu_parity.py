@@ -664,7 +664,7 @@ def test_c_example_runs():
 def test_option_validation_and_roundtrip():
     """ks_set_option rejects out-of-range values with KS_EARG and keeps the old
     value; accepted values read back (effective values for fused_comm/persistent)."""
-    bad = {"poll_batch": [0, 5000], "gemv_rows": [3, 32], "gemv_split": [-1, 65], "gemv_kernel": [3],
+    bad = {"poll_batch": [-1, 5000], "gemv_rows": [3, 32], "gemv_split": [-1, 65], "gemv_kernel": [3],
            "persistent": [3, -1], "gemv_unroll": [3, 16], "persist_grid": [-1], "gemvt_shape": [203, 304, 4],
            "small": [3, -1]}
     good = {"poll_batch": 7, "gemv_rows": 4, "gemv_split": 2, "gemv_kernel": 1, "gemv_unroll": 2,
