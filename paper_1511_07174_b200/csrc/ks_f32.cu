@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include "ks_device.cuh"
+#include "ks_common.cuh"
 #include "ks_internal.h"
 
 namespace ks {
@@ -21,23 +22,11 @@ namespace {
 constexpr int kNT = 256;
 using VA = VecArgsT<float>;
 
-__device__ __forceinline__ int64_t mloc(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
-__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
-__device__ __forceinline__ int64_t gidx(const Layout& L, int64_t j) {
-    int g = 0;
-    while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
-    return (int64_t)g * L.chunk + (j - L.row0[g]);
-}
-__device__ __forceinline__ float slots(const Layout& L, const float* G, int q) {
-    float s = 0.0f;
-    for (int g = 0; g < L.P; ++g) s += G[(int64_t)g * L.chunk + L.pslot + q];
-    return s;
-}
 
 // r0 = b (x0 = 0), x = 0, rhat = r0, slots <r0, r0>
 __global__ void __launch_bounds__(kNT) k_setup_r_f32(VA a) {
     __shared__ float red[kNT / 32];
-    const int64_t m = mloc(a.L), r0 = a.L.row0[a.L.rank];
+    const int64_t m = rows_of(a.L), r0 = a.L.row0[a.L.rank];
     float* rl = a.G_r + (int64_t)a.L.rank * a.L.chunk;
     float acc[1] = {0.0f};
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
@@ -80,7 +69,7 @@ __global__ void __launch_bounds__(kNT) k_init_f32(VA a, int bicgstab, double tol
         for (int q = 0; q < 4; ++q) st->rho[q] = st->alpha[q] = st->omega[q] = 1.0;
         const float nb = sqrtf(acc[0]);
         st->nb = nb;
-        const float rr = slots(a.L, a.G_r, 1);
+        const float rr = slot_sum(a.L, a.G_r, 1);
         if (!bicgstab) st->rho[0] = rr;
         if (nb == 0.0f) {
             st->bzero = 1; st->converged = 1; st->status = KS_OK; st->relres = 0.0; st->done = 1;
@@ -106,7 +95,7 @@ __global__ void __launch_bounds__(kNT) k_finish_f32(VA a, int bicgstab) {
         st->iters = maxit;
         st->status = KS_EMAXIT;
         if (bicgstab && maxit >= 1) {
-            const float rel = sqrtf(slots(a.L, a.G_r + (maxit & 1) * a.gpar, 1)) / (float)st->nb;
+            const float rel = sqrtf(slot_sum(a.L, a.G_r + (maxit & 1) * a.gpar, 1)) / (float)st->nb;
             if (a.hist && maxit - 1 < st->hist_cap) a.hist[maxit - 1] = rel;
             st->relres = rel;
             if (rel <= (float)st->tol) { st->converged = 1; st->status = KS_OK; }
@@ -114,14 +103,14 @@ __global__ void __launch_bounds__(kNT) k_finish_f32(VA a, int bicgstab) {
         st->done = 1;
     }
     if (st->bzero) {
-        const int64_t m = mloc(a.L);
+        const int64_t m = rows_of(a.L);
         for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
             a.x_loc[i] = 0.0f;
     }
 }
 
 __global__ void __launch_bounds__(kNT) k_pack_x_f32(VA a) {
-    const int64_t m = mloc(a.L);
+    const int64_t m = rows_of(a.L);
     float* xl = a.G_v + (int64_t)a.L.rank * a.L.chunk;
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
         xl[i] = a.x_loc[i];

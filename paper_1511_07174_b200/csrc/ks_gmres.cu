@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include "ks_device.cuh"
+#include "ks_common.cuh"
 #include "ks_internal.h"
 
 namespace ks {
@@ -27,15 +28,8 @@ namespace {
 constexpr int kNT = 256;
 constexpr int kNW = kNT / 32;
 
-__device__ __forceinline__ int64_t mloc(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
-__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
 __device__ __forceinline__ bool done_or_ended(const GmresArgs& g) {
     return *(volatile const int*)&g.a.st->done != 0 || *(volatile const int*)&g.gs->cycle_end != 0;
-}
-__device__ __forceinline__ int64_t gidx(const Layout& L, int64_t j) {
-    int g = 0;
-    while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
-    return (int64_t)g * L.chunk + (j - L.row0[g]);
 }
 __device__ __forceinline__ double* Vcol(const GmresArgs& g, int i) { return g.V + (int64_t)i * g.ldv; }
 
@@ -73,7 +67,7 @@ __device__ void multidot_finish(const GmresArgs& g, const double* vals, int nv, 
 // ends up with the block's nv partials in `vals` (shared).
 __device__ void block_multidot(const GmresArgs& g, const double* w, int nv, double* vals) {
     __shared__ double red[8 * kNW];
-    const int64_t m = mloc(g.a.L);
+    const int64_t m = rows_of(g.a.L);
     for (int i0 = 0; i0 < nv; i0 += 8) {
         double acc[8];
 #pragma unroll
@@ -114,7 +108,7 @@ __global__ void __launch_bounds__(kNT) k_gm_orth(GmresArgs g, int j, int pass) {
         h[threadIdx.x] = s;
     }
     __syncthreads();
-    const int64_t m = mloc(L);
+    const int64_t m = rows_of(L);
     double* w = g.a.q_loc;
     if (pass == 1) {
         // update, then pass-2 partial dots on the updated elements
@@ -170,7 +164,7 @@ __global__ void __launch_bounds__(kNT) k_gm_step_end(GmresArgs g, int j, long lo
     double nrm2 = 0.0;
     for (int q = 0; q < L.P; ++q) nrm2 += g.hx[(int64_t)q * kMaxBasis];
     const double hn = sqrt(nrm2);
-    const int64_t m = mloc(L);
+    const int64_t m = rows_of(L);
     double* vn = Vcol(g, j + 1);
     double* gown = g.a.G_r + (int64_t)L.rank * L.chunk;
     if (hn != 0.0) {
@@ -229,7 +223,7 @@ __global__ void __launch_bounds__(kNT) k_gm_start(GmresArgs g) {
         if (lead()) { st->relres = rel; st->converged = 1; st->status = KS_OK; st->done = 1; g.gs->skip = 1; }
         return;
     }
-    const int64_t m = mloc(L);
+    const int64_t m = rows_of(L);
     double* v0 = Vcol(g, 0);
     double* gown = g.a.G_r + (int64_t)L.rank * L.chunk;
     for (int64_t e = blockIdx.x * (int64_t)kNT + threadIdx.x; e < m; e += (int64_t)gridDim.x * kNT) {
@@ -264,7 +258,7 @@ __global__ void __launch_bounds__(kNT) k_gm_cycle_end(GmresArgs g, long long k_e
         }
     }
     __syncthreads();
-    const int64_t m = mloc(g.a.L);
+    const int64_t m = rows_of(g.a.L);
     for (int64_t e = blockIdx.x * (int64_t)kNT + threadIdx.x; e < m; e += (int64_t)gridDim.x * kNT) {
         double xe = g.a.x_loc[e];
         for (int i = 0; i < jd; ++i) xe = fma(y[i], Vcol(g, i)[e], xe);

@@ -74,7 +74,7 @@ __device__ bool xch_vec(const PersistArgs<double>& P, const double* src, unsigne
     const VecArgs& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
-    const int64_t m = m_of(L), off = (int64_t)(s & 1) * a.gpar;
+    const int64_t m = rows_of(L), off = (int64_t)(s & 1) * a.gpar;
     const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x, gstride = (int64_t)gridDim.x * kNT;
     for (int64_t i = tid0; i < m; i += gstride) {
         const double v = src[i];
@@ -86,7 +86,7 @@ __device__ bool xch_vec(const PersistArgs<double>& P, const double* src, unsigne
     if (!xwait(a, kPhaseR, e)) return false;
     for (int64_t j = tid0; j < L.n; j += gstride) {
         int o;
-        dst[j] = __ldcg(a.G_r + off + gidx_p(L, j, &o));
+        dst[j] = __ldcg(a.G_r + off + gidx_owner(L, j, &o));
     }
     return grid_sync(P.bar, st);
 }
@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(kNT, 4) k_gm_cycle(GPArgs A) {
     const GmresArgs& g = A.g;
     const Layout& L = a.L;
     DevState* st = a.st;
-    if (done_flag(st)) return;
-    const int64_t m = m_of(L);
+    if (is_done(st)) return;
+    const int64_t m = rows_of(L);
     const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x, gstride = (int64_t)gridDim.x * kNT;
     long long k = *(volatile const long long*)&st->iters;   // inner steps completed so far
     const long long maxit = st->maxit;

@@ -35,11 +35,11 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
-    const int64_t m = m_of(L), r0 = L.row0[L.rank];
+    const int64_t m = rows_of(L), r0 = L.row0[L.rank];
     const int64_t gstride = (int64_t)gridDim.x * kNT;
     const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
     for (long long k = P.k0; k <= P.k1; ++k) {
-        if (done_flag(st)) break;
+        if (is_done(st)) break;
         // A1: q = A p, sigma_g = <p_loc, q>
         T d1, d2;
         gemv_phase<kR, kU>(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
@@ -88,13 +88,13 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
                 flags_out(a, kPhaseR, k);
             }
             if (!wait_ph(a, kPhaseR, k)) return;
-            rho1 = slots_sum(L, par_ptr(a.G_r, a.gpar, k), 1);
+            rho1 = slot_sum(L, par_ptr(a.G_r, a.gpar, k), 1);
         }
         // A5: test, beta, p = r + beta p (full, replicated)
         const T rel = sqrt(rho1) / (T)st->nb;
         if (rel <= (T)st->tol) {
             if (lead()) {
-                hist_put(st, a.hist, k - 1, rel);
+                put_hist(st, a.hist, k - 1, rel);
                 st->relres = rel; st->iters = k; st->converged = 1; st->status = KS_OK; st->done = 1;
             }
             break;
@@ -103,11 +103,11 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
         const T* Gr = par_ptr(a.G_r, a.gpar, k);
         for (int64_t j = tid0; j < L.n; j += gstride) {
             int o;
-            const int64_t gj = gidx_p(L, j, &o);
+            const int64_t gj = gidx_owner(L, j, &o);
             a.p_full[j] = fma(beta, a.p_full[j], Gr[gj]);
         }
         if (lead()) {
-            hist_put(st, a.hist, k - 1, rel);
+            put_hist(st, a.hist, k - 1, rel);
             st->relres = rel; st->iters = k; st->rho[k & 3] = rho1; st->alpha[k & 3] = alpha;
             if (!a.peer) a.G_r[ro + L.pslot + 1] = rho1;    // for the multi-kernel path / finish
         }
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
-    const int64_t m = m_of(L), r0 = L.row0[L.rank];
+    const int64_t m = rows_of(L), r0 = L.row0[L.rank];
     const int64_t gstride = (int64_t)gridDim.x * kNT;
     const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
     // scalars of the previous iteration (written by the previous launch / init)
@@ -130,20 +130,20 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
     T omega_prev = (T)st->omega[(P.k0 - 1) & 3];
     T rho_next = T(0), rr_next = T(0);
     for (long long i = P.k0; i <= P.k1; ++i) {
-        if (done_flag(st)) break;
+        if (is_done(st)) break;
         // B8 (test of i-1) + B1
         if (a.peer && i >= 2 && !wait_ph(a, kPhaseR, i - 1)) return;
         const T* Gr = par_ptr(a.G_r, a.gpar, i - 1);
         // P == 1: after the first iteration of a launch the partials are in registers
         // (every CTA computed them), so no barrier is needed to read the lead's slots
         const bool carried = !a.peer && i > P.k0;
-        const T rho = carried ? rho_next : slots_sum(L, Gr, 0);
+        const T rho = carried ? rho_next : slot_sum(L, Gr, 0);
         T rel = T(0);
         if (i >= 2) {
-            rel = sqrt(carried ? rr_next : slots_sum(L, Gr, 1)) / (T)st->nb;
+            rel = sqrt(carried ? rr_next : slot_sum(L, Gr, 1)) / (T)st->nb;
             if (rel <= (T)st->tol) {
                 if (lead()) {
-                    hist_put(st, a.hist, i - 2, rel);
+                    put_hist(st, a.hist, i - 2, rel);
                     st->relres = rel; st->iters = i - 1; st->converged = 1; st->status = KS_OK; st->done = 1;
                 }
                 break;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
         }
         if (rho == T(0) || !isfinite(rho)) {
             if (lead()) {
-                if (i >= 2) { hist_put(st, a.hist, i - 2, rel); st->relres = rel; }
+                if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
                 st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1;
             }
             break;
@@ -159,18 +159,18 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
         if (i == 1) {
             for (int64_t j = tid0; j < L.n; j += gstride) {
                 int o;
-                a.p_full[j] = Gr[gidx_p(L, j, &o)];
+                a.p_full[j] = Gr[gidx_owner(L, j, &o)];
             }
         } else {
             const T beta = (rho / rho_prev) * (alpha_prev / omega_prev);
             for (int64_t j = tid0; j < L.n; j += gstride) {
                 int o;
-                const int64_t gj = gidx_p(L, j, &o);
+                const int64_t gj = gidx_owner(L, j, &o);
                 a.p_full[j] = fma(beta, fma(-omega_prev, a.v_full[j], a.p_full[j]), Gr[gj]);
             }
         }
         if (lead()) {
-            if (i >= 2) { hist_put(st, a.hist, i - 2, rel); st->relres = rel; }
+            if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
             st->rho[i & 3] = rho;
             st->iters = i - 1;
         }
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
                 flags_out(a, kPhaseV, i);
             }
             if (!wait_ph(a, kPhaseV, i)) return;
-            gam = slots_sum(L, par_ptr(a.G_v, a.gpar, i), 0);
+            gam = slot_sum(L, par_ptr(a.G_v, a.gpar, i), 0);
         }
         if (gam == T(0) || !isfinite(gam)) {
             if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
         T sacc[1] = {T(0)};
         for (int64_t j = tid0; j < L.n; j += gstride) {
             int o;
-            const int64_t gj = gidx_p(L, j, &o);
+            const int64_t gj = gidx_owner(L, j, &o);
             const T v = a.peer ? __ldcg(a.pp.G_v[o] + (i & 1) * a.gpar + gj)
                                     : a.G_v[(i & 1) * a.gpar + gj];
             a.v_full[j] = v;
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
         if (srel <= (T)st->tol) {                          // half-step exit
             for (int64_t l = tid0; l < m; l += gstride) a.x_loc[l] = fma(alpha, a.p_full[r0 + l], a.x_loc[l]);
             if (lead()) {
-                hist_put(st, a.hist, i - 1, srel);
+                put_hist(st, a.hist, i - 1, srel);
                 st->alpha[i & 3] = alpha;
                 st->relres = srel; st->half = 1; st->half_iter = i; st->converged = 1;
                 st->status = KS_OK; st->iters = i; st->done = 1;

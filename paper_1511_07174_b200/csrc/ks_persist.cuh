@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "ks_device.cuh"
+#include "ks_common.cuh"
 #include "ks_internal.h"
 #include "ks_tile.cuh"
 
@@ -21,36 +22,9 @@ constexpr int kNW = kNT / 32;
 // GEMV tile shape of the persistent kernels (rows R x unrolled column blocks U);
 // instantiated for the shapes the tuning sweep found at the streaming ceiling.
 
-// -- small helpers (the same conventions as ks_vec.cu) ------------------------
-__device__ __forceinline__ int64_t m_of(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
-__device__ __forceinline__ int64_t gidx_p(const Layout& L, int64_t j, int* owner) {
-    int g = 0;
-    while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
-    *owner = g;
-    return (int64_t)g * L.chunk + (j - L.row0[g]);
-}
+// -- small helpers (layout / state accessors are shared: ks_common.cuh) ---------
 template <class T>
 __device__ __forceinline__ T* par_ptr(T* G, int64_t par, long long k) { return G + (k & 1) * par; }
-__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
-__device__ __forceinline__ bool done_flag(const DevState* st) { return *(volatile const int*)&st->done != 0; }
-__device__ __forceinline__ unsigned long long epoch(const DevState* st, long long k) {
-    return *(volatile const unsigned long long*)&st->ebase + (unsigned long long)k;
-}
-template <class T>
-__device__ __forceinline__ T slots_sum(const Layout& L, const T* G, int q) {
-    T s = T(0);
-    for (int g = 0; g < L.P; ++g) s += G[(int64_t)g * L.chunk + L.pslot + q];
-    return s;
-}
-template <class T>
-__device__ __forceinline__ T scal_sum(const Layout& L, const T* S, int q) {
-    T s = T(0);
-    for (int g = 0; g < L.P; ++g) s += S[g * kScalSlot + q];
-    return s;
-}
-__device__ __forceinline__ void hist_put(DevState* st, double* hist, long long k1, double v) {
-    if (hist && k1 >= 0 && k1 < st->hist_cap) hist[k1] = v;
-}
 
 // Grid-wide barrier (all CTAs co-resident: cooperative launch).  One 64-bit
 // arrival counter, zeroed by the launcher before every launch and never reset
@@ -108,7 +82,7 @@ __device__ __forceinline__ void grid_total(const T* bpart, int q0, T (&out)[K], 
 // Fused-mode wait for phase ph of iteration k from every rank (all CTAs).
 template <class T>
 __device__ __forceinline__ bool wait_ph(const VecArgsT<T>& a, int ph, long long k) {
-    const bool ok = wait_flags(a.flags + ph * kMaxRanks, a.L.P, epoch(a.st, k));
+    const bool ok = wait_flags(a.flags + ph * kMaxRanks, a.L.P, epoch_of(a.st, k));
     if (!ok && threadIdx.x == 0) { a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1; }
     return ok;
 }
@@ -116,7 +90,7 @@ template <class T>
 __device__ __forceinline__ void flags_out(const VecArgsT<T>& a, int ph, long long k) {
     unsigned long long* f[kMaxRanks];
     for (int g = 0; g < a.L.P; ++g) f[g] = a.pp.flags[g] + ph * kMaxRanks + a.L.rank;
-    publish_flags(f, a.L.P, epoch(a.st, k));
+    publish_flags(f, a.L.P, epoch_of(a.st, k));
 }
 
 template <class T>
@@ -135,7 +109,7 @@ struct PersistArgs {
 template <int kR, int kU, class T>
 __device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w1, T& d1, T& d2,
                            T* red, const T* bsub = nullptr) {
-    const int64_t m = m_of(P.a.L);
+    const int64_t m = rows_of(P.a.L);
     const int64_t tiles = (m + kR - 1) / kR;
     const int64_t ncb = P.ncols / (Vec16<T>::W * kNT);
     d1 = T(0);

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kNT, 2) k_cg_small(PersistArgs<T> P) {
     const int64_t n = L.n;
     const int64_t gstride = (int64_t)gridDim.x * kNT;
     const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
-    if (done_flag(st)) return;
+    if (is_done(st)) return;
     {
         const T* rin = par_ptr(a.G_r, a.gpar, P.k0 - 1);
         for (int64_t j = threadIdx.x; j < P.ncols; j += kNT) {
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kNT, 2) k_cg_small(PersistArgs<T> P) {
         T* rout = par_ptr(a.G_r, a.gpar, k);
         for (int64_t i = tid0; i < n; i += gstride) rout[i] = sr[i];
         if (lead()) {
-            hist_put(st, a.hist, k - 1, rel);
+            put_hist(st, a.hist, k - 1, rel);
             rout[L.pslot + 1] = rho1;
             st->relres = rel; st->iters = k; st->alpha[k & 3] = alpha;
         }
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
     const int64_t n = L.n;
     const int64_t gstride = (int64_t)gridDim.x * kNT;
     const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
-    if (done_flag(st)) return;
+    if (is_done(st)) return;
     const T* rin = par_ptr(a.G_r, a.gpar, P.k0 - 1);
     for (int64_t j = threadIdx.x; j < P.ncols; j += kNT) {
         sp[j] = j < n ? a.p_full[j] : T(0);
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
             rel = sqrt(rr) / (T)st->nb;
             if (rel <= (T)st->tol) {
                 if (lead()) {
-                    hist_put(st, a.hist, i - 2, rel);
+                    put_hist(st, a.hist, i - 2, rel);
                     st->relres = rel; st->iters = i - 1; st->converged = 1; st->status = KS_OK; st->done = 1;
                 }
                 return;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
         }
         if (rho == T(0) || !isfinite(rho)) {
             if (lead()) {
-                if (i >= 2) { hist_put(st, a.hist, i - 2, rel); st->relres = rel; }
+                if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
                 st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1;
             }
             return;
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
             for (int64_t j = threadIdx.x; j < n; j += kNT) sp[j] = fma(beta, fma(-omega_prev, sv[j], sp[j]), ss[j]);
         }
         if (lead()) {
-            if (i >= 2) { hist_put(st, a.hist, i - 2, rel); st->relres = rel; }
+            if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
             st->rho[i & 3] = rho;
             st->iters = i - 1;
         }
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
         if (srel <= (T)st->tol) {                          // half-step exit
             for (int64_t l = tid0; l < n; l += gstride) a.x_loc[l] = fma(alpha, sp[l], a.x_loc[l]);
             if (lead()) {
-                hist_put(st, a.hist, i - 1, srel);
+                put_hist(st, a.hist, i - 1, srel);
                 st->alpha[i & 3] = alpha;
                 st->relres = srel; st->half = 1; st->half_iter = i; st->converged = 1;
                 st->status = KS_OK; st->iters = i; st->done = 1;

@@ -22,6 +22,7 @@
 #include <stdint.h>
 
 #include "ks_device.cuh"
+#include "ks_common.cuh"
 #include "ks_internal.h"
 
 namespace ks {
@@ -30,11 +31,6 @@ namespace {
 
 constexpr int kNT = 256;
 
-__device__ __forceinline__ int64_t gidx(const Layout& L, int64_t j) {
-    int g = 0;
-    while (g + 1 < L.P && j >= L.row0[g + 1]) ++g;
-    return (int64_t)g * L.chunk + (j - L.row0[g]);
-}
 // Gather buffers are double-buffered by iteration parity in the fused mode
 // (gpar/spar = 0 in NCCL mode: one buffer, gathered in place).
 __device__ __forceinline__ double* Gpar(const VecArgs& a, double* G, long long k) {
@@ -45,29 +41,6 @@ __device__ __forceinline__ double* Spar(const VecArgs& a, long long k) {
 }
 __device__ __forceinline__ double* own_chunk(const VecArgs& a, double* G) {
     return G + (int64_t)a.L.rank * a.L.chunk;
-}
-__device__ __forceinline__ double sum_slots(const Layout& L, const double* G, int k) {
-    double s = 0.0;
-    for (int g = 0; g < L.P; ++g) s += G[(int64_t)g * L.chunk + L.pslot + k];
-    return s;
-}
-__device__ __forceinline__ double sum_scal(const Layout& L, const double* S, int k) {
-    double s = 0.0;
-    for (int g = 0; g < L.P; ++g) s += S[g * kScalSlot + k];
-    return s;
-}
-__device__ __forceinline__ bool is_done(const DevState* st) {
-    return *(volatile const int*)&st->done != 0;
-}
-__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
-__device__ __forceinline__ int64_t m_loc(const Layout& L) {
-    return L.row0[L.rank + 1] - L.row0[L.rank];
-}
-__device__ __forceinline__ void put_hist(DevState* st, double* hist, long long k1, double v) {
-    if (hist && k1 >= 0 && k1 < st->hist_cap) hist[k1] = v;
-}
-__device__ __forceinline__ unsigned long long epoch_of(const DevState* st, long long k) {
-    return *(volatile const unsigned long long*)&st->ebase + (unsigned long long)k;
 }
 // Fused mode: wait for phase `ph` of iteration k from every rank.  A timeout
 // marks the solve failed (KS_ENCCL) instead of hanging.
@@ -100,7 +73,7 @@ __device__ __forceinline__ void publish_phase(const VecArgs& a, int ph, long lon
 // ---------------------------------------------------------------- setup (A0/B0)
 __global__ void __launch_bounds__(kNT) k_setup_r(VecArgs a, int have_x0, const double* x0_full) {
     __shared__ double red[kNT / 32];
-    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    const int64_t m = rows_of(a.L), r0 = a.L.row0[a.L.rank];
     double* rl = own_chunk(a, a.G_r);
     double acc[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
@@ -131,7 +104,7 @@ __global__ void __launch_bounds__(kNT) k_setup_r(VecArgs a, int have_x0, const d
 __global__ void __launch_bounds__(kNT) k_setup_local(VecArgs a) {
     __shared__ double red[kNT / 32];
     const Layout& L = a.L;
-    const int64_t m = m_loc(L), r0 = L.row0[L.rank];
+    const int64_t m = rows_of(L), r0 = L.row0[L.rank];
     double acc[1] = {0.0};
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < L.n; j += (int64_t)gridDim.x * kNT) {
         const double bj = a.b_full[j];
@@ -197,7 +170,7 @@ __global__ void __launch_bounds__(kNT) k_cg_init(VecArgs a, double tol, long lon
     if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
         DevState* st = a.st;
         init_state(st, tol, maxit, hist_cap, ebase);
-        const double rho0 = sum_slots(a.L, a.G_r, 1);
+        const double rho0 = slot_sum(a.L, a.G_r, 1);
         st->rho[0] = rho0;
         init_decide(st, acc[0], rho0);
     }
@@ -211,13 +184,13 @@ __global__ void __launch_bounds__(kNT) k_cg_update(VecArgs a, const long long* k
     DevState* st = a.st;
     if (is_done(st)) return;
     if (!wait_phase(a, kPhaseS, k)) return;                   // sigma partials of iteration k
-    const double sigma = sum_scal(a.L, Spar(a, k), 0);
+    const double sigma = scal_sum(a.L, Spar(a, k), 0);
     if (!(sigma > 0.0)) {                                   // Q9: NOTSPD, x unchanged
         if (lead()) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
         return;
     }
     const double alpha = st->rho[(k - 1) & 3] / sigma;
-    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    const int64_t m = rows_of(a.L), r0 = a.L.row0[a.L.rank];
     const double* rin = own_chunk(a, Gpar(a, a.G_r, k - 1));   // r_{k-1}
     const double* pl = a.p_full + r0;
     double acc[1] = {0.0};
@@ -243,7 +216,7 @@ __global__ void __launch_bounds__(kNT) k_cg_direction(VecArgs a, const long long
     if (is_done(st)) return;
     if (!wait_phase(a, kPhaseR, k)) return;
     const double* Gr = Gpar(a, a.G_r, k);
-    const double rho1 = sum_slots(a.L, Gr, 1);
+    const double rho1 = slot_sum(a.L, Gr, 1);
     const double rel = sqrt(rho1) / st->nb;
     if (rel <= st->tol) {
         if (lead()) {
@@ -269,7 +242,7 @@ __global__ void __launch_bounds__(kNT) k_finish(VecArgs a, int bicgstab) {
         st->iters = maxit;
         st->status = KS_EMAXIT;
         if (bicgstab && maxit >= 1) {                     // test of the last full step
-            const double rel = sqrt(sum_slots(a.L, Gpar(a, a.G_r, maxit), 1)) / st->nb;
+            const double rel = sqrt(slot_sum(a.L, Gpar(a, a.G_r, maxit), 1)) / st->nb;
             put_hist(st, a.hist, maxit - 1, rel);
             st->relres = rel;
             if (rel <= st->tol) { st->converged = 1; st->status = KS_OK; }
@@ -277,7 +250,7 @@ __global__ void __launch_bounds__(kNT) k_finish(VecArgs a, int bicgstab) {
         st->done = 1;
     }
     if (st->bzero) {                                      // Q6: b = 0 -> x = 0
-        const int64_t m = m_loc(a.L);
+        const int64_t m = rows_of(a.L);
         for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
             a.x_loc[i] = 0.0;
     }
@@ -296,7 +269,7 @@ __global__ void __launch_bounds__(kNT) k_bs_init(VecArgs a, double tol, long lon
     if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
         DevState* st = a.st;
         init_state(st, tol, maxit, hist_cap, ebase);   // rho_old = alpha = omega = 1 (Q8)
-        init_decide(st, acc[0], sum_slots(a.L, a.G_r, 1));
+        init_decide(st, acc[0], slot_sum(a.L, a.G_r, 1));
     }
 }
 
@@ -308,10 +281,10 @@ __global__ void __launch_bounds__(kNT) k_bs_p(VecArgs a, const long long* kdev, 
     if (is_done(st)) return;
     if (i >= 2 && !wait_phase(a, kPhaseR, i - 1)) return;
     const double* Gr = Gpar(a, a.G_r, i - 1);              // r_{i-1} (+ partials)
-    const double rho = sum_slots(a.L, Gr, 0);
+    const double rho = slot_sum(a.L, Gr, 0);
     double rel = 0.0;
     if (i >= 2) {
-        rel = sqrt(sum_slots(a.L, Gr, 1)) / st->nb;
+        rel = sqrt(slot_sum(a.L, Gr, 1)) / st->nb;
         if (rel <= st->tol) {
             if (lead()) {
                 put_hist(st, a.hist, i - 2, rel);
@@ -360,7 +333,7 @@ __global__ void __launch_bounds__(kNT) k_bs_s(VecArgs a, const long long* kdev, 
     // local buffer.  A full local copy is kept for the next bs_p.
     const double* Gv = Gpar(a, a.G_v, i);
     const double* Gr = Gpar(a, a.G_r, i - 1);
-    const double g = sum_slots(a.L, Gv, 0);
+    const double g = slot_sum(a.L, Gv, 0);
     if (g == 0.0 || !isfinite(g)) {
         if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
         return;
@@ -397,7 +370,7 @@ __global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, const long long* kdev,
     const long long i = koff + (kdev ? *kdev : 0);
     __shared__ double red[2 * (kNT / 32)];
     DevState* st = a.st;
-    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    const int64_t m = rows_of(a.L), r0 = a.L.row0[a.L.rank];
     const double* pl = a.p_full + r0;
     if (is_done(st)) {
         if (st->half_iter == i) {
@@ -409,7 +382,7 @@ __global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, const long long* kdev,
     }
     if (!wait_phase(a, kPhaseS, i)) return;                   // <t,s>, <t,t> partials
     const double* Si = Spar(a, i);
-    const double ts = sum_scal(a.L, Si, 0), tt = sum_scal(a.L, Si, 1);
+    const double ts = scal_sum(a.L, Si, 0), tt = scal_sum(a.L, Si, 1);
     const double om = ts / tt;
     if (tt == 0.0 || !isfinite(tt) || om == 0.0 || !isfinite(om)) {
         if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
@@ -443,7 +416,7 @@ __global__ void __launch_bounds__(kNT) k_bs_xr(VecArgs a, const long long* kdev,
 __global__ void __launch_bounds__(kNT) k_bicg_init(VecArgs a, double tol, long long maxit,
                                                    long long hist_cap, unsigned long long ebase) {
     __shared__ double red[kNT / 32];
-    const int64_t m = m_loc(a.L);
+    const int64_t m = rows_of(a.L);
     double acc[1] = {0.0};
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT) {
         a.p_full[j] = a.G_r[gidx(a.L, j)];                  // p0 = r0
@@ -456,8 +429,8 @@ __global__ void __launch_bounds__(kNT) k_bicg_init(VecArgs a, double tol, long l
     if (grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0) {
         DevState* st = a.st;
         init_state(st, tol, maxit, hist_cap, ebase);
-        st->rho[0] = sum_slots(a.L, a.G_r, 0);              // <rt0, r0>
-        init_decide(st, acc[0], sum_slots(a.L, a.G_r, 1));
+        st->rho[0] = slot_sum(a.L, a.G_r, 0);              // <rt0, r0>
+        init_decide(st, acc[0], slot_sum(a.L, a.G_r, 1));
     }
 }
 
@@ -470,13 +443,13 @@ __global__ void __launch_bounds__(kNT) k_bicg_update(VecArgs a, long long k) {
     DevState* st = a.st;
     if (is_done(st)) return;
     if (!wait_phase(a, kPhaseS, k) || !wait_phase(a, kPhaseV, k)) return;
-    const double sigma = sum_scal(a.L, Spar(a, k), 0);
+    const double sigma = scal_sum(a.L, Spar(a, k), 0);
     if (sigma == 0.0 || !isfinite(sigma)) {
         if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = k - 1; st->done = 1; }
         return;
     }
     const double alpha = st->rho[(k - 1) & 3] / sigma;
-    const int64_t m = m_loc(a.L), r0 = a.L.row0[a.L.rank];
+    const int64_t m = rows_of(a.L), r0 = a.L.row0[a.L.rank];
     const double* rin = own_chunk(a, Gpar(a, a.G_r, k - 1));   // r_{k-1}
     const double* qslots = Gpar(a, a.G_v, k);                   // fused: P slots of qt rows
     double acc[2] = {0.0, 0.0};
@@ -512,8 +485,8 @@ __global__ void __launch_bounds__(kNT) k_bicg_direction(VecArgs a, long long k) 
     if (is_done(st)) return;
     if (!wait_phase(a, kPhaseR, k)) return;
     const double* Gr = Gpar(a, a.G_r, k);
-    const double rho1 = sum_slots(a.L, Gr, 0);
-    const double rel = sqrt(sum_slots(a.L, Gr, 1)) / st->nb;
+    const double rho1 = slot_sum(a.L, Gr, 0);
+    const double rel = sqrt(slot_sum(a.L, Gr, 1)) / st->nb;
     if (rel <= st->tol) {
         if (lead()) {
             put_hist(st, a.hist, k - 1, rel);
@@ -531,7 +504,7 @@ __global__ void __launch_bounds__(kNT) k_bicg_direction(VecArgs a, long long k) 
     const double beta = rho1 / st->rho[(k - 1) & 3];
     for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < a.L.n; j += (int64_t)gridDim.x * kNT)
         a.p_full[j] = fma(beta, a.p_full[j], Gr[gidx(a.L, j)]);
-    const int64_t m = m_loc(a.L);
+    const int64_t m = rows_of(a.L);
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
         a.pt_loc[i] = fma(beta, a.pt_loc[i], a.rhat_loc[i]);
     if (lead()) {
@@ -545,11 +518,11 @@ __global__ void k_advance(long long* kdev, long long by) {
 }
 
 __global__ void k_true_res_final(VecArgs a) {
-    if (lead()) a.st->true_rr = sum_scal(a.L, a.S, 1);
+    if (lead()) a.st->true_rr = scal_sum(a.L, a.S, 1);
 }
 
 __global__ void __launch_bounds__(kNT) k_pack_x(VecArgs a) {
-    const int64_t m = m_loc(a.L);
+    const int64_t m = rows_of(a.L);
     double* xl = own_chunk(a, a.G_v);
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT)
         xl[i] = a.x_loc[i];
