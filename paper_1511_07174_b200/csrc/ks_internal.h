@@ -236,13 +236,15 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
                    T* bpart, unsigned* bar, long long k0, long long k1, int grid, int rows, int unroll,
                    cudaStream_t st);
 
-// Small-n single-GPU kernels (ks_small.cu, NEXT-2): full-length vectors in every
-// CTA's shared memory, 1 (CG) / 2 (BiCGSTAB) grid barriers per iteration.
-// small_grid returns 0 when the vectors do not fit in shared memory.
+// Small-n kernels (ks_small.cu, NEXT-2): full-length vectors in every CTA's shared
+// memory, 1 (CG) / 2 (BiCGSTAB) grid barriers per iteration.  kind: 0 = CG, 1 =
+// BiCGSTAB (P = 1), 2 = CG over P > 1 GPUs with the fused exchange (allgather-only:
+// one exchange + one barrier per iteration; a = vargs(true)).  small_grid (rows =
+// this rank's rows) returns 0 when the vectors do not fit in shared memory.
 template <class T>
-int small_grid(int bicgstab, int num_sms, int64_t n, int64_t ncols);
+int small_grid(int kind, int num_sms, int64_t rows, int64_t ncols);
 template <class T>
-int launch_small(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
+int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
                  unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st);
 
 // NEXT-4 (FP32) support kernels (ks_f32.cu): K1 in FP32, setup/init/finish in

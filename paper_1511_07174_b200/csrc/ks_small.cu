@@ -140,6 +140,107 @@ __global__ void __launch_bounds__(kNT, 2) k_cg_small(PersistArgs<T> P) {
     }
 }
 
+// ------------------------------------------- CG on P > 1 GPUs (fused exchange)
+// Allgather-only schedule on the small-n kernel:
+// each rank computes its rows of q = A p and stores them into every rank's G_v
+// (parity k) -- the one exchange of the iteration; then every CTA of every rank
+// forms sigma = <p, q>, r -= alpha q, rho' = <r, r> and p = r + beta p over the full
+// length in its own shared memory.  The full-length sums run in one fixed order,
+// so every CTA of every rank takes the same decisions.  One grid barrier and one
+// exchange per iteration (the general fused kernels: three barriers, two
+// exchanges).
+template <class T, int kR, int kU>
+__global__ void __launch_bounds__(kNT, 2) k_cg_small_peer(PersistArgs<T> P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sp = reinterpret_cast<T*>(smem_raw);   // p (ncols, zero padded)
+    T* sr = sp + P.ncols;                     // r (n)
+    T* sq = sr + P.ncols;                     // gathered q (n)
+    __shared__ T red[(kR > 2 ? kR : 2) * kNW];
+    const VecArgsT<T>& a = P.a;
+    const Layout& L = a.L;
+    DevState* st = a.st;
+    const int64_t n = L.n, m = rows_of(L), r0 = L.row0[L.rank];
+    const int64_t gstride = (int64_t)gridDim.x * kNT;
+    const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
+    if (is_done(st)) return;
+    {
+        const T* rin = par_ptr(a.G_r, a.gpar, P.k0 - 1);
+        for (int64_t j = threadIdx.x; j < P.ncols; j += kNT) {
+            sp[j] = j < n ? a.p_full[j] : T(0);
+            if (j < n) sr[j] = rin[gidx(L, j)];
+        }
+    }
+    T rho = (T)st->rho[(P.k0 - 1) & 3];
+    __syncthreads();
+    const int64_t tiles = (m + kR - 1) / kR;
+    const int64_t ncb = P.ncols / (Vec16<T>::W * kNT);
+    for (long long k = P.k0; k <= P.k1; ++k) {
+        // A1 + A4': this rank's rows of q = A p, stored into every rank's G_v (parity k)
+        const int64_t qo = (k & 1) * a.gpar + (int64_t)L.rank * L.chunk;
+        bool pushed = false;
+        for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int64_t t0 = tile * kR;
+            const int nvalid = (int)min((int64_t)kR, m - t0);
+            T acc[kR];
+            stream_rows<kR, kU, kNT, T, true>(P.A, P.lda, t0, nvalid, sp, 0, ncb, acc);
+            block_sum<kNT, kR>(acc, red);
+            if (threadIdx.x == 0) {
+                for (int r = 0; r < nvalid; ++r)
+                    for (int g = 0; g < L.P; ++g) a.pp.G_v[g][qo + t0 + r] = acc[r];
+                pushed = true;
+            }
+        }
+        if (pushed) __threadfence_system();
+        if (!grid_sync(P.bar, st)) return;
+        if (lead()) flags_out(a, kPhaseV, k);
+        if (!wait_ph(a, kPhaseV, k)) return;
+        // A2: sigma = <p, q> over the full length (every CTA; same order everywhere)
+        const T* qg = par_ptr(a.G_v, a.gpar, k);
+        T sig[1] = {T(0)};
+        for (int64_t j = threadIdx.x; j < n; j += kNT) {
+            const T qj = __ldcg(qg + gidx(L, j));
+            sq[j] = qj;
+            sig[0] = fma(sp[j], qj, sig[0]);
+        }
+        cta_total<1>(sig, red);
+        const T sigma = sig[0];
+        if (!(sigma > T(0))) {                              // Q9
+            if (lead()) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
+            return;
+        }
+        const T alpha = rho / sigma;
+        // A3: x += alpha p (own rows); r -= alpha q, rho' = <r, r> (full length)
+        for (int64_t i = tid0; i < m; i += gstride) a.x_loc[i] = fma(alpha, sp[r0 + i], a.x_loc[i]);
+        T acc[1] = {T(0)};
+        for (int64_t j = threadIdx.x; j < n; j += kNT) {
+            const T r = fma(-alpha, sq[j], sr[j]);
+            sr[j] = r;
+            acc[0] = fma(r, r, acc[0]);
+        }
+        cta_total<1>(acc, red);
+        const T rho1 = acc[0];
+        const T rel = sqrt(rho1) / (T)st->nb;
+        T* rout = par_ptr(a.G_r, a.gpar, k);              // this rank's full copy of r
+        for (int64_t j = tid0; j < n; j += gstride) rout[gidx(L, j)] = sr[j];
+        if (lead()) {
+            put_hist(st, a.hist, k - 1, rel);
+            for (int g = 0; g < L.P; ++g) rout[(int64_t)g * L.chunk + L.pslot + 1] = g == 0 ? rho1 : T(0);
+            st->relres = rel; st->iters = k; st->alpha[k & 3] = alpha;
+        }
+        if (rel <= (T)st->tol) {
+            if (lead()) { st->converged = 1; st->status = KS_OK; st->done = 1; }
+            return;
+        }
+        // A5: p = r + beta p (full length, shared memory)
+        const T beta = rho1 / rho;
+        for (int64_t j = threadIdx.x; j < n; j += kNT) sp[j] = fma(beta, sp[j], sr[j]);
+        __syncthreads();
+        for (int64_t i = tid0; i < n; i += gstride) a.p_full[i] = sp[i];
+        if (lead()) st->rho[k & 3] = rho1;
+        rho = rho1;
+    }
+}
+
 // ------------------------------------------------------------ BiCGSTAB (B1-B8)
 template <class T, int kR, int kU>
 __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
@@ -302,31 +403,34 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
 // Tile shape: R = 4 rows, U = 2 column blocks (C1: 256 tiles of 8 KiB rows).
 constexpr int kSR = 4, kSU = 2;
 
+// kind: 0 = CG, 1 = BiCGSTAB (P = 1), 2 = CG with the fused exchange (P > 1)
 template <class T>
-const void* kern(int bicgstab) {
-    return bicgstab ? (const void*)k_bs_small<T, kSR, kSU> : (const void*)k_cg_small<T, kSR, kSU>;
+const void* kern(int kind) {
+    return kind == 2 ? (const void*)k_cg_small_peer<T, kSR, kSU>
+         : kind == 1 ? (const void*)k_bs_small<T, kSR, kSU> : (const void*)k_cg_small<T, kSR, kSU>;
 }
 template <class T>
-size_t smem_bytes(int bicgstab, int64_t ncols) {
-    return (size_t)(bicgstab ? 3 : 2) * (size_t)ncols * sizeof(T);
+size_t smem_bytes(int kind, int64_t ncols) {
+    return (size_t)(kind == 0 ? 2 : 3) * (size_t)ncols * sizeof(T);
 }
 
 }  // namespace
 
-// Grid for the small kernels, 0 if the vectors do not fit in shared memory.
+// Grid for the small kernels (rows = this rank's rows), 0 if the vectors do not
+// fit in shared memory.
 template <class T>
-int small_grid(int bicgstab, int num_sms, int64_t n, int64_t ncols) {
-    const size_t sm = smem_bytes<T>(bicgstab, ncols);
+int small_grid(int kind, int num_sms, int64_t rows, int64_t ncols) {
+    const size_t sm = smem_bytes<T>(kind, ncols);
     int dev = 0, optin = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
     if (sm + 1024 > (size_t)optin) return 0;
-    const void* k = kern<T>(bicgstab);
+    const void* k = kern<T>(kind);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return 0;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kNT, sm);
     if (per_sm < 1) return 0;
-    const int64_t tiles = (n + kSR - 1) / kSR;
+    const int64_t tiles = (rows + kSR - 1) / kSR;
     int64_t g = (int64_t)per_sm * num_sms;
     if (g > tiles) g = tiles;
     if (g > kPartStride / kSlots) g = kPartStride / kSlots;   // bpart region: grid x kSlots
@@ -335,7 +439,7 @@ int small_grid(int bicgstab, int num_sms, int64_t n, int64_t ncols) {
 }
 
 template <class T>
-int launch_small(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
+int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
                  unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st) {
     PersistArgs<T> P;
     P.a = a;
@@ -349,8 +453,8 @@ int launch_small(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, in
     void* args[] = {&P};
     cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
     if (e != cudaSuccess) return -(int)e;
-    e = cudaLaunchCooperativeKernel(kern<T>(bicgstab), dim3((unsigned)grid), dim3(kNT), args,
-                                                smem_bytes<T>(bicgstab, ncols), st);
+    e = cudaLaunchCooperativeKernel(kern<T>(kind), dim3((unsigned)grid), dim3(kNT), args,
+                                    smem_bytes<T>(kind, ncols), st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 

@@ -27,12 +27,20 @@ void persist_shape(const ks_ctx* c, const Rank& r, int* rows, int* unroll) {
     if (*rows == 0 && *unroll == 0 && r.L.pslot <= 4096) { *rows = 4; *unroll = 2; }
 }
 
-// Grid of the small-n shared-memory kernels (ks_small.cu), 0 = not used.
+// Small-n shared-memory kernels (ks_small.cu): their kind for this solve (0 CG,
+// 1 BiCGSTAB, 2 CG over P > 1 with the fused exchange), -1 = not used.
+int small_kind(const ks_ctx* c, int bicgstab) {
+    if (c->opt.small == 0) return -1;
+    if (c->opt.small == 2 && c->n * (int64_t)c->esz > ks_ctx::kSmallAutoMaxBytes) return -1;
+    if (c->P == 1) return bicgstab ? 1 : 0;
+    return (!bicgstab && c->fused()) ? 2 : -1;
+}
+// Grid of the small-n kernels, 0 = not used.
 template <class T>
 int small_path_grid(const ks_ctx* c, const Rank& r, int bicgstab) {
-    if (c->P != 1 || c->opt.small == 0) return 0;
-    if (c->opt.small == 2 && c->n * (int64_t)c->esz > ks_ctx::kSmallAutoMaxBytes) return 0;
-    int g = small_grid<T>(bicgstab, r.num_sms, c->n, c->ld);
+    const int kind = small_kind(c, bicgstab);
+    if (kind < 0) return 0;
+    int g = small_grid<T>(kind, r.num_sms, r.m, c->ld);
     if (g > 0 && c->opt.persist_grid > 0) g = (int)std::min<int64_t>(g, c->opt.persist_grid);
     return g;
 }
@@ -132,8 +140,8 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
             const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
             prof.pre(slot);
             const int rc = sgrid > 0
-                ? launch_small<double>(kind, r.vargs(false), r.A, c->ld, c->ld, r.scr.part + 2 * kPartStride,
-                                       r.scr.ticket + 8, k, kend, sgrid, r.stream)
+                ? launch_small<double>(small_kind(c, kind), r.vargs(c->fused()), r.A, c->ld, c->ld,
+                                       r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, sgrid, r.stream)
                 : launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
                                          r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
                                          prows, punroll, r.stream);
@@ -428,8 +436,8 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
         const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
         prof.pre(slot);
         const int rc = sgrid > 0
-            ? launch_small<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld, bpart,
-                                  r.scr.ticket + 8, k, kend, sgrid, r.stream)
+            ? launch_small<float>(small_kind(c, bicgstab), a, reinterpret_cast<const float*>(r.A), c->ld,
+                                  c->ld, bpart, r.scr.ticket + 8, k, kend, sgrid, r.stream)
             : launch_persist<float>(bicgstab, a, reinterpret_cast<const float*>(r.A), c->ld, c->ld,
                                     bpart, r.scr.ticket + 8, k, kend, pgrid, prows, punroll, r.stream);
         prof.post(slot);

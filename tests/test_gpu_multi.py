@@ -60,6 +60,46 @@ def test_multi_gemv_and_cg(P):
 
 @needs2
 @pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_multi_small_cg_allgather_only(P, dtype):
+    """Small-n CG over P GPUs (k_cg_small_peer: one exchange of q slices and one grid
+    barrier per iteration, all O(n) work redundant in shared memory) vs the oracle
+    and vs the general fused kernels (small = 0): ragged n, x0, maxit, multi-launch."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    from test_gpu_parity import bars_f32
+    for n in (1002, 4096):
+        A, c, b = synth.gspd(n, 1e3)
+        if dtype == "f32":
+            xo, ho, ro = oracle.cg_f32(A, b, tol=1e-5)
+        else:
+            xo, ho, ro = oracle.cg(A, b, tol=1e-10)
+        outs = []
+        for small in (1, 0):
+            with ks.Context(n, ngpus=P, dtype=dtype) as ctx:
+                ctx.set_option("small", small)
+                ctx.generate("spd", seed=synth.SEED, table=c, want_b=False)
+                if dtype == "f32":
+                    bb = b.astype(np.float32).astype(np.float64)
+                    x, h, r = ctx.cg(bb, tol=1e-5)
+                    bars_f32(x, h, r, xo, ho, ro)
+                else:
+                    x, h, r = ctx.cg(b, tol=1e-10)
+                    bars(x, h, r, xo, ho, ro)
+                    ctx.set_option("poll_batch", 7)
+                    x2, h2, r2 = ctx.cg(b, tol=1e-10)
+                    assert r2.iterations == r.iterations and np.array_equal(x2, x) and np.array_equal(h2, h)
+                    x0 = np.random.default_rng(n).standard_normal(n)
+                    xo0, ho0, ro0 = oracle.cg(A, b, x0=x0, tol=1e-30, maxit=9)
+                    x9, h9, r9 = ctx.cg(b, x0=x0, tol=1e-30, maxit=9)
+                    assert r9.status == ks.KS_EMAXIT and r9.iterations == 9
+                    bars(x9, h9, r9, xo0, ho0, ro0, iters_tol=0)
+                outs.append(r.iterations)
+        assert abs(outs[0] - outs[1]) <= 2
+
+
+@needs2
+@pytest.mark.parametrize("P", [2, 4])
 def test_multi_bicgstab(P):
     if ngpu() < P:
         pytest.skip(f"needs {P} GPUs")
