@@ -13,7 +13,7 @@ for P in [p for p in (1, 2, 4) if p <= torch.cuda.device_count()]:
             with ks.Context(n, ngpus=P) as ctx:
                 b = ctx.generate(kind, seed=synth.SEED, table=synth.spd_table(n, 1e2) if kind == "spd" else None, kd=4)
                 ctx.set_option("true_residual", 0)
-                ctx.set_option("small", 0)
+                ctx.set_option("small", int(os.environ.get("KS_SMALL", "0")))
                 for fused in ((1, 0) if P > 1 else (1,)):
                     ctx.set_option("fused_comm", fused)
                     ctx.set_option("persistent", 2)
