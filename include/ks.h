@@ -126,11 +126,12 @@ typedef enum {
     KS_OPT_GEMVT_SHAPE = 11,  /* tuning: K1T 16-byte vectors per                  */
                               /* thread per row (1/2/4) * 100 + rows in flight    */
                               /* (4/8/16); default 204 (profiles/r01_gemvt_sweep) */
-    KS_OPT_SMALL = 12         /* CG / BiCGSTAB on one GPU with the persistent     */
-                              /* path: 1 = small-n kernels that keep the full     */
-                              /* vectors in every CTA's shared memory (1 grid     */
-                              /* barrier per CG iteration, 2 per BiCGSTAB one)    */
-                              /* when they fit; 0 = off; 2 (default) = auto (on   */
+    KS_OPT_SMALL = 12         /* persistent path: 1 = small-n kernels that keep   */
+                              /* the full vectors in every CTA's shared memory    */
+                              /* (CG and BiCGSTAB on one GPU: 1 / 2 grid barriers */
+                              /* per iteration; CG on P > 1 GPUs with the fused   */
+                              /* exchange: one q exchange + 1 barrier) when they  */
+                              /* fit; 0 = off; 2 (default) = auto (on             */
                               /* when a vector is <= 32 KiB: FP64 n <= 4096, FP32 */
                               /* n <= 8192)                                       */
 } ks_option;
