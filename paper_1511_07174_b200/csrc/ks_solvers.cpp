@@ -33,7 +33,7 @@ int small_kind(const ks_ctx* c, int bicgstab) {
     if (c->opt.small == 0) return -1;
     if (c->opt.small == 2 && c->n * (int64_t)c->esz > ks_ctx::kSmallAutoMaxBytes) return -1;
     if (c->P == 1) return bicgstab ? 1 : 0;
-    return c->fused() ? (bicgstab ? 3 : 2) : -1;
+    return (!bicgstab && c->fused()) ? 2 : -1;
 }
 // Grid of the small-n kernels, 0 = not used.
 template <class T>
