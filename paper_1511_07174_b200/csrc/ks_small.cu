@@ -1,4 +1,4 @@
-// NEXT-2, second stage: the small-n single-GPU kernels.
+// NEXT-2, second stage: the small-n kernels.
 //
 // For an L2-resident system (C1: n = 1024, 8 MiB) an iteration is a chain of
 // grid-wide dependencies, each ~2 us (barrier + reading the CTA partials), with
@@ -18,7 +18,8 @@
 // reduction then orders everything.  The global copies of r, p, v (and G_r's
 // partial slots) are refreshed every iteration by their owning threads, so a
 // later launch (the next poll batch) or the finish kernels see current state.
-// P == 1 only (the multi-GPU path gathers r / v between ranks instead).
+// k_cg_small / k_bs_small run on one GPU; k_cg_small_peer is the CG variant for
+// P > 1 GPUs with the fused exchange (see its comment).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
