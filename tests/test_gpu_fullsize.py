@@ -123,3 +123,23 @@ def test_c4_131072_one_gpu():
     nb = float(np.linalg.norm(b))
     for i in [0, 1, 65535, 65536, 131071]:
         assert abs(b[i] - op.rows(i, 1, x)[0]) <= 10 * 1e-10 * nb
+
+
+@pytest.mark.parametrize("method", ["bicg", "gmres"])
+def test_fullsize_next3_true_residual(method):
+    """NEXT-3 at the headline size (C3: G-DD(65536, 16), tol 1e-10) in the launch
+    configuration of the defaults (BiCG: K1 + K1T; GMRES(30): persistent cycle
+    kernel): converged, and the true residual recomputed by the oracle with
+    on-the-fly rows (long double) within 10 tol and equal to the library's own."""
+    spec = synth.spec("dd", N, kd=16)
+    with ks.Context(N) as ctx:
+        b = ctx.generate("dd", seed=synth.SEED, kd=16)
+        kw = {"restart": 30} if method == "gmres" else {}
+        x, h, r = getattr(ctx, method)(b, tol=1e-10, **kw)
+    assert r.converged and r.status == ks.KS_OK and 0 < r.iterations < 200
+    op = oracle.Operator(gen=spec, threads=THREADS)
+    tr = oracle.true_relres_ld(op, b, x)
+    assert tr <= 10 * 1e-10
+    assert abs(tr - r.true_relres) <= 1e-3 * tr + 1e-15
+    if method == "gmres":                      # minimal residual: non-increasing history
+        assert np.all(h[1:] <= h[:-1] * (1 + 1e-12))
