@@ -218,6 +218,15 @@ ks_status ks_get_option(const ks_ctx* ctx, ks_option opt, int64_t* value);
 /* Number of GPUs (shards) this context drives locally, and the global P.        */
 ks_status ks_info(const ks_ctx* ctx, int32_t* local_gpus, int32_t* nranks, int64_t* n, int64_t* ld);
 
+/* Guard-zone check (a test facility: compute-sanitizer is not available on the
+ * GPU pool).  With the environment variable KS_GUARD=1 set when the library is
+ * loaded, every device buffer the library allocates (except the CUDA-IPC exchange
+ * buffer) is surrounded by 4 KiB canary zones.  *violations receives the number of
+ * zones found corrupted -- out-of-bounds writes by some kernel -- on the context's
+ * GPUs now plus any found when buffers were freed; -1 when KS_GUARD is not set.
+ * Synchronises the context's devices.                                            */
+ks_status ks_check_guards(const ks_ctx* ctx, int64_t* violations);
+
 /* Last error message of ctx (or of the calling thread when ctx == NULL).         */
 const char* ks_last_error(const ks_ctx* ctx);
 

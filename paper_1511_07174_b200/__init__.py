@@ -34,7 +34,7 @@ OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 
 EXPORTS = ["ks_create", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
            "ks_generate", "ks_matvec", "ks_matvec_t", "ks_time_matvec", "ks_cg", "ks_bicgstab",
            "ks_bicg", "ks_gmres",
-           "ks_set_option", "ks_get_option", "ks_info", "ks_last_error", "ks_version"]
+           "ks_set_option", "ks_get_option", "ks_info", "ks_check_guards", "ks_last_error", "ks_version"]
 
 
 class KsError(RuntimeError):
@@ -107,6 +107,7 @@ def lib():
             "ks_set_option": [vp, C.c_int, i64],
             "ks_get_option": [vp, C.c_int, C.POINTER(i64)],
             "ks_info": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64), C.POINTER(i64)],
+            "ks_check_guards": [vp, C.POINTER(i64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -218,6 +219,12 @@ class Context:
 
     def set_option(self, name: str, value: int):
         self._check(lib().ks_set_option(self._h, OPTIONS[name], int(value)))
+
+    def check_guards(self) -> int:
+        """Corrupted guard zones (out-of-bounds writes) with KS_GUARD=1; -1 otherwise."""
+        v = C.c_int64()
+        self._check(lib().ks_check_guards(self._h, C.byref(v)))
+        return v.value
 
     def get_option(self, name: str) -> int:
         v = C.c_int64()

@@ -187,7 +187,7 @@ ks_status ks_load_rows(ks_ctx* c, int64_t row_begin, int64_t nrows, const double
             if (c->dtype == KS_FLOAT32) {                 // FP64 rows -> device staging -> FP32
                 const int64_t chunk = std::max<int64_t>(1, (int64_t)(8 << 20) / c->n);
                 double* stage = nullptr;
-                KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&stage), (size_t)std::min(chunk, e - b) * c->n * sizeof(double)));
+                ks::dev_alloc_t(&stage, (size_t)std::min(chunk, e - b) * c->n);
                 for (int64_t i = b; i < e; i += chunk) {
                     const int64_t cnt = std::min(chunk, e - i);
                     KS_CUDA(cudaMemcpy2DAsync(stage, (size_t)c->n * sizeof(double), A + (i - row_begin) * lda,
@@ -197,7 +197,7 @@ ks_status ks_load_rows(ks_ctx* c, int64_t row_begin, int64_t nrows, const double
                                         cnt, c->n, r.stream);
                 }
                 KS_CUDA(cudaStreamSynchronize(r.stream));
-                KS_CUDA(cudaFree(stage));
+                ks::dev_free(stage);
                 for (int64_t i = b; i < e; ++i) {
                     auto& f = r.loaded[(size_t)(i - r.row0)];
                     if (!f) { f = 1; ++r.loaded_count; }
@@ -227,7 +227,7 @@ ks_status ks_generate(ks_ctx* c, const ks_gen_spec* spec, double* b_out) {
         c->for_each_rank([&](Rank& r) {
             if (spec->kind == 0) {
                 double* tab = nullptr;
-                KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&tab), (size_t)c->n * sizeof(double)));
+                ks::dev_alloc_t(&tab, (size_t)c->n);
                 KS_CUDA(cudaMemcpyAsync(tab, spec->spd_table, (size_t)c->n * sizeof(double),
                                         cudaMemcpyDefault, r.stream));
                 if (c->dtype == KS_FLOAT32)
@@ -235,7 +235,7 @@ ks_status ks_generate(ks_ctx* c, const ks_gen_spec* spec, double* b_out) {
                 else
                     ks::launch_gen_spd(r.A, c->ld, r.row0, r.m, c->n, spec->seed, tab, r.stream);
                 KS_CUDA(cudaStreamSynchronize(r.stream));
-                KS_CUDA(cudaFree(tab));
+                ks::dev_free(tab);
             } else {
                 if (c->dtype == KS_FLOAT32)
                     ks::launch_gen_dd_f32(reinterpret_cast<float*>(r.A), c->ld, r.row0, r.m, c->n, spec->seed, spec->kd, r.stream);
@@ -245,11 +245,11 @@ ks_status ks_generate(ks_ctx* c, const ks_gen_spec* spec, double* b_out) {
             KS_CUDA(cudaGetLastError());
             if (b_out && c->writes_host(r)) {
                 double* bd = nullptr;                     // b is FP64 at the ABI
-                KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&bd), (size_t)c->n * sizeof(double)));
+                ks::dev_alloc_t(&bd, (size_t)c->n);
                 ks::launch_gen_rhs(bd, c->n, spec->seed, r.stream);
                 KS_CUDA(cudaMemcpyAsync(b_out, bd, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
                 KS_CUDA(cudaStreamSynchronize(r.stream));
-                KS_CUDA(cudaFree(bd));
+                ks::dev_free(bd);
             }
             KS_CUDA(cudaStreamSynchronize(r.stream));
             std::fill(r.loaded.begin(), r.loaded.end(), 1);
@@ -266,7 +266,7 @@ ks_status ks_matvec(ks_ctx* c, const double* x, double* y) {
             if (r.loaded_count < r.m) throw KsError(KS_ESTATE, "matrix not fully loaded");
             if (c->dtype == KS_FLOAT32) {
                 double* tmp = nullptr;
-                KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&tmp), (size_t)c->n * sizeof(double)));
+                ks::dev_alloc_t(&tmp, (size_t)c->n);
                 KS_CUDA(cudaMemcpyAsync(tmp, x, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
                 ks::launch_d2f(tmp, reinterpret_cast<float*>(r.s_full), c->n, r.stream);
                 ks::GemvParamsT<float> p{};
@@ -281,7 +281,7 @@ ks_status ks_matvec(ks_ctx* c, const double* x, double* y) {
                     KS_CUDA(cudaMemcpyAsync(y, tmp, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
                 KS_CUDA(cudaStreamSynchronize(r.stream));
                 KS_CUDA(cudaGetLastError());
-                KS_CUDA(cudaFree(tmp));
+                ks::dev_free(tmp);
                 return;
             }
             KS_CUDA(cudaMemcpyAsync(r.s_full, x, (size_t)c->n * sizeof(double), cudaMemcpyDefault,
@@ -508,6 +508,14 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             o.small = v; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
+    return KS_OK;
+}
+
+ks_status ks_check_guards(const ks_ctx* c, int64_t* violations) {
+    if (!c || !violations) return fail(nullptr, KS_EARG, "NULL argument");
+    std::vector<int> devs;
+    for (const auto& r : c->ranks) devs.push_back(r.dev);
+    *violations = ks::guard_check(devs);
     return KS_OK;
 }
 

@@ -48,13 +48,13 @@ VecArgs Rank::vargs(bool fused) const {
 
 template <class T>
 static void dmalloc(T** p, size_t count) {
-    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+    dev_alloc_t(p, std::max<size_t>(count, 1));
     KS_CUDA(cudaMemset(*p, 0, std::max<size_t>(count, 1) * sizeof(T)));
 }
 // element buffers of the context's dtype (double* members hold floats in FP32 contexts)
 static void emalloc(double** p, size_t count, size_t esz) {
     const size_t bytes = std::max<size_t>(count, 1) * esz;
-    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+    *p = static_cast<double*>(dev_alloc(bytes));
     KS_CUDA(cudaMemset(*p, 0, bytes));
 }
 template <class T>
@@ -130,14 +130,15 @@ void rank_free(Rank& r) {
     cudaDeviceSynchronize();
     for (void* p : r.ipc_opened) cudaIpcCloseMemHandle(p);
     r.ipc_opened.clear();
+    if (r.xbuf) cudaFree(r.xbuf);                 // IPC-exported: plain cudaMalloc
     for (void* p : {(void*)r.A, (void*)r.b_full, (void*)r.x_loc, (void*)r.p_full, (void*)r.s_full, (void*)r.v_full,
-                    (void*)r.q_loc, (void*)r.rhat_loc, (void*)r.xbuf,
+                    (void*)r.q_loc, (void*)r.rhat_loc,
                     (void*)r.st, (void*)r.hist, (void*)r.scr.part, (void*)r.scr.ticket,
                     (void*)r.scr.qpart, (void*)r.scr.tile_ticket, (void*)r.table_tmp,
                     (void*)r.kdev, (void*)r.pt_loc, (void*)r.U, (void*)r.qt_loc,
                     (void*)r.upart, (void*)r.col_ticket, (void*)r.gmV, (void*)r.gmH,
                     (void*)r.gm_hx, (void*)r.gm_state})
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
     if (r.h_done) cudaFreeHost(r.h_done);
     if (r.h_state) cudaFreeHost(r.h_state);
     for (auto e : r.ev_poll) if (e) cudaEventDestroy(e);
@@ -287,12 +288,12 @@ const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done, l
     const int64_t nrc = (r.m + rc - 1) / rc;
     const int64_t need = nrc * c->ld;
     if (need > r.upart_cap) {
-        if (r.upart) KS_CUDA(cudaFree(r.upart));
-        if (r.col_ticket) KS_CUDA(cudaFree(r.col_ticket));
+        dev_free(r.upart);
+        dev_free(r.col_ticket);
         r.upart = nullptr;
         r.col_ticket = nullptr;
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.upart), (size_t)need * sizeof(double)));
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.col_ticket), (size_t)(c->ld / 512 + 2) * sizeof(unsigned)));
+        dev_alloc_t(&r.upart, (size_t)need);
+        dev_alloc_t(&r.col_ticket, (size_t)(c->ld / 512 + 2));
         KS_CUDA(cudaMemset(r.col_ticket, 0, (size_t)(c->ld / 512 + 2) * sizeof(unsigned)));
         r.upart_cap = need;
     }

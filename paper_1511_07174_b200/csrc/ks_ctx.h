@@ -25,6 +25,15 @@ void nccl_check(ncclResult_t r, const char* what);
 #define KS_CUDA(x) ::ks::cuda_check((x), #x)
 #define KS_NCCL(x) ::ks::nccl_check((x), #x)
 
+// Device allocation of library buffers (ks_alloc.cpp): plain cudaMalloc/cudaFree, or
+// with KS_GUARD=1 4 KiB canary zones around every buffer for out-of-bounds-write
+// detection.  guard_check counts corrupted zones on the given devices (-1: off).
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+int64_t guard_check(const std::vector<int>& devs);
+template <class T>
+inline void dev_alloc_t(T** p, size_t count) { *p = static_cast<T*>(dev_alloc(count * sizeof(T))); }
+
 struct Rank {
     int rank = 0, dev = 0, num_sms = 148;
     cudaStream_t stream = nullptr;

@@ -197,10 +197,10 @@ GemvParams gp(const ks_ctx* c, const Rank& r, const double* x, double* y) {
 void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_cap) {
     const size_t nbytes = (size_t)c->n * sizeof(double);
     if (hist_cap > r.hist_alloc) {
-        KS_CUDA(cudaFree(r.hist));
+        dev_free(r.hist);
         r.hist = nullptr;
         r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.hist), (size_t)r.hist_alloc * sizeof(double)));
+        dev_alloc_t(&r.hist, (size_t)r.hist_alloc);
     }
     KS_CUDA(cudaMemcpyAsync(r.b_full, b, nbytes, cudaMemcpyDefault, r.stream));
     VecArgs a = r.vargs(false);   // setup gathers r0 with NCCL into parity 0
@@ -403,15 +403,15 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
     if (hist_cap > r.hist_alloc) {
-        KS_CUDA(cudaFree(r.hist));
+        dev_free(r.hist);
         r.hist = nullptr;
         r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.hist), (size_t)r.hist_alloc * sizeof(double)));
+        dev_alloc_t(&r.hist, (size_t)r.hist_alloc);
     }
     const bool fused = c->fused();
     VecArgsT<float> a0 = r.vargs_f32(false), a = r.vargs_f32(fused);
     double* tmp = nullptr;                              // FP64 staging of b / x
-    KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&tmp), (size_t)c->n * sizeof(double)));
+    dev_alloc_t(&tmp, (size_t)c->n);
     KS_CUDA(cudaMemcpyAsync(tmp, b, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
     r.launches += launch_d2f(tmp, a.b_full_mut(), c->n, r.stream);
     r.launches += launch_setup_r_f32(a0, r.stream);
@@ -493,7 +493,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
             KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault, r.stream));
         KS_CUDA(cudaStreamSynchronize(r.stream));
     }
-    KS_CUDA(cudaFree(tmp));
+    dev_free(tmp);
     if (rep) {
         float ms = 0.f;
         KS_CUDA(cudaEventElapsedTime(&ms, r.ev_t0, r.ev_t1));
@@ -529,22 +529,22 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
     r.gemv_seconds = 0.0;
     const size_t nbytes = (size_t)c->n * sizeof(double);
     if (hist_cap > r.hist_alloc) {
-        KS_CUDA(cudaFree(r.hist));
+        dev_free(r.hist);
         r.hist = nullptr;
         r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.hist), (size_t)r.hist_alloc * sizeof(double)));
+        dev_alloc_t(&r.hist, (size_t)r.hist_alloc);
     }
     if (r.gm_m < restart || !r.gmV) {
         for (void* p : {(void*)r.gmV, (void*)r.gmH, (void*)r.gm_hx, (void*)r.gm_state})
-            if (p) KS_CUDA(cudaFree(p));
+            dev_free(p);
         r.gm_ldv = (r.m + 31) / 32 * 32;
         r.gm_m = restart;
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gmV), (size_t)(restart + 1) * r.gm_ldv * sizeof(double)));
+        dev_alloc_t(&r.gmV, (size_t)(restart + 1) * r.gm_ldv);
         const size_t hsz = (size_t)(restart + 1) * restart + 3 * (size_t)(restart + 1);
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gmH), hsz * sizeof(double)));
+        dev_alloc_t(&r.gmH, hsz);
         KS_CUDA(cudaMemset(r.gmH, 0, hsz * sizeof(double)));
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gm_hx), (size_t)c->P * kMaxBasis * sizeof(double)));
-        KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&r.gm_state), sizeof(GmresState)));
+        dev_alloc_t(&r.gm_hx, (size_t)c->P * kMaxBasis);
+        dev_alloc_t(&r.gm_state, 1);
         KS_CUDA(cudaMemset(r.gm_state, 0, sizeof(GmresState)));
     }
     VecArgs a = r.vargs(false);
