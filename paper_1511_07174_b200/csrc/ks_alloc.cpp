@@ -73,6 +73,12 @@ void* dev_alloc(size_t bytes) {
     int dev = 0;
     KS_CUDA(cudaGetDevice(&dev));
     void* user = base + kGuard;
+    // detector self-test (KS_GUARD_SELFTEST=1): one byte past the end of every buffer
+    static const bool selftest = [] {
+        const char* v = std::getenv("KS_GUARD_SELFTEST");
+        return v && v[0] == '1';
+    }();
+    if (selftest) KS_CUDA(cudaMemset(base + kGuard + padded, 0, 1));
     std::lock_guard<std::mutex> lk(g_mu);
     registry()[user] = Entry{base, padded, dev};
     return user;
