@@ -129,11 +129,12 @@ typedef enum {
     KS_OPT_SMALL = 12         /* persistent path: 1 = small-n kernels that keep   */
                               /* the full vectors in every CTA's shared memory    */
                               /* (CG and BiCGSTAB on one GPU: 1 / 2 grid barriers */
-                              /* per iteration; CG on P > 1 GPUs with the fused   */
-                              /* exchange: one q exchange + 1 barrier) when they  */
-                              /* fit; 0 = off; 2 (default) = auto (on             */
+                              /* per iteration; on P > 1 GPUs with the fused      */
+                              /* exchange CG: one q exchange + 1 barrier,         */
+                              /* BiCGSTAB: v and t exchanges + 2 barriers) when   */
+                              /* they fit; 0 = off; 2 (default) = auto (on        */
                               /* when a vector is <= 32 KiB: FP64 n <= 4096, FP32 */
-                              /* n <= 8192)                                       */
+                              /* n <= 8192; BiCGSTAB on P > 1: <= 16 KiB)         */
 } ks_option;
 
 /* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL

@@ -238,8 +238,8 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
 
 // Small-n kernels (ks_small.cu, NEXT-2): full-length vectors in every CTA's shared
 // memory, 1 (CG) / 2 (BiCGSTAB) grid barriers per iteration.  kind: 0 = CG, 1 =
-// BiCGSTAB (P = 1), 2 = CG over P > 1 GPUs with the fused exchange (allgather-only:
-// one exchange + one barrier per iteration; a = vargs(true)).  small_grid (rows =
+// BiCGSTAB (P = 1), 2 = CG, 3 = BiCGSTAB over P > 1 GPUs with the fused exchange
+// (allgather-only: one / two exchanges and barriers per iteration; a = vargs(true)).  small_grid (rows =
 // this rank's rows) returns 0 when the vectors do not fit in shared memory.
 template <class T>
 int small_grid(int kind, int num_sms, int64_t rows, int64_t ncols);

@@ -17,9 +17,11 @@
 // CTA partials) are double-buffered by iteration parity; the single barrier per
 // reduction then orders everything.  The global copies of r, p, v (and G_r's
 // partial slots) are refreshed every iteration by their owning threads, so a
-// later launch (the next poll batch) or the finish kernels see current state.
-// k_cg_small / k_bs_small run on one GPU; k_cg_small_peer is the CG variant for
-// P > 1 GPUs with the fused exchange (see its comment).
+// later launch (the next poll batch) or the finish kernels see current state --
+// each only after the iteration's first grid barrier, since before it a slow CTA
+// may still be loading the previous values at the start of its launch.
+// k_cg_small / k_bs_small run on one GPU; k_cg_small_peer / k_bs_small_peer are the
+// variants for P > 1 GPUs with the fused exchange (see their comments).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -242,6 +244,209 @@ __global__ void __launch_bounds__(kNT, 2) k_cg_small_peer(PersistArgs<T> P) {
     }
 }
 
+// --------------------------------------- BiCGSTAB on P > 1 GPUs (fused exchange)
+// Allgather-only BiCGSTAB on the small-n kernel: the two GEMV outputs (v rows,
+// t rows) are the iteration's only exchanges (into every rank's G_v / G_r, parity
+// i); everything else -- <rhat, v>, s, ||s||, <t, s>, <t, t>, r, <rhat, r>, <r, r>,
+// p -- is formed over the full length in every CTA's shared memory, in one fixed
+// order.  Two exchanges and two grid barriers per iteration (general fused
+// kernels: three and five).  rhat (full length) is kept in shared memory and, for
+// later launches of the same solve, in s_full.  The test of the last iteration of
+// the solve is made in-kernel (the general path defers it to k_finish).
+template <class T, int kR, int kU>
+__global__ void __launch_bounds__(kNT, 1) k_bs_small_peer(PersistArgs<T> P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sp = reinterpret_cast<T*>(smem_raw);   // p (ncols, zero padded)
+    T* ss = sp + P.ncols;                     // r -> s -> r (ncols, zero padded)
+    T* sv = ss + P.ncols;                     // v (n)
+    T* sh = sv + P.ncols;                     // rhat (n)
+    __shared__ T red[(kR > 2 ? kR : 2) * kNW];
+    const VecArgsT<T>& a = P.a;
+    const Layout& L = a.L;
+    DevState* st = a.st;
+    const int64_t n = L.n, m = rows_of(L), r0 = L.row0[L.rank];
+    const int64_t gstride = (int64_t)gridDim.x * kNT;
+    const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
+    if (is_done(st)) return;
+    const T* rin = par_ptr(a.G_r, a.gpar, P.k0 - 1);
+    for (int64_t j = threadIdx.x; j < P.ncols; j += kNT) {
+        sp[j] = j < n ? a.p_full[j] : T(0);
+        ss[j] = j < n ? rin[gidx(L, j)] : T(0);
+        if (j < n) {
+            sv[j] = a.v_full[j];
+            sh[j] = P.k0 == 1 ? ss[j] : a.s_full[j];      // rhat = r0 (Q7)
+        }
+    }
+    if (P.k0 == 1)
+        for (int64_t j = tid0; j < n; j += gstride) a.s_full[j] = rin[gidx(L, j)];
+    T rho = slot_sum(L, rin, 0), rr = slot_sum(L, rin, 1);
+    T rho_prev = (T)st->rho[(P.k0 - 1) & 3], alpha_prev = (T)st->alpha[(P.k0 - 1) & 3];
+    T omega_prev = (T)st->omega[(P.k0 - 1) & 3];
+    const long long maxit = st->maxit;
+    __syncthreads();
+    const int64_t tiles = (m + kR - 1) / kR;
+    const int64_t ncb = P.ncols / (Vec16<T>::W * kNT);
+    // this rank's rows of y = A x (x in shared memory) into slot `off` of every rank's G
+    auto gemv_push = [&](const T* xs, T* const* G, int64_t off) {
+        bool pushed = false;
+        for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int64_t t0 = tile * kR;
+            const int nvalid = (int)min((int64_t)kR, m - t0);
+            T acc[kR];
+            stream_rows<kR, kU, kNT, T, true>(P.A, P.lda, t0, nvalid, xs, 0, ncb, acc);
+            block_sum<kNT, kR>(acc, red);
+            if (threadIdx.x == 0) {
+                for (int r = 0; r < nvalid; ++r)
+                    for (int g = 0; g < L.P; ++g) G[g][off + t0 + r] = acc[r];
+                pushed = true;
+            }
+        }
+        if (pushed) __threadfence_system();
+    };
+    for (long long i = P.k0; i <= P.k1; ++i) {
+        // B8 (test of i-1) + B1
+        T rel = T(0);
+        if (i >= 2) {
+            rel = sqrt(rr) / (T)st->nb;
+            if (rel <= (T)st->tol) {
+                if (lead()) {
+                    put_hist(st, a.hist, i - 2, rel);
+                    st->relres = rel; st->iters = i - 1; st->converged = 1; st->status = KS_OK; st->done = 1;
+                }
+                return;
+            }
+        }
+        if (rho == T(0) || !isfinite(rho)) {
+            if (lead()) {
+                if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
+                st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1;
+            }
+            return;
+        }
+        if (i == 1) {
+            for (int64_t j = threadIdx.x; j < n; j += kNT) sp[j] = ss[j];
+        } else {
+            const T beta = (rho / rho_prev) * (alpha_prev / omega_prev);
+            for (int64_t j = threadIdx.x; j < n; j += kNT) sp[j] = fma(beta, fma(-omega_prev, sv[j], sp[j]), ss[j]);
+        }
+        if (lead()) {
+            if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
+            st->rho[i & 3] = rho;
+            st->iters = i - 1;
+        }
+        __syncthreads();
+        // B2/B3: v rows -> every rank's G_v (parity i); gather
+        const int64_t po = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
+        gemv_push(sp, a.pp.G_v, po);
+        if (!grid_sync(P.bar, st)) return;
+        // p to global only now: before this barrier a slow CTA may still be loading
+        // the previous p at the start of the launch
+        for (int64_t j = tid0; j < n; j += gstride) a.p_full[j] = sp[j];
+        if (lead()) flags_out(a, kPhaseV, i);
+        if (!wait_ph(a, kPhaseV, i)) return;
+        // B4: gamma = <rhat, v> (full length), alpha
+        const T* vg = par_ptr(a.G_v, a.gpar, i);
+        T gm[1] = {T(0)};
+        for (int64_t j = threadIdx.x; j < n; j += kNT) {
+            const T vj = __ldcg(vg + gidx(L, j));
+            sv[j] = vj;
+            gm[0] = fma(sh[j], vj, gm[0]);
+        }
+        cta_total<1>(gm, red);
+        const T gam = gm[0];
+        if (gam == T(0) || !isfinite(gam)) {
+            if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+            return;
+        }
+        const T alpha = rho / gam;
+        // B5: s = r - alpha v, ||s|| (full length), half-step test
+        T sacc[1] = {T(0)};
+        for (int64_t j = threadIdx.x; j < n; j += kNT) {
+            const T s = fma(-alpha, sv[j], ss[j]);
+            ss[j] = s;
+            sacc[0] = fma(s, s, sacc[0]);
+        }
+        cta_total<1>(sacc, red);
+        for (int64_t j = tid0; j < n; j += gstride) a.v_full[j] = sv[j];
+        const T srel = sqrt(sacc[0]) / (T)st->nb;
+        if (srel <= (T)st->tol) {
+            for (int64_t l = tid0; l < m; l += gstride) a.x_loc[l] = fma(alpha, sp[r0 + l], a.x_loc[l]);
+            if (lead()) {
+                put_hist(st, a.hist, i - 1, srel);
+                st->alpha[i & 3] = alpha;
+                st->relres = srel; st->half = 1; st->half_iter = i; st->converged = 1;
+                st->status = KS_OK; st->iters = i; st->done = 1;
+            }
+            return;
+        }
+        // B6: t rows -> every rank's G_r (parity i); gather
+        gemv_push(ss, a.pp.G_r, po);
+        if (!grid_sync(P.bar, st)) return;
+        if (lead()) flags_out(a, kPhaseS, i);
+        if (!wait_ph(a, kPhaseS, i)) return;
+        // B7: <t, s>, <t, t> (full length), omega
+        const T* tg = par_ptr(a.G_r, a.gpar, i);
+        T tv[2] = {T(0), T(0)};
+        for (int64_t j = threadIdx.x; j < n; j += kNT) {
+            const T tj = __ldcg(tg + gidx(L, j));
+            tv[0] = fma(tj, ss[j], tv[0]);
+            tv[1] = fma(tj, tj, tv[1]);
+        }
+        cta_total<2>(tv, red);
+        const T ts = tv[0], tt = tv[1];
+        const T om = ts / tt;
+        if (tt == T(0) || !isfinite(tt) || om == T(0) || !isfinite(om)) {
+            if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+            return;
+        }
+        // x += alpha p + omega s (own rows); r = s - omega t, <rhat, r>, <r, r> (full length)
+        for (int64_t l = tid0; l < m; l += gstride)
+            a.x_loc[l] = fma(om, ss[r0 + l], fma(alpha, sp[r0 + l], a.x_loc[l]));
+        __syncthreads();
+        T acc[2] = {T(0), T(0)};
+        for (int64_t j = threadIdx.x; j < n; j += kNT) {
+            const T r = fma(-om, __ldcg(tg + gidx(L, j)), ss[j]);
+            ss[j] = r;
+            acc[0] = fma(sh[j], r, acc[0]);
+            acc[1] = fma(r, r, acc[1]);
+        }
+        cta_total<2>(acc, red);
+        if (lead()) {
+            st->alpha[i & 3] = alpha;
+            st->omega[i & 3] = om;
+            st->iters = i;
+        }
+        rho_prev = rho;
+        alpha_prev = alpha;
+        omega_prev = om;
+        rho = acc[0];
+        rr = acc[1];
+        if (i == P.k1) {
+            if (i == maxit) {                          // test of the solve's last step (B8)
+                if (lead()) {
+                    const T relm = sqrt(rr) / (T)st->nb;
+                    put_hist(st, a.hist, i - 1, relm);
+                    st->relres = relm;
+                    if (relm <= (T)st->tol) { st->converged = 1; st->status = KS_OK; }
+                    else st->status = KS_EMAXIT;
+                    st->done = 1;
+                }
+                return;
+            }
+            // hand r and its partial slots to the next launch (after every CTA read t)
+            if (!grid_sync(P.bar, st)) return;
+            T* rout = par_ptr(a.G_r, a.gpar, i);
+            for (int64_t j = tid0; j < n; j += gstride) rout[gidx(L, j)] = ss[j];
+            if (lead()) {
+                for (int g = 0; g < L.P; ++g) {
+                    rout[(int64_t)g * L.chunk + L.pslot + 0] = g == 0 ? rho : T(0);
+                    rout[(int64_t)g * L.chunk + L.pslot + 1] = g == 0 ? rr : T(0);
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------ BiCGSTAB (B1-B8)
 template <class T, int kR, int kU>
 __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
@@ -299,7 +504,6 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
             st->iters = i - 1;
         }
         __syncthreads();
-        for (int64_t j = tid0; j < n; j += gstride) a.p_full[j] = sp[j];
         // B3: v = A p (parity buffer), <rhat, v> partial
         T* vb = par_ptr(a.G_v, a.gpar, i);
         T d1 = T(0), d2 = T(0);
@@ -321,6 +525,9 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
         }
         if (threadIdx.x == 0) P.bpart[blockIdx.x * kSlots + (i & 1) * 4 + 0] = d1;
         if (!grid_sync(P.bar, st)) return;
+        // p to global only now: before this barrier a slow CTA may still be loading
+        // the previous p at the start of the launch
+        for (int64_t j = tid0; j < n; j += gstride) a.p_full[j] = sp[j];
         T gm[1] = {T(0)};
         for (int b = threadIdx.x; b < (int)gridDim.x; b += kNT)
             gm[0] += __ldcg(P.bpart + (int64_t)b * kSlots + (i & 1) * 4 + 0);
@@ -404,15 +611,16 @@ __global__ void __launch_bounds__(kNT, 2) k_bs_small(PersistArgs<T> P) {
 // Tile shape: R = 4 rows, U = 2 column blocks (C1: 256 tiles of 8 KiB rows).
 constexpr int kSR = 4, kSU = 2;
 
-// kind: 0 = CG, 1 = BiCGSTAB (P = 1), 2 = CG with the fused exchange (P > 1)
+// kind: 0 = CG, 1 = BiCGSTAB (P = 1), 2 = CG, 3 = BiCGSTAB with the fused exchange (P > 1)
 template <class T>
 const void* kern(int kind) {
-    return kind == 2 ? (const void*)k_cg_small_peer<T, kSR, kSU>
+    return kind == 3 ? (const void*)k_bs_small_peer<T, kSR, kSU>
+         : kind == 2 ? (const void*)k_cg_small_peer<T, kSR, kSU>
          : kind == 1 ? (const void*)k_bs_small<T, kSR, kSU> : (const void*)k_cg_small<T, kSR, kSU>;
 }
 template <class T>
 size_t smem_bytes(int kind, int64_t ncols) {
-    return (size_t)(kind == 0 ? 2 : 3) * (size_t)ncols * sizeof(T);
+    return (size_t)(kind == 0 ? 2 : kind == 3 ? 4 : 3) * (size_t)ncols * sizeof(T);
 }
 
 }  // namespace

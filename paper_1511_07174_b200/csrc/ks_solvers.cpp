@@ -33,7 +33,12 @@ int small_kind(const ks_ctx* c, int bicgstab) {
     if (c->opt.small == 0) return -1;
     if (c->opt.small == 2 && c->n * (int64_t)c->esz > ks_ctx::kSmallAutoMaxBytes) return -1;
     if (c->P == 1) return bicgstab ? 1 : 0;
-    return (!bicgstab && c->fused()) ? 2 : -1;
+    if (!c->fused()) return -1;
+    // BiCGSTAB over P > 1: the shared-memory schedule wins up to 16 KiB vectors
+    // (n = 512: 33 -> 20 us/iteration at P = 2); at 32 KiB the general fused
+    // kernels are faster (n = 4096, P = 2: 52 vs 60 us), profiles/r01_exchange_cost_small_peer2.jsonl
+    if (bicgstab && c->opt.small == 2 && c->n * (int64_t)c->esz > ks_ctx::kSmallAutoMaxBytes / 2) return -1;
+    return bicgstab ? 3 : 2;
 }
 // Grid of the small-n kernels, 0 = not used.
 template <class T>

@@ -100,6 +100,47 @@ def test_multi_small_cg_allgather_only(P, dtype):
 
 @needs2
 @pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_multi_small_bicgstab_allgather_only(P, dtype):
+    """Small-n BiCGSTAB over P GPUs (k_bs_small_peer: v and t slices are the only
+    exchanges, two grid barriers per iteration) vs the oracle and the general fused
+    kernels: ragged n, half-step exit, maxit (in-kernel final test), x0, and a
+    multi-launch solve (rhat and r handed over between launches)."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    from test_gpu_parity import bars_f32
+    for n, kd in ((1003, 4), (4096, 16)):
+        A, b = synth.gdd(n, kd)
+        if dtype == "f32":
+            xo, ho, ro = oracle.bicgstab_f32(A, b, tol=1e-5)
+        else:
+            xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
+        its = []
+        for small in (1, 0):
+            with ks.Context(n, ngpus=P, dtype=dtype) as ctx:
+                ctx.set_option("small", small)
+                ctx.load_rows(A)
+                if dtype == "f32":
+                    x, h, r = ctx.bicgstab(b.astype(np.float32).astype(np.float64), tol=1e-5)
+                    bars_f32(x, h, r, xo, ho, ro)
+                else:
+                    x, h, r = ctx.bicgstab(b, tol=1e-10)
+                    bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+                    assert r.half_step_exit == ro.half_step_exit
+                    ctx.set_option("poll_batch", 3)
+                    x2, h2, r2 = ctx.bicgstab(b, tol=1e-10)
+                    assert r2.iterations == r.iterations and np.array_equal(x2, x) and np.array_equal(h2, h)
+                    x0 = np.random.default_rng(n).standard_normal(n)
+                    xo5, ho5, ro5 = oracle.bicgstab(A, b, x0=x0, tol=1e-30, maxit=5)
+                    x5, h5, r5 = ctx.bicgstab(b, x0=x0, tol=1e-30, maxit=5)
+                    assert r5.status == ks.KS_EMAXIT and r5.iterations == 5 and len(h5) == 5
+                    bars(x5, h5, r5, xo5, ho5, ro5, iters_tol=0, floor=FLOOR_BS)
+                its.append(r.iterations)
+        assert abs(its[0] - its[1]) <= 2
+
+
+@needs2
+@pytest.mark.parametrize("P", [2, 4])
 def test_multi_bicgstab(P):
     if ngpu() < P:
         pytest.skip(f"needs {P} GPUs")
