@@ -37,8 +37,10 @@ def gemv_bound_check(A, x, y):
 
 
 # Absolute floor of the history bar (relres units), reading Q17:
-# CG 1e-14 (survey App. A.5); BiCGSTAB 1e-12 -- the oracle disagrees with itself
-# by 6.4e-14 on a permuted copy of G-DD(1024,16) (test_Q17_bicgstab_floor).
+# CG 1e-14 (survey App. A.5); BiCGSTAB 1e-12 -- 24 legitimate summation orders of
+# the oracle itself (symmetric permutations of G-DD(1024,16)) differ by up to
+# 5.5e-13 near relres 1e-10, so 2e-13 would reject correct results
+# (test_oracle_exact_pins.py::test_Q17_bicgstab_floor_distribution).
 FLOOR_CG, FLOOR_BS = 1e-14, 1e-12
 
 
@@ -216,7 +218,8 @@ def test_spec_examples_gpu():
     with ks.Context(100) as ctx:
         # SPEC.md:560.  BiCGSTAB is chaotic on this nonnormal matrix (the oracle gives
         # 106 vs 104 iterations on a permuted copy; histories diverge from iteration
-        # 19), so the pin is SPEC's own property plus the true residual.
+        # 20: test_chaos_convection_diffusion_not_a_parity_input), so the pin is
+        # SPEC's own property plus the true residual.
         A = synth.convection_diffusion(100, 0.1)
         ctx.load_rows(A)
         x, h, r = ctx.bicgstab(np.ones(100), tol=1e-8)
@@ -246,7 +249,8 @@ def test_bicgstab_parity(n, kd, variant):
 def test_bicgstab_x0_breakdown_maxit():
     # G-DD (positive spread diagonal): histories are order-insensitive here.  A
     # random-sign diagonal (synth.random_dd) is NOT a parity input: the oracle
-    # differs from itself by 1e-3 at iteration 5 on a permuted copy (chaos).
+    # differs from itself by > 1e-3 within 7 iterations on a reversed copy
+    # (test_chaos_random_sign_diagonal_not_a_parity_input).
     n = 300
     A, _ = synth.gdd(n, 4, seed=synth.SEED2)
     rng = np.random.default_rng(6)
