@@ -101,6 +101,7 @@ def lib():
         L.or_hash.restype = u64
         L.or_hash.argtypes = [u64, u64, u64]
         L.or_gen_rows.argtypes = [C.POINTER(_Gen), i64, i64, _D, i64]
+        L.or_gen_rows_par.argtypes = [C.POINTER(_Gen), i64, i64, _D, i64, i32]
         L.or_gen_rhs.argtypes = [i64, u64, _D]
         _lib = L
     return _lib
@@ -347,11 +348,16 @@ def hash64(seed: int, stream: int, key: int) -> int:
     return int(lib().or_hash(seed, stream, key))
 
 
-def gen_rows(gen: dict, r0: int, nrows: int) -> np.ndarray:
+def gen_rows(gen: dict, r0: int, nrows: int, threads: int = 1) -> np.ndarray:
+    """Rows [r0, r0 + nrows) of the generated matrix (bitwise the same for any
+    thread count: rows are expanded independently)."""
     n = int(gen["n"])
     op = Operator(gen=gen)
     A = np.empty((nrows, n))
-    lib().or_gen_rows(op._op.gen, r0, nrows, _p(A), n)
+    if threads > 1:
+        lib().or_gen_rows_par(op._op.gen, r0, nrows, _p(A), n, threads)
+    else:
+        lib().or_gen_rows(op._op.gen, r0, nrows, _p(A), n)
     return A
 
 

@@ -117,6 +117,15 @@ void or_gen_rows(const or_gen* g, int64_t r0, int64_t nrows, double* A, int64_t 
     for (int64_t r = 0; r < nrows; ++r) or_gen_row(g, r0 + r, A + r * lda);
 }
 
+/* The same rows expanded by `threads` OpenMP threads (rows are independent, so
+ * the result is bitwise equal to or_gen_rows); used to store the n = 65536
+ * matrices on the host for the full-size parity runs and the CPU baseline. */
+void or_gen_rows_par(const or_gen* g, int64_t r0, int64_t nrows, double* A, int64_t lda,
+                     int32_t threads) {
+#pragma omp parallel for schedule(static) num_threads(threads < 1 ? 1 : threads)
+    for (int64_t r = 0; r < nrows; ++r) or_gen_row(g, r0 + r, A + r * lda);
+}
+
 /* b_i = 2*U53(seed,2,i) - 1 */
 void or_gen_rhs(int64_t n, uint64_t seed, double* b) {
     for (int64_t i = 0; i < n; ++i) b[i] = 2.0 * u53(seed, 2, (uint64_t)i) - 1.0;

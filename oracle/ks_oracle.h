@@ -94,6 +94,8 @@ double or_true_relres_ld(const or_op* op, const double* b, const double* x);
 uint64_t or_hash(uint64_t seed, uint64_t stream, uint64_t key);
 void or_gen_row(const or_gen* g, int64_t i, double* row);
 void or_gen_rows(const or_gen* g, int64_t r0, int64_t nrows, double* A, int64_t lda);
+void or_gen_rows_par(const or_gen* g, int64_t r0, int64_t nrows, double* A, int64_t lda,
+                     int32_t threads);
 void or_gen_rhs(int64_t n, uint64_t seed, double* b);
 
 #ifdef __cplusplus

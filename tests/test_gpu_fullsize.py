@@ -5,7 +5,11 @@ checks what it can compute one by one, and properties that hold at any size:
   * sampled GEMV rows vs the oracle's on-the-fly generated rows (P9 bound),
   * CG x vs the long-double closed-form solution (P6), survey App. A.8 counts (P14),
   * BiCGSTAB true residual by the oracle with on-the-fly rows (P11),
-  * the first BiCGSTAB iterations vs the oracle itself (north-star bars).
+  * the C3 gate: the WHOLE BiCGSTAB history (23 iterations)
+    and x vs the oracle's own full solve on G-DD(65536, 16) -- the oracle stores
+    the 34 GB matrix on the host when RAM allows (else generates rows on the fly)
+    and runs row-parallel on all host cores (every row sum sequential, so bitwise
+    the 1-thread oracle) -- on 1 GPU and on every P in {2, 4, 8} the box has.
 """
 import os
 
@@ -22,7 +26,48 @@ from test_gpu_parity import FLOOR_BS, bars, gamma  # noqa: E402
 
 N = 65536
 THREADS = os.cpu_count() or 1
-SAMPLE = [0, 1, 511, 512, 4095, 32767, 32768, 65534, 65535] + \
+
+
+def _mem_available() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def oracle_operator(kind: str, n: int, **kw):
+    """The oracle's operator for a generated matrix at full size: stored rows
+    (expanded by the oracle's own generator on all host cores) when the host has
+    room for them, else rows generated on the fly.  Same entries, same order,
+    bitwise the same GEMV either way (test_true_relres_stored_equals_on_the_fly)."""
+    spec = synth.spec(kind, n, **kw)
+    if _mem_available() > 1.25 * 8.0 * n * n + 16e9:
+        A = oracle.gen_rows(spec, 0, n, threads=THREADS)
+        return oracle.Operator(A, threads=THREADS), "stored"
+    return oracle.Operator(gen=spec, threads=THREADS), "on-the-fly"
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.fixture(scope="module")
+def c3_oracle():
+    """The oracle's full C3 solve: BiCGSTAB on G-DD(65536, 16), tol 1e-10, x0 = 0
+    (46 GEMVs).  Survey App. A.8: 23 iterations, full-step exit."""
+    b = synth.rhs(N)
+    op, mode = oracle_operator("dd", N, kd=16)
+    xo, ho, ro = oracle.bicgstab(op, b, tol=1e-10)
+    del op
+    return b, xo, ho, ro, mode
+
+
+SAMPLE =[0, 1, 511, 512, 4095, 32767, 32768, 65534, 65535] + \
     list(np.random.default_rng(65536).integers(0, N, 23))
 
 
@@ -82,6 +127,29 @@ def test_fullsize_bicgstab_true_residual_and_first_iterations():
     # the oracle itself, 2 iterations (4 GEMVs with on-the-fly rows)
     xo, ho, ro = oracle.bicgstab(op, b, tol=0.0, maxit=2)
     bars(x2, h2, r2, xo, ho, ro, iters_tol=0, floor=FLOOR_BS)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_c3_bicgstab_full_history_and_x_vs_oracle(P, c3_oracle):
+    """C3 gate, north-star bars on the whole run at the headline size, in the
+    bench's launch configuration (persistent kernels, fused exchange for P > 1):
+    every history entry (Q17 floor), x within 1e-9 of the oracle's x, iteration
+    count within 2 (expected: equal), same exit kind."""
+    if _ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    b, xo, ho, ro, mode = c3_oracle
+    assert ro.converged and ro.iterations == 23 and not ro.half_step_exit, (ro, mode)
+    with ks.Context(N, ngpus=P) as ctx:
+        bg = ctx.generate("dd", seed=synth.SEED, kd=16)
+        assert np.array_equal(bg, b)                               # P12
+        x, h, r = ctx.bicgstab(bg, tol=1e-10)
+    assert r.converged and r.half_step_exit == ro.half_step_exit
+    assert len(h) == r.iterations and len(ho) == ro.iterations
+    bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+    k = min(len(h), len(ho))
+    assert k >= 21
+    assert np.all(np.abs(h[:k] - ho[:k]) <= 1e-8 * ho[:k] + FLOOR_BS)
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
 
 
 def _first50(h, ho, floor):

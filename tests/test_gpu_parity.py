@@ -246,6 +246,35 @@ def test_bicgstab_parity(n, kd, variant):
     assert r.true_relres <= 10 * 1e-10
 
 
+@pytest.mark.parametrize("persistent", [1, 0])
+def test_large_shard_shape_odd_n(persistent):
+    """The production large-n configuration (a shard of > 4096 rows selects the
+    persistent GEMV phase's R = 2 / U = 4 shape; small-n kernels off) at an odd n:
+    a ragged last row tile and a ragged last 512-column block, both methods, vs the
+    oracle with the north-star bars.  persistent = 0 runs the multi-kernel K1 path
+    at the same n."""
+    n = 5003
+    D, bd = synth.gdd(n, 16)
+    xo, ho, ro = oracle.bicgstab(oracle.Operator(D, threads=os.cpu_count() or 1), bd, tol=1e-10)
+    S = synth.random_spd(n, 100.0, 9)
+    bs = np.random.default_rng(9).standard_normal(n)
+    xc, hc, rc = oracle.cg(oracle.Operator(S, threads=os.cpu_count() or 1), bs, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.set_option("small", 0)
+        ctx.set_option("persistent", persistent)
+        ctx.load_rows(D)
+        x, h, r = ctx.bicgstab(bd, tol=1e-10)
+    bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+    assert r.converged and r.half_step_exit == ro.half_step_exit
+    with ks.Context(n) as ctx:
+        ctx.set_option("small", 0)
+        ctx.set_option("persistent", persistent)
+        ctx.load_rows(S)
+        x, h, r = ctx.cg(bs, tol=1e-10)
+    bars(x, h, r, xc, hc, rc)
+    assert r.converged
+
+
 def test_bicgstab_x0_breakdown_maxit():
     # G-DD (positive spread diagonal): histories are order-insensitive here.  A
     # random-sign diagonal (synth.random_dd) is NOT a parity input: the oracle
