@@ -79,6 +79,36 @@ def environment(local: int) -> dict:
     return env
 
 
+def topology(world: int, local: int) -> dict:
+    """Rank -> GPU map and the peer topology the fused exchange runs over (the
+    fused path makes no NCCL call per iteration, so NCCL's own communicator lines
+    say little about it)."""
+    import torch
+    import torch.distributed as dist
+    me = {"rank": int(os.environ.get("RANK", 0)), "local_rank": local,
+          "device": torch.cuda.get_device_name(local),
+          "pci": torch.cuda.get_device_properties(local).pci_bus_id
+          if hasattr(torch.cuda.get_device_properties(local), "pci_bus_id") else None}
+    ranks = [me]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, me)
+    nd = torch.cuda.device_count()
+    p2p = {f"{i}->{j}": bool(torch.cuda.can_device_access_peer(i, j))
+           for i in range(nd) for j in range(nd) if i != j}
+    links = None
+    try:
+        out = subprocess.run(["nvidia-smi", "topo", "-m"], capture_output=True, text=True,
+                             timeout=10).stdout
+        rows = [ln.split() for ln in out.splitlines() if ln.startswith("GPU")]
+        links = {r[0]: r[1:1 + nd] for r in rows[:nd]} if rows else None
+    except Exception:
+        pass
+    return {"world_size": world, "ranks": ranks, "visible_gpus": nd,
+            "peer_access_all_pairs": all(p2p.values()) if p2p else None,
+            "nvidia_smi_topo": links}
+
+
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -233,7 +263,7 @@ def run_ours(args):
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
     if args.gpus != world:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -368,6 +398,7 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    topo = topology(world, local)          # collective: every rank takes part
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -410,6 +441,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "generate_s": t_gen,
             "env": environment(local),
+            "topology": topo,
         }
         json_out.write(json.dumps(line) + "\n")
         json_out.flush()
@@ -436,9 +468,26 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return relaunch(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: re-execute this same command
+    under torch.distributed.run with one process per GPU (the driver's own launch
+    line), so N ranks always run -- never a silent one-GPU run."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -28,9 +28,13 @@ def ngpu():
 
 needs2 = pytest.mark.skipif("ngpu() < 2", reason="needs >= 2 GPUs (gpurun --gpus 2)")
 
+# every multi-GPU test runs at each P the box has (the 8-GPU box of the driver's
+# scaling step included); a P above the device count skips
+PS = [2, 4, 8]
+
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 def test_multi_gemv_and_cg(P):
     if ngpu() < P:
         pytest.skip(f"needs {P} GPUs")
@@ -59,7 +63,7 @@ def test_multi_gemv_and_cg(P):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_multi_small_cg_allgather_only(P, dtype):
     """Small-n CG over P GPUs (k_cg_small_peer: one exchange of q slices and one grid
@@ -99,7 +103,7 @@ def test_multi_small_cg_allgather_only(P, dtype):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_multi_small_bicgstab_allgather_only(P, dtype):
     """Small-n BiCGSTAB over P GPUs (k_bs_small_peer: v and t slices are the only
@@ -140,7 +144,7 @@ def test_multi_small_bicgstab_allgather_only(P, dtype):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 def test_multi_bicgstab(P):
     if ngpu() < P:
         pytest.skip(f"needs {P} GPUs")
@@ -155,7 +159,7 @@ def test_multi_bicgstab(P):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 def test_fused_collectives_bitwise_equal_nccl(P):
     """NEXT-1: the fused NVLink peer-store collectives carry the same partials and
     sum them in the same rank order as the NCCL allgathers, so x, the history and
@@ -191,7 +195,7 @@ def test_fused_collectives_bitwise_equal_nccl(P):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 def test_multi_persistent_fused(P):
     """NEXT-1 + NEXT-2 together: persistent cooperative kernels on every GPU with
     the fused NVLink exchange; bars vs the oracle; identical on repeat."""
@@ -216,7 +220,7 @@ def test_multi_persistent_fused(P):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 @pytest.mark.parametrize("fused", [1, 0])
 def test_multi_bicg(P, fused):
     """NEXT-3 BiCG at P GPUs: K1T partials reduce-scattered either inside K1T over
@@ -244,7 +248,7 @@ def test_multi_bicg(P, fused):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 @pytest.mark.parametrize("persistent", [0, 1])
 def test_multi_gmres(P, persistent):
     """NEXT-3 GMRES(m) at P GPUs: multi-kernel path with NCCL exchanges of the CGS2
@@ -270,7 +274,7 @@ def test_multi_gmres(P, persistent):
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 def test_multi_f32(P):
     """NEXT-4 at P GPUs: FP32 persistent kernels with the fused NVLink exchange."""
     if ngpu() < P:
@@ -308,7 +312,7 @@ def test_multi_edge_cases():
 
 
 @needs2
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", PS)
 def test_torchrun_borrowed_comm(tmp_path, P):
     """One process per GPU (torchrun, nccl); every rank returns the same x and
     history; results meet the bars vs the oracle."""
@@ -360,11 +364,14 @@ def test_torchrun_borrowed_comm(tmp_path, P):
 
 
 @needs2
-def test_multi_fullsize_65536():
-    """C3/C3' at P = all GPUs (<= 4), default path (persistent + fused): CG vs the
-    closed form and the survey's counts; BiCGSTAB counts/histories and the true
-    residual by the oracle with on-the-fly rows (pins P6, P11, P14 at scale)."""
-    P = min(4, ngpu())
+@pytest.mark.parametrize("P", PS)
+def test_multi_fullsize_65536(P):
+    """C3/C3' at P GPUs, default path (persistent + fused): CG vs the closed form
+    and the survey's counts; BiCGSTAB counts/histories and the true residual by the
+    oracle with on-the-fly rows (pins P6, P11, P14 at scale).  The C3 history/x gate
+    vs the oracle's full solve at every P is test_gpu_fullsize.py's."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
     n = 65536
     c = synth.spd_table(n, 1e4)
     with ks.Context(n, ngpus=P) as ctx:
@@ -383,20 +390,46 @@ def test_multi_fullsize_65536():
     assert oracle.true_relres_ld(op, b, x) <= 10 * 1e-10
 
 
-@pytest.mark.skipif("ngpu() < 4", reason="needs 4 GPUs (137 GB per GPU)")
-def test_c5_262144_p4():
-    """C5: n = 262144 (550 GB in total, 137 GB per GPU) at P = 4: CG vs the closed
-    form (survey: 1070 iterations); BiCGSTAB converges with a small true residual
-    checked by the oracle on sampled rows (on-the-fly generation)."""
+@needs2
+@pytest.mark.parametrize("P", PS)
+def test_c4_131072_multi(P):
+    """C4 (n = 131072, 137 GB in total) strong-scaled over P GPUs: CG to tol 1e-10
+    vs the closed form (P6), the survey count 979 (P14), the same count as one GPU
+    would take (P13: survey App. A.8), and sampled true-residual rows by the oracle
+    (P11, on-the-fly rows)."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    n = 131072
+    c = synth.spd_table(n, 1e4)
+    with ks.Context(n, ngpus=P) as ctx:
+        b = ctx.generate("spd", seed=synth.SEED, table=c)
+        x, h, r = ctx.cg(b, tol=1e-10)
+    assert r.converged and abs(r.iterations - 979) <= 2, r
+    xcf = oracle.spd_exact_solve_ld(c, synth.SEED, b)
+    assert np.linalg.norm(x - xcf) <= 1e4 * 1e-10 * np.linalg.norm(xcf)
+    assert r.true_relres <= 10 * 1e-10
+    op = oracle.Operator(gen=synth.spec("spd", n, kappa=1e4), threads=min(8, os.cpu_count() or 1))
+    nb = float(np.linalg.norm(b))
+    for i in (0, 16383, 16384, 65535, 65536, 131071):
+        assert abs(b[i] - op.rows(i, 1, x)[0]) <= 10 * 1e-10 * nb
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_c5_262144(P):
+    """C5: n = 262144 (550 GB in total; 137 / 69 GB per GPU at P = 4 / 8): CG vs the
+    closed form (survey: 1070 iterations); BiCGSTAB converges with a small true
+    residual checked by the oracle on sampled rows (on-the-fly generation)."""
+    if ngpu() < P:
+        pytest.skip(f"needs {P} GPUs (C5 does not fit fewer)")
     n = 262144
     c = synth.spd_table(n, 1e4)
-    with ks.Context(n, ngpus=4) as ctx:
+    with ks.Context(n, ngpus=P) as ctx:
         b = ctx.generate("spd", seed=synth.SEED, table=c)
         x, h, r = ctx.cg(b, tol=1e-10)
         assert r.converged and abs(r.iterations - 1070) <= 2
         xcf = oracle.spd_exact_solve_ld(c, synth.SEED, b)
         assert np.linalg.norm(x - xcf) <= 1e4 * 1e-10 * np.linalg.norm(xcf)
-    with ks.Context(n, ngpus=4) as ctx:
+    with ks.Context(n, ngpus=P) as ctx:
         b = ctx.generate("dd", seed=synth.SEED, kd=16)
         x, h, r = ctx.bicgstab(b, tol=1e-10)
     assert r.converged and r.iterations <= 30 and r.true_relres <= 10 * 1e-10
