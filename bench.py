@@ -15,7 +15,10 @@ on (torch's current stream, borrowed), max over ranks.
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 --impl reference times the CPU oracle (oracle/, the only baseline this paper
-has) on a bounded row sample of the same workload, on rank 0 only.
+has) on the same full workload -- K oracle iterations of each method after W
+warm-up iterations, all host cores, plus one single-thread step -- on rank 0 only.
+The matrices are stored on the host when RAM allows (2 x 34.4 GB at n = 65536),
+else generated row by row on the fly.
 """
 from __future__ import annotations
 
@@ -173,54 +176,81 @@ def clocks_bad(c):
 
 # ------------------------------------------------------------ CPU oracle
 
-def oracle_step_sample(n: int, rows: int, threads: int, budget_s: float, steps: int | None = None,
-                       warmup: int = 0):
-    """Times the CPU oracle on a bounded row sample of the bench workload: per
-    step the 3 GEMVs of one CG + one BiCGSTAB iteration (oracle or_gemv:
-    sequential FP64 row sums, rows spread over `threads` OpenMP threads -- bitwise
-    equal to 1 thread) on `rows` rows of each n-wide matrix, extrapolated x n/rows,
-    plus the O(n) vector work of both iterations (10 full-length dots/axpys)."""
+def host_info() -> dict:
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            names = [ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")]
+        info["cpu_model"] = names[0] if names else None
+    except OSError:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                k, v = ln.split(":", 1)
+                if k in ("MemTotal", "MemAvailable"):
+                    info[k] = int(v.split()[0]) * 1024
+    except OSError:
+        pass
+    return info
+
+
+def oracle_full_steps(n: int, steps: int, warmup: int, threads: int, one_thread: bool = True) -> dict:
+    """Times the CPU oracle AS IT STANDS on the full bench workload: the oracle's
+    own CG (or_cg) and BiCGSTAB (or_bicgstab) run `steps` iterations each (tol = 0,
+    fixed length) on G-SPD(n, 1e4) and G-DD(n, 16) -- a step is one CG + one
+    BiCGSTAB iteration, 3 full n x n GEMVs and all the vector work.  The matrices
+    are stored on the host (expanded by the oracle's generator on all cores) when
+    RAM allows, else the oracle generates every row on the fly.  `threads` = the
+    row-parallel OpenMP variant (each row sum stays sequential: bitwise the
+    1-thread oracle); with one_thread, one further step runs on a single thread
+    (PAPER.md:95's "serial version [that] uses one CPU")."""
     import oracle
     import synth
-    r0 = n // 2 - rows // 2
-    Aspd = oracle.gen_rows(synth.spec("spd", n, kappa=1e4, seed=SEED), r0, rows)
-    Add = oracle.gen_rows(synth.spec("dd", n, kd=16, seed=SEED), r0, rows)
-    x = synth.rhs(n, SEED)
-    y = np.empty(rows)
-    L = oracle.lib()
-    P = oracle._p
+    info = host_info()
+    need = 2 * 8.0 * n * n
+    stored = info.get("MemAvailable", 0) > 1.25 * need + 16e9
+    t_gen = time.perf_counter()
+    specs = {"cg": synth.spec("spd", n, kappa=1e4, seed=SEED), "bicgstab": synth.spec("dd", n, kd=16, seed=SEED)}
+    mats = {k: oracle.gen_rows(s, 0, n, threads=threads) if stored else None for k, s in specs.items()}
+    t_gen = time.perf_counter() - t_gen
 
-    def one():
-        t0 = time.perf_counter()
-        L.or_gemv(rows, n, P(Aspd), n, P(x), P(y), threads)   # CG:       q = A p
-        L.or_gemv(rows, n, P(Add), n, P(x), P(y), threads)    # BiCGSTAB: v = A p
-        L.or_gemv(rows, n, P(Add), n, P(x), P(y), threads)    # BiCGSTAB: t = A s
-        t1 = time.perf_counter()
-        z = x.copy()
-        for _ in range(5):
-            oracle.dot(x, z)
-            z = oracle.axpy(0.5, x, z)
-        return t1 - t0, time.perf_counter() - t1
+    def op(k, th):
+        return oracle.Operator(mats[k], threads=th) if stored else oracle.Operator(gen=specs[k], threads=th)
 
-    for _ in range(warmup):
-        one()
-    g, v = [], []
-    t_start = time.perf_counter()
-    while True:
-        a, b = one()
-        g.append(a)
-        v.append(b)
-        if steps is not None and len(g) >= steps:
-            break
-        if steps is None and time.perf_counter() - t_start >= budget_s:
-            break
-    full = statistics.mean(g) * (n / rows) + statistics.mean(v)
-    return {"value": 1.0 / full, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"rows [{r0},{r0 + rows}) of G-SPD(n={n},1e4) and G-DD(n={n},16): 3 oracle "
-                      f"GEMVs per step (sequential FP64 row sums, OpenMP over rows on {threads} "
-                      f"threads), extrapolated x{n / rows:.0f}, + 10 full-length oracle dot/axpy; "
-                      f"{len(g)} sampled steps",
-            "seconds_per_step": full, "sampled_steps": len(g)}
+    b = {"cg": synth.rhs(n, SEED), "bicgstab": synth.rhs(n, SEED)}
+    ops = {k: op(k, threads) for k in specs}
+    if warmup > 0:
+        oracle.cg(ops["cg"], b["cg"], tol=0.0, maxit=warmup)
+        oracle.bicgstab(ops["bicgstab"], b["bicgstab"], tol=0.0, maxit=warmup)
+    t0 = time.perf_counter()
+    _, _, r1 = oracle.cg(ops["cg"], b["cg"], tol=0.0, maxit=steps)
+    t1 = time.perf_counter()
+    _, _, r2 = oracle.bicgstab(ops["bicgstab"], b["bicgstab"], tol=0.0, maxit=steps)
+    t2 = time.perf_counter()
+    assert r1.iterations == steps and r2.iterations == steps, (r1, r2)
+    sec = (t2 - t0) / steps
+    out = {"value": 1.0 / sec, "unit": UNIT, "cores": threads, "kind": "oracle",
+           "sample": f"the full workload, not a sample: the oracle's own CG and BiCGSTAB, {steps} "
+                     f"iterations each (tol=0) on G-SPD(n={n},1e4) and G-DD(n={n},16), "
+                     f"{'host-stored rows' if stored else 'rows generated on the fly'}, "
+                     f"row-parallel on {threads} threads (sequential FP64 row sums); "
+                     f"{warmup} warm-up iterations per method untimed",
+           "seconds_per_step": sec, "timed_steps": steps,
+           "cg_iters_per_s": steps / (t1 - t0), "bicgstab_iters_per_s": steps / (t2 - t1),
+           "matrix": "stored" if stored else "on-the-fly", "generate_s": t_gen, "host": info}
+    if one_thread:
+        o1 = {k: op(k, 1) for k in specs}
+        s0 = time.perf_counter()
+        oracle.cg(o1["cg"], b["cg"], tol=0.0, maxit=1)
+        s1 = time.perf_counter()
+        oracle.bicgstab(o1["bicgstab"], b["bicgstab"], tol=0.0, maxit=1)
+        s2 = time.perf_counter()
+        out["one_thread"] = {"value": 1.0 / (s2 - s0), "unit": UNIT, "cores": 1,
+                             "seconds_per_step": s2 - s0, "cg_seconds_per_iter": s1 - s0,
+                             "bicgstab_seconds_per_iter": s2 - s1, "timed_steps": 1,
+                             "gemv_GBps": 3 * 8.0 * n * n / (s2 - s0) / 1e9}
+    return out
 
 
 def run_reference(args):
@@ -229,10 +259,10 @@ def run_reference(args):
         return 0
     threads = os.cpu_count() or 1
     n = args.n
-    rows = max(64, min(n, args.ref_rows))
     t0 = time.perf_counter()
-    cpu = oracle_step_sample(n, rows, threads, budget_s=0, steps=args.steps, warmup=args.warmup)
+    cpu = oracle_full_steps(n, args.steps, args.warmup, threads, one_thread=True)
     wall = time.perf_counter() - t0
+    cpu["fits_in_run"] = cpu["seconds_per_step"] * args.steps <= wall
     line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / cpu["value"], "higher_is_better": True, "scaling": "strong",
@@ -402,7 +432,7 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = oracle_step_sample(n, args.cpu_rows, os.cpu_count() or 1, budget_s=args.cpu_budget)
+            cpu = oracle_full_steps(n, args.cpu_steps, 1, os.cpu_count() or 1, one_thread=True)
         value = K / sec
         T_roof = lambda g: g * 8.0 * n * n / world / (NOMINAL_HBM * 1e9) + \
             g * 8.0 * n * (world - 1) / world / 0.9e12
@@ -459,9 +489,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--size", dest="n", type=int, default=65536)   # not "--n": torchrun would take it as an abbreviation of its own options
-    ap.add_argument("--cpu-rows", type=int, default=2048)
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--cpu-steps", type=int, default=3)      # cpu_baseline leg: full oracle steps
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--comm", choices=["fused", "nccl"], default="fused")
     ap.add_argument("--kernels", choices=["persistent", "multi"], default="persistent")
