@@ -23,7 +23,7 @@ def test_clock_rules():
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--size", "4096",
-                          "--steps", "3", "--warmup", "3", "--ref-rows", "256"], cwd=ROOT,
+                          "--steps", "3", "--warmup", "3"], cwd=ROOT,
                          capture_output=True, text=True, timeout=300, check=True).stdout
     line = json.loads(out.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
