@@ -126,7 +126,7 @@ typedef enum {
     KS_OPT_GEMVT_SHAPE = 11,  /* tuning: K1T 16-byte vectors per                  */
                               /* thread per row (1/2/4) * 100 + rows in flight    */
                               /* (4/8/16); default 204 (profiles/r01_gemvt_sweep) */
-    KS_OPT_SMALL = 12         /* persistent path: 1 = small-n kernels that keep   */
+    KS_OPT_SMALL = 12,        /* persistent path: 1 = small-n kernels that keep   */
                               /* the full vectors in every CTA's shared memory    */
                               /* (CG and BiCGSTAB on one GPU: 1 / 2 grid barriers */
                               /* per iteration; on P > 1 GPUs with the fused      */
@@ -135,6 +135,11 @@ typedef enum {
                               /* they fit; 0 = off; 2 (default) = auto (on        */
                               /* when a vector is <= 32 KiB: FP64 n <= 4096, FP32 */
                               /* n <= 8192; BiCGSTAB on P > 1: <= 16 KiB)         */
+    KS_OPT_JOIN_TIMEOUT_MS = 13 /* fused exchange (P > 1): every solve starts with  */
+                              /* an on-device rendezvous of all ranks (no host    */
+                              /* sync); a rank that does not arrive within this   */
+                              /* many ms (default 120000) fails the solve with    */
+                              /* KS_ENCCL.  In-loop waits stay bounded at 10 s.   */
 } ks_option;
 
 /* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL

@@ -30,7 +30,7 @@ STATUS_NAMES = {0: "OK", 1: "EARG", 2: "EDIM", 3: "ENOTSPD", 4: "EMAXIT", 5: "EB
 OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 3,
            "gemv_split": 4, "gemv_kernel": 5, "use_graphs": 6, "fused_comm": 7,
            "persistent": 8, "gemv_unroll": 9, "persist_grid": 10,
-           "gemvt_shape": 11, "small": 12}
+           "gemvt_shape": 11, "small": 12, "join_timeout_ms": 13}
 EXPORTS = ["ks_create", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
            "ks_generate", "ks_matvec", "ks_matvec_t", "ks_time_matvec", "ks_cg", "ks_bicgstab",
            "ks_bicg", "ks_gmres",
@@ -152,6 +152,26 @@ def _f64(a, n: int, name: str):
     return a
 
 
+def _out64(a, n: int | None, name: str):
+    """An OUTPUT buffer: written in place by the library, so it must already be a
+    contiguous 1-D float64 array / tensor (a converted copy would leave the
+    caller's buffer unwritten; a wrong dtype or stride would overflow it)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
+        import torch
+        if a.dtype != torch.float64 or a.dim() != 1 or not a.is_contiguous() or \
+                (n is not None and a.numel() != n):
+            raise ValueError(f"{name}: need a contiguous 1-D float64 tensor"
+                             + (f" of {n} elements" if n is not None else ""))
+        return a
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.ndim != 1 or \
+            not a.flags["C_CONTIGUOUS"] or not a.flags["WRITEABLE"] or (n is not None and a.shape[0] != n):
+        raise ValueError(f"{name}: need a writeable contiguous 1-D float64 array"
+                         + (f" of {n} elements" if n is not None else ""))
+    return a
+
+
 class Context:
     """Opaque solver context: A resident in HBM, row-block sharded."""
 
@@ -266,14 +286,14 @@ class Context:
     # -- compute ----------------------------------------------------------------
     def matvec(self, x, out=None):
         x = _f64(x, self.n, "x")
-        y = np.empty(self.n) if out is None else _f64(out, self.n, "out")
+        y = np.empty(self.n) if out is None else _out64(out, self.n, "out")
         self._check(lib().ks_matvec(self._h, _ptr(x), _ptr(y)))
         return y
 
     def matvec_t(self, x, out=None):
         """y = A^T x (the transposed GEMV of BiCG)."""
         x = _f64(x, self.n, "x")
-        y = np.empty(self.n) if out is None else _f64(out, self.n, "out")
+        y = np.empty(self.n) if out is None else _out64(out, self.n, "out")
         self._check(lib().ks_matvec_t(self._h, _ptr(x), _ptr(y)))
         return y
 
@@ -286,11 +306,13 @@ class Context:
         b = _f64(b, self.n, "b")
         x0 = _f64(x0, self.n, "x0")
         maxit = 10 * self.n if maxit is None else int(maxit)
-        x = np.empty(self.n) if out is None else _f64(out, self.n, "out")
+        x = np.empty(self.n) if out is None else _out64(out, self.n, "out")
         if hist is True:
             hist = np.zeros(max(1, min(maxit, hist_cap)))
         elif hist is False or hist is None:
             hist = None
+        else:
+            hist = _out64(hist, None, "hist")
         cap = 0 if hist is None else (hist.shape[0] if isinstance(hist, np.ndarray) else hist.numel())
         rep = _Report()
         st = fn(self._h, _ptr(b), _ptr(x0), float(tol), maxit, _ptr(x), _ptr(hist), cap,

@@ -24,6 +24,18 @@ ks_status fail(ks_ctx* c, ks_status code, const std::string& msg) {
     return code;
 }
 
+// Every local rank must hold all of its rows before a call that runs a collective
+// schedule: checked up front for ALL local ranks, so in single-process multi-GPU
+// mode an unloaded shard is an error on every rank rather than one rank throwing
+// while its peers wait in a fused exchange.  In multi-process mode
+// each process checks its own shard; a peer that stops here makes the others'
+// solve-start rendezvous fail with KS_ENCCL after its timeout, never hang.
+bool all_loaded(const ks_ctx* c) {
+    for (const Rank& r : c->ranks)
+        if (r.loaded_count < r.m) return false;
+    return true;
+}
+
 template <class F>
 ks_status guarded(ks_ctx* c, F&& f) {
     if (c && c->poisoned) return fail(c, KS_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
@@ -261,9 +273,9 @@ ks_status ks_generate(ks_ctx* c, const ks_gen_spec* spec, double* b_out) {
 
 ks_status ks_matvec(ks_ctx* c, const double* x, double* y) {
     if (!c || !x || !y) return fail(c, KS_EARG, "NULL argument");
+    if (!c->poisoned && !all_loaded(c)) return fail(c, KS_ESTATE, "matrix not fully loaded");
     return guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
-            if (r.loaded_count < r.m) throw KsError(KS_ESTATE, "matrix not fully loaded");
             if (c->dtype == KS_FLOAT32) {
                 double* tmp = nullptr;
                 ks::dev_alloc_t(&tmp, (size_t)c->n);
@@ -361,6 +373,8 @@ static ks_status solve(ks_ctx* c, int method, const double* b, const double* x0,
         if (x0) return fail(c, KS_EARG, "FP32 path: x0 must be NULL (zero start)");
         if (!(c->P == 1 || c->fused())) return fail(c, KS_EARG, "FP32 path needs P == 1 or peer access");
     }
+    if (c->poisoned) return fail(c, KS_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    if (!all_loaded(c)) return fail(c, KS_ESTATE, "matrix not fully loaded: call ks_load_rows / ks_generate first");
     std::vector<ks_report> reps(c->ranks.size());
     std::vector<int64_t> stat(c->ranks.size(), 0);
     ks_status st = guarded(c, [&] {
@@ -419,6 +433,8 @@ ks_status ks_gmres(ks_ctx* c, const double* b, const double* x0, double tol, int
     if (restart < 1 || restart >= ks::kMaxBasis) return fail(c, KS_EARG, "restart must be in [1, 63]");
     if (hist_cap < 0 || (hist_cap > 0 && !hist)) return fail(c, KS_EARG, "bad hist/hist_cap");
     if (!hist) hist_cap = 0;
+    if (c->poisoned) return fail(c, KS_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    if (!all_loaded(c)) return fail(c, KS_ESTATE, "matrix not fully loaded: call ks_load_rows / ks_generate first");
     std::vector<ks_report> reps(c->ranks.size());
     std::vector<int64_t> stat(c->ranks.size(), 0);
     ks_status st = guarded(c, [&] {
@@ -445,9 +461,9 @@ ks_status ks_gmres(ks_ctx* c, const double* b, const double* x0, double tol, int
 ks_status ks_matvec_t(ks_ctx* c, const double* x, double* y) {
     if (!c || !x || !y) return fail(c, KS_EARG, "NULL argument");
     if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "ks_matvec_t is FP64-only");
+    if (!c->poisoned && !all_loaded(c)) return fail(c, KS_ESTATE, "matrix not fully loaded");
     return guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
-            if (r.loaded_count < r.m) throw KsError(KS_ESTATE, "matrix not fully loaded");
             KS_CUDA(cudaMemcpyAsync(r.q_loc, x + r.row0, (size_t)r.m * sizeof(double), cudaMemcpyDefault,
                                     r.stream));
             const double* mine = ks::gemv_t(c, r, r.q_loc, nullptr);
@@ -506,6 +522,9 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
         case KS_OPT_SMALL:
             if (v < 0 || v > 2) return fail(c, KS_EARG, "small must be 0, 1 or 2");
             o.small = v; break;
+        case KS_OPT_JOIN_TIMEOUT_MS:
+            if (v < 1 || v > 3600000) return fail(c, KS_EARG, "join timeout must be in [1, 3600000] ms");
+            o.join_timeout_ms = v; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -536,6 +555,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_PERSIST_GRID: *v = o.persist_grid; break;
         case KS_OPT_GEMVT_SHAPE: *v = o.gemvt_shape; break;
         case KS_OPT_SMALL: *v = o.small; break;
+        case KS_OPT_JOIN_TIMEOUT_MS: *v = o.join_timeout_ms; break;
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

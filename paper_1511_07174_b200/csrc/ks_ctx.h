@@ -126,6 +126,7 @@ struct Options {
     int64_t persist_grid = 0; // tuning: persistent CTAs (0 = auto)
     int64_t gemvt_shape = 204; // tuning: K1T vectors/thread/row * 100 + rows in flight
     int64_t small = 2;        // 0 off, 1 on, 2 auto: small-n shared-memory kernels (P == 1)
+    int64_t join_timeout_ms = 120000;   // fused P > 1: solve-start rendezvous bound
 };
 
 }  // namespace ks

@@ -21,7 +21,8 @@ constexpr int kNumTickets = 64;
 constexpr int kPhaseS = 0;   // scalar partials  (CG sigma; BiCGSTAB <t,s>, <t,t>)
 constexpr int kPhaseR = 1;   // r slice + <rhat,r>, <r,r> / rho' partials
 constexpr int kPhaseV = 2;   // BiCGSTAB v slice + <rhat,v>
-constexpr int kNumPhases = 3;
+constexpr int kPhaseJ = 3;   // solve-start rendezvous (epoch = the solve's ebase)
+constexpr int kNumPhases = 4;
 
 // Peer (NVLink, unified-address) pointers to every rank's exchange buffers,
 // parity-0 bases; rank g's own entries point at its local memory.
@@ -178,6 +179,14 @@ int launch_bs_xr(const VecArgs& a, const long long* kdev, long long i, cudaStrea
 int launch_bs_finish(const VecArgs& a, cudaStream_t st);
 int launch_true_res_final(const VecArgs& a, cudaStream_t st);
 int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chunk
+// Solve-start rendezvous of the fused exchange (P > 1): releases `epoch` into
+// flag [kPhaseJ][rank] of every rank and waits (bounded by timeout_ms) until every
+// rank has released it -- i.e. every rank's stream has finished its previous solve
+// and initialised this one.  Host-side skew between ranks is absorbed here, so the
+// in-loop waits' timeout only bounds in-kernel skew.  A timeout marks the solve
+// failed (KS_ENCCL).  Launched after the init kernel, before the iteration loop.
+template <class T>
+int launch_join(const VecArgsT<T>& a, unsigned long long epoch, long long timeout_ms, cudaStream_t st);
 // Iteration kernels use k = koff + (kdev ? *kdev : 0): a captured batch of
 // iterations (CUDA graph) is replayed with *kdev advanced by k_advance.
 int launch_advance(long long* kdev, long long by, cudaStream_t st);

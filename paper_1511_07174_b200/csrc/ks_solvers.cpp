@@ -323,6 +323,7 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
     r.launches += launch_cg_init(a, tol, maxit, hist_cap, ebase, r.stream);
+    if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
     double* sig = r.S + (int64_t)r.rank * kScalSlot;
     GemvParams pq = gp(c, r, r.p_full, r.q_loc);
     pq.w1 = r.p_full + r.row0;                 // sigma_g = <p_loc, q_loc>
@@ -359,6 +360,7 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
     r.launches += launch_bs_init(a, tol, maxit, hist_cap, ebase, r.stream);
+    if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
     double* vown = r.G_v + (int64_t)r.rank * r.L.chunk;
     GemvParams pv = gp(c, r, r.p_full, vown);  // B3: v = A p, <rhat, v>_g
     pv.w1 = r.rhat_loc;
@@ -424,6 +426,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
     r.launches += launch_init_f32(a, bicgstab, tol, maxit, hist_cap, ebase, r.stream);
+    if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
     const int64_t B = poll_batch(c, true, maxit);
     const int gemvs = bicgstab ? 2 : 1;
     Prof prof(c, r, 1);
@@ -588,6 +591,7 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
         gf.a = r.vargs(c->fused());
         const unsigned long long ebase = r.epoch_next;
         r.epoch_next += gm_epochs(maxit, restart);
+        if (c->fused()) r.launches += launch_join(gf.a, ebase, c->opt.join_timeout_ms, r.stream);
         for (cycle = 0; cycle < max_cycles; ++cycle) {
             const int slot = (int)(cycle & 1);
             prof.begin(slot);
@@ -685,6 +689,7 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
     r.launches += launch_bicg_init(a, tol, maxit, hist_cap, ebase, r.stream);
+    if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
     GemvParams pq = gp(c, r, r.p_full, r.q_loc);   // q = A p, sigma_g = <pt_loc, q>
     pq.w1 = r.pt_loc;
     pq.out1 = r.S + (int64_t)r.rank * kScalSlot;

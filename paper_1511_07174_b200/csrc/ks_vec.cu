@@ -537,7 +537,34 @@ unsigned grid_for(int64_t len, int num_sms) {
 
 int64_t mloc_h(const Layout& L) { return L.row0[L.rank + 1] - L.row0[L.rank]; }
 
+template <class T>
+__global__ void k_join(VecArgsT<T> a, unsigned long long epoch, unsigned long long timeout_ns) {
+    if (threadIdx.x != 0) return;
+    unsigned long long* f[kMaxRanks];
+    for (int g = 0; g < a.L.P; ++g) f[g] = a.pp.flags[g] + kPhaseJ * kMaxRanks + a.L.rank;
+    publish_flags(f, a.L.P, epoch);
+    const unsigned long long t0 = globaltimer_ns();
+    for (int g = 0; g < a.L.P; ++g) {
+        while (flag_acquire_sys(a.flags + kPhaseJ * kMaxRanks + g) < epoch) {
+            if (globaltimer_ns() - t0 > timeout_ns) {
+                a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1;
+                return;
+            }
+            __nanosleep(64);
+        }
+    }
+}
+
 }  // namespace
+
+template <class T>
+int launch_join(const VecArgsT<T>& a, unsigned long long epoch, long long timeout_ms, cudaStream_t st) {
+    const unsigned long long ns = (unsigned long long)(timeout_ms > 0 ? timeout_ms : 1) * 1000000ULL;
+    k_join<T><<<1, 32, 0, st>>>(a, epoch, ns);
+    return 1;
+}
+template int launch_join<double>(const VecArgsT<double>&, unsigned long long, long long, cudaStream_t);
+template int launch_join<float>(const VecArgsT<float>&, unsigned long long, long long, cudaStream_t);
 
 int launch_setup_local(const VecArgs& a, cudaStream_t st) {
     k_setup_local<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a);

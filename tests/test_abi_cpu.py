@@ -83,3 +83,23 @@ def test_c_example_links_against_the_abi():
     from paper_1511_07174_b200 import _build
     exe = _build.build_example()
     assert os.path.exists(exe)
+
+
+def test_output_buffers_are_validated_not_copied():
+    """out= and hist= are written in place by the library: a wrong dtype, a strided
+    view or a read-only array is rejected instead of silently copied (the caller's
+    buffer would never be written) or overflowed."""
+    import pytest
+    from paper_1511_07174_b200 import _out64
+    ok = np.zeros(8)
+    assert _out64(ok, 8, "x") is ok
+    assert _out64(np.zeros(5), None, "hist").shape == (5,)
+    bad = [np.zeros(8, np.float32), np.zeros(16)[::2], np.zeros((2, 4)), np.zeros(7), [0.0] * 8]
+    ro = np.zeros(8)
+    ro.flags.writeable = False
+    bad.append(ro)
+    for b in bad:
+        with pytest.raises(ValueError):
+            _out64(b, 8, "out")
+    with pytest.raises(ValueError):
+        _out64(np.zeros(4, np.float32), None, "hist")

@@ -312,6 +312,58 @@ def test_multi_edge_cases():
 
 
 @needs2
+def test_partial_load_is_an_error_on_every_rank():
+    """Single process driving 2 GPUs with only the first shard loaded: every call
+    that runs a collective schedule returns KS_ESTATE up front (no rank enters a
+    fused exchange its peer never joins), and the context stays usable."""
+    n = 512
+    A = synth.random_spd(n, 10.0, 3)
+    b = np.random.default_rng(3).standard_normal(n)
+    with ks.Context(n, ngpus=2) as ctx:
+        r0, r1 = ctx.row_range(0)
+        ctx.load_rows(A[r0:r1], r0)
+        for call in (lambda: ctx.cg(b), lambda: ctx.bicgstab(b), lambda: ctx.bicg(b),
+                     lambda: ctx.gmres(b), lambda: ctx.matvec(b), lambda: ctx.matvec_t(b)):
+            with pytest.raises(ks.KsError) as e:
+                call()
+            assert e.value.status == ks.KS_ESTATE
+        ctx.load_rows(A[r1:], r1)
+        xo, ho, ro = oracle.cg(A, b, tol=1e-10)
+        x, h, r = ctx.cg(b, tol=1e-10)
+        bars(x, h, r, xo, ho, ro)
+
+
+def _skew_run(tmp_path, delay, tmo, port):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(ROOT, "tools", "dist_skew.py"), "1024", str(delay), str(tmo), str(tmp_path)]
+    subprocess.run(cmd, check=True, timeout=300, cwd=ROOT)
+    return [json.load(open(tmp_path / f"skew_r{g}.json")) for g in range(2)]
+
+
+@needs2
+def test_solve_start_rendezvous_absorbs_host_skew(tmp_path):
+    """One process per GPU, the last rank calls every solve 12 s after its peer --
+    beyond the 10 s bound of the in-loop waits.  The on-device rendezvous at solve
+    start (k_join, default bound 120 s) absorbs it: both ranks converge with
+    identical results."""
+    res = _skew_run(tmp_path, 12.0, 120000, 29561)
+    for name in ("cg", "bicgstab"):
+        assert res[0][name]["status"] == ks.KS_OK and res[1][name]["status"] == ks.KS_OK, res
+        assert res[0][name] == res[1][name]
+
+
+@needs2
+def test_solve_start_rendezvous_times_out_without_hanging(tmp_path):
+    """Join bound 2 s, peer 6 s late: the early rank fails with KS_ENCCL and the late
+    rank (which finds the early rank's join flag, then waits in the loop for
+    exchanges that never come) fails too -- an error on both, never a hang."""
+    res = _skew_run(tmp_path, 6.0, 2000, 29563)
+    assert res[0]["cg"]["status"] == ks.KS_ENCCL, res
+    assert res[1]["cg"]["status"] == ks.KS_ENCCL, res
+
+
+@needs2
 @pytest.mark.parametrize("P", PS)
 def test_torchrun_borrowed_comm(tmp_path, P):
     """One process per GPU (torchrun, nccl); every rank returns the same x and
