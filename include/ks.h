@@ -142,13 +142,22 @@ typedef enum {
                               /* KS_ENCCL.  In-loop waits stay bounded at 10 s.   */
 } ks_option;
 
-/* One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL
+/* Creates the opaque object that encapsulates the distributed matrix and its
+ * communication ("encapsulation of data and distribution and communication in
+ * opaque objects"; the data distribution level of Fig. 2,
+ * PAPER.md:64-76; Step 3 "Allocate memory ... in the device memory",
+ * PAPER.md:83).  Row blocks instead of the paper's bidimensional mesh
+ * (Q24).
+ * One process drives GPUs 0..ngpus-1 (one worker thread and stream per GPU, NCCL
  * communicator from ncclCommInitAll when ngpus > 1).  n >= 1, 1 <= ngpus <= 16
  * and <= device count, dtype = KS_FLOAT64 or KS_FLOAT32.  Allocates each shard (m_g x ld)
  * plus O(n) vectors with cudaMalloc and zero-fills them.                        */
 ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
 
-/* One rank of a multi-process job (one process per GPU, e.g. torchrun).
+/* One rank of a multi-process job (one process per GPU, e.g. torchrun) -- the
+ * paper's one-MPI-process-per-node model ("MPI ... for the
+ * communication between processors"), NCCL over NVLink in place of
+ * MPI over Ethernet.
  * nccl_comm: a BORROWED ncclComm_t of nranks ranks (e.g. torch's
  * ProcessGroupNCCL._comm_ptr()), or NULL when nranks == 1.  stream: a BORROWED
  * cudaStream_t on `device` (NULL -> the context creates its own).  Both must
@@ -156,27 +165,41 @@ ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
 ks_status ks_create_rank(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t rank, int32_t nranks,
                          void* nccl_comm, int32_t device, void* stream);
 
-/* Frees every device allocation of the context (never the borrowed comm/stream). */
+/* Frees every device allocation of the context (never the borrowed comm/stream):
+ * Step 8 "Memory clean up".  Always allowed, also on a poisoned
+ * context; ctx == NULL is a no-op returning KS_OK.                              */
 ks_status ks_destroy(ks_ctx* ctx);
 
-/* Row range [*row_begin, *row_end) of shard `shard` (0 <= shard < P). */
+/* Row range [*row_begin, *row_end) of shard `shard` (0 <= shard < P): the
+ * distribution of the matrix over the processors ("distribution of
+ * vectors and matrices on processors"; 1-D row blocks, Q15/Q24).
+ * shard outside [0, P) -> KS_EARG.                                               */
 ks_status ks_row_range(const ks_ctx* ctx, int32_t shard, int64_t* row_begin, int64_t* row_end);
 
-/* Copies rows [row_begin, row_begin + nrows) of A (row-major, leading dimension
+/* Step 4 "Copy matrices from host memory to device memory" for a
+ * distributed matrix.
+ * Copies rows [row_begin, row_begin + nrows) of A (row-major, leading dimension
  * lda >= n; row r of the argument is global row row_begin + r) into the shards
  * that own them; rows owned by other ranks of a multi-process job are ignored.
  * Rows may be loaded in any chunks; a reloaded row is overwritten.               */
 ks_status ks_load_rows(ks_ctx* ctx, int64_t row_begin, int64_t nrows, const double* A, int64_t lda);
 
-/* Expands the generator spec on the device into every shard (K0), and writes b
- * (n doubles, generated on the device) to b_out if non-NULL.                    */
+/* Step 2 "Initialize matrices and vectors" done on the device: the
+ * paper's workload is only "60000 rows and columns", so the
+ * synthetic inputs of SURVEY.md sec.8(d).2 are expanded into every shard (K0),
+ * bitwise equal to the oracle's expansion.  b (n doubles, generated on the
+ * device) goes to b_out if non-NULL.  Bad kind / kd < 1 / missing table ->
+ * KS_EARG; marks every row loaded.                                              */
 ks_status ks_generate(ks_ctx* ctx, const ks_gen_spec* spec, double* b_out);
 
 /* y = A x (n doubles each).  The plain GEMV building block.        */
 ks_status ks_matvec(ks_ctx* ctx, const double* x, double* y);
 
-/* Times `reps` back-to-back K1 GEMV launches on device-resident data with CUDA
- * events; *seconds_per_matvec = elapsed/reps (max over this context's GPUs).    */
+/* Measurement of the O(n^2) matrix-vector product that dominates a Krylov
+ * iteration (SURVEY.md sec.8(d).5 "GEMV metric").
+ * Times `reps` back-to-back K1 GEMV launches on device-resident data with CUDA
+ * events; *seconds_per_matvec = elapsed/reps (max over this context's GPUs).
+ * reps < 1 -> KS_EARG.  No host data is read or written.                        */
 ks_status ks_time_matvec(ks_ctx* ctx, int32_t reps, double* seconds_per_matvec);
 
 /* CG.  b: n doubles (required).  x0: n doubles or NULL
@@ -221,7 +244,8 @@ ks_status ks_matvec_t(ks_ctx* ctx, const double* x, double* y);
 ks_status ks_set_option(ks_ctx* ctx, ks_option opt, int64_t value);
 ks_status ks_get_option(const ks_ctx* ctx, ks_option opt, int64_t* value);
 
-/* Number of GPUs (shards) this context drives locally, and the global P.        */
+/* Number of GPUs (shards) this context drives locally, and the global P, n and
+ * the padded device row length ld (the distribution).              */
 ks_status ks_info(const ks_ctx* ctx, int32_t* local_gpus, int32_t* nranks, int64_t* n, int64_t* ld);
 
 /* Guard-zone check (a test facility: compute-sanitizer is not available on the
