@@ -135,11 +135,16 @@ typedef enum {
                               /* they fit; 0 = off; 2 (default) = auto (on        */
                               /* when a vector is <= 32 KiB: FP64 n <= 4096, FP32 */
                               /* n <= 8192; BiCGSTAB on P > 1: <= 16 KiB)         */
-    KS_OPT_JOIN_TIMEOUT_MS = 13 /* fused exchange (P > 1): every solve starts with  */
+    KS_OPT_JOIN_TIMEOUT_MS = 13, /* fused exchange (P > 1): every solve starts with  */
                               /* an on-device rendezvous of all ranks (no host    */
                               /* sync); a rank that does not arrive within this   */
                               /* many ms (default 120000) fails the solve with    */
                               /* KS_ENCCL.  In-loop waits stay bounded at 10 s.   */
+    KS_OPT_TINY = 14          /* 1 (default): one GPU, FP64, n <= 1024, whole     */
+                              /* solve in one launch -> the register-resident     */
+                              /* kernels (A in shared memory, vectors replicated  */
+                              /* in registers, LL-format exchange of the GEMV     */
+                              /* output: no grid barrier); 0 = off                */
 } ks_option;
 
 /* Creates the opaque object that encapsulates the distributed matrix and its

@@ -525,6 +525,9 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
         case KS_OPT_JOIN_TIMEOUT_MS:
             if (v < 1 || v > 3600000) return fail(c, KS_EARG, "join timeout must be in [1, 3600000] ms");
             o.join_timeout_ms = v; break;
+        case KS_OPT_TINY:
+            if (v < 0 || v > 1) return fail(c, KS_EARG, "tiny must be 0 or 1");
+            o.tiny = v; break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -556,6 +559,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_GEMVT_SHAPE: *v = o.gemvt_shape; break;
         case KS_OPT_SMALL: *v = o.small; break;
         case KS_OPT_JOIN_TIMEOUT_MS: *v = o.join_timeout_ms; break;
+        case KS_OPT_TINY: *v = o.tiny; break;
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

@@ -82,6 +82,7 @@ struct Rank {
     int64_t hist_alloc = 0;
     Scratch scr{};
     double* table_tmp = nullptr;
+    uint64_t* ll = nullptr;     // LL exchange slots of the tiny kernels (4 * ld words, lazily)
 
     // host
     int* h_done = nullptr;      // pinned, 2 slots
@@ -127,6 +128,7 @@ struct Options {
     int64_t gemvt_shape = 204; // tuning: K1T vectors/thread/row * 100 + rows in flight
     int64_t small = 2;        // 0 off, 1 on, 2 auto: small-n shared-memory kernels (P == 1)
     int64_t join_timeout_ms = 120000;   // fused P > 1: solve-start rendezvous bound
+    int64_t tiny = 1;         // 1 auto, 0 off: register-resident kernels (P == 1, n <= 1024)
 };
 
 }  // namespace ks

@@ -256,6 +256,15 @@ template <class T>
 int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
                  unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st);
 
+// Tiny kernels (ks_tiny.cu, NEXT-2): one GPU, FP64, n <= 1024: A resident in shared
+// memory, full vectors replicated in registers, GEMV outputs exchanged through an
+// LL-format global buffer (ll: 4 * ld uint64 words, zeroed once).  The whole solve
+// in one launch (they always finish the solve).  tiny_grid returns 0 when not
+// applicable.
+int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld);
+int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll, int grid,
+                cudaStream_t st);
+
 // NEXT-4 (FP32) support kernels (ks_f32.cu): K1 in FP32, setup/init/finish in
 // FP32, conversions at the FP64 ABI boundary, FP32 generators.
 int launch_gemv_f32(const GemvParamsT<float>& p, const Scratch& s, int ticket_id, cudaStream_t st);

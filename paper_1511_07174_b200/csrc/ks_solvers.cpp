@@ -103,10 +103,17 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     const bool persist = c->persistent();
     const int64_t B = poll_batch(c, persist, maxit);
     Prof prof(c, r, persist ? 1 : B * gemvs_per_iter);
-    int pgrid = 0, sgrid = 0;
+    int pgrid = 0, sgrid = 0, tgrid = 0;
     int prows = 0, punroll = 0;
-    if (persist) sgrid = small_path_grid<double>(c, r, kind);
-    if (persist && sgrid == 0) {
+    // tiny kernels: one GPU, the whole solve in one launch (they always finish it)
+    if (persist && c->P == 1 && c->opt.tiny && c->opt.small != 0 && B >= maxit)
+        tgrid = tiny_grid(kind, r.num_sms, c->n, c->ld);
+    if (tgrid > 0 && !r.ll) {
+        dev_alloc_t(&r.ll, (size_t)(4 * c->ld));
+        KS_CUDA(cudaMemsetAsync(r.ll, 0, (size_t)(4 * c->ld) * sizeof(uint64_t), r.stream));
+    }
+    if (persist && tgrid == 0) sgrid = small_path_grid<double>(c, r, kind);
+    if (persist && tgrid == 0 && sgrid == 0) {
         persist_shape(c, r, &prows, &punroll);
         pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, prows, punroll);
         if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
@@ -144,7 +151,9 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
         if (persist) {                                    // one cooperative launch per batch
             const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
             prof.pre(slot);
-            const int rc = sgrid > 0
+            const int rc = tgrid > 0
+                ? launch_tiny(kind, r.vargs(false), r.A, c->ld, r.ll, tgrid, r.stream)
+                : sgrid > 0
                 ? launch_small<double>(small_kind(c, kind), r.vargs(c->fused()), r.A, c->ld, c->ld,
                                        r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, sgrid, r.stream)
                 : launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,

@@ -1,0 +1,437 @@
+// NEXT-2, third stage: the register-resident whole-solve
+// kernels for C1-sized systems (one GPU, FP64, n <= 1024 -- the matrix fits in
+// the shared memory of the SMs, 8 MiB at n = 1024).
+//
+// Where the small-n kernels (ks_small.cu) re-read A from L2 every GEMV and pay a
+// global arrival counter (one atomic per CTA, a fence, a spin) per reduction,
+// here:
+//   * each CTA owns a contiguous block of <= kRM rows of A and keeps it in its
+//     shared memory for the whole solve (loaded once per launch with
+//     cp.async.bulk, one bulk copy per row);
+//   * every CTA holds the full-length vectors x, r, p (BiCGSTAB: also rhat, v, s)
+//     REPLICATED in registers, in one fixed column-ownership layout (thread t
+//     owns columns 2t + 512u + {0, 1}); every O(n) step of the recurrence and every
+//     full-length dot runs redundantly in every CTA in one fixed order, so all
+//     CTAs hold bitwise-identical vectors and take identical decisions;
+//   * the only grid-wide step is the exchange of the GEMV output (q = A p; v and
+//     t for BiCGSTAB): each CTA stores its rows into a global slot in the LL
+//     ("low-latency") format -- every 8-byte word carries 32 bits of the value
+//     and a 32-bit epoch, written with single-copy-atomic 8-byte stores -- and
+//     every thread polls exactly the words it needs until both halves carry the
+//     exchange's epoch.  No fence, no atomic, no barrier: one store propagation
+//     plus one L2 round trip per exchange.
+// Epochs: exchange "which" (CG 0; BiCGSTAB 0 = v, 1 = t) of iteration k carries
+// 2 (ebase + k) + which; the solves of a context advance ebase by maxit + 2, so
+// the epochs of one LL buffer only ever grow and a stale word never matches.
+// Slots are double-buffered (CG: parity of k; BiCGSTAB: slot 0 = v, slot 1 = t):
+// a CTA overwrites a slot only after it has read every CTA's previous use of the
+// other slot, which every CTA wrote only after reading this one.
+//
+// Same recurrences as every other path (SURVEY.md sec.8(c).3 / .4, rows A1-A5,
+// B1-B8); the kernels make every decision in-kernel (including the test of the
+// last BiCGSTAB step) and always leave st->done = 1, so they are used only when
+// one launch runs the whole solve (the default poll batch).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ks_device.cuh"
+#include "ks_common.cuh"
+#include "ks_internal.h"
+#include "ks_tma.cuh"
+
+namespace ks {
+
+namespace {
+
+constexpr int kTT = 256;            // threads per CTA
+constexpr int kTW = kTT / 32;
+constexpr int kRM = 8;              // max rows of A per CTA (shared memory: kRM * ld * 8 B)
+
+__device__ __forceinline__ void ll_store(uint64_t* slot, double v, uint32_t flag) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(v);
+    const uint64_t lo = (bits & 0xffffffffull) | ((uint64_t)flag << 32);
+    const uint64_t hi = (bits >> 32) | ((uint64_t)flag << 32);
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(lo), "l"(hi) : "memory");
+}
+__device__ __forceinline__ void ll_load(const uint64_t* slot, uint64_t& lo, uint64_t& hi) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
+}
+__device__ __forceinline__ double ll_value(uint64_t lo, uint64_t hi) {
+    return __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
+}
+
+// Reads the V values of this thread's columns (2t + 512u + {0, 1}) from an LL slot,
+// spinning until every word carries `flag`.  Columns >= n read as 0.  Bounded:
+// returns false after kWaitTimeoutNs (a bug, never a peer: all CTAs are resident).
+template <int V>
+__device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t flag, double (&out)[V]) {
+    bool have[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int j = 2 * threadIdx.x + 512 * (v >> 1) + (v & 1);
+        have[v] = j >= n;
+        out[v] = 0.0;
+    }
+    unsigned long long t0 = 0;
+    for (int spin = 0;; ++spin) {
+        bool all = true;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (have[v]) continue;
+            const int j = 2 * threadIdx.x + 512 * (v >> 1) + (v & 1);
+            uint64_t lo, hi;
+            ll_load(slot + 2 * (int64_t)j, lo, hi);
+            if ((uint32_t)(lo >> 32) == flag && (uint32_t)(hi >> 32) == flag) {
+                out[v] = ll_value(lo, hi);
+                have[v] = true;
+            } else {
+                all = false;
+            }
+        }
+        if (all) return true;
+        if ((spin & 255) == 255) {
+            if (t0 == 0) t0 = globaltimer_ns();
+            else if (globaltimer_ns() - t0 > kWaitTimeoutNs) return false;
+        }
+    }
+}
+
+// Block sum of K values (fixed tree; every thread gets the same bits).
+template <int K>
+__device__ __forceinline__ void tsum(double (&v)[K], double* red) { block_sum<kTT, K>(v, red); }
+
+// GEMV rows [0, R) of this CTA's shared-memory block against the register-resident
+// full-length x (this thread's V columns); thread t < R returns row t's sum.
+// Per-thread row partials -> warp butterfly -> warp sums in warp order.
+template <int V>
+__device__ __forceinline__ double gemv_rows(const double* As, int64_t ld, int R, const double (&x)[V],
+                                            double* wred) {
+    double acc[kRM];
+#pragma unroll
+    for (int i = 0; i < kRM; ++i) {
+        acc[i] = 0.0;
+        if (i < R) {
+            const double* row = As + (int64_t)i * ld + 2 * threadIdx.x;
+#pragma unroll
+            for (int u = 0; u < V / 2; ++u) {
+                const double2 a = *reinterpret_cast<const double2*>(row + 512 * u);
+                acc[i] = fma(a.x, x[2 * u], acc[i]);
+                acc[i] = fma(a.y, x[2 * u + 1], acc[i]);
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < kRM; ++i) {
+        if (i < R) {
+            const double s = warp_sum(acc[i]);
+            if (lane == 0) wred[i * kTW + w] = s;
+        }
+    }
+    __syncthreads();
+    double q = 0.0;
+    if (threadIdx.x < R) {
+#pragma unroll
+        for (int ww = 0; ww < kTW; ++ww) q += wred[threadIdx.x * kTW + ww];
+    }
+    return q;
+}
+
+struct TinyArgs {
+    VecArgs a;
+    const double* A;
+    int64_t lda;
+    uint64_t* ll;        // 2 slots x ld entries x 2 words (LL format)
+};
+
+// This CTA's rows [rb, rb + R): balanced contiguous blocks.
+__device__ __forceinline__ void my_rows(int n, int& rb, int& R) {
+    const int q = n / (int)gridDim.x, rem = n % (int)gridDim.x, b = (int)blockIdx.x;
+    rb = b * q + min(b, rem);
+    R = q + (b < rem ? 1 : 0);
+}
+
+// Loads rows [rb, rb + R) of A into shared memory: one bulk copy per row.
+__device__ __forceinline__ void load_rows_smem(const double* A, int64_t lda, int rb, int R, double* As,
+                                               uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)(lda * sizeof(double));
+        mbar_expect_tx(bar, bytes * (uint32_t)R);
+        const uint64_t pol = policy_evict_first();
+        for (int i = 0; i < R; ++i) bulk_g2s(As + (int64_t)i * lda, A + (int64_t)(rb + i) * lda, bytes, bar, pol);
+    }
+    mbar_wait(bar, 0);
+}
+
+__device__ __forceinline__ int col_of(int v) { return 2 * threadIdx.x + 512 * (v >> 1) + (v & 1); }
+
+// ------------------------------------------------------------------ CG (A1-A5)
+template <int V>
+__global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw);
+    __shared__ double wred[kRM * kTW];
+    __shared__ double red[kTW];
+    __shared__ __align__(8) uint64_t bar;
+    const VecArgs& a = T.a;
+    DevState* st = a.st;
+    const int n = (int)a.L.n;
+    if (is_done(st)) return;
+    int rb, R;
+    my_rows(n, rb, R);
+    load_rows_smem(T.A, T.lda, rb, R, As, &bar);
+    double x[V], r[V], p[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int j = col_of(v);
+        const bool in = j < n;
+        x[v] = in ? a.x_loc[j] : 0.0;
+        r[v] = in ? a.G_r[j] : 0.0;           // r0 (P = 1: chunk 0 = the full vector)
+        p[v] = in ? a.p_full[j] : 0.0;        // p0 = r0
+    }
+    double rho = st->rho[0];
+    const double nb = st->nb, tol = st->tol;
+    const long long maxit = st->maxit;
+    const unsigned long long eb = st->ebase;
+    const bool lead0 = blockIdx.x == 0;
+    long long k = 1;
+    int status = KS_EMAXIT, conv = 0;
+    long long iters = maxit;
+    for (; k <= maxit; ++k) {
+        // A1: q rows = A p; LL exchange (the grid-wide step)
+        const double qrow = gemv_rows<V>(As, T.lda, R, p, wred);
+        const uint32_t flag = (uint32_t)(2ull * (eb + (unsigned long long)k));
+        uint64_t* slot = T.ll + (int64_t)(k & 1) * 2 * T.lda;
+        if (threadIdx.x < R) ll_store(slot + 2 * (int64_t)(rb + threadIdx.x), qrow, flag);
+        double q[V];
+        if (!ll_gather<V>(slot, n, flag, q)) {
+            if (lead0 && threadIdx.x == 0) { st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1; }
+            return;
+        }
+        // A2: sigma = <p, q> (full length, every CTA)
+        double s1[1] = {0.0};
+#pragma unroll
+        for (int v = 0; v < V; ++v) s1[0] = fma(p[v], q[v], s1[0]);
+        tsum<1>(s1, red);
+        const double sigma = s1[0];
+        if (!(sigma > 0.0)) { status = KS_ENOTSPD; iters = k - 1; break; }   // Q9: x unchanged
+        const double alpha = rho / sigma;
+        // A3: x += alpha p; r -= alpha q; rho' = <r, r>
+        double s2[1] = {0.0};
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            x[v] = fma(alpha, p[v], x[v]);
+            r[v] = fma(-alpha, q[v], r[v]);
+            s2[0] = fma(r[v], r[v], s2[0]);
+        }
+        tsum<1>(s2, red);
+        const double rho1 = s2[0];
+        const double rel = sqrt(rho1) / nb;
+        if (lead0 && threadIdx.x == 0) {
+            put_hist(st, a.hist, k - 1, rel);
+            st->relres = rel;
+        }
+        if (rel <= tol) { status = KS_OK; conv = 1; iters = k; break; }
+        // A5: p = r + beta p
+        const double beta = rho1 / rho;
+#pragma unroll
+        for (int v = 0; v < V; ++v) p[v] = fma(beta, p[v], r[v]);
+        rho = rho1;
+    }
+    if (lead0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int j = col_of(v);
+            if (j < n) { a.x_loc[j] = x[v]; a.p_full[j] = p[v]; a.G_r[j] = r[v]; }
+        }
+        if (threadIdx.x == 0) {
+            st->iters = iters; st->status = status; st->converged = conv;
+            st->rho[iters & 3] = rho;
+            st->done = 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------- BiCGSTAB (B1-B8)
+template <int V>
+__global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw);
+    __shared__ double wred[kRM * kTW];
+    __shared__ double red[2 * kTW];
+    __shared__ __align__(8) uint64_t bar;
+    const VecArgs& a = T.a;
+    DevState* st = a.st;
+    const int n = (int)a.L.n;
+    if (is_done(st)) return;
+    int rb, R;
+    my_rows(n, rb, R);
+    load_rows_smem(T.A, T.lda, rb, R, As, &bar);
+    double x[V], r[V], p[V], v_[V], rh[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int j = col_of(v);
+        const bool in = j < n;
+        x[v] = in ? a.x_loc[j] : 0.0;
+        r[v] = in ? a.G_r[j] : 0.0;           // r0
+        rh[v] = in ? a.rhat_loc[j] : 0.0;     // rhat = r0 (Q7)
+        p[v] = 0.0;                           // v = p = 0 (Q8)
+        v_[v] = 0.0;
+    }
+    const double nb = st->nb, tol = st->tol;
+    const long long maxit = st->maxit;
+    const unsigned long long eb = st->ebase;
+    const bool lead0 = blockIdx.x == 0;
+    double rho = slot_sum(a.L, a.G_r, 0);     // rho_1 = <rhat, r0>
+    double rho_old = 1.0, alpha = 1.0, omega = 1.0;
+    int status = KS_EMAXIT, conv = 0, brk = 0, half = 0;
+    long long iters = maxit;
+    for (long long i = 1; i <= maxit; ++i) {
+        if (rho == 0.0 || !isfinite(rho)) { status = KS_EBREAKDOWN; brk = 1; iters = i - 1; break; }
+        // B1: p = r + beta (p - omega v)   (i = 1: p = r exactly)
+        const double beta = (rho / rho_old) * (alpha / omega);
+#pragma unroll
+        for (int v = 0; v < V; ++v) p[v] = i == 1 ? r[v] : fma(beta, fma(-omega, v_[v], p[v]), r[v]);
+        // B2/B3: v = A p, exchange (slot 0)
+        const uint32_t fv = (uint32_t)(2ull * (eb + (unsigned long long)i));
+        double vrow = gemv_rows<V>(As, T.lda, R, p, wred);
+        if (threadIdx.x < R) ll_store(T.ll + 2 * (int64_t)(rb + threadIdx.x), vrow, fv);
+        if (!ll_gather<V>(T.ll, n, fv, v_)) {
+            if (lead0 && threadIdx.x == 0) { st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1; }
+            return;
+        }
+        // B4: gamma = <rhat, v>; alpha; s = r - alpha v; ||s||^2
+        double g1[1] = {0.0};
+#pragma unroll
+        for (int v = 0; v < V; ++v) g1[0] = fma(rh[v], v_[v], g1[0]);
+        tsum<1>(g1, red);
+        const double gam = g1[0];
+        if (gam == 0.0 || !isfinite(gam)) { status = KS_EBREAKDOWN; brk = 1; iters = i - 1; break; }
+        alpha = rho / gam;
+        double s[V];
+        double ss[1] = {0.0};
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            s[v] = fma(-alpha, v_[v], r[v]);
+            ss[0] = fma(s[v], s[v], ss[0]);
+        }
+        tsum<1>(ss, red);
+        const double srel = sqrt(ss[0]) / nb;
+        if (srel <= tol) {                                     // B5: half-step exit
+#pragma unroll
+            for (int v = 0; v < V; ++v) x[v] = fma(alpha, p[v], x[v]);
+            if (lead0 && threadIdx.x == 0) { put_hist(st, a.hist, i - 1, srel); st->relres = srel; }
+            status = KS_OK; conv = 1; half = 1; iters = i;
+            break;
+        }
+        // B6: t = A s, exchange (slot 1); <t, s>, <t, t>
+        const uint32_t ft = fv + 1u;
+        const double trow = gemv_rows<V>(As, T.lda, R, s, wred);
+        uint64_t* slot1 = T.ll + 2 * T.lda;
+        if (threadIdx.x < R) ll_store(slot1 + 2 * (int64_t)(rb + threadIdx.x), trow, ft);
+        double t[V];
+        if (!ll_gather<V>(slot1, n, ft, t)) {
+            if (lead0 && threadIdx.x == 0) { st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1; }
+            return;
+        }
+        double d2[2] = {0.0, 0.0};
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            d2[0] = fma(t[v], s[v], d2[0]);
+            d2[1] = fma(t[v], t[v], d2[1]);
+        }
+        tsum<2>(d2, red);
+        const double tt = d2[1];
+        if (tt == 0.0 || !isfinite(tt)) { status = KS_EBREAKDOWN; brk = 1; iters = i - 1; break; }
+        const double om = d2[0] / tt;
+        if (om == 0.0 || !isfinite(om)) { status = KS_EBREAKDOWN; brk = 1; iters = i - 1; break; }
+        // B7: x = (x + alpha p) + omega s; r = s - omega t; <rhat, r>, <r, r>
+        double d3[2] = {0.0, 0.0};
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            x[v] = fma(om, s[v], fma(alpha, p[v], x[v]));
+            r[v] = fma(-om, t[v], s[v]);
+            d3[0] = fma(rh[v], r[v], d3[0]);
+            d3[1] = fma(r[v], r[v], d3[1]);
+        }
+        tsum<2>(d3, red);
+        omega = om;
+        rho_old = rho;
+        rho = d3[0];
+        // B8: history, convergence test
+        const double rel = sqrt(d3[1]) / nb;
+        if (lead0 && threadIdx.x == 0) { put_hist(st, a.hist, i - 1, rel); st->relres = rel; }
+        if (rel <= tol) { status = KS_OK; conv = 1; iters = i; break; }
+    }
+    if (lead0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int j = col_of(v);
+            if (j < n) { a.x_loc[j] = x[v]; a.p_full[j] = p[v]; a.v_full[j] = v_[v]; a.G_r[j] = r[v]; }
+        }
+        if (threadIdx.x == 0) {
+            st->iters = iters; st->status = status; st->converged = conv; st->breakdown = brk;
+            st->half = half; st->half_iter = half ? iters : 0;
+            st->alpha[iters & 3] = alpha; st->omega[iters & 3] = omega; st->rho[iters & 3] = rho;
+            st->done = 1;
+        }
+    }
+}
+
+template <int V>
+const void* kern(int bicgstab) {
+    return bicgstab ? (const void*)k_bs_tiny<V> : (const void*)k_cg_tiny<V>;
+}
+const void* kern_v(int bicgstab, int V) {
+    return V == 2 ? kern<2>(bicgstab) : kern<4>(bicgstab);
+}
+
+}  // namespace
+
+// Grid of the tiny kernels for an n x n FP64 system on one GPU (ld = padded row
+// length), 0 when not applicable: n <= 1024 (the full vectors fit in registers,
+// 4 values per thread and vector), every CTA's rows fit in shared memory (<= kRM),
+// one co-resident CTA per SM.
+int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld) {
+    if (n < 1 || n > 1024 || ld > 1024) return 0;
+    const int V = ld <= 512 ? 2 : 4;
+    int g = num_sms;
+    if (g > n) g = (int)n;
+    const int64_t rmax = (n + g - 1) / g;
+    if (rmax > kRM) return 0;
+    const size_t sm = (size_t)rmax * (size_t)ld * sizeof(double);
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+    if (sm + 4096 > (size_t)optin) return 0;
+    const void* k = kern_v(bicgstab, V);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return 0;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTT, sm);
+    if (per_sm < 1) return 0;
+    return g;
+}
+
+int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll, int grid,
+                cudaStream_t st) {
+    TinyArgs T;
+    T.a = a;
+    T.A = A;
+    T.lda = lda;
+    T.ll = ll;
+    const int n = (int)a.L.n;
+    const int64_t rmax = (n + grid - 1) / grid;
+    const size_t sm = (size_t)rmax * (size_t)lda * sizeof(double);
+    void* args[] = {&T};
+    const cudaError_t e = cudaLaunchCooperativeKernel(kern_v(bicgstab, lda <= 512 ? 2 : 4), dim3((unsigned)grid),
+                                                      dim3(kTT), args, sm, st);
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+}  // namespace ks

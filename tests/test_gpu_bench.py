@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("n", [4096, 8192])
 def test_bench_json_contract(n):
     out = subprocess.run([sys.executable, "bench.py", "--size", str(n), "--steps", "5", "--warmup", "3",
-                          "--cpu-rows", "64", "--cpu-budget", "2"], cwd=ROOT, capture_output=True,
+                          "--cpu-steps", "1"], cwd=ROOT, capture_output=True,
                          text=True, timeout=600, check=True).stdout
     lines = out.strip().splitlines()
     assert len(lines) == 1, out                      # exactly one JSON line on stdout
@@ -32,6 +32,7 @@ def test_bench_json_contract(n):
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-12
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    assert cb["one_thread"]["cores"] == 1 and cb["one_thread"]["value"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 16 * n and e["d2h_bytes_per_step"] == 16 * (n + 1)
     assert d["gpu_launches"] > 0

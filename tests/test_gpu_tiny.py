@@ -1,0 +1,152 @@
+"""GPU parity of the register-resident tiny kernels (ks_tiny.cu: one GPU, FP64,
+n <= 1024, A in shared memory, vectors replicated in registers, LL-format exchange
+of the GEMV output) vs the oracle, at the north-star bars (Q17-Q19), on
+ragged n (CTAs owning 0..8 rows; n < 148 CTAs; n not a multiple of the 512-double
+row padding) and on every exit of SURVEY.md sec.8(c).3/.4: convergence, the
+half-step exit, maxit, b = 0, NOTSPD, BiCGSTAB breakdown, x0 != 0.  Repeated solves
+on one context (CG and BiCGSTAB interleaved) check the LL epochs never match a
+stale word."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+ks = pytest.importorskip("paper_1511_07174_b200")
+
+from test_gpu_parity import FLOOR_BS, bars  # noqa: E402
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 100, 147, 148, 149, 296, 511, 513, 777, 1000, 1024])
+def test_tiny_parity_ragged(n):
+    A = synth.random_spd(n, 100.0, n)
+    rng = np.random.default_rng(n + 1)
+    b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+    D = synth.random_dd(n, n + 2)
+    bd = rng.standard_normal(n)
+    xo, ho, ro = oracle.cg(A, b, x0=x0, tol=1e-10)
+    yo, hyo, ryo = oracle.bicgstab(D, bd, x0=x0, tol=1e-10)
+    res = {}
+    for tiny in (1, 0):
+        with ks.Context(n) as ctx, ks.Context(n) as dtx:
+            ctx.set_option("tiny", tiny)
+            dtx.set_option("tiny", tiny)
+            ctx.load_rows(A)
+            dtx.load_rows(D)
+            x, h, r = ctx.cg(b, x0=x0, tol=1e-10)
+            bars(x, h, r, xo, ho, ro)
+            y, hy, ry = dtx.bicgstab(bd, x0=x0, tol=1e-10)
+            bars(y, hy, ry, yo, hyo, ryo, floor=FLOOR_BS)
+            assert ry.half_step_exit == ryo.half_step_exit
+            assert r.true_relres <= 1e-9 and ry.true_relres <= 1e-9
+            res[tiny] = (x, y)
+    if n >= 148:   # a different summation order really ran (not a silent fallback)
+        assert not (np.array_equal(res[1][0], res[0][0]) and np.array_equal(res[1][1], res[0][1]))
+
+
+def test_tiny_c1_configs():
+    """C1 = G-SPD(1024, 1e3): CG 130 iterations; C1b = G-DD(1024, 16): BiCGSTAB 34
+    (half-step exit) -- SURVEY.md App. A.8 counts, bars vs the oracle."""
+    n = 1024
+    A, c, b = synth.gspd(n, 1e3)
+    xo, ho, ro = oracle.cg(A, b, tol=1e-10)
+    D, bd = synth.gdd(n, 16)
+    yo, hyo, ryo = oracle.bicgstab(D, bd, tol=1e-10)
+    with ks.Context(n) as ctx, ks.Context(n) as dtx:
+        ctx.generate("spd", seed=synth.SEED, table=c)
+        x, h, r = ctx.cg(b, tol=1e-10)
+        assert r.iterations == 130 and r.converged
+        bars(x, h, r, xo, ho, ro)
+        dtx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        y, hy, ry = dtx.bicgstab(bd, tol=1e-10)
+        assert ry.iterations == 34 and ry.half_step_exit and ry.matvecs == 67
+        bars(y, hy, ry, yo, hyo, ryo, floor=FLOOR_BS)
+
+
+def test_tiny_exits():
+    n = 300
+    A = synth.random_spd(n, 50.0, 9)
+    D = synth.random_dd(n, 9)
+    rng = np.random.default_rng(9)
+    b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        # b = 0 (Q6)
+        x, h, r = ctx.cg(np.zeros(n), tol=1e-10)
+        assert r.iterations == 0 and r.converged and np.all(x == 0)
+        # maxit = 0: x = x0, EMAXIT
+        x, h, r = ctx.cg(b, x0=x0, tol=1e-10, maxit=0)
+        assert r.iterations == 0 and r.status == ks.KS_EMAXIT and np.array_equal(x, x0)
+        # maxit = 5: the oracle's x after 5 iterations
+        xo, ho, ro = oracle.cg(A, b, x0=x0, tol=0.0, maxit=5)
+        x, h, r = ctx.cg(b, x0=x0, tol=0.0, maxit=5)
+        assert r.iterations == 5 and r.status == ks.KS_EMAXIT and len(h) == 5
+        assert np.linalg.norm(x - xo) <= 1e-12 * np.linalg.norm(xo)
+        assert np.all(np.abs(h - ho) <= 1e-12 * ho)
+    with ks.Context(n) as ctx:                       # NOTSPD at k = 1: x unchanged
+        ctx.load_rows(-A)
+        x, h, r = ctx.cg(b, x0=x0, tol=1e-10)
+        assert r.status == ks.KS_ENOTSPD and r.iterations == 0 and np.array_equal(x, x0)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(D)
+        xo, ho, ro = oracle.bicgstab(D, b, tol=0.0, maxit=4)
+        x, h, r = ctx.bicgstab(b, tol=0.0, maxit=4)
+        assert r.iterations == 4 and r.status == ks.KS_EMAXIT and r.matvecs == 8 and len(h) == 4
+        assert np.linalg.norm(x - xo) <= 1e-12 * np.linalg.norm(xo)
+        assert np.all(np.abs(h - ho) <= 1e-12 * ho)
+    # block-diagonal 2x2 rotations, integer b: <rhat, A r0> = sum(a b - b a) = 0 exactly
+    K = np.zeros((n, n))
+    for i in range(0, n, 2):
+        K[i, i + 1], K[i + 1, i] = 1.0, -1.0
+    bi = rng.integers(-3, 4, n).astype(np.float64)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(K)
+        x, h, r = ctx.bicgstab(bi, tol=1e-10)
+        xo, ho, ro = oracle.bicgstab(K, bi, tol=1e-10)
+        assert ro.status == ks.KS_EBREAKDOWN and ro.iterations == 0
+        assert r.status == ks.KS_EBREAKDOWN and r.breakdown and r.iterations == 0 and np.all(x == 0)
+
+
+def test_tiny_spec_half_step_example():
+    """[[2,1],[0,3]] x = [3,3] -> x = [1,1], a half-step exit at
+    iteration 1 (pin P2)."""
+    with ks.Context(2) as ctx:
+        ctx.load_rows(np.array([[2.0, 1.0], [0.0, 3.0]]))
+        x, h, r = ctx.bicgstab(np.array([3.0, 3.0]), tol=1e-12)
+        assert r.iterations == 1 and r.half_step_exit and r.matvecs == 1
+        assert np.allclose(x, [1.0, 1.0], rtol=0, atol=4e-16)
+
+
+def test_tiny_repeated_solves_one_context():
+    """CG, BiCGSTAB, CG, BiCGSTAB on one context (one LL buffer): every repeat is
+    bitwise equal to the first solve of its method (stale LL words never match)."""
+    n = 700
+    A = synth.random_spd(n, 30.0, 4)
+    b = np.random.default_rng(4).standard_normal(n)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        first = {}
+        for rep in range(3):
+            for m in ("cg", "bicgstab"):
+                x, h, r = getattr(ctx, m)(b, tol=1e-10)
+                assert r.converged
+                if m not in first:
+                    first[m] = (x, h, r.iterations)
+                else:
+                    assert r.iterations == first[m][2]
+                    assert np.array_equal(x, first[m][0]) and np.array_equal(h, first[m][1])
+
+
+def test_tiny_not_used_for_multi_launch_batches():
+    """An explicit poll batch (several launches per solve) runs the small-n kernels
+    instead; results stay within the bars."""
+    n = 1024
+    A, c, b = synth.gspd(n, 1e3)
+    xo, ho, ro = oracle.cg(A, b, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.generate("spd", seed=synth.SEED, table=c)
+        ctx.set_option("poll_batch", 16)
+        x, h, r = ctx.cg(b, tol=1e-10)
+        bars(x, h, r, xo, ho, ro)
+        assert r.kernel_launches >= 130 // 16

@@ -24,6 +24,7 @@ CONFIGS = {
     "C5bs": ("bicgstab", 262144, dict(kd=16), 4),
     "C3bicg": ("bicg", 65536, dict(kd=16), 30),       # NEXT-3: BiCG (A p and A^T pt)
     "C1bicg": ("bicg", 1024, dict(kd=16), 200),
+    "C1bs": ("bicgstab", 1024, dict(kd=16), 30),        # C1b: converges at 34 (no breakdown at tol 0)
     "C3gmres": ("gmres", 65536, dict(kd=16), 30),     # NEXT-3: GMRES(30)
     "C1gmres": ("gmres", 1024, dict(kd=16), 200),
     "C2bs": ("bicgstab", 32768, dict(kd=16), 50),       # per-rank size of n = 65536 at P = 8 (P = 2)
@@ -70,11 +71,13 @@ def main():
         ctx.set_option("profile_gemv", 1)
         if "KS_PERSISTENT" in os.environ:                # comparisons: force the kernel mode
             ctx.set_option("persistent", int(os.environ["KS_PERSISTENT"]))
+        if "KS_TINY" in os.environ:                      # comparisons: tiny kernels on / off
+            ctx.set_option("tiny", int(os.environ["KS_TINY"]))
         if "KS_FUSED" in os.environ:                     # comparisons: fused vs NCCL exchange
             ctx.set_option("fused_comm", int(os.environ["KS_FUSED"]))
         solve(b, tol=0.0, maxit=2, hist=False)                     # warm-up
         _, _, r = solve(b, tol=0.0, maxit=K, hist=False)
-        ips = K / r.seconds_loop
+        ips = r.iterations / r.seconds_loop
         g = 1 if method in ("cg", "gmres") else 2   # GEMVs per iteration
         m = ctx.row_range(rank)[1] - ctx.row_range(rank)[0]
         esz = 4.0 if dtype == "f32" else 8.0
@@ -84,7 +87,7 @@ def main():
         ctx.set_option("true_residual", 1)
         x, h, rt = solve(b, tol=1e-5 if dtype == "f32" else 1e-10)
         rec = {"config": name, "dtype": dtype, "method": method, "n": n, "P": world, "gen_s": tgen,
-               "fixed_iters": K, "iters_per_s": ips, "frac_roofline_8TBps": ips * t_roof,
+               "fixed_iters": K, "iters_run": r.iterations, "iters_per_s": ips, "us_per_iter": 1e6 / ips, "frac_roofline_8TBps": ips * t_roof,
                "gemv_GBps_per_gpu": gemv_bw / 1e9, "iters_to_tol": rt.iterations,
                "converged": rt.converged, "half_step_exit": rt.half_step_exit,
                "true_relres": rt.true_relres, "solve_s": rt.seconds_total, "hist0": h[:3].tolist()}
