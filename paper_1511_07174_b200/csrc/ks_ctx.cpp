@@ -41,6 +41,7 @@ VecArgs Rank::vargs(bool fused) const {
     a.G_r = G_r;
     a.G_v = G_v;
     a.S = S;
+    a.X = X;
     a.scr = scr;
     a.num_sms = num_sms;
     return a;
@@ -86,7 +87,8 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         const size_t g = 2 * P * (size_t)r.L.chunk * e;
         const size_t sb = (2 * P * kScalSlot * e + 511) / 512 * 512;
         const size_t fb = (kNumPhases * kMaxRanks * sizeof(unsigned long long) + 511) / 512 * 512;
-        const size_t total = 2 * g + sb + fb;
+        const size_t xb = ((size_t)ld * e + 511) / 512 * 512;
+        const size_t total = 2 * g + sb + fb + xb;
         char* base = nullptr;
         KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total));
         KS_CUDA(cudaMemset(base, 0, total));
@@ -96,10 +98,12 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         r.G_v = reinterpret_cast<double*>(base + g);
         r.S = reinterpret_cast<double*>(base + 2 * g);
         r.flags = reinterpret_cast<unsigned long long*>(base + 2 * g + sb);
+        r.X = reinterpret_cast<double*>(base + 2 * g + sb + fb);
         for (int q = 0; q < kMaxRanks; ++q) {
-            r.pp.G_r[q] = r.pp.G_v[q] = r.pp.S[q] = nullptr;
+            r.pp.G_r[q] = r.pp.G_v[q] = r.pp.S[q] = r.pp.X[q] = nullptr;
             r.pp.flags[q] = nullptr;
         }
+        r.pp.X[r.rank] = r.X;
         r.pp.G_r[r.rank] = r.G_r;
         r.pp.G_v[r.rank] = r.G_v;
         r.pp.S[r.rank] = r.S;
@@ -116,6 +120,7 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     dmalloc(&r.scr.qpart, r.scr.qpart_cap);
     dmalloc(&r.scr.tile_ticket, r.scr.tile_cap);
     KS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&r.h_done), 2 * sizeof(int)));
+    KS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&r.h_hist), (size_t)kHistStage * sizeof(double)));
     KS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&r.h_state), sizeof(DevState)));
     for (auto& e : r.ev_poll) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreate(&r.ev_t0));
@@ -140,6 +145,7 @@ void rank_free(Rank& r) {
                     (void*)r.gm_hx, (void*)r.gm_state, (void*)r.ll})
         if (p) dev_free(p);
     if (r.h_done) cudaFreeHost(r.h_done);
+    if (r.h_hist) cudaFreeHost(r.h_hist);
     if (r.h_state) cudaFreeHost(r.h_state);
     for (auto e : r.ev_poll) if (e) cudaEventDestroy(e);
     if (r.ev_t0) cudaEventDestroy(r.ev_t0);
@@ -189,8 +195,10 @@ VecArgsT<float> Rank::vargs_f32(bool fused) const {
         a.pp.G_v[g] = as<float>(pp.G_v[g]);
         a.pp.S[g] = as<float>(pp.S[g]);
         a.pp.flags[g] = pp.flags[g];
+        a.pp.X[g] = as<float>(pp.X[g]);
     }
     a.flags = flags;
+    a.X = as<float>(X);
     return a;
 }
 
@@ -218,7 +226,8 @@ void setup_peers(ks_ctx* c) {
     auto boff = [&](const void* p) {
         return (size_t)(static_cast<const char*>(p) - reinterpret_cast<const char*>(c->ranks[0].xbuf));
     };
-    const size_t offGv = boff(c->ranks[0].G_v), offS = boff(c->ranks[0].S), offF = boff(c->ranks[0].flags);
+    const size_t offGv = boff(c->ranks[0].G_v), offS = boff(c->ranks[0].S), offF = boff(c->ranks[0].flags),
+                 offX = boff(c->ranks[0].X);
     if (!c->multiprocess) {
         bool ok = true;
         for (auto& a : c->ranks)
@@ -238,6 +247,7 @@ void setup_peers(ks_ctx* c) {
                 a.pp.G_v[b.rank] = b.G_v;
                 a.pp.S[b.rank] = b.S;
                 a.pp.flags[b.rank] = b.flags;
+                a.pp.X[b.rank] = b.X;
             }
             a.peer_ok = ok;
         }
@@ -268,6 +278,7 @@ void setup_peers(ks_ctx* c) {
         r.pp.G_v[g] = reinterpret_cast<double*>(d + offGv);
         r.pp.S[g] = reinterpret_cast<double*>(d + offS);
         r.pp.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
+        r.pp.X[g] = reinterpret_cast<double*>(d + offX);
     }
     // every rank must agree, or none uses the fused path (collectives must match)
     int* dok = nullptr;

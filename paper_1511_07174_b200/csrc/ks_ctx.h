@@ -73,6 +73,7 @@ struct Rank {
     double* G_v = nullptr;      // 2 * P * chunk
     double* S = nullptr;        // 2 * P * kScalSlot
     unsigned long long* flags = nullptr;   // [kNumPhases][kMaxRanks]
+    double* X = nullptr;        // ld elements: contiguous full x (end-of-solve gather)
     PeerPtrs pp{};
     bool peer_ok = false;       // every rank's exchange buffers are load/store reachable
     std::vector<void*> ipc_opened;
@@ -86,6 +87,7 @@ struct Rank {
 
     // host
     int* h_done = nullptr;      // pinned, 2 slots
+    double* h_hist = nullptr;   // pinned staging of short histories (kHistStage entries)
     DevState* h_state = nullptr; // pinned
     std::vector<unsigned char> loaded;  // per local row
     int64_t loaded_count = 0;
@@ -105,6 +107,7 @@ struct Rank {
         int variant = 0, rows = 0, splits = 0, fused = 0;
     } graphs[2];
 
+    bool bar_zeroed = false;    // the start kernel zeroed the grid-barrier counter
     int64_t launches = 0;
     int64_t gemv_launches = 0;
     double gemv_seconds = 0.0;
@@ -162,6 +165,7 @@ struct ks_ctx {
 };
 
 namespace ks {
+constexpr int64_t kHistStage = 4096;   // histories up to this long are staged: one sync per solve
 void rank_alloc(ks_ctx* c, Rank& r);
 void rank_free(Rank& r);
 void setup_peers(ks_ctx* c);   // peer access / CUDA IPC of the exchange buffers

@@ -22,7 +22,8 @@ constexpr int kPhaseS = 0;   // scalar partials  (CG sigma; BiCGSTAB <t,s>, <t,t
 constexpr int kPhaseR = 1;   // r slice + <rhat,r>, <r,r> / rho' partials
 constexpr int kPhaseV = 2;   // BiCGSTAB v slice + <rhat,v>
 constexpr int kPhaseJ = 3;   // solve-start rendezvous (epoch = the solve's ebase)
-constexpr int kNumPhases = 4;
+constexpr int kPhaseX = 4;   // end-of-solve x gather (epoch = ebase + maxit + 1)
+constexpr int kNumPhases = 5;
 
 // Peer (NVLink, unified-address) pointers to every rank's exchange buffers,
 // parity-0 bases; rank g's own entries point at its local memory.
@@ -32,6 +33,7 @@ struct PeerPtrsT {
     T* G_v[kMaxRanks];
     T* S[kMaxRanks];
     unsigned long long* flags[kMaxRanks];   // [kNumPhases][kMaxRanks] epochs
+    T* X[kMaxRanks];                        // full-length x (contiguous), end-of-solve gather
 };
 using PeerPtrs = PeerPtrsT<double>;
 
@@ -160,6 +162,7 @@ struct VecArgsT {
     int peer;              // 1: fused NVLink peer-store collectives
     PeerPtrsT<T> pp;
     unsigned long long* flags;   // own [kNumPhases][kMaxRanks]
+    T* X;                  // own full-length x gather buffer (exchange allocation)
     T* b_full_mut() const { return const_cast<T*>(b_full); }
 };
 using VecArgs = VecArgsT<double>;
@@ -187,6 +190,19 @@ int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chun
 // failed (KS_ENCCL).  Launched after the init kernel, before the iteration loop.
 template <class T>
 int launch_join(const VecArgsT<T>& a, unsigned long long epoch, long long timeout_ms, cudaStream_t st);
+// Solve start with x0 = 0 in ONE launch (rows A0 / B0): r0 = b into G_r (every rank
+// holds all of b: no gather), x = 0, rhat = r0, CG p0 = r0, ||b||^2 = <r0, r0> in
+// the partial slots, the solver state (init_state / init_decide), and -- when
+// join_ms > 0 (fused P > 1) -- the solve-start rendezvous of launch_join.  It also
+// zeroes the persistent kernels' grid-barrier counter (scr.ticket + 8), so the first
+// persistent launch of the solve needs no memset (bar_zeroed).
+int launch_start(const VecArgs& a, int bicgstab, double tol, long long maxit, long long hist_cap,
+                 unsigned long long ebase, long long join_ms, cudaStream_t st);
+// Solve end in ONE launch: the k_finish decisions (BiCGSTAB test of the last step,
+// EMAXIT, b = 0 -> x = 0) and, when gather (fused P > 1), the x gather: every rank
+// stores its rows of x into every rank's contiguous X buffer over NVLink and
+// releases kPhaseX with `epoch`; the launch returns when every rank's rows arrived.
+int launch_end(const VecArgs& a, int bicgstab, int gather, unsigned long long epoch, cudaStream_t st);
 // Iteration kernels use k = koff + (kdev ? *kdev : 0): a captured batch of
 // iterations (CUDA graph) is replayed with *kdev advanced by k_advance.
 int launch_advance(long long* kdev, long long by, cudaStream_t st);
@@ -243,7 +259,7 @@ int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll);
 template <class T>
 int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
                    T* bpart, unsigned* bar, long long k0, long long k1, int grid, int rows, int unroll,
-                   cudaStream_t st);
+                   cudaStream_t st, bool bar_zeroed = false);
 
 // Small-n kernels (ks_small.cu, NEXT-2): full-length vectors in every CTA's shared
 // memory, 1 (CG) / 2 (BiCGSTAB) grid barriers per iteration.  kind: 0 = CG, 1 =
@@ -254,7 +270,7 @@ template <class T>
 int small_grid(int kind, int num_sms, int64_t rows, int64_t ncols);
 template <class T>
 int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
-                 unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st);
+                 unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st, bool bar_zeroed = false);
 
 // Tiny kernels (ks_tiny.cu, NEXT-2): one GPU, FP64, n <= 1024: A resident in shared
 // memory, full vectors replicated in registers, GEMV outputs exchanged through an

@@ -331,7 +331,7 @@ int persist_grid(int bicgstab, int num_sms, int64_t mmax, int rows, int unroll) 
 template <class T>
 int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols,
                    T* bpart, unsigned* bar, long long k0, long long k1, int grid, int rows, int unroll,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool bar_zeroed) {
     PersistArgs<T> P;
     P.a = a;
     P.A = A;
@@ -342,8 +342,11 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
     P.k0 = k0;
     P.k1 = k1;
     void* args[] = {&P};
-    cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
-    if (e != cudaSuccess) return -(int)e;
+    cudaError_t e = cudaSuccess;
+    if (!bar_zeroed) {
+        e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
+        if (e != cudaSuccess) return -(int)e;
+    }
     e = cudaLaunchCooperativeKernel(pick<T>(bicgstab, rows, unroll), dim3((unsigned)grid),
                                                 dim3(kNT), args, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
@@ -352,8 +355,8 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
 template int persist_grid<double>(int, int, int64_t, int, int);
 template int persist_grid<float>(int, int, int64_t, int, int);
 template int launch_persist<double>(int, const VecArgsT<double>&, const double*, int64_t, int64_t, double*,
-                                    unsigned*, long long, long long, int, int, int, cudaStream_t);
+                                    unsigned*, long long, long long, int, int, int, cudaStream_t, bool);
 template int launch_persist<float>(int, const VecArgsT<float>&, const float*, int64_t, int64_t, float*,
-                                   unsigned*, long long, long long, int, int, int, cudaStream_t);
+                                   unsigned*, long long, long long, int, int, int, cudaStream_t, bool);
 
 }  // namespace ks

@@ -649,7 +649,7 @@ int small_grid(int kind, int num_sms, int64_t rows, int64_t ncols) {
 
 template <class T>
 int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
-                 unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st) {
+                 unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st, bool bar_zeroed) {
     PersistArgs<T> P;
     P.a = a;
     P.A = A;
@@ -660,8 +660,11 @@ int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_
     P.k0 = k0;
     P.k1 = k1;
     void* args[] = {&P};
-    cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
-    if (e != cudaSuccess) return -(int)e;
+    cudaError_t e = cudaSuccess;
+    if (!bar_zeroed) {
+        e = cudaMemsetAsync(bar, 0, sizeof(unsigned long long), st);   // grid_sync counter
+        if (e != cudaSuccess) return -(int)e;
+    }
     e = cudaLaunchCooperativeKernel(kern<T>(kind), dim3((unsigned)grid), dim3(kNT), args,
                                     smem_bytes<T>(kind, ncols), st);
     return e == cudaSuccess ? 1 : -(int)e;
@@ -670,8 +673,8 @@ int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_
 template int small_grid<double>(int, int, int64_t, int64_t);
 template int small_grid<float>(int, int, int64_t, int64_t);
 template int launch_small<double>(int, const VecArgsT<double>&, const double*, int64_t, int64_t, double*,
-                                  unsigned*, long long, long long, int, cudaStream_t);
+                                  unsigned*, long long, long long, int, cudaStream_t, bool);
 template int launch_small<float>(int, const VecArgsT<float>&, const float*, int64_t, int64_t, float*,
-                                 unsigned*, long long, long long, int, cudaStream_t);
+                                 unsigned*, long long, long long, int, cudaStream_t, bool);
 
 }  // namespace ks

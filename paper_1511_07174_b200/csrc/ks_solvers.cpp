@@ -151,19 +151,21 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
         if (persist) {                                    // one cooperative launch per batch
             const int64_t kend = std::min<int64_t>(maxit, k + B - 1);
             prof.pre(slot);
+            const bool z = r.bar_zeroed && k == 1;
             const int rc = tgrid > 0
                 ? launch_tiny(kind, r.vargs(false), r.A, c->ld, r.ll, tgrid, r.stream)
                 : sgrid > 0
                 ? launch_small<double>(small_kind(c, kind), r.vargs(c->fused()), r.A, c->ld, c->ld,
-                                       r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, sgrid, r.stream)
+                                       r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, sgrid, r.stream, z)
                 : launch_persist<double>(kind, r.vargs(c->fused()), r.A, c->ld, c->ld,
                                          r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, pgrid,
-                                         prows, punroll, r.stream);
+                                         prows, punroll, r.stream, z);
             prof.post(slot);
             if (rc < 0) KS_CUDA((cudaError_t)(-rc));
             r.launches += 1;
             r.gemv_launches += (kend - k + 1) * gemvs_per_iter;
             k = kend + 1;
+            if (k > maxit) break;        // last launch: nothing left to stop early
         } else if (use_graph && k + B - 1 <= maxit) {
             KS_CUDA(cudaGraphLaunch(g->exec, r.stream));   // iterations k .. k+B-1
             r.launches += g->launches;
@@ -183,6 +185,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
         }
         ++batch;
     }
+    r.bar_zeroed = false;
     KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
     if (c->opt.profile_gemv) {            // otherwise finish_and_copy's synchronisation covers it
         KS_CUDA(cudaStreamSynchronize(r.stream));
@@ -208,14 +211,29 @@ GemvParams gp(const ks_ctx* c, const Rank& r, const double* x, double* y) {
 
 // Setup shared by both methods (rows A0 / B0): b and x0 in; r0 = b - A x0
 // (K1 residual mode) or r0 = b; x_loc; rhat; partial <r0, r0>; allgather G_r.
-void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_cap) {
-    const size_t nbytes = (size_t)c->n * sizeof(double);
+void ensure_hist(Rank& r, int64_t hist_cap) {
     if (hist_cap > r.hist_alloc) {
         dev_free(r.hist);
         r.hist = nullptr;
         r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
         dev_alloc_t(&r.hist, (size_t)r.hist_alloc);
     }
+}
+
+// CG / BiCGSTAB with x0 = 0: b in, then rows A0/B0 + state init (+ the rendezvous
+// for the fused exchange) as ONE kernel (launch_start).
+void start(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, int64_t maxit, int64_t hist_cap,
+           unsigned long long ebase) {
+    ensure_hist(r, hist_cap);
+    KS_CUDA(cudaMemcpyAsync(r.b_full, b, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+    r.launches += launch_start(r.vargs(c->fused()), bicgstab, tol, maxit, hist_cap, ebase,
+                               c->fused() ? c->opt.join_timeout_ms : 0, r.stream);
+    r.bar_zeroed = true;
+}
+
+void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_cap) {
+    const size_t nbytes = (size_t)c->n * sizeof(double);
+    ensure_hist(r, hist_cap);
     KS_CUDA(cudaMemcpyAsync(r.b_full, b, nbytes, cudaMemcpyDefault, r.stream));
     VecArgs a = r.vargs(false);   // setup gathers r0 with NCCL into parity 0
     if (x0) {
@@ -234,20 +252,27 @@ void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_c
 }
 
 // Final x: gather, optional true residual ||b - A x|| (one extra GEMV), copy out.
+// end_mode: 0 = the caller already ran its finish kernel (x gathered with NCCL for
+// P > 1); 1 = CG / BiCGSTAB: launch_end runs the finish decisions and, with the
+// fused exchange, gathers x into every rank's contiguous X over NVLink (no NCCL
+// call, no extra launch).  One stream synchronisation when the history is short.
 void finish_and_copy(ks_ctx* c, Rank& r, double* x, double* hist, int64_t hist_cap,
-                     ks_report* rep, bool bicgstab, const Clock::time_point& t_start) {
+                     ks_report* rep, bool bicgstab, const Clock::time_point& t_start, int64_t maxit,
+                     int end_mode = 0, unsigned long long x_epoch = 0) {
     VecArgs a = r.vargs(false);   // final x gather / true residual: NCCL, parity 0
-    const double* xfull_dev = nullptr;
-    if (c->P > 1) {
+    const bool fused_x = end_mode == 1 && c->P > 1 && c->fused();
+    if (end_mode == 1) r.launches += launch_end(r.vargs(c->fused()), bicgstab ? 1 : 0, fused_x ? 1 : 0,
+                                                x_epoch, r.stream);
+    const double* xsrc = c->P == 1 ? r.x_loc : fused_x ? r.X : nullptr;   // contiguous full x
+    if (c->P > 1 && !fused_x) {
         r.launches += launch_pack_x(a, r.stream);
         allgather(c, r, r.G_v, r.L.chunk);
     }
     if (c->opt.true_residual) {
-        if (c->P > 1) copy_chunks_to(c, r, r.G_v, r.s_full, cudaMemcpyDeviceToDevice);
-        else KS_CUDA(cudaMemcpyAsync(r.s_full, r.x_loc, (size_t)c->n * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, r.stream));
-        xfull_dev = r.s_full;
-        GemvParams p = gp(c, r, xfull_dev, r.q_loc);
+        if (xsrc) KS_CUDA(cudaMemcpyAsync(r.s_full, xsrc, (size_t)c->n * sizeof(double),
+                                          cudaMemcpyDeviceToDevice, r.stream));
+        else copy_chunks_to(c, r, r.G_v, r.s_full, cudaMemcpyDeviceToDevice);
+        GemvParams p = gp(c, r, r.s_full, r.q_loc);
         p.bsub = r.b_full + r.row0;
         p.out2 = r.S + (int64_t)r.rank * kScalSlot + 1;
         gemv(c, r, p);
@@ -255,19 +280,38 @@ void finish_and_copy(ks_ctx* c, Rank& r, double* x, double* hist, int64_t hist_c
         r.launches += launch_true_res_final(a, r.stream);
     }
     KS_CUDA(cudaMemcpyAsync(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost, r.stream));
-    if (c->writes_host(r)) {              // x does not depend on the state: same synchronisation
-        if (c->P > 1) copy_chunks_to(c, r, r.G_v, x, cudaMemcpyDefault);
-        else KS_CUDA(cudaMemcpyAsync(x, r.x_loc, (size_t)c->n * sizeof(double), cudaMemcpyDefault,
-                                     r.stream));
+    const bool out = c->writes_host(r);
+    if (out) {                            // x does not depend on the state: same synchronisation
+        if (xsrc) KS_CUDA(cudaMemcpyAsync(x, xsrc, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+        else copy_chunks_to(c, r, r.G_v, x, cudaMemcpyDefault);
     }
+    // history: at most min(maxit, hist_cap) entries; a short one is staged in pinned
+    // memory in the same batch (the valid prefix is copied out after the one sync)
+    const int64_t nh_max = std::min<int64_t>(hist_cap, maxit);
+    const bool staged = out && hist && nh_max > 0 && nh_max <= kHistStage;
+    if (staged)
+        KS_CUDA(cudaMemcpyAsync(r.h_hist, r.hist, (size_t)nh_max * sizeof(double), cudaMemcpyDeviceToHost,
+                                r.stream));
     KS_CUDA(cudaStreamSynchronize(r.stream));
     const DevState& s = *r.h_state;
-    if (c->writes_host(r)) {
+    if (out) {
         const int64_t nh = std::min<int64_t>(s.iters, hist_cap);
         if (hist && nh > 0) {
-            KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault,
-                                    r.stream));
-            KS_CUDA(cudaStreamSynchronize(r.stream));
+            if (staged) {
+                cudaPointerAttributes at{};
+                const bool dev_dst = cudaPointerGetAttributes(&at, hist) == cudaSuccess &&
+                                     at.type == cudaMemoryTypeDevice;
+                if (!dev_dst) {
+                    std::memcpy(hist, r.h_hist, (size_t)nh * sizeof(double));
+                } else {
+                    KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault, r.stream));
+                    KS_CUDA(cudaStreamSynchronize(r.stream));
+                }
+            } else {
+                KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault,
+                                        r.stream));
+                KS_CUDA(cudaStreamSynchronize(r.stream));
+            }
         }
     }
     if (rep) {
@@ -326,13 +370,17 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
     r.launches = 0;
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
-    setup(c, r, b, x0, hist_cap);
     const bool fused = c->fused();
     VecArgs a = r.vargs(fused);
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
-    r.launches += launch_cg_init(a, tol, maxit, hist_cap, ebase, r.stream);
-    if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
+    if (!x0) {
+        start(c, r, 0, b, tol, maxit, hist_cap, ebase);     // A0 + init (+ rendezvous): one launch
+    } else {
+        setup(c, r, b, x0, hist_cap);
+        r.launches += launch_cg_init(a, tol, maxit, hist_cap, ebase, r.stream);
+        if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
+    }
     double* sig = r.S + (int64_t)r.rank * kScalSlot;
     GemvParams pq = gp(c, r, r.p_full, r.q_loc);
     pq.w1 = r.p_full + r.row0;                 // sigma_g = <p_loc, q_loc>
@@ -351,8 +399,7 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
         if (!fused) allgather(c, r, r.G_r, r.L.chunk); // A4 (C1)
         r.launches += launch_cg_direction(a, kdev, k, r.stream); // A5
     });
-    r.launches += launch_cg_finish(a, r.stream);
-    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start, maxit, 1, ebase + (unsigned long long)maxit + 1);
     return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
 }
 
@@ -363,13 +410,17 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     r.launches = 0;
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
-    setup(c, r, b, x0, hist_cap);
     const bool fused = c->fused();
     VecArgs a = r.vargs(fused);
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
-    r.launches += launch_bs_init(a, tol, maxit, hist_cap, ebase, r.stream);
-    if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
+    if (!x0) {
+        start(c, r, 1, b, tol, maxit, hist_cap, ebase);     // B0 + init (+ rendezvous): one launch
+    } else {
+        setup(c, r, b, x0, hist_cap);
+        r.launches += launch_bs_init(a, tol, maxit, hist_cap, ebase, r.stream);
+        if (fused) r.launches += launch_join(a, ebase, c->opt.join_timeout_ms, r.stream);
+    }
     double* vown = r.G_v + (int64_t)r.rank * r.L.chunk;
     GemvParams pv = gp(c, r, r.p_full, vown);  // B3: v = A p, <rhat, v>_g
     pv.w1 = r.rhat_loc;
@@ -404,8 +455,7 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
         r.launches += launch_bs_xr(a, kdev, i, r.stream); // B7 (+ fused C1)
         if (!fused) allgather(c, r, r.G_r, r.L.chunk);   // B8 partials + r (C1)
     });
-    r.launches += launch_bs_finish(a, r.stream);
-    finish_and_copy(c, r, x, hist, hist_cap, rep, true, t_start);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, true, t_start, maxit, 1, ebase + (unsigned long long)maxit + 1);
     return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
 }
 
@@ -625,7 +675,7 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
         KS_CUDA(cudaMemcpy(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost));
         r.gemv_launches = r.h_state->iters;
         r.launches += launch_cg_finish(a, r.stream);
-        finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+        finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start, maxit);
         return r.h_state->status;
     }
     while (true) {
@@ -676,7 +726,7 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
     prof.harvest(0);
     prof.harvest(1);
     r.launches += launch_cg_finish(a, r.stream);
-    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start, maxit);
     return r.h_state->status;
 }
 
@@ -740,7 +790,7 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
     prof.harvest(0);
     prof.harvest(1);
     r.launches += launch_cg_finish(a, r.stream);
-    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start);
+    finish_and_copy(c, r, x, hist, hist_cap, rep, false, t_start, maxit);
     if (rep) rep->matvecs = 2 * rep->iterations;
     return r.h_state->status;
 }

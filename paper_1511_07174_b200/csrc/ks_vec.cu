@@ -555,7 +555,120 @@ __global__ void k_join(VecArgsT<T> a, unsigned long long epoch, unsigned long lo
     }
 }
 
+// Rows A0 / B0 with x0 = 0 plus the solver-state init (and the rendezvous) in one
+// launch; the arithmetic is k_setup_local's / k_setup_r's and k_cg_init's /
+// k_bs_init's: r0 = b, <r0, r0> = ||b||^2 in one fixed-order grid reduction.
+__global__ void __launch_bounds__(kNT) k_start(VecArgs a, int bicgstab, double tol, long long maxit,
+                                               long long hist_cap, unsigned long long ebase,
+                                               unsigned long long join_ns) {
+    __shared__ double red[kNT / 32];
+    const Layout& L = a.L;
+    const int64_t m = rows_of(L), r0 = L.row0[L.rank];
+    const int64_t gs = (int64_t)gridDim.x * kNT;
+    double acc[1] = {0.0};
+    for (int64_t j = blockIdx.x * (int64_t)kNT + threadIdx.x; j < L.n; j += gs) {
+        const double bj = a.b_full[j];
+        a.G_r[gidx(L, j)] = bj;                       // r0 = b (Q5), parity 0
+        if (!bicgstab) a.p_full[j] = bj;               // CG: p0 = r0 (full, replicated)
+        acc[0] = fma(bj, bj, acc[0]);
+    }
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += gs) {
+        a.x_loc[i] = 0.0;
+        a.rhat_loc[i] = a.b_full[r0 + i];              // rhat = r0 (Q7)
+    }
+    block_sum<kNT, 1>(acc, red);
+    if (!(grid_sum<kNT, 1>(acc, a.scr.part, a.scr.ticket, red) && threadIdx.x == 0)) return;
+    for (int g = 0; g < L.P; ++g) {
+        a.G_r[(int64_t)g * L.chunk + L.pslot + 0] = g == 0 ? acc[0] : 0.0;   // <rhat, r0>
+        a.G_r[(int64_t)g * L.chunk + L.pslot + 1] = g == 0 ? acc[0] : 0.0;   // <r0, r0>
+    }
+    DevState* st = a.st;
+    *reinterpret_cast<unsigned long long*>(a.scr.ticket + 8) = 0ull;   // persistent grid-barrier counter
+    init_state(st, tol, maxit, hist_cap, ebase);     // BiCGSTAB: rho_old = alpha = omega = 1 (Q8)
+    if (!bicgstab) st->rho[0] = acc[0];
+    init_decide(st, acc[0], acc[0]);
+    if (join_ns == 0) return;
+    unsigned long long* f[kMaxRanks];                 // the rendezvous (launch_join)
+    for (int g = 0; g < L.P; ++g) f[g] = a.pp.flags[g] + kPhaseJ * kMaxRanks + L.rank;
+    publish_flags(f, L.P, ebase);
+    const unsigned long long t0 = globaltimer_ns();
+    for (int g = 0; g < L.P; ++g) {
+        while (flag_acquire_sys(a.flags + kPhaseJ * kMaxRanks + g) < ebase) {
+            if (globaltimer_ns() - t0 > join_ns) {
+                st->peer_timeout = 1; st->status = KS_ENCCL; st->done = 1;
+                return;
+            }
+            __nanosleep(64);
+        }
+    }
+}
+
+// k_finish + (gather) the fused end-of-solve x gather into every rank's X.
+__global__ void __launch_bounds__(kNT) k_end(VecArgs a, int bicgstab, int gather, unsigned long long epoch) {
+    __shared__ int s_last;
+    DevState* st = a.st;
+    const Layout& L = a.L;
+    if (bicgstab && !is_done(st) && st->maxit >= 1 && !wait_phase(a, kPhaseR, st->maxit)) return;
+    if (lead() && !st->done) {
+        const long long maxit = st->maxit;
+        st->iters = maxit;
+        st->status = KS_EMAXIT;
+        if (bicgstab && maxit >= 1) {                     // test of the last full step
+            const double rel = sqrt(slot_sum(L, Gpar(a, a.G_r, maxit), 1)) / st->nb;
+            put_hist(st, a.hist, maxit - 1, rel);
+            st->relres = rel;
+            if (rel <= st->tol) { st->converged = 1; st->status = KS_OK; }
+        }
+        st->done = 1;
+    }
+    const int bz = st->bzero;                             // set by the start kernel only
+    const int64_t m = rows_of(L), r0 = L.row0[L.rank];
+    bool stored = false;
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kNT) {
+        double xv = a.x_loc[i];
+        if (bz) { xv = 0.0; a.x_loc[i] = 0.0; }           // Q6: b = 0 -> x = 0
+        if (gather) {
+            for (int g = 0; g < L.P; ++g) a.pp.X[g][r0 + i] = xv;
+            stored = true;
+        }
+    }
+    if (!gather) return;
+    if (stored) __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* ticket = a.scr.ticket + 16;
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (s_last) *ticket = 0u;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    unsigned long long* f[kMaxRanks];
+    for (int g = 0; g < L.P; ++g) f[g] = a.pp.flags[g] + kPhaseX * kMaxRanks + L.rank;
+    publish_flags(f, L.P, epoch);
+    const unsigned long long t0 = globaltimer_ns();
+    for (int g = 0; g < L.P; ++g) {
+        while (flag_acquire_sys(a.flags + kPhaseX * kMaxRanks + g) < epoch) {
+            if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
+                st->peer_timeout = 1; st->status = KS_ENCCL;
+                return;
+            }
+            __nanosleep(32);
+        }
+    }
+}
+
 }  // namespace
+
+int launch_start(const VecArgs& a, int bicgstab, double tol, long long maxit, long long hist_cap,
+                 unsigned long long ebase, long long join_ms, cudaStream_t st) {
+    const unsigned long long ns = join_ms > 0 ? (unsigned long long)join_ms * 1000000ULL : 0ULL;
+    k_start<<<grid_for(a.L.n, a.num_sms), kNT, 0, st>>>(a, bicgstab, tol, maxit, hist_cap, ebase, ns);
+    return 1;
+}
+int launch_end(const VecArgs& a, int bicgstab, int gather, unsigned long long epoch, cudaStream_t st) {
+    k_end<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a, bicgstab, gather, epoch);
+    return 1;
+}
 
 template <class T>
 int launch_join(const VecArgsT<T>& a, unsigned long long epoch, long long timeout_ms, cudaStream_t st) {
