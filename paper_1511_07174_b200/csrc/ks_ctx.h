@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <functional>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -108,6 +109,7 @@ struct Rank {
     } graphs[2];
 
     bool bar_zeroed = false;    // the start kernel zeroed the grid-barrier counter
+    std::map<long long, int> grid_memo;   // launch geometry (occupancy queries) per kernel kind
     int64_t launches = 0;
     int64_t gemv_launches = 0;
     double gemv_seconds = 0.0;

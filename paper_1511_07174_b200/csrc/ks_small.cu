@@ -635,7 +635,9 @@ int small_grid(int kind, int num_sms, int64_t rows, int64_t ncols) {
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
     if (sm + 1024 > (size_t)optin) return 0;
     const void* k = kern<T>(kind);
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return 0;
+    // the attribute is per function (shared by every context on the device): allow the
+    // device maximum, so a launch of any context's size stays valid after a memo hit
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) return 0;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kNT, sm);
     if (per_sm < 1) return 0;

@@ -40,12 +40,25 @@ int small_kind(const ks_ctx* c, int bicgstab) {
     if (bicgstab && c->opt.small == 2 && c->n * (int64_t)c->esz > ks_ctx::kSmallAutoMaxBytes / 2) return -1;
     return bicgstab ? 3 : 2;
 }
+// Launch geometry of a kernel kind, memoised per rank: the occupancy queries behind
+// it cost tens of microseconds of host time per call (a context's n, ld and device
+// never change).  key: (what << 48) | kind / shape.
+template <class F>
+int memo_grid(Rank& r, long long key, F&& f) {
+    auto it = r.grid_memo.find(key);
+    if (it != r.grid_memo.end()) return it->second;
+    const int g = f();
+    r.grid_memo.emplace(key, g);
+    return g;
+}
+
 // Grid of the small-n kernels, 0 = not used.
 template <class T>
-int small_path_grid(const ks_ctx* c, const Rank& r, int bicgstab) {
+int small_path_grid(const ks_ctx* c, Rank& r, int bicgstab) {
     const int kind = small_kind(c, bicgstab);
     if (kind < 0) return 0;
-    int g = small_grid<T>(kind, r.num_sms, r.m, c->ld);
+    int g = memo_grid(r, (1LL << 48) | ((long long)sizeof(T) << 40) | kind,
+                      [&] { return small_grid<T>(kind, r.num_sms, r.m, c->ld); });
     if (g > 0 && c->opt.persist_grid > 0) g = (int)std::min<int64_t>(g, c->opt.persist_grid);
     return g;
 }
@@ -107,7 +120,7 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     int prows = 0, punroll = 0;
     // tiny kernels: one GPU, the whole solve in one launch (they always finish it)
     if (persist && c->P == 1 && c->opt.tiny && c->opt.small != 0 && B >= maxit)
-        tgrid = tiny_grid(kind, r.num_sms, c->n, c->ld);
+        tgrid = memo_grid(r, (2LL << 48) | kind, [&] { return tiny_grid(kind, r.num_sms, c->n, c->ld); });
     if (tgrid > 0 && !r.ll) {
         dev_alloc_t(&r.ll, (size_t)(4 * c->ld));
         KS_CUDA(cudaMemsetAsync(r.ll, 0, (size_t)(4 * c->ld) * sizeof(uint64_t), r.stream));
@@ -115,7 +128,8 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     if (persist && tgrid == 0) sgrid = small_path_grid<double>(c, r, kind);
     if (persist && tgrid == 0 && sgrid == 0) {
         persist_shape(c, r, &prows, &punroll);
-        pgrid = persist_grid<double>(kind, r.num_sms, r.L.pslot, prows, punroll);
+        pgrid = memo_grid(r, (3LL << 48) | ((long long)prows << 24) | ((long long)punroll << 8) | kind,
+                          [&] { return persist_grid<double>(kind, r.num_sms, r.L.pslot, prows, punroll); });
         if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
     }
     const bool use_graph = !persist && c->opt.use_graphs && !c->opt.profile_gemv && B >= 2 && maxit >= B;
@@ -371,6 +385,7 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
     const bool fused = c->fused();
+    ensure_hist(r, hist_cap);                 // before vargs: it may move r.hist
     VecArgs a = r.vargs(fused);
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
@@ -411,6 +426,7 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
     const bool fused = c->fused();
+    ensure_hist(r, hist_cap);                 // before vargs: it may move r.hist
     VecArgs a = r.vargs(fused);
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
@@ -491,7 +507,8 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     Prof prof(c, r, 1);
     int prows = 0, punroll = 0;
     persist_shape(c, r, &prows, &punroll);
-    int pgrid = persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, prows, punroll);
+    int pgrid = memo_grid(r, (4LL << 48) | ((long long)prows << 24) | ((long long)punroll << 8) | bicgstab,
+                          [&] { return persist_grid<float>(bicgstab, r.num_sms, r.L.pslot, prows, punroll); });
     if (c->opt.persist_grid > 0) pgrid = (int)std::min<int64_t>(pgrid, c->opt.persist_grid);
     const int sgrid = small_path_grid<float>(c, r, bicgstab);
     float* bpart = reinterpret_cast<float*>(r.scr.part + 2 * kPartStride);

@@ -35,6 +35,10 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "ks_device.cuh"
 #include "ks_common.cuh"
 #include "ks_internal.h"
@@ -143,7 +147,20 @@ struct TinyArgs {
     const double* A;
     int64_t lda;
     uint64_t* ll;        // 2 slots x ld entries x 2 words (LL format)
+    // debug (KS_TINY_TRACE=k): thread 0 of every CTA stamps %clock64 at the phase
+    // boundaries of CG iteration k (kTrace stamps per CTA) and %globaltimer once
+    unsigned long long* trace;
+    long long trace_k;
 };
+constexpr int kTrace = 8;
+__device__ __forceinline__ void stamp(const TinyArgs& T, long long k, int i) {
+    if (T.trace && k == T.trace_k && threadIdx.x == 0) {
+        long long c;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+        T.trace[blockIdx.x * kTrace + i] = (unsigned long long)c;
+        if (i == 0) T.trace[gridDim.x * kTrace + blockIdx.x] = globaltimer_ns();
+    }
+}
 
 // This CTA's rows [rb, rb + R): balanced contiguous blocks.
 __device__ __forceinline__ void my_rows(int n, int& rb, int& R) {
@@ -204,8 +221,10 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
     int status = KS_EMAXIT, conv = 0;
     long long iters = maxit;
     for (; k <= maxit; ++k) {
+        stamp(T, k, 0);
         // A1: q rows = A p; LL exchange (the grid-wide step)
         const double qrow = gemv_rows<V>(As, T.lda, R, p, wred);
+        stamp(T, k, 1);
         const uint32_t flag = (uint32_t)(2ull * (eb + (unsigned long long)k));
         uint64_t* slot = T.ll + (int64_t)(k & 1) * 2 * T.lda;
         if (threadIdx.x < R) ll_store(slot + 2 * (int64_t)(rb + threadIdx.x), qrow, flag);
@@ -214,12 +233,14 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
             if (lead0 && threadIdx.x == 0) { st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1; }
             return;
         }
+        stamp(T, k, 2);
         // A2: sigma = <p, q> (full length, every CTA)
         double s1[1] = {0.0};
 #pragma unroll
         for (int v = 0; v < V; ++v) s1[0] = fma(p[v], q[v], s1[0]);
         tsum<1>(s1, red);
         const double sigma = s1[0];
+        stamp(T, k, 3);
         if (!(sigma > 0.0)) { status = KS_ENOTSPD; iters = k - 1; break; }   // Q9: x unchanged
         const double alpha = rho / sigma;
         // A3: x += alpha p; r -= alpha q; rho' = <r, r>
@@ -232,6 +253,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
         }
         tsum<1>(s2, red);
         const double rho1 = s2[0];
+        stamp(T, k, 4);
         const double rel = sqrt(rho1) / nb;
         if (lead0 && threadIdx.x == 0) {
             put_hist(st, a.hist, k - 1, rel);
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
 #pragma unroll
         for (int v = 0; v < V; ++v) p[v] = fma(beta, p[v], r[v]);
         rho = rho1;
+        stamp(T, k, 5);
     }
     if (lead0) {
 #pragma unroll
@@ -411,7 +434,7 @@ int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld) {
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
     if (sm + 4096 > (size_t)optin) return 0;
     const void* k = kern_v(bicgstab, V);
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return 0;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) return 0;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTT, sm);
     if (per_sm < 1) return 0;
@@ -428,9 +451,34 @@ int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, ui
     const int n = (int)a.L.n;
     const int64_t rmax = (n + grid - 1) / grid;
     const size_t sm = (size_t)rmax * (size_t)lda * sizeof(double);
+    T.trace = nullptr;
+    T.trace_k = 0;
+    const char* tr = bicgstab ? nullptr : std::getenv("KS_TINY_TRACE");   // debug facility
+    if (tr) {
+        T.trace_k = std::atoll(tr);
+        if (cudaMalloc(&T.trace, (size_t)grid * (kTrace + 1) * sizeof(unsigned long long)) != cudaSuccess)
+            T.trace = nullptr;
+        else cudaMemsetAsync(T.trace, 0, (size_t)grid * (kTrace + 1) * sizeof(unsigned long long), st);
+    }
     void* args[] = {&T};
     const cudaError_t e = cudaLaunchCooperativeKernel(kern_v(bicgstab, lda <= 512 ? 2 : 4), dim3((unsigned)grid),
                                                       dim3(kTT), args, sm, st);
+    if (T.trace) {                      // dump: one line per CTA, clock deltas then the start time
+        std::vector<unsigned long long> h((size_t)grid * (kTrace + 1));
+        cudaMemcpyAsync(h.data(), T.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(T.trace);
+        const char* out = std::getenv("KS_TINY_TRACE_OUT");
+        if (FILE* f = std::fopen(out ? out : "tiny_trace.txt", "a")) {
+            for (int b = 0; b < grid; ++b) {
+                std::fprintf(f, "%d %llu", b, h[(size_t)grid * kTrace + b]);
+                for (int i = 1; i < 6; ++i)
+                    std::fprintf(f, " %lld", (long long)(h[(size_t)b * kTrace + i] - h[(size_t)b * kTrace + i - 1]));
+                std::fprintf(f, "\n");
+            }
+            std::fclose(f);
+        }
+    }
     return e == cudaSuccess ? 1 : -(int)e;
 }
 

@@ -193,6 +193,8 @@ def test_cg_edge_cases():
         # hist_cap smaller than the iteration count
         x, h, r = ctx.cg(b, tol=1e-10, hist_cap=5)
         assert len(h) == 5 and r.iterations > 5
+        ctx.set_option("tiny", 0)   # the tiny kernels run only single-launch solves
+        x, h, r = ctx.cg(b, tol=1e-10, hist_cap=5)
         for q in (1, 3, 64):   # poll batch does not change the result
             ctx.set_option("poll_batch", q)
             x2, h2, r2 = ctx.cg(b, tol=1e-10)
@@ -358,6 +360,7 @@ def test_persistent_vs_multikernel_parity(persistent, small):
             ctx.load_rows(A)
             ctx.set_option("persistent", persistent)
             ctx.set_option("small", small)
+            ctx.set_option("tiny", 0)    # single-launch only: tests/test_gpu_tiny.py
             assert ctx.get_option("persistent") == persistent
             x, h, r = getattr(ctx, method)(b, tol=1e-10)
             x2, h2, r2 = getattr(ctx, method)(b, tol=1e-10)

@@ -18,15 +18,27 @@ ks = pytest.importorskip("paper_1511_07174_b200")
 from test_gpu_parity import FLOOR_BS, bars  # noqa: E402
 
 
+def gspd_any(n):
+    """G-SPD for any n: the leading n x n block of G-SPD(n + n mod 2, 1e3) (still SPD,
+    interlaced near-uniform spectrum).  Parity-safe -- two summation orders agree far
+    inside the history bar -- for n >= 147 (checked against a numpy-order CG during
+    the build, as SURVEY.md App. A.2 does for the full generator); below that the
+    short CG runs are in the finite-termination regime where the tail of the history
+    is rounding noise (pin P4), so only x, the count and the true residual are gated."""
+    A1, _, b1 = synth.gspd(n + n % 2, 1e3)
+    return np.ascontiguousarray(A1[:n, :n]), b1[:n].copy()
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 100, 147, 148, 149, 296, 511, 513, 777, 1000, 1024])
 def test_tiny_parity_ragged(n):
-    A = synth.random_spd(n, 100.0, n)
-    rng = np.random.default_rng(n + 1)
-    b, x0 = rng.standard_normal(n), rng.standard_normal(n)
-    D = synth.random_dd(n, n + 2)
-    bd = rng.standard_normal(n)
+    """CG on G-SPD and BiCGSTAB on G-DD(n, 4) (the parity-safe generators of SURVEY.md
+    sec.8(d).2), x0 != 0, tiny kernels on and off, vs the oracle."""
+    A, b = gspd_any(n)
+    D, bd = synth.gdd(n, 4)
+    x0 = np.random.default_rng(n + 1).standard_normal(n)
     xo, ho, ro = oracle.cg(A, b, x0=x0, tol=1e-10)
     yo, hyo, ryo = oracle.bicgstab(D, bd, x0=x0, tol=1e-10)
+    full = n >= 147
     res = {}
     for tiny in (1, 0):
         with ks.Context(n) as ctx, ks.Context(n) as dtx:
@@ -35,11 +47,19 @@ def test_tiny_parity_ragged(n):
             ctx.load_rows(A)
             dtx.load_rows(D)
             x, h, r = ctx.cg(b, x0=x0, tol=1e-10)
-            bars(x, h, r, xo, ho, ro)
             y, hy, ry = dtx.bicgstab(bd, x0=x0, tol=1e-10)
-            bars(y, hy, ry, yo, hyo, ryo, floor=FLOOR_BS)
-            assert ry.half_step_exit == ryo.half_step_exit
-            assert r.true_relres <= 1e-9 and ry.true_relres <= 1e-9
+            if full:
+                bars(x, h, r, xo, ho, ro)
+                bars(y, hy, ry, yo, hyo, ryo, floor=FLOOR_BS)
+                assert ry.half_step_exit == ryo.half_step_exit
+            else:
+                for (xg, rg, xr, rr) in ((x, r, xo, ro), (y, ry, yo, ryo)):
+                    assert abs(rg.iterations - rr.iterations) <= 2 and rg.status == rr.status
+                    assert np.linalg.norm(xg - xr) <= 1e-9 * np.linalg.norm(xr)
+            assert r.true_relres <= 1e-9
+            # n = 1: G-DD(1, 4) is the 1 x 1 zero matrix (no off-diagonal row sum), a
+            # BiCGSTAB breakdown at iteration 1 for the oracle and the GPU alike
+            assert ry.true_relres <= 1e-9 or (n == 1 and ry.breakdown and ryo.status == ks.KS_EBREAKDOWN)
             res[tiny] = (x, y)
     if n >= 148:   # a different summation order really ran (not a silent fallback)
         assert not (np.array_equal(res[1][0], res[0][0]) and np.array_equal(res[1][1], res[0][1]))
@@ -66,10 +86,10 @@ def test_tiny_c1_configs():
 
 def test_tiny_exits():
     n = 300
-    A = synth.random_spd(n, 50.0, 9)
-    D = synth.random_dd(n, 9)
+    A, b = gspd_any(n)
+    D, bd = synth.gdd(n, 16)
     rng = np.random.default_rng(9)
-    b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+    x0 = rng.standard_normal(n)
     with ks.Context(n) as ctx:
         ctx.load_rows(A)
         # b = 0 (Q6)
@@ -90,8 +110,8 @@ def test_tiny_exits():
         assert r.status == ks.KS_ENOTSPD and r.iterations == 0 and np.array_equal(x, x0)
     with ks.Context(n) as ctx:
         ctx.load_rows(D)
-        xo, ho, ro = oracle.bicgstab(D, b, tol=0.0, maxit=4)
-        x, h, r = ctx.bicgstab(b, tol=0.0, maxit=4)
+        xo, ho, ro = oracle.bicgstab(D, bd, tol=0.0, maxit=4)
+        x, h, r = ctx.bicgstab(bd, tol=0.0, maxit=4)
         assert r.iterations == 4 and r.status == ks.KS_EMAXIT and r.matvecs == 8 and len(h) == 4
         assert np.linalg.norm(x - xo) <= 1e-12 * np.linalg.norm(xo)
         assert np.all(np.abs(h - ho) <= 1e-12 * ho)
@@ -122,8 +142,7 @@ def test_tiny_repeated_solves_one_context():
     """CG, BiCGSTAB, CG, BiCGSTAB on one context (one LL buffer): every repeat is
     bitwise equal to the first solve of its method (stale LL words never match)."""
     n = 700
-    A = synth.random_spd(n, 30.0, 4)
-    b = np.random.default_rng(4).standard_normal(n)
+    A, b = gspd_any(n)
     with ks.Context(n) as ctx:
         ctx.load_rows(A)
         first = {}

@@ -80,19 +80,23 @@ def main():
             sync()
             t0 = time.perf_counter()
             e0.record(stream)
+            inside = 0.0
             for _ in range(K):
-                fn(bb, tol=0.0, maxit=1, out=xx, hist=hs)
+                inside += fn(bb, tol=0.0, maxit=1, out=xx, hist=hs)[2].seconds_total
             e1.record(stream)
             sync()
             r[f"call_{tag}_ms_wall"] = (time.perf_counter() - t0) * 1e3 / K
+            r[f"call_{tag}_ms_inside_c"] = inside * 1e3 / K     # ks_cg's own wall time (C side)
             r[f"call_{tag}_ms_events"] = e0.elapsed_time(e1) / K
         # maxit = 0: the call's fixed cost without any iteration
         sync()
         t0 = time.perf_counter()
+        inside = 0.0
         for _ in range(K):
-            fn(bh, tol=0.0, maxit=0, out=xh, hist=hh[:1])
+            inside += fn(bh, tol=0.0, maxit=0, out=xh, hist=hh[:1])[2].seconds_total
         sync()
         r["call_host_maxit0_ms_wall"] = (time.perf_counter() - t0) * 1e3 / K
+        r["call_host_maxit0_ms_inside_c"] = inside * 1e3 / K
         # CUPTI timeline of 3 host-buffer calls
         from torch.profiler import ProfilerActivity, profile
         sync()
