@@ -240,6 +240,21 @@ ks_status ks_bicg(ks_ctx* ctx, const double* b, const double* x0, double tol, in
 ks_status ks_gmres(ks_ctx* ctx, const double* b, const double* x0, double tol, int32_t restart,
                    int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep);
 
+/* Multi-RHS CG (SURVEY.md sec.8(f) "multi-RHS"; reading Q30): nrhs
+ * (1..8) independent CG recurrences of sec.8(c).3 -- column k is exactly the CG of
+ * ks_cg on (A, b_k): its own alpha, beta, stopping test and NOTSPD exit -- sharing
+ * every pass over A: each iteration is ONE skinny GEMM Q = A P (TMA-fed, FP64), so
+ * the HBM bytes per iteration are those of a single GEMV.  Converged columns stop
+ * updating; the solve ends when every column has stopped or after maxit.
+ * B, X: n x nrhs, column-major (column k at B + k*n), required; X0: same or NULL
+ * (zero start).  hist: NULL or hist_cap x nrhs column-major (column k at
+ * hist + k*hist_cap), receives min(iterations_k, hist_cap) values ||r||/||b_k||.
+ * reps: NULL or nrhs reports (true_relres -1: not computed).  One GPU (P == 1),
+ * FP64 contexts only (else KS_EARG).  Returns the worst column status:
+ * KS_ENOTSPD > KS_EMAXIT > KS_OK.                                                 */
+ks_status ks_cg_multi(ks_ctx* ctx, int32_t nrhs, const double* B, const double* X0, double tol, int64_t maxit,
+                      double* X, double* hist, int64_t hist_cap, ks_report* reps);
+
 /* y = A^T x (n doubles each): the transposed GEMV building block of BiCG (K1T). */
 ks_status ks_matvec_t(ks_ctx* ctx, const double* x, double* y);
 

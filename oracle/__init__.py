@@ -244,6 +244,26 @@ def bicgstab(A, b, x0=None, tol=1e-8, maxit=None, trace: int = 0):
     return out
 
 
+def cg_multi(A, B, X0=None, tol=1e-8, maxit=None):
+    """Multi-RHS CG (SURVEY.md sec.8(f) "multi-RHS"; reading Q30): column k
+    of the n x nrhs block B is solved by the CG of sec.8(c).3 on (A, B[:, k]) with its
+    own scalars and stopping test -- exactly ``cg`` per column (the GPU shares the
+    passes over A between the columns; the recurrences are independent).  Returns
+    (X n x nrhs, [hist_k], [report_k])."""
+    B = np.asarray(B, dtype=np.float64)
+    if B.ndim != 2:
+        raise ValueError("B must be n x nrhs")
+    X = np.empty_like(B)
+    hs, reps = [], []
+    for k in range(B.shape[1]):
+        x0 = None if X0 is None else np.asarray(X0, dtype=np.float64)[:, k]
+        x, h, r = cg(A, B[:, k], x0=x0, tol=tol, maxit=maxit)
+        X[:, k] = x
+        hs.append(h)
+        reps.append(r)
+    return X, hs, reps
+
+
 def gemv_t(A, x) -> np.ndarray:
     """y = A^T x for row-major A (sequential sums over rows)."""
     A = np.ascontiguousarray(A, dtype=np.float64)

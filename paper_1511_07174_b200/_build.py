@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build", "ks")
 LIB = os.path.join(HERE, "libks.so")
 
-SOURCES = ["ks_gemv.cu", "ks_vec.cu", "ks_gen.cu", "ks_persist.cu", "ks_small.cu", "ks_tiny.cu", "ks_gmres.cu", "ks_gmres_persist.cu", "ks_f32.cu", "ks_alloc.cpp", "ks_ctx.cpp", "ks_solvers.cpp", "ks_abi.cpp"]
+SOURCES = ["ks_gemv.cu", "ks_vec.cu", "ks_gen.cu", "ks_persist.cu", "ks_small.cu", "ks_tiny.cu", "ks_multi.cu", "ks_gmres.cu", "ks_gmres_persist.cu", "ks_f32.cu", "ks_alloc.cpp", "ks_ctx.cpp", "ks_solvers.cpp", "ks_abi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

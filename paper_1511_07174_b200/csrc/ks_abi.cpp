@@ -458,6 +458,38 @@ ks_status ks_gmres(ks_ctx* c, const double* b, const double* x0, double tol, int
     return s;
 }
 
+ks_status ks_cg_multi(ks_ctx* c, int32_t nrhs, const double* B, const double* X0, double tol, int64_t maxit,
+                      double* X, double* hist, int64_t hist_cap, ks_report* reps) {
+    if (!c) return fail(nullptr, KS_EARG, "ctx is NULL");
+    if (!B || !X) return fail(c, KS_EARG, "B and X are required");
+    if (nrhs < 1 || nrhs > ks::kMaxRhs) return fail(c, KS_EARG, "nrhs must be in [1, 8]");
+    if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "multi-RHS CG is FP64-only");
+    if (c->P != 1) return fail(c, KS_EARG, "multi-RHS CG runs on one GPU (P == 1)");
+    if (!(tol >= 0.0)) return fail(c, KS_EARG, "tol must be >= 0");
+    if (maxit < 0) return fail(c, KS_EARG, "maxit must be >= 0");
+    if (hist_cap < 0 || (hist_cap > 0 && !hist)) return fail(c, KS_EARG, "bad hist/hist_cap");
+    if (!hist) hist_cap = 0;
+    if (c->poisoned) return fail(c, KS_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    if (!all_loaded(c)) return fail(c, KS_ESTATE, "matrix not fully loaded: call ks_load_rows / ks_generate first");
+    int64_t stat = 0;
+    ks_status st = guarded(c, [&] {
+        c->for_each_rank([&](Rank& r) {
+            stat = ks::run_cg_multi(c, r, nrhs, B, X0, tol, maxit, X, hist, hist_cap, reps);
+            KS_CUDA(cudaGetLastError());
+        });
+        return KS_OK;
+    });
+    if (st != KS_OK) return st;
+    const ks_status s = status_of(stat);
+    if (s != KS_OK) {
+        const char* what = s == KS_EMAXIT ? "maximum iterations reached (some column)"
+                                          : "CG: <p, A p> <= 0 in some column (matrix not SPD)";
+        c->last_error = what;
+        g_tls_error = what;
+    }
+    return s;
+}
+
 ks_status ks_matvec_t(ks_ctx* c, const double* x, double* y) {
     if (!c || !x || !y) return fail(c, KS_EARG, "NULL argument");
     if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "ks_matvec_t is FP64-only");

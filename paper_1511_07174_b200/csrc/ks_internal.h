@@ -281,6 +281,35 @@ int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld);
 int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll, int grid,
                 cudaStream_t st);
 
+// Multi-RHS CG (ks_multi.cu, SURVEY.md sec.8(f) "multi-RHS"): K <= kMaxRhs independent
+// CG recurrences sharing every pass over A (one GPU, FP64).  Per-column state:
+struct MultiCol {
+    double nb, rho, relres;
+    long long iters;
+    int status, active, converged, bzero;
+};
+constexpr int kMaxRhs = 8;
+struct MultiState { MultiCol col[kMaxRhs]; };
+struct MultiArgs {
+    int nrhs, has_x0;
+    int64_t n, m, ld, ldm, row0;   // ldm: stride of the K rows of X, R, Q; ld: of P
+    double tol;
+    long long maxit;
+    double* X;                     // K x ldm: x (own rows)
+    double* R;                     // K x ldm: b on entry, then r
+    double* Q;                     // K x ldm: A p
+    double* Pf;                    // K x ld: p (full length); x0 on entry when has_x0
+    double* hist;                  // K x hist_cap (column k at hist + k * hist_cap), nullable
+    int64_t hist_cap;
+    MultiState* ms;
+    DevState* st;                  // error reporting (grid-barrier timeout)
+    double* bpart;                 // gridDim.x x 2K CTA partials
+    unsigned* bar;                 // grid-barrier counter (zeroed by the launcher)
+};
+int multi_k(int nrhs);             // kernel width K for nrhs columns (0: unsupported)
+int multi_grid(int K, int num_sms);
+int launch_cg_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st);
+
 // NEXT-4 (FP32) support kernels (ks_f32.cu): K1 in FP32, setup/init/finish in
 // FP32, conversions at the FP64 ABI boundary, FP32 generators.
 int launch_gemv_f32(const GemvParamsT<float>& p, const Scratch& s, int ticket_id, cudaStream_t st);

@@ -1,0 +1,430 @@
+// Multi-RHS CG ("multi-RHS": with K right-hand sides the GEMV
+// becomes a skinny GEMM, Q = A P with P n x K).  K independent CG recurrences
+// (sec.8(c).3 per column: own alpha, beta, stopping test, NOTSPD exit; DESIGN.md
+// reading Q30) share every pass over A, so one HBM stream of A serves K iterations:
+// K/4 flop per byte instead of 1/4.  FP64 on the CUDA cores -- B200's FP64 tensor
+// path is no faster than the FP64 pipes, and at K <= 8 the GEMM stays HBM-bound.
+//
+// One persistent cooperative kernel per solve (one GPU), one CTA per SM, 8 consumer
+// warps + 1 TMA producer warp:
+//   * A is cut into bands of kMB = 32 rows (round-robin over the CTAs) and chunks of
+//     kMC = 128 columns; a stage = the A tile (32 x 128, 32 KiB) + the matching P tile
+//     (K x 128), both brought into shared memory by 2-D TMA loads
+//     (cp.async.bulk.tensor, tensor maps built on the host) completing on a
+//     full-mbarrier; kMS stages in flight; consumers release a stage through an
+//     empty-mbarrier (one arrival per warp);
+//   * consumer warp w owns rows 4w..4w+3 of the band, lane l the column pairs
+//     2l and 64 + 2l of each chunk: 4 x K accumulators per thread, the P pair loaded
+//     once per column pair and reused for the 4 rows (shared-memory traffic ~3x the
+//     A bytes at K = 8, conflict-free 512-byte rows);
+//   * at the end of a band the 32 lanes' partials are summed by a butterfly; lane 0
+//     writes q and accumulates sigma_k = <p_k, q_k> over its rows;
+//   * the O(n) phases (alpha, x, r, rho', beta, p per column) run between grid
+//     barriers as in the single-RHS persistent kernel; every sum is fixed-order.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ks_device.cuh"
+#include "ks_common.cuh"
+#include "ks_internal.h"
+#include "ks_persist.cuh"
+#include "ks_tma.cuh"
+
+namespace ks {
+
+namespace {
+
+constexpr int kMB = 32;                   // rows per band
+constexpr int kMC = 128;                  // columns per chunk
+constexpr int kMS = 4;                    // pipeline stages
+constexpr int kMW = 8;                    // consumer warps
+constexpr int kMT = (kMW + 1) * 32;       // + the producer warp
+constexpr int kMCT = kMW * 32;            // consumer threads
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Sum over the consumer threads of K values (fixed tree), result in every consumer
+// thread; the producer warp takes part in the barriers only.
+template <int K>
+__device__ __forceinline__ void csum(double (&v)[K], double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+    __syncthreads();
+    if (lane == 0 && w < kMW) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) red[k * kMW + w] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double t = lane < kMW ? red[k * kMW + lane] : 0.0;
+        v[k] = warp_sum(t);
+    }
+}
+
+template <int K>
+struct MultiSmem {
+    double A[kMS][kMB * kMC];
+    double P[kMS][K * kMC];
+    uint64_t full[kMS], empty[kMS];
+    double red[2 * K * kMW];
+    double wpart[kMW][K];
+};
+
+// Q = A P (this CTA's bands) and sigma partials <P_k, Q_k> over the CTA's rows in
+// band order.  `it` is the pipeline position, identical in producer and consumers.
+template <int K>
+__device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const MultiArgs& M, MultiSmem<K>& S,
+                           uint32_t& it, double (&sig)[K]) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nbands = (int)((M.m + kMB - 1) / kMB);
+    const int nchunks = (int)(M.ld / kMC);
+#pragma unroll
+    for (int k = 0; k < K; ++k) sig[k] = 0.0;
+    if (w == kMW) {                                        // ---- TMA producer warp
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // P written by the generic proxy
+            const uint32_t bytes = (uint32_t)(kMB * kMC + K * kMC) * sizeof(double);
+            for (int b = blockIdx.x; b < nbands; b += gridDim.x) {
+                for (int c = 0; c < nchunks; ++c, ++it) {
+                    const int s = (int)(it % kMS);
+                    const uint32_t ph = (it / kMS) & 1u;
+                    mbar_wait(&S.empty[s], ph ^ 1u);
+                    mbar_expect_tx(&S.full[s], bytes);
+                    tma_load_2d(S.A[s], tmA, c * kMC, b * kMB, &S.full[s]);
+                    tma_load_2d(S.P[s], tmP, c * kMC, 0, &S.full[s]);
+                }
+            }
+        } else {
+            for (int b = blockIdx.x; b < nbands; b += gridDim.x) it += (uint32_t)nchunks;
+        }
+        return;
+    }
+    for (int b = blockIdx.x; b < nbands; b += gridDim.x) {  // ---- consumer warps
+        double acc[4][K];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[rr][k] = 0.0;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+            const int s = (int)(it % kMS);
+            const uint32_t ph = (it / kMS) & 1u;
+            mbar_wait(&S.full[s], ph);
+            const double* At = S.A[s] + (4 * w) * kMC + 2 * lane;
+            const double* Pt = S.P[s] + 2 * lane;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                double2 p[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) p[k] = *reinterpret_cast<const double2*>(Pt + k * kMC + 64 * u);
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    const double2 a = *reinterpret_cast<const double2*>(At + rr * kMC + 64 * u);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        acc[rr][k] = fma(a.x, p[k].x, acc[rr][k]);
+                        acc[rr][k] = fma(a.y, p[k].y, acc[rr][k]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[s]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[rr][k] = warp_sum(acc[rr][k]);
+        if (lane == 0) {
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const int64_t row = (int64_t)b * kMB + 4 * w + rr;
+                if (row < M.m) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        M.Q[k * M.ldm + row] = acc[rr][k];
+                        sig[k] = fma(M.Pf[k * M.ld + M.row0 + row], acc[rr][k], sig[k]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// CTA-order totals of K partial slots (q0 .. q0 + K - 1 of kSlotsM per CTA).
+template <int K>
+__device__ __forceinline__ void totals(const double* bpart, int q0, double (&out)[K], double* red) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double acc = 0.0;
+        if (threadIdx.x < kMCT)
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += kMCT) acc += __ldcg(bpart + (int64_t)b * 2 * K + q0 + k);
+        out[k] = acc;
+    }
+    csum<K>(out, red);
+}
+
+template <int K>
+__global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensorMap tmA,
+                                               const __grid_constant__ CUtensorMap tmP, MultiArgs M) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    MultiSmem<K>& S = *reinterpret_cast<MultiSmem<K>*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    MultiState* ms = M.ms;
+    DevState* st = M.st;
+    const int tid = threadIdx.x;
+    const bool cons = tid < kMCT;
+    const int64_t gs = (int64_t)gridDim.x * kMCT;
+    const int64_t t0 = (int64_t)blockIdx.x * kMCT + tid;
+    const int64_t m = M.m;
+    if (tid == 0) {
+        for (int s = 0; s < kMS; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kMW); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid == kMW * 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmP) : "memory");
+    }
+    __syncthreads();
+    uint32_t it = 0;
+    double sig[K];
+    // ---- setup (row A0 per column): r0 = b - A x0 (or b), x = x0 (or 0), p = r0,
+    // nb = ||b||, rho0 = <r0, r0>, the 0-iteration exits (Q2, Q6)
+    if (M.has_x0) {                        // P holds x0 (host copy): Q = A x0
+        gemm_phase<K>(&tmA, &tmP, M, S, it, sig);
+        if (!pk::grid_sync(M.bar, st)) return;   // every CTA's rows of Q before they are read
+    }
+    {
+        double v[2 * K];
+#pragma unroll
+        for (int k = 0; k < 2 * K; ++k) v[k] = 0.0;
+        if (cons) {
+            for (int64_t i = t0; i < m; i += gs) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const double bk = M.R[k * M.ldm + i];          // the host put b here
+                    const double r = M.has_x0 ? bk - M.Q[k * M.ldm + i] : bk;
+                    v[k] = fma(bk, bk, v[k]);
+                    v[K + k] = fma(r, r, v[K + k]);
+                }
+            }
+        }
+        csum<2 * K>(v, S.red);
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v[k];
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        double tb[K], tr[K];
+        totals<K>(M.bpart, 0, tb, S.red);
+        totals<K>(M.bpart, K, tr, S.red);
+        if (cons) {
+            for (int64_t i = t0; i < m; i += gs) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    double r = M.R[k * M.ldm + i];
+                    if (M.has_x0) {
+                        r -= M.Q[k * M.ldm + i];
+                        M.X[k * M.ldm + i] = M.Pf[k * M.ld + i];       // x = x0
+                        M.R[k * M.ldm + i] = r;
+                    } else {
+                        M.X[k * M.ldm + i] = 0.0;
+                    }
+                    const bool z = !(k < M.nrhs) || tb[k] == 0.0;
+                    if (z) { M.X[k * M.ldm + i] = 0.0; M.R[k * M.ldm + i] = 0.0; r = 0.0; }
+                    M.Pf[k * M.ld + i] = r;                            // p0 = r0 (P = 1: full length)
+                }
+            }
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+            for (int k = 0; k < K; ++k) {
+                MultiCol& cl = ms->col[k];
+                cl.nb = sqrt(tb[k]);
+                cl.rho = tr[k];
+                cl.iters = 0;
+                cl.relres = 0.0;
+                cl.status = KS_EMAXIT;
+                cl.active = 1;
+                if (k >= M.nrhs || tb[k] == 0.0) {               // padding column / Q6: b = 0
+                    cl.active = 0; cl.status = KS_OK; cl.converged = 1; cl.bzero = 1;
+                } else {
+                    cl.converged = 0; cl.bzero = 0;
+                    cl.relres = sqrt(tr[k]) / cl.nb;
+                    if (cl.relres <= M.tol) { cl.active = 0; cl.status = KS_OK; cl.converged = 1; }   // Q2
+                }
+            }
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+    }
+    // ---- iterations (rows A1-A5 per column)
+    for (long long k1 = 1; k1 <= M.maxit; ++k1) {
+        int act[K];
+        int any = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) { act[k] = *(volatile const int*)&ms->col[k].active; any |= act[k]; }
+        if (!any) break;
+        // A1: Q = A P, sigma partials
+        gemm_phase<K>(&tmA, &tmP, M, S, it, sig);
+        __syncthreads();
+        if ((tid & 31) == 0 && tid < kMCT) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) S.wpart[tid >> 5][k] = sig[k];
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int ww = 0; ww < kMW; ++ww) s += S.wpart[ww][k];
+                M.bpart[(int64_t)blockIdx.x * 2 * K + k] = s;
+            }
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        // A2: sigma, alpha (per active column; NOTSPD ends that column, x unchanged)
+        double sg[K], alpha[K], rho[K];
+        totals<K>(M.bpart, 0, sg, S.red);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            rho[k] = *(volatile const double*)&ms->col[k].rho;
+            if (act[k] && !(sg[k] > 0.0)) {
+                act[k] = 0;
+                if (blockIdx.x == 0 && tid == 0) {
+                    ms->col[k].active = 0; ms->col[k].status = KS_ENOTSPD; ms->col[k].iters = k1 - 1;
+                }
+            }
+            alpha[k] = act[k] ? rho[k] / sg[k] : 0.0;
+        }
+        // A3: x += alpha p; r -= alpha q; rho' partials
+        double rr[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) rr[k] = 0.0;
+        if (cons) {
+            for (int64_t i = t0; i < m; i += gs) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (!act[k]) continue;
+                    const double pk_ = M.Pf[k * M.ld + M.row0 + i];
+                    M.X[k * M.ldm + i] = fma(alpha[k], pk_, M.X[k * M.ldm + i]);
+                    const double r = fma(-alpha[k], M.Q[k * M.ldm + i], M.R[k * M.ldm + i]);
+                    M.R[k * M.ldm + i] = r;
+                    rr[k] = fma(r, r, rr[k]);
+                }
+            }
+        }
+        csum<K>(rr, S.red);
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + K + k] = rr[k];
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        // A5: test, beta, p = r + beta p
+        double rho1[K], beta[K];
+        totals<K>(M.bpart, K, rho1, S.red);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            beta[k] = 0.0;
+            if (!act[k]) continue;
+            const double rel = sqrt(rho1[k]) / ms->col[k].nb;
+            if (blockIdx.x == 0 && tid == 0) {
+                MultiCol& cl = ms->col[k];
+                if (M.hist && k1 - 1 < M.hist_cap) M.hist[(int64_t)k * M.hist_cap + (k1 - 1)] = rel;
+                cl.relres = rel; cl.iters = k1;
+            }
+            if (rel <= M.tol) {
+                act[k] = 0;
+                if (blockIdx.x == 0 && tid == 0) { ms->col[k].active = 0; ms->col[k].status = KS_OK; ms->col[k].converged = 1; }
+                continue;
+            }
+            beta[k] = rho1[k] / rho[k];
+        }
+        if (cons) {
+            for (int64_t j = t0; j < M.n; j += gs) {
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (act[k]) M.Pf[k * M.ld + j] = fma(beta[k], M.Pf[k * M.ld + j], M.R[k * M.ldm + j]);
+            }
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) if (act[k]) ms->col[k].rho = rho1[k];
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+    }
+}
+
+template <int K>
+const void* kern_m() { return (const void*)k_cgm<K>; }
+size_t smem_m(int K) {
+    const size_t b = K <= 4 ? sizeof(MultiSmem<4>) : sizeof(MultiSmem<8>);
+    return b + 1024;
+}
+
+}  // namespace
+
+int multi_k(int nrhs) { return nrhs <= 4 ? 4 : nrhs <= 8 ? 8 : 0; }
+
+int multi_grid(int K, int num_sms) {
+    const void* k = K == 4 ? kern_m<4>() : kern_m<8>();
+    const size_t sm = smem_m(K);
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+    if (sm > (size_t)optin) return 0;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return 0; }
+    const int dyn_max = optin - (int)fa.sharedSizeBytes;     // opt-in limit minus static smem
+    if ((size_t)dyn_max < sm ||
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kMT, sm);
+    if (per_sm < 1) return 0;
+    return num_sms;
+}
+
+// 2-D tensor map of a row-major FP64 matrix (rows x cols, leading dimension ld
+// elements), box = box_rows x box_cols, zero fill out of bounds.
+static bool make_map(CUtensorMap* tm, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                     int box_cols) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return false;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int launch_cg_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st) {
+    CUtensorMap tmA, tmP;
+    if (!make_map(&tmA, A, M.m, M.ld, M.ld, kMB, kMC)) return -(int)cudaErrorInvalidValue;
+    if (!make_map(&tmP, M.Pf, K, M.ld, M.ld, K, kMC)) return -(int)cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(M.bar, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return -(int)e;
+    MultiArgs Mc = M;
+    void* args[] = {&tmA, &tmP, &Mc};
+    e = cudaLaunchCooperativeKernel(K == 4 ? kern_m<4>() : kern_m<8>(), dim3((unsigned)grid), dim3(kMT), args,
+                                    smem_m(K), st);
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+}  // namespace ks

@@ -637,7 +637,14 @@ int small_grid(int kind, int num_sms, int64_t rows, int64_t ncols) {
     const void* k = kern<T>(kind);
     // the attribute is per function (shared by every context on the device): allow the
     // device maximum, so a launch of any context's size stays valid after a memo hit
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) return 0;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return 0; }
+    const int dyn_max = optin - (int)fa.sharedSizeBytes;     // opt-in limit minus static smem
+    if ((size_t)dyn_max < sm ||
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kNT, sm);
     if (per_sm < 1) return 0;

@@ -812,4 +812,106 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
     return r.h_state->status;
 }
 
+// Multi-RHS CG (ks_multi.cu): nrhs <= 8 independent CG
+// recurrences sharing every pass over A, one persistent launch per solve; one GPU.
+// B, X0, X: n x nrhs column-major (column k at + k n); hist: hist_cap x nrhs
+// column-major; reps: nrhs reports.  Returns the worst column status
+// (ENOTSPD > EMAXIT > OK).
+int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double* X0, double tol, int64_t maxit,
+                     double* X, double* hist, int64_t hist_cap, ks_report* reps) {
+    const auto t_start = Clock::now();
+    check_loaded(c, r);
+    const int K = multi_k(nrhs);
+    const int64_t n = c->n, ld = c->ld, ldm = (r.m + 63) / 64 * 64;
+    if (K != r.mK) {
+        for (double* p : {r.mX, r.mR, r.mQ, r.mP}) dev_free(p);
+        dev_alloc_t(&r.mX, (size_t)(K * ldm));
+        dev_alloc_t(&r.mR, (size_t)(K * ldm));
+        dev_alloc_t(&r.mQ, (size_t)(K * ldm));
+        dev_alloc_t(&r.mP, (size_t)(K * ld));
+        if (!r.mstate) dev_alloc_t(&r.mstate, 1);
+        r.mK = K;
+    }
+    const int64_t hc = hist ? hist_cap : 0;
+    if (hc > 0 && hc * K > r.mhist_cap) {
+        dev_free(r.mhist);
+        r.mhist = nullptr;
+        r.mhist_cap = hc * K;
+        dev_alloc_t(&r.mhist, (size_t)r.mhist_cap);
+    }
+    const size_t e = sizeof(double);
+    // b -> R (K rows of stride ldm), padding rows zero; x0 -> P; P zero elsewhere
+    KS_CUDA(cudaMemsetAsync(r.mR, 0, (size_t)(K * ldm) * e, r.stream));
+    KS_CUDA(cudaMemsetAsync(r.mP, 0, (size_t)(K * ld) * e, r.stream));
+    KS_CUDA(cudaMemcpy2DAsync(r.mR, (size_t)ldm * e, B, (size_t)n * e, (size_t)n * e, (size_t)nrhs,
+                              cudaMemcpyDefault, r.stream));
+    if (X0)
+        KS_CUDA(cudaMemcpy2DAsync(r.mP, (size_t)ld * e, X0, (size_t)n * e, (size_t)n * e, (size_t)nrhs,
+                                  cudaMemcpyDefault, r.stream));
+    MultiArgs M{};
+    M.nrhs = nrhs;
+    M.has_x0 = X0 ? 1 : 0;
+    M.n = n;
+    M.m = r.m;
+    M.ld = ld;
+    M.ldm = ldm;
+    M.row0 = r.row0;
+    M.tol = tol;
+    M.maxit = maxit;
+    M.X = r.mX;
+    M.R = r.mR;
+    M.Q = r.mQ;
+    M.Pf = r.mP;
+    M.hist = hc > 0 ? r.mhist : nullptr;
+    M.hist_cap = hc;
+    M.ms = r.mstate;
+    M.st = r.st;
+    M.bpart = r.scr.part + 2 * kPartStride;
+    M.bar = r.scr.ticket + 8;
+    const int grid = memo_grid(r, (5LL << 48) | K, [&] { return multi_grid(K, r.num_sms); });
+    if (grid <= 0) throw KsError(KS_ECUDA, "multi-RHS kernel does not fit this device");
+    KS_CUDA(cudaMemsetAsync(&r.st->peer_timeout, 0, sizeof(int), r.stream));
+    KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+    const int rc = launch_cg_multi(K, M, r.A, grid, r.stream);
+    if (rc < 0) KS_CUDA((cudaError_t)(-rc));
+    KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    // out: X columns, state, histories -- one synchronisation
+    MultiState hs;
+    KS_CUDA(cudaMemcpy2DAsync(X, (size_t)n * e, r.mX, (size_t)ldm * e, (size_t)n * e, (size_t)nrhs,
+                              cudaMemcpyDefault, r.stream));
+    KS_CUDA(cudaMemcpyAsync(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost, r.stream));
+    KS_CUDA(cudaMemcpyAsync(&hs, r.mstate, sizeof(MultiState), cudaMemcpyDeviceToHost, r.stream));
+    const int64_t nh = std::min<int64_t>(hc, maxit);
+    if (nh > 0)
+        KS_CUDA(cudaMemcpy2DAsync(hist, (size_t)hist_cap * e, r.mhist, (size_t)hc * e, (size_t)nh * e,
+                                  (size_t)nrhs, cudaMemcpyDefault, r.stream));
+    KS_CUDA(cudaStreamSynchronize(r.stream));
+    if (r.h_state->peer_timeout) throw KsError(KS_ECUDA, "multi-RHS kernel: grid barrier timed out");
+    float ms = 0.f;
+    KS_CUDA(cudaEventElapsedTime(&ms, r.ev_t0, r.ev_t1));
+    int64_t worst = KS_OK;
+    for (int k = 0; k < nrhs; ++k) {
+        const MultiCol& cl = hs.col[k];
+        const int64_t stt = cl.active ? (int64_t)KS_EMAXIT : (int64_t)cl.status;
+        if (stt == KS_ENOTSPD) worst = KS_ENOTSPD;
+        else if (stt == KS_EMAXIT && worst == KS_OK) worst = KS_EMAXIT;
+        if (reps) {
+            ks_report R;
+            std::memset(&R, 0, sizeof R);
+            R.iterations = cl.active ? maxit : cl.iters;
+            R.matvecs = R.iterations;
+            R.converged = cl.converged;
+            R.status = (int32_t)stt;
+            R.relres = cl.bzero ? 0.0 : cl.relres;
+            R.true_relres = -1.0;
+            R.seconds_loop = ms * 1e-3;
+            R.seconds_total = std::chrono::duration<double>(Clock::now() - t_start).count();
+            R.gemv_launches = hs.col[0].iters;
+            R.kernel_launches = 1;
+            reps[k] = R;
+        }
+    }
+    return worst;
+}
+
 }  // namespace ks

@@ -101,13 +101,69 @@ __device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t 
     }
 }
 
-// Block sum of K values (fixed tree; every thread gets the same bits).
+// Block sum of K values (fixed tree; every thread gets the same bits): butterfly in
+// each warp, warp sums through shared memory, each thread adds the kTW warp sums in
+// warp order.  ONE __syncthreads: `red` holds two buffers used alternately (a thread
+// rewrites buffer b only after the barrier of the call in between, which every
+// thread reaches after reading b), `par` toggles per call.
 template <int K>
-__device__ __forceinline__ void tsum(double (&v)[K], double* red) { block_sum<kTT, K>(v, red); }
+__device__ __forceinline__ void tsum(double (&v)[K], double* red, int& par) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    static_assert(K <= 2, "red holds two buffers of 2 * kTW");
+    double* rb = red + par * (2 * kTW);     // fixed stride: calls of different K alternate safely
+    par ^= 1;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) rb[k * kTW + w] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < kTW; ++ww) t += rb[k * kTW + ww];
+        v[k] = t;
+    }
+}
+
+// Warp sums of kRM = 8 per-thread row partials in 9 shuffles (transpose reduction):
+// three halving exchanges (16, 8, 4) leave lane l one row, (l >> 2) & 7 in bit-reversed
+// order below, then two butterfly steps (2, 1).  Returns the row sum and its row.
+__device__ __forceinline__ double warp_rows8(double (&a)[kRM], int& row) {
+    const int lane = threadIdx.x & 31;
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    double v4[4], v2[2], v1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? a[i] : a[i + 4];
+        const double keep = b4 ? a[i + 4] : a[i];
+        v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? v4[i] : v4[i + 2];
+        const double keep = b3 ? v4[i + 2] : v4[i];
+        v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+        const double send = b2 ? v2[0] : v2[1];
+        const double keep = b2 ? v2[1] : v2[0];
+        v1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    row = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+    return v1;
+}
 
 // GEMV rows [0, R) of this CTA's shared-memory block against the register-resident
 // full-length x (this thread's V columns); thread t < R returns row t's sum.
-// Per-thread row partials -> warp butterfly -> warp sums in warp order.
+// Per-thread row partials -> transpose warp reduction -> warp sums in warp order.
 template <int V>
 __device__ __forceinline__ double gemv_rows(const double* As, int64_t ld, int R, const double (&x)[V],
                                             double* wred) {
@@ -126,13 +182,9 @@ __device__ __forceinline__ double gemv_rows(const double* As, int64_t ld, int R,
         }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int i = 0; i < kRM; ++i) {
-        if (i < R) {
-            const double s = warp_sum(acc[i]);
-            if (lane == 0) wred[i * kTW + w] = s;
-        }
-    }
+    int row;
+    const double s = warp_rows8(acc, row);
+    if ((lane & 3) == 0) wred[row * kTW + w] = s;
     __syncthreads();
     double q = 0.0;
     if (threadIdx.x < R) {
@@ -194,8 +246,9 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);
     __shared__ double wred[kRM * kTW];
-    __shared__ double red[kTW];
+    __shared__ double red[2 * 2 * kTW];
     __shared__ __align__(8) uint64_t bar;
+    int par = 0;
     const VecArgs& a = T.a;
     DevState* st = a.st;
     const int n = (int)a.L.n;
@@ -238,7 +291,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
         double s1[1] = {0.0};
 #pragma unroll
         for (int v = 0; v < V; ++v) s1[0] = fma(p[v], q[v], s1[0]);
-        tsum<1>(s1, red);
+        tsum<1>(s1, red, par);
         const double sigma = s1[0];
         stamp(T, k, 3);
         if (!(sigma > 0.0)) { status = KS_ENOTSPD; iters = k - 1; break; }   // Q9: x unchanged
@@ -251,7 +304,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
             r[v] = fma(-alpha, q[v], r[v]);
             s2[0] = fma(r[v], r[v], s2[0]);
         }
-        tsum<1>(s2, red);
+        tsum<1>(s2, red, par);
         const double rho1 = s2[0];
         stamp(T, k, 4);
         const double rel = sqrt(rho1) / nb;
@@ -287,8 +340,9 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);
     __shared__ double wred[kRM * kTW];
-    __shared__ double red[2 * kTW];
+    __shared__ double red[2 * 2 * kTW];
     __shared__ __align__(8) uint64_t bar;
+    int par = 0;
     const VecArgs& a = T.a;
     DevState* st = a.st;
     const int n = (int)a.L.n;
@@ -333,7 +387,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         double g1[1] = {0.0};
 #pragma unroll
         for (int v = 0; v < V; ++v) g1[0] = fma(rh[v], v_[v], g1[0]);
-        tsum<1>(g1, red);
+        tsum<1>(g1, red, par);
         const double gam = g1[0];
         if (gam == 0.0 || !isfinite(gam)) { status = KS_EBREAKDOWN; brk = 1; iters = i - 1; break; }
         alpha = rho / gam;
@@ -344,7 +398,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
             s[v] = fma(-alpha, v_[v], r[v]);
             ss[0] = fma(s[v], s[v], ss[0]);
         }
-        tsum<1>(ss, red);
+        tsum<1>(ss, red, par);
         const double srel = sqrt(ss[0]) / nb;
         if (srel <= tol) {                                     // B5: half-step exit
 #pragma unroll
@@ -369,7 +423,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
             d2[0] = fma(t[v], s[v], d2[0]);
             d2[1] = fma(t[v], t[v], d2[1]);
         }
-        tsum<2>(d2, red);
+        tsum<2>(d2, red, par);
         const double tt = d2[1];
         if (tt == 0.0 || !isfinite(tt)) { status = KS_EBREAKDOWN; brk = 1; iters = i - 1; break; }
         const double om = d2[0] / tt;
@@ -383,7 +437,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
             d3[0] = fma(rh[v], r[v], d3[0]);
             d3[1] = fma(r[v], r[v], d3[1]);
         }
-        tsum<2>(d3, red);
+        tsum<2>(d3, red, par);
         omega = om;
         rho_old = rho;
         rho = d3[0];
@@ -434,7 +488,14 @@ int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld) {
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
     if (sm + 4096 > (size_t)optin) return 0;
     const void* k = kern_v(bicgstab, V);
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) return 0;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return 0; }
+    const int dyn_max = optin - (int)fa.sharedSizeBytes;     // opt-in limit minus static smem
+    if ((size_t)dyn_max < sm ||
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTT, sm);
     if (per_sm < 1) return 0;

@@ -1,0 +1,110 @@
+"""GPU parity of multi-RHS CG (ks_cg_multi: one TMA-fed skinny GEMM per iteration,
+K independent CG recurrences; reading Q30) vs the oracle, column by
+column, at the north-star bars (Q17-Q19).  Inputs: G-SPD (SURVEY.md sec.8(d).2,
+parity-safe: uniform spectrum), K right-hand sides from the sec.8(d).2 hash with
+seeds SEED + k; ragged n (partial 32-row bands, padded 128-column chunks); nrhs
+1..8 (kernel widths 4 and 8 with padding columns); every per-column exit."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+ks = pytest.importorskip("paper_1511_07174_b200")
+
+from test_gpu_parity import bars  # noqa: E402
+
+
+def gspd_any(n, kappa=1e3):
+    A1, _, _ = synth.gspd(n + n % 2, kappa)
+    return np.ascontiguousarray(A1[:n, :n])
+
+
+def rhs_block(n, k):
+    return np.column_stack([synth.rhs(n, synth.SEED + j) for j in range(k)])
+
+
+@pytest.mark.parametrize("n,nrhs", [(1024, 1), (1024, 4), (1000, 3), (2050, 5), (4096, 8), (777, 8)])
+def test_multi_rhs_parity(n, nrhs):
+    A = gspd_any(n)
+    B = rhs_block(n, nrhs)
+    Xo, ho, ro = oracle.cg_multi(A, B, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        X, h, r = ctx.cg_multi(B, tol=1e-10)
+    for k in range(nrhs):
+        bars(X[:, k], h[k], r[k], Xo[:, k], ho[k], ro[k])
+        assert r[k].converged and r[k].status == ks.KS_OK
+
+
+def test_multi_rhs_matches_single_rhs_cg():
+    """Column k of the block solve meets the bars against the single-RHS GPU CG
+    (the same recurrence through K1/the persistent kernels)."""
+    n = 2048
+    A = gspd_any(n, 1e4)
+    B = rhs_block(n, 6)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        X, h, r = ctx.cg_multi(B, tol=1e-10)
+        for k in range(6):
+            x1, h1, r1 = ctx.cg(B[:, k], tol=1e-10)
+            bars(X[:, k], h[k], r[k], x1, h1, r1)
+
+
+def test_multi_rhs_x0_and_exits():
+    n = 600
+    A = gspd_any(n)
+    B = rhs_block(n, 5)
+    B[:, 2] = 0.0                                    # Q6: b = 0 -> x = 0, 0 iterations
+    X0 = np.random.default_rng(3).standard_normal((n, 5))
+    X0[:, 4] = np.linalg.solve(A, B[:, 4])           # (near) exact start: 0-iteration exit
+    Xo, ho, ro = oracle.cg_multi(A, B, X0=X0, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        X, h, r = ctx.cg_multi(B, X0=X0, tol=1e-10)
+        for k in (0, 1, 3):
+            bars(X[:, k], h[k], r[k], Xo[:, k], ho[k], ro[k])
+        assert r[2].iterations == 0 and r[2].converged and np.all(X[:, 2] == 0)
+        assert r[4].iterations == ro[4].iterations == 0 and np.array_equal(X[:, 4], X0[:, 4])
+        # maxit: every column stops at maxit = 6 with the oracle's x after 6 steps
+        Xo6, ho6, _ = oracle.cg_multi(A, B[:, :2], tol=0.0, maxit=6)
+        X6, h6, r6 = ctx.cg_multi(B[:, :2], tol=0.0, maxit=6)
+        for k in range(2):
+            assert r6[k].status == ks.KS_EMAXIT and r6[k].iterations == 6 and len(h6[k]) == 6
+            assert np.linalg.norm(X6[:, k] - Xo6[:, k]) <= 1e-12 * np.linalg.norm(Xo6[:, k])
+        # repeated solve: bitwise identical
+        X2, h2, r2 = ctx.cg_multi(B, X0=X0, tol=1e-10)
+        assert np.array_equal(X2, X) and all(np.array_equal(a, b) for a, b in zip(h, h2))
+
+
+def test_multi_rhs_per_column_notspd():
+    """diag(1..m, -1..-m): a right-hand side in the positive eigenspace converges, one
+    touching the negative eigenspace meets <p, A p> < 0 (NOTSPD for that column only,
+    x = x0); the call returns KS_ENOTSPD (worst column)."""
+    m = 300
+    d = np.concatenate([np.arange(1, m + 1), -np.arange(1, m + 1)]).astype(np.float64)
+    A = np.diag(d)
+    n = 2 * m
+    b0 = np.concatenate([np.ones(m), np.zeros(m)])
+    b1 = np.concatenate([np.zeros(m), np.ones(m)])
+    B = np.column_stack([b0, b1])
+    Xo, ho, ro = oracle.cg_multi(A, B, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        X, h, r = ctx.cg_multi(B, tol=1e-10)
+    assert ro[0].status == ks.KS_OK and r[0].status == ks.KS_OK
+    bars(X[:, 0], h[0], r[0], Xo[:, 0], ho[0], ro[0])
+    assert ro[1].status == r[1].status == ks.KS_ENOTSPD and r[1].iterations == ro[1].iterations == 0
+    assert np.all(X[:, 1] == 0)
+
+
+def test_multi_rhs_argument_errors():
+    n = 64
+    with ks.Context(n) as ctx:
+        ctx.load_rows(np.eye(n))
+        with pytest.raises(ks.KsError) as e:
+            ctx.cg_multi(np.ones((n, 9)))
+        assert e.value.status == ks.KS_EARG
+        X, h, r = ctx.cg_multi(np.ones((n, 2)), tol=1e-12)     # A = I: 1 iteration, x = b
+        assert all(q.iterations == 1 for q in r) and np.allclose(X, 1.0, rtol=0, atol=1e-15)

@@ -1,0 +1,46 @@
+"""Multi-RHS CG throughput (ks_cg_multi) at n = 65536 FP64 on one GPU: for
+nrhs = 1, 2, 4, 8, a fixed-length solve (tol = 0) of `iters` iterations; reports
+iterations/s, right-hand-side-iterations/s and the A-stream GB/s of the TMA-fed
+skinny GEMM (8 n^2 bytes per iteration, algorithmic), next to single-RHS ks_cg.
+
+    python tools/multi_rhs_bench.py [--size 65536] [--iters 20]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--size", type=int, default=65536)
+    ap.add_argument("--iters", type=int, default=20)
+    a = ap.parse_args()
+    import paper_1511_07174_b200 as ks
+    import synth
+    n, K = a.size, a.iters
+    with ks.Context(n) as ctx:
+        b = ctx.generate("spd", seed=synth.SEED, table=synth.spd_table(n, 1e4))
+        ctx.set_option("true_residual", 0)
+        ctx.cg(b, tol=0.0, maxit=2, hist=False)
+        _, _, r1 = ctx.cg(b, tol=0.0, maxit=K, hist=False)
+        single = K / r1.seconds_loop
+        print(json.dumps({"nrhs": 1, "kernel": "ks_cg", "iters_per_s": single,
+                          "GBps": 8.0 * n * n * single / 1e9}), flush=True)
+        for nrhs in (1, 2, 4, 8):
+            B = np.column_stack([b] + [synth.rhs(n, synth.SEED + j) for j in range(1, nrhs)])
+            ctx.cg_multi(B, tol=0.0, maxit=2, hist=False)
+            X, h, r = ctx.cg_multi(B, tol=0.0, maxit=K, hist=False)
+            t = r[0].seconds_loop
+            ips = K / t
+            print(json.dumps({"nrhs": nrhs, "kernel": "ks_cg_multi", "iters_per_s": ips,
+                              "rhs_iters_per_s": nrhs * ips, "GBps": 8.0 * n * n * ips / 1e9,
+                              "speedup_vs_single_rhs_cg": nrhs * ips / single,
+                              "statuses": [q.status for q in r]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
