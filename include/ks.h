@@ -103,8 +103,8 @@ typedef enum {
                               /* 16 on the multi-kernel path                      */
     KS_OPT_GEMV_ROWS = 3,     /* K1 rows per CTA tile: 2, 4, 8, 16 (0 = auto)     */
     KS_OPT_GEMV_SPLIT = 4,    /* K1 column splits per tile (0 = auto)             */
-    KS_OPT_GEMV_KERNEL = 5,   /* K1 variant: 0 = auto, 1 = LDG stream, 2 = TMA    */
-                              /* bulk-copy ring                                   */
+    KS_OPT_GEMV_KERNEL = 5,   /* K1 variant: 0 = auto, 1 = LDG stream (the only   */
+                              /* one; round 1's TMA ring was removed)             */
     KS_OPT_USE_GRAPHS = 6,    /* 1: replay each poll batch as a CUDA graph        */
     KS_OPT_FUSED_COMM = 7,    /* 1 (default): when P > 1 and every GPU pair has   */
                               /* peer access, the producing kernels store their   */

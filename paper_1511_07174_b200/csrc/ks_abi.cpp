@@ -535,7 +535,7 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             if (v < 0 || v > 64) return fail(c, KS_EARG, "split must be in [0, 64]");
             o.gemv_split = v; break;
         case KS_OPT_GEMV_KERNEL:
-            if (v < 0 || v > 2) return fail(c, KS_EARG, "kernel must be 0, 1 or 2");
+            if (v < 0 || v > 1) return fail(c, KS_EARG, "kernel must be 0 or 1 (the TMA variant was removed)");
             o.gemv_kernel = v; break;
         case KS_OPT_USE_GRAPHS: o.use_graphs = v ? 1 : 0; break;
         case KS_OPT_FUSED_COMM: o.fused_comm = v ? 1 : 0; break;

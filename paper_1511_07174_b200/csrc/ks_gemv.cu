@@ -19,11 +19,10 @@
 // combined in tile order by the last-arriving tile -- the result is bitwise
 // independent of CTA scheduling.
 //
-// Variant 2 ("TMA bulk ring"): same tiling, but one elected thread streams the
-// R row segments of each column block into a shared-memory ring with
-// cp.async.bulk (TMA, SASS UBLKCP) completing on mbarriers, with an L2
-// evict-first cache hint; all warps consume from shared memory.  Deep
-// memory-level parallelism without register staging.
+// (Round 1 also had a TMA bulk-ring variant with one producer thread; it measured
+// 4.3-6.8 TB/s against this stream's 7.4 and was removed.  The warp-specialised
+// TMA pipeline -- producer warp, 2-D tensor-map loads, 40 KiB stages, consumer
+// warps -- is the multi-RHS GEMM, ks_multi.cu.)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,7 +31,6 @@
 
 #include "ks_device.cuh"
 #include "ks_tile.cuh"
-#include "ks_tma.cuh"
 #include "ks_internal.h"
 
 namespace ks {
@@ -43,7 +41,7 @@ constexpr int kNT = 256;  // threads per CTA
 constexpr int kNW = kNT / 32;
 
 
-// Tile epilogue shared by both variants.  `acc` holds the full-row sums (valid in
+// Tile epilogue.  `acc` holds the full-row sums (valid in
 // every thread).  Returns nothing; handles split-K combine, y store, dots.
 template <int R, class T>
 __device__ __forceinline__ void gemv_epilogue(const GemvParamsT<T>& p, T (&acc)[R], int64_t tile,
@@ -149,85 +147,6 @@ __global__ void __launch_bounds__(kNT) k1_gemv_ldg(GemvParamsT<T> p, int S, int6
     gemv_epilogue<R>(p, acc, tile, s, S, tiles, qpart, tile_ticket, dpart, ticket, red);
 }
 
-// ----------------------------------------------------------------------------
-// Variant 2: cp.async.bulk (TMA) ring.  Stage = R row segments of CW doubles.
-// ----------------------------------------------------------------------------
-constexpr int kCW = 512;          // columns per stage per row (4 KiB per row segment)
-
-template <int R, int STAGES>
-__global__ void __launch_bounds__(kNT) k1_gemv_tma(GemvParams p, int S, int64_t tiles,
-                                                   double* qpart, unsigned* tile_ticket,
-                                                   double* dpart, unsigned* ticket) {
-    extern __shared__ __align__(128) unsigned char dyn_smem[];
-    double* ring = reinterpret_cast<double*>(dyn_smem);  // STAGES * R * kCW
-    __shared__ __align__(8) uint64_t full_bar[STAGES];
-    __shared__ __align__(8) uint64_t empty_bar[STAGES];
-    __shared__ double red[R * kNW];
-    if (p.done && *(volatile const int*)p.done) return;
-
-    const int64_t unit = blockIdx.x;
-    const int64_t tile = unit / S;
-    const int s = (int)(unit % S);
-    const int64_t r0 = tile * R;
-    const int nvalid = (int)min((int64_t)R, p.m - r0);
-    const int64_t nst = p.ncols / kCW;                 // column stages of the row
-    const int64_t st0 = s * nst / S, st1 = (s + 1) * nst / S;
-    const int64_t nsteps = st1 - st0;
-
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&full_bar[i], 1);
-            mbar_init(&empty_bar[i], kNW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    const uint64_t pol = policy_evict_first();
-    const uint32_t stage_bytes = (uint32_t)(nvalid * kCW * sizeof(double));
-    auto produce = [&](int64_t step) {
-        const int slot = (int)(step % STAGES);
-        double* dst = ring + (int64_t)slot * R * kCW;
-        mbar_expect_tx(&full_bar[slot], stage_bytes);
-        const int64_t c = (st0 + step) * kCW;
-        for (int r = 0; r < nvalid; ++r)
-            bulk_g2s(dst + r * kCW, p.A + (r0 + r) * p.lda + c, kCW * sizeof(double),
-                     &full_bar[slot], pol);
-    };
-    if (threadIdx.x == 0) {
-        for (int64_t q = 0; q < min((int64_t)STAGES, nsteps); ++q) produce(q);
-    }
-
-    double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    const int warp = threadIdx.x >> 5;
-    for (int64_t step = 0; step < nsteps; ++step) {
-        const int slot = (int)(step % STAGES);
-        const uint32_t parity = (uint32_t)((step / STAGES) & 1);
-        const int64_t c = (st0 + step) * kCW + 2 * threadIdx.x;
-        const double2 xv = ld_x(p.x + c);
-        mbar_wait(&full_bar[slot], parity);
-        const double* src = ring + (int64_t)slot * R * kCW + 2 * threadIdx.x;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int rr = min(r, nvalid - 1);
-            const double2 a = *reinterpret_cast<const double2*>(src + rr * kCW);
-            acc[r] = fma(a.x, xv.x, acc[r]);
-            acc[r] = fma(a.y, xv.y, acc[r]);
-        }
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty_bar[slot]);
-        if (threadIdx.x == 0 && step + STAGES < nsteps) {
-            mbar_wait(&empty_bar[slot], parity);
-            produce(step + STAGES);
-        }
-        (void)warp;
-    }
-    block_sum<kNT, R>(acc, red);
-    gemv_epilogue<R>(p, acc, tile, s, S, tiles, qpart, tile_ticket, dpart, ticket, red);
-}
-
 template <int R, int U>
 void launch_ldg(const GemvParams& p, const GemvConfig& c, const Scratch& s, int ticket_id, cudaStream_t st) {
     const int64_t tiles = (p.m + R - 1) / R;
@@ -247,21 +166,7 @@ int launch_rows(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
     // dots of more than kPartStride/2 tiles go to the split-K scratch tail
     if (tiles * 2 > kPartStride) dpart = s.qpart + (s.qpart_cap - tiles * 2);
     unsigned* ticket = s.ticket + ticket_id;
-    if (c.variant == 2) {
-        constexpr int STAGES = (R >= 16) ? 3 : (R >= 8 ? 6 : 12);
-        const size_t smem = (size_t)STAGES * R * kCW * sizeof(double);
-        auto kern = k1_gemv_tma<R, STAGES>;
-        static std::atomic<unsigned> attr_set{0};  // one bit per device
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (!(attr_set & (1u << dev))) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr_set |= 1u << dev;
-        }
-        kern<<<(unsigned)grid, kNT, smem, st>>>(p, c.splits, tiles, s.qpart, s.tile_ticket, dpart,
-                                               ticket);
-        return 1;
-    }
+
     // LDG stream: unroll U (tuning sweep; default 16 loads in flight per thread)
     const int U = c.unroll > 0 ? c.unroll : (R >= 16 ? 1 : (R >= 8 ? 2 : 4));
     switch (U) {
@@ -278,12 +183,14 @@ int launch_rows(const GemvParams& p, const GemvConfig& c, const Scratch& s, int 
 GemvConfig choose_gemv(int64_t m, int64_t ncols, int num_sms, int rows_opt, int split_opt,
                        int variant_opt) {
     GemvConfig c;
-    c.variant = variant_opt == 2 ? 2 : 1;
+    (void)variant_opt;
+    c.variant = 1;
     // measured on B200 at n = 65536 (profiles/r01_gemv_sweep*.json): LDG R=2/U=4
-    // 7.41 TB/s, R=4/U=2 7.40, R=4/U=4 6.84-7.43 (box dependent), R=8 <= 7.18;
-    // TMA R=16 6.82, R=8 6.00, R=4 4.28
+    // 7.41 TB/s, R=4/U=2 7.40, R=4/U=4 6.84-7.43 (box dependent), R=8 <= 7.18.  The
+    // round-1 single-producer-thread TMA variant (6.82 / 6.00 / 4.28 TB/s at R = 16 / 8 /
+    // 4) was removed in round 2; the warp-specialised TMA pipeline lives in ks_multi.cu.
     c.rows = (rows_opt == 2 || rows_opt == 4 || rows_opt == 8 || rows_opt == 16) ? rows_opt
-                                                                                  : (c.variant == 2 ? 16 : 2);
+                                                                                  : 2;
     c.unroll = 0;
     const int64_t tiles = (m + c.rows - 1) / c.rows;
     const int64_t ncb = std::max<int64_t>(1, ncols / (2 * kNT));   // == ncols / kCW

@@ -1,13 +1,13 @@
 // NEXT-2, third stage: the register-resident whole-solve
 // kernels for C1-sized systems (one GPU, FP64, n <= 1024 -- the matrix fits in
-// the shared memory of the SMs, 8 MiB at n = 1024).
+// the register files of the SMs: 8 MiB at n = 1024 = 56 KiB per SM of 256 KiB).
 //
 // Where the small-n kernels (ks_small.cu) re-read A from L2 every GEMV and pay a
 // global arrival counter (one atomic per CTA, a fence, a spin) per reduction,
 // here:
-//   * each CTA owns a contiguous block of <= kRM rows of A and keeps it in its
-//     shared memory for the whole solve (loaded once per launch with
-//     cp.async.bulk, one bulk copy per row);
+//   * each CTA owns a contiguous block of <= kRM rows of A and keeps it in
+//     REGISTERS for the whole solve (thread t holds its columns of those rows,
+//     loaded once per launch): the GEMV reads no memory at all;
 //   * every CTA holds the full-length vectors x, r, p (BiCGSTAB: also rhat, v, s)
 //     REPLICATED in registers, in one fixed column-ownership layout (thread t
 //     owns columns 2t + 512u + {0, 1}); every O(n) step of the recurrence and every
@@ -69,7 +69,8 @@ __device__ __forceinline__ double ll_value(uint64_t lo, uint64_t hi) {
 // spinning until every word carries `flag`.  Columns >= n read as 0.  Bounded:
 // returns false after kWaitTimeoutNs (a bug, never a peer: all CTAs are resident).
 template <int V>
-__device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t flag, double (&out)[V]) {
+__device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t flag, double (&out)[V],
+                                          unsigned backoff_ns) {
     bool have[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -94,11 +95,56 @@ __device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t 
             }
         }
         if (all) return true;
+        if (backoff_ns) __nanosleep(backoff_ns);     // fewer polls in flight while waiting
         if ((spin & 255) == 255) {
             if (t0 == 0) t0 = globaltimer_ns();
             else if (globaltimer_ns() - t0 > kWaitTimeoutNs) return false;
         }
     }
+}
+
+// Exchange, mode 1 (KS_TINY_XCHG=1, tuning): plain values + one ready flag per CTA.
+// Slot layout: lda doubles of data, then one 64-bit flag per CTA.  Writers: value
+// stores, __threadfence, barrier, one flag store; readers: warp 0 polls the flags
+// (acquire), barrier, every thread reads its values through L2.
+__device__ __forceinline__ void fx_put(uint64_t* slot, int64_t lda, int rb, int R, double v, uint64_t flag) {
+    double* data = reinterpret_cast<double*>(slot);
+    if (threadIdx.x < R) {
+        __stcg(data + rb + threadIdx.x, v);
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long* f = reinterpret_cast<unsigned long long*>(slot + lda) + blockIdx.x;
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(f), "l"((unsigned long long)flag) : "memory");
+    }
+}
+template <int V>
+__device__ __forceinline__ bool fx_get(const uint64_t* slot, int64_t lda, int n, uint64_t flag, double (&out)[V]) {
+    __shared__ int s_ok;
+    if (threadIdx.x < 32) {
+        const unsigned long long* f = reinterpret_cast<const unsigned long long*>(slot + lda);
+        bool ok = true;
+        const unsigned long long t0 = globaltimer_ns();
+        for (int j = threadIdx.x; j < (int)gridDim.x && ok; j += 32) {
+            for (;;) {
+                unsigned long long v;
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f + j) : "memory");
+                if (v == flag) break;
+                if (globaltimer_ns() - t0 > kWaitTimeoutNs) { ok = false; break; }
+            }
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (threadIdx.x == 0) s_ok = ok;
+    }
+    __syncthreads();
+    const double* data = reinterpret_cast<const double*>(slot);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int j = 2 * threadIdx.x + 512 * (v >> 1) + (v & 1);
+        out[v] = j < n ? __ldcg(data + j) : 0.0;
+    }
+    return s_ok != 0;
 }
 
 // Block sum of K values (fixed tree; every thread gets the same bits): butterfly in
@@ -161,25 +207,35 @@ __device__ __forceinline__ double warp_rows8(double (&a)[kRM], int& row) {
     return v1;
 }
 
-// GEMV rows [0, R) of this CTA's shared-memory block against the register-resident
-// full-length x (this thread's V columns); thread t < R returns row t's sum.
-// Per-thread row partials -> transpose warp reduction -> warp sums in warp order.
+// Loads this thread's slice of rows [rb, rb + R) of A into registers: a[i][v] =
+// A[rb + i][col_of(v)] (zero for i >= R or columns >= ld), once per launch.
 template <int V>
-__device__ __forceinline__ double gemv_rows(const double* As, int64_t ld, int R, const double (&x)[V],
+__device__ __forceinline__ void load_rows_reg(const double* A, int64_t lda, int rb, int R, double (&a)[kRM][V]) {
+#pragma unroll
+    for (int i = 0; i < kRM; ++i) {
+#pragma unroll
+        for (int u = 0; u < V / 2; ++u) {
+            double2 v2 = make_double2(0.0, 0.0);
+            if (i < R) v2 = __ldg(reinterpret_cast<const double2*>(A + (int64_t)(rb + i) * lda + 2 * threadIdx.x + 512 * u));
+            a[i][2 * u] = v2.x;
+            a[i][2 * u + 1] = v2.y;
+        }
+    }
+}
+
+// GEMV rows [0, R) of this CTA's block, held in registers (a), against the
+// register-resident full-length x (this thread's V columns); thread t < R returns
+// row t's sum.  Per-thread row partials -> transpose warp reduction -> warp sums in
+// warp order.  No shared-memory traffic for A.
+template <int V>
+__device__ __forceinline__ double gemv_rows(const double (&a)[kRM][V], int R, const double (&x)[V],
                                             double* wred) {
     double acc[kRM];
 #pragma unroll
     for (int i = 0; i < kRM; ++i) {
         acc[i] = 0.0;
-        if (i < R) {
-            const double* row = As + (int64_t)i * ld + 2 * threadIdx.x;
 #pragma unroll
-            for (int u = 0; u < V / 2; ++u) {
-                const double2 a = *reinterpret_cast<const double2*>(row + 512 * u);
-                acc[i] = fma(a.x, x[2 * u], acc[i]);
-                acc[i] = fma(a.y, x[2 * u + 1], acc[i]);
-            }
-        }
+        for (int v = 0; v < V; ++v) acc[i] = fma(a[i][v], x[v], acc[i]);
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int row;
@@ -203,6 +259,7 @@ struct TinyArgs {
     // boundaries of CG iteration k (kTrace stamps per CTA) and %globaltimer once
     unsigned long long* trace;
     long long trace_k;
+    unsigned backoff;    // ns of __nanosleep after an unsuccessful LL poll round (0: spin)
 };
 constexpr int kTrace = 8;
 __device__ __forceinline__ void stamp(const TinyArgs& T, long long k, int i) {
@@ -221,33 +278,13 @@ __device__ __forceinline__ void my_rows(int n, int& rb, int& R) {
     R = q + (b < rem ? 1 : 0);
 }
 
-// Loads rows [rb, rb + R) of A into shared memory: one bulk copy per row.
-__device__ __forceinline__ void load_rows_smem(const double* A, int64_t lda, int rb, int R, double* As,
-                                               uint64_t* bar) {
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t bytes = (uint32_t)(lda * sizeof(double));
-        mbar_expect_tx(bar, bytes * (uint32_t)R);
-        const uint64_t pol = policy_evict_first();
-        for (int i = 0; i < R; ++i) bulk_g2s(As + (int64_t)i * lda, A + (int64_t)(rb + i) * lda, bytes, bar, pol);
-    }
-    mbar_wait(bar, 0);
-}
-
 __device__ __forceinline__ int col_of(int v) { return 2 * threadIdx.x + 512 * (v >> 1) + (v & 1); }
 
 // ------------------------------------------------------------------ CG (A1-A5)
-template <int V>
+template <int V, int XM>
 __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* As = reinterpret_cast<double*>(smem_raw);
     __shared__ double wred[kRM * kTW];
     __shared__ double red[2 * 2 * kTW];
-    __shared__ __align__(8) uint64_t bar;
     int par = 0;
     const VecArgs& a = T.a;
     DevState* st = a.st;
@@ -255,7 +292,8 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
     if (is_done(st)) return;
     int rb, R;
     my_rows(n, rb, R);
-    load_rows_smem(T.A, T.lda, rb, R, As, &bar);
+    double Ar[kRM][V];
+    load_rows_reg<V>(T.A, T.lda, rb, R, Ar);
     double x[V], r[V], p[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -276,13 +314,20 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
     for (; k <= maxit; ++k) {
         stamp(T, k, 0);
         // A1: q rows = A p; LL exchange (the grid-wide step)
-        const double qrow = gemv_rows<V>(As, T.lda, R, p, wred);
+        const double qrow = gemv_rows<V>(Ar, R, p, wred);
         stamp(T, k, 1);
         const uint32_t flag = (uint32_t)(2ull * (eb + (unsigned long long)k));
         uint64_t* slot = T.ll + (int64_t)(k & 1) * 2 * T.lda;
-        if (threadIdx.x < R) ll_store(slot + 2 * (int64_t)(rb + threadIdx.x), qrow, flag);
         double q[V];
-        if (!ll_gather<V>(slot, n, flag, q)) {
+        bool got;
+        if (XM == 0) {
+            if (threadIdx.x < R) ll_store(slot + 2 * (int64_t)(rb + threadIdx.x), qrow, flag);
+            got = ll_gather<V>(slot, n, flag, q, T.backoff);
+        } else {
+            fx_put(slot, T.lda, rb, R, qrow, flag);
+            got = fx_get<V>(slot, T.lda, n, flag, q);
+        }
+        if (!got) {
             if (lead0 && threadIdx.x == 0) { st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1; }
             return;
         }
@@ -335,13 +380,10 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
 }
 
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
-template <int V>
+template <int V, int XM>
 __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* As = reinterpret_cast<double*>(smem_raw);
     __shared__ double wred[kRM * kTW];
     __shared__ double red[2 * 2 * kTW];
-    __shared__ __align__(8) uint64_t bar;
     int par = 0;
     const VecArgs& a = T.a;
     DevState* st = a.st;
@@ -349,7 +391,8 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
     if (is_done(st)) return;
     int rb, R;
     my_rows(n, rb, R);
-    load_rows_smem(T.A, T.lda, rb, R, As, &bar);
+    double Ar[kRM][V];
+    load_rows_reg<V>(T.A, T.lda, rb, R, Ar);
     double x[V], r[V], p[V], v_[V], rh[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -377,9 +420,16 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         for (int v = 0; v < V; ++v) p[v] = i == 1 ? r[v] : fma(beta, fma(-omega, v_[v], p[v]), r[v]);
         // B2/B3: v = A p, exchange (slot 0)
         const uint32_t fv = (uint32_t)(2ull * (eb + (unsigned long long)i));
-        double vrow = gemv_rows<V>(As, T.lda, R, p, wred);
-        if (threadIdx.x < R) ll_store(T.ll + 2 * (int64_t)(rb + threadIdx.x), vrow, fv);
-        if (!ll_gather<V>(T.ll, n, fv, v_)) {
+        double vrow = gemv_rows<V>(Ar, R, p, wred);
+        bool got;
+        if (XM == 0) {
+            if (threadIdx.x < R) ll_store(T.ll + 2 * (int64_t)(rb + threadIdx.x), vrow, fv);
+            got = ll_gather<V>(T.ll, n, fv, v_, T.backoff);
+        } else {
+            fx_put(T.ll, T.lda, rb, R, vrow, fv);
+            got = fx_get<V>(T.ll, T.lda, n, fv, v_);
+        }
+        if (!got) {
             if (lead0 && threadIdx.x == 0) { st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1; }
             return;
         }
@@ -409,11 +459,17 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         }
         // B6: t = A s, exchange (slot 1); <t, s>, <t, t>
         const uint32_t ft = fv + 1u;
-        const double trow = gemv_rows<V>(As, T.lda, R, s, wred);
+        const double trow = gemv_rows<V>(Ar, R, s, wred);
         uint64_t* slot1 = T.ll + 2 * T.lda;
-        if (threadIdx.x < R) ll_store(slot1 + 2 * (int64_t)(rb + threadIdx.x), trow, ft);
         double t[V];
-        if (!ll_gather<V>(slot1, n, ft, t)) {
+        if (XM == 0) {
+            if (threadIdx.x < R) ll_store(slot1 + 2 * (int64_t)(rb + threadIdx.x), trow, ft);
+            got = ll_gather<V>(slot1, n, ft, t, T.backoff);
+        } else {
+            fx_put(slot1, T.lda, rb, R, trow, ft);
+            got = fx_get<V>(slot1, T.lda, n, ft, t);
+        }
+        if (!got) {
             if (lead0 && threadIdx.x == 0) { st->peer_timeout = 1; st->status = KS_ECUDA; st->done = 1; }
             return;
         }
@@ -461,19 +517,24 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
     }
 }
 
-template <int V>
+template <int V, int XM>
 const void* kern(int bicgstab) {
-    return bicgstab ? (const void*)k_bs_tiny<V> : (const void*)k_cg_tiny<V>;
+    return bicgstab ? (const void*)k_bs_tiny<V, XM> : (const void*)k_cg_tiny<V, XM>;
+}
+int xchg_mode() {
+    const char* e = std::getenv("KS_TINY_XCHG");   // tuning: 0 = LL (default), 1 = ready flags
+    return e && std::atoi(e) == 1 ? 1 : 0;
 }
 const void* kern_v(int bicgstab, int V) {
-    return V == 2 ? kern<2>(bicgstab) : kern<4>(bicgstab);
+    if (xchg_mode() == 1) return V == 2 ? kern<2, 1>(bicgstab) : kern<4, 1>(bicgstab);
+    return V == 2 ? kern<2, 0>(bicgstab) : kern<4, 0>(bicgstab);
 }
 
 }  // namespace
 
 // Grid of the tiny kernels for an n x n FP64 system on one GPU (ld = padded row
 // length), 0 when not applicable: n <= 1024 (the full vectors fit in registers,
-// 4 values per thread and vector), every CTA's rows fit in shared memory (<= kRM),
+// 4 values per thread and vector), every CTA's rows fit in registers (<= kRM),
 // one co-resident CTA per SM.
 int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld) {
     if (n < 1 || n > 1024 || ld > 1024) return 0;
@@ -482,24 +543,12 @@ int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld) {
     if (g > n) g = (int)n;
     const int64_t rmax = (n + g - 1) / g;
     if (rmax > kRM) return 0;
-    const size_t sm = (size_t)rmax * (size_t)ld * sizeof(double);
-    int dev = 0, optin = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
-    if (sm + 4096 > (size_t)optin) return 0;
-    const void* k = kern_v(bicgstab, V);
-    cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return 0; }
-    const int dyn_max = optin - (int)fa.sharedSizeBytes;     // opt-in limit minus static smem
-    if ((size_t)dyn_max < sm ||
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) != cudaSuccess) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_v(bicgstab, V), kTT, 0) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTT, sm);
-    if (per_sm < 1) return 0;
-    return g;
+    return per_sm >= 1 ? g : 0;
 }
 
 int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll, int grid,
@@ -509,11 +558,10 @@ int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, ui
     T.A = A;
     T.lda = lda;
     T.ll = ll;
-    const int n = (int)a.L.n;
-    const int64_t rmax = (n + grid - 1) / grid;
-    const size_t sm = (size_t)rmax * (size_t)lda * sizeof(double);
     T.trace = nullptr;
     T.trace_k = 0;
+    T.backoff = 0;
+    if (const char* bo = std::getenv("KS_TINY_BACKOFF")) T.backoff = (unsigned)std::atoi(bo);   // tuning
     const char* tr = bicgstab ? nullptr : std::getenv("KS_TINY_TRACE");   // debug facility
     if (tr) {
         T.trace_k = std::atoll(tr);
@@ -523,7 +571,7 @@ int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, ui
     }
     void* args[] = {&T};
     const cudaError_t e = cudaLaunchCooperativeKernel(kern_v(bicgstab, lda <= 512 ? 2 : 4), dim3((unsigned)grid),
-                                                      dim3(kTT), args, sm, st);
+                                                      dim3(kTT), args, 0, st);
     if (T.trace) {                      // dump: one line per CTA, clock deltas then the start time
         std::vector<unsigned long long> h((size_t)grid * (kTrace + 1));
         cudaMemcpyAsync(h.data(), T.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);

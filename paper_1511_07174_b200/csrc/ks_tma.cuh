@@ -1,6 +1,6 @@
-// TMA bulk-copy (cp.async.bulk) and mbarrier helpers shared by the TMA variant of
-// K1 (ks_gemv.cu) and the TMA-fed GEMV phase of the persistent kernels
-// (ks_persist.cuh).
+// mbarrier and TMA (cp.async.bulk) helpers of the multi-RHS GEMM pipeline
+// (ks_multi.cu: 2-D tensor-map loads into a shared-memory ring, full/empty
+// mbarriers between the producer warp and the consumer warps).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -10,7 +10,7 @@ out = {"n": n}
 with ks.Context(n) as ctx:
     t = time.time(); b = ctx.generate("dd", seed=synth.SEED, kd=16); out["gen_dd_s"] = time.time() - t
     res = {}
-    for var in (1, 2):
+    for var in (1,):   # the round-1 TMA variant (2) was removed
         for rows in (4, 8, 16):
             ctx.set_option("gemv_kernel", var); ctx.set_option("gemv_rows", rows)
             s = ctx.time_matvec(10)

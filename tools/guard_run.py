@@ -11,7 +11,7 @@ import synth
 assert os.environ.get("KS_GUARD") == "1", "run with KS_GUARD=1"
 ngpu = torch.cuda.device_count()
 total = 0
-modes = [{}, {"persistent": 0}, {"persistent": 0, "use_graphs": 1}, {"persistent": 0, "gemv_kernel": 2},
+modes = [{}, {"persistent": 0}, {"persistent": 0, "use_graphs": 1}, {"persistent": 0, "gemv_rows": 8},
          {"persistent": 0, "gemv_split": 3}, {"small": 0}, {"poll_batch": 3}, {"gemv_rows": 4, "gemv_unroll": 2}]
 for P in [p for p in (1, 2, 4) if p <= ngpu]:
     for n in (777, 2050):

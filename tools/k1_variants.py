@@ -1,5 +1,6 @@
-"""K1 variants at n = 65536 (and 32768), 1 GPU: LDG stream (default R=2/U=4 and
-R=4/U=2) vs the TMA bulk-copy ring (R = 4, 8, 16).  ks_time_matvec, best of 3 x 10.
+"""K1 shapes at n = 65536 (and 32768), 1 GPU: the LDG stream at R=2/U=4 (default),
+R=4/U=2 and R=4/U=4 (round 1 also timed a TMA ring, since removed:
+profiles/r01_k1_variants.json).  ks_time_matvec, best of 3 x 10.
 -> gpurun_out/k1_variants.json"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -9,7 +10,7 @@ res = []
 for n in (65536, 32768):
     with ks.Context(n) as ctx:
         ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
-        for variant, R, U in ((1, 0, 0), (1, 4, 2), (2, 4, 0), (2, 8, 0), (2, 16, 0)):
+        for variant, R, U in ((1, 0, 0), (1, 4, 2), (1, 4, 4)):
             ctx.set_option("gemv_kernel", variant)
             ctx.set_option("gemv_rows", R)
             ctx.set_option("gemv_unroll", U)

@@ -9,7 +9,7 @@ for n in (1024, 777):
     D = synth.gdd(n, 4)[0]
     b = synth.rhs(n)
     for opts in ({"persistent": 1}, {"persistent": 0}, {"persistent": 0, "use_graphs": 1},
-                 {"persistent": 0, "gemv_kernel": 2}, {"persistent": 0, "gemv_split": 3}):
+                 {"persistent": 0, "gemv_rows": 8}, {"persistent": 0, "gemv_split": 3}):
         with ks.Context(n) as c1, ks.Context(n) as c2:
             c1.load_rows(A); c2.load_rows(D)
             for k, v in opts.items():
