@@ -413,6 +413,35 @@ def run_ours(args):
     e2e_s = e2e_region(True)
     e2e_solve_s = e2e_region(False)
 
+    # extras (outside the timed region, one GPU only): multi-RHS CG on the resident
+    # CG matrix (8 right-hand sides share each pass over A) and the
+    # C1 latency path (n = 1024, tiny register-resident kernels)
+    extras = None
+    if world == 1 and not args.no_extras:
+        extras = {}
+        B = np.column_stack([b_cg] + [synth.rhs(n, SEED + j) for j in range(1, 8)])
+        cg_ctx.cg_multi(B, tol=0.0, maxit=2, hist=False)
+        _, _, rm = cg_ctx.cg_multi(B, tol=0.0, maxit=K, hist=False)
+        ips_m = K / rm[0].seconds_loop
+        extras["multi_rhs_cg"] = {
+            "nrhs": 8, "iters_per_s": ips_m, "rhs_iters_per_s": 8 * ips_m,
+            "A_stream_GBps": 8.0 * n * n * ips_m / 1e9, "vs_single_rhs_cg": 8 * ips_m / (K / cg_loop),
+            "kernel": "k_cgm<8> (TMA 2-D tensor-map loads, producer warp + 8 consumer warps, FP64 skinny GEMM)"}
+        with ks.Context.from_rank(1024, 0, 1, None, local, stream.cuda_stream) as c1:
+            bt = c1.generate("spd", seed=SEED, table=synth.spd_table(1024, 1e3))
+            c1.cg(bt, tol=0.0, maxit=2, hist=False)
+            _, _, r1 = c1.cg(bt, tol=0.0, maxit=200, hist=False)
+            _, _, r1t = c1.cg(bt, tol=1e-10, hist=False)
+        with ks.Context.from_rank(1024, 0, 1, None, local, stream.cuda_stream) as c1:
+            bd1 = c1.generate("dd", seed=SEED, kd=16)
+            c1.bicgstab(bd1, tol=0.0, maxit=2, hist=False)
+            _, _, r2 = c1.bicgstab(bd1, tol=0.0, maxit=30, hist=False)
+        extras["c1_latency"] = {
+            "cg_us_per_iter": 1e6 * r1.seconds_loop / r1.iterations,
+            "bicgstab_us_per_iter": 1e6 * r2.seconds_loop / r2.iterations,
+            "cg_iters_to_tol_1e-10": r1t.iterations,
+            "kernel": "k_cg_tiny / k_bs_tiny (A in registers, LL exchange)"}
+
     # roofline of the dominant kernel (K1 GEMV): algorithmic bytes 8*m*n per launch
     gemv_avg = gemv_s / max(1, gemv_n)
     achieved = 8.0 * m * n / gemv_avg / 1e9
@@ -469,6 +498,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clocks, "remeasured": remeasured,
             "cpu_baseline": cpu,
+            "extras": extras,
             "generate_s": t_gen,
             "env": environment(local),
             "topology": topo,
@@ -491,6 +521,7 @@ def main():
     ap.add_argument("--size", dest="n", type=int, default=65536)   # not "--n": torchrun would take it as an abbreviation of its own options
     ap.add_argument("--cpu-steps", type=int, default=3)      # cpu_baseline leg: full oracle steps
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--comm", choices=["fused", "nccl"], default="fused")
     ap.add_argument("--kernels", choices=["persistent", "multi"], default="persistent")
     args = ap.parse_args()

@@ -345,6 +345,7 @@ GemvConfig gemv_config(const ks_ctx* c, const Rank& r) {
 void ks_ctx::for_each_rank(const std::function<void(ks::Rank&)>& fn) {
     if (ranks.size() == 1) {
         ks::cuda_check(cudaSetDevice(ranks[0].dev), "cudaSetDevice");
+        cudaGetLastError();   // drop a stale, already-reported non-sticky error (e.g. an OOM)
         fn(ranks[0]);
         return;
     }
@@ -355,6 +356,7 @@ void ks_ctx::for_each_rank(const std::function<void(ks::Rank&)>& fn) {
         th.emplace_back([&, rp = &r] {
             try {
                 ks::cuda_check(cudaSetDevice(rp->dev), "cudaSetDevice");
+                cudaGetLastError();
                 fn(*rp);
             } catch (...) {
                 std::lock_guard<std::mutex> g(mu);

@@ -298,17 +298,23 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
 // Persistent GEMV shape: default R=2, U=4 (the sweep's best: CG 211.5 / BiCGSTAB
 // 105.3 it/s at n = 65536 vs 206.6 / 103.4 for R=4/U=2, profiles/r01_persist_sweep.json);
 // (4,2) and (4,4) selectable through KS_OPT_GEMV_ROWS / KS_OPT_GEMV_UNROLL.
+// (1, 8): one-row tiles for shards whose 2-row tile count would leave a badly filled
+// last wave over the resident CTAs (ks_solvers.cpp persist_shape).
 template <class T>
 const void* pick(int bicgstab, int rows, int unroll) {
-    const int shape = (rows == 4 && unroll == 2) ? 1 : (rows == 4 && unroll == 4) ? 2 : 0;
+    const int shape = (rows == 4 && unroll == 2) ? 1 : (rows == 4 && unroll == 4) ? 2 : (rows == 1) ? 3 : 0;
     if (bicgstab) {
         return shape == 1 ? (const void*)k_bs_persist<T, 4, 2>
-             : shape == 2 ? (const void*)k_bs_persist<T, 4, 4> : (const void*)k_bs_persist<T, 2, 4>;
+             : shape == 2 ? (const void*)k_bs_persist<T, 4, 4>
+             : shape == 3 ? (const void*)k_bs_persist<T, 1, 8> : (const void*)k_bs_persist<T, 2, 4>;
     }
     return shape == 1 ? (const void*)k_cg_persist<T, 4, 2>
-         : shape == 2 ? (const void*)k_cg_persist<T, 4, 4> : (const void*)k_cg_persist<T, 2, 4>;
+         : shape == 2 ? (const void*)k_cg_persist<T, 4, 4>
+         : shape == 3 ? (const void*)k_cg_persist<T, 1, 8> : (const void*)k_cg_persist<T, 2, 4>;
 }
-int rows_of(int rows, int unroll) { return (rows == 4 && (unroll == 2 || unroll == 4)) ? 4 : 2; }
+int rows_of(int rows, int unroll) {
+    return (rows == 4 && (unroll == 2 || unroll == 4)) ? 4 : rows == 1 ? 1 : 2;
+}
 
 int coop_grid(const void* kern, int num_sms, int64_t mmax, int R) {
     int per_sm = 0;

@@ -65,31 +65,42 @@ __device__ __forceinline__ double ll_value(uint64_t lo, uint64_t hi) {
     return __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
 }
 
+__device__ __forceinline__ void ll_load2(const uint64_t* slot, uint64_t (&w)[4]) {
+    asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(slot) : "memory");
+}
+
 // Reads the V values of this thread's columns (2t + 512u + {0, 1}) from an LL slot,
-// spinning until every word carries `flag`.  Columns >= n read as 0.  Bounded:
+// spinning until every word carries `flag`.  The two entries of a column pair are
+// 32 contiguous bytes: one 256-bit load (LDG.256) per pair and poll round, each of
+// its four 8-byte words checked on its own.  Columns >= n read as 0.  Bounded:
 // returns false after kWaitTimeoutNs (a bug, never a peer: all CTAs are resident).
 template <int V>
 __device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t flag, double (&out)[V],
                                           unsigned backoff_ns) {
-    bool have[V];
+    constexpr int U = V / 2;
+    bool have[U];
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-        const int j = 2 * threadIdx.x + 512 * (v >> 1) + (v & 1);
-        have[v] = j >= n;
-        out[v] = 0.0;
+    for (int u = 0; u < U; ++u) {
+        const int j = 2 * threadIdx.x + 512 * u;
+        have[u] = j >= n;
+        out[2 * u] = out[2 * u + 1] = 0.0;
     }
     unsigned long long t0 = 0;
     for (int spin = 0;; ++spin) {
         bool all = true;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            if (have[v]) continue;
-            const int j = 2 * threadIdx.x + 512 * (v >> 1) + (v & 1);
-            uint64_t lo, hi;
-            ll_load(slot + 2 * (int64_t)j, lo, hi);
-            if ((uint32_t)(lo >> 32) == flag && (uint32_t)(hi >> 32) == flag) {
-                out[v] = ll_value(lo, hi);
-                have[v] = true;
+        for (int u = 0; u < U; ++u) {
+            if (have[u]) continue;
+            const int j = 2 * threadIdx.x + 512 * u;
+            uint64_t w[4];
+            ll_load2(slot + 2 * (int64_t)j, w);
+            const bool ok0 = (uint32_t)(w[0] >> 32) == flag && (uint32_t)(w[1] >> 32) == flag;
+            const bool ok1 = j + 1 >= n || ((uint32_t)(w[2] >> 32) == flag && (uint32_t)(w[3] >> 32) == flag);
+            if (ok0 && ok1) {
+                out[2 * u] = ll_value(w[0], w[1]);
+                if (j + 1 < n) out[2 * u + 1] = ll_value(w[2], w[3]);
+                have[u] = true;
             } else {
                 all = false;
             }

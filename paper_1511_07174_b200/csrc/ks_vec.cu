@@ -633,9 +633,12 @@ __global__ void __launch_bounds__(kNT) k_end(VecArgs a, int bicgstab, int gather
         }
     }
     if (!gather) return;
-    if (stored) __threadfence_system();
+    (void)stored;
+    // every thread's remote stores, then ONE system-scope fence per CTA (cumulative over
+    // the barrier, the pattern NCCL's primitives use) before the CTA's ticket arrival
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence_system();
         unsigned* ticket = a.scr.ticket + 16;
         s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
         if (s_last) *ticket = 0u;
