@@ -21,22 +21,30 @@ using Clock = std::chrono::steady_clock;
 // Persistent GEMV shape: the tuning options if set, else R=4/U=2 for small shards
 // (<= 4096 rows: fewer, fuller tiles; C1 CG 13.4 vs 15.8 us/iteration,
 // profiles/r01_small_sweep.json) and the kernels' default R=2/U=4 above.
-// Shards above that: R = 2 unless its tile count leaves the last wave over the
-// resident CTAs (4 per SM) badly filled -- n = 16384 at P = 4 has 2048 two-row tiles
-// on 592 CTAs, 3.46 waves, so every GEMV runs 4 waves' time (16 % lost); one-row
+// Either default is replaced when its tile count leaves the last wave over the
+// resident CTAs (4 per SM) badly filled -- n = 16384 at P = 4 has 1024 four-row
+// tiles on 592 CTAs, 1.73 waves, so every GEMV takes 2 waves' time (13 % lost); one-row
 // tiles (R = 1, U = 8: still 8 loads of 16 B in flight per thread) give 6.92 -> 7.
 void persist_shape(const ks_ctx* c, const Rank& r, int* rows, int* unroll) {
     *rows = (int)c->opt.gemv_rows;
     *unroll = (int)c->opt.gemv_unroll;
     if (*rows != 0 || *unroll != 0) return;
-    if (r.L.pslot <= 4096) { *rows = 4; *unroll = 2; return; }
-    const int64_t G = 4LL * r.num_sms, m = r.L.pslot;
+    const int64_t cap = 4LL * r.num_sms, m = r.L.pslot;
     auto fill = [&](int64_t R) {                  // useful fraction of the last-wave-padded work
         const int64_t tiles = (m + R - 1) / R;
+        const int64_t G = std::min(tiles, cap);
         const int64_t waves = (tiles + G - 1) / G;
         return (double)tiles / (double)(waves * G);
     };
-    if (fill(1) > fill(2) + 0.03) { *rows = 1; *unroll = 8; }
+    const int def_r = m <= 4096 ? 4 : 2;
+    *rows = def_r;
+    *unroll = def_r == 4 ? 2 : 4;
+    double best = fill(def_r);
+    for (int R : {2, 1}) {
+        if (R == def_r) continue;
+        const double f = fill(R);
+        if (f > best + 0.03) { best = f; *rows = R; *unroll = R == 1 ? 8 : 4; }
+    }
 }
 
 // Small-n shared-memory kernels (ks_small.cu): their kind for this solve (0 CG,

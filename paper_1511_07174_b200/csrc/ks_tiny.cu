@@ -77,7 +77,7 @@ __device__ __forceinline__ void ll_load2(const uint64_t* slot, uint64_t (&w)[4])
 // returns false after kWaitTimeoutNs (a bug, never a peer: all CTAs are resident).
 template <int V>
 __device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t flag, double (&out)[V],
-                                          unsigned backoff_ns) {
+                                          unsigned backoff_ns, int wide) {
     constexpr int U = V / 2;
     bool have[U];
 #pragma unroll
@@ -94,7 +94,12 @@ __device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t 
             if (have[u]) continue;
             const int j = 2 * threadIdx.x + 512 * u;
             uint64_t w[4];
-            ll_load2(slot + 2 * (int64_t)j, w);
+            if (wide) {
+                ll_load2(slot + 2 * (int64_t)j, w);
+            } else {
+                ll_load(slot + 2 * (int64_t)j, w[0], w[1]);
+                ll_load(slot + 2 * (int64_t)j + 2, w[2], w[3]);
+            }
             const bool ok0 = (uint32_t)(w[0] >> 32) == flag && (uint32_t)(w[1] >> 32) == flag;
             const bool ok1 = j + 1 >= n || ((uint32_t)(w[2] >> 32) == flag && (uint32_t)(w[3] >> 32) == flag);
             if (ok0 && ok1) {
@@ -271,6 +276,7 @@ struct TinyArgs {
     unsigned long long* trace;
     long long trace_k;
     unsigned backoff;    // ns of __nanosleep after an unsuccessful LL poll round (0: spin)
+    int wide;            // 1: one 256-bit load per column pair and poll round (0: two 128-bit)
 };
 constexpr int kTrace = 8;
 __device__ __forceinline__ void stamp(const TinyArgs& T, long long k, int i) {
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
         bool got;
         if (XM == 0) {
             if (threadIdx.x < R) ll_store(slot + 2 * (int64_t)(rb + threadIdx.x), qrow, flag);
-            got = ll_gather<V>(slot, n, flag, q, T.backoff);
+            got = ll_gather<V>(slot, n, flag, q, T.backoff, T.wide);
         } else {
             fx_put(slot, T.lda, rb, R, qrow, flag);
             got = fx_get<V>(slot, T.lda, n, flag, q);
@@ -435,7 +441,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         bool got;
         if (XM == 0) {
             if (threadIdx.x < R) ll_store(T.ll + 2 * (int64_t)(rb + threadIdx.x), vrow, fv);
-            got = ll_gather<V>(T.ll, n, fv, v_, T.backoff);
+            got = ll_gather<V>(T.ll, n, fv, v_, T.backoff, T.wide);
         } else {
             fx_put(T.ll, T.lda, rb, R, vrow, fv);
             got = fx_get<V>(T.ll, T.lda, n, fv, v_);
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         double t[V];
         if (XM == 0) {
             if (threadIdx.x < R) ll_store(slot1 + 2 * (int64_t)(rb + threadIdx.x), trow, ft);
-            got = ll_gather<V>(slot1, n, ft, t, T.backoff);
+            got = ll_gather<V>(slot1, n, ft, t, T.backoff, T.wide);
         } else {
             fx_put(slot1, T.lda, rb, R, trow, ft);
             got = fx_get<V>(slot1, T.lda, n, ft, t);
@@ -573,6 +579,8 @@ int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, ui
     T.trace_k = 0;
     T.backoff = 0;
     if (const char* bo = std::getenv("KS_TINY_BACKOFF")) T.backoff = (unsigned)std::atoi(bo);   // tuning
+    T.wide = 1;
+    if (const char* wd = std::getenv("KS_TINY_WIDE")) T.wide = std::atoi(wd) != 0;               // tuning
     const char* tr = bicgstab ? nullptr : std::getenv("KS_TINY_TRACE");   // debug facility
     if (tr) {
         T.trace_k = std::atoll(tr);
