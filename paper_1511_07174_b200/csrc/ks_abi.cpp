@@ -464,23 +464,26 @@ ks_status ks_cg_multi(ks_ctx* c, int32_t nrhs, const double* B, const double* X0
     if (!B || !X) return fail(c, KS_EARG, "B and X are required");
     if (nrhs < 1 || nrhs > ks::kMaxRhs) return fail(c, KS_EARG, "nrhs must be in [1, 8]");
     if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "multi-RHS CG is FP64-only");
-    if (c->P != 1) return fail(c, KS_EARG, "multi-RHS CG runs on one GPU (P == 1)");
+    if (c->P != 1 && !c->fused()) return fail(c, KS_EARG, "multi-RHS CG over P > 1 GPUs needs peer access (fused exchange)");
     if (!(tol >= 0.0)) return fail(c, KS_EARG, "tol must be >= 0");
     if (maxit < 0) return fail(c, KS_EARG, "maxit must be >= 0");
     if (hist_cap < 0 || (hist_cap > 0 && !hist)) return fail(c, KS_EARG, "bad hist/hist_cap");
     if (!hist) hist_cap = 0;
     if (c->poisoned) return fail(c, KS_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
     if (!all_loaded(c)) return fail(c, KS_ESTATE, "matrix not fully loaded: call ks_load_rows / ks_generate first");
-    int64_t stat = 0;
+    std::vector<int64_t> stat(c->ranks.size(), 0);
     ks_status st = guarded(c, [&] {
         c->for_each_rank([&](Rank& r) {
-            stat = ks::run_cg_multi(c, r, nrhs, B, X0, tol, maxit, X, hist, hist_cap, reps);
+            const size_t i = (size_t)(&r - c->ranks.data());
+            // reports from the rank that writes the host outputs (all ranks agree)
+            stat[i] = ks::run_cg_multi(c, r, nrhs, B, X0, tol, maxit, X, hist, hist_cap,
+                                       c->writes_host(r) ? reps : nullptr);
             KS_CUDA(cudaGetLastError());
         });
         return KS_OK;
     });
     if (st != KS_OK) return st;
-    const ks_status s = status_of(stat);
+    const ks_status s = status_of(stat[0]);
     if (s != KS_OK) {
         const char* what = s == KS_EMAXIT ? "maximum iterations reached (some column)"
                                           : "CG: <p, A p> <= 0 in some column (matrix not SPD)";

@@ -88,7 +88,12 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         const size_t sb = (2 * P * kScalSlot * e + 511) / 512 * 512;
         const size_t fb = (kNumPhases * kMaxRanks * sizeof(unsigned long long) + 511) / 512 * 512;
         const size_t xb = ((size_t)ld * e + 511) / 512 * 512;
-        const size_t total = 2 * g + sb + fb + xb;
+        // multi-RHS CG over P > 1 (FP64 contexts): r slices, rank partials, gathered x
+        const bool mm = c->dtype == KS_FLOAT64 && P > 1;
+        const size_t mrb = mm ? 2 * P * (size_t)kMaxRhs * (size_t)r.L.chunk * sizeof(double) : 0;
+        const size_t msb = mm ? (2 * P * 2 * (size_t)kMaxRhs * sizeof(double) + 511) / 512 * 512 : 0;
+        const size_t mxb = mm ? (size_t)kMaxRhs * (size_t)ld * sizeof(double) : 0;
+        const size_t total = 2 * g + sb + fb + xb + mrb + msb + mxb;
         char* base = nullptr;
         KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total));
         KS_CUDA(cudaMemset(base, 0, total));
@@ -99,6 +104,17 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         r.S = reinterpret_cast<double*>(base + 2 * g);
         r.flags = reinterpret_cast<unsigned long long*>(base + 2 * g + sb);
         r.X = reinterpret_cast<double*>(base + 2 * g + sb + fb);
+        r.MR = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb) : nullptr;
+        r.MS = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb) : nullptr;
+        r.MX = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb + msb) : nullptr;
+        for (int q = 0; q < kMaxRanks; ++q) {
+            r.mpeer.MR[q] = r.mpeer.MS[q] = r.mpeer.MX[q] = nullptr;
+            r.mpeer.flags[q] = nullptr;
+        }
+        r.mpeer.MR[r.rank] = r.MR;
+        r.mpeer.MS[r.rank] = r.MS;
+        r.mpeer.MX[r.rank] = r.MX;
+        r.mpeer.flags[r.rank] = r.flags;
         for (int q = 0; q < kMaxRanks; ++q) {
             r.pp.G_r[q] = r.pp.G_v[q] = r.pp.S[q] = r.pp.X[q] = nullptr;
             r.pp.flags[q] = nullptr;
@@ -229,6 +245,9 @@ void setup_peers(ks_ctx* c) {
     };
     const size_t offGv = boff(c->ranks[0].G_v), offS = boff(c->ranks[0].S), offF = boff(c->ranks[0].flags),
                  offX = boff(c->ranks[0].X);
+    const bool mm = c->ranks[0].MR != nullptr;
+    const size_t offMR = mm ? boff(c->ranks[0].MR) : 0, offMS = mm ? boff(c->ranks[0].MS) : 0,
+                 offMX = mm ? boff(c->ranks[0].MX) : 0;
     if (!c->multiprocess) {
         bool ok = true;
         for (auto& a : c->ranks)
@@ -249,6 +268,10 @@ void setup_peers(ks_ctx* c) {
                 a.pp.S[b.rank] = b.S;
                 a.pp.flags[b.rank] = b.flags;
                 a.pp.X[b.rank] = b.X;
+                a.mpeer.MR[b.rank] = b.MR;
+                a.mpeer.MS[b.rank] = b.MS;
+                a.mpeer.MX[b.rank] = b.MX;
+                a.mpeer.flags[b.rank] = b.flags;
             }
             a.peer_ok = ok;
         }
@@ -280,6 +303,12 @@ void setup_peers(ks_ctx* c) {
         r.pp.S[g] = reinterpret_cast<double*>(d + offS);
         r.pp.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
         r.pp.X[g] = reinterpret_cast<double*>(d + offX);
+        r.mpeer.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
+        if (mm) {
+            r.mpeer.MR[g] = reinterpret_cast<double*>(d + offMR);
+            r.mpeer.MS[g] = reinterpret_cast<double*>(d + offMS);
+            r.mpeer.MX[g] = reinterpret_cast<double*>(d + offMX);
+        }
     }
     // every rank must agree, or none uses the fused path (collectives must match)
     int* dok = nullptr;

@@ -75,6 +75,8 @@ struct Rank {
     double* S = nullptr;        // 2 * P * kScalSlot
     unsigned long long* flags = nullptr;   // [kNumPhases][kMaxRanks]
     double* X = nullptr;        // ld elements: contiguous full x (end-of-solve gather)
+    double *MR = nullptr, *MS = nullptr, *MX = nullptr;   // multi-RHS exchange regions (P > 1)
+    MultiPeer mpeer{};
     PeerPtrs pp{};
     bool peer_ok = false;       // every rank's exchange buffers are load/store reachable
     std::vector<void*> ipc_opened;

@@ -290,8 +290,23 @@ struct MultiCol {
 };
 constexpr int kMaxRhs = 8;
 struct MultiState { MultiCol col[kMaxRhs]; };
+// P > 1: every rank's multi-RHS exchange regions (fifth to seventh regions of the
+// exchange allocation) and epoch flags.
+struct MultiPeer {
+    double* MR[kMaxRanks];                  // [2 parities][P][kMaxRhs][chunk]: r slices
+    double* MS[kMaxRanks];                  // [2][P][2 kMaxRhs]: rank partial scalars
+    double* MX[kMaxRanks];                  // [kMaxRhs][ld]: the gathered x
+    unsigned long long* flags[kMaxRanks];
+};
 struct MultiArgs {
     int nrhs, has_x0;
+    int peer;                      // 1: P > 1 with the fused NVLink exchange
+    Layout L;
+    MultiPeer mp;
+    double *MRo, *MSo;             // this rank's own regions (read side)
+    unsigned long long* flags;     // own [kNumPhases][kMaxRanks]
+    unsigned long long ebase;      // epochs: setup ebase, iteration k ebase + k, x gather ebase + maxit + 1
+    unsigned long long join_ns;
     int64_t n, m, ld, ldm, row0;   // ldm: stride of the K rows of X, R, Q; ld: of P
     double tol;
     long long maxit;

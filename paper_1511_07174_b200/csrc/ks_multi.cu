@@ -172,6 +172,42 @@ __device__ __forceinline__ void totals(const double* bpart, int q0, double (&out
     csum<K>(out, red);
 }
 
+// ---- P > 1 (fused NVLink exchange) ------------------------------------------
+// Rank all-reduce of NV scalars that every CTA of this rank holds identically
+// (CTA-order totals): the lead stores them into slots [q0, q0 + NV) of this rank's
+// row of every rank's MS[par] and releases `ph` with `epoch`; every CTA waits for
+// all ranks (thread 0 spins, the barrier orders the rest) and sums the P rows in
+// rank order.  P == 1: v unchanged.
+template <int NV>
+__device__ __forceinline__ bool rank_sum(const MultiArgs& M, double (&v)[NV], int par, int q0, int ph,
+                                         unsigned long long epoch) {
+    if (!M.peer) return true;
+    const int P = M.L.P, me = M.L.rank;
+    const int64_t row = 2 * kMaxRhs, pst = (int64_t)P * row;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int g = 0; g < P; ++g)
+            for (int k = 0; k < NV; ++k) M.mp.MS[g][par * pst + (int64_t)me * row + q0 + k] = v[k];
+        unsigned long long* f[kMaxRanks];
+        for (int g = 0; g < P; ++g) f[g] = M.mp.flags[g] + ph * kMaxRanks + me;
+        publish_flags(f, P, epoch);
+    }
+    if (!wait_flags(M.flags + ph * kMaxRanks, P, epoch)) {
+        if (threadIdx.x == 0) { M.st->peer_timeout = 1; M.st->status = KS_ENCCL; M.st->done = 1; }
+        return false;
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double t = 0.0;
+        for (int g = 0; g < P; ++g) t += __ldcg(M.MSo + par * pst + (int64_t)g * row + q0 + k);
+        v[k] = t;
+    }
+    return true;
+}
+// MR[par][g][k][chunk]: rank g's rows of column k of r (parity par)
+__device__ __forceinline__ int64_t mr_off(const MultiArgs& M, int par, int g, int k) {
+    return (((int64_t)par * M.L.P + g) * kMaxRhs + k) * M.L.chunk;
+}
+
 template <int K>
 __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensorMap tmA,
                                                const __grid_constant__ CUtensorMap tmP, MultiArgs M) {
@@ -185,6 +221,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     const int64_t gs = (int64_t)gridDim.x * kMCT;
     const int64_t t0 = (int64_t)blockIdx.x * kMCT + tid;
     const int64_t m = M.m;
+    const bool peer = M.peer != 0;
     if (tid == 0) {
         for (int s = 0; s < kMS; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kMW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -193,12 +230,26 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmP) : "memory");
     }
+    if (peer && blockIdx.x == 0 && tid == 0) {     // solve-start rendezvous (k_join's protocol)
+        unsigned long long* f[kMaxRanks];
+        for (int g = 0; g < M.L.P; ++g) f[g] = M.mp.flags[g] + kPhaseJ * kMaxRanks + M.L.rank;
+        publish_flags(f, M.L.P, M.ebase);
+        const unsigned long long tj = globaltimer_ns();
+        for (int g = 0; g < M.L.P; ++g) {
+            while (flag_acquire_sys(M.flags + kPhaseJ * kMaxRanks + g) < M.ebase) {
+                if (globaltimer_ns() - tj > M.join_ns) { st->peer_timeout = 1; st->status = KS_ENCCL; st->done = 1; break; }
+                __nanosleep(64);
+            }
+        }
+    }
     __syncthreads();
+    if (peer && !pk::grid_sync(M.bar, st)) return;
+    if (*(volatile const int*)&st->done) return;
     uint32_t it = 0;
     double sig[K];
     // ---- setup (row A0 per column): r0 = b - A x0 (or b), x = x0 (or 0), p = r0,
     // nb = ||b||, rho0 = <r0, r0>, the 0-iteration exits (Q2, Q6)
-    if (M.has_x0) {                        // P holds x0 (host copy): Q = A x0
+    if (M.has_x0) {                        // P holds the full x0 (host copy): Q = A x0
         gemm_phase<K>(&tmA, &tmP, M, S, it, sig);
         if (!pk::grid_sync(M.bar, st)) return;   // every CTA's rows of Q before they are read
     }
@@ -210,54 +261,67 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
             for (int64_t i = t0; i < m; i += gs) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const double bk = M.R[k * M.ldm + i];          // the host put b here
+                    const double bk = M.R[k * M.ldm + i];          // the host put b's own rows here
                     const double r = M.has_x0 ? bk - M.Q[k * M.ldm + i] : bk;
                     v[k] = fma(bk, bk, v[k]);
                     v[K + k] = fma(r, r, v[K + k]);
+                    M.R[k * M.ldm + i] = r;
+                    M.X[k * M.ldm + i] = M.has_x0 ? M.Pf[k * M.ld + M.row0 + i] : 0.0;   // x = x0
+                    if (peer)
+                        for (int g = 0; g < M.L.P; ++g) M.mp.MR[g][mr_off(M, 0, M.L.rank, k) + i] = r;
                 }
             }
         }
+        if (peer) { __syncthreads(); if (tid == 0) __threadfence_system(); }
         csum<2 * K>(v, S.red);
         if (tid == 0) {
 #pragma unroll
             for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
-        double tb[K], tr[K];
-        totals<K>(M.bpart, 0, tb, S.red);
-        totals<K>(M.bpart, K, tr, S.red);
+        double tbr[2 * K];
+        {
+            double tb[K], tr[K];
+            totals<K>(M.bpart, 0, tb, S.red);
+            totals<K>(M.bpart, K, tr, S.red);
+#pragma unroll
+            for (int k = 0; k < K; ++k) { tbr[k] = tb[k]; tbr[K + k] = tr[k]; }
+        }
+        if (!rank_sum<2 * K>(M, tbr, 0, 0, kPhaseR, M.ebase)) return;   // ||b||^2, <r0, r0> over the ranks
         if (cons) {
-            for (int64_t i = t0; i < m; i += gs) {
+            for (int64_t i = t0; i < m; i += gs)                         // Q6: b = 0 -> x = 0
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (!(k < M.nrhs) || tbr[k] == 0.0) M.X[k * M.ldm + i] = 0.0;
+            int o = 0;
+            for (int64_t j = t0; j < M.n; j += gs) {                      // p0 = r0 (full length)
+                int64_t jl = j;
+                if (peer) {
+                    while (o + 1 < M.L.P && j >= M.L.row0[o + 1]) ++o;   // j only grows per thread
+                    jl = j - M.L.row0[o];
+                }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    double r = M.R[k * M.ldm + i];
-                    if (M.has_x0) {
-                        r -= M.Q[k * M.ldm + i];
-                        M.X[k * M.ldm + i] = M.Pf[k * M.ld + i];       // x = x0
-                        M.R[k * M.ldm + i] = r;
-                    } else {
-                        M.X[k * M.ldm + i] = 0.0;
-                    }
-                    const bool z = !(k < M.nrhs) || tb[k] == 0.0;
-                    if (z) { M.X[k * M.ldm + i] = 0.0; M.R[k * M.ldm + i] = 0.0; r = 0.0; }
-                    M.Pf[k * M.ld + i] = r;                            // p0 = r0 (P = 1: full length)
+                    const bool z = !(k < M.nrhs) || tbr[k] == 0.0;
+                    const double r = peer ? __ldcg(M.MRo + mr_off(M, 0, o, k) + jl) : M.R[k * M.ldm + j];
+                    M.Pf[k * M.ld + j] = z ? 0.0 : r;
                 }
             }
         }
         if (blockIdx.x == 0 && tid == 0) {
             for (int k = 0; k < K; ++k) {
                 MultiCol& cl = ms->col[k];
-                cl.nb = sqrt(tb[k]);
-                cl.rho = tr[k];
+                cl.nb = sqrt(tbr[k]);
+                cl.rho = tbr[K + k];
                 cl.iters = 0;
                 cl.relres = 0.0;
                 cl.status = KS_EMAXIT;
                 cl.active = 1;
-                if (k >= M.nrhs || tb[k] == 0.0) {               // padding column / Q6: b = 0
+                if (k >= M.nrhs || tbr[k] == 0.0) {               // padding column / Q6: b = 0
                     cl.active = 0; cl.status = KS_OK; cl.converged = 1; cl.bzero = 1;
                 } else {
                     cl.converged = 0; cl.bzero = 0;
-                    cl.relres = sqrt(tr[k]) / cl.nb;
+                    cl.relres = sqrt(tbr[K + k]) / cl.nb;
                     if (cl.relres <= M.tol) { cl.active = 0; cl.status = KS_OK; cl.converged = 1; }   // Q2
                 }
             }
@@ -266,6 +330,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     }
     // ---- iterations (rows A1-A5 per column)
     for (long long k1 = 1; k1 <= M.maxit; ++k1) {
+        const int par = (int)(k1 & 1);
         int act[K];
         int any = 0;
 #pragma unroll
@@ -288,9 +353,10 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
             }
         }
         if (!pk::grid_sync(M.bar, st)) return;
-        // A2: sigma, alpha (per active column; NOTSPD ends that column, x unchanged)
+        // A2: sigma (rank all-reduce), alpha (per active column; NOTSPD ends that column, x unchanged)
         double sg[K], alpha[K], rho[K];
         totals<K>(M.bpart, 0, sg, S.red);
+        if (!rank_sum<K>(M, sg, par, 0, kPhaseS, M.ebase + (unsigned long long)k1)) return;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             rho[k] = *(volatile const double*)&ms->col[k].rho;
@@ -302,7 +368,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
             }
             alpha[k] = act[k] ? rho[k] / sg[k] : 0.0;
         }
-        // A3: x += alpha p; r -= alpha q; rho' partials
+        // A3: x += alpha p; r -= alpha q (own rows, pushed to every rank); rho' partials
         double rr[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) rr[k] = 0.0;
@@ -315,19 +381,24 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
                     M.X[k * M.ldm + i] = fma(alpha[k], pk_, M.X[k * M.ldm + i]);
                     const double r = fma(-alpha[k], M.Q[k * M.ldm + i], M.R[k * M.ldm + i]);
                     M.R[k * M.ldm + i] = r;
+                    if (peer)
+                        for (int g = 0; g < M.L.P; ++g) M.mp.MR[g][mr_off(M, par, M.L.rank, k) + i] = r;
                     rr[k] = fma(r, r, rr[k]);
                 }
             }
         }
+        if (peer) { __syncthreads(); if (tid == 0) __threadfence_system(); }
         csum<K>(rr, S.red);
         if (tid == 0) {
 #pragma unroll
             for (int k = 0; k < K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + K + k] = rr[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
-        // A5: test, beta, p = r + beta p
+        // A4 + A5: rho' (rank all-reduce; releases the pushed r slices too), test, beta,
+        // p = r + beta p over the full length
         double rho1[K], beta[K];
         totals<K>(M.bpart, K, rho1, S.red);
+        if (!rank_sum<K>(M, rho1, par, K, kPhaseR, M.ebase + (unsigned long long)k1)) return;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             beta[k] = 0.0;
@@ -346,10 +417,19 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
             beta[k] = rho1[k] / rho[k];
         }
         if (cons) {
+            int o = 0;
             for (int64_t j = t0; j < M.n; j += gs) {
+                int64_t jl = j;
+                if (peer) {
+                    while (o + 1 < M.L.P && j >= M.L.row0[o + 1]) ++o;   // j only grows per thread
+                    jl = j - M.L.row0[o];
+                }
 #pragma unroll
                 for (int k = 0; k < K; ++k)
-                    if (act[k]) M.Pf[k * M.ld + j] = fma(beta[k], M.Pf[k * M.ld + j], M.R[k * M.ldm + j]);
+                    if (act[k]) {
+                        const double r = peer ? __ldcg(M.MRo + mr_off(M, par, o, k) + jl) : M.R[k * M.ldm + j];
+                        M.Pf[k * M.ld + j] = fma(beta[k], M.Pf[k * M.ld + j], r);
+                    }
             }
         }
         if (blockIdx.x == 0 && tid == 0) {
@@ -357,6 +437,28 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
             for (int k = 0; k < K; ++k) if (act[k]) ms->col[k].rho = rho1[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
+    }
+    // ---- end: P > 1 gathers X into every rank's contiguous MX (K x ld)
+    if (peer) {
+        if (cons)
+            for (int64_t i = t0; i < m; i += gs)
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    for (int g = 0; g < M.L.P; ++g) M.mp.MX[g][k * M.ld + M.row0 + i] = M.X[k * M.ldm + i];
+        __syncthreads();
+        if (tid == 0) __threadfence_system();
+        if (!pk::grid_sync(M.bar, st)) return;
+        if (blockIdx.x == 0) {
+            if (tid == 0) {
+                unsigned long long* f[kMaxRanks];
+                for (int g = 0; g < M.L.P; ++g) f[g] = M.mp.flags[g] + kPhaseX * kMaxRanks + M.L.rank;
+                publish_flags(f, M.L.P, M.ebase + (unsigned long long)M.maxit + 1ull);
+            }
+            if (!wait_flags(M.flags + kPhaseX * kMaxRanks, M.L.P, M.ebase + (unsigned long long)M.maxit + 1ull) &&
+                tid == 0) {
+                st->peer_timeout = 1; st->status = KS_ENCCL;
+            }
+        }
     }
 }
 

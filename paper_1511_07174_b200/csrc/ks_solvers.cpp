@@ -863,7 +863,8 @@ int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double
     // b -> R (K rows of stride ldm), padding rows zero; x0 -> P; P zero elsewhere
     KS_CUDA(cudaMemsetAsync(r.mR, 0, (size_t)(K * ldm) * e, r.stream));
     KS_CUDA(cudaMemsetAsync(r.mP, 0, (size_t)(K * ld) * e, r.stream));
-    KS_CUDA(cudaMemcpy2DAsync(r.mR, (size_t)ldm * e, B, (size_t)n * e, (size_t)n * e, (size_t)nrhs,
+    // this rank's rows of b (P = 1: all of them)
+    KS_CUDA(cudaMemcpy2DAsync(r.mR, (size_t)ldm * e, B + r.row0, (size_t)n * e, (size_t)r.m * e, (size_t)nrhs,
                               cudaMemcpyDefault, r.stream));
     if (X0)
         KS_CUDA(cudaMemcpy2DAsync(r.mP, (size_t)ld * e, X0, (size_t)n * e, (size_t)n * e, (size_t)nrhs,
@@ -888,6 +889,15 @@ int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double
     M.st = r.st;
     M.bpart = r.scr.part + 2 * kPartStride;
     M.bar = r.scr.ticket + 8;
+    M.peer = c->P > 1 ? 1 : 0;
+    M.L = r.L;
+    M.mp = r.mpeer;
+    M.MRo = r.MR;
+    M.MSo = r.MS;
+    M.flags = r.flags;
+    M.ebase = r.epoch_next;
+    r.epoch_next += (unsigned long long)maxit + 2;
+    M.join_ns = (unsigned long long)c->opt.join_timeout_ms * 1000000ULL;
     const int grid = memo_grid(r, (5LL << 48) | K, [&] { return multi_grid(K, r.num_sms); });
     if (grid <= 0) throw KsError(KS_ECUDA, "multi-RHS kernel does not fit this device");
     KS_CUDA(cudaMemsetAsync(&r.st->peer_timeout, 0, sizeof(int), r.stream));
@@ -897,16 +907,23 @@ int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double
     KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
     // out: X columns, state, histories -- one synchronisation
     MultiState hs;
-    KS_CUDA(cudaMemcpy2DAsync(X, (size_t)n * e, r.mX, (size_t)ldm * e, (size_t)n * e, (size_t)nrhs,
-                              cudaMemcpyDefault, r.stream));
+    if (c->writes_host(r)) {
+        if (c->P > 1)                     // gathered in-kernel into this rank's MX (K x ld)
+            KS_CUDA(cudaMemcpy2DAsync(X, (size_t)n * e, r.MX, (size_t)ld * e, (size_t)n * e, (size_t)nrhs,
+                                      cudaMemcpyDefault, r.stream));
+        else
+            KS_CUDA(cudaMemcpy2DAsync(X, (size_t)n * e, r.mX, (size_t)ldm * e, (size_t)n * e, (size_t)nrhs,
+                                      cudaMemcpyDefault, r.stream));
+    }
     KS_CUDA(cudaMemcpyAsync(r.h_state, r.st, sizeof(DevState), cudaMemcpyDeviceToHost, r.stream));
     KS_CUDA(cudaMemcpyAsync(&hs, r.mstate, sizeof(MultiState), cudaMemcpyDeviceToHost, r.stream));
     const int64_t nh = std::min<int64_t>(hc, maxit);
-    if (nh > 0)
+    if (nh > 0 && c->writes_host(r))
         KS_CUDA(cudaMemcpy2DAsync(hist, (size_t)hist_cap * e, r.mhist, (size_t)hc * e, (size_t)nh * e,
                                   (size_t)nrhs, cudaMemcpyDefault, r.stream));
     KS_CUDA(cudaStreamSynchronize(r.stream));
-    if (r.h_state->peer_timeout) throw KsError(KS_ECUDA, "multi-RHS kernel: grid barrier timed out");
+    if (r.h_state->peer_timeout)
+        throw KsError(c->P > 1 ? KS_ENCCL : KS_ECUDA, "multi-RHS kernel: a barrier or peer wait timed out");
     float ms = 0.f;
     KS_CUDA(cudaEventElapsedTime(&ms, r.ev_t0, r.ev_t1));
     int64_t worst = KS_OK;
