@@ -93,7 +93,9 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         const size_t mrb = mm ? 2 * P * (size_t)kMaxRhs * (size_t)r.L.chunk * sizeof(double) : 0;
         const size_t msb = mm ? (2 * P * 2 * (size_t)kMaxRhs * sizeof(double) + 511) / 512 * 512 : 0;
         const size_t mxb = mm ? (size_t)kMaxRhs * (size_t)ld * sizeof(double) : 0;
-        const size_t total = 2 * g + sb + fb + xb + mrb + msb + mxb;
+        // tiny kernels over P > 1 (n <= 1024): their LL exchange slots, 4 ld words
+        const size_t llb = (P > 1 && ld <= 1024) ? 4 * (size_t)ld * sizeof(uint64_t) : 0;
+        const size_t total = 2 * g + sb + fb + xb + mrb + msb + mxb + llb;
         char* base = nullptr;
         KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total));
         KS_CUDA(cudaMemset(base, 0, total));
@@ -107,6 +109,9 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         r.MR = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb) : nullptr;
         r.MS = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb) : nullptr;
         r.MX = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb + msb) : nullptr;
+        r.llx = llb ? reinterpret_cast<uint64_t*>(base + 2 * g + sb + fb + xb + mrb + msb + mxb) : nullptr;
+        for (int q = 0; q < kMaxRanks; ++q) r.llpeer[q] = nullptr;
+        r.llpeer[r.rank] = r.llx;
         for (int q = 0; q < kMaxRanks; ++q) {
             r.mpeer.MR[q] = r.mpeer.MS[q] = r.mpeer.MX[q] = nullptr;
             r.mpeer.flags[q] = nullptr;
@@ -248,6 +253,8 @@ void setup_peers(ks_ctx* c) {
     const bool mm = c->ranks[0].MR != nullptr;
     const size_t offMR = mm ? boff(c->ranks[0].MR) : 0, offMS = mm ? boff(c->ranks[0].MS) : 0,
                  offMX = mm ? boff(c->ranks[0].MX) : 0;
+    const bool hasll = c->ranks[0].llx != nullptr;
+    const size_t offLL = hasll ? boff(c->ranks[0].llx) : 0;
     if (!c->multiprocess) {
         bool ok = true;
         for (auto& a : c->ranks)
@@ -272,6 +279,7 @@ void setup_peers(ks_ctx* c) {
                 a.mpeer.MS[b.rank] = b.MS;
                 a.mpeer.MX[b.rank] = b.MX;
                 a.mpeer.flags[b.rank] = b.flags;
+                a.llpeer[b.rank] = b.llx;
             }
             a.peer_ok = ok;
         }
@@ -304,6 +312,7 @@ void setup_peers(ks_ctx* c) {
         r.pp.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
         r.pp.X[g] = reinterpret_cast<double*>(d + offX);
         r.mpeer.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
+        if (hasll) r.llpeer[g] = reinterpret_cast<uint64_t*>(d + offLL);
         if (mm) {
             r.mpeer.MR[g] = reinterpret_cast<double*>(d + offMR);
             r.mpeer.MS[g] = reinterpret_cast<double*>(d + offMS);

@@ -272,14 +272,16 @@ template <class T>
 int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_t ncols, T* bpart,
                  unsigned* bar, long long k0, long long k1, int grid, cudaStream_t st, bool bar_zeroed = false);
 
-// Tiny kernels (ks_tiny.cu, NEXT-2): one GPU, FP64, n <= 1024: A resident in shared
-// memory, full vectors replicated in registers, GEMV outputs exchanged through an
-// LL-format global buffer (ll: 4 * ld uint64 words, zeroed once).  The whole solve
+// Tiny kernels (ks_tiny.cu, NEXT-2): FP64, n <= 1024: A resident in registers, full
+// vectors replicated in registers, GEMV outputs exchanged through an LL-format global
+// buffer (ll: 4 * ld uint64 words, zeroed once).  The whole solve
 // in one launch (they always finish the solve).  tiny_grid returns 0 when not
 // applicable.
-int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld);
-int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll, int grid,
-                cudaStream_t st);
+// P > 1 (fused exchange): the LL words go over NVLink into every rank's buffer (llp,
+// a region of the exchange allocation), x0f = the full x0 or NULL.  m = this rank's rows.
+int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t m, int64_t ld);
+int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll,
+                uint64_t* const* llp, const double* x0f, int grid, cudaStream_t st);
 
 // Multi-RHS CG (ks_multi.cu, SURVEY.md sec.8(f) "multi-RHS"): K <= kMaxRhs independent
 // CG recurrences sharing every pass over A (one GPU, FP64).  Per-column state:

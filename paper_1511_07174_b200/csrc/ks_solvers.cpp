@@ -139,9 +139,11 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
     int pgrid = 0, sgrid = 0, tgrid = 0;
     int prows = 0, punroll = 0;
     // tiny kernels: one GPU, the whole solve in one launch (they always finish it)
-    if (persist && c->P == 1 && c->opt.tiny && c->opt.small != 0 && B >= maxit)
-        tgrid = memo_grid(r, (2LL << 48) | kind, [&] { return tiny_grid(kind, r.num_sms, c->n, c->ld); });
-    if (tgrid > 0 && !r.ll) {
+    // tiny kernels: n <= 1024, the whole solve in one launch (they always finish it);
+    // P > 1 only with the fused exchange (their LL slots live in the exchange allocation)
+    if (persist && (c->P == 1 || (c->fused() && r.llx)) && c->opt.tiny && c->opt.small != 0 && B >= maxit)
+        tgrid = memo_grid(r, (2LL << 48) | kind, [&] { return tiny_grid(kind, r.num_sms, c->n, r.m, c->ld); });
+    if (tgrid > 0 && c->P == 1 && !r.ll) {
         dev_alloc_t(&r.ll, (size_t)(4 * c->ld));
         KS_CUDA(cudaMemsetAsync(r.ll, 0, (size_t)(4 * c->ld) * sizeof(uint64_t), r.stream));
     }
@@ -187,7 +189,8 @@ void run_loop(ks_ctx* c, Rank& r, int kind, int64_t maxit, int gemvs_per_iter, I
             prof.pre(slot);
             const bool z = r.bar_zeroed && k == 1;
             const int rc = tgrid > 0
-                ? launch_tiny(kind, r.vargs(false), r.A, c->ld, r.ll, tgrid, r.stream)
+                ? launch_tiny(kind, r.vargs(c->fused()), r.A, c->ld, c->P == 1 ? r.ll : r.llx, r.llpeer,
+                              r.x0_full, tgrid, r.stream)
                 : sgrid > 0
                 ? launch_small<double>(small_kind(c, kind), r.vargs(c->fused()), r.A, c->ld, c->ld,
                                        r.scr.part + 2 * kPartStride, r.scr.ticket + 8, k, kend, sgrid, r.stream, z)
@@ -409,6 +412,7 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
     VecArgs a = r.vargs(fused);
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
+    r.x0_full = x0 ? r.s_full : nullptr;     // setup() puts the full x0 there
     if (!x0) {
         start(c, r, 0, b, tol, maxit, hist_cap, ebase);     // A0 + init (+ rendezvous): one launch
     } else {
@@ -450,6 +454,7 @@ int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, doub
     VecArgs a = r.vargs(fused);
     const unsigned long long ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
+    r.x0_full = x0 ? r.s_full : nullptr;
     if (!x0) {
         start(c, r, 1, b, tol, maxit, hist_cap, ebase);     // B0 + init (+ rendezvous): one launch
     } else {

@@ -58,6 +58,14 @@ __device__ __forceinline__ void ll_store(uint64_t* slot, double v, uint32_t flag
     const uint64_t hi = (bits >> 32) | ((uint64_t)flag << 32);
     asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(lo), "l"(hi) : "memory");
 }
+// system scope: the LL words of the P > 1 variant are stored over NVLink into every
+// rank's buffer (each 8-byte word still single-copy atomic)
+__device__ __forceinline__ void ll_store_sys(uint64_t* slot, double v, uint32_t flag) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(v);
+    const uint64_t lo = (bits & 0xffffffffull) | ((uint64_t)flag << 32);
+    const uint64_t hi = (bits >> 32) | ((uint64_t)flag << 32);
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(lo), "l"(hi) : "memory");
+}
 __device__ __forceinline__ void ll_load(const uint64_t* slot, uint64_t& lo, uint64_t& hi) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
 }
@@ -67,6 +75,10 @@ __device__ __forceinline__ double ll_value(uint64_t lo, uint64_t hi) {
 
 __device__ __forceinline__ void ll_load2(const uint64_t* slot, uint64_t (&w)[4]) {
     asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(slot) : "memory");
+}
+__device__ __forceinline__ void ll_load2_sys(const uint64_t* slot, uint64_t (&w)[4]) {
+    asm volatile("ld.relaxed.sys.global.v4.u64 {%0, %1, %2, %3}, [%4];"
                  : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(slot) : "memory");
 }
 
@@ -94,7 +106,9 @@ __device__ __forceinline__ bool ll_gather(const uint64_t* slot, int n, uint32_t 
             if (have[u]) continue;
             const int j = 2 * threadIdx.x + 512 * u;
             uint64_t w[4];
-            if (wide) {
+            if (wide == 2) {
+                ll_load2_sys(slot + 2 * (int64_t)j, w);
+            } else if (wide) {
                 ll_load2(slot + 2 * (int64_t)j, w);
             } else {
                 ll_load(slot + 2 * (int64_t)j, w[0], w[1]);
@@ -270,7 +284,9 @@ struct TinyArgs {
     VecArgs a;
     const double* A;
     int64_t lda;
-    uint64_t* ll;        // 2 slots x ld entries x 2 words (LL format)
+    uint64_t* ll;        // 2 slots x ld entries x 2 words (LL format), this rank's
+    uint64_t* llp[kMaxRanks];   // P > 1: every rank's LL buffer (exchange allocation)
+    const double* x0f;   // P > 1: the full x0 (NULL: zero start)
     // debug (KS_TINY_TRACE=k): thread 0 of every CTA stamps %clock64 at the phase
     // boundaries of CG iteration k (kTrace stamps per CTA) and %globaltimer once
     unsigned long long* trace;
@@ -288,7 +304,7 @@ __device__ __forceinline__ void stamp(const TinyArgs& T, long long k, int i) {
     }
 }
 
-// This CTA's rows [rb, rb + R): balanced contiguous blocks.
+// This CTA's rows [rb, rb + R) of the rank's m rows: balanced contiguous blocks.
 __device__ __forceinline__ void my_rows(int n, int& rb, int& R) {
     const int q = n / (int)gridDim.x, rem = n % (int)gridDim.x, b = (int)blockIdx.x;
     rb = b * q + min(b, rem);
@@ -296,6 +312,17 @@ __device__ __forceinline__ void my_rows(int n, int& rb, int& R) {
 }
 
 __device__ __forceinline__ int col_of(int v) { return 2 * threadIdx.x + 512 * (v >> 1) + (v & 1); }
+
+// Publishes this CTA's rows (thread t < R: global row grow = row0 + rb + t) of the GEMV
+// output into slot `off` (words) of every rank's LL buffer (P = 1: the own buffer).
+__device__ __forceinline__ void ll_publish(const TinyArgs& T, int64_t off, int64_t grow, double v, uint32_t flag) {
+    const int P = T.a.L.P;
+    if (P == 1) {
+        ll_store(T.ll + off + 2 * grow, v, flag);
+    } else {
+        for (int g = 0; g < P; ++g) ll_store_sys(T.llp[g] + off + 2 * grow, v, flag);
+    }
+}
 
 // ------------------------------------------------------------------ CG (A1-A5)
 template <int V, int XM>
@@ -307,8 +334,11 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
     DevState* st = a.st;
     const int n = (int)a.L.n;
     if (is_done(st)) return;
+    const int P = a.L.P, m = (int)rows_of(a.L);
+    const int64_t row0 = a.L.row0[a.L.rank];
+    const int wide = P > 1 ? 2 : T.wide;           // P > 1: system-scope polls of the LL words
     int rb, R;
-    my_rows(n, rb, R);
+    my_rows(m, rb, R);
     double Ar[kRM][V];
     load_rows_reg<V>(T.A, T.lda, rb, R, Ar);
     double x[V], r[V], p[V];
@@ -316,9 +346,9 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
     for (int v = 0; v < V; ++v) {
         const int j = col_of(v);
         const bool in = j < n;
-        x[v] = in ? a.x_loc[j] : 0.0;
-        r[v] = in ? a.G_r[j] : 0.0;           // r0 (P = 1: chunk 0 = the full vector)
-        p[v] = in ? a.p_full[j] : 0.0;        // p0 = r0
+        x[v] = !in ? 0.0 : P == 1 ? a.x_loc[j] : (T.x0f ? T.x0f[j] : 0.0);   // x0 (replicated)
+        r[v] = in ? a.G_r[gidx(a.L, j)] : 0.0;  // r0 (gather buffer, parity 0: every rank has all of it)
+        p[v] = in ? a.p_full[j] : 0.0;          // p0 = r0
     }
     double rho = st->rho[0];
     const double nb = st->nb, tol = st->tol;
@@ -338,8 +368,8 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
         double q[V];
         bool got;
         if (XM == 0) {
-            if (threadIdx.x < R) ll_store(slot + 2 * (int64_t)(rb + threadIdx.x), qrow, flag);
-            got = ll_gather<V>(slot, n, flag, q, T.backoff, T.wide);
+            if (threadIdx.x < R) ll_publish(T, (int64_t)(k & 1) * 2 * T.lda, row0 + rb + threadIdx.x, qrow, flag);
+            got = ll_gather<V>(slot, n, flag, q, T.backoff, wide);
         } else {
             fx_put(slot, T.lda, rb, R, qrow, flag);
             got = fx_get<V>(slot, T.lda, n, flag, q);
@@ -386,7 +416,9 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int j = col_of(v);
-            if (j < n) { a.x_loc[j] = x[v]; a.p_full[j] = p[v]; a.G_r[j] = r[v]; }
+            if (j >= row0 && j < row0 + m) a.x_loc[j - row0] = x[v];      // own rows
+            if (j < n) a.p_full[j] = p[v];
+            if (P == 1 && j < n) a.G_r[j] = r[v];
         }
         if (threadIdx.x == 0) {
             st->iters = iters; st->status = status; st->converged = conv;
@@ -406,8 +438,11 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
     DevState* st = a.st;
     const int n = (int)a.L.n;
     if (is_done(st)) return;
+    const int P = a.L.P, m = (int)rows_of(a.L);
+    const int64_t row0 = a.L.row0[a.L.rank];
+    const int wide = P > 1 ? 2 : T.wide;           // P > 1: system-scope polls of the LL words
     int rb, R;
-    my_rows(n, rb, R);
+    my_rows(m, rb, R);
     double Ar[kRM][V];
     load_rows_reg<V>(T.A, T.lda, rb, R, Ar);
     double x[V], r[V], p[V], v_[V], rh[V];
@@ -415,9 +450,9 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
     for (int v = 0; v < V; ++v) {
         const int j = col_of(v);
         const bool in = j < n;
-        x[v] = in ? a.x_loc[j] : 0.0;
-        r[v] = in ? a.G_r[j] : 0.0;           // r0
-        rh[v] = in ? a.rhat_loc[j] : 0.0;     // rhat = r0 (Q7)
+        x[v] = !in ? 0.0 : P == 1 ? a.x_loc[j] : (T.x0f ? T.x0f[j] : 0.0);
+        r[v] = in ? a.G_r[gidx(a.L, j)] : 0.0;  // r0
+        rh[v] = r[v];                           // rhat = r0 (Q7)
         p[v] = 0.0;                           // v = p = 0 (Q8)
         v_[v] = 0.0;
     }
@@ -440,8 +475,8 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         double vrow = gemv_rows<V>(Ar, R, p, wred);
         bool got;
         if (XM == 0) {
-            if (threadIdx.x < R) ll_store(T.ll + 2 * (int64_t)(rb + threadIdx.x), vrow, fv);
-            got = ll_gather<V>(T.ll, n, fv, v_, T.backoff, T.wide);
+            if (threadIdx.x < R) ll_publish(T, 0, row0 + rb + threadIdx.x, vrow, fv);
+            got = ll_gather<V>(T.ll, n, fv, v_, T.backoff, wide);
         } else {
             fx_put(T.ll, T.lda, rb, R, vrow, fv);
             got = fx_get<V>(T.ll, T.lda, n, fv, v_);
@@ -480,8 +515,8 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         uint64_t* slot1 = T.ll + 2 * T.lda;
         double t[V];
         if (XM == 0) {
-            if (threadIdx.x < R) ll_store(slot1 + 2 * (int64_t)(rb + threadIdx.x), trow, ft);
-            got = ll_gather<V>(slot1, n, ft, t, T.backoff, T.wide);
+            if (threadIdx.x < R) ll_publish(T, 2 * T.lda, row0 + rb + threadIdx.x, trow, ft);
+            got = ll_gather<V>(slot1, n, ft, t, T.backoff, wide);
         } else {
             fx_put(slot1, T.lda, rb, R, trow, ft);
             got = fx_get<V>(slot1, T.lda, n, ft, t);
@@ -523,7 +558,9 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int j = col_of(v);
-            if (j < n) { a.x_loc[j] = x[v]; a.p_full[j] = p[v]; a.v_full[j] = v_[v]; a.G_r[j] = r[v]; }
+            if (j >= row0 && j < row0 + m) a.x_loc[j - row0] = x[v];      // own rows
+            if (j < n) { a.p_full[j] = p[v]; a.v_full[j] = v_[v]; }
+            if (P == 1 && j < n) a.G_r[j] = r[v];
         }
         if (threadIdx.x == 0) {
             st->iters = iters; st->status = status; st->converged = conv; st->breakdown = brk;
@@ -542,8 +579,8 @@ int xchg_mode() {
     const char* e = std::getenv("KS_TINY_XCHG");   // tuning: 0 = LL (default), 1 = ready flags
     return e && std::atoi(e) == 1 ? 1 : 0;
 }
-const void* kern_v(int bicgstab, int V) {
-    if (xchg_mode() == 1) return V == 2 ? kern<2, 1>(bicgstab) : kern<4, 1>(bicgstab);
+const void* kern_v(int bicgstab, int V, int P = 1) {
+    if (xchg_mode() == 1 && P == 1) return V == 2 ? kern<2, 1>(bicgstab) : kern<4, 1>(bicgstab);
     return V == 2 ? kern<2, 0>(bicgstab) : kern<4, 0>(bicgstab);
 }
 
@@ -553,12 +590,12 @@ const void* kern_v(int bicgstab, int V) {
 // length), 0 when not applicable: n <= 1024 (the full vectors fit in registers,
 // 4 values per thread and vector), every CTA's rows fit in registers (<= kRM),
 // one co-resident CTA per SM.
-int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld) {
-    if (n < 1 || n > 1024 || ld > 1024) return 0;
+int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t m, int64_t ld) {
+    if (n < 1 || n > 1024 || ld > 1024 || m < 1) return 0;
     const int V = ld <= 512 ? 2 : 4;
     int g = num_sms;
-    if (g > n) g = (int)n;
-    const int64_t rmax = (n + g - 1) / g;
+    if (g > m) g = (int)m;
+    const int64_t rmax = (m + g - 1) / g;
     if (rmax > kRM) return 0;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_v(bicgstab, V), kTT, 0) != cudaSuccess) {
@@ -568,13 +605,15 @@ int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t ld) {
     return per_sm >= 1 ? g : 0;
 }
 
-int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll, int grid,
-                cudaStream_t st) {
+int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll,
+                uint64_t* const* llp, const double* x0f, int grid, cudaStream_t st) {
     TinyArgs T;
     T.a = a;
     T.A = A;
     T.lda = lda;
     T.ll = ll;
+    for (int g = 0; g < kMaxRanks; ++g) T.llp[g] = (llp && g < a.L.P) ? llp[g] : nullptr;
+    T.x0f = x0f;
     T.trace = nullptr;
     T.trace_k = 0;
     T.backoff = 0;
@@ -589,7 +628,7 @@ int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, ui
         else cudaMemsetAsync(T.trace, 0, (size_t)grid * (kTrace + 1) * sizeof(unsigned long long), st);
     }
     void* args[] = {&T};
-    const cudaError_t e = cudaLaunchCooperativeKernel(kern_v(bicgstab, lda <= 512 ? 2 : 4), dim3((unsigned)grid),
+    const cudaError_t e = cudaLaunchCooperativeKernel(kern_v(bicgstab, lda <= 512 ? 2 : 4, a.L.P), dim3((unsigned)grid),
                                                       dim3(kTT), args, 0, st);
     if (T.trace) {                      // dump: one line per CTA, clock deltas then the start time
         std::vector<unsigned long long> h((size_t)grid * (kTrace + 1));

@@ -169,3 +169,40 @@ def test_tiny_not_used_for_multi_launch_batches():
         x, h, r = ctx.cg(b, tol=1e-10)
         bars(x, h, r, xo, ho, ro)
         assert r.kernel_launches >= 130 // 16
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_tiny_over_p_gpus(P):
+    """Tiny kernels over P GPUs (fused exchange): every rank's CTAs own its rows, the
+    LL words of the GEMV output go over NVLink into every rank's buffer, x, r, p are
+    replicated in every CTA of every rank.  CG and BiCGSTAB vs the oracle (x0 too),
+    tiny on vs off, and a repeated solve bitwise equal."""
+    if _ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    for n in (300, 1024):
+        A, b = gspd_any(n)
+        D, bd = synth.gdd(n, 16)
+        x0 = np.random.default_rng(n).standard_normal(n)
+        xo, ho, ro = oracle.cg(A, b, x0=x0, tol=1e-10)
+        yo, hyo, ryo = oracle.bicgstab(D, bd, tol=1e-10)
+        res = {}
+        for tiny in (1, 0):
+            with ks.Context(n, ngpus=P) as ctx, ks.Context(n, ngpus=P) as dtx:
+                ctx.set_option("tiny", tiny)
+                dtx.set_option("tiny", tiny)
+                ctx.load_rows(A)
+                dtx.load_rows(D)
+                x, h, r = ctx.cg(b, x0=x0, tol=1e-10)
+                bars(x, h, r, xo, ho, ro)
+                y, hy, ry = dtx.bicgstab(bd, tol=1e-10)
+                bars(y, hy, ry, yo, hyo, ryo, floor=FLOOR_BS)
+                assert ry.half_step_exit == ryo.half_step_exit
+                x2, h2, r2 = ctx.cg(b, x0=x0, tol=1e-10)
+                assert np.array_equal(x2, x) and np.array_equal(h2, h)
+                res[tiny] = (x, y)
+        assert not (np.array_equal(res[1][0], res[0][0]) and np.array_equal(res[1][1], res[0][1]))
