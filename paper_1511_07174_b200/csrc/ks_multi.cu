@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     }
     __syncthreads();
     if (peer && !pk::grid_sync(M.bar, st)) return;
-    if (*(volatile const int*)&st->done) return;
+    if (*(volatile const int*)&st->peer_timeout) return;   // the rendezvous failed (reset by the host)
     uint32_t it = 0;
     double sig[K];
     // ---- setup (row A0 per column): r0 = b - A x0 (or b), x = x0 (or 0), p = r0,

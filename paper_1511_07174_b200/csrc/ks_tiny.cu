@@ -280,6 +280,39 @@ __device__ __forceinline__ double gemv_rows(const double (&a)[kRM][V], int R, co
     return q;
 }
 
+// gemv_rows plus one CTA-wide sum riding on the same barrier: `side` (per-thread
+// partial) -> warp butterfly -> warp sums added in warp order (the tsum tree), so the
+// result is the same in every thread and every CTA.  (BiCGSTAB: ||s||^2 with t = A s.)
+template <int V>
+__device__ __forceinline__ double gemv_rows_side(const double (&a)[kRM][V], int R, const double (&x)[V],
+                                                 double* wred, double side, double& side_sum) {
+    double acc[kRM];
+#pragma unroll
+    for (int i = 0; i < kRM; ++i) {
+        acc[i] = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[i] = fma(a[i][v], x[v], acc[i]);
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) side += __shfl_xor_sync(0xffffffffu, side, o);
+    int row;
+    const double s = warp_rows8(acc, row);
+    if ((lane & 3) == 0) wred[row * kTW + w] = s;
+    if (lane == 0) wred[kRM * kTW + w] = side;
+    __syncthreads();
+    double q = 0.0;
+    if (threadIdx.x < R) {
+#pragma unroll
+        for (int ww = 0; ww < kTW; ++ww) q += wred[threadIdx.x * kTW + ww];
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kTW; ++ww) t += wred[kRM * kTW + ww];
+    side_sum = t;
+    return q;
+}
+
 struct TinyArgs {
     VecArgs a;
     const double* A;
@@ -431,7 +464,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
 template <int V, int XM>
 __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
-    __shared__ double wred[kRM * kTW];
+    __shared__ double wred[(kRM + 1) * kTW];
     __shared__ double red[2 * 2 * kTW];
     int par = 0;
     const VecArgs& a = T.a;
@@ -494,14 +527,17 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         if (gam == 0.0 || !isfinite(gam)) { status = KS_EBREAKDOWN; brk = 1; iters = i - 1; break; }
         alpha = rho / gam;
         double s[V];
-        double ss[1] = {0.0};
+        double ss = 0.0;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             s[v] = fma(-alpha, v_[v], r[v]);
-            ss[0] = fma(s[v], s[v], ss[0]);
+            ss = fma(s[v], s[v], ss);
         }
-        tsum<1>(ss, red, par);
-        const double srel = sqrt(ss[0]) / nb;
+        // B5 + B6: t rows = A s computed alongside ||s||^2 (one barrier for both); t is
+        // published only when the half-step test does not end the solve
+        double sst;
+        const double trow = gemv_rows_side<V>(Ar, R, s, wred, ss, sst);
+        const double srel = sqrt(sst) / nb;
         if (srel <= tol) {                                     // B5: half-step exit
 #pragma unroll
             for (int v = 0; v < V; ++v) x[v] = fma(alpha, p[v], x[v]);
@@ -511,7 +547,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         }
         // B6: t = A s, exchange (slot 1); <t, s>, <t, t>
         const uint32_t ft = fv + 1u;
-        const double trow = gemv_rows<V>(Ar, R, s, wred);
+
         uint64_t* slot1 = T.ll + 2 * T.lda;
         double t[V];
         if (XM == 0) {

@@ -82,6 +82,7 @@ def test_multi_small_cg_allgather_only(P, dtype):
         for small in (1, 0):
             with ks.Context(n, ngpus=P, dtype=dtype) as ctx:
                 ctx.set_option("small", small)
+                ctx.set_option("tiny", 0)     # the small-n kernels themselves (tiny: test_gpu_tiny.py)
                 ctx.generate("spd", seed=synth.SEED, table=c, want_b=False)
                 if dtype == "f32":
                     bb = b.astype(np.float32).astype(np.float64)
@@ -123,6 +124,7 @@ def test_multi_small_bicgstab_allgather_only(P, dtype):
         for small in (1, 0):
             with ks.Context(n, ngpus=P, dtype=dtype) as ctx:
                 ctx.set_option("small", small)
+                ctx.set_option("tiny", 0)     # the small-n kernels themselves (tiny: test_gpu_tiny.py)
                 ctx.load_rows(A)
                 if dtype == "f32":
                     x, h, r = ctx.bicgstab(b.astype(np.float32).astype(np.float64), tol=1e-5)

@@ -40,7 +40,8 @@ def test_multi_rhs_parity(n, nrhs):
 
 def test_multi_rhs_matches_single_rhs_cg():
     """Column k of the block solve meets the bars against the single-RHS GPU CG
-    (the same recurrence through K1/the persistent kernels)."""
+    (the same recurrence through K1/the persistent kernels); single- and multi-RHS
+    solves interleave on one context (their device states are independent)."""
     n = 2048
     A = gspd_any(n, 1e4)
     B = rhs_block(n, 6)
@@ -50,6 +51,10 @@ def test_multi_rhs_matches_single_rhs_cg():
         for k in range(6):
             x1, h1, r1 = ctx.cg(B[:, k], tol=1e-10)
             bars(X[:, k], h[k], r[k], x1, h1, r1)
+        X2, h2, r2 = ctx.cg_multi(B, tol=1e-10)        # after single-RHS solves
+        assert np.array_equal(X2, X) and [q.iterations for q in r2] == [q.iterations for q in r]
+        X3, _, r3 = ctx.cg_multi(B, tol=0.0, maxit=7)
+        assert all(q.iterations == 7 and q.status == ks.KS_EMAXIT for q in r3)
 
 
 def test_multi_rhs_x0_and_exits():

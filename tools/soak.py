@@ -24,22 +24,43 @@ rng = np.random.default_rng(2024)
 ctxs, fails, stats = {}, [], {"solves": 0, "iters": 0}
 t0 = time.time()
 for it in range(rounds):
-    n = int(rng.choice([1000, 2049, 4096, 5003]))
-    method = str(rng.choice(["cg", "bicgstab", "bicg", "gmres"]))
+    n = int(rng.choice([300, 777, 1024, 1000, 2049, 4096, 5003]))
+    method = str(rng.choice(["cg", "bicgstab", "bicg", "gmres", "cg_multi"]))
     if method == "cg" and n % 2:
         n += 1                                   # G-SPD needs an even n
     key = (n, method)
     if key not in ctxs:
         c = ks.Context.from_process_group(n) if WORLD > 1 else ks.Context(n, ngpus=P)
-        if method == "cg":
+        if method in ("cg", "cg_multi"):
             c.generate("spd", seed=synth.SEED, table=synth.spd_table(n, 1e3), want_b=False)
         else:
             c.generate("dd", seed=synth.SEED, kd=16, want_b=False)
-        c.set_option("poll_batch", int(rng.choice([1, 3, 16])))
+        # 0 = auto: one launch per solve (tiny kernels at n <= 1024); else split launches
+        c.set_option("poll_batch", int(rng.choice([0, 0, 1, 3, 16])))
         ctxs[key] = c
     c = ctxs[key]
     b = synth.rhs(n, synth.SEED + it)
+    if method == "cg_multi":                      # multi-RHS: a block of k right-hand sides
+        k = int(rng.integers(1, 9))
+        B = np.column_stack([synth.rhs(n, synth.SEED + 1000 * it + j) for j in range(k)])
+        if rng.random() < 0.3:
+            mx = int(rng.integers(1, 12))
+            X1, _, r1 = c.cg_multi(B, tol=0.0, maxit=mx)
+            X2, _, r2 = c.cg_multi(B, tol=0.0, maxit=mx)
+            if not np.array_equal(X1, X2):
+                fails.append({"round": it, "n": n, "method": method, "why": "not repeatable"})
+        else:
+            X, _, rs = c.cg_multi(B, tol=1e-10)
+            for j in range(k):
+                res = np.linalg.norm(c.matvec(X[:, j]) - B[:, j]) / np.linalg.norm(B[:, j])
+                if not (rs[j].converged and res <= 1e-8):
+                    fails.append({"round": it, "n": n, "method": method, "why": f"col {j} true {res}"})
+            stats["iters"] += max(q.iterations for q in rs)
+        stats["solves"] += 1
+        continue
     kw = {"restart": int(rng.choice([5, 20]))} if method == "gmres" else {}
+    if method in ("cg", "bicgstab") and rng.random() < 0.25:
+        kw["x0"] = rng.standard_normal(n)
     fixed = rng.random() < 0.3
     if fixed:
         mx = int(rng.integers(1, 12))
