@@ -7,9 +7,10 @@
 //
 // One persistent cooperative kernel per solve (one GPU), one CTA per SM, 8 consumer
 // warps + 1 TMA producer warp:
-//   * A is cut into bands of kMB = 32 rows (round-robin over the CTAs) and chunks of
-//     kMC = 128 columns; a stage = the A tile (32 x 128, 32 KiB) + the matching P tile
-//     (K x 128), both brought into shared memory by 2-D TMA loads
+//   * A is cut into bands of 32 rows (round-robin over the CTAs) and chunks of
+//     128 columns; a stage = the A tile (32 x 128, 32 KiB) + the matching P tile
+//     (K x 128), both brought into shared memory by 2-D TMA loads (K = 8: 64 x 64
+//     tiles, 8 rows per warp -- see the shape note below)
 //     (cp.async.bulk.tensor, tensor maps built on the host) completing on a
 //     full-mbarrier; kMS stages in flight; consumers release a stage through an
 //     empty-mbarrier (one arrival per warp);
@@ -27,6 +28,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "ks_device.cuh"
 #include "ks_common.cuh"
 #include "ks_internal.h"
@@ -37,8 +40,10 @@ namespace ks {
 
 namespace {
 
-constexpr int kMB = 32;                   // rows per band
-constexpr int kMC = 128;                  // columns per chunk
+// GEMM shape: WR rows per consumer warp (band = 8 WR rows), CH columns per chunk
+// (CH / 64 column pairs per lane).  (4, 128): 32 x 128 A tiles, the P pair reused for
+// 4 rows; (8, 64): 64 x 64 tiles, the P pair reused for 8 rows -- half the
+// shared-memory reads of P per FMA, for K = 8 where shared-memory bandwidth binds.
 constexpr int kMS = 4;                    // pipeline stages
 constexpr int kMW = 8;                    // consumer warps
 constexpr int kMT = (kMW + 1) * 32;       // + the producer warp
@@ -71,10 +76,10 @@ __device__ __forceinline__ void csum(double (&v)[K], double* red) {
     }
 }
 
-template <int K>
+template <int K, int WR, int CH>
 struct MultiSmem {
-    double A[kMS][kMB * kMC];
-    double P[kMS][K * kMC];
+    double A[kMS][8 * WR * CH];
+    double P[kMS][K * CH];
     uint64_t full[kMS], empty[kMS];
     double red[2 * K * kMW];
     double wpart[kMW][K];
@@ -82,26 +87,27 @@ struct MultiSmem {
 
 // Q = A P (this CTA's bands) and sigma partials <P_k, Q_k> over the CTA's rows in
 // band order.  `it` is the pipeline position, identical in producer and consumers.
-template <int K>
-__device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const MultiArgs& M, MultiSmem<K>& S,
-                           uint32_t& it, double (&sig)[K]) {
+template <int K, int WR, int CH>
+__device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const MultiArgs& M,
+                           MultiSmem<K, WR, CH>& S, uint32_t& it, double (&sig)[K]) {
+    constexpr int BAND = kMW * WR, NP = CH / 64;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nbands = (int)((M.m + kMB - 1) / kMB);
-    const int nchunks = (int)(M.ld / kMC);
+    const int nbands = (int)((M.m + BAND - 1) / BAND);
+    const int nchunks = (int)(M.ld / CH);
 #pragma unroll
     for (int k = 0; k < K; ++k) sig[k] = 0.0;
     if (w == kMW) {                                        // ---- TMA producer warp
         if (lane == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");   // P written by the generic proxy
-            const uint32_t bytes = (uint32_t)(kMB * kMC + K * kMC) * sizeof(double);
+            const uint32_t bytes = (uint32_t)(BAND * CH + K * CH) * sizeof(double);
             for (int b = blockIdx.x; b < nbands; b += gridDim.x) {
                 for (int c = 0; c < nchunks; ++c, ++it) {
                     const int s = (int)(it % kMS);
                     const uint32_t ph = (it / kMS) & 1u;
                     mbar_wait(&S.empty[s], ph ^ 1u);
                     mbar_expect_tx(&S.full[s], bytes);
-                    tma_load_2d(S.A[s], tmA, c * kMC, b * kMB, &S.full[s]);
-                    tma_load_2d(S.P[s], tmP, c * kMC, 0, &S.full[s]);
+                    tma_load_2d(S.A[s], tmA, c * CH, b * BAND, &S.full[s]);
+                    tma_load_2d(S.P[s], tmP, c * CH, 0, &S.full[s]);
                 }
             }
         } else {
@@ -110,25 +116,25 @@ __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const
         return;
     }
     for (int b = blockIdx.x; b < nbands; b += gridDim.x) {  // ---- consumer warps
-        double acc[4][K];
+        double acc[WR][K];
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr)
+        for (int rr = 0; rr < WR; ++rr)
 #pragma unroll
             for (int k = 0; k < K; ++k) acc[rr][k] = 0.0;
         for (int c = 0; c < nchunks; ++c, ++it) {
             const int s = (int)(it % kMS);
             const uint32_t ph = (it / kMS) & 1u;
             mbar_wait(&S.full[s], ph);
-            const double* At = S.A[s] + (4 * w) * kMC + 2 * lane;
+            const double* At = S.A[s] + (WR * w) * CH + 2 * lane;
             const double* Pt = S.P[s] + 2 * lane;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < NP; ++u) {
                 double2 p[K];
 #pragma unroll
-                for (int k = 0; k < K; ++k) p[k] = *reinterpret_cast<const double2*>(Pt + k * kMC + 64 * u);
+                for (int k = 0; k < K; ++k) p[k] = *reinterpret_cast<const double2*>(Pt + k * CH + 64 * u);
 #pragma unroll
-                for (int rr = 0; rr < 4; ++rr) {
-                    const double2 a = *reinterpret_cast<const double2*>(At + rr * kMC + 64 * u);
+                for (int rr = 0; rr < WR; ++rr) {
+                    const double2 a = *reinterpret_cast<const double2*>(At + rr * CH + 64 * u);
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         acc[rr][k] = fma(a.x, p[k].x, acc[rr][k]);
@@ -140,13 +146,13 @@ __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const
             if (lane == 0) mbar_arrive(&S.empty[s]);
         }
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr)
+        for (int rr = 0; rr < WR; ++rr)
 #pragma unroll
             for (int k = 0; k < K; ++k) acc[rr][k] = warp_sum(acc[rr][k]);
         if (lane == 0) {
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-                const int64_t row = (int64_t)b * kMB + 4 * w + rr;
+            for (int rr = 0; rr < WR; ++rr) {
+                const int64_t row = (int64_t)b * BAND + WR * w + rr;
                 if (row < M.m) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
@@ -208,11 +214,11 @@ __device__ __forceinline__ int64_t mr_off(const MultiArgs& M, int par, int g, in
     return (((int64_t)par * M.L.P + g) * kMaxRhs + k) * M.L.chunk;
 }
 
-template <int K>
-__global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensorMap tmA,
+template <int K, int WR, int CH>
+__global__ void __maxnreg__(224) k_cgm(const __grid_constant__ CUtensorMap tmA,
                                                const __grid_constant__ CUtensorMap tmP, MultiArgs M) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    MultiSmem<K>& S = *reinterpret_cast<MultiSmem<K>*>(
+    MultiSmem<K, WR, CH>& S = *reinterpret_cast<MultiSmem<K, WR, CH>*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     MultiState* ms = M.ms;
     DevState* st = M.st;
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     // ---- setup (row A0 per column): r0 = b - A x0 (or b), x = x0 (or 0), p = r0,
     // nb = ||b||, rho0 = <r0, r0>, the 0-iteration exits (Q2, Q6)
     if (M.has_x0) {                        // P holds the full x0 (host copy): Q = A x0
-        gemm_phase<K>(&tmA, &tmP, M, S, it, sig);
+        gemm_phase<K, WR, CH>(&tmA, &tmP, M, S, it, sig);
         if (!pk::grid_sync(M.bar, st)) return;   // every CTA's rows of Q before they are read
     }
     {
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
         for (int k = 0; k < K; ++k) { act[k] = *(volatile const int*)&ms->col[k].active; any |= act[k]; }
         if (!any) break;
         // A1: Q = A P, sigma partials
-        gemm_phase<K>(&tmA, &tmP, M, S, it, sig);
+        gemm_phase<K, WR, CH>(&tmA, &tmP, M, S, it, sig);
         __syncthreads();
         if ((tid & 31) == 0 && tid < kMCT) {
 #pragma unroll
@@ -462,10 +468,19 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     }
 }
 
-template <int K>
-const void* kern_m() { return (const void*)k_cgm<K>; }
-size_t smem_m(int K) {
-    const size_t b = K <= 4 ? sizeof(MultiSmem<4>) : sizeof(MultiSmem<8>);
+// shapes: 0 = (4 rows/warp, 128 columns), 1 = (8, 64)
+int multi_shape(int K) {
+    if (const char* e = std::getenv("KS_MULTI_SHAPE")) return std::atoi(e) == 1 ? 1 : 0;   // tuning
+    return K == 8 ? 1 : 0;
+}
+const void* kern_m(int K, int shape) {
+    if (K == 4) return shape == 1 ? (const void*)k_cgm<4, 8, 64> : (const void*)k_cgm<4, 4, 128>;
+    return shape == 1 ? (const void*)k_cgm<8, 8, 64> : (const void*)k_cgm<8, 4, 128>;
+}
+size_t smem_m(int K, int shape) {
+    size_t b;
+    if (K == 4) b = shape == 1 ? sizeof(MultiSmem<4, 8, 64>) : sizeof(MultiSmem<4, 4, 128>);
+    else b = shape == 1 ? sizeof(MultiSmem<8, 8, 64>) : sizeof(MultiSmem<8, 4, 128>);
     return b + 1024;
 }
 
@@ -474,8 +489,9 @@ size_t smem_m(int K) {
 int multi_k(int nrhs) { return nrhs <= 4 ? 4 : nrhs <= 8 ? 8 : 0; }
 
 int multi_grid(int K, int num_sms) {
-    const void* k = K == 4 ? kern_m<4>() : kern_m<8>();
-    const size_t sm = smem_m(K);
+    const int shape = multi_shape(K);
+    const void* k = kern_m(K, shape);
+    const size_t sm = smem_m(K, shape);
     int dev = 0, optin = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
@@ -517,15 +533,17 @@ static bool make_map(CUtensorMap* tm, const double* base, int64_t rows, int64_t 
 }
 
 int launch_cg_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st) {
+    const int shape = multi_shape(K);
+    const int band = shape == 1 ? 64 : 32, ch = shape == 1 ? 64 : 128;
     CUtensorMap tmA, tmP;
-    if (!make_map(&tmA, A, M.m, M.ld, M.ld, kMB, kMC)) return -(int)cudaErrorInvalidValue;
-    if (!make_map(&tmP, M.Pf, K, M.ld, M.ld, K, kMC)) return -(int)cudaErrorInvalidValue;
+    if (!make_map(&tmA, A, M.m, M.ld, M.ld, band, ch)) return -(int)cudaErrorInvalidValue;
+    if (!make_map(&tmP, M.Pf, K, M.ld, M.ld, K, ch)) return -(int)cudaErrorInvalidValue;
     cudaError_t e = cudaMemsetAsync(M.bar, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return -(int)e;
     MultiArgs Mc = M;
     void* args[] = {&tmA, &tmP, &Mc};
-    e = cudaLaunchCooperativeKernel(K == 4 ? kern_m<4>() : kern_m<8>(), dim3((unsigned)grid), dim3(kMT), args,
-                                    smem_m(K), st);
+    e = cudaLaunchCooperativeKernel(kern_m(K, shape), dim3((unsigned)grid), dim3(kMT), args,
+                                    smem_m(K, shape), st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 

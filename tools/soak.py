@@ -26,7 +26,7 @@ t0 = time.time()
 for it in range(rounds):
     n = int(rng.choice([300, 777, 1024, 1000, 2049, 4096, 5003]))
     method = str(rng.choice(["cg", "bicgstab", "bicg", "gmres", "cg_multi"]))
-    if method == "cg" and n % 2:
+    if method in ("cg", "cg_multi") and n % 2:
         n += 1                                   # G-SPD needs an even n
     key = (n, method)
     if key not in ctxs:
