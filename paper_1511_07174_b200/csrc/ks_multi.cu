@@ -5,16 +5,16 @@
 // K/4 flop per byte instead of 1/4.  FP64 on the CUDA cores -- B200's FP64 tensor
 // path is no faster than the FP64 pipes, and at K <= 8 the GEMM stays HBM-bound.
 //
-// One persistent cooperative kernel per solve (one GPU), one CTA per SM, 8 consumer
-// warps + 1 TMA producer warp:
-//   * A is cut into bands of 32 rows (round-robin over the CTAs) and chunks of
-//     128 columns; a stage = the A tile (32 x 128, 32 KiB) + the matching P tile
-//     (K x 128), both brought into shared memory by 2-D TMA loads (K = 8: 64 x 64
+// One persistent cooperative kernel per solve, one CTA per SM, 7 consumer warps +
+// 1 TMA producer warp:
+//   * A is cut into bands of 28 rows (round-robin over the CTAs) and chunks of
+//     128 columns; a stage = the A tile (28 x 128, 28 KiB) + the matching P tile
+//     (K x 128), both brought into shared memory by 2-D TMA loads (K = 8: 56 x 64
 //     tiles, 8 rows per warp -- see the shape note below)
 //     (cp.async.bulk.tensor, tensor maps built on the host) completing on a
 //     full-mbarrier; kMS stages in flight; consumers release a stage through an
 //     empty-mbarrier (one arrival per warp);
-//   * consumer warp w owns rows 4w..4w+3 of the band, lane l the column pairs
+//   * consumer warp w owns rows 4w..4w+3 of the band (shape (4, 128)), lane l the column pairs
 //     2l and 64 + 2l of each chunk: 4 x K accumulators per thread, the P pair loaded
 //     once per column pair and reused for the 4 rows (shared-memory traffic ~3x the
 //     A bytes at K = 8, conflict-free 512-byte rows);
@@ -40,12 +40,14 @@ namespace ks {
 
 namespace {
 
-// GEMM shape: WR rows per consumer warp (band = 8 WR rows), CH columns per chunk
-// (CH / 64 column pairs per lane).  (4, 128): 32 x 128 A tiles, the P pair reused for
-// 4 rows; (8, 64): 64 x 64 tiles, the P pair reused for 8 rows -- half the
+// GEMM shape: WR rows per consumer warp (band = kMW WR rows), CH columns per chunk
+// (CH / 64 column pairs per lane).  (4, 128): 28 x 128 A tiles, the P pair reused for
+// 4 rows; (8, 64): 56 x 64 tiles, the P pair reused for 8 rows -- half the
 // shared-memory reads of P per FMA, for K = 8 where shared-memory bandwidth binds.
 constexpr int kMS = 4;                    // pipeline stages
-constexpr int kMW = 8;                    // consumer warps
+// 7 consumer warps + 1 producer warp = 8 warps, 2 per SM sub-partition: up to 255
+// registers per thread (9 warps put 3 on one sub-partition, capping them at 168)
+constexpr int kMW = 7;                    // consumer warps
 constexpr int kMT = (kMW + 1) * 32;       // + the producer warp
 constexpr int kMCT = kMW * 32;            // consumer threads
 
@@ -78,7 +80,7 @@ __device__ __forceinline__ void csum(double (&v)[K], double* red) {
 
 template <int K, int WR, int CH>
 struct MultiSmem {
-    double A[kMS][8 * WR * CH];
+    double A[kMS][kMW * WR * CH];
     double P[kMS][K * CH];
     uint64_t full[kMS], empty[kMS];
     double red[2 * K * kMW];
@@ -215,7 +217,7 @@ __device__ __forceinline__ int64_t mr_off(const MultiArgs& M, int par, int g, in
 }
 
 template <int K, int WR, int CH>
-__global__ void __maxnreg__(224) k_cgm(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensorMap tmA,
                                                const __grid_constant__ CUtensorMap tmP, MultiArgs M) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     MultiSmem<K, WR, CH>& S = *reinterpret_cast<MultiSmem<K, WR, CH>*>(
@@ -534,7 +536,7 @@ static bool make_map(CUtensorMap* tm, const double* base, int64_t rows, int64_t 
 
 int launch_cg_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st) {
     const int shape = multi_shape(K);
-    const int band = shape == 1 ? 64 : 32, ch = shape == 1 ? 64 : 128;
+    const int band = kMW * (shape == 1 ? 8 : 4), ch = shape == 1 ? 64 : 128;
     CUtensorMap tmA, tmP;
     if (!make_map(&tmA, A, M.m, M.ld, M.ld, band, ch)) return -(int)cudaErrorInvalidValue;
     if (!make_map(&tmP, M.Pf, K, M.ld, M.ld, K, ch)) return -(int)cudaErrorInvalidValue;

@@ -695,6 +695,7 @@ def test_c_example_runs():
     assert d["bicgstab"]["converged"] == 1 and abs(d["bicgstab"]["iterations"] - 30) <= 2   # App. A.8
     assert d["bicgstab"]["true_relres"] <= 1e-9
     assert d["cg"]["converged"] == 1 and d["cg"]["true_relres"] <= 1e-10
+    assert d["cg_multi"]["converged"] == 1 and d["cg_multi"]["max_true_relres"] <= 1e-10
 
 
 def test_option_validation_and_roundtrip():
