@@ -4,6 +4,7 @@ iterations/s, right-hand-side-iterations/s and the A-stream GB/s of the TMA-fed
 skinny GEMM (8 n^2 bytes per iteration, algorithmic), next to single-RHS ks_cg.
 
     python tools/multi_rhs_bench.py [--size 65536] [--iters 20]
+    torchrun --nproc-per-node P tools/multi_rhs_bench.py      (row blocks over P GPUs)
 """
 import argparse
 import json
@@ -22,25 +23,37 @@ def main():
     import paper_1511_07174_b200 as ks
     import synth
     n, K = a.size, a.iters
-    with ks.Context(n) as ctx:
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        local = int(os.environ["LOCAL_RANK"])
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    out = print if rank == 0 else (lambda *x, **y: None)
+    with (ks.Context.from_process_group(n) if world > 1 else ks.Context(n)) as ctx:
         b = ctx.generate("spd", seed=synth.SEED, table=synth.spd_table(n, 1e4))
         ctx.set_option("true_residual", 0)
         ctx.cg(b, tol=0.0, maxit=2, hist=False)
         _, _, r1 = ctx.cg(b, tol=0.0, maxit=K, hist=False)
         single = K / r1.seconds_loop
-        print(json.dumps({"nrhs": 1, "kernel": "ks_cg", "iters_per_s": single,
-                          "GBps": 8.0 * n * n * single / 1e9}), flush=True)
+        out(json.dumps({"P": world, "nrhs": 1, "kernel": "ks_cg", "iters_per_s": single,
+                        "GBps_per_gpu": 8.0 * n * n * single / world / 1e9}), flush=True)
         for nrhs in (1, 2, 4, 8):
             B = np.column_stack([b] + [synth.rhs(n, synth.SEED + j) for j in range(1, nrhs)])
             ctx.cg_multi(B, tol=0.0, maxit=2, hist=False)
             X, h, r = ctx.cg_multi(B, tol=0.0, maxit=K, hist=False)
             t = r[0].seconds_loop
             ips = K / t
-            print(json.dumps({"nrhs": nrhs, "kernel": "ks_cg_multi", "iters_per_s": ips,
-                              "rhs_iters_per_s": nrhs * ips, "GBps": 8.0 * n * n * ips / 1e9,
+            out(json.dumps({"P": world, "nrhs": nrhs, "kernel": "ks_cg_multi", "iters_per_s": ips,
+                              "rhs_iters_per_s": nrhs * ips, "GBps_per_gpu": 8.0 * n * n * ips / world / 1e9,
                               "speedup_vs_single_rhs_cg": nrhs * ips / single,
                               "statuses": [q.status for q in r]}), flush=True)
 
 
 if __name__ == "__main__":
     main()
+    if int(os.environ.get("WORLD_SIZE", 1)) > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
