@@ -44,7 +44,9 @@ namespace {
 // (CH / 64 column pairs per lane).  (4, 128): 28 x 128 A tiles, the P pair reused for
 // 4 rows; (8, 64): 56 x 64 tiles, the P pair reused for 8 rows -- half the
 // shared-memory reads of P per FMA, for K = 8 where shared-memory bandwidth binds.
-constexpr int kMS = 4;                    // pipeline stages
+// pipeline stages of a shape: 4, or 3 when a stage holds 56 KiB of A (8 x 128)
+template <int WR, int CH>
+struct Stages { static constexpr int value = (WR * CH >= 1024) ? 3 : 4; };
 // 7 consumer warps + 1 producer warp = 8 warps, 2 per SM sub-partition: up to 255
 // registers per thread (9 warps put 3 on one sub-partition, capping them at 168)
 constexpr int kMW = 7;                    // consumer warps
@@ -80,6 +82,7 @@ __device__ __forceinline__ void csum(double (&v)[K], double* red) {
 
 template <int K, int WR, int CH>
 struct MultiSmem {
+    static constexpr int kMS = Stages<WR, CH>::value;
     double A[kMS][kMW * WR * CH];
     double P[kMS][K * CH];
     uint64_t full[kMS], empty[kMS];
@@ -93,6 +96,7 @@ template <int K, int WR, int CH>
 __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const MultiArgs& M,
                            MultiSmem<K, WR, CH>& S, uint32_t& it, double (&sig)[K]) {
     constexpr int BAND = kMW * WR, NP = CH / 64;
+    constexpr int kMS = MultiSmem<K, WR, CH>::kMS;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nbands = (int)((M.m + BAND - 1) / BAND);
     const int nchunks = (int)(M.ld / CH);
@@ -129,7 +133,8 @@ __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const
             mbar_wait(&S.full[s], ph);
             const double* At = S.A[s] + (WR * w) * CH + 2 * lane;
             const double* Pt = S.P[s] + 2 * lane;
-#pragma unroll
+            constexpr int UNP = WR >= 8 ? 1 : NP;   // 8 rows x K: one column pair live at a time
+#pragma unroll UNP
             for (int u = 0; u < NP; ++u) {
                 double2 p[K];
 #pragma unroll
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     const int64_t m = M.m;
     const bool peer = M.peer != 0;
     if (tid == 0) {
-        for (int s = 0; s < kMS; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kMW); }
+        for (int s = 0; s < MultiSmem<K, WR, CH>::kMS; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kMW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid == kMW * 32) {
@@ -470,19 +475,26 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     }
 }
 
-// shapes: 0 = (4 rows/warp, 128 columns), 1 = (8, 64)
+// shapes: 0 = (4 rows/warp, 128 columns, 4 stages), 1 = (8, 64, 4), 2 = (8, 128, 3)
 int multi_shape(int K) {
-    if (const char* e = std::getenv("KS_MULTI_SHAPE")) return std::atoi(e) == 1 ? 1 : 0;   // tuning
+    if (const char* e = std::getenv("KS_MULTI_SHAPE")) {                // tuning
+        const int v = std::atoi(e);
+        return v == 1 || v == 2 ? v : 0;
+    }
     return K == 8 ? 1 : 0;
 }
 const void* kern_m(int K, int shape) {
-    if (K == 4) return shape == 1 ? (const void*)k_cgm<4, 8, 64> : (const void*)k_cgm<4, 4, 128>;
-    return shape == 1 ? (const void*)k_cgm<8, 8, 64> : (const void*)k_cgm<8, 4, 128>;
+    if (K == 4) return shape == 1 ? (const void*)k_cgm<4, 8, 64>
+                     : shape == 2 ? (const void*)k_cgm<4, 8, 128> : (const void*)k_cgm<4, 4, 128>;
+    return shape == 1 ? (const void*)k_cgm<8, 8, 64>
+         : shape == 2 ? (const void*)k_cgm<8, 8, 128> : (const void*)k_cgm<8, 4, 128>;
 }
 size_t smem_m(int K, int shape) {
     size_t b;
-    if (K == 4) b = shape == 1 ? sizeof(MultiSmem<4, 8, 64>) : sizeof(MultiSmem<4, 4, 128>);
-    else b = shape == 1 ? sizeof(MultiSmem<8, 8, 64>) : sizeof(MultiSmem<8, 4, 128>);
+    if (K == 4) b = shape == 1 ? sizeof(MultiSmem<4, 8, 64>) : shape == 2 ? sizeof(MultiSmem<4, 8, 128>)
+                                                                        : sizeof(MultiSmem<4, 4, 128>);
+    else b = shape == 1 ? sizeof(MultiSmem<8, 8, 64>) : shape == 2 ? sizeof(MultiSmem<8, 8, 128>)
+                                                                   : sizeof(MultiSmem<8, 4, 128>);
     return b + 1024;
 }
 
@@ -536,7 +548,7 @@ static bool make_map(CUtensorMap* tm, const double* base, int64_t rows, int64_t 
 
 int launch_cg_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st) {
     const int shape = multi_shape(K);
-    const int band = kMW * (shape == 1 ? 8 : 4), ch = shape == 1 ? 64 : 128;
+    const int band = kMW * (shape == 0 ? 4 : 8), ch = shape == 1 ? 64 : 128;
     CUtensorMap tmA, tmP;
     if (!make_map(&tmA, A, M.m, M.ld, M.ld, band, ch)) return -(int)cudaErrorInvalidValue;
     if (!make_map(&tmP, M.Pf, K, M.ld, M.ld, K, ch)) return -(int)cudaErrorInvalidValue;
