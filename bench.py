@@ -426,7 +426,7 @@ def run_ours(args):
         extras["multi_rhs_cg"] = {
             "nrhs": 8, "iters_per_s": ips_m, "rhs_iters_per_s": 8 * ips_m,
             "A_stream_GBps": 8.0 * n * n * ips_m / 1e9, "vs_single_rhs_cg": 8 * ips_m / (K / cg_loop),
-            "kernel": "k_cgm<8,8,64> (TMA 2-D tensor-map loads, producer warp + 7 consumer warps, FP64 skinny GEMM)"}
+            "kernel": "k_cgm<8,8,128> (TMA 2-D tensor-map loads, producer warp + 7 consumer warps, FP64 skinny GEMM)"}
         with ks.Context.from_rank(1024, 0, 1, None, local, stream.cuda_stream) as c1:
             bt = c1.generate("spd", seed=SEED, table=synth.spd_table(1024, 1e3))
             c1.cg(bt, tol=0.0, maxit=2, hist=False)

@@ -42,8 +42,9 @@ namespace {
 
 // GEMM shape: WR rows per consumer warp (band = kMW WR rows), CH columns per chunk
 // (CH / 64 column pairs per lane).  (4, 128): 28 x 128 A tiles, the P pair reused for
-// 4 rows; (8, 64): 56 x 64 tiles, the P pair reused for 8 rows -- half the
-// shared-memory reads of P per FMA, for K = 8 where shared-memory bandwidth binds.
+// 4 rows; (8, 64) and (8, 128): 56-row bands, the P pair reused for 8 rows -- half the
+// shared-memory reads of P per FMA.  (8, 128) with 3 stages of 64 KiB is the default
+// (1 KiB row segments per TMA box row; best for K = 4 and 8 on the same box).
 // pipeline stages of a shape: 4, or 3 when a stage holds 56 KiB of A (8 x 128)
 template <int WR, int CH>
 struct Stages { static constexpr int value = (WR * CH >= 1024) ? 3 : 4; };
@@ -481,7 +482,8 @@ int multi_shape(int K) {
         const int v = std::atoi(e);
         return v == 1 || v == 2 ? v : 0;
     }
-    return K == 8 ? 1 : 0;
+    (void)K;
+    return 2;   // measured best for K = 4 and 8 (profiles/r02_multi_rhs_shapes.jsonl)
 }
 const void* kern_m(int K, int shape) {
     if (K == 4) return shape == 1 ? (const void*)k_cgm<4, 8, 64>

@@ -323,14 +323,10 @@ int coop_grid(const void* kern, int num_sms, int64_t mmax, int R) {
     const int64_t cap = (int64_t)per_sm * num_sms;
     const int64_t tiles = (mmax + R - 1) / R;
     int64_t g = tiles < num_sms ? num_sms : tiles;
-    if (g > cap) {
-        // tiles are dealt round-robin, so a GEMV takes ceil(tiles / g) tiles' time: use
-        // the fewest CTAs that keep that wave count (every CTA then gets w or w - 1
-        // tiles): n = 65536 has 32768 two-row tiles, 592 CTAs -> 55.35 waves padded to
-        // 56 (1.2 % of every GEMV lost); 586 CTAs -> 55.92.
-        const int64_t waves = (tiles + cap - 1) / cap;
-        g = (tiles + waves - 1) / waves;
-    }
+    // (Tried in round 2: the fewest CTAs keeping the wave count -- 586 instead of 592 at
+    // n = 65536 to fill the last wave; no gain at n = 65536 and a loss where it cut the
+    // grid to 512 CTAs (n = 16384, P = 4): fewer loads in flight.  Full occupancy wins.)
+    if (g > cap) g = cap;
     return (int)g;
 }
 

@@ -32,8 +32,8 @@ void persist_shape(const ks_ctx* c, const Rank& r, int* rows, int* unroll) {
     const int64_t cap = 4LL * r.num_sms, m = r.L.pslot;
     auto fill = [&](int64_t R) {                  // useful fraction of the last-wave-padded work
         const int64_t tiles = (m + R - 1) / R;
-        const int64_t waves = (tiles + cap - 1) / cap;
-        const int64_t G = (tiles + waves - 1) / waves;   // coop_grid's CTA count
+        const int64_t G = std::min(tiles, cap);     // coop_grid's CTA count
+        const int64_t waves = (tiles + G - 1) / G;
         return (double)tiles / (double)(waves * G);
     };
     const int def_r = m <= 4096 ? 4 : 2;
