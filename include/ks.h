@@ -255,6 +255,16 @@ ks_status ks_gmres(ks_ctx* ctx, const double* b, const double* x0, double tol, i
 ks_status ks_cg_multi(ks_ctx* ctx, int32_t nrhs, const double* B, const double* X0, double tol, int64_t maxit,
                       double* X, double* hist, int64_t hist_cap, ks_report* reps);
 
+/* Multi-RHS BiCGSTAB (reading Q30 applied to sec.8(c).4): nrhs (1..8) independent
+ * BiCGSTAB recurrences -- column k is exactly ks_bicgstab on (A, b_k): own rho,
+ * alpha, omega, breakdown tests and half-step exit -- sharing both GEMMs of every
+ * iteration (v = A P and t = A S, TMA-fed, FP64).  Arguments, layouts and reports as
+ * ks_cg_multi (half_step_exit, breakdown, matvecs = 2 iterations - half per column).
+ * One GPU (P == 1; else KS_EARG), FP64.  Returns the worst column status:
+ * KS_EBREAKDOWN > KS_EMAXIT > KS_OK.                                              */
+ks_status ks_bicgstab_multi(ks_ctx* ctx, int32_t nrhs, const double* B, const double* X0, double tol,
+                            int64_t maxit, double* X, double* hist, int64_t hist_cap, ks_report* reps);
+
 /* y = A^T x (n doubles each): the transposed GEMV building block of BiCG (K1T). */
 ks_status ks_matvec_t(ks_ctx* ctx, const double* x, double* y);
 

@@ -264,6 +264,25 @@ def cg_multi(A, B, X0=None, tol=1e-8, maxit=None):
     return X, hs, reps
 
 
+def bicgstab_multi(A, B, X0=None, tol=1e-8, maxit=None):
+    """Multi-RHS BiCGSTAB (reading Q30 applied to SURVEY.md sec.8(c).4):
+    column k of B solved by ``bicgstab`` on (A, B[:, k]) -- the recurrences are
+    independent; the GPU shares the two GEMMs of each iteration between the columns.
+    Returns (X n x nrhs, [hist_k], [report_k])."""
+    B = np.asarray(B, dtype=np.float64)
+    if B.ndim != 2:
+        raise ValueError("B must be n x nrhs")
+    X = np.empty_like(B)
+    hs, reps = [], []
+    for k in range(B.shape[1]):
+        x0 = None if X0 is None else np.asarray(X0, dtype=np.float64)[:, k]
+        x, h, r = bicgstab(A, B[:, k], x0=x0, tol=tol, maxit=maxit)
+        X[:, k] = x
+        hs.append(h)
+        reps.append(r)
+    return X, hs, reps
+
+
 def gemv_t(A, x) -> np.ndarray:
     """y = A^T x for row-major A (sequential sums over rows)."""
     A = np.ascontiguousarray(A, dtype=np.float64)

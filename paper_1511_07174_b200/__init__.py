@@ -34,7 +34,7 @@ OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 
            "tiny": 14}
 EXPORTS = ["ks_create", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
            "ks_generate", "ks_matvec", "ks_matvec_t", "ks_time_matvec", "ks_cg", "ks_bicgstab",
-           "ks_bicg", "ks_gmres", "ks_cg_multi",
+           "ks_bicg", "ks_gmres", "ks_cg_multi", "ks_bicgstab_multi",
            "ks_set_option", "ks_get_option", "ks_info", "ks_check_guards", "ks_last_error", "ks_version"]
 
 
@@ -106,6 +106,7 @@ def lib():
             "ks_cg": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
             "ks_bicgstab": [vp, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
             "ks_cg_multi": [vp, i32, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
+            "ks_bicgstab_multi": [vp, i32, vp, vp, dbl, i64, vp, vp, i64, C.POINTER(_Report)],
             "ks_set_option": [vp, C.c_int, i64],
             "ks_get_option": [vp, C.c_int, C.POINTER(i64)],
             "ks_info": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64), C.POINTER(i64)],
@@ -350,6 +351,14 @@ class Context:
         """Multi-RHS CG (ks_cg_multi): B is n x nrhs (1 <= nrhs <= 8), column k one
         right-hand side; independent CG recurrences sharing every pass over A.
         Returns (X n x nrhs, [hist_k], [Report_k])."""
+        return self._multi(lib().ks_cg_multi, B, X0, tol, maxit, hist, hist_cap)
+
+    def bicgstab_multi(self, B, X0=None, tol: float = 1e-8, maxit: int | None = None, *, hist=True,
+                       hist_cap: int = 1 << 16):
+        """Multi-RHS BiCGSTAB (ks_bicgstab_multi, one GPU): as cg_multi."""
+        return self._multi(lib().ks_bicgstab_multi, B, X0, tol, maxit, hist, hist_cap)
+
+    def _multi(self, fn, B, X0, tol, maxit, hist, hist_cap):
         B = np.asfortranarray(B, dtype=np.float64)
         if B.ndim != 2 or B.shape[0] != self.n:
             raise ValueError(f"B must be ({self.n}, nrhs)")
@@ -362,8 +371,8 @@ class Context:
         cap = max(1, min(maxit, hist_cap)) if hist else 0
         H = np.zeros((cap, k), order="F") if hist else None
         reps = (_Report * k)()
-        st = lib().ks_cg_multi(self._h, k, _ptr(B), _ptr(X0), float(tol), maxit, _ptr(X), _ptr(H), cap, reps)
-        self._check(st, ok=(KS_OK, KS_EMAXIT, KS_ENOTSPD))
+        st = fn(self._h, k, _ptr(B), _ptr(X0), float(tol), maxit, _ptr(X), _ptr(H), cap, reps)
+        self._check(st, ok=(KS_OK, KS_EMAXIT, KS_ENOTSPD, KS_EBREAKDOWN))
         R = [Report(int(q.iterations), int(q.matvecs), bool(q.converged), bool(q.breakdown),
                     bool(q.half_step_exit), int(q.status), float(q.relres), float(q.true_relres),
                     float(q.seconds_loop), float(q.seconds_total), float(q.seconds_gemv),

@@ -458,12 +458,13 @@ ks_status ks_gmres(ks_ctx* c, const double* b, const double* x0, double tol, int
     return s;
 }
 
-ks_status ks_cg_multi(ks_ctx* c, int32_t nrhs, const double* B, const double* X0, double tol, int64_t maxit,
-                      double* X, double* hist, int64_t hist_cap, ks_report* reps) {
+static ks_status solve_multi(ks_ctx* c, int bicgstab, int32_t nrhs, const double* B, const double* X0, double tol,
+                             int64_t maxit, double* X, double* hist, int64_t hist_cap, ks_report* reps) {
     if (!c) return fail(nullptr, KS_EARG, "ctx is NULL");
     if (!B || !X) return fail(c, KS_EARG, "B and X are required");
     if (nrhs < 1 || nrhs > ks::kMaxRhs) return fail(c, KS_EARG, "nrhs must be in [1, 8]");
-    if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "multi-RHS CG is FP64-only");
+    if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "multi-RHS solvers are FP64-only");
+    if (bicgstab && c->P != 1) return fail(c, KS_EARG, "multi-RHS BiCGSTAB runs on one GPU (P == 1)");
     if (c->P != 1 && !c->fused()) return fail(c, KS_EARG, "multi-RHS CG over P > 1 GPUs needs peer access (fused exchange)");
     if (!(tol >= 0.0)) return fail(c, KS_EARG, "tol must be >= 0");
     if (maxit < 0) return fail(c, KS_EARG, "maxit must be >= 0");
@@ -476,8 +477,8 @@ ks_status ks_cg_multi(ks_ctx* c, int32_t nrhs, const double* B, const double* X0
         c->for_each_rank([&](Rank& r) {
             const size_t i = (size_t)(&r - c->ranks.data());
             // reports from the rank that writes the host outputs (all ranks agree)
-            stat[i] = ks::run_cg_multi(c, r, nrhs, B, X0, tol, maxit, X, hist, hist_cap,
-                                       c->writes_host(r) ? reps : nullptr);
+            stat[i] = ks::run_multi(c, r, bicgstab, nrhs, B, X0, tol, maxit, X, hist, hist_cap,
+                                    c->writes_host(r) ? reps : nullptr);
             KS_CUDA(cudaGetLastError());
         });
         return KS_OK;
@@ -486,11 +487,22 @@ ks_status ks_cg_multi(ks_ctx* c, int32_t nrhs, const double* B, const double* X0
     const ks_status s = status_of(stat[0]);
     if (s != KS_OK) {
         const char* what = s == KS_EMAXIT ? "maximum iterations reached (some column)"
-                                          : "CG: <p, A p> <= 0 in some column (matrix not SPD)";
+                         : s == KS_EBREAKDOWN ? "BiCGSTAB breakdown in some column (zero or non-finite scalar)"
+                                              : "CG: <p, A p> <= 0 in some column (matrix not SPD)";
         c->last_error = what;
         g_tls_error = what;
     }
     return s;
+}
+
+ks_status ks_cg_multi(ks_ctx* c, int32_t nrhs, const double* B, const double* X0, double tol, int64_t maxit,
+                      double* X, double* hist, int64_t hist_cap, ks_report* reps) {
+    return solve_multi(c, 0, nrhs, B, X0, tol, maxit, X, hist, hist_cap, reps);
+}
+
+ks_status ks_bicgstab_multi(ks_ctx* c, int32_t nrhs, const double* B, const double* X0, double tol, int64_t maxit,
+                            double* X, double* hist, int64_t hist_cap, ks_report* reps) {
+    return solve_multi(c, 1, nrhs, B, X0, tol, maxit, X, hist, hist_cap, reps);
 }
 
 ks_status ks_matvec_t(ks_ctx* c, const double* x, double* y) {

@@ -164,7 +164,8 @@ void rank_free(Rank& r) {
                     (void*)r.kdev, (void*)r.pt_loc, (void*)r.U, (void*)r.qt_loc,
                     (void*)r.upart, (void*)r.col_ticket, (void*)r.gmV, (void*)r.gmH,
                     (void*)r.gm_hx, (void*)r.gm_state, (void*)r.ll, (void*)r.mX, (void*)r.mR,
-                    (void*)r.mQ, (void*)r.mP, (void*)r.mhist, (void*)r.mstate})
+                    (void*)r.mQ, (void*)r.mP, (void*)r.mhist, (void*)r.mstate, (void*)r.mRh,
+                    (void*)r.mT, (void*)r.mS})
         if (p) dev_free(p);
     if (r.h_done) cudaFreeHost(r.h_done);
     if (r.h_hist) cudaFreeHost(r.h_hist);

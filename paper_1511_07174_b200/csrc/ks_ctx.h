@@ -92,6 +92,7 @@ struct Rank {
     uint64_t* ll = nullptr;     // LL exchange slots of the tiny kernels (4 * ld words, lazily)
     // multi-RHS CG workspace (lazily sized by the kernel width K and the history cap)
     double *mX = nullptr, *mR = nullptr, *mQ = nullptr, *mP = nullptr, *mhist = nullptr;
+    double *mRh = nullptr, *mT = nullptr, *mS = nullptr;   // multi-RHS BiCGSTAB
     MultiState* mstate = nullptr;
     int mK = 0;
     int64_t mhist_cap = 0;
@@ -193,8 +194,8 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
                   int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep);
 int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
                  double* x, double* hist, int64_t hist_cap, ks_report* rep);
-int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double* X0, double tol, int64_t maxit,
-                     double* X, double* hist, int64_t hist_cap, ks_report* reps);
+int64_t run_multi(ks_ctx* c, Rank& r, int bicgstab, int nrhs, const double* B, const double* X0, double tol,
+                  int64_t maxit, double* X, double* hist, int64_t hist_cap, ks_report* reps);
 // K1T into r.U (chunk layout); for P > 1 reduce-scattered into r.qt_loc.  Returns the
 // pointer holding this rank's rows of A^T x.
 // k > 0 with the fused exchange (BiCG loop): the reduce-scatter is fused into K1T

@@ -289,6 +289,8 @@ struct MultiCol {
     double nb, rho, relres;
     long long iters;
     int status, active, converged, bzero;
+    double rho_old, alpha, omega;      // BiCGSTAB
+    int half, breakdown;               // BiCGSTAB
 };
 constexpr int kMaxRhs = 8;
 struct MultiState { MultiCol col[kMaxRhs]; };
@@ -316,6 +318,9 @@ struct MultiArgs {
     double* R;                     // K x ldm: b on entry, then r
     double* Q;                     // K x ldm: A p
     double* Pf;                    // K x ld: p (full length); x0 on entry when has_x0
+    double* Sf;                    // BiCGSTAB: K x ld: s (full length, the second GEMM's input)
+    double* Rh;                    // BiCGSTAB: K x ldm: rhat
+    double* T;                     // BiCGSTAB: K x ldm: t = A s (Q holds v = A p)
     double* hist;                  // K x hist_cap (column k at hist + k * hist_cap), nullable
     int64_t hist_cap;
     MultiState* ms;
@@ -326,6 +331,10 @@ struct MultiArgs {
 int multi_k(int nrhs);             // kernel width K for nrhs columns (0: unsupported)
 int multi_grid(int K, int num_sms);
 int launch_cg_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st);
+// multi-RHS BiCGSTAB (one GPU): K independent BiCGSTAB recurrences (SURVEY.md
+// sec.8(c).4 per column) sharing both GEMMs (v = A p, t = A s) of every iteration
+int multi_grid_bs(int K, int num_sms);
+int launch_bicgstab_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st);
 
 // NEXT-4 (FP32) support kernels (ks_f32.cu): K1 in FP32, setup/init/finish in
 // FP32, conversions at the FP64 ABI boundary, FP32 generators.

@@ -89,13 +89,18 @@ struct MultiSmem {
     uint64_t full[kMS], empty[kMS];
     double red[2 * K * kMW];
     double wpart[kMW][K];
+    double wpart2[kMW][K];
 };
 
 // Q = A P (this CTA's bands) and sigma partials <P_k, Q_k> over the CTA's rows in
 // band order.  `it` is the pipeline position, identical in producer and consumers.
-template <int K, int WR, int CH>
+// Output rows go to out[k * ldm + row]; d1_k = sum over the rows of W[k * ldw + woff + row]
+// * out_k (CG: sigma = <p, q>; BiCGSTAB: <rhat, v>, <s, t>), d2_k = <out_k, out_k> when DOT2.
+template <int K, int WR, int CH, bool DOT2 = false>
 __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const MultiArgs& M,
-                           MultiSmem<K, WR, CH>& S, uint32_t& it, double (&sig)[K]) {
+                           MultiSmem<K, WR, CH>& S, uint32_t& it, double (&sig)[K], double* out = nullptr,
+                           const double* W = nullptr, int64_t ldw = 0, int64_t woff = 0, double* d2 = nullptr) {
+    if (!out) { out = M.Q; W = M.Pf; ldw = M.ld; woff = M.row0; }
     constexpr int BAND = kMW * WR, NP = CH / 64;
     constexpr int kMS = MultiSmem<K, WR, CH>::kMS;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -103,6 +108,10 @@ __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const
     const int nchunks = (int)(M.ld / CH);
 #pragma unroll
     for (int k = 0; k < K; ++k) sig[k] = 0.0;
+    if (DOT2) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) d2[k] = 0.0;
+    }
     if (w == kMW) {                                        // ---- TMA producer warp
         if (lane == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");   // P written by the generic proxy
@@ -164,8 +173,9 @@ __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const
                 if (row < M.m) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
-                        M.Q[k * M.ldm + row] = acc[rr][k];
-                        sig[k] = fma(M.Pf[k * M.ld + M.row0 + row], acc[rr][k], sig[k]);
+                        out[k * M.ldm + row] = acc[rr][k];
+                        sig[k] = fma(W[k * ldw + woff + row], acc[rr][k], sig[k]);
+                        if (DOT2) d2[k] = fma(acc[rr][k], acc[rr][k], d2[k]);
                     }
                 }
             }
@@ -476,6 +486,276 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
     }
 }
 
+// ---- multi-RHS BiCGSTAB (one GPU): rows B0-B8 of SURVEY.md sec.8(c).4 per column,
+// the two GEMMs of an iteration (v = A p from P, t = A s from S) shared by the K
+// columns.  Per column: own rho, alpha, omega, the exact-zero / non-finite breakdown
+// tests (Q9), the half-step exit; a stopped column stops updating.  5 grid barriers
+// per iteration, as the single-RHS persistent BiCGSTAB.
+template <int K, int WR, int CH>
+__global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensorMap tmA,
+                                               const __grid_constant__ CUtensorMap tmP,
+                                               const __grid_constant__ CUtensorMap tmS, MultiArgs M) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    MultiSmem<K, WR, CH>& S = *reinterpret_cast<MultiSmem<K, WR, CH>*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    MultiState* ms = M.ms;
+    DevState* st = M.st;
+    const int tid = threadIdx.x;
+    const bool cons = tid < kMCT;
+    const int64_t gs = (int64_t)gridDim.x * kMCT;
+    const int64_t t0 = (int64_t)blockIdx.x * kMCT + tid;
+    const int64_t n = M.n;                 // one GPU: m == n
+    const bool lead = blockIdx.x == 0 && tid == 0;
+    if (tid == 0) {
+        for (int s = 0; s < MultiSmem<K, WR, CH>::kMS; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kMW); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid == kMW * 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmP) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmS) : "memory");
+    }
+    __syncthreads();
+    uint32_t it = 0;
+    double d1[K], d2[K];
+    // ---- B0: r0 = b - A x0 (or b), rhat = r0, x = x0 (or 0), ||b||, rho_1 = <rhat, r0>
+    if (M.has_x0) {
+        gemm_phase<K, WR, CH>(&tmA, &tmP, M, S, it, d1);          // Q = A x0 (P holds x0)
+        if (!pk::grid_sync(M.bar, st)) return;
+    }
+    {
+        double v[2 * K];
+#pragma unroll
+        for (int k = 0; k < 2 * K; ++k) v[k] = 0.0;
+        if (cons) {
+            for (int64_t i = t0; i < n; i += gs) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const double bk = M.R[k * M.ldm + i];
+                    const double r = M.has_x0 ? bk - M.Q[k * M.ldm + i] : bk;
+                    v[k] = fma(bk, bk, v[k]);
+                    v[K + k] = fma(r, r, v[K + k]);
+                    M.R[k * M.ldm + i] = r;
+                    M.Rh[k * M.ldm + i] = r;                           // rhat = r0 (Q7)
+                    M.X[k * M.ldm + i] = M.has_x0 ? M.Pf[k * M.ld + i] : 0.0;
+                }
+            }
+        }
+        csum<2 * K>(v, S.red);
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v[k];
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        double tb[K], tr[K];
+        totals<K>(M.bpart, 0, tb, S.red);
+        totals<K>(M.bpart, K, tr, S.red);
+        if (cons) {
+            for (int64_t i = t0; i < n; i += gs)
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (!(k < M.nrhs) || tb[k] == 0.0) M.X[k * M.ldm + i] = 0.0;   // Q6
+        }
+        if (lead) {
+            for (int k = 0; k < K; ++k) {
+                MultiCol& cl = ms->col[k];
+                cl.nb = sqrt(tb[k]);
+                cl.rho = tr[k];                                   // <rhat, r0> = <r0, r0>
+                cl.rho_old = cl.alpha = cl.omega = 1.0;           // Q8
+                cl.iters = 0; cl.relres = 0.0; cl.status = KS_EMAXIT; cl.active = 1;
+                cl.half = 0; cl.breakdown = 0;
+                if (k >= M.nrhs || tb[k] == 0.0) {
+                    cl.active = 0; cl.status = KS_OK; cl.converged = 1; cl.bzero = 1;
+                } else {
+                    cl.converged = 0; cl.bzero = 0;
+                    cl.relres = sqrt(tr[k]) / cl.nb;
+                    if (cl.relres <= M.tol) { cl.active = 0; cl.status = KS_OK; cl.converged = 1; }   // Q2
+                }
+            }
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+    }
+    for (long long i1 = 1; i1 <= M.maxit; ++i1) {
+        int act[K];
+        int any = 0;
+        double rho[K], beta[K], omega[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const MultiCol& cl = ms->col[k];
+            act[k] = *(volatile const int*)&cl.active;
+            rho[k] = *(volatile const double*)&cl.rho;
+            omega[k] = *(volatile const double*)&cl.omega;
+            beta[k] = 0.0;
+            if (act[k] && (rho[k] == 0.0 || !isfinite(rho[k]))) {          // Q9: rho breakdown
+                act[k] = 0;
+                if (lead) { ms->col[k].active = 0; ms->col[k].status = KS_EBREAKDOWN; ms->col[k].breakdown = 1;
+                            ms->col[k].iters = i1 - 1; }
+            }
+            if (act[k]) beta[k] = (rho[k] / *(volatile const double*)&cl.rho_old) * (*(volatile const double*)&cl.alpha / omega[k]);
+            any |= act[k];
+        }
+        if (!any) break;
+        // B1: p = r + beta (p - omega v)   (i = 1: p = r)
+        if (cons) {
+            for (int64_t j = t0; j < n; j += gs)
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (act[k]) {
+                        const double r = M.R[k * M.ldm + j];
+                        M.Pf[k * M.ld + j] = i1 == 1 ? r
+                            : fma(beta[k], fma(-omega[k], M.Q[k * M.ldm + j], M.Pf[k * M.ld + j]), r);
+                    }
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        // B3: v = A p (into Q), gamma partials <rhat, v>
+        gemm_phase<K, WR, CH>(&tmA, &tmP, M, S, it, d1, M.Q, M.Rh, M.ldm, 0);
+        __syncthreads();
+        if ((tid & 31) == 0 && tid < kMCT) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) S.wpart[tid >> 5][k] = d1[k];
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double t = 0.0;
+                for (int ww = 0; ww < kMW; ++ww) t += S.wpart[ww][k];
+                M.bpart[(int64_t)blockIdx.x * 2 * K + k] = t;
+            }
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        double gam[K], alpha[K];
+        totals<K>(M.bpart, 0, gam, S.red);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (act[k] && (gam[k] == 0.0 || !isfinite(gam[k]))) {          // Q9
+                act[k] = 0;
+                if (lead) { ms->col[k].active = 0; ms->col[k].status = KS_EBREAKDOWN; ms->col[k].breakdown = 1;
+                            ms->col[k].iters = i1 - 1; }
+            }
+            alpha[k] = act[k] ? rho[k] / gam[k] : 0.0;
+        }
+        // B4: s = r - alpha v (full length), ||s||^2
+        double ssp[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) ssp[k] = 0.0;
+        if (cons) {
+            for (int64_t j = t0; j < n; j += gs)
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (act[k]) {
+                        const double sv = fma(-alpha[k], M.Q[k * M.ldm + j], M.R[k * M.ldm + j]);
+                        M.Sf[k * M.ld + j] = sv;
+                        ssp[k] = fma(sv, sv, ssp[k]);
+                    }
+        }
+        csum<K>(ssp, S.red);
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + K + k] = ssp[k];
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        double ss[K];
+        totals<K>(M.bpart, K, ss, S.red);
+        int half[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            half[k] = 0;
+            if (!act[k]) continue;
+            const double srel = sqrt(ss[k]) / ms->col[k].nb;
+            if (srel <= M.tol) {                                           // B5: half-step exit
+                half[k] = 1;
+                act[k] = 0;
+                if (lead) {
+                    MultiCol& cl = ms->col[k];
+                    if (M.hist && i1 - 1 < M.hist_cap) M.hist[(int64_t)k * M.hist_cap + (i1 - 1)] = srel;
+                    cl.relres = srel; cl.iters = i1; cl.half = 1; cl.converged = 1; cl.status = KS_OK;
+                    cl.active = 0; cl.alpha = alpha[k];
+                }
+            }
+        }
+        if (cons) {                                                        // half step: x += alpha p
+            for (int64_t j = t0; j < n; j += gs)
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (half[k]) M.X[k * M.ldm + j] = fma(alpha[k], M.Pf[k * M.ld + j], M.X[k * M.ldm + j]);
+        }
+        // B6: t = A s (into T), <s, t> and <t, t>
+        gemm_phase<K, WR, CH, true>(&tmA, &tmS, M, S, it, d1, M.T, M.Sf, M.ld, 0, d2);
+        __syncthreads();
+        if ((tid & 31) == 0 && tid < kMCT) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) { S.wpart[tid >> 5][k] = d1[k]; S.wpart2[tid >> 5][k] = d2[k]; }
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double a1 = 0.0, a2 = 0.0;
+                for (int ww = 0; ww < kMW; ++ww) { a1 += S.wpart[ww][k]; a2 += S.wpart2[ww][k]; }
+                M.bpart[(int64_t)blockIdx.x * 2 * K + k] = a1;
+                M.bpart[(int64_t)blockIdx.x * 2 * K + K + k] = a2;
+            }
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        double ts[K], tt[K], om[K];
+        totals<K>(M.bpart, 0, ts, S.red);
+        totals<K>(M.bpart, K, tt, S.red);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            om[k] = 0.0;
+            if (!act[k]) continue;
+            bool bad = tt[k] == 0.0 || !isfinite(tt[k]);
+            if (!bad) { om[k] = ts[k] / tt[k]; bad = om[k] == 0.0 || !isfinite(om[k]); }
+            if (bad) {                                                     // Q9
+                act[k] = 0;
+                if (lead) { ms->col[k].active = 0; ms->col[k].status = KS_EBREAKDOWN; ms->col[k].breakdown = 1;
+                            ms->col[k].iters = i1 - 1; }
+            }
+        }
+        // B7: x = (x + alpha p) + omega s; r = s - omega t; <rhat, r>, <r, r>
+        double v2[2 * K];
+#pragma unroll
+        for (int k = 0; k < 2 * K; ++k) v2[k] = 0.0;
+        if (cons) {
+            for (int64_t j = t0; j < n; j += gs)
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (act[k]) {
+                        const double sv = M.Sf[k * M.ld + j];
+                        M.X[k * M.ldm + j] = fma(om[k], sv, fma(alpha[k], M.Pf[k * M.ld + j], M.X[k * M.ldm + j]));
+                        const double r = fma(-om[k], M.T[k * M.ldm + j], sv);
+                        M.R[k * M.ldm + j] = r;
+                        v2[k] = fma(M.Rh[k * M.ldm + j], r, v2[k]);
+                        v2[K + k] = fma(r, r, v2[K + k]);
+                    }
+        }
+        csum<2 * K>(v2, S.red);
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v2[k];
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+        double rhn[K], rr[K];
+        totals<K>(M.bpart, 0, rhn, S.red);
+        totals<K>(M.bpart, K, rr, S.red);
+        // B8: history, test; rho_old = rho, rho = <rhat, r>
+        if (lead) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (!act[k]) continue;
+                MultiCol& cl = ms->col[k];
+                const double rel = sqrt(rr[k]) / cl.nb;
+                if (M.hist && i1 - 1 < M.hist_cap) M.hist[(int64_t)k * M.hist_cap + (i1 - 1)] = rel;
+                cl.relres = rel; cl.iters = i1;
+                cl.rho_old = rho[k]; cl.rho = rhn[k]; cl.alpha = alpha[k]; cl.omega = om[k];
+                if (rel <= M.tol) { cl.active = 0; cl.converged = 1; cl.status = KS_OK; }
+            }
+        }
+        if (!pk::grid_sync(M.bar, st)) return;
+    }
+}
+
 // shapes: 0 = (4 rows/warp, 128 columns, 4 stages), 1 = (8, 64, 4), 2 = (8, 128, 3)
 int multi_shape(int K) {
     if (const char* e = std::getenv("KS_MULTI_SHAPE")) {                // tuning
@@ -490,6 +770,9 @@ const void* kern_m(int K, int shape) {
                      : shape == 2 ? (const void*)k_cgm<4, 8, 128> : (const void*)k_cgm<4, 4, 128>;
     return shape == 1 ? (const void*)k_cgm<8, 8, 64>
          : shape == 2 ? (const void*)k_cgm<8, 8, 128> : (const void*)k_cgm<8, 4, 128>;
+}
+const void* kern_bs(int K) {
+    return K == 4 ? (const void*)k_bsm<4, 8, 128> : (const void*)k_bsm<8, 8, 128>;
 }
 size_t smem_m(int K, int shape) {
     size_t b;
@@ -546,6 +829,38 @@ static bool make_map(CUtensorMap* tm, const double* base, int64_t rows, int64_t 
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int multi_grid_bs(int K, int num_sms) {
+    const void* k = kern_bs(K);
+    const size_t sm = smem_m(K, 2);
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); return 0; }
+    const int dyn_max = optin - (int)fa.sharedSizeBytes;
+    if ((size_t)dyn_max < sm ||
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kMT, sm);
+    return per_sm >= 1 ? num_sms : 0;
+}
+
+int launch_bicgstab_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st) {
+    CUtensorMap tmA, tmP, tmS;
+    if (!make_map(&tmA, A, M.m, M.ld, M.ld, kMW * 8, 128)) return -(int)cudaErrorInvalidValue;
+    if (!make_map(&tmP, M.Pf, K, M.ld, M.ld, K, 128)) return -(int)cudaErrorInvalidValue;
+    if (!make_map(&tmS, M.Sf, K, M.ld, M.ld, K, 128)) return -(int)cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(M.bar, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return -(int)e;
+    MultiArgs Mc = M;
+    void* args[] = {&tmA, &tmP, &tmS, &Mc};
+    e = cudaLaunchCooperativeKernel(kern_bs(K), dim3((unsigned)grid), dim3(kMT), args, smem_m(K, 2), st);
+    return e == cudaSuccess ? 1 : -(int)e;
 }
 
 int launch_cg_multi(int K, const MultiArgs& M, const double* A, int grid, cudaStream_t st) {

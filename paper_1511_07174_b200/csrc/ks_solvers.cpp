@@ -842,20 +842,27 @@ int64_t run_bicg(ks_ctx* c, Rank& r, const double* b, const double* x0, double t
 // B, X0, X: n x nrhs column-major (column k at + k n); hist: hist_cap x nrhs
 // column-major; reps: nrhs reports.  Returns the worst column status
 // (ENOTSPD > EMAXIT > OK).
-int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double* X0, double tol, int64_t maxit,
-                     double* X, double* hist, int64_t hist_cap, ks_report* reps) {
+int64_t run_multi(ks_ctx* c, Rank& r, int bicgstab, int nrhs, const double* B, const double* X0, double tol,
+                  int64_t maxit, double* X, double* hist, int64_t hist_cap, ks_report* reps) {
     const auto t_start = Clock::now();
     check_loaded(c, r);
     const int K = multi_k(nrhs);
     const int64_t n = c->n, ld = c->ld, ldm = (r.m + 63) / 64 * 64;
     if (K != r.mK) {
-        for (double* p : {r.mX, r.mR, r.mQ, r.mP}) dev_free(p);
+        for (double* p : {r.mX, r.mR, r.mQ, r.mP, r.mRh, r.mT, r.mS}) dev_free(p);
+        r.mRh = r.mT = r.mS = nullptr;
         dev_alloc_t(&r.mX, (size_t)(K * ldm));
         dev_alloc_t(&r.mR, (size_t)(K * ldm));
         dev_alloc_t(&r.mQ, (size_t)(K * ldm));
         dev_alloc_t(&r.mP, (size_t)(K * ld));
         if (!r.mstate) dev_alloc_t(&r.mstate, 1);
         r.mK = K;
+    }
+    if (bicgstab && !r.mS) {                 // BiCGSTAB: rhat, t, and the full-length s
+        dev_alloc_t(&r.mRh, (size_t)(K * ldm));
+        dev_alloc_t(&r.mT, (size_t)(K * ldm));
+        dev_alloc_t(&r.mS, (size_t)(K * ld));
+        KS_CUDA(cudaMemsetAsync(r.mS, 0, (size_t)(K * ld) * sizeof(double), r.stream));
     }
     const int64_t hc = hist ? hist_cap : 0;
     if (hc > 0 && hc * K > r.mhist_cap) {
@@ -903,11 +910,16 @@ int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double
     M.ebase = r.epoch_next;
     r.epoch_next += (unsigned long long)maxit + 2;
     M.join_ns = (unsigned long long)c->opt.join_timeout_ms * 1000000ULL;
-    const int grid = memo_grid(r, (5LL << 48) | K, [&] { return multi_grid(K, r.num_sms); });
+    M.Sf = r.mS;
+    M.Rh = r.mRh;
+    M.T = r.mT;
+    const int grid = bicgstab ? memo_grid(r, (6LL << 48) | K, [&] { return multi_grid_bs(K, r.num_sms); })
+                              : memo_grid(r, (5LL << 48) | K, [&] { return multi_grid(K, r.num_sms); });
     if (grid <= 0) throw KsError(KS_ECUDA, "multi-RHS kernel does not fit this device");
     KS_CUDA(cudaMemsetAsync(&r.st->peer_timeout, 0, sizeof(int), r.stream));
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
-    const int rc = launch_cg_multi(K, M, r.A, grid, r.stream);
+    const int rc = bicgstab ? launch_bicgstab_multi(K, M, r.A, grid, r.stream)
+                            : launch_cg_multi(K, M, r.A, grid, r.stream);
     if (rc < 0) KS_CUDA((cudaError_t)(-rc));
     KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
     // out: X columns, state, histories -- one synchronisation
@@ -935,13 +947,15 @@ int64_t run_cg_multi(ks_ctx* c, Rank& r, int nrhs, const double* B, const double
     for (int k = 0; k < nrhs; ++k) {
         const MultiCol& cl = hs.col[k];
         const int64_t stt = cl.active ? (int64_t)KS_EMAXIT : (int64_t)cl.status;
-        if (stt == KS_ENOTSPD) worst = KS_ENOTSPD;
+        if (stt == KS_ENOTSPD || stt == KS_EBREAKDOWN) worst = stt;
         else if (stt == KS_EMAXIT && worst == KS_OK) worst = KS_EMAXIT;
         if (reps) {
             ks_report R;
             std::memset(&R, 0, sizeof R);
             R.iterations = cl.active ? maxit : cl.iters;
-            R.matvecs = R.iterations;
+            R.matvecs = bicgstab ? 2 * R.iterations - (cl.half ? 1 : 0) : R.iterations;
+            R.half_step_exit = bicgstab ? cl.half : 0;
+            R.breakdown = bicgstab ? cl.breakdown : 0;
             R.converged = cl.converged;
             R.status = (int32_t)stt;
             R.relres = cl.bzero ? 0.0 : cl.relres;

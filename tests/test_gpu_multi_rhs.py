@@ -148,3 +148,67 @@ def test_multi_rhs_over_p_gpus(P):
         for k in range(2):
             assert rs[k].iterations == 5
             assert np.linalg.norm(Xs[:, k] - Xso[:, k]) <= 1e-12 * np.linalg.norm(Xso[:, k])
+
+
+# ---------------------------------------------------------------- multi-RHS BiCGSTAB
+
+def gdd_block(n, k, kd=4):
+    D, b = synth.gdd(n, kd)
+    return D, np.column_stack([b] + [synth.rhs(n, synth.SEED + j) for j in range(1, k)])
+
+
+@pytest.mark.parametrize("n,nrhs", [(1024, 1), (1000, 3), (2050, 5), (4096, 8), (777, 8)])
+def test_bicgstab_multi_parity(n, nrhs):
+    """Multi-RHS BiCGSTAB vs oracle.bicgstab_multi column by column (G-DD kd = 4:
+    the parity-safe BiCGSTAB input), half-step exits per column."""
+    from test_gpu_parity import FLOOR_BS
+    D, B = gdd_block(n, nrhs)
+    Xo, ho, ro = oracle.bicgstab_multi(D, B, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(D)
+        X, h, r = ctx.bicgstab_multi(B, tol=1e-10)
+    for k in range(nrhs):
+        bars(X[:, k], h[k], r[k], Xo[:, k], ho[k], ro[k], floor=FLOOR_BS)
+        assert r[k].converged and r[k].half_step_exit == ro[k].half_step_exit
+        assert r[k].matvecs == 2 * r[k].iterations - (1 if r[k].half_step_exit else 0)
+
+
+def test_bicgstab_multi_exits_and_repeat():
+    """x0, a b = 0 column, maxit (the oracle's x after 5 steps), a per-column
+    breakdown (a rotation block), repeat bitwise, and the single-RHS GPU solver agree."""
+    from test_gpu_parity import FLOOR_BS
+    n = 600
+    D, B = gdd_block(n, 4, kd=16)
+    B[:, 2] = 0.0
+    X0 = np.random.default_rng(5).standard_normal((n, 4))
+    Xo, ho, ro = oracle.bicgstab_multi(D, B, X0=X0, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(D)
+        X, h, r = ctx.bicgstab_multi(B, X0=X0, tol=1e-10)
+        for k in (0, 1, 3):
+            bars(X[:, k], h[k], r[k], Xo[:, k], ho[k], ro[k], floor=FLOOR_BS)
+        assert r[2].iterations == 0 and np.all(X[:, 2] == 0)
+        X2, h2, r2 = ctx.bicgstab_multi(B, X0=X0, tol=1e-10)
+        assert np.array_equal(X2, X)
+        Xo5, _, _ = oracle.bicgstab_multi(D, B[:, :2], tol=0.0, maxit=5)
+        X5, h5, r5 = ctx.bicgstab_multi(B[:, :2], tol=0.0, maxit=5)
+        for k in range(2):
+            assert r5[k].iterations == 5 and r5[k].status == ks.KS_EMAXIT and len(h5[k]) == 5
+            assert np.linalg.norm(X5[:, k] - Xo5[:, k]) <= 1e-12 * np.linalg.norm(Xo5[:, k])
+        x1, h1, r1 = ctx.bicgstab(B[:, 0], tol=1e-10)
+        Xs, hs, rs = ctx.bicgstab_multi(B[:, :1], tol=1e-10)
+        bars(Xs[:, 0], hs[0], rs[0], x1, h1, r1, floor=FLOOR_BS)
+    A = np.zeros((n, n))
+    A[: n // 2, : n // 2] = np.diag(np.arange(1.0, n // 2 + 1))
+    for i in range(n // 2, n, 2):
+        A[i, i + 1], A[i + 1, i] = 1.0, -1.0
+    Bb = np.zeros((n, 2))
+    Bb[: n // 2, 0] = 1.0
+    Bb[n // 2, 1] = 1.0
+    Xo, ho, ro = oracle.bicgstab_multi(A, Bb, tol=1e-10)
+    with ks.Context(n) as ctx:
+        ctx.load_rows(A)
+        X, h, r = ctx.bicgstab_multi(Bb, tol=1e-10)
+    assert ro[1].status == r[1].status == ks.KS_EBREAKDOWN and r[1].iterations == 0 and np.all(X[:, 1] == 0)
+    assert r[0].status == ks.KS_OK
+    bars(X[:, 0], h[0], r[0], Xo[:, 0], ho[0], ro[0], floor=FLOOR_BS)

@@ -206,3 +206,25 @@ def test_tiny_over_p_gpus(P):
                 assert np.array_equal(x2, x) and np.array_equal(h2, h)
                 res[tiny] = (x, y)
         assert not (np.array_equal(res[1][0], res[0][0]) and np.array_equal(res[1][1], res[0][1]))
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_tiny_bitwise_independent_of_p(P):
+    """Each GEMV row is summed in the same order whichever CTA of whichever rank owns
+    it, and every full-length dot runs in the same thread layout in every CTA, so the
+    tiny kernels' x and history on P GPUs equal the one-GPU results bit for bit."""
+    if _ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    n = 1000
+    A, b = gspd_any(n)
+    D, bd = synth.gdd(n, 4)
+    out = {}
+    for q in (1, P):
+        with ks.Context(n, ngpus=q) as ctx, ks.Context(n, ngpus=q) as dtx:
+            ctx.load_rows(A)
+            dtx.load_rows(D)
+            out[q] = (ctx.cg(b, tol=1e-10), dtx.bicgstab(bd, tol=1e-10))
+    for k in range(2):
+        x1, h1, r1 = out[1][k]
+        xp, hp, rp = out[P][k]
+        assert r1.iterations == rp.iterations and np.array_equal(x1, xp) and np.array_equal(h1, hp)

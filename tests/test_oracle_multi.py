@@ -58,3 +58,43 @@ def test_per_column_notspd_and_x0():
     X, hs, reps = oracle.cg_multi(A, B, X0=X0, tol=1e-12)
     assert reps[0].status == oracle.OK and reps[0].iterations == 1 and np.array_equal(X[:, 0], [1.0, 0.0])
     assert reps[1].status == oracle.ENOTSPD and reps[1].iterations == 0 and np.all(X[:, 1] == 0)
+
+
+def test_bicgstab_multi_spec_example_and_second_column():
+    """SPEC.md:559 ([[2,1],[0,3]] x = [3,3] -> [1,1], a half-step exit at iteration 1)
+    next to b = A [1, 2] = [4, 6] and b = 0, in one block."""
+    A = np.array([[2.0, 1.0], [0.0, 3.0]])
+    B = np.array([[3.0, 4.0, 0.0], [3.0, 6.0, 0.0]])
+    X, hs, reps = oracle.bicgstab_multi(A, B, tol=1e-14)
+    assert np.allclose(X[:, 0], [1.0, 1.0], rtol=8 * EPS, atol=0)
+    assert reps[0].iterations == 1 and reps[0].half_step_exit
+    assert np.allclose(X[:, 1], [1.0, 2.0], rtol=8 * EPS, atol=0)
+    assert np.all(X[:, 2] == 0) and reps[2].iterations == 0 and reps[2].converged
+
+
+def test_bicgstab_multi_per_column_breakdown():
+    """A = diag(2, 2) (+) [[0, 1], [-1, 0]]: b = e1 lies in the diagonal block (one
+    half step, exact), b = e3 in the rotation block meets <rhat, A r0> = <e3, -e4> = 0
+    at iteration 1 (BREAKDOWN, 0 iterations, x = 0) -- per column."""
+    A = np.zeros((4, 4))
+    A[0, 0] = A[1, 1] = 2.0
+    A[2, 3], A[3, 2] = 1.0, -1.0
+    B = np.zeros((4, 2))
+    B[0, 0] = 1.0
+    B[2, 1] = 1.0
+    X, hs, reps = oracle.bicgstab_multi(A, B, tol=1e-14)
+    assert reps[0].status == oracle.OK and np.allclose(X[:, 0], [0.5, 0, 0, 0], rtol=0, atol=4 * EPS)
+    assert reps[1].status == oracle.EBREAKDOWN and reps[1].iterations == 0 and np.all(X[:, 1] == 0)
+
+
+def test_bicgstab_multi_column_permutation():
+    rng = np.random.default_rng(11)
+    n = 30
+    A = rng.standard_normal((n, n)) + n * np.eye(n)
+    B = rng.standard_normal((n, 4))
+    X, hs, reps = oracle.bicgstab_multi(A, B, tol=1e-12)
+    perm = [2, 0, 3, 1]
+    Xp, hsp, repsp = oracle.bicgstab_multi(A, B[:, perm], tol=1e-12)
+    assert np.array_equal(Xp, X[:, perm])
+    for j, k in enumerate(perm):
+        assert np.array_equal(hsp[j], hs[k]) and repsp[j].iterations == reps[k].iterations
