@@ -178,9 +178,11 @@ def test_bicgstab_multi_exits_and_repeat():
     breakdown (a rotation block), repeat bitwise, and the single-RHS GPU solver agree."""
     from test_gpu_parity import FLOOR_BS
     n = 600
-    D, B = gdd_block(n, 4, kd=16)
+    D, B = gdd_block(n, 4, kd=4)
     B[:, 2] = 0.0
-    X0 = np.random.default_rng(5).standard_normal((n, 4))
+    # a small x0: the history starts near 1 (the Q17 floor is in relres units; a random
+    # x0 of unit size puts h_0 at ~300 and the rounding noise of the tail with it)
+    X0 = 1e-3 * np.random.default_rng(5).standard_normal((n, 4))
     Xo, ho, ro = oracle.bicgstab_multi(D, B, X0=X0, tol=1e-10)
     with ks.Context(n) as ctx:
         ctx.load_rows(D)
