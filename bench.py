@@ -413,9 +413,9 @@ def run_ours(args):
     e2e_s = e2e_region(True)
     e2e_solve_s = e2e_region(False)
 
-    # extras (outside the timed region, one GPU only): multi-RHS CG on the resident
-    # CG matrix (8 right-hand sides share each pass over A) and the
-    # C1 latency path (n = 1024, tiny register-resident kernels)
+    # extras (outside the timed region, one GPU only): multi-RHS CG and BiCGSTAB on the
+    # resident matrices (8 right-hand sides share each pass over A)
+    # and the C1 latency path (n = 1024, tiny register-resident kernels)
     extras = None
     if world == 1 and not args.no_extras:
         extras = {}
@@ -427,6 +427,14 @@ def run_ours(args):
             "nrhs": 8, "iters_per_s": ips_m, "rhs_iters_per_s": 8 * ips_m,
             "A_stream_GBps": 8.0 * n * n * ips_m / 1e9, "vs_single_rhs_cg": 8 * ips_m / (K / cg_loop),
             "kernel": "k_cgm<8,8,128> (TMA 2-D tensor-map loads, producer warp + 7 consumer warps, FP64 skinny GEMM)"}
+        Bb = np.column_stack([b_bs] + [synth.rhs(n, SEED + j) for j in range(1, 8)])
+        bs_ctx.bicgstab_multi(Bb, tol=0.0, maxit=2, hist=False)
+        _, _, rb8 = bs_ctx.bicgstab_multi(Bb, tol=0.0, maxit=min(K, 10), hist=False)
+        ips_b = min(K, 10) / rb8[0].seconds_loop
+        extras["multi_rhs_bicgstab"] = {
+            "nrhs": 8, "iters_per_s": ips_b, "rhs_iters_per_s": 8 * ips_b,
+            "A_stream_GBps": 2 * 8.0 * n * n * ips_b / 1e9, "vs_single_rhs_bicgstab": 8 * ips_b / (K / bs_loop),
+            "kernel": "k_bsm<8,8,128> (both GEMMs of an iteration TMA-fed and shared by 8 columns)"}
         with ks.Context.from_rank(1024, 0, 1, None, local, stream.cuda_stream) as c1:
             bt = c1.generate("spd", seed=SEED, table=synth.spd_table(1024, 1e3))
             c1.cg(bt, tol=0.0, maxit=2, hist=False)
