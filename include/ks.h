@@ -249,8 +249,8 @@ ks_status ks_gmres(ks_ctx* ctx, const double* b, const double* x0, double tol, i
  * B, X: n x nrhs, column-major (column k at B + k*n), required; X0: same or NULL
  * (zero start).  hist: NULL or hist_cap x nrhs column-major (column k at
  * hist + k*hist_cap), receives min(iterations_k, hist_cap) values ||r||/||b_k||.
- * reps: NULL or nrhs reports (true_relres -1: not computed).  One GPU (P == 1),
- * FP64 contexts only (else KS_EARG).  Returns the worst column status:
+ * reps: NULL or nrhs reports (true_relres -1: not computed).  P == 1, or P > 1 with
+ * the fused exchange (peer access between all GPUs); FP64 contexts only (else KS_EARG).  Returns the worst column status:
  * KS_ENOTSPD > KS_EMAXIT > KS_OK.                                                 */
 ks_status ks_cg_multi(ks_ctx* ctx, int32_t nrhs, const double* B, const double* X0, double tol, int64_t maxit,
                       double* X, double* hist, int64_t hist_cap, ks_report* reps);
@@ -260,7 +260,8 @@ ks_status ks_cg_multi(ks_ctx* ctx, int32_t nrhs, const double* B, const double* 
  * alpha, omega, breakdown tests and half-step exit -- sharing both GEMMs of every
  * iteration (v = A P and t = A S, TMA-fed, FP64).  Arguments, layouts and reports as
  * ks_cg_multi (half_step_exit, breakdown, matvecs = 2 iterations - half per column).
- * One GPU (P == 1; else KS_EARG), FP64.  Returns the worst column status:
+ * P == 1, or P > 1 with the fused exchange (v and r slices and the per-column dots
+ * exchanged over NVLink in-kernel), FP64.  Returns the worst column status:
  * KS_EBREAKDOWN > KS_EMAXIT > KS_OK.                                              */
 ks_status ks_bicgstab_multi(ks_ctx* ctx, int32_t nrhs, const double* B, const double* X0, double tol,
                             int64_t maxit, double* X, double* hist, int64_t hist_cap, ks_report* reps);

@@ -464,8 +464,7 @@ static ks_status solve_multi(ks_ctx* c, int bicgstab, int32_t nrhs, const double
     if (!B || !X) return fail(c, KS_EARG, "B and X are required");
     if (nrhs < 1 || nrhs > ks::kMaxRhs) return fail(c, KS_EARG, "nrhs must be in [1, 8]");
     if (c->dtype != KS_FLOAT64) return fail(c, KS_EARG, "multi-RHS solvers are FP64-only");
-    if (bicgstab && c->P != 1) return fail(c, KS_EARG, "multi-RHS BiCGSTAB runs on one GPU (P == 1)");
-    if (c->P != 1 && !c->fused()) return fail(c, KS_EARG, "multi-RHS CG over P > 1 GPUs needs peer access (fused exchange)");
+    if (c->P != 1 && !c->fused()) return fail(c, KS_EARG, "multi-RHS solvers over P > 1 GPUs need peer access (fused exchange)");
     if (!(tol >= 0.0)) return fail(c, KS_EARG, "tol must be >= 0");
     if (maxit < 0) return fail(c, KS_EARG, "maxit must be >= 0");
     if (hist_cap < 0 || (hist_cap > 0 && !hist)) return fail(c, KS_EARG, "bad hist/hist_cap");

@@ -91,11 +91,12 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         // multi-RHS CG over P > 1 (FP64 contexts): r slices, rank partials, gathered x
         const bool mm = c->dtype == KS_FLOAT64 && P > 1;
         const size_t mrb = mm ? 2 * P * (size_t)kMaxRhs * (size_t)r.L.chunk * sizeof(double) : 0;
-        const size_t msb = mm ? (2 * P * 2 * (size_t)kMaxRhs * sizeof(double) + 511) / 512 * 512 : 0;
+        const size_t msb = mm ? (2 * P * 6 * (size_t)kMaxRhs * sizeof(double) + 511) / 512 * 512 : 0;
         const size_t mxb = mm ? (size_t)kMaxRhs * (size_t)ld * sizeof(double) : 0;
+        const size_t mvb = mrb;                     // v slices of multi-RHS BiCGSTAB
         // tiny kernels over P > 1 (n <= 1024): their LL exchange slots, 4 ld words
         const size_t llb = (P > 1 && ld <= 1024) ? 4 * (size_t)ld * sizeof(uint64_t) : 0;
-        const size_t total = 2 * g + sb + fb + xb + mrb + msb + mxb + llb;
+        const size_t total = 2 * g + sb + fb + xb + mrb + msb + mxb + llb + mvb;
         char* base = nullptr;
         KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total));
         KS_CUDA(cudaMemset(base, 0, total));
@@ -110,15 +111,17 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         r.MS = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb) : nullptr;
         r.MX = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb + msb) : nullptr;
         r.llx = llb ? reinterpret_cast<uint64_t*>(base + 2 * g + sb + fb + xb + mrb + msb + mxb) : nullptr;
+        r.MV = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb + msb + mxb + llb) : nullptr;
         for (int q = 0; q < kMaxRanks; ++q) r.llpeer[q] = nullptr;
         r.llpeer[r.rank] = r.llx;
         for (int q = 0; q < kMaxRanks; ++q) {
-            r.mpeer.MR[q] = r.mpeer.MS[q] = r.mpeer.MX[q] = nullptr;
+            r.mpeer.MR[q] = r.mpeer.MS[q] = r.mpeer.MX[q] = r.mpeer.MV[q] = nullptr;
             r.mpeer.flags[q] = nullptr;
         }
         r.mpeer.MR[r.rank] = r.MR;
         r.mpeer.MS[r.rank] = r.MS;
         r.mpeer.MX[r.rank] = r.MX;
+        r.mpeer.MV[r.rank] = r.MV;
         r.mpeer.flags[r.rank] = r.flags;
         for (int q = 0; q < kMaxRanks; ++q) {
             r.pp.G_r[q] = r.pp.G_v[q] = r.pp.S[q] = r.pp.X[q] = nullptr;
@@ -254,6 +257,7 @@ void setup_peers(ks_ctx* c) {
     const bool mm = c->ranks[0].MR != nullptr;
     const size_t offMR = mm ? boff(c->ranks[0].MR) : 0, offMS = mm ? boff(c->ranks[0].MS) : 0,
                  offMX = mm ? boff(c->ranks[0].MX) : 0;
+    const size_t offMV = mm ? boff(c->ranks[0].MV) : 0;
     const bool hasll = c->ranks[0].llx != nullptr;
     const size_t offLL = hasll ? boff(c->ranks[0].llx) : 0;
     if (!c->multiprocess) {
@@ -279,6 +283,7 @@ void setup_peers(ks_ctx* c) {
                 a.mpeer.MR[b.rank] = b.MR;
                 a.mpeer.MS[b.rank] = b.MS;
                 a.mpeer.MX[b.rank] = b.MX;
+                a.mpeer.MV[b.rank] = b.MV;
                 a.mpeer.flags[b.rank] = b.flags;
                 a.llpeer[b.rank] = b.llx;
             }
@@ -318,6 +323,7 @@ void setup_peers(ks_ctx* c) {
             r.mpeer.MR[g] = reinterpret_cast<double*>(d + offMR);
             r.mpeer.MS[g] = reinterpret_cast<double*>(d + offMS);
             r.mpeer.MX[g] = reinterpret_cast<double*>(d + offMX);
+            r.mpeer.MV[g] = reinterpret_cast<double*>(d + offMV);
         }
     }
     // every rank must agree, or none uses the fused path (collectives must match)

@@ -75,7 +75,7 @@ struct Rank {
     double* S = nullptr;        // 2 * P * kScalSlot
     unsigned long long* flags = nullptr;   // [kNumPhases][kMaxRanks]
     double* X = nullptr;        // ld elements: contiguous full x (end-of-solve gather)
-    double *MR = nullptr, *MS = nullptr, *MX = nullptr;   // multi-RHS exchange regions (P > 1)
+    double *MR = nullptr, *MS = nullptr, *MX = nullptr, *MV = nullptr;   // multi-RHS exchange regions (P > 1)
     uint64_t* llx = nullptr;    // tiny kernels' LL slots in the exchange allocation (P > 1, ld <= 1024)
     const double* x0_full = nullptr;   // the current solve's full x0 on the device (s_full) or NULL
     uint64_t* llpeer[kMaxRanks] = {};

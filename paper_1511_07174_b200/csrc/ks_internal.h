@@ -298,7 +298,8 @@ struct MultiState { MultiCol col[kMaxRhs]; };
 // exchange allocation) and epoch flags.
 struct MultiPeer {
     double* MR[kMaxRanks];                  // [2 parities][P][kMaxRhs][chunk]: r slices
-    double* MS[kMaxRanks];                  // [2][P][2 kMaxRhs]: rank partial scalars
+    double* MV[kMaxRanks];                  // [2 parities][P][kMaxRhs][chunk]: v slices (BiCGSTAB)
+    double* MS[kMaxRanks];                  // [2][P][6 kMaxRhs]: rank partial scalars
     double* MX[kMaxRanks];                  // [kMaxRhs][ld]: the gathered x
     unsigned long long* flags[kMaxRanks];
 };
@@ -307,7 +308,7 @@ struct MultiArgs {
     int peer;                      // 1: P > 1 with the fused NVLink exchange
     Layout L;
     MultiPeer mp;
-    double *MRo, *MSo;             // this rank's own regions (read side)
+    double *MRo, *MVo, *MSo;       // this rank's own regions (read side)
     unsigned long long* flags;     // own [kNumPhases][kMaxRanks]
     unsigned long long ebase;      // epochs: setup ebase, iteration k ebase + k, x gather ebase + maxit + 1
     unsigned long long join_ns;

@@ -53,6 +53,11 @@ struct Stages { static constexpr int value = (WR * CH >= 1024) ? 3 : 4; };
 constexpr int kMW = 7;                    // consumer warps
 constexpr int kMT = (kMW + 1) * 32;       // + the producer warp
 constexpr int kMCT = kMW * 32;            // consumer threads
+// MS rows (rank partial scalars, per parity and rank): slot ranges per exchange phase
+// of one iteration, disjoint so a fast rank's next phase never overwrites a slot a
+// slow rank is still reading (CG: sigma [0, K), rho' [K, 2K); BiCGSTAB: <rhat, v>,
+// (<t,s>, <t,t>), (<rhat,r>, <r,r>)).
+constexpr int kMsV = 0, kMsS = 2 * kMaxRhs, kMsR = 4 * kMaxRhs, kMsRow = 6 * kMaxRhs;
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
     asm volatile(
@@ -207,7 +212,7 @@ __device__ __forceinline__ bool rank_sum(const MultiArgs& M, double (&v)[NV], in
                                          unsigned long long epoch) {
     if (!M.peer) return true;
     const int P = M.L.P, me = M.L.rank;
-    const int64_t row = 2 * kMaxRhs, pst = (int64_t)P * row;
+    const int64_t row = kMsRow, pst = (int64_t)P * row;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         for (int g = 0; g < P; ++g)
             for (int k = 0; k < NV; ++k) M.mp.MS[g][par * pst + (int64_t)me * row + q0 + k] = v[k];
@@ -227,9 +232,44 @@ __device__ __forceinline__ bool rank_sum(const MultiArgs& M, double (&v)[NV], in
     }
     return true;
 }
-// MR[par][g][k][chunk]: rank g's rows of column k of r (parity par)
+// MR / MV [par][g][k][chunk]: rank g's rows of column k of r / v (parity par)
 __device__ __forceinline__ int64_t mr_off(const MultiArgs& M, int par, int g, int k) {
     return (((int64_t)par * M.L.P + g) * kMaxRhs + k) * M.L.chunk;
+}
+// element j of column k of a full-length vector gathered in MR / MV; o = owner of j
+// (advanced monotonically by the caller's grid-stride loop)
+__device__ __forceinline__ double gathered(const MultiArgs& M, const double* G, int par, int k, int64_t j, int& o) {
+    while (o + 1 < M.L.P && j >= M.L.row0[o + 1]) ++o;
+    return __ldcg(G + mr_off(M, par, o, k) + (j - M.L.row0[o]));
+}
+
+// End of a P > 1 solve: every rank stores its rows of X into every rank's contiguous
+// MX (K x ld), one system fence per CTA, a grid barrier, then CTA 0 releases kPhaseX
+// (epoch ebase + maxit + 1) and waits for every rank's.
+template <int K, class Smem>
+__device__ void gather_x(const MultiArgs& M, Smem& S) {
+    (void)S;
+    const int tid = threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * kMCT, t0 = (int64_t)blockIdx.x * kMCT + tid;
+    if (tid < kMCT)
+        for (int64_t i = t0; i < M.m; i += gs)
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                for (int g = 0; g < M.L.P; ++g) M.mp.MX[g][k * M.ld + M.row0 + i] = M.X[k * M.ldm + i];
+    __syncthreads();
+    if (tid == 0) __threadfence_system();
+    if (!pk::grid_sync(M.bar, M.st)) return;
+    if (blockIdx.x == 0) {
+        if (tid == 0) {
+            unsigned long long* f[kMaxRanks];
+            for (int g = 0; g < M.L.P; ++g) f[g] = M.mp.flags[g] + kPhaseX * kMaxRanks + M.L.rank;
+            publish_flags(f, M.L.P, M.ebase + (unsigned long long)M.maxit + 1ull);
+        }
+        if (!wait_flags(M.flags + kPhaseX * kMaxRanks, M.L.P, M.ebase + (unsigned long long)M.maxit + 1ull) &&
+            tid == 0) {
+            M.st->peer_timeout = 1; M.st->status = KS_ENCCL;
+        }
+    }
 }
 
 template <int K, int WR, int CH>
@@ -463,34 +503,17 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
         if (!pk::grid_sync(M.bar, st)) return;
     }
     // ---- end: P > 1 gathers X into every rank's contiguous MX (K x ld)
-    if (peer) {
-        if (cons)
-            for (int64_t i = t0; i < m; i += gs)
-#pragma unroll
-                for (int k = 0; k < K; ++k)
-                    for (int g = 0; g < M.L.P; ++g) M.mp.MX[g][k * M.ld + M.row0 + i] = M.X[k * M.ldm + i];
-        __syncthreads();
-        if (tid == 0) __threadfence_system();
-        if (!pk::grid_sync(M.bar, st)) return;
-        if (blockIdx.x == 0) {
-            if (tid == 0) {
-                unsigned long long* f[kMaxRanks];
-                for (int g = 0; g < M.L.P; ++g) f[g] = M.mp.flags[g] + kPhaseX * kMaxRanks + M.L.rank;
-                publish_flags(f, M.L.P, M.ebase + (unsigned long long)M.maxit + 1ull);
-            }
-            if (!wait_flags(M.flags + kPhaseX * kMaxRanks, M.L.P, M.ebase + (unsigned long long)M.maxit + 1ull) &&
-                tid == 0) {
-                st->peer_timeout = 1; st->status = KS_ENCCL;
-            }
-        }
-    }
+    if (peer) gather_x<K>(M, S);
 }
 
-// ---- multi-RHS BiCGSTAB (one GPU): rows B0-B8 of SURVEY.md sec.8(c).4 per column,
-// the two GEMMs of an iteration (v = A p from P, t = A s from S) shared by the K
-// columns.  Per column: own rho, alpha, omega, the exact-zero / non-finite breakdown
-// tests (Q9), the half-step exit; a stopped column stops updating.  5 grid barriers
-// per iteration, as the single-RHS persistent BiCGSTAB.
+// ---- multi-RHS BiCGSTAB: rows B0-B8 of SURVEY.md sec.8(c).4 per column, the two
+// GEMMs of an iteration (v = A p from P, t = A s from S) shared by the K columns.  Per
+// column: own rho, alpha, omega, the exact-zero / non-finite breakdown tests (Q9), the
+// half-step exit; a stopped column stops updating.  5 grid barriers per iteration, as
+// the single-RHS persistent BiCGSTAB.  P > 1 (fused exchange): the v and r slices go
+// into every rank's MV / MR regions (parity of the iteration), <rhat, v>, (<t, s>,
+// <t, t>) and (<rhat, r>, <r, r>) are rank all-reduces in disjoint MS slots; s, p and
+// ||s||^2 are formed over the full length on every rank from the gathered r and v.
 template <int K, int WR, int CH>
 __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensorMap tmA,
                                                const __grid_constant__ CUtensorMap tmP,
@@ -504,8 +527,10 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
     const bool cons = tid < kMCT;
     const int64_t gs = (int64_t)gridDim.x * kMCT;
     const int64_t t0 = (int64_t)blockIdx.x * kMCT + tid;
-    const int64_t n = M.n;                 // one GPU: m == n
+    const int64_t n = M.n, m = M.m, row0 = M.row0;
     const bool lead = blockIdx.x == 0 && tid == 0;
+    const bool peer = M.peer != 0;
+    const int me = M.L.rank;
     if (tid == 0) {
         for (int s = 0; s < MultiSmem<K, WR, CH>::kMS; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kMW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -515,12 +540,26 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmP) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmS) : "memory");
     }
+    if (peer && lead) {                          // solve-start rendezvous (k_join's protocol)
+        unsigned long long* f[kMaxRanks];
+        for (int g = 0; g < M.L.P; ++g) f[g] = M.mp.flags[g] + kPhaseJ * kMaxRanks + me;
+        publish_flags(f, M.L.P, M.ebase);
+        const unsigned long long tj = globaltimer_ns();
+        for (int g = 0; g < M.L.P; ++g) {
+            while (flag_acquire_sys(M.flags + kPhaseJ * kMaxRanks + g) < M.ebase) {
+                if (globaltimer_ns() - tj > M.join_ns) { st->peer_timeout = 1; st->status = KS_ENCCL; st->done = 1; break; }
+                __nanosleep(64);
+            }
+        }
+    }
     __syncthreads();
+    if (peer && !pk::grid_sync(M.bar, st)) return;
+    if (*(volatile const int*)&st->peer_timeout) return;
     uint32_t it = 0;
     double d1[K], d2[K];
     // ---- B0: r0 = b - A x0 (or b), rhat = r0, x = x0 (or 0), ||b||, rho_1 = <rhat, r0>
     if (M.has_x0) {
-        gemm_phase<K, WR, CH>(&tmA, &tmP, M, S, it, d1);          // Q = A x0 (P holds x0)
+        gemm_phase<K, WR, CH>(&tmA, &tmP, M, S, it, d1);          // Q = A x0 (P holds the full x0)
         if (!pk::grid_sync(M.bar, st)) return;
     }
     {
@@ -528,7 +567,7 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
 #pragma unroll
         for (int k = 0; k < 2 * K; ++k) v[k] = 0.0;
         if (cons) {
-            for (int64_t i = t0; i < n; i += gs) {
+            for (int64_t i = t0; i < m; i += gs) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const double bk = M.R[k * M.ldm + i];
@@ -537,38 +576,47 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
                     v[K + k] = fma(r, r, v[K + k]);
                     M.R[k * M.ldm + i] = r;
                     M.Rh[k * M.ldm + i] = r;                           // rhat = r0 (Q7)
-                    M.X[k * M.ldm + i] = M.has_x0 ? M.Pf[k * M.ld + i] : 0.0;
+                    M.X[k * M.ldm + i] = M.has_x0 ? M.Pf[k * M.ld + row0 + i] : 0.0;
+                    if (peer)
+                        for (int g = 0; g < M.L.P; ++g) M.mp.MR[g][mr_off(M, 0, me, k) + i] = r;
                 }
             }
         }
+        if (peer) { __syncthreads(); if (tid == 0) __threadfence_system(); }
         csum<2 * K>(v, S.red);
         if (tid == 0) {
 #pragma unroll
             for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
-        double tb[K], tr[K];
-        totals<K>(M.bpart, 0, tb, S.red);
-        totals<K>(M.bpart, K, tr, S.red);
+        double tbr[2 * K];
+        {
+            double tb[K], tr[K];
+            totals<K>(M.bpart, 0, tb, S.red);
+            totals<K>(M.bpart, K, tr, S.red);
+#pragma unroll
+            for (int k = 0; k < K; ++k) { tbr[k] = tb[k]; tbr[K + k] = tr[k]; }
+        }
+        if (!rank_sum<2 * K>(M, tbr, 0, kMsR, kPhaseR, M.ebase)) return;
         if (cons) {
-            for (int64_t i = t0; i < n; i += gs)
+            for (int64_t i = t0; i < m; i += gs)
 #pragma unroll
                 for (int k = 0; k < K; ++k)
-                    if (!(k < M.nrhs) || tb[k] == 0.0) M.X[k * M.ldm + i] = 0.0;   // Q6
+                    if (!(k < M.nrhs) || tbr[k] == 0.0) M.X[k * M.ldm + i] = 0.0;   // Q6
         }
         if (lead) {
             for (int k = 0; k < K; ++k) {
                 MultiCol& cl = ms->col[k];
-                cl.nb = sqrt(tb[k]);
-                cl.rho = tr[k];                                   // <rhat, r0> = <r0, r0>
+                cl.nb = sqrt(tbr[k]);
+                cl.rho = tbr[K + k];                              // <rhat, r0> = <r0, r0>
                 cl.rho_old = cl.alpha = cl.omega = 1.0;           // Q8
                 cl.iters = 0; cl.relres = 0.0; cl.status = KS_EMAXIT; cl.active = 1;
                 cl.half = 0; cl.breakdown = 0;
-                if (k >= M.nrhs || tb[k] == 0.0) {
+                if (k >= M.nrhs || tbr[k] == 0.0) {
                     cl.active = 0; cl.status = KS_OK; cl.converged = 1; cl.bzero = 1;
                 } else {
                     cl.converged = 0; cl.bzero = 0;
-                    cl.relres = sqrt(tr[k]) / cl.nb;
+                    cl.relres = sqrt(tbr[K + k]) / cl.nb;
                     if (cl.relres <= M.tol) { cl.active = 0; cl.status = KS_OK; cl.converged = 1; }   // Q2
                 }
             }
@@ -576,6 +624,7 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
         if (!pk::grid_sync(M.bar, st)) return;
     }
     for (long long i1 = 1; i1 <= M.maxit; ++i1) {
+        const int par = (int)(i1 & 1), pprev = par ^ 1;
         int act[K];
         int any = 0;
         double rho[K], beta[K], omega[K];
@@ -595,19 +644,21 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
             any |= act[k];
         }
         if (!any) break;
-        // B1: p = r + beta (p - omega v)   (i = 1: p = r)
+        // B1: p = r + beta (p - omega v) over the full length   (i = 1: p = r)
         if (cons) {
+            int o = 0, o2 = 0;
             for (int64_t j = t0; j < n; j += gs)
 #pragma unroll
                 for (int k = 0; k < K; ++k)
                     if (act[k]) {
-                        const double r = M.R[k * M.ldm + j];
-                        M.Pf[k * M.ld + j] = i1 == 1 ? r
-                            : fma(beta[k], fma(-omega[k], M.Q[k * M.ldm + j], M.Pf[k * M.ld + j]), r);
+                        const double r = peer ? gathered(M, M.MRo, pprev, k, j, o) : M.R[k * M.ldm + j];
+                        if (i1 == 1) { M.Pf[k * M.ld + j] = r; continue; }
+                        const double vv = peer ? gathered(M, M.MVo, pprev, k, j, o2) : M.Q[k * M.ldm + j];
+                        M.Pf[k * M.ld + j] = fma(beta[k], fma(-omega[k], vv, M.Pf[k * M.ld + j]), r);
                     }
         }
         if (!pk::grid_sync(M.bar, st)) return;
-        // B3: v = A p (into Q), gamma partials <rhat, v>
+        // B3: v = A p (own rows, into Q; P > 1: pushed to every rank's MV), <rhat, v> partials
         gemm_phase<K, WR, CH>(&tmA, &tmP, M, S, it, d1, M.Q, M.Rh, M.ldm, 0);
         __syncthreads();
         if ((tid & 31) == 0 && tid < kMCT) {
@@ -624,8 +675,21 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
             }
         }
         if (!pk::grid_sync(M.bar, st)) return;
+        if (peer) {                                  // every CTA's rows of v are complete: push them
+            if (cons)
+                for (int64_t i = t0; i < m; i += gs)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const double vv = M.Q[k * M.ldm + i];
+                        for (int g = 0; g < M.L.P; ++g) M.mp.MV[g][mr_off(M, par, me, k) + i] = vv;
+                    }
+            __syncthreads();
+            if (tid == 0) __threadfence_system();
+            if (!pk::grid_sync(M.bar, st)) return;
+        }
         double gam[K], alpha[K];
         totals<K>(M.bpart, 0, gam, S.red);
+        if (!rank_sum<K>(M, gam, par, kMsV, kPhaseV, M.ebase + (unsigned long long)i1)) return;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             if (act[k] && (gam[k] == 0.0 || !isfinite(gam[k]))) {          // Q9
@@ -635,16 +699,19 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
             }
             alpha[k] = act[k] ? rho[k] / gam[k] : 0.0;
         }
-        // B4: s = r - alpha v (full length), ||s||^2
+        // B4: s = r - alpha v over the full length (identical on every rank), ||s||^2
         double ssp[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) ssp[k] = 0.0;
         if (cons) {
+            int o = 0, o2 = 0;
             for (int64_t j = t0; j < n; j += gs)
 #pragma unroll
                 for (int k = 0; k < K; ++k)
                     if (act[k]) {
-                        const double sv = fma(-alpha[k], M.Q[k * M.ldm + j], M.R[k * M.ldm + j]);
+                        const double r = peer ? gathered(M, M.MRo, pprev, k, j, o) : M.R[k * M.ldm + j];
+                        const double vv = peer ? gathered(M, M.MVo, par, k, j, o2) : M.Q[k * M.ldm + j];
+                        const double sv = fma(-alpha[k], vv, r);
                         M.Sf[k * M.ld + j] = sv;
                         ssp[k] = fma(sv, sv, ssp[k]);
                     }
@@ -675,13 +742,13 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
             }
         }
         if (cons) {                                                        // half step: x += alpha p
-            for (int64_t j = t0; j < n; j += gs)
+            for (int64_t i = t0; i < m; i += gs)
 #pragma unroll
                 for (int k = 0; k < K; ++k)
-                    if (half[k]) M.X[k * M.ldm + j] = fma(alpha[k], M.Pf[k * M.ld + j], M.X[k * M.ldm + j]);
+                    if (half[k]) M.X[k * M.ldm + i] = fma(alpha[k], M.Pf[k * M.ld + row0 + i], M.X[k * M.ldm + i]);
         }
-        // B6: t = A s (into T), <s, t> and <t, t>
-        gemm_phase<K, WR, CH, true>(&tmA, &tmS, M, S, it, d1, M.T, M.Sf, M.ld, 0, d2);
+        // B6: t = A s (own rows, into T), <s, t> and <t, t> partials
+        gemm_phase<K, WR, CH, true>(&tmA, &tmS, M, S, it, d1, M.T, M.Sf, M.ld, row0, d2);
         __syncthreads();
         if ((tid & 31) == 0 && tid < kMCT) {
 #pragma unroll
@@ -698,62 +765,81 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
             }
         }
         if (!pk::grid_sync(M.bar, st)) return;
-        double ts[K], tt[K], om[K];
-        totals<K>(M.bpart, 0, ts, S.red);
-        totals<K>(M.bpart, K, tt, S.red);
+        double tst[2 * K];
+        {
+            double ts[K], tt[K];
+            totals<K>(M.bpart, 0, ts, S.red);
+            totals<K>(M.bpart, K, tt, S.red);
+#pragma unroll
+            for (int k = 0; k < K; ++k) { tst[k] = ts[k]; tst[K + k] = tt[k]; }
+        }
+        if (!rank_sum<2 * K>(M, tst, par, kMsS, kPhaseS, M.ebase + (unsigned long long)i1)) return;
+        double om[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             om[k] = 0.0;
             if (!act[k]) continue;
-            bool bad = tt[k] == 0.0 || !isfinite(tt[k]);
-            if (!bad) { om[k] = ts[k] / tt[k]; bad = om[k] == 0.0 || !isfinite(om[k]); }
+            const double tt = tst[K + k];
+            bool bad = tt == 0.0 || !isfinite(tt);
+            if (!bad) { om[k] = tst[k] / tt; bad = om[k] == 0.0 || !isfinite(om[k]); }
             if (bad) {                                                     // Q9
                 act[k] = 0;
                 if (lead) { ms->col[k].active = 0; ms->col[k].status = KS_EBREAKDOWN; ms->col[k].breakdown = 1;
                             ms->col[k].iters = i1 - 1; }
             }
         }
-        // B7: x = (x + alpha p) + omega s; r = s - omega t; <rhat, r>, <r, r>
+        // B7: x = (x + alpha p) + omega s; r = s - omega t (own rows; P > 1: pushed);
+        // <rhat, r>, <r, r> partials
         double v2[2 * K];
 #pragma unroll
         for (int k = 0; k < 2 * K; ++k) v2[k] = 0.0;
         if (cons) {
-            for (int64_t j = t0; j < n; j += gs)
+            for (int64_t i = t0; i < m; i += gs)
 #pragma unroll
                 for (int k = 0; k < K; ++k)
                     if (act[k]) {
-                        const double sv = M.Sf[k * M.ld + j];
-                        M.X[k * M.ldm + j] = fma(om[k], sv, fma(alpha[k], M.Pf[k * M.ld + j], M.X[k * M.ldm + j]));
-                        const double r = fma(-om[k], M.T[k * M.ldm + j], sv);
-                        M.R[k * M.ldm + j] = r;
-                        v2[k] = fma(M.Rh[k * M.ldm + j], r, v2[k]);
+                        const double sv = M.Sf[k * M.ld + row0 + i];
+                        M.X[k * M.ldm + i] = fma(om[k], sv, fma(alpha[k], M.Pf[k * M.ld + row0 + i], M.X[k * M.ldm + i]));
+                        const double r = fma(-om[k], M.T[k * M.ldm + i], sv);
+                        M.R[k * M.ldm + i] = r;
+                        if (peer)
+                            for (int g = 0; g < M.L.P; ++g) M.mp.MR[g][mr_off(M, par, me, k) + i] = r;
+                        v2[k] = fma(M.Rh[k * M.ldm + i], r, v2[k]);
                         v2[K + k] = fma(r, r, v2[K + k]);
                     }
         }
+        if (peer) { __syncthreads(); if (tid == 0) __threadfence_system(); }
         csum<2 * K>(v2, S.red);
         if (tid == 0) {
 #pragma unroll
             for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v2[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
-        double rhn[K], rr[K];
-        totals<K>(M.bpart, 0, rhn, S.red);
-        totals<K>(M.bpart, K, rr, S.red);
+        double rr2[2 * K];
+        {
+            double rhn[K], rr[K];
+            totals<K>(M.bpart, 0, rhn, S.red);
+            totals<K>(M.bpart, K, rr, S.red);
+#pragma unroll
+            for (int k = 0; k < K; ++k) { rr2[k] = rhn[k]; rr2[K + k] = rr[k]; }
+        }
+        if (!rank_sum<2 * K>(M, rr2, par, kMsR, kPhaseR, M.ebase + (unsigned long long)i1)) return;
         // B8: history, test; rho_old = rho, rho = <rhat, r>
         if (lead) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 if (!act[k]) continue;
                 MultiCol& cl = ms->col[k];
-                const double rel = sqrt(rr[k]) / cl.nb;
+                const double rel = sqrt(rr2[K + k]) / cl.nb;
                 if (M.hist && i1 - 1 < M.hist_cap) M.hist[(int64_t)k * M.hist_cap + (i1 - 1)] = rel;
                 cl.relres = rel; cl.iters = i1;
-                cl.rho_old = rho[k]; cl.rho = rhn[k]; cl.alpha = alpha[k]; cl.omega = om[k];
+                cl.rho_old = rho[k]; cl.rho = rr2[k]; cl.alpha = alpha[k]; cl.omega = om[k];
                 if (rel <= M.tol) { cl.active = 0; cl.converged = 1; cl.status = KS_OK; }
             }
         }
         if (!pk::grid_sync(M.bar, st)) return;
     }
+    if (peer) gather_x<K>(M, S);
 }
 
 // shapes: 0 = (4 rows/warp, 128 columns, 4 stages), 1 = (8, 64, 4), 2 = (8, 128, 3)

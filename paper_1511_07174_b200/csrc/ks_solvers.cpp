@@ -905,6 +905,7 @@ int64_t run_multi(ks_ctx* c, Rank& r, int bicgstab, int nrhs, const double* B, c
     M.L = r.L;
     M.mp = r.mpeer;
     M.MRo = r.MR;
+    M.MVo = r.MV;
     M.MSo = r.MS;
     M.flags = r.flags;
     M.ebase = r.epoch_next;

@@ -214,3 +214,28 @@ def test_bicgstab_multi_exits_and_repeat():
     assert ro[1].status == r[1].status == ks.KS_EBREAKDOWN and r[1].iterations == 0 and np.all(X[:, 1] == 0)
     assert r[0].status == ks.KS_OK
     bars(X[:, 0], h[0], r[0], Xo[:, 0], ho[0], ro[0], floor=FLOOR_BS)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_bicgstab_multi_over_p_gpus(P):
+    """Multi-RHS BiCGSTAB over P GPUs: v and r slices through every rank's exchange
+    regions, the per-column dots as rank all-reduces; per-column bars vs the oracle
+    (half-step exits, a b = 0 column, small x0), bitwise repeat, and the one-GPU
+    result within the bars."""
+    if _ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    from test_gpu_parity import FLOOR_BS
+    n = 2050
+    D, B = gdd_block(n, 5)
+    B[:, 3] = 0.0
+    X0 = 1e-3 * np.random.default_rng(P).standard_normal((n, 5))
+    Xo, ho, ro = oracle.bicgstab_multi(D, B, X0=X0, tol=1e-10)
+    with ks.Context(n, ngpus=P) as ctx:
+        ctx.load_rows(D)
+        X, h, r = ctx.bicgstab_multi(B, X0=X0, tol=1e-10)
+        for k in (0, 1, 2, 4):
+            bars(X[:, k], h[k], r[k], Xo[:, k], ho[k], ro[k], floor=FLOOR_BS)
+            assert r[k].half_step_exit == ro[k].half_step_exit
+        assert r[3].iterations == 0 and np.all(X[:, 3] == 0)
+        X2, _, _ = ctx.bicgstab_multi(B, X0=X0, tol=1e-10)
+        assert np.array_equal(X2, X)
