@@ -201,7 +201,7 @@ def test_bicgstab_multi_exits_and_repeat():
         Xs, hs, rs = ctx.bicgstab_multi(B[:, :1], tol=1e-10)
         bars(Xs[:, 0], hs[0], rs[0], x1, h1, r1, floor=FLOOR_BS)
     A = np.zeros((n, n))
-    A[: n // 2, : n // 2] = np.diag(np.arange(1.0, n // 2 + 1))
+    A[: n // 2, : n // 2] = np.diag(1.0 + np.arange(n // 2) % 4)   # 4 distinct eigenvalues: a few exact steps
     for i in range(n // 2, n, 2):
         A[i, i + 1], A[i + 1, i] = 1.0, -1.0
     Bb = np.zeros((n, 2))

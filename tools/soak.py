@@ -25,7 +25,7 @@ ctxs, fails, stats = {}, [], {"solves": 0, "iters": 0}
 t0 = time.time()
 for it in range(rounds):
     n = int(rng.choice([300, 777, 1024, 1000, 2049, 4096, 5003]))
-    method = str(rng.choice(["cg", "bicgstab", "bicg", "gmres", "cg_multi"]))
+    method = str(rng.choice(["cg", "bicgstab", "bicg", "gmres", "cg_multi", "bicgstab_multi"]))
     if method in ("cg", "cg_multi") and n % 2:
         n += 1                                   # G-SPD needs an even n
     key = (n, method)
@@ -40,17 +40,17 @@ for it in range(rounds):
         ctxs[key] = c
     c = ctxs[key]
     b = synth.rhs(n, synth.SEED + it)
-    if method == "cg_multi":                      # multi-RHS: a block of k right-hand sides
+    if method in ("cg_multi", "bicgstab_multi"):  # multi-RHS: a block of k right-hand sides
         k = int(rng.integers(1, 9))
         B = np.column_stack([synth.rhs(n, synth.SEED + 1000 * it + j) for j in range(k)])
         if rng.random() < 0.3:
             mx = int(rng.integers(1, 12))
-            X1, _, r1 = c.cg_multi(B, tol=0.0, maxit=mx)
-            X2, _, r2 = c.cg_multi(B, tol=0.0, maxit=mx)
+            X1, _, r1 = getattr(c, method)(B, tol=0.0, maxit=mx)
+            X2, _, r2 = getattr(c, method)(B, tol=0.0, maxit=mx)
             if not np.array_equal(X1, X2):
                 fails.append({"round": it, "n": n, "method": method, "why": "not repeatable"})
         else:
-            X, _, rs = c.cg_multi(B, tol=1e-10)
+            X, _, rs = getattr(c, method)(B, tol=1e-10)
             for j in range(k):
                 res = np.linalg.norm(c.matvec(X[:, j]) - B[:, j]) / np.linalg.norm(B[:, j])
                 if not (rs[j].converged and res <= 1e-8):
