@@ -25,7 +25,8 @@ constexpr unsigned char kPattern = 0xA5;
 
 struct Entry {
     char* base;
-    size_t bytes;
+    size_t bytes;    // the caller's exact size
+    size_t padded;   // rounded up to 256 bytes (the trailing zone starts at bytes, not here)
     int dev;
 };
 
@@ -48,11 +49,17 @@ int64_t g_violations = 0;   // corrupted zones found at free time
 int zone_errors(const Entry& e) {
     std::vector<unsigned char> h(kGuard);
     int bad = 0;
-    for (const char* z : {e.base, e.base + kGuard + e.bytes}) {
-        if (cudaMemcpy(h.data(), z, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
-        for (unsigned char b : h)
-            if (b != kPattern) { ++bad; break; }
-    }
+    // leading zone, then the trailing zone from the exact end of the buffer: the
+    // alignment padding [bytes, padded) is canary too (overruns of up to
+    // 255 bytes into the padding used to go unseen)
+    const size_t tail = e.padded - e.bytes + kGuard;
+    std::vector<unsigned char> t(tail);
+    if (cudaMemcpy(h.data(), e.base, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    for (unsigned char b : h)
+        if (b != kPattern) { ++bad; break; }
+    if (cudaMemcpy(t.data(), e.base + kGuard + e.bytes, tail, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    for (unsigned char b : t)
+        if (b != kPattern) { ++bad; break; }
     return bad;
 }
 
@@ -69,7 +76,7 @@ void* dev_alloc(size_t bytes) {
     char* base = nullptr;
     KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), padded + 2 * kGuard));
     KS_CUDA(cudaMemset(base, kPattern, kGuard));
-    KS_CUDA(cudaMemset(base + kGuard + padded, kPattern, kGuard));
+    KS_CUDA(cudaMemset(base + kGuard + bytes, kPattern, padded - bytes + kGuard));
     int dev = 0;
     KS_CUDA(cudaGetDevice(&dev));
     void* user = base + kGuard;
@@ -78,9 +85,9 @@ void* dev_alloc(size_t bytes) {
         const char* v = std::getenv("KS_GUARD_SELFTEST");
         return v && v[0] == '1';
     }();
-    if (selftest) KS_CUDA(cudaMemset(base + kGuard + padded, 0, 1));
+    if (selftest) KS_CUDA(cudaMemset(base + kGuard + bytes, 0, 1));   // the first byte past the buffer
     std::lock_guard<std::mutex> lk(g_mu);
-    registry()[user] = Entry{base, padded, dev};
+    registry()[user] = Entry{base, bytes, padded, dev};
     return user;
 }
 

@@ -12,9 +12,10 @@ assert os.environ.get("KS_GUARD") == "1", "run with KS_GUARD=1"
 ngpu = torch.cuda.device_count()
 total = 0
 modes = [{}, {"persistent": 0}, {"persistent": 0, "use_graphs": 1}, {"persistent": 0, "gemv_rows": 8},
-         {"persistent": 0, "gemv_split": 3}, {"small": 0}, {"poll_batch": 3}, {"gemv_rows": 4, "gemv_unroll": 2}]
+         {"persistent": 0, "gemv_split": 3}, {"small": 0}, {"poll_batch": 3}, {"gemv_rows": 4, "gemv_unroll": 2},
+         {"tiny": 0}]
 for P in [p for p in (1, 2, 4) if p <= ngpu]:
-    for n in (777, 2050):
+    for n in (300, 777, 1024, 2050):            # n <= 1024: the tiny kernels by default
         A = synth.random_spd(n, 100.0, 1)
         D = synth.gdd(n, 4, seed=synth.SEED2)[0]
         b = synth.rhs(n)
@@ -35,6 +36,10 @@ for P in [p for p in (1, 2, 4) if p <= ngpu]:
                         c2.bicg(b, tol=tol, maxit=40)
                         c2.gmres(b, tol=tol, restart=7, maxit=40)
                         c2.matvec_t(b)
+                        if not opts:                    # multi-RHS kernels (TMA GEMM), 3 columns
+                            B = np.column_stack([b, synth.rhs(n, synth.SEED + 1), np.zeros(n)])
+                            c1.cg_multi(B, tol=tol, maxit=30)
+                            c2.bicgstab_multi(B, X0=1e-3 * np.ones((n, 3)), tol=tol, maxit=20)
                     v1, v2 = c1.check_guards(), c2.check_guards()
                     total = max(total, v1, v2)
                     if v1 or v2:
