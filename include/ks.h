@@ -140,11 +140,20 @@ typedef enum {
                               /* sync); a rank that does not arrive within this   */
                               /* many ms (default 120000) fails the solve with    */
                               /* KS_ENCCL.  In-loop waits stay bounded at 10 s.   */
-    KS_OPT_TINY = 14          /* 1 (default): one GPU, FP64, n <= 1024, whole     */
+    KS_OPT_TINY = 14,         /* 1 (default): one GPU, FP64, n <= 1024, whole     */
                               /* solve in one launch -> the register-resident     */
                               /* kernels (A in shared memory, vectors replicated  */
                               /* in registers, LL-format exchange of the GEMV     */
                               /* output: no grid barrier); 0 = off                */
+    KS_OPT_JITTER = 15        /* race detection: seed (0 = off, default) of       */
+                              /* pseudo-random delays (<= ~4 us, a quarter of the */
+                              /* visits) at every synchronisation point of the    */
+                              /* persistent, small, tiny and multi-RHS kernels    */
+                              /* (grid-barrier arrival / departure, flag publish  */
+                              /* and wait, LL store and poll).  Results must not  */
+                              /* change: the kernels' sums have fixed orders and  */
+                              /* their exchanges are epoch-tagged, so a run with  */
+                              /* jitter equals a run without it bit for bit.      */
 } ks_option;
 
 /* Creates the opaque object that encapsulates the distributed matrix and its
@@ -158,6 +167,20 @@ typedef enum {
  * and <= device count, dtype = KS_FLOAT64 or KS_FLOAT32.  Allocates each shard (m_g x ld)
  * plus O(n) vectors with cudaMalloc and zero-fills them.                        */
 ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
+
+/* As ks_create, with rank g on device devices[g] (nranks entries, 1..16, each a
+ * valid device ordinal).  A device may be listed more than once: its ranks split its
+ * SMs (each rank's persistent grids are sized from SM count / ranks on that device,
+ * so co-running ranks stay co-resident) and exchange over the same fused
+ * load/store path as ranks on different GPUs ("communication ...
+ * encapsulated in opaque objects": the distribution does not depend on where the
+ * ranks run).  Such a context has no NCCL communicator (NCCL rejects two ranks on
+ * one GPU): its non-fused collectives are host-driven peer copies ordered by
+ * events.  Meant for validating the P > 1 schedules on fewer GPUs than ranks; results
+ * equal the oracle's within the same bars, not bitwise those of P distinct GPUs
+ * (the grid sizes, and so the partial-sum orders, differ).  KS_EARG for a bad
+ * device list or missing peer access, KS_EDIM for n < nranks.                    */
+ks_status ks_create_on(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t nranks, const int32_t* devices);
 
 /* One rank of a multi-process job (one process per GPU, e.g. torchrun) -- the
  * paper's one-MPI-process-per-node model ("MPI ... for the

@@ -31,8 +31,8 @@ OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 
            "gemv_split": 4, "gemv_kernel": 5, "use_graphs": 6, "fused_comm": 7,
            "persistent": 8, "gemv_unroll": 9, "persist_grid": 10,
            "gemvt_shape": 11, "small": 12, "join_timeout_ms": 13,
-           "tiny": 14}
-EXPORTS = ["ks_create", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
+           "tiny": 14, "jitter": 15}
+EXPORTS = ["ks_create", "ks_create_on", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
            "ks_generate", "ks_matvec", "ks_matvec_t", "ks_time_matvec", "ks_cg", "ks_bicgstab",
            "ks_bicg", "ks_gmres", "ks_cg_multi", "ks_bicgstab_multi",
            "ks_set_option", "ks_get_option", "ks_info", "ks_check_guards", "ks_last_error", "ks_version"]
@@ -93,6 +93,7 @@ def lib():
         pp = C.POINTER(C.c_void_p)
         sig = {
             "ks_create": [pp, i64, C.c_int, i32],
+            "ks_create_on": [pp, i64, C.c_int, i32, C.POINTER(i32)],
             "ks_create_rank": [pp, i64, C.c_int, i32, i32, vp, i32, vp],
             "ks_destroy": [vp],
             "ks_row_range": [vp, i32, C.POINTER(i64), C.POINTER(i64)],
@@ -178,11 +179,17 @@ def _out64(a, n: int | None, name: str):
 class Context:
     """Opaque solver context: A resident in HBM, row-block sharded."""
 
-    def __init__(self, n: int, ngpus: int = 1, *, dtype: str = "f64", _handle=None):
+    def __init__(self, n: int, ngpus: int = 1, *, dtype: str = "f64", devices=None, _handle=None):
+        """ngpus ranks on GPUs 0..ngpus-1, or rank g on devices[g] (ks_create_on: a
+        device may repeat -- its ranks split its SMs; for validating P > 1 schedules
+        on fewer GPUs)."""
         self._h = C.c_void_p()
         self.dtype = "f32" if DTYPES[dtype] == 1 else "f64"
         if _handle is not None:
             self._h = _handle
+        elif devices is not None:
+            devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+            self._check(lib().ks_create_on(C.byref(self._h), int(n), DTYPES[dtype], len(devices), devs))
         else:
             self._check(lib().ks_create(C.byref(self._h), int(n), DTYPES[dtype], int(ngpus)))
         lg, nr, nn, ld = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()

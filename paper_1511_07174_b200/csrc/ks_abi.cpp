@@ -1,6 +1,7 @@
 // L4: the extern "C" boundary declared in include/ks.h.  Validates arguments
 // before any work, converts internal exceptions to ks_status + message, and
 // poisons the context on CUDA/NCCL/allocation errors.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -81,34 +82,48 @@ ks_status status_of(int64_t s) { return (ks_status)s; }
 
 extern "C" {
 
-ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus) {
+ks_status ks_create_on(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t nranks, const int32_t* devices) {
     if (!out) return fail(nullptr, KS_EARG, "out is NULL");
     *out = nullptr;
     if (dtype != KS_FLOAT64 && dtype != KS_FLOAT32) return fail(nullptr, KS_EARG, "dtype must be KS_FLOAT64 or KS_FLOAT32");
     if (n < 1) return fail(nullptr, KS_EDIM, "n must be >= 1");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
-    if (ngpus < 1 || ngpus > ks::kMaxRanks || ngpus > ndev)
-        return fail(nullptr, KS_EARG, "ngpus must be in [1, min(16, device count=" + std::to_string(ndev) + ")]");
-    if (n < ngpus) return fail(nullptr, KS_EDIM, "n must be >= ngpus");
+    if (nranks < 1 || nranks > ks::kMaxRanks || !devices)
+        return fail(nullptr, KS_EARG, "nranks must be in [1, 16] and devices non-NULL");
+    std::vector<int> devs((size_t)nranks);
+    bool shared = false;
+    for (int g = 0; g < nranks; ++g) {
+        devs[g] = devices[g];
+        if (devs[g] < 0 || devs[g] >= ndev)
+            return fail(nullptr, KS_EARG, "devices[" + std::to_string(g) + "] is not a device (count=" +
+                                              std::to_string(ndev) + ")");
+        for (int h = 0; h < g; ++h) shared = shared || devs[h] == devs[g];
+    }
+    if (n < nranks) return fail(nullptr, KS_EDIM, "n must be >= nranks");
     ks_ctx* c = new ks_ctx();
     c->n = n;
-    c->P = ngpus;
+    c->P = nranks;
     c->dtype = dtype;
     c->esz = dtype == KS_FLOAT32 ? sizeof(float) : sizeof(double);
-    c->ranks.resize((size_t)ngpus);
-    for (int g = 0; g < ngpus; ++g) { c->ranks[g].rank = g; c->ranks[g].dev = g; }
+    c->shared_dev = shared;
+    c->ranks.resize((size_t)nranks);
+    for (int g = 0; g < nranks; ++g) {
+        c->ranks[g].rank = g;
+        c->ranks[g].dev = devs[g];
+        c->ranks[g].dev_share = (int)std::count(devs.begin(), devs.end(), devs[g]);
+    }
     make_layout(c);
     ks_status st = guarded(c, [&] {
-        if (ngpus > 1) {
-            std::vector<ncclComm_t> comms((size_t)ngpus);
-            std::vector<int> devs((size_t)ngpus);
-            for (int g = 0; g < ngpus; ++g) devs[g] = g;
-            KS_NCCL(ncclCommInitAll(comms.data(), ngpus, devs.data()));
-            for (int g = 0; g < ngpus; ++g) { c->ranks[g].comm = comms[g]; c->ranks[g].own_comm = true; }
+        if (nranks > 1 && !shared) {
+            std::vector<ncclComm_t> comms((size_t)nranks);
+            KS_NCCL(ncclCommInitAll(comms.data(), nranks, devs.data()));
+            for (int g = 0; g < nranks; ++g) { c->ranks[g].comm = comms[g]; c->ranks[g].own_comm = true; }
         }
         c->for_each_rank([&](Rank& r) { ks::rank_alloc(c, r); });
         ks::setup_peers(c);
+        if (shared && !c->ranks[0].peer_ok)
+            throw ks::KsError(KS_EARG, "ranks sharing a device need peer access between all listed devices");
         return KS_OK;
     });
     if (st != KS_OK) {
@@ -118,6 +133,20 @@ ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus) {
     }
     *out = c;
     return KS_OK;
+}
+
+ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus) {
+    if (!out) return fail(nullptr, KS_EARG, "out is NULL");
+    *out = nullptr;
+    if (dtype != KS_FLOAT64 && dtype != KS_FLOAT32) return fail(nullptr, KS_EARG, "dtype must be KS_FLOAT64 or KS_FLOAT32");
+    if (n < 1) return fail(nullptr, KS_EDIM, "n must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
+    if (ngpus < 1 || ngpus > ks::kMaxRanks || ngpus > ndev)
+        return fail(nullptr, KS_EARG, "ngpus must be in [1, min(16, device count=" + std::to_string(ndev) + ")]");
+    std::vector<int32_t> devs((size_t)ngpus);
+    for (int g = 0; g < ngpus; ++g) devs[g] = g;
+    return ks_create_on(out, n, dtype, ngpus, devs.data());
 }
 
 ks_status ks_create_rank(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t rank, int32_t nranks,
@@ -574,6 +603,22 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
         case KS_OPT_TINY:
             if (v < 0 || v > 1) return fail(c, KS_EARG, "tiny must be 0 or 1");
             o.tiny = v; break;
+        case KS_OPT_JITTER: {
+            if (v < 0 || v > 0xffffffffLL) return fail(c, KS_EARG, "jitter seed must be in [0, 2^32)");
+            const unsigned seed = (unsigned)v;
+            ks_status st = guarded(c, [&] {
+                c->for_each_rank([&](Rank& r) {
+                    KS_CUDA(cudaStreamSynchronize(r.stream));
+                    KS_CUDA(cudaMemcpy(&r.st->jitter, &seed, sizeof(seed), cudaMemcpyHostToDevice));
+                    r.jitter = seed;
+                    for (auto& g : r.graphs) g.kind = -1;   // captured kernel parameters are stale
+                });
+                return KS_OK;
+            });
+            if (st != KS_OK) return st;
+            o.jitter = v;
+            break;
+        }
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -606,6 +651,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_SMALL: *v = o.small; break;
         case KS_OPT_JOIN_TIMEOUT_MS: *v = o.join_timeout_ms; break;
         case KS_OPT_TINY: *v = o.tiny; break;
+        case KS_OPT_JITTER: *v = o.jitter; break;
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

@@ -24,6 +24,7 @@ VecArgs Rank::vargs(bool fused) const {
     a.gpar = fused ? (int64_t)L.P * L.chunk : 0;
     a.spar = fused ? (int64_t)L.P * kScalSlot : 0;
     a.peer = fused ? 1 : 0;
+    a.jitter = jitter;
     a.pp = pp;
     a.flags = flags;
     a.L = L;
@@ -64,6 +65,10 @@ static T* as(double* p) { return reinterpret_cast<T*>(p); }
 void rank_alloc(ks_ctx* c, Rank& r) {
     KS_CUDA(cudaSetDevice(r.dev));
     KS_CUDA(cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, r.dev));
+    // ranks sharing a GPU split its SMs: every persistent grid of a rank is sized from
+    // num_sms, so the co-running ranks' grids stay co-resident (their in-kernel waits
+    // on each other need that)
+    r.num_sms = std::max(1, r.num_sms / std::max(1, r.dev_share));
     if (!r.stream) {
         KS_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
         r.own_stream = true;
@@ -149,6 +154,7 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     for (auto& e : r.ev_poll) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     KS_CUDA(cudaEventCreate(&r.ev_t0));
     KS_CUDA(cudaEventCreate(&r.ev_t1));
+    for (auto& e : r.ev_coll) KS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     r.loaded.assign((size_t)r.m, 0);
     r.loaded_count = 0;
     KS_CUDA(cudaDeviceSynchronize());
@@ -176,6 +182,8 @@ void rank_free(Rank& r) {
     for (auto e : r.ev_poll) if (e) cudaEventDestroy(e);
     if (r.ev_t0) cudaEventDestroy(r.ev_t0);
     if (r.ev_t1) cudaEventDestroy(r.ev_t1);
+    for (auto e : r.ev_coll) if (e) cudaEventDestroy(e);
+    if (r.rs_stage) dev_free(r.rs_stage);
     for (auto e : r.ev_gemv) cudaEventDestroy(e);
     for (auto& g : r.graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
     r.ev_gemv.clear();
@@ -184,13 +192,95 @@ void rank_free(Rank& r) {
     r = Rank{};
 }
 
+void HostBarrier::reset(int parties) {
+    std::lock_guard<std::mutex> g(mu);
+    n = parties;
+    count = 0;
+    aborted = false;
+}
+
+void HostBarrier::wait() {
+    std::unique_lock<std::mutex> g(mu);
+    if (aborted) throw KsError(KS_ENCCL, "host collective: a peer rank failed");
+    const unsigned long long my = gen;
+    if (++count == n) {
+        count = 0;
+        ++gen;
+        cv.notify_all();
+        return;
+    }
+    cv.wait(g, [&] { return gen != my || aborted; });
+    if (gen == my) throw KsError(KS_ENCCL, "host collective: a peer rank failed");
+}
+
+void HostBarrier::abort() {
+    std::lock_guard<std::mutex> g(mu);
+    aborted = true;
+    cv.notify_all();
+}
+
+namespace {
+
+// Host-driven collective step of a shared-device context (one process, no NCCL):
+// every rank records `ev_coll[0]` after its producer, the worker threads meet, each
+// stream waits for every peer's producer and pulls what it needs with peer copies
+// (`pull`), records `ev_coll[1]`, the threads meet again and each stream waits for
+// every peer's pulls -- so no rank overwrites a region a peer is still reading.
+// Stream-ordered: no host synchronisation with the device.
+template <class F>
+void host_collective(const ks_ctx* c, Rank& r, F&& pull) {
+    KS_CUDA(cudaEventRecord(r.ev_coll[0], r.stream));
+    c->hbar->wait();
+    for (const Rank& h : c->ranks)
+        if (h.rank != r.rank) KS_CUDA(cudaStreamWaitEvent(r.stream, h.ev_coll[0], 0));
+    pull();
+    KS_CUDA(cudaEventRecord(r.ev_coll[1], r.stream));
+    c->hbar->wait();
+    for (const Rank& h : c->ranks)
+        if (h.rank != r.rank) KS_CUDA(cudaStreamWaitEvent(r.stream, h.ev_coll[1], 0));
+}
+
+}  // namespace
+
 // In-place allgather of one chunk per rank (count_per_rank doubles at G + rank*chunk).
+// G is one of the exchange regions (G_r, G_v, S) of this rank's exchange allocation.
 void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank) {
     if (c->P == 1) return;
     char* base = reinterpret_cast<char*>(G);
-    KS_NCCL(ncclAllGather(base + (size_t)r.rank * (size_t)count_per_rank * c->esz, base,
-                          (size_t)count_per_rank, c->dtype == KS_FLOAT32 ? ncclFloat : ncclDouble,
-                          r.comm, r.stream));
+    const size_t cb = (size_t)count_per_rank * c->esz;
+    if (!r.comm) {                      // ranks sharing a GPU: host-driven peer copies
+        const size_t off = (size_t)(base - reinterpret_cast<char*>(r.xbuf));
+        if (!c->shared_dev || off >= r.xbuf_bytes) throw KsError(KS_ESTATE, "allgather without a communicator");
+        host_collective(c, r, [&] {
+            for (const Rank& h : c->ranks) {
+                if (h.rank == r.rank) continue;
+                const char* src = reinterpret_cast<const char*>(h.xbuf) + off + (size_t)h.rank * cb;
+                KS_CUDA(cudaMemcpyAsync(base + (size_t)h.rank * cb, src, cb, cudaMemcpyDefault, r.stream));
+            }
+        });
+        return;
+    }
+    KS_NCCL(ncclAllGather(base + (size_t)r.rank * cb, base, (size_t)count_per_rank,
+                          c->dtype == KS_FLOAT32 ? ncclFloat : ncclDouble, r.comm, r.stream));
+}
+
+// Sum over ranks of every rank's slot `r.rank` of U (chunk layout) into r.qt_loc:
+// the reduce-scatter of K1T.  Shared-device contexts: peer copies of the P slots into
+// a staging buffer, then a rank-ordered sum (launch_sum_slots).
+static void reduce_scatter_u(const ks_ctx* c, Rank& r) {
+    const int64_t chunk = r.L.chunk;
+    if (r.comm) {
+        KS_NCCL(ncclReduceScatter(r.U, r.qt_loc, (size_t)chunk, ncclDouble, ncclSum, r.comm, r.stream));
+        return;
+    }
+    if (!c->shared_dev) throw KsError(KS_ESTATE, "reduce-scatter without a communicator");
+    if (!r.rs_stage) dev_alloc_t(&r.rs_stage, (size_t)c->P * (size_t)chunk);
+    host_collective(c, r, [&] {
+        for (const Rank& h : c->ranks)
+            KS_CUDA(cudaMemcpyAsync(r.rs_stage + (int64_t)h.rank * chunk, h.U + (int64_t)r.rank * chunk,
+                                    (size_t)chunk * sizeof(double), cudaMemcpyDefault, r.stream));
+    });
+    r.launches += launch_sum_slots(r.rs_stage, c->P, chunk, r.qt_loc, r.num_sms, r.stream);
 }
 
 // Copies the P row slices held in chunk layout to a contiguous n-vector.
@@ -216,6 +306,7 @@ VecArgsT<float> Rank::vargs_f32(bool fused) const {
     a.gpar = fused ? (int64_t)L.P * L.chunk : 0;
     a.spar = fused ? (int64_t)L.P * kScalSlot : 0;
     a.peer = fused ? 1 : 0;
+    a.jitter = jitter;
     for (int g = 0; g < kMaxRanks; ++g) {
         a.pp.G_r[g] = as<float>(pp.G_r[g]);
         a.pp.G_v[g] = as<float>(pp.G_v[g]);
@@ -371,7 +462,7 @@ const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done, l
     r.launches += launch_gemv_t(r.A, c->ld, r.m, c->n, x_loc, rc, r.upart, r.col_ticket, r.U, r.L, done,
                                 shape, r.stream);
     if (c->P == 1) return r.U;
-    KS_NCCL(ncclReduceScatter(r.U, r.qt_loc, (size_t)r.L.chunk, ncclDouble, ncclSum, r.comm, r.stream));
+    reduce_scatter_u(c, r);
     return r.qt_loc;
 }
 
@@ -397,6 +488,7 @@ void ks_ctx::for_each_rank(const std::function<void(ks::Rank&)>& fn) {
     std::vector<std::thread> th;
     std::exception_ptr first;
     std::mutex mu;
+    hbar->reset((int)ranks.size());
     for (auto& r : ranks) {
         th.emplace_back([&, rp = &r] {
             try {
@@ -404,8 +496,11 @@ void ks_ctx::for_each_rank(const std::function<void(ks::Rank&)>& fn) {
                 cudaGetLastError();
                 fn(*rp);
             } catch (...) {
-                std::lock_guard<std::mutex> g(mu);
-                if (!first) first = std::current_exception();
+                {
+                    std::lock_guard<std::mutex> g(mu);
+                    if (!first) first = std::current_exception();
+                }
+                hbar->abort();   // peers waiting in a host collective fail instead of blocking
             }
         });
     }

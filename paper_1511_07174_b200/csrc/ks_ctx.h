@@ -6,7 +6,10 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <functional>
+#include <memory>
+#include <mutex>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -35,8 +38,24 @@ int64_t guard_check(const std::vector<int>& devs);
 template <class T>
 inline void dev_alloc_t(T** p, size_t count) { *p = static_cast<T*>(dev_alloc(count * sizeof(T))); }
 
+// Rendezvous of the worker threads of one process (for_each_rank) for the host-driven
+// collectives of a context whose ranks share devices (no NCCL communicator: NCCL
+// rejects two ranks on one GPU).  abort() releases every waiter with an error when a
+// rank failed, so the others cannot block on it.
+struct HostBarrier {
+    std::mutex mu;
+    std::condition_variable cv;
+    int n = 0, count = 0;
+    unsigned long long gen = 0;
+    bool aborted = false;
+    void reset(int parties);
+    void wait();     // throws KsError(KS_ENCCL) after abort()
+    void abort();
+};
+
 struct Rank {
     int rank = 0, dev = 0, num_sms = 148;
+    int dev_share = 1;          // ranks of this context on the same GPU (its SMs are split)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     ncclComm_t comm = nullptr;
@@ -82,6 +101,7 @@ struct Rank {
     MultiPeer mpeer{};
     PeerPtrs pp{};
     bool peer_ok = false;       // every rank's exchange buffers are load/store reachable
+    unsigned jitter = 0;        // KS_OPT_JITTER seed (also in st->jitter)
     std::vector<void*> ipc_opened;
     unsigned long long epoch_next = 1;
     DevState* st = nullptr;
@@ -107,6 +127,8 @@ struct Rank {
     // events
     cudaEvent_t ev_poll[2]{};
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+    cudaEvent_t ev_coll[2]{};           // host-driven collectives (shared-device contexts)
+    double* rs_stage = nullptr;         // P * chunk: host-driven reduce-scatter staging
     std::vector<cudaEvent_t> ev_gemv;   // profiling pairs
 
     // CUDA-graph replay of one poll batch (KS_OPT_USE_GRAPHS)
@@ -145,6 +167,7 @@ struct Options {
     int64_t small = 2;        // 0 off, 1 on, 2 auto: small-n shared-memory kernels (P == 1)
     int64_t join_timeout_ms = 120000;   // fused P > 1: solve-start rendezvous bound
     int64_t tiny = 1;         // 1 auto, 0 off: register-resident kernels (P == 1, n <= 1024)
+    int64_t jitter = 0;       // race-detection delays at sync points (seed; 0 off)
 };
 
 }  // namespace ks
@@ -155,6 +178,10 @@ struct ks_ctx {
     size_t esz = sizeof(double);   // bytes per element of A and the device vectors
     int P = 1;               // global number of ranks
     bool multiprocess = false;
+    // some ranks share a GPU (ks_create_on with a repeated device): no NCCL
+    // communicator; the non-fused collectives are host-driven peer copies
+    bool shared_dev = false;
+    std::unique_ptr<ks::HostBarrier> hbar = std::make_unique<ks::HostBarrier>();
     std::vector<ks::Rank> ranks;   // local ranks (1 in multi-process mode)
     ks::Options opt;
     bool poisoned = false;

@@ -68,6 +68,26 @@ __device__ __forceinline__ bool grid_sum(T (&v)[K], T* part, unsigned* ticket, T
     return true;
 }
 
+// ---- race detection (KS_OPT_JITTER) -----------------------------------------
+// At a synchronisation point (grid-barrier arrival and departure, flag publish and
+// wait, LL store and poll) a pseudo-random quarter of the visits of each warp sleep
+// up to ~4 us, so the order in which CTAs, warps and ranks reach every hand-over
+// changes from run to run.  The kernels' results do not depend on that order (fixed
+// summation trees, epoch-tagged exchanges), so a run with jitter must equal a run
+// without it bit for bit; a missing barrier or fence shows up as a difference or a
+// hang-timeout instead (tests/test_gpu_race.py).  seed = 0: one predictable branch.
+__device__ __forceinline__ void jitter_at(unsigned seed, unsigned site) {
+    if (seed == 0u) return;
+    unsigned h = seed ^ (blockIdx.x * 0x9E3779B1u) ^ (site * 0x85EBCA77u) ^ ((threadIdx.x >> 5) * 0xC2B2AE3Du) ^
+                 (unsigned)clock64();
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    h *= 0x297A2D39u;
+    h ^= h >> 15;
+    if ((h & 3u) == 0u) __nanosleep(h >> 20);
+}
+
 // ---- fused NVLink collectives: epoch flags ---------------------------------
 __device__ __forceinline__ void flag_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

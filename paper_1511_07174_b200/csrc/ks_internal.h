@@ -62,6 +62,8 @@ struct DevState {
     unsigned long long ebase;  // epoch of iteration k is ebase + k (fused collectives)
     int done, status, converged, breakdown, half, bzero;
     int peer_timeout;          // a fused-collective wait timed out (error)
+    unsigned jitter;           // race-detection delays at sync points (KS_OPT_JITTER; 0 off)
+    unsigned jitter_pad;
 };
 
 // Scratch for deterministic last-block grid reductions.
@@ -160,6 +162,7 @@ struct VecArgsT {
     // iteration-parity double buffering of G_r / G_v / S (0 in NCCL mode)
     int64_t gpar, spar;
     int peer;              // 1: fused NVLink peer-store collectives
+    unsigned jitter;       // KS_OPT_JITTER seed (0: off), ks_device.cuh jitter_at
     PeerPtrsT<T> pp;
     unsigned long long* flags;   // own [kNumPhases][kMaxRanks]
     T* X;                  // own full-length x gather buffer (exchange allocation)
@@ -182,6 +185,8 @@ int launch_bs_xr(const VecArgs& a, const long long* kdev, long long i, cudaStrea
 int launch_bs_finish(const VecArgs& a, cudaStream_t st);
 int launch_true_res_final(const VecArgs& a, cudaStream_t st);
 int launch_pack_x(const VecArgs& a, cudaStream_t st);   // x_loc -> G_v own chunk
+// out = rank-ordered sum of the P slots S[g*chunk ..] (host-driven reduce-scatter)
+int launch_sum_slots(const double* S, int P, int64_t chunk, double* out, int num_sms, cudaStream_t st);
 // Solve-start rendezvous of the fused exchange (P > 1): releases `epoch` into
 // flag [kPhaseJ][rank] of every rank and waits (bounded by timeout_ms) until every
 // rank has released it -- i.e. every rank's stream has finished its previous solve

@@ -218,8 +218,10 @@ __device__ __forceinline__ bool rank_sum(const MultiArgs& M, double (&v)[NV], in
             for (int k = 0; k < NV; ++k) M.mp.MS[g][par * pst + (int64_t)me * row + q0 + k] = v[k];
         unsigned long long* f[kMaxRanks];
         for (int g = 0; g < P; ++g) f[g] = M.mp.flags[g] + ph * kMaxRanks + me;
+        jitter_at(*(volatile const unsigned*)&M.st->jitter, 5u);
         publish_flags(f, P, epoch);
     }
+    if (threadIdx.x == 0) jitter_at(*(volatile const unsigned*)&M.st->jitter, 3u);
     if (!wait_flags(M.flags + ph * kMaxRanks, P, epoch)) {
         if (threadIdx.x == 0) { M.st->peer_timeout = 1; M.st->status = KS_ENCCL; M.st->done = 1; }
         return false;

@@ -41,9 +41,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned 
 }
 __device__ bool grid_sync(unsigned* bar, DevState* st) {
     __shared__ int s_ok;
+    __shared__ unsigned s_jit;
     __syncthreads();
     if (threadIdx.x == 0) {
         int ok = 1;
+        const unsigned jit = *(volatile const unsigned*)&st->jitter;
+        jitter_at(jit, 1u);                       // arrival order (race detection; 0: off)
         unsigned long long* cnt = reinterpret_cast<unsigned long long*>(bar);
         __threadfence();
         const unsigned long long old = atomicAdd(cnt, 1ull);
@@ -61,8 +64,10 @@ __device__ bool grid_sync(unsigned* bar, DevState* st) {
             __threadfence();   // last arrival: acquire the other CTAs' writes
         }
         s_ok = ok;
+        s_jit = jit;
     }
     __syncthreads();
+    jitter_at(s_jit, 2u);                         // departure order of the warps
     return s_ok != 0;
 }
 
@@ -82,6 +87,7 @@ __device__ __forceinline__ void grid_total(const T* bpart, int q0, T (&out)[K], 
 // Fused-mode wait for phase ph of iteration k from every rank (all CTAs).
 template <class T>
 __device__ __forceinline__ bool wait_ph(const VecArgsT<T>& a, int ph, long long k) {
+    if (threadIdx.x == 0) jitter_at(a.jitter, 3u);
     const bool ok = wait_flags(a.flags + ph * kMaxRanks, a.L.P, epoch_of(a.st, k));
     if (!ok && threadIdx.x == 0) { a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1; }
     return ok;
@@ -90,6 +96,7 @@ template <class T>
 __device__ __forceinline__ void flags_out(const VecArgsT<T>& a, int ph, long long k) {
     unsigned long long* f[kMaxRanks];
     for (int g = 0; g < a.L.P; ++g) f[g] = a.pp.flags[g] + ph * kMaxRanks + a.L.rank;
+    jitter_at(a.jitter, 4u);
     publish_flags(f, a.L.P, epoch_of(a.st, k));
 }
 

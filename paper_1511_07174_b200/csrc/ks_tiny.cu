@@ -401,7 +401,9 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
         double q[V];
         bool got;
         if (XM == 0) {
+            jitter_at(T.a.jitter, 6u);
             if (threadIdx.x < R) ll_publish(T, (int64_t)(k & 1) * 2 * T.lda, row0 + rb + threadIdx.x, qrow, flag);
+            jitter_at(T.a.jitter, 7u);
             got = ll_gather<V>(slot, n, flag, q, T.backoff, wide);
         } else {
             fx_put(slot, T.lda, rb, R, qrow, flag);
@@ -508,7 +510,9 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         double vrow = gemv_rows<V>(Ar, R, p, wred);
         bool got;
         if (XM == 0) {
+            jitter_at(T.a.jitter, 6u);
             if (threadIdx.x < R) ll_publish(T, 0, row0 + rb + threadIdx.x, vrow, fv);
+            jitter_at(T.a.jitter, 7u);
             got = ll_gather<V>(T.ll, n, fv, v_, T.backoff, wide);
         } else {
             fx_put(T.ll, T.lda, rb, R, vrow, fv);
@@ -551,7 +555,9 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
         uint64_t* slot1 = T.ll + 2 * T.lda;
         double t[V];
         if (XM == 0) {
+            jitter_at(T.a.jitter, 6u);
             if (threadIdx.x < R) ll_publish(T, 2 * T.lda, row0 + rb + threadIdx.x, trow, ft);
+            jitter_at(T.a.jitter, 7u);
             got = ll_gather<V>(slot1, n, ft, t, T.backoff, wide);
         } else {
             fx_put(slot1, T.lda, rb, R, trow, ft);

@@ -749,6 +749,19 @@ int launch_true_res_final(const VecArgs& a, cudaStream_t st) {
     k_true_res_final<<<1, 32, 0, st>>>(a);
     return 1;
 }
+// out[i] = sum over g = 0..P-1 (in rank order) of S[g * chunk + i]: the reduction
+// half of a host-driven reduce-scatter (shared-device contexts, ks_ctx.cpp).
+__global__ void k_sum_slots(const double* __restrict__ S, int P, int64_t chunk, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < chunk; i += (int64_t)gridDim.x * kNT) {
+        double s = S[i];
+        for (int g = 1; g < P; ++g) s += S[(int64_t)g * chunk + i];
+        out[i] = s;
+    }
+}
+int launch_sum_slots(const double* S, int P, int64_t chunk, double* out, int num_sms, cudaStream_t st) {
+    k_sum_slots<<<grid_for(chunk, num_sms), kNT, 0, st>>>(S, P, chunk, out);
+    return 1;
+}
 int launch_pack_x(const VecArgs& a, cudaStream_t st) {
     k_pack_x<<<grid_for(mloc_h(a.L), a.num_sms), kNT, 0, st>>>(a);
     return 1;

@@ -1,0 +1,40 @@
+"""Rank layouts of the P > 1 GPU tests.
+
+("gpus", P): P ranks on GPUs 0..P-1 (ks_create); skipped on a box with fewer GPUs.
+("shared", P): P ranks all on GPU 0 (ks_create_on with a repeated device): the same
+P > 1 schedules -- fused load/store exchange, rendezvous, x gather, host-driven
+collectives in place of NCCL -- with each rank's persistent grids on 148/P SMs.  It
+runs on any GPU box, so the P > 1 paths are checked even where only one GPU exists.
+"""
+import pytest
+
+PS_GPUS = (2, 4, 8)
+PS_SHARED = (2, 4)
+
+
+def ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+def layouts(gpus=PS_GPUS, shared=PS_SHARED):
+    return ([pytest.param(("gpus", P), id=f"gpus{P}") for P in gpus] +
+            [pytest.param(("shared", P), id=f"shared{P}") for P in shared])
+
+
+def need(lay):
+    """Skips when the box cannot host the layout; returns P."""
+    mode, P = lay
+    if ngpu() < 1:
+        pytest.skip("needs a GPU")
+    if mode == "gpus" and ngpu() < P:
+        pytest.skip(f"needs {P} GPUs")
+    return P
+
+
+def context(n, lay, **kw):
+    import paper_1511_07174_b200 as ks
+    mode, P = lay
+    if mode == "gpus":
+        return ks.Context(n, ngpus=P, **kw)
+    return ks.Context(n, devices=[0] * P, **kw)

@@ -55,6 +55,13 @@ def test_version_and_errors_without_gpu():
     assert st == ks.KS_EARG
     st = ks.lib().ks_create_rank(C.byref(h), 16, 0, 2, 2, None, 0, None)
     assert st == ks.KS_EARG
+    st = ks.lib().ks_create_on(C.byref(h), 16, 0, 2, None)
+    assert st == ks.KS_EARG
+    devs = (C.c_int32 * 2)(0, 0)
+    st = ks.lib().ks_create_on(C.byref(h), 16, 0, 2, devs)     # no device 0 here
+    assert st == ks.KS_EARG and b"not a device" in ks.lib().ks_last_error(None)
+    st = ks.lib().ks_create_on(C.byref(h), 16, 0, 17, devs)
+    assert st == ks.KS_EARG
     assert ks.lib().ks_destroy(None) == ks.KS_OK
 
 

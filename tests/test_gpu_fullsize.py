@@ -26,6 +26,7 @@ from test_gpu_parity import FLOOR_BS, bars, gamma  # noqa: E402
 
 N = 65536
 THREADS = os.cpu_count() or 1
+from layouts import context, layouts, need  # noqa: E402
 
 
 def _mem_available() -> int:
@@ -129,17 +130,16 @@ def test_fullsize_bicgstab_true_residual_and_first_iterations():
     bars(x2, h2, r2, xo, ho, ro, iters_tol=0, floor=FLOOR_BS)
 
 
-@pytest.mark.parametrize("P", [1, 2, 4, 8])
-def test_c3_bicgstab_full_history_and_x_vs_oracle(P, c3_oracle):
+@pytest.mark.parametrize("lay", [pytest.param(("gpus", 1), id="gpus1")] + layouts(shared=(2,)))
+def test_c3_bicgstab_full_history_and_x_vs_oracle(lay, c3_oracle):
     """C3 gate, north-star bars on the whole run at the headline size, in the
     bench's launch configuration (persistent kernels, fused exchange for P > 1):
     every history entry (Q17 floor), x within 1e-9 of the oracle's x, iteration
     count within 2 (expected: equal), same exit kind."""
-    if _ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     b, xo, ho, ro, mode = c3_oracle
     assert ro.converged and ro.iterations == 23 and not ro.half_step_exit, (ro, mode)
-    with ks.Context(N, ngpus=P) as ctx:
+    with context(N, lay) as ctx:
         bg = ctx.generate("dd", seed=synth.SEED, kd=16)
         assert np.array_equal(bg, b)                               # P12
         x, h, r = ctx.bicgstab(bg, tol=1e-10)

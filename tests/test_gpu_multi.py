@@ -18,6 +18,7 @@ ks = pytest.importorskip("paper_1511_07174_b200")
 torch = pytest.importorskip("torch")
 
 from test_gpu_parity import FLOOR_BS, bars, gemv_bound_check  # noqa: E402
+from layouts import context, layouts, need  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -33,16 +34,14 @@ needs2 = pytest.mark.skipif("ngpu() < 2", reason="needs >= 2 GPUs (gpurun --gpus
 PS = [2, 4, 8]
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
-def test_multi_gemv_and_cg(P):
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+@pytest.mark.parametrize("lay", layouts())
+def test_multi_gemv_and_cg(lay):
+    P = need(lay)
     n = 2050   # uneven partition: first n mod P shards get one more row
     rng = np.random.default_rng(P)
     A = rng.standard_normal((n, n))
     x = rng.standard_normal(n)
-    with ks.Context(n, ngpus=P) as ctx:
+    with context(n, lay) as ctx:
         assert ctx.nranks == P and ctx.local_gpus == P
         assert [ctx.row_range(g) for g in range(P)] == ks.partition(n, P)
         ctx.load_rows(A[:1000])
@@ -52,7 +51,7 @@ def test_multi_gemv_and_cg(P):
     n = 2048
     As, c, b = synth.gspd(n, 1e4)
     xo, ho, ro = oracle.cg(As, b, tol=1e-10)
-    with ks.Context(n, ngpus=P) as ctx:
+    with context(n, lay) as ctx:
         ctx.generate("spd", seed=synth.SEED, table=c)
         xg, hg, rg = ctx.cg(b, tol=1e-10)
     bars(xg, hg, rg, xo, ho, ro)
@@ -62,15 +61,13 @@ def test_multi_gemv_and_cg(P):
     assert r1.iterations == rg.iterations
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
+@pytest.mark.parametrize("lay", layouts())
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_multi_small_cg_allgather_only(P, dtype):
+def test_multi_small_cg_allgather_only(lay, dtype):
     """Small-n CG over P GPUs (k_cg_small_peer: one exchange of q slices and one grid
     barrier per iteration, all O(n) work redundant in shared memory) vs the oracle
     and vs the general fused kernels (small = 0): ragged n, x0, maxit, multi-launch."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     from test_gpu_parity import bars_f32
     for n in (1002, 4096):
         A, c, b = synth.gspd(n, 1e3)
@@ -80,7 +77,7 @@ def test_multi_small_cg_allgather_only(P, dtype):
             xo, ho, ro = oracle.cg(A, b, tol=1e-10)
         outs = []
         for small in (1, 0):
-            with ks.Context(n, ngpus=P, dtype=dtype) as ctx:
+            with context(n, lay, dtype=dtype) as ctx:
                 ctx.set_option("small", small)
                 ctx.set_option("tiny", 0)     # the small-n kernels themselves (tiny: test_gpu_tiny.py)
                 ctx.generate("spd", seed=synth.SEED, table=c, want_b=False)
@@ -103,16 +100,14 @@ def test_multi_small_cg_allgather_only(P, dtype):
         assert abs(outs[0] - outs[1]) <= 2
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
+@pytest.mark.parametrize("lay", layouts())
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_multi_small_bicgstab_allgather_only(P, dtype):
+def test_multi_small_bicgstab_allgather_only(lay, dtype):
     """Small-n BiCGSTAB over P GPUs (k_bs_small_peer: v and t slices are the only
     exchanges, two grid barriers per iteration) vs the oracle and the general fused
     kernels: ragged n, half-step exit, maxit (in-kernel final test), x0, and a
     multi-launch solve (rhat and r handed over between launches)."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     from test_gpu_parity import bars_f32
     for n, kd in ((1003, 4), (4096, 16)):
         A, b = synth.gdd(n, kd)
@@ -122,7 +117,7 @@ def test_multi_small_bicgstab_allgather_only(P, dtype):
             xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
         its = []
         for small in (1, 0):
-            with ks.Context(n, ngpus=P, dtype=dtype) as ctx:
+            with context(n, lay, dtype=dtype) as ctx:
                 ctx.set_option("small", small)
                 ctx.set_option("tiny", 0)     # the small-n kernels themselves (tiny: test_gpu_tiny.py)
                 ctx.load_rows(A)
@@ -145,33 +140,29 @@ def test_multi_small_bicgstab_allgather_only(P, dtype):
         assert abs(its[0] - its[1]) <= 2
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
-def test_multi_bicgstab(P):
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+@pytest.mark.parametrize("lay", layouts())
+def test_multi_bicgstab(lay):
+    P = need(lay)
     for n, kd in [(1024, 4), (4096, 16), (1001, 4)]:
         A, b = synth.gdd(n, kd)
         xo, ho, ro = oracle.bicgstab(A, b, tol=1e-10)
-        with ks.Context(n, ngpus=P) as ctx:
+        with context(n, lay) as ctx:
             ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
             x, h, r = ctx.bicgstab(b, tol=1e-10)
         bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
         assert r.half_step_exit == ro.half_step_exit
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
-def test_fused_collectives_bitwise_equal_nccl(P):
+@pytest.mark.parametrize("lay", layouts())
+def test_fused_collectives_bitwise_equal_nccl(lay):
     """NEXT-1: the fused NVLink peer-store collectives carry the same partials and
     sum them in the same rank order as the NCCL allgathers, so x, the history and
     the iteration count must be bitwise identical in both modes (and with graphs)."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     n = 4100
     D, bd = synth.gdd(n, 16)
     Cs, cs, bs = synth.gspd(4096, 1e4)
-    with ks.Context(n, ngpus=P) as ctx, ks.Context(4096, ngpus=P) as cc:
+    with context(n, lay) as ctx, context(4096, lay) as cc:
         ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
         cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
         assert ctx.get_option("fused_comm") == 1, "peer access expected on NVSwitch B200s"
@@ -196,16 +187,14 @@ def test_fused_collectives_bitwise_equal_nccl(P):
     bars(x, h, r, xo, ho, ro)
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
-def test_multi_persistent_fused(P):
+@pytest.mark.parametrize("lay", layouts())
+def test_multi_persistent_fused(lay):
     """NEXT-1 + NEXT-2 together: persistent cooperative kernels on every GPU with
     the fused NVLink exchange; bars vs the oracle; identical on repeat."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     D, bd = synth.gdd(4096, 16)
     Cs, cs, bs = synth.gspd(4096, 1e4)
-    with ks.Context(4096, ngpus=P) as ctx, ks.Context(4096, ngpus=P) as cc:
+    with context(4096, lay) as ctx, context(4096, lay) as cc:
         ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
         cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
         for cx in (ctx, cc):
@@ -221,19 +210,17 @@ def test_multi_persistent_fused(P):
     bars(xc, hc, rc, xo, ho, ro)
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
+@pytest.mark.parametrize("lay", layouts())
 @pytest.mark.parametrize("fused", [1, 0])
-def test_multi_bicg(P, fused):
+def test_multi_bicg(lay, fused):
     """NEXT-3 BiCG at P GPUs: K1T partials reduce-scattered either inside K1T over
     NVLink peer stores (fused = 1, default) or by ncclReduceScatter (fused = 0);
     x0 and maxit included."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     for n, kd in [(1024, 4), (4099, 16)]:
         A, b = synth.gdd(n, kd)
         xo, ho, ro = oracle.bicg(A, b, tol=1e-10)
-        with ks.Context(n, ngpus=P) as ctx:
+        with context(n, lay) as ctx:
             ctx.set_option("fused_comm", fused)
             assert ctx.get_option("fused_comm") == fused
             ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
@@ -249,21 +236,19 @@ def test_multi_bicg(P, fused):
         gemv_bound_check(np.ascontiguousarray(A.T), xt, yt)
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
+@pytest.mark.parametrize("lay", layouts())
 @pytest.mark.parametrize("persistent", [0, 1])
-def test_multi_gmres(P, persistent):
+def test_multi_gmres(lay, persistent):
     """NEXT-3 GMRES(m) at P GPUs: multi-kernel path with NCCL exchanges of the CGS2
     partial dots (persistent = 0), or one persistent kernel per restart cycle with
     the exchanges fused over NVLink (persistent = 1); x0, maxit and a restart
     length that does not divide maxit included."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     for n, kd, m in [(1024, 16, 30), (4099, 16, 8), (2050, 4, 3)]:
         A, b = synth.gdd(n, kd)
         x0 = np.random.default_rng(n).standard_normal(n) if n == 2050 else None
         xo, ho, ro = oracle.gmres(A, b, x0=x0, tol=1e-10, restart=m)
-        with ks.Context(n, ngpus=P) as ctx:
+        with context(n, lay) as ctx:
             ctx.set_option("persistent", persistent)
             ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
             assert ctx.get_option("persistent") == persistent and ctx.get_option("fused_comm") == 1
@@ -275,19 +260,17 @@ def test_multi_gmres(P, persistent):
             bars(x7, h7, r7, xo7, ho7, ro7, iters_tol=0)
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
-def test_multi_f32(P):
+@pytest.mark.parametrize("lay", layouts())
+def test_multi_f32(lay):
     """NEXT-4 at P GPUs: FP32 persistent kernels with the fused NVLink exchange."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     from test_gpu_parity import bars_f32
     n = 4096
     A, b = synth.gdd(n, 16)
     xo, ho, ro = oracle.bicgstab_f32(A, b, tol=1e-5)
     Cs, cs, bs = synth.gspd(n, 1e2)
     xc, hc, rc = oracle.cg_f32(Cs, bs, tol=1e-5)
-    with ks.Context(n, ngpus=P, dtype="f32") as ctx, ks.Context(n, ngpus=P, dtype="f32") as cc:
+    with context(n, lay, dtype="f32") as ctx, context(n, lay, dtype="f32") as cc:
         ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
         cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
         x, h, r = ctx.bicgstab(b.astype(np.float32).astype(np.float64), tol=1e-5)
@@ -296,11 +279,12 @@ def test_multi_f32(P):
     bars_f32(x2, h2, r2, xc, hc, rc)
 
 
-@needs2
-def test_multi_edge_cases():
+@pytest.mark.parametrize("lay", layouts(gpus=(2,), shared=(2,)))
+def test_multi_edge_cases(lay):
+    need(lay)
     n = 64
     A = synth.random_spd(n, 10.0, 1)
-    with ks.Context(n, ngpus=2) as ctx:
+    with context(n, lay) as ctx:
         ctx.load_rows(A)
         x, h, r = ctx.cg(np.zeros(n), tol=1e-10)
         assert r.iterations == 0 and np.all(x == 0)
@@ -313,15 +297,16 @@ def test_multi_edge_cases():
         bars(x, h, r, xo, ho, ro)
 
 
-@needs2
-def test_partial_load_is_an_error_on_every_rank():
+@pytest.mark.parametrize("lay", layouts(gpus=(2,), shared=(2,)))
+def test_partial_load_is_an_error_on_every_rank(lay):
     """Single process driving 2 GPUs with only the first shard loaded: every call
     that runs a collective schedule returns KS_ESTATE up front (no rank enters a
     fused exchange its peer never joins), and the context stays usable."""
+    need(lay)
     n = 512
     A = synth.random_spd(n, 10.0, 3)
     b = np.random.default_rng(3).standard_normal(n)
-    with ks.Context(n, ngpus=2) as ctx:
+    with context(n, lay) as ctx:
         r0, r1 = ctx.row_range(0)
         ctx.load_rows(A[r0:r1], r0)
         for call in (lambda: ctx.cg(b), lambda: ctx.bicgstab(b), lambda: ctx.bicg(b),
@@ -417,25 +402,23 @@ def test_torchrun_borrowed_comm(tmp_path, P):
     bars(np.array(R["x"]), np.array(R["h"]), Rep, xo, ho, ro, floor=FLOOR_BS)
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
-def test_multi_fullsize_65536(P):
+@pytest.mark.parametrize("lay", layouts(shared=(2,)))
+def test_multi_fullsize_65536(lay):
     """C3/C3' at P GPUs, default path (persistent + fused): CG vs the closed form
     and the survey's counts; BiCGSTAB counts/histories and the true residual by the
     oracle with on-the-fly rows (pins P6, P11, P14 at scale).  The C3 history/x gate
     vs the oracle's full solve at every P is test_gpu_fullsize.py's."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     n = 65536
     c = synth.spd_table(n, 1e4)
-    with ks.Context(n, ngpus=P) as ctx:
+    with context(n, lay) as ctx:
         b = ctx.generate("spd", seed=synth.SEED, table=c)
         x, h, r = ctx.cg(b, tol=1e-10)
     assert r.converged and abs(r.iterations - 840) <= 2
     assert np.allclose(h[:3], [0.5745285, 0.4442545, 0.3710058], rtol=5e-7, atol=0)
     xcf = oracle.spd_exact_solve_ld(c, synth.SEED, b)
     assert np.linalg.norm(x - xcf) <= 1e4 * 1e-10 * np.linalg.norm(xcf)
-    with ks.Context(n, ngpus=P) as ctx:
+    with context(n, lay) as ctx:
         b = ctx.generate("dd", seed=synth.SEED, kd=16)
         x, h, r = ctx.bicgstab(b, tol=1e-10)
     assert r.converged and abs(r.iterations - 23) <= 2
@@ -444,18 +427,16 @@ def test_multi_fullsize_65536(P):
     assert oracle.true_relres_ld(op, b, x) <= 10 * 1e-10
 
 
-@needs2
-@pytest.mark.parametrize("P", PS)
-def test_c4_131072_multi(P):
+@pytest.mark.parametrize("lay", layouts(shared=(2,)))
+def test_c4_131072_multi(lay):
     """C4 (n = 131072, 137 GB in total) strong-scaled over P GPUs: CG to tol 1e-10
     vs the closed form (P6), the survey count 979 (P14), the same count as one GPU
     would take (P13: survey App. A.8), and sampled true-residual rows by the oracle
     (P11, on-the-fly rows)."""
-    if ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     n = 131072
     c = synth.spd_table(n, 1e4)
-    with ks.Context(n, ngpus=P) as ctx:
+    with context(n, lay) as ctx:
         b = ctx.generate("spd", seed=synth.SEED, table=c)
         x, h, r = ctx.cg(b, tol=1e-10)
     assert r.converged and abs(r.iterations - 979) <= 2, r

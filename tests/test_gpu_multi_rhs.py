@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 ks = pytest.importorskip("paper_1511_07174_b200")
 
 from test_gpu_parity import bars  # noqa: E402
+from layouts import context, layouts, need  # noqa: E402
 
 
 def gspd_any(n, kappa=1e3):
@@ -120,21 +121,20 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_multi_rhs_over_p_gpus(P):
+@pytest.mark.parametrize("lay", layouts())
+def test_multi_rhs_over_p_gpus(lay):
     """Multi-RHS CG over P GPUs (row blocks; per iteration the K columns' sigma and
     rho' partials are all-reduced and the r slices gathered through the fused NVLink
     exchange inside the persistent kernel; x gathered in-kernel): per-column bars vs
     the oracle on a ragged n, with x0 and a b = 0 column; bitwise equal to a repeat."""
-    if _ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     n = 2050
     A = gspd_any(n)
     B = rhs_block(n, 6)
     B[:, 3] = 0.0
     X0 = np.random.default_rng(P).standard_normal((n, 6))
     Xo, ho, ro = oracle.cg_multi(A, B, X0=X0, tol=1e-10)
-    with ks.Context(n, ngpus=P) as ctx:
+    with context(n, lay) as ctx:
         assert ctx.get_option("fused_comm") == 1
         ctx.load_rows(A)
         X, h, r = ctx.cg_multi(B, X0=X0, tol=1e-10)
@@ -216,21 +216,20 @@ def test_bicgstab_multi_exits_and_repeat():
     bars(X[:, 0], h[0], r[0], Xo[:, 0], ho[0], ro[0], floor=FLOOR_BS)
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_bicgstab_multi_over_p_gpus(P):
+@pytest.mark.parametrize("lay", layouts())
+def test_bicgstab_multi_over_p_gpus(lay):
     """Multi-RHS BiCGSTAB over P GPUs: v and r slices through every rank's exchange
     regions, the per-column dots as rank all-reduces; per-column bars vs the oracle
     (half-step exits, a b = 0 column, small x0), bitwise repeat, and the one-GPU
     result within the bars."""
-    if _ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     from test_gpu_parity import FLOOR_BS
     n = 2050
     D, B = gdd_block(n, 5)
     B[:, 3] = 0.0
     X0 = 1e-3 * np.random.default_rng(P).standard_normal((n, 5))
     Xo, ho, ro = oracle.bicgstab_multi(D, B, X0=X0, tol=1e-10)
-    with ks.Context(n, ngpus=P) as ctx:
+    with context(n, lay) as ctx:
         ctx.load_rows(D)
         X, h, r = ctx.bicgstab_multi(B, X0=X0, tol=1e-10)
         for k in (0, 1, 2, 4):

@@ -16,6 +16,7 @@ pytestmark = pytest.mark.gpu
 ks = pytest.importorskip("paper_1511_07174_b200")
 
 from test_gpu_parity import FLOOR_BS, bars  # noqa: E402
+from layouts import context, layouts, need  # noqa: E402
 
 
 def gspd_any(n):
@@ -176,14 +177,13 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_tiny_over_p_gpus(P):
+@pytest.mark.parametrize("lay", layouts())
+def test_tiny_over_p_gpus(lay):
     """Tiny kernels over P GPUs (fused exchange): every rank's CTAs own its rows, the
     LL words of the GEMV output go over NVLink into every rank's buffer, x, r, p are
     replicated in every CTA of every rank.  CG and BiCGSTAB vs the oracle (x0 too),
     tiny on vs off, and a repeated solve bitwise equal."""
-    if _ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     for n in (300, 1024):
         A, b = gspd_any(n)
         D, bd = synth.gdd(n, 4)      # kd = 4: the parity-safe G-DD of the ragged tests
@@ -192,7 +192,7 @@ def test_tiny_over_p_gpus(P):
         yo, hyo, ryo = oracle.bicgstab(D, bd, tol=1e-10)
         res = {}
         for tiny in (1, 0):
-            with ks.Context(n, ngpus=P) as ctx, ks.Context(n, ngpus=P) as dtx:
+            with context(n, lay) as ctx, context(n, lay) as dtx:
                 ctx.set_option("tiny", tiny)
                 dtx.set_option("tiny", tiny)
                 ctx.load_rows(A)
@@ -208,19 +208,19 @@ def test_tiny_over_p_gpus(P):
         assert not (np.array_equal(res[1][0], res[0][0]) and np.array_equal(res[1][1], res[0][1]))
 
 
-@pytest.mark.parametrize("P", [2, 4])
-def test_tiny_bitwise_independent_of_p(P):
+@pytest.mark.parametrize("lay", layouts(gpus=(2, 4), shared=(2, 4)))
+def test_tiny_bitwise_independent_of_p(lay):
     """Each GEMV row is summed in the same order whichever CTA of whichever rank owns
     it, and every full-length dot runs in the same thread layout in every CTA, so the
     tiny kernels' x and history on P GPUs equal the one-GPU results bit for bit."""
-    if _ngpu() < P:
-        pytest.skip(f"needs {P} GPUs")
+    P = need(lay)
     n = 1000
     A, b = gspd_any(n)
     D, bd = synth.gdd(n, 4)
     out = {}
     for q in (1, P):
-        with ks.Context(n, ngpus=q) as ctx, ks.Context(n, ngpus=q) as dtx:
+        lq = ("gpus", 1) if q == 1 else lay
+        with context(n, lq) as ctx, context(n, lq) as dtx:
             ctx.load_rows(A)
             dtx.load_rows(D)
             out[q] = (ctx.cg(b, tol=1e-10), dtx.bicgstab(bd, tol=1e-10))
