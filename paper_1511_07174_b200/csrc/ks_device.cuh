@@ -76,8 +76,7 @@ __device__ __forceinline__ bool grid_sum(T (&v)[K], T* part, unsigned* ticket, T
 // summation trees, epoch-tagged exchanges), so a run with jitter must equal a run
 // without it bit for bit; a missing barrier or fence shows up as a difference or a
 // hang-timeout instead (tests/test_gpu_race.py).  seed = 0: one predictable branch.
-__device__ __forceinline__ void jitter_at(unsigned seed, unsigned site) {
-    if (seed == 0u) return;
+static __device__ __noinline__ void jitter_sleep(unsigned seed, unsigned site) {
     unsigned h = seed ^ (blockIdx.x * 0x9E3779B1u) ^ (site * 0x85EBCA77u) ^ ((threadIdx.x >> 5) * 0xC2B2AE3Du) ^
                  (unsigned)clock64();
     h ^= h >> 15;
@@ -86,6 +85,10 @@ __device__ __forceinline__ void jitter_at(unsigned seed, unsigned site) {
     h *= 0x297A2D39u;
     h ^= h >> 15;
     if ((h & 3u) == 0u) __nanosleep(h >> 20);
+}
+// out of line: the hot kernels only pay a predictable branch (no registers held for it)
+__device__ __forceinline__ void jitter_at(unsigned seed, unsigned site) {
+    if (__builtin_expect(seed != 0u, 0)) jitter_sleep(seed, site);
 }
 
 // ---- fused NVLink collectives: epoch flags ---------------------------------
