@@ -636,6 +636,10 @@ int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t m, int64_t ld) {
     if (n < 1 || n > 1024 || ld > 1024 || m < 1) return 0;
     const int V = ld <= 512 ? 2 : 4;
     int g = num_sms;
+    if (const char* tg = std::getenv("KS_TINY_GRID")) {     // tuning: fewer CTAs (fewer LL pollers)
+        const int v = std::atoi(tg);
+        if (v >= 1 && v < g) g = v;
+    }
     if (g > m) g = (int)m;
     const int64_t rmax = (m + g - 1) / g;
     if (rmax > kRM) return 0;

@@ -12,3 +12,4 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?";
 CMD="python bench.py --steps 16 --warmup 3 --no-cpu-baseline --no-extras"
 timeout 300 $CMD > $O/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+timeout 600 python tools/tiny_grid_ab.py > $O/tiny_grid_ab.jsonl 2> $O/tiny_grid_ab.err; echo "tiny grid rc=$?"; cat $O/tiny_grid_ab.jsonl
