@@ -2,6 +2,7 @@
 #include "ks_ctx.h"
 
 #include <algorithm>
+#include <chrono>
 #include <exception>
 #include <mutex>
 #include <thread>
@@ -209,7 +210,12 @@ void HostBarrier::wait() {
         cv.notify_all();
         return;
     }
-    cv.wait(g, [&] { return gen != my || aborted; });
+    // bounded: a rank that never arrives (a bug) fails the call instead of hanging it
+    if (!cv.wait_for(g, std::chrono::seconds(120), [&] { return gen != my || aborted; })) {
+        aborted = true;
+        cv.notify_all();
+        throw KsError(KS_ENCCL, "host collective: timed out waiting for the peer ranks");
+    }
     if (gen == my) throw KsError(KS_ENCCL, "host collective: a peer rank failed");
 }
 
