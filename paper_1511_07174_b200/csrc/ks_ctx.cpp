@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <exception>
 #include <mutex>
 #include <thread>
@@ -69,7 +70,11 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     // ranks sharing a GPU split its SMs: every persistent grid of a rank is sized from
     // num_sms, so the co-running ranks' grids stay co-resident (their in-kernel waits
     // on each other need that)
-    r.num_sms = std::max(1, r.num_sms / std::max(1, r.dev_share));
+    if (r.dev_share > 1) {
+        int slack = 0;                               // tuning: SMs held back from the split
+        if (const char* e = std::getenv("KS_SHARED_SLACK")) slack = std::max(0, std::atoi(e));
+        r.num_sms = std::max(1, (r.num_sms - slack) / r.dev_share);
+    }
     if (!r.stream) {
         KS_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
         r.own_stream = true;
@@ -255,12 +260,20 @@ void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank) {
     char* base = reinterpret_cast<char*>(G);
     const size_t cb = (size_t)count_per_rank * c->esz;
     if (!r.comm) {                      // ranks sharing a GPU: host-driven peer copies
-        const size_t off = (size_t)(base - reinterpret_cast<char*>(r.xbuf));
-        if (!c->shared_dev || off >= r.xbuf_bytes) throw KsError(KS_ESTATE, "allgather without a communicator");
+        if (!c->shared_dev) throw KsError(KS_ESTATE, "allgather without a communicator");
+        // G lies in this rank's exchange allocation or its GMRES partials; the peer's
+        // copy of the region sits at the same offset of the peer's allocation
+        const char* xb = reinterpret_cast<const char*>(r.xbuf);
+        const char* hb = reinterpret_cast<const char*>(r.gm_hx);
+        const bool in_x = base >= xb && base < xb + r.xbuf_bytes;
+        const bool in_h = hb && base >= hb && base < hb + (size_t)c->P * kMaxBasis * sizeof(double);
+        if (!in_x && !in_h) throw KsError(KS_ESTATE, "allgather: buffer outside the exchange regions");
+        const size_t off = (size_t)(base - (in_x ? xb : hb));
         host_collective(c, r, [&] {
             for (const Rank& h : c->ranks) {
                 if (h.rank == r.rank) continue;
-                const char* src = reinterpret_cast<const char*>(h.xbuf) + off + (size_t)h.rank * cb;
+                const char* src = reinterpret_cast<const char*>(in_x ? (const void*)h.xbuf : (const void*)h.gm_hx) +
+                                  off + (size_t)h.rank * cb;
                 KS_CUDA(cudaMemcpyAsync(base + (size_t)h.rank * cb, src, cb, cudaMemcpyDefault, r.stream));
             }
         });

@@ -13,6 +13,12 @@ sys.path.insert(0, %r + "/tests")
 import numpy as np
 import paper_1511_07174_b200 as ks, synth, oracle
 case, P = sys.argv[1], int(sys.argv[2])
+_Ctx = ks.Context
+class _C(_Ctx):
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.set_option("join_timeout_ms", 15000)
+ks.Context = _C
 out = {"case": case, "P": P}
 t0 = time.time()
 try:
@@ -73,9 +79,9 @@ cases = sys.argv[1:] or ["bs1024:2", "bs1024:4", "x064:2", "x01000:2", "gm1024:2
 for cs in cases:
     case, P = cs.split(":")
     try:
-        r = subprocess.run([sys.executable, "-c", CHILD, case, P], capture_output=True, text=True, timeout=240)
+        r = subprocess.run([sys.executable, "-c", CHILD, case, P], capture_output=True, text=True, timeout=150)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else json.dumps(
             {"case": case, "P": int(P), "rc": r.returncode, "stderr": r.stderr[-600:]})
     except subprocess.TimeoutExpired:
-        line = json.dumps({"case": case, "P": int(P), "timeout": 240})
+        line = json.dumps({"case": case, "P": int(P), "timeout": 150})
     print(line, flush=True)
