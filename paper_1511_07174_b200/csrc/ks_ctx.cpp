@@ -166,9 +166,22 @@ void rank_alloc(ks_ctx* c, Rank& r) {
     KS_CUDA(cudaDeviceSynchronize());
 }
 
+// Buffers replaced while a call runs are freed at the start of the next call (or at
+// destroy), never inside it: cudaFree synchronises the whole device, and on a GPU
+// shared by several ranks of one context that would wait on a peer's kernel that
+// spins for this rank's not-yet-launched work.
+void retire(Rank& r, void* p) {
+    if (p) r.retired.push_back(p);
+}
+void flush_retired(Rank& r) {
+    for (void* p : r.retired) dev_free(p);
+    r.retired.clear();
+}
+
 void rank_free(Rank& r) {
     if (cudaSetDevice(r.dev) != cudaSuccess) return;
     cudaDeviceSynchronize();
+    flush_retired(r);
     for (void* p : r.ipc_opened) cudaIpcCloseMemHandle(p);
     r.ipc_opened.clear();
     if (r.xbuf) cudaFree(r.xbuf);                 // IPC-exported: plain cudaMalloc
@@ -455,8 +468,8 @@ const double* gemv_t(ks_ctx* c, Rank& r, const double* x_loc, const int* done, l
     const int64_t nrc = (r.m + rc - 1) / rc;
     const int64_t need = nrc * c->ld;
     if (need > r.upart_cap) {
-        dev_free(r.upart);
-        dev_free(r.col_ticket);
+        retire(r, r.upart);
+        retire(r, r.col_ticket);
         r.upart = nullptr;
         r.col_ticket = nullptr;
         dev_alloc_t(&r.upart, (size_t)need);
@@ -498,6 +511,8 @@ GemvConfig gemv_config(const ks_ctx* c, const Rank& r) {
 }  // namespace ks
 
 void ks_ctx::for_each_rank(const std::function<void(ks::Rank&)>& fn) {
+    for (auto& r : ranks)                 // nothing of this context is in flight between calls
+        if (!r.retired.empty() && cudaSetDevice(r.dev) == cudaSuccess) ks::flush_retired(r);
     if (ranks.size() == 1) {
         ks::cuda_check(cudaSetDevice(ranks[0].dev), "cudaSetDevice");
         cudaGetLastError();   // drop a stale, already-reported non-sticky error (e.g. an OOM)

@@ -129,6 +129,7 @@ struct Rank {
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
     cudaEvent_t ev_coll[2]{};           // host-driven collectives (shared-device contexts)
     double* rs_stage = nullptr;         // P * chunk: host-driven reduce-scatter staging
+    std::vector<void*> retired;         // replaced during a call, freed before the next (retire)
     std::vector<cudaEvent_t> ev_gemv;   // profiling pairs
 
     // CUDA-graph replay of one poll batch (KS_OPT_USE_GRAPHS)
@@ -208,6 +209,8 @@ namespace ks {
 constexpr int64_t kHistStage = 4096;   // histories up to this long are staged: one sync per solve
 void rank_alloc(ks_ctx* c, Rank& r);
 void rank_free(Rank& r);
+void retire(Rank& r, void* p);     // free at the start of the next call (no cudaFree inside a call)
+void flush_retired(Rank& r);
 void setup_peers(ks_ctx* c);   // peer access / CUDA IPC of the exchange buffers
 void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank);   // dtype-aware
 void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cudaMemcpyKind kind);

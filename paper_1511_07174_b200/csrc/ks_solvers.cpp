@@ -250,7 +250,7 @@ GemvParams gp(const ks_ctx* c, const Rank& r, const double* x, double* y) {
 // (K1 residual mode) or r0 = b; x_loc; rhat; partial <r0, r0>; allgather G_r.
 void ensure_hist(Rank& r, int64_t hist_cap) {
     if (hist_cap > r.hist_alloc) {
-        dev_free(r.hist);
+        retire(r, r.hist);
         r.hist = nullptr;
         r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
         dev_alloc_t(&r.hist, (size_t)r.hist_alloc);
@@ -510,7 +510,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     r.gemv_launches = 0;
     r.gemv_seconds = 0.0;
     if (hist_cap > r.hist_alloc) {
-        dev_free(r.hist);
+        retire(r, r.hist);
         r.hist = nullptr;
         r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
         dev_alloc_t(&r.hist, (size_t)r.hist_alloc);
@@ -602,7 +602,7 @@ int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
             KS_CUDA(cudaMemcpyAsync(hist, r.hist, (size_t)nh * sizeof(double), cudaMemcpyDefault, r.stream));
         KS_CUDA(cudaStreamSynchronize(r.stream));
     }
-    dev_free(tmp);
+    retire(r, tmp);
     if (rep) {
         float ms = 0.f;
         KS_CUDA(cudaEventElapsedTime(&ms, r.ev_t0, r.ev_t1));
@@ -638,23 +638,23 @@ int64_t run_gmres(ks_ctx* c, Rank& r, const double* b, const double* x0, double 
     r.gemv_seconds = 0.0;
     const size_t nbytes = (size_t)c->n * sizeof(double);
     if (hist_cap > r.hist_alloc) {
-        dev_free(r.hist);
+        retire(r, r.hist);
         r.hist = nullptr;
         r.hist_alloc = std::max<int64_t>(hist_cap, 2 * r.hist_alloc);
         dev_alloc_t(&r.hist, (size_t)r.hist_alloc);
     }
     if (r.gm_m < restart || !r.gmV) {
         for (void* p : {(void*)r.gmV, (void*)r.gmH, (void*)r.gm_hx, (void*)r.gm_state})
-            dev_free(p);
+            retire(r, p);
         r.gm_ldv = (r.m + 31) / 32 * 32;
         r.gm_m = restart;
         dev_alloc_t(&r.gmV, (size_t)(restart + 1) * r.gm_ldv);
         const size_t hsz = (size_t)(restart + 1) * restart + 3 * (size_t)(restart + 1);
         dev_alloc_t(&r.gmH, hsz);
-        KS_CUDA(cudaMemset(r.gmH, 0, hsz * sizeof(double)));
+        KS_CUDA(cudaMemsetAsync(r.gmH, 0, hsz * sizeof(double), r.stream));
         dev_alloc_t(&r.gm_hx, (size_t)c->P * kMaxBasis);
         dev_alloc_t(&r.gm_state, 1);
-        KS_CUDA(cudaMemset(r.gm_state, 0, sizeof(GmresState)));
+        KS_CUDA(cudaMemsetAsync(r.gm_state, 0, sizeof(GmresState), r.stream));
     }
     VecArgs a = r.vargs(false);
     GmresArgs g;
@@ -849,7 +849,7 @@ int64_t run_multi(ks_ctx* c, Rank& r, int bicgstab, int nrhs, const double* B, c
     const int K = multi_k(nrhs);
     const int64_t n = c->n, ld = c->ld, ldm = (r.m + 63) / 64 * 64;
     if (K != r.mK) {
-        for (double* p : {r.mX, r.mR, r.mQ, r.mP, r.mRh, r.mT, r.mS}) dev_free(p);
+        for (double* p : {r.mX, r.mR, r.mQ, r.mP, r.mRh, r.mT, r.mS}) retire(r, p);
         r.mRh = r.mT = r.mS = nullptr;
         dev_alloc_t(&r.mX, (size_t)(K * ldm));
         dev_alloc_t(&r.mR, (size_t)(K * ldm));
@@ -866,7 +866,7 @@ int64_t run_multi(ks_ctx* c, Rank& r, int bicgstab, int nrhs, const double* B, c
     }
     const int64_t hc = hist ? hist_cap : 0;
     if (hc > 0 && hc * K > r.mhist_cap) {
-        dev_free(r.mhist);
+        retire(r, r.mhist);
         r.mhist = nullptr;
         r.mhist_cap = hc * K;
         dev_alloc_t(&r.mhist, (size_t)r.mhist_cap);
