@@ -169,17 +169,17 @@ typedef enum {
 ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
 
 /* As ks_create, with rank g on device devices[g] (nranks entries, 1..16, each a
- * valid device ordinal).  A device may be listed more than once: its ranks split its
- * SMs (each rank's persistent grids are sized from SM count / ranks on that device,
- * so co-running ranks stay co-resident) and exchange over the same fused
- * load/store path as ranks on different GPUs ("communication ...
- * encapsulated in opaque objects": the distribution does not depend on where the
- * ranks run).  Such a context has no NCCL communicator (NCCL rejects two ranks on
- * one GPU): its non-fused collectives are host-driven peer copies ordered by
- * events.  Meant for validating the P > 1 schedules on fewer GPUs than ranks; results
- * equal the oracle's within the same bars, not bitwise those of P distinct GPUs
- * (the grid sizes, and so the partial-sum orders, differ).  KS_EARG for a bad
- * device list or missing peer access, KS_EDIM for n < nranks.                    */
+ * valid device ordinal).  A device may be listed more than once, to run the P > 1
+ * schedule (row-block partition, allgathers of the direction-vector ingredients,
+ * rank-ordered scalar sums, x gather: "communication ... encapsulated in
+ * opaque objects", PAPER.md:78 data distribution) on fewer GPUs than ranks.  Such a
+ * context has no NCCL communicator (NCCL rejects two ranks on one GPU) and never
+ * runs kernels that wait on each other (separate launches on one GPU have no
+ * co-residency guarantee): its collectives are host-driven peer copies ordered by
+ * events, KS_OPT_FUSED_COMM is 0 and cannot be set, and the kernels that need the
+ * fused exchange at P > 1 (persistent, small-n, tiny, multi-RHS) are not used.
+ * Results equal the oracle's within the same bars; they are not bitwise those of
+ * the fused path.  KS_EARG for a bad device list, KS_EDIM for n < nranks.        */
 ks_status ks_create_on(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t nranks, const int32_t* devices);
 
 /* One rank of a multi-process job (one process per GPU, e.g. torchrun) -- the

@@ -107,6 +107,12 @@ ks_status ks_create_on(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t nranks, 
     c->dtype = dtype;
     c->esz = dtype == KS_FLOAT32 ? sizeof(float) : sizeof(double);
     c->shared_dev = shared;
+    // Ranks sharing a GPU never run kernels that wait on each other: separate launches
+    // on one GPU have no co-residency guarantee (B200_PROFILING.md; 2-4 such ranks as
+    // processes on one B200 raised Xid 109).  Their exchanges are the host-driven
+    // collectives, so the fused exchange (and the persistent / small-n / tiny /
+    // multi-RHS kernels that need it) stays off.
+    if (shared) c->opt.fused_comm = 0;
     c->ranks.resize((size_t)nranks);
     for (int g = 0; g < nranks; ++g) {
         c->ranks[g].rank = g;
@@ -122,8 +128,6 @@ ks_status ks_create_on(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t nranks, 
         }
         c->for_each_rank([&](Rank& r) { ks::rank_alloc(c, r); });
         ks::setup_peers(c);
-        if (shared && !c->ranks[0].peer_ok)
-            throw ks::KsError(KS_EARG, "ranks sharing a device need peer access between all listed devices");
         return KS_OK;
     });
     if (st != KS_OK) {
@@ -581,7 +585,11 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             if (v < 0 || v > 1) return fail(c, KS_EARG, "kernel must be 0 or 1 (the TMA variant was removed)");
             o.gemv_kernel = v; break;
         case KS_OPT_USE_GRAPHS: o.use_graphs = v ? 1 : 0; break;
-        case KS_OPT_FUSED_COMM: o.fused_comm = v ? 1 : 0; break;
+        case KS_OPT_FUSED_COMM:
+            if (v && c->shared_dev)
+                return fail(c, KS_EARG, "ranks sharing a GPU cannot use the fused exchange (kernels that wait on "
+                                        "each other have no co-residency guarantee across launches)");
+            o.fused_comm = v ? 1 : 0; break;
         case KS_OPT_PERSISTENT:
             if (v < 0 || v > 2) return fail(c, KS_EARG, "persistent must be 0, 1 or 2");
             o.persistent = v; break;

@@ -3,7 +3,6 @@
 
 #include <algorithm>
 #include <chrono>
-#include <cstdlib>
 #include <exception>
 #include <mutex>
 #include <thread>
@@ -67,14 +66,6 @@ static T* as(double* p) { return reinterpret_cast<T*>(p); }
 void rank_alloc(ks_ctx* c, Rank& r) {
     KS_CUDA(cudaSetDevice(r.dev));
     KS_CUDA(cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, r.dev));
-    // ranks sharing a GPU split its SMs: every persistent grid of a rank is sized from
-    // num_sms, so the co-running ranks' grids stay co-resident (their in-kernel waits
-    // on each other need that)
-    if (r.dev_share > 1) {
-        int slack = 0;                               // tuning: SMs held back from the split
-        if (const char* e = std::getenv("KS_SHARED_SLACK")) slack = std::max(0, std::atoi(e));
-        r.num_sms = std::max(1, (r.num_sms - slack) / r.dev_share);
-    }
     if (!r.stream) {
         KS_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
         r.own_stream = true;

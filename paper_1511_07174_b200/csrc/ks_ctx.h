@@ -55,7 +55,7 @@ struct HostBarrier {
 
 struct Rank {
     int rank = 0, dev = 0, num_sms = 148;
-    int dev_share = 1;          // ranks of this context on the same GPU (its SMs are split)
+    int dev_share = 1;          // ranks of this context on the same GPU
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     ncclComm_t comm = nullptr;
@@ -180,7 +180,7 @@ struct ks_ctx {
     int P = 1;               // global number of ranks
     bool multiprocess = false;
     // some ranks share a GPU (ks_create_on with a repeated device): no NCCL
-    // communicator; the non-fused collectives are host-driven peer copies
+    // communicator, no fused exchange; the collectives are host-driven peer copies
     bool shared_dev = false;
     std::unique_ptr<ks::HostBarrier> hbar = std::make_unique<ks::HostBarrier>();
     std::vector<ks::Rank> ranks;   // local ranks (1 in multi-process mode)

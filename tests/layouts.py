@@ -1,10 +1,13 @@
 """Rank layouts of the P > 1 GPU tests.
 
 ("gpus", P): P ranks on GPUs 0..P-1 (ks_create); skipped on a box with fewer GPUs.
-("shared", P): P ranks all on GPU 0 (ks_create_on with a repeated device): the same
-P > 1 schedules -- fused load/store exchange, rendezvous, x gather, host-driven
-collectives in place of NCCL -- with each rank's persistent grids on 148/P SMs.  It
-runs on any GPU box, so the P > 1 paths are checked even where only one GPU exists.
+("shared", P): P ranks all on GPU 0 (ks_create_on with a repeated device): the P > 1
+schedule -- row-block partition, allgathers of r / p / v ingredients, rank-ordered
+scalar sums, x gather -- through host-driven peer-copy collectives (no NCCL, no fused
+exchange: kernels that wait on each other are never launched separately on one GPU,
+B200_PROFILING.md).  It runs on any GPU box, so the allgather schedule of rows A4 / B2
+is checked against the oracle even where only one GPU exists; the fused NVLink kernels
+(NEXT-1) need the ("gpus", P) layouts.
 """
 import pytest
 

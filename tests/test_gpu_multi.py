@@ -61,7 +61,7 @@ def test_multi_gemv_and_cg(lay):
     assert r1.iterations == rg.iterations
 
 
-@pytest.mark.parametrize("lay", layouts())
+@pytest.mark.parametrize("lay", layouts(shared=()))
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_multi_small_cg_allgather_only(lay, dtype):
     """Small-n CG over P GPUs (k_cg_small_peer: one exchange of q slices and one grid
@@ -100,7 +100,7 @@ def test_multi_small_cg_allgather_only(lay, dtype):
         assert abs(outs[0] - outs[1]) <= 2
 
 
-@pytest.mark.parametrize("lay", layouts())
+@pytest.mark.parametrize("lay", layouts(shared=()))
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_multi_small_bicgstab_allgather_only(lay, dtype):
     """Small-n BiCGSTAB over P GPUs (k_bs_small_peer: v and t slices are the only
@@ -153,7 +153,7 @@ def test_multi_bicgstab(lay):
         assert r.half_step_exit == ro.half_step_exit
 
 
-@pytest.mark.parametrize("lay", layouts())
+@pytest.mark.parametrize("lay", layouts(shared=()))
 def test_fused_collectives_bitwise_equal_nccl(lay):
     """NEXT-1: the fused NVLink peer-store collectives carry the same partials and
     sum them in the same rank order as the NCCL allgathers, so x, the history and
@@ -187,7 +187,7 @@ def test_fused_collectives_bitwise_equal_nccl(lay):
     bars(x, h, r, xo, ho, ro)
 
 
-@pytest.mark.parametrize("lay", layouts())
+@pytest.mark.parametrize("lay", layouts(shared=()))
 def test_multi_persistent_fused(lay):
     """NEXT-1 + NEXT-2 together: persistent cooperative kernels on every GPU with
     the fused NVLink exchange; bars vs the oracle; identical on repeat."""
@@ -214,9 +214,11 @@ def test_multi_persistent_fused(lay):
 @pytest.mark.parametrize("fused", [1, 0])
 def test_multi_bicg(lay, fused):
     """NEXT-3 BiCG at P GPUs: K1T partials reduce-scattered either inside K1T over
-    NVLink peer stores (fused = 1, default) or by ncclReduceScatter (fused = 0);
-    x0 and maxit included."""
+    NVLink peer stores (fused = 1, default) or by ncclReduceScatter (fused = 0; ranks
+    sharing a GPU: the host-driven reduce-scatter); x0 and maxit included."""
     P = need(lay)
+    if fused and lay[0] == "shared":
+        pytest.skip("ranks sharing a GPU run the host-driven collectives only")
     for n, kd in [(1024, 4), (4099, 16)]:
         A, b = synth.gdd(n, kd)
         xo, ho, ro = oracle.bicg(A, b, tol=1e-10)
@@ -251,7 +253,8 @@ def test_multi_gmres(lay, persistent):
         with context(n, lay) as ctx:
             ctx.set_option("persistent", persistent)
             ctx.generate("dd", seed=synth.SEED, kd=kd, want_b=False)
-            assert ctx.get_option("persistent") == persistent and ctx.get_option("fused_comm") == 1
+            fused = 0 if lay[0] == "shared" else 1       # shared GPU: host collectives, multi-kernel
+            assert ctx.get_option("persistent") == (persistent and fused) and ctx.get_option("fused_comm") == fused
             x, h, r = ctx.gmres(b, x0=x0, tol=1e-10, restart=m)
             bars(x, h, r, xo, ho, ro)
             xo7, ho7, ro7 = oracle.gmres(A, b, x0=x0, tol=1e-30, restart=m, maxit=7)
@@ -260,7 +263,7 @@ def test_multi_gmres(lay, persistent):
             bars(x7, h7, r7, xo7, ho7, ro7, iters_tol=0)
 
 
-@pytest.mark.parametrize("lay", layouts())
+@pytest.mark.parametrize("lay", layouts(shared=()))
 def test_multi_f32(lay):
     """NEXT-4 at P GPUs: FP32 persistent kernels with the fused NVLink exchange."""
     P = need(lay)

@@ -121,7 +121,7 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("lay", layouts())
+@pytest.mark.parametrize("lay", layouts(shared=()))
 def test_multi_rhs_over_p_gpus(lay):
     """Multi-RHS CG over P GPUs (row blocks; per iteration the K columns' sigma and
     rho' partials are all-reduced and the r slices gathered through the fused NVLink
@@ -216,7 +216,7 @@ def test_bicgstab_multi_exits_and_repeat():
     bars(X[:, 0], h[0], r[0], Xo[:, 0], ho[0], ro[0], floor=FLOOR_BS)
 
 
-@pytest.mark.parametrize("lay", layouts())
+@pytest.mark.parametrize("lay", layouts(shared=()))
 def test_bicgstab_multi_over_p_gpus(lay):
     """Multi-RHS BiCGSTAB over P GPUs: v and r slices through every rank's exchange
     regions, the per-column dots as rank all-reduces; per-column bars vs the oracle
