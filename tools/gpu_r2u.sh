@@ -1,12 +1,12 @@
 #!/bin/bash
-# Round-2 rehearsal on one GPU after the shared-device layouts and the jitter mode:
-# race tests first, the whole GPU suite, smoke, bench, ncu launch list, ncu full.
+# Round-2 rehearsal on one GPU: shared-GPU (host-collective) layouts and race tests
+# first, then the whole GPU suite, smoke, bench, ncu launch list, tiny-grid A/B.
 set -u
 O=gpurun_out/r2u
 mkdir -p $O
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv > $O/gpu.txt
-timeout 1200 python -m pytest tests/test_gpu_race.py -q --timeout 300 -p no:cacheprovider > $O/race.log 2>&1; echo "race rc=$?" >> $O/race.log; tail -3 $O/race.log
-timeout 2400 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider --ignore=tests/test_gpu_race.py > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log; tail -3 $O/pytest_gpu.log
+timeout 1200 python -m pytest tests -m gpu -q --timeout 300 --tb=short -p no:cacheprovider -k "shared or race" > $O/shared_race.log 2>&1; echo "shared+race rc=$?" >> $O/shared_race.log; tail -4 $O/shared_race.log
+timeout 2400 python -m pytest tests -m gpu -q --timeout 600 --tb=short -p no:cacheprovider -k "not shared and not race" > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log; tail -3 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"; cat $O/bench.json
 CMD="python bench.py --steps 16 --warmup 3 --no-cpu-baseline --no-extras"
