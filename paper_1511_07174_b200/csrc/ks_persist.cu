@@ -14,6 +14,7 @@
 // can run inside a persistent kernel): partial scalars and r slices are pushed
 // to every rank and flagged; v is pulled.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <math.h>
 #include <stdint.h>
 
@@ -29,8 +30,8 @@ namespace {
 using namespace pk;
 
 // ---------------------------------------------------------------- CG (A1-A5)
-template <class T, int kR, int kU>
-__global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
+template <class T, int kR, int kU, int kMinB = 4>
+__global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
     __shared__ T red[(kR > 2 ? kR : 2) * kNW];
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
@@ -116,8 +117,8 @@ __global__ void __launch_bounds__(kNT, 4) k_cg_persist(PersistArgs<T> P) {
 }
 
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
-template <class T, int kR, int kU>
-__global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
+template <class T, int kR, int kU, int kMinB = 4>
+__global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
     __shared__ T red[(kR > 2 ? kR : 2) * kNW];
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
@@ -300,9 +301,20 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist(PersistArgs<T> P) {
 // (4,2) and (4,4) selectable through KS_OPT_GEMV_ROWS / KS_OPT_GEMV_UNROLL.
 // (1, 8): one-row tiles for shards whose 2-row tile count would leave a badly filled
 // last wave over the resident CTAs (ks_solvers.cpp persist_shape).
+// KS_PERSIST_OCC=5 (tuning): the default (2, 4) shape compiled for 5 CTAs per SM
+// (48 registers; the GEMV loop stays spill-free) instead of 4 (64 registers).
+bool occ5() {
+    static const bool v = [] {
+        const char* e = std::getenv("KS_PERSIST_OCC");
+        return e && std::atoi(e) == 5;
+    }();
+    return v;
+}
 template <class T>
 const void* pick(int bicgstab, int rows, int unroll) {
     const int shape = (rows == 4 && unroll == 2) ? 1 : (rows == 4 && unroll == 4) ? 2 : (rows == 1) ? 3 : 0;
+    if (shape == 0 && occ5())
+        return bicgstab ? (const void*)k_bs_persist<T, 2, 4, 5> : (const void*)k_cg_persist<T, 2, 4, 5>;
     if (bicgstab) {
         return shape == 1 ? (const void*)k_bs_persist<T, 4, 2>
              : shape == 2 ? (const void*)k_bs_persist<T, 4, 4>

@@ -13,3 +13,8 @@ CMD="python bench.py --steps 16 --warmup 3 --no-cpu-baseline --no-extras"
 timeout 300 $CMD > $O/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
 timeout 600 python tools/tiny_grid_ab.py > $O/tiny_grid_ab.jsonl 2> $O/tiny_grid_ab.err; echo "tiny grid rc=$?"; cat $O/tiny_grid_ab.jsonl
+for rep in 1 2; do for occ in 4 5; do
+  KS_PERSIST_OCC=$occ timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-extras > $O/occ$occ.json 2>/dev/null
+  python -c "import json,sys; d=json.loads(open('$O/occ$occ.json').read().strip().splitlines()[-1]); print(json.dumps({'occ': $occ, 'rep': $rep, 'value': d['value'], 'frac': d['roofline']['frac'], 'e2e': d['e2e']['value']}))" >> $O/occ_ab.jsonl
+done; done
+cat $O/occ_ab.jsonl
