@@ -145,7 +145,7 @@ typedef enum {
                               /* kernels (A in shared memory, vectors replicated  */
                               /* in registers, LL-format exchange of the GEMV     */
                               /* output: no grid barrier); 0 = off                */
-    KS_OPT_JITTER = 15        /* race detection: seed (0 = off, default) of       */
+    KS_OPT_JITTER = 15,       /* race detection: seed (0 = off, default) of       */
                               /* pseudo-random delays (<= ~4 us, a quarter of the */
                               /* visits) at every synchronisation point of the    */
                               /* persistent, small, tiny and multi-RHS kernels    */
@@ -154,6 +154,14 @@ typedef enum {
                               /* change: the kernels' sums have fixed orders and  */
                               /* their exchanges are epoch-tagged, so a run with  */
                               /* jitter equals a run without it bit for bit.      */
+    KS_OPT_LL_XCHG = 16       /* 1 (default): the persistent CG / BiCGSTAB        */
+                              /* kernels over P > 1 GPUs hand the r / v slices   */
+                              /* and the rank partial scalars over as LL words   */
+                              /* (32 payload bits + the iteration epoch per 8-B  */
+                              /* word, one 16-B system-scope store per value     */
+                              /* into every rank) that consumers poll: no fence, */
+                              /* no flag.  Same sums in the same order: results   */
+                              /* equal the fence + flag handovers (0) bitwise.   */
 } ks_option;
 
 /* Creates the opaque object that encapsulates the distributed matrix and its

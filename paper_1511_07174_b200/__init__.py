@@ -31,7 +31,7 @@ OPTIONS = {"true_residual": 0, "profile_gemv": 1, "poll_batch": 2, "gemv_rows": 
            "gemv_split": 4, "gemv_kernel": 5, "use_graphs": 6, "fused_comm": 7,
            "persistent": 8, "gemv_unroll": 9, "persist_grid": 10,
            "gemvt_shape": 11, "small": 12, "join_timeout_ms": 13,
-           "tiny": 14, "jitter": 15}
+           "tiny": 14, "jitter": 15, "ll_xchg": 16}
 EXPORTS = ["ks_create", "ks_create_on", "ks_create_rank", "ks_destroy", "ks_row_range", "ks_load_rows",
            "ks_generate", "ks_matvec", "ks_matvec_t", "ks_time_matvec", "ks_cg", "ks_bicgstab",
            "ks_bicg", "ks_gmres", "ks_cg_multi", "ks_bicgstab_multi",

@@ -627,6 +627,11 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             o.jitter = v;
             break;
         }
+        case KS_OPT_LL_XCHG:
+            if (v < 0 || v > 1) return fail(c, KS_EARG, "ll_xchg must be 0 or 1");
+            o.ll_xchg = v;
+            for (auto& r : c->ranks) r.ll_on = (int)v;
+            break;
         default: return fail(c, KS_EARG, "unknown option");
     }
     return KS_OK;
@@ -660,6 +665,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_JOIN_TIMEOUT_MS: *v = o.join_timeout_ms; break;
         case KS_OPT_TINY: *v = o.tiny; break;
         case KS_OPT_JITTER: *v = o.jitter; break;
+        case KS_OPT_LL_XCHG: *v = (o.ll_xchg && c->fused()) ? 1 : 0; break;   // effective value
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;

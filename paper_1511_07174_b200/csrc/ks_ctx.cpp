@@ -26,6 +26,8 @@ VecArgs Rank::vargs(bool fused) const {
     a.spar = fused ? (int64_t)L.P * kScalSlot : 0;
     a.peer = fused ? 1 : 0;
     a.jitter = jitter;
+    a.ll = (fused && llg) ? ll_on : 0;
+    a.llg = llg;
     a.pp = pp;
     a.flags = flags;
     a.L = L;
@@ -70,6 +72,7 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         KS_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
         r.own_stream = true;
     }
+    r.ll_on = (int)c->opt.ll_xchg;
     const int64_t ld = c->ld;
     const size_t P = (size_t)c->P;
     const size_t e = c->esz;
@@ -98,7 +101,8 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         const size_t mvb = mrb;                     // v slices of multi-RHS BiCGSTAB
         // tiny kernels over P > 1 (n <= 1024): their LL exchange slots, 4 ld words
         const size_t llb = (P > 1 && ld <= 1024) ? 4 * (size_t)ld * sizeof(uint64_t) : 0;
-        const size_t total = 2 * g + sb + fb + xb + mrb + msb + mxb + llb + mvb;
+        const size_t lgb = P > 1 ? (size_t)ll_words(ld) * sizeof(uint64_t) : 0;   // persistent LL handovers
+        const size_t total = 2 * g + sb + fb + xb + mrb + msb + mxb + llb + mvb + lgb;
         char* base = nullptr;
         KS_CUDA(cudaMalloc(reinterpret_cast<void**>(&base), total));
         KS_CUDA(cudaMemset(base, 0, total));
@@ -114,6 +118,7 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         r.MX = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb + msb) : nullptr;
         r.llx = llb ? reinterpret_cast<uint64_t*>(base + 2 * g + sb + fb + xb + mrb + msb + mxb) : nullptr;
         r.MV = mm ? reinterpret_cast<double*>(base + 2 * g + sb + fb + xb + mrb + msb + mxb + llb) : nullptr;
+        r.llg = lgb ? reinterpret_cast<uint64_t*>(base + 2 * g + sb + fb + xb + mrb + msb + mxb + llb + mvb) : nullptr;
         for (int q = 0; q < kMaxRanks; ++q) r.llpeer[q] = nullptr;
         r.llpeer[r.rank] = r.llx;
         for (int q = 0; q < kMaxRanks; ++q) {
@@ -128,7 +133,9 @@ void rank_alloc(ks_ctx* c, Rank& r) {
         for (int q = 0; q < kMaxRanks; ++q) {
             r.pp.G_r[q] = r.pp.G_v[q] = r.pp.S[q] = r.pp.X[q] = nullptr;
             r.pp.flags[q] = nullptr;
+            r.pp.llg[q] = nullptr;
         }
+        r.pp.llg[r.rank] = r.llg;
         r.pp.X[r.rank] = r.X;
         r.pp.G_r[r.rank] = r.G_r;
         r.pp.G_v[r.rank] = r.G_v;
@@ -330,7 +337,10 @@ VecArgsT<float> Rank::vargs_f32(bool fused) const {
     a.spar = fused ? (int64_t)L.P * kScalSlot : 0;
     a.peer = fused ? 1 : 0;
     a.jitter = jitter;
+    a.ll = (fused && llg) ? ll_on : 0;
+    a.llg = llg;
     for (int g = 0; g < kMaxRanks; ++g) {
+        a.pp.llg[g] = pp.llg[g];
         a.pp.G_r[g] = as<float>(pp.G_r[g]);
         a.pp.G_v[g] = as<float>(pp.G_v[g]);
         a.pp.S[g] = as<float>(pp.S[g]);
@@ -374,6 +384,8 @@ void setup_peers(ks_ctx* c) {
     const size_t offMV = mm ? boff(c->ranks[0].MV) : 0;
     const bool hasll = c->ranks[0].llx != nullptr;
     const size_t offLL = hasll ? boff(c->ranks[0].llx) : 0;
+    const bool hasllg = c->ranks[0].llg != nullptr;
+    const size_t offLLG = hasllg ? boff(c->ranks[0].llg) : 0;
     if (!c->multiprocess) {
         bool ok = true;
         for (auto& a : c->ranks)
@@ -400,6 +412,7 @@ void setup_peers(ks_ctx* c) {
                 a.mpeer.MV[b.rank] = b.MV;
                 a.mpeer.flags[b.rank] = b.flags;
                 a.llpeer[b.rank] = b.llx;
+                a.pp.llg[b.rank] = b.llg;
             }
             a.peer_ok = ok;
         }
@@ -433,6 +446,7 @@ void setup_peers(ks_ctx* c) {
         r.pp.X[g] = reinterpret_cast<double*>(d + offX);
         r.mpeer.flags[g] = reinterpret_cast<unsigned long long*>(d + offF);
         if (hasll) r.llpeer[g] = reinterpret_cast<uint64_t*>(d + offLL);
+        if (hasllg) r.pp.llg[g] = reinterpret_cast<uint64_t*>(d + offLLG);
         if (mm) {
             r.mpeer.MR[g] = reinterpret_cast<double*>(d + offMR);
             r.mpeer.MS[g] = reinterpret_cast<double*>(d + offMS);

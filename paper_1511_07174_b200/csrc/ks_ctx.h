@@ -96,6 +96,8 @@ struct Rank {
     double* X = nullptr;        // ld elements: contiguous full x (end-of-solve gather)
     double *MR = nullptr, *MS = nullptr, *MX = nullptr, *MV = nullptr;   // multi-RHS exchange regions (P > 1)
     uint64_t* llx = nullptr;    // tiny kernels' LL slots in the exchange allocation (P > 1, ld <= 1024)
+    uint64_t* llg = nullptr;    // persistent kernels' LL handover region (P > 1, ll_words(ld) words)
+    int ll_on = 0;              // KS_OPT_LL_XCHG (effective with the fused exchange)
     const double* x0_full = nullptr;   // the current solve's full x0 on the device (s_full) or NULL
     uint64_t* llpeer[kMaxRanks] = {};
     MultiPeer mpeer{};
@@ -169,6 +171,7 @@ struct Options {
     int64_t join_timeout_ms = 120000;   // fused P > 1: solve-start rendezvous bound
     int64_t tiny = 1;         // 1 auto, 0 off: register-resident kernels (P == 1, n <= 1024)
     int64_t jitter = 0;       // race-detection delays at sync points (seed; 0 off)
+    int64_t ll_xchg = 1;      // LL handovers in the persistent kernels (P > 1, fused)
 };
 
 }  // namespace ks

@@ -24,6 +24,20 @@ constexpr int kPhaseV = 2;   // BiCGSTAB v slice + <rhat,v>
 constexpr int kPhaseJ = 3;   // solve-start rendezvous (epoch = the solve's ebase)
 constexpr int kPhaseX = 4;   // end-of-solve x gather (epoch = ebase + maxit + 1)
 constexpr int kNumPhases = 5;
+// LL handover region of the persistent kernels over P > 1 GPUs (KS_OPT_LL_XCHG): every
+// entry is one double as two 8-byte words (32 payload bits + the 32-bit epoch each),
+// stored with one 16-byte system-scope store by the producer straight into every
+// rank's region; consumers poll their local copy until both words carry the epoch --
+// no fence, no flag.  Layout (u64 words): [2 parities][3 vectors (r, v, spare)][ld] x 2,
+// then [2 parities][kLlPhases][kMaxRanks][2 scalars] x 2.
+constexpr int kLlPhases = 4;   // 0: CG sigma / BiCGSTAB gamma, 1: rho' / (rhat,r),(r,r), 2: (t,s),(t,t)
+__host__ __device__ constexpr int64_t ll_words(int64_t ld) { return 2 * 3 * ld * 2 + 2 * kLlPhases * kMaxRanks * 2 * 2; }
+__host__ __device__ inline int64_t ll_vec_off(int64_t ld, int par, int vec, int64_t j) {
+    return (((int64_t)par * 3 + vec) * ld + j) * 2;
+}
+__host__ __device__ inline int64_t ll_scal_off(int64_t ld, int par, int ph, int rank, int q) {
+    return 2 * 3 * ld * 2 + ((((int64_t)par * kLlPhases + ph) * kMaxRanks + rank) * 2 + q) * 2;
+}
 
 // Peer (NVLink, unified-address) pointers to every rank's exchange buffers,
 // parity-0 bases; rank g's own entries point at its local memory.
@@ -34,6 +48,7 @@ struct PeerPtrsT {
     T* S[kMaxRanks];
     unsigned long long* flags[kMaxRanks];   // [kNumPhases][kMaxRanks] epochs
     T* X[kMaxRanks];                        // full-length x (contiguous), end-of-solve gather
+    uint64_t* llg[kMaxRanks];               // LL handover slots of the persistent kernels (P > 1)
 };
 using PeerPtrs = PeerPtrsT<double>;
 
@@ -163,6 +178,8 @@ struct VecArgsT {
     int64_t gpar, spar;
     int peer;              // 1: fused NVLink peer-store collectives
     unsigned jitter;       // KS_OPT_JITTER seed (0: off), ks_device.cuh jitter_at
+    int ll;                // 1: LL handovers in the persistent kernels (P > 1, KS_OPT_LL_XCHG)
+    uint64_t* llg;         // own LL handover region (ll_words(ld) words), nullptr for P == 1
     PeerPtrsT<T> pp;
     unsigned long long* flags;   // own [kNumPhases][kMaxRanks]
     T* X;                  // own full-length x gather buffer (exchange allocation)

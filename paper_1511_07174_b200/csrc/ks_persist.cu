@@ -49,7 +49,14 @@ __global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
         T sig[1];
         grid_total<1>(P.bpart, 0, sig, red);
         T sigma = sig[0];
-        if (a.peer) {                                   // A2 fused C2
+        if (a.peer && a.ll) {                           // A2 fused C2, LL words
+            if (lead()) {
+                const double v = (double)sigma;
+                ll_push_scal(a, (int)(k & 1), 0, &v, 1, ll_epoch(st, k));
+            }
+            if (!ll_sum_scal<1>(a, (int)(k & 1), 0, ll_epoch(st, k), sig)) return;
+            sigma = sig[0];
+        } else if (a.peer) {                            // A2 fused C2
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) a.pp.S[g][(k & 1) * a.spar + L.rank * kScalSlot] = sigma;
                 flags_out(a, kPhaseS, k);
@@ -66,24 +73,36 @@ __global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
         const T* rin = par_ptr(a.G_r, a.gpar, k - 1) + (int64_t)L.rank * L.chunk;
         const int64_t ro = (k & 1) * a.gpar + (int64_t)L.rank * L.chunk;
         T acc[1] = {T(0)};
+        const uint32_t ep = ll_epoch(st, k);
+        if (a.peer && a.ll) jitter_at(a.jitter, 8u);
         for (int64_t i = tid0; i < m; i += gstride) {
             a.x_loc[i] = fma(alpha, a.p_full[r0 + i], a.x_loc[i]);
             const T r = fma(-alpha, a.q_loc[i], rin[i]);
-            if (a.peer) {
+            if (a.peer && a.ll) {                       // A4 as LL words (own chunk kept plain: next rin)
+                a.G_r[ro + i] = r;
+                for (int g = 0; g < L.P; ++g) ll_put_sys(a.pp.llg[g] + ll_vec_off(L.ld, (int)(k & 1), 0, r0 + i), (double)r, ep);
+            } else if (a.peer) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + i] = r;
             } else {
                 a.G_r[ro + i] = r;
             }
             acc[0] = fma(r, r, acc[0]);
         }
-        if (a.peer && tid0 < m) __threadfence_system();   // only threads that stored remotely
+        if (a.peer && !a.ll && tid0 < m) __threadfence_system();   // only threads that stored remotely
         block_sum<kNT, 1>(acc, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = acc[0];
         if (!grid_sync(P.bar, st)) return;
         T rr[1];
         grid_total<1>(P.bpart, 1, rr, red);
         T rho1 = rr[0];
-        if (a.peer) {                                   // A4 fused C1 (+ partials)
+        if (a.peer && a.ll) {                           // rho' rank partials, LL words
+            if (lead()) {
+                const double v = (double)rho1;
+                ll_push_scal(a, (int)(k & 1), 1, &v, 1, ep);
+            }
+            if (!ll_sum_scal<1>(a, (int)(k & 1), 1, ep, rr)) return;
+            rho1 = rr[0];
+        } else if (a.peer) {                            // A4 fused C1 (+ partials)
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + L.pslot + 1] = rho1;
                 flags_out(a, kPhaseR, k);
@@ -102,10 +121,21 @@ __global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
         }
         const T beta = rho1 / (T)st->rho[(k - 1) & 3];
         const T* Gr = par_ptr(a.G_r, a.gpar, k);
-        for (int64_t j = tid0; j < L.n; j += gstride) {
-            int o;
-            const int64_t gj = gidx_owner(L, j, &o);
-            a.p_full[j] = fma(beta, a.p_full[j], Gr[gj]);
+        if (a.peer && a.ll) {                           // p = r + beta p, r polled from the LL slots
+            bool ok = true;
+            jitter_at(a.jitter, 9u);
+            for (int64_t j = tid0; j < L.n && ok; j += gstride) {
+                double rj = 0.0;
+                ok = ll_get_sys(a.llg + ll_vec_off(L.ld, (int)(k & 1), 0, j), ep, rj);
+                a.p_full[j] = fma(beta, a.p_full[j], (T)rj);
+            }
+            if (!ok) { st->peer_timeout = 1; st->status = KS_ENCCL; st->done = 1; return; }
+        } else {
+            for (int64_t j = tid0; j < L.n; j += gstride) {
+                int o;
+                const int64_t gj = gidx_owner(L, j, &o);
+                a.p_full[j] = fma(beta, a.p_full[j], Gr[gj]);
+            }
         }
         if (lead()) {
             put_hist(st, a.hist, k - 1, rel);
@@ -133,15 +163,20 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
     for (long long i = P.k0; i <= P.k1; ++i) {
         if (is_done(st)) break;
         // B8 (test of i-1) + B1
-        if (a.peer && i >= 2 && !wait_ph(a, kPhaseR, i - 1)) return;
+        const bool llx = a.peer && a.ll;               // LL handovers (KS_OPT_LL_XCHG)
+        const uint32_t ep_prev = ll_epoch(st, i - 1), ep = ll_epoch(st, i);
+        const int par_prev = (int)((i - 1) & 1), par = (int)(i & 1);
+        if (a.peer && !llx && i >= 2 && !wait_ph(a, kPhaseR, i - 1)) return;
         const T* Gr = par_ptr(a.G_r, a.gpar, i - 1);
         // P == 1: after the first iteration of a launch the partials are in registers
         // (every CTA computed them), so no barrier is needed to read the lead's slots
         const bool carried = !a.peer && i > P.k0;
-        const T rho = carried ? rho_next : slot_sum(L, Gr, 0);
+        T rv_prev[2] = {T(0), T(0)};
+        if (llx && i >= 2 && !ll_sum_scal<2>(a, par_prev, 1, ep_prev, rv_prev)) return;
+        const T rho = carried ? rho_next : (llx && i >= 2) ? rv_prev[0] : slot_sum(L, Gr, 0);
         T rel = T(0);
         if (i >= 2) {
-            rel = sqrt(carried ? rr_next : slot_sum(L, Gr, 1)) / (T)st->nb;
+            rel = sqrt(carried ? rr_next : llx ? rv_prev[1] : slot_sum(L, Gr, 1)) / (T)st->nb;
             if (rel <= (T)st->tol) {
                 if (lead()) {
                     put_hist(st, a.hist, i - 2, rel);
@@ -162,6 +197,16 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
                 int o;
                 a.p_full[j] = Gr[gidx_owner(L, j, &o)];
             }
+        } else if (llx) {                               // r of i-1 polled from the LL slots
+            const T beta = (rho / rho_prev) * (alpha_prev / omega_prev);
+            bool ok = true;
+            jitter_at(a.jitter, 9u);
+            for (int64_t j = tid0; j < L.n && ok; j += gstride) {
+                double rj = 0.0;
+                ok = ll_get_sys(a.llg + ll_vec_off(L.ld, par_prev, 0, j), ep_prev, rj);
+                a.p_full[j] = fma(beta, fma(-omega_prev, a.v_full[j], a.p_full[j]), (T)rj);
+            }
+            if (!ok) { st->peer_timeout = 1; st->status = KS_ENCCL; st->done = 1; return; }
         } else {
             const T beta = (rho / rho_prev) * (alpha_prev / omega_prev);
             for (int64_t j = tid0; j < L.n; j += gstride) {
@@ -185,7 +230,19 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         T gm[1];
         grid_total<1>(P.bpart, 0, gm, red);
         T gam = gm[0];
-        if (a.peer) {                                   // B2/B4: v pulled, partial pushed
+        if (llx) {                                      // B2/B4: v rows and the rank partial as LL words
+            if (lead()) {
+                const double g1 = (double)gam;
+                ll_push_scal(a, par, 0, &g1, 1, ep);
+            }
+            jitter_at(a.jitter, 8u);
+            for (int64_t l = tid0; l < m; l += gstride) {
+                const double vl = (double)a.G_v[vo + l];
+                for (int g = 0; g < L.P; ++g) ll_put_sys(a.pp.llg[g] + ll_vec_off(L.ld, par, 1, r0 + l), vl, ep);
+            }
+            if (!ll_sum_scal<1>(a, par, 0, ep, gm)) return;
+            gam = gm[0];
+        } else if (a.peer) {                            // B2/B4: v pulled, partial pushed
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_v[g][vo + L.pslot] = gam;
                 flags_out(a, kPhaseV, i);
@@ -200,15 +257,36 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         const T alpha = rho / gam;
         // B4/B5: s = r - alpha v (full n, redundant), ||s||^2
         T sacc[1] = {T(0)};
-        for (int64_t j = tid0; j < L.n; j += gstride) {
-            int o;
-            const int64_t gj = gidx_owner(L, j, &o);
-            const T v = a.peer ? __ldcg(a.pp.G_v[o] + (i & 1) * a.gpar + gj)
-                                    : a.G_v[(i & 1) * a.gpar + gj];
-            a.v_full[j] = v;
-            const T s = fma(-alpha, v, Gr[gj]);
-            a.s_full[j] = s;
-            sacc[0] = fma(s, s, sacc[0]);
+        if (llx) {
+            bool ok = true;
+            jitter_at(a.jitter, 9u);
+            for (int64_t j = tid0; j < L.n && ok; j += gstride) {
+                double vj = 0.0, rj = 0.0;
+                ok = ll_get_sys(a.llg + ll_vec_off(L.ld, par, 1, j), ep, vj);
+                if (i >= 2) {
+                    ok = ok && ll_get_sys(a.llg + ll_vec_off(L.ld, par_prev, 0, j), ep_prev, rj);
+                } else {
+                    int o;
+                    rj = (double)Gr[gidx_owner(L, j, &o)];
+                }
+                const T v = (T)vj;
+                a.v_full[j] = v;
+                const T s = fma(-alpha, v, (T)rj);
+                a.s_full[j] = s;
+                sacc[0] = fma(s, s, sacc[0]);
+            }
+            if (!ok) { st->peer_timeout = 1; st->status = KS_ENCCL; st->done = 1; return; }
+        } else {
+            for (int64_t j = tid0; j < L.n; j += gstride) {
+                int o;
+                const int64_t gj = gidx_owner(L, j, &o);
+                const T v = a.peer ? __ldcg(a.pp.G_v[o] + (i & 1) * a.gpar + gj)
+                                        : a.G_v[(i & 1) * a.gpar + gj];
+                a.v_full[j] = v;
+                const T s = fma(-alpha, v, Gr[gj]);
+                a.s_full[j] = s;
+                sacc[0] = fma(s, s, sacc[0]);
+            }
         }
         block_sum<kNT, 1>(sacc, red);
         if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = sacc[0];
@@ -233,7 +311,15 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         T tv[2];
         grid_total<2>(P.bpart, 2, tv, red);
         T ts = tv[0], tt = tv[1];
-        if (a.peer) {                                   // B7 fused C2
+        if (llx) {                                      // B7 C2 as LL words
+            if (lead()) {
+                const double w2[2] = {(double)ts, (double)tt};
+                ll_push_scal(a, par, 2, w2, 2, ep);
+            }
+            if (!ll_sum_scal<2>(a, par, 2, ep, tv)) return;
+            ts = tv[0];
+            tt = tv[1];
+        } else if (a.peer) {                            // B7 fused C2
             if (lead()) {
                 for (int g = 0; g < L.P; ++g) {
                     a.pp.S[g][(i & 1) * a.spar + L.rank * kScalSlot + 0] = ts;
@@ -253,11 +339,15 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         // B7: x += alpha p + omega s; r = s - omega t; <rhat, r>_g, <r, r>_g
         const int64_t ro = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
         T acc[2] = {T(0), T(0)};
+        if (llx) jitter_at(a.jitter, 8u);
         for (int64_t l = tid0; l < m; l += gstride) {
             const T s = a.s_full[r0 + l];
             a.x_loc[l] = fma(om, s, fma(alpha, a.p_full[r0 + l], a.x_loc[l]));
             const T r = fma(-om, a.q_loc[l], s);
-            if (a.peer) {
+            if (llx) {
+                a.G_r[ro + l] = r;
+                for (int g = 0; g < L.P; ++g) ll_put_sys(a.pp.llg[g] + ll_vec_off(L.ld, par, 0, r0 + l), (double)r, ep);
+            } else if (a.peer) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + l] = r;
             } else {
                 a.G_r[ro + l] = r;
@@ -265,20 +355,25 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
             acc[0] = fma(a.rhat_loc[l], r, acc[0]);
             acc[1] = fma(r, r, acc[1]);
         }
-        if (a.peer && tid0 < m) __threadfence_system();   // only threads that stored remotely
+        if (a.peer && !llx && tid0 < m) __threadfence_system();   // only threads that stored remotely
         block_sum<kNT, 2>(acc, red);
         if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 0] = acc[0]; P.bpart[blockIdx.x * 4 + 1] = acc[1]; }
         if (!grid_sync(P.bar, st)) return;
         T rv[2];
         grid_total<2>(P.bpart, 0, rv, red);
         if (lead()) {
-            if (a.peer) {
+            if (llx) {                                  // consumed at the top of i + 1
+                const double w2[2] = {(double)rv[0], (double)rv[1]};
+                ll_push_scal(a, par, 1, w2, 2, ep);
+            }
+            // the flag protocol also at the solve's last step: k_end tests it from G_r
+            if (a.peer && (!llx || i == (long long)st->maxit)) {
                 for (int g = 0; g < L.P; ++g) {
                     a.pp.G_r[g][ro + L.pslot + 0] = rv[0];
                     a.pp.G_r[g][ro + L.pslot + 1] = rv[1];
                 }
                 flags_out(a, kPhaseR, i);
-            } else {
+            } else if (!a.peer) {
                 a.G_r[ro + L.pslot + 0] = rv[0];
                 a.G_r[ro + L.pslot + 1] = rv[1];
             }

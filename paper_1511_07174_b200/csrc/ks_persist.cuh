@@ -100,6 +100,74 @@ __device__ __forceinline__ void flags_out(const VecArgsT<T>& a, int ph, long lon
     publish_flags(f, a.L.P, epoch_of(a.st, k));
 }
 
+// ---- LL handovers over P > 1 GPUs (KS_OPT_LL_XCHG; layout: ks_internal.h ll_*) ----
+// One value = two 8-byte words, each 32 payload bits + the 32-bit epoch, written with
+// one 16-byte system-scope store into every rank's region; a reader polls its local
+// copy until both words carry the epoch.  Each 8-byte word is single-copy atomic, so a
+// matching pair is the value: no fence on the producer side, no flag.  Values travel
+// as double (exact for float).
+__device__ __forceinline__ void ll_put_sys(uint64_t* slot, double v, uint32_t ep) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(v);
+    const uint64_t lo = (bits & 0xffffffffull) | ((uint64_t)ep << 32);
+    const uint64_t hi = (bits >> 32) | ((uint64_t)ep << 32);
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(lo), "l"(hi) : "memory");
+}
+// Polls one value (bounded: false after kWaitTimeoutNs -- a lost peer).
+__device__ __forceinline__ bool ll_get_sys(const uint64_t* slot, uint32_t ep, double& v) {
+    unsigned long long t0 = 0;
+    for (int spin = 0;; ++spin) {
+        uint64_t lo, hi;
+        asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(slot) : "memory");
+        if ((uint32_t)(lo >> 32) == ep && (uint32_t)(hi >> 32) == ep) {
+            v = __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
+            return true;
+        }
+        if ((spin & 63) == 63) {
+            if (t0 == 0) t0 = globaltimer_ns();
+            else if (globaltimer_ns() - t0 > kWaitTimeoutNs) return false;
+        }
+    }
+}
+__device__ __forceinline__ uint32_t ll_epoch(const DevState* st, long long k) { return (uint32_t)epoch_of(st, k); }
+// Rank-partial all-reduce of K scalars of LL phase ph: the lead CTA pushed its rank's
+// values (ll_push_scal); every CTA polls the P x K words (thread g * K + q) and sums
+// them in rank order (the order scal_sum / slot_sum use), so every thread of every
+// CTA of every rank ends with the same bits.  False (all threads) on a timeout.
+template <class T>
+__device__ __forceinline__ void ll_push_scal(const VecArgsT<T>& a, int par, int ph, const double* v, int K,
+                                             uint32_t ep) {
+    jitter_at(a.jitter, 8u);
+    for (int g = 0; g < a.L.P; ++g)
+        for (int q = 0; q < K; ++q) ll_put_sys(a.pp.llg[g] + ll_scal_off(a.L.ld, par, ph, a.L.rank, q), v[q], ep);
+}
+template <int K, class T>
+__device__ __forceinline__ bool ll_sum_scal(const VecArgsT<T>& a, int par, int ph, uint32_t ep, T (&out)[K]) {
+    __shared__ double s_v[kMaxRanks * 2];
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) s_ok = 1;
+    __syncthreads();
+    const int P = a.L.P;
+    if ((int)threadIdx.x < P * K) {
+        jitter_at(a.jitter, 9u);
+        const int g = threadIdx.x / K, q = threadIdx.x % K;
+        double v = 0.0;
+        if (!ll_get_sys(a.llg + ll_scal_off(a.L.ld, par, ph, g, q), ep, v)) s_ok = 0;
+        s_v[g * K + q] = v;
+    }
+    __syncthreads();
+    if (!s_ok) {
+        if (threadIdx.x == 0) { a.st->peer_timeout = 1; a.st->status = KS_ENCCL; a.st->done = 1; }
+        return false;
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        T t = T(0);
+        for (int g = 0; g < P; ++g) t += (T)s_v[g * K + q];
+        out[q] = t;
+    }
+    return true;
+}
+
 template <class T>
 struct PersistArgs {
     VecArgsT<T> a;

@@ -210,6 +210,47 @@ def test_multi_persistent_fused(lay):
     bars(xc, hc, rc, xo, ho, ro)
 
 
+@pytest.mark.parametrize("lay", layouts(shared=()))
+def test_ll_handovers_bitwise_equal_flags(lay):
+    """KS_OPT_LL_XCHG: the persistent kernels over P GPUs hand the r / v slices and the
+    rank partials over as LL words (no fence, no flag) instead of stores + fence + epoch
+    flag; the same values are summed in the same order, so x, the history and the
+    iteration count must be bitwise identical in both modes -- single- and multi-launch
+    (poll batch), x0, fixed length (the last step's test in k_end), CG and BiCGSTAB --
+    and meet the bars vs the oracle."""
+    P = need(lay)
+    n = 4100
+    D, bd = synth.gdd(n, 16)
+    Cs, cs, bs = synth.gspd(4096, 1e4)
+    x0 = np.random.default_rng(P).standard_normal(n)
+    with context(n, lay) as ctx, context(4096, lay) as cc:
+        ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
+        res = {}
+        for ll in (0, 1):
+            for batch in (0, 5):
+                for cx in (ctx, cc):
+                    cx.set_option("persistent", 1)
+                    cx.set_option("small", 0)
+                    cx.set_option("ll_xchg", ll)
+                    cx.set_option("poll_batch", batch)
+                    assert cx.get_option("ll_xchg") == ll
+                res[(ll, batch)] = (ctx.bicgstab(bd, tol=1e-10), cc.cg(bs, tol=1e-10),
+                                    ctx.bicgstab(bd, x0=x0, tol=0.0, maxit=13),
+                                    cc.cg(bs, x0=x0[:4096], tol=0.0, maxit=17))
+        ref = res[(0, 0)]
+        for key, val in res.items():
+            for (x, h, r), (xr, hr, rr) in zip(val, ref):
+                assert r.iterations == rr.iterations and r.status == rr.status, key
+                assert np.array_equal(x, xr) and np.array_equal(h, hr), key
+    xo, ho, ro = oracle.bicgstab(D, bd, tol=1e-10)
+    x, h, r = ref[0]
+    bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+    xo, ho, ro = oracle.cg(Cs, bs, tol=1e-10)
+    x, h, r = ref[1]
+    bars(x, h, r, xo, ho, ro)
+
+
 @pytest.mark.parametrize("lay", layouts())
 @pytest.mark.parametrize("fused", [1, 0])
 def test_multi_bicg(lay, fused):

@@ -12,3 +12,4 @@ for P in 2 4; do
   python -c "import json;d=json.loads(open('$O/bench_p$P.json').read().strip().splitlines()[-1]);print($P, d['n_gpus'], d['value'], d['e2e']['value'], d['roofline']['frac'], d['clocks'])"
 done
 timeout 600 python tools/soak.py 4 200 > $O/soak_p4.json 2> $O/soak_p4.err; echo "soak4 rc=$?"; tail -c 300 $O/soak_p4.json
+timeout 900 python tools/ll_ab.py > $O/ll_ab.jsonl 2> $O/ll_ab.err; echo "ll_ab rc=$?"; cat $O/ll_ab.jsonl
