@@ -188,14 +188,20 @@ __device__ void gemm_phase(const CUtensorMap* tmA, const CUtensorMap* tmP, const
     }
 }
 
-// CTA-order totals of K partial slots (q0 .. q0 + K - 1 of kSlotsM per CTA).
+// Per-CTA partial slots: kBSlots * K doubles per CTA.  Phases whose partials are
+// written without a grid barrier after the previous phase's totals were read use
+// disjoint slots: BiCGSTAB's B4 (||s||^2) -> [K, 2K), B6 (<t,s>, <t,t>) -> [2K, 4K),
+// B7 (<rhat,r>, <r,r>) -> [4K, 6K) -- with shared slots a fast CTA's B6 / B7 partials
+// could overwrite a slot a slow CTA was still summing (found by KS_OPT_JITTER).
+constexpr int kBSlots = 6;
+// CTA-order totals of K partial slots (q0 .. q0 + K - 1 of the kBSlots * K per CTA).
 template <int K>
 __device__ __forceinline__ void totals(const double* bpart, int q0, double (&out)[K], double* red) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         double acc = 0.0;
         if (threadIdx.x < kMCT)
-            for (int b = threadIdx.x; b < (int)gridDim.x; b += kMCT) acc += __ldcg(bpart + (int64_t)b * 2 * K + q0 + k);
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += kMCT) acc += __ldcg(bpart + (int64_t)b * kBSlots * K + q0 + k);
         out[k] = acc;
     }
     csum<K>(out, red);
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
         csum<2 * K>(v, S.red);
         if (tid == 0) {
 #pragma unroll
-            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v[k];
+            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * kBSlots * K + k] = v[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
         double tbr[2 * K];
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
             for (int k = 0; k < K; ++k) {
                 double s = 0.0;
                 for (int ww = 0; ww < kMW; ++ww) s += S.wpart[ww][k];
-                M.bpart[(int64_t)blockIdx.x * 2 * K + k] = s;
+                M.bpart[(int64_t)blockIdx.x * kBSlots * K + k] = s;
             }
         }
         if (!pk::grid_sync(M.bar, st)) return;
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(kMT, 1) k_cgm(const __grid_constant__ CUtensor
         csum<K>(rr, S.red);
         if (tid == 0) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + K + k] = rr[k];
+            for (int k = 0; k < K; ++k) M.bpart[(int64_t)blockIdx.x * kBSlots * K + K + k] = rr[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
         // A4 + A5: rho' (rank all-reduce; releases the pushed r slices too), test, beta,
@@ -588,7 +594,7 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
         csum<2 * K>(v, S.red);
         if (tid == 0) {
 #pragma unroll
-            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v[k];
+            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * kBSlots * K + k] = v[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
         double tbr[2 * K];
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
             for (int k = 0; k < K; ++k) {
                 double t = 0.0;
                 for (int ww = 0; ww < kMW; ++ww) t += S.wpart[ww][k];
-                M.bpart[(int64_t)blockIdx.x * 2 * K + k] = t;
+                M.bpart[(int64_t)blockIdx.x * kBSlots * K + k] = t;
             }
         }
         if (!pk::grid_sync(M.bar, st)) return;
@@ -721,7 +727,7 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
         csum<K>(ssp, S.red);
         if (tid == 0) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + K + k] = ssp[k];
+            for (int k = 0; k < K; ++k) M.bpart[(int64_t)blockIdx.x * kBSlots * K + K + k] = ssp[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
         double ss[K];
@@ -762,16 +768,16 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
             for (int k = 0; k < K; ++k) {
                 double a1 = 0.0, a2 = 0.0;
                 for (int ww = 0; ww < kMW; ++ww) { a1 += S.wpart[ww][k]; a2 += S.wpart2[ww][k]; }
-                M.bpart[(int64_t)blockIdx.x * 2 * K + k] = a1;
-                M.bpart[(int64_t)blockIdx.x * 2 * K + K + k] = a2;
+                M.bpart[(int64_t)blockIdx.x * kBSlots * K + 2 * K + k] = a1;
+                M.bpart[(int64_t)blockIdx.x * kBSlots * K + 3 * K + k] = a2;
             }
         }
         if (!pk::grid_sync(M.bar, st)) return;
         double tst[2 * K];
         {
             double ts[K], tt[K];
-            totals<K>(M.bpart, 0, ts, S.red);
-            totals<K>(M.bpart, K, tt, S.red);
+            totals<K>(M.bpart, 2 * K, ts, S.red);
+            totals<K>(M.bpart, 3 * K, tt, S.red);
 #pragma unroll
             for (int k = 0; k < K; ++k) { tst[k] = ts[k]; tst[K + k] = tt[k]; }
         }
@@ -814,14 +820,14 @@ __global__ void __launch_bounds__(kMT, 1) k_bsm(const __grid_constant__ CUtensor
         csum<2 * K>(v2, S.red);
         if (tid == 0) {
 #pragma unroll
-            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * 2 * K + k] = v2[k];
+            for (int k = 0; k < 2 * K; ++k) M.bpart[(int64_t)blockIdx.x * kBSlots * K + 4 * K + k] = v2[k];
         }
         if (!pk::grid_sync(M.bar, st)) return;
         double rr2[2 * K];
         {
             double rhn[K], rr[K];
-            totals<K>(M.bpart, 0, rhn, S.red);
-            totals<K>(M.bpart, K, rr, S.red);
+            totals<K>(M.bpart, 4 * K, rhn, S.red);
+            totals<K>(M.bpart, 5 * K, rr, S.red);
 #pragma unroll
             for (int k = 0; k < K; ++k) { rr2[k] = rhn[k]; rr2[K + k] = rr[k]; }
         }
