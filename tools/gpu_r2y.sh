@@ -7,6 +7,8 @@ mkdir -p $O
 nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm --format=csv > $O/gpu.txt
 timeout 2700 python -m pytest tests -m gpu -q --timeout 900 --tb=short -p no:cacheprovider > $O/pytest_gpu4.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu4.log
 tail -5 $O/pytest_gpu4.log
+CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py > $O/bench_p1.json 2> $O/bench_p1.err; echo "bench p1 rc=$?"
+python -c "import json;d=json.loads(open('$O/bench_p1.json').read().strip().splitlines()[-1]);print(1, d['value'], d['e2e']['value'], d['roofline']['frac'], d['clocks'], json.dumps(d.get('extras', {}).get('c1_latency')))"
 for P in 2 4; do
   timeout 600 python bench.py --gpus $P > $O/bench_p$P.json 2> $O/bench_p$P.err; echo "bench p$P rc=$?"
   python -c "import json;d=json.loads(open('$O/bench_p$P.json').read().strip().splitlines()[-1]);print($P, d['n_gpus'], d['value'], d['e2e']['value'], d['roofline']['frac'], d['clocks'])"
