@@ -165,9 +165,9 @@ void rank_alloc(ks_ctx* c, Rank& r) {
 }
 
 // Buffers replaced while a call runs are freed at the start of the next call (or at
-// destroy), never inside it: cudaFree synchronises the whole device, and on a GPU
-// shared by several ranks of one context that would wait on a peer's kernel that
-// spins for this rank's not-yet-launched work.
+// destroy), never inside it: cudaFree synchronises the whole device, so inside a call
+// it can wait on a kernel that spins for a peer rank's not-yet-launched work (found
+// with ranks sharing a GPU, §15.7).
 void retire(Rank& r, void* p) {
     if (p) r.retired.push_back(p);
 }
@@ -263,6 +263,23 @@ void host_collective(const ks_ctx* c, Rank& r, F&& pull) {
 }
 
 }  // namespace
+
+// Ranks sharing one GPU: rank 0 runs `launch` once on its stream after every rank's
+// stream reached this point (events), and every rank's stream continues after it --
+// a single launch may then serve all ranks (their kernels wait on each other, so
+// they must be ONE launch to be co-resident).
+void host_launch_once(const ks_ctx* c, Rank& r, const std::function<void()>& launch) {
+    KS_CUDA(cudaEventRecord(r.ev_coll[0], r.stream));
+    c->hbar->wait();
+    if (r.rank == 0) {
+        for (const Rank& h : c->ranks)
+            if (h.rank != 0) KS_CUDA(cudaStreamWaitEvent(r.stream, h.ev_coll[0], 0));
+        launch();
+        KS_CUDA(cudaEventRecord(r.ev_coll[1], r.stream));
+    }
+    c->hbar->wait();
+    if (r.rank != 0) KS_CUDA(cudaStreamWaitEvent(r.stream, c->ranks[0].ev_coll[1], 0));
+}
 
 // In-place allgather of one chunk per rank (count_per_rank doubles at G + rank*chunk).
 // G is one of the exchange regions (G_r, G_v, S) of this rank's exchange allocation.

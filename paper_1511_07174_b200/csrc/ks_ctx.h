@@ -216,6 +216,7 @@ void retire(Rank& r, void* p);     // free at the start of the next call (no cud
 void flush_retired(Rank& r);
 void setup_peers(ks_ctx* c);   // peer access / CUDA IPC of the exchange buffers
 void allgather(const ks_ctx* c, Rank& r, double* G, int64_t count_per_rank);   // dtype-aware
+void host_launch_once(const ks_ctx* c, Rank& r, const std::function<void()>& launch);   // shared GPU
 void copy_chunks_to(const ks_ctx* c, Rank& r, const double* G, double* dst, cudaMemcpyKind kind);
 int64_t run_f32(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, int64_t maxit,
                 double* x, double* hist, int64_t hist_cap, ks_report* rep);

@@ -302,8 +302,15 @@ int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_
 // P > 1 (fused exchange): the LL words go over NVLink into every rank's buffer (llp,
 // a region of the exchange allocation), x0f = the full x0 or NULL.  m = this rank's rows.
 int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t m, int64_t ld);
+// the emulated-rank tiny launch of `blocks` CTAs is co-resident on one GPU
+bool tiny_emu_fits(int bicgstab, int64_t lda, int blocks, int num_sms);
 int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll,
                 uint64_t* const* llp, const double* x0f, int grid, cudaStream_t st);
+// Ranks sharing one GPU: every rank's tiny kernel as one cooperative launch of P * g
+// CTAs (rank h = block / g); a[h] / A[h] / ll[h] / llp[h] are rank h's arguments.  The
+// lead CTA of each rank also writes the full x into that rank's X.
+int launch_tiny_emu(int bicgstab, const VecArgs* const* a, const double* const* A, int64_t lda,
+                    uint64_t* const* ll, uint64_t* const* const* llp, int P, int g, cudaStream_t st);
 
 // Multi-RHS CG (ks_multi.cu, SURVEY.md sec.8(f) "multi-RHS"): K <= kMaxRhs independent
 // CG recurrences sharing every pass over A (one GPU, FP64).  Per-column state:

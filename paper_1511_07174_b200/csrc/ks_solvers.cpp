@@ -295,13 +295,15 @@ void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_c
 // call, no extra launch).  One stream synchronisation when the history is short.
 void finish_and_copy(ks_ctx* c, Rank& r, double* x, double* hist, int64_t hist_cap,
                      ks_report* rep, bool bicgstab, const Clock::time_point& t_start, int64_t maxit,
-                     int end_mode = 0, unsigned long long x_epoch = 0) {
+                     int end_mode = 0, unsigned long long x_epoch = 0, bool x_ready = false) {
     VecArgs a = r.vargs(false);   // final x gather / true residual: NCCL, parity 0
     const bool fused_x = end_mode == 1 && c->P > 1 && c->fused();
     if (end_mode == 1) r.launches += launch_end(r.vargs(c->fused()), bicgstab ? 1 : 0, fused_x ? 1 : 0,
                                                 x_epoch, r.stream);
-    const double* xsrc = c->P == 1 ? r.x_loc : fused_x ? r.X : nullptr;   // contiguous full x
-    if (c->P > 1 && !fused_x) {
+    // contiguous full x: P == 1 x_loc; fused: gathered into X by k_end; x_ready: the
+    // emulated-rank tiny kernels wrote it into X
+    const double* xsrc = c->P == 1 ? r.x_loc : (fused_x || x_ready) ? r.X : nullptr;
+    if (c->P > 1 && !fused_x && !x_ready) {
         r.launches += launch_pack_x(a, r.stream);
         allgather(c, r, r.G_v, r.L.chunk);
     }
@@ -400,8 +402,73 @@ void fuse_gemv(const ks_ctx* c, const Rank& r, GemvParams& p, int phase, double*
     p.ebase = &r.st->ebase;
 }
 
+// Ranks sharing one GPU, n <= 1024, x0 = 0, the whole solve in one launch: the tiny
+// kernels of all ranks as ONE cooperative launch (their LL exchange between ranks is
+// the fused exchange's; one launch makes the waiting CTAs co-resident).  Returns the
+// per-rank CTA count, 0 when not applicable (then the host-collective schedule runs);
+// depends only on context state, so every rank decides the same.
+int tiny_emu_grid(const ks_ctx* c, int bicgstab, int64_t maxit) {
+    if (!c->shared_dev || c->P < 2 || c->dtype != KS_FLOAT64) return 0;
+    if (!c->opt.tiny || c->opt.small == 0 || c->opt.persistent == 0) return 0;
+    if (c->opt.poll_batch > 0 && c->opt.poll_batch < maxit) return 0;
+    for (const auto& h : c->ranks)
+        if (h.dev != c->ranks[0].dev || !h.llx) return 0;
+    const Rank& r0 = c->ranks[0];                  // the first ranks hold the extra rows
+    const int g = tiny_grid(bicgstab, r0.num_sms, c->n, r0.m, c->ld);
+    if (g == 0 || !tiny_emu_fits(bicgstab, c->ld, c->P * g, r0.num_sms)) return 0;
+    return g;
+}
+
+int64_t run_tiny_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, int64_t maxit,
+                     double* x, double* hist, int64_t hist_cap, ks_report* rep, int g) {
+    const auto t_start = Clock::now();
+    r.launches = 0;
+    r.gemv_launches = 0;
+    r.gemv_seconds = 0.0;
+    ensure_hist(r, hist_cap);
+    const unsigned long long ebase = r.epoch_next;
+    r.epoch_next += (unsigned long long)maxit + 2;
+    r.x0_full = nullptr;
+    KS_CUDA(cudaMemcpyAsync(r.b_full, b, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
+    // rows A0 / B0 + state init in the fused layout; no rendezvous (no cross-launch wait)
+    r.launches += launch_start(r.vargs(true), bicgstab, tol, maxit, hist_cap, ebase, 0, r.stream);
+    r.bar_zeroed = true;
+    KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+    host_launch_once(c, r, [&] {
+        VecArgs va[kMaxRanks];
+        const VecArgs* av[kMaxRanks];
+        const double* Av[kMaxRanks];
+        uint64_t* llv[kMaxRanks];
+        uint64_t* const* llpv[kMaxRanks];
+        for (int h = 0; h < c->P; ++h) {
+            const Rank& rh = c->ranks[(size_t)h];
+            va[h] = rh.vargs(true);
+            av[h] = &va[h];
+            Av[h] = rh.A;
+            llv[h] = rh.llx;
+            llpv[h] = rh.llpeer;
+        }
+        const int rc = launch_tiny_emu(bicgstab, av, Av, c->ld, llv, llpv, c->P, g, r.stream);
+        if (rc < 0) KS_CUDA((cudaError_t)(-rc));
+        r.launches += 1;
+    });
+    r.bar_zeroed = false;
+    r.gemv_launches = 0;
+    KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    finish_and_copy(c, r, x, hist, hist_cap, rep, bicgstab != 0, t_start, maxit, 1,
+                    ebase + (unsigned long long)maxit + 1, true);
+    r.gemv_launches = bicgstab ? 2 * r.h_state->iters - (r.h_state->half ? 1 : 0) : r.h_state->iters;
+    if (rep) rep->gemv_launches = r.gemv_launches;
+    return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
+}
+
 int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
                double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    if (!x0)
+        if (const int g = tiny_emu_grid(c, 0, maxit)) {
+            check_loaded(c, r);
+            return run_tiny_emu(c, r, 0, b, tol, maxit, x, hist, hist_cap, rep, g);
+        }
     const auto t_start = Clock::now();
     check_loaded(c, r);
     r.launches = 0;
@@ -444,6 +511,11 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
 
 int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,
                      int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep) {
+    if (!x0)
+        if (const int g = tiny_emu_grid(c, 1, maxit)) {
+            check_loaded(c, r);
+            return run_tiny_emu(c, r, 1, b, tol, maxit, x, hist, hist_cap, rep, g);
+        }
     const auto t_start = Clock::now();
     check_loaded(c, r);
     r.launches = 0;

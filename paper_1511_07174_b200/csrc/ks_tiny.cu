@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "ks_device.cuh"
@@ -327,6 +328,15 @@ struct TinyArgs {
     long long trace_k;
     unsigned backoff;    // ns of __nanosleep after an unsuccessful LL poll round (0: spin)
     int wide;            // 1: one 256-bit load per column pair and poll round (0: two 128-bit)
+    int xfull;           // 1: the lead CTA also writes the full x into the rank's X (emulated ranks)
+};
+// Ranks sharing one GPU (ks_create_on): all ranks' CTAs in ONE cooperative launch --
+// CTA b serves rank b / g as its block b % g -- so the CTAs that wait on each other's
+// LL words are co-resident by construction (separate launches would not be).
+constexpr int kMaxEmu = 8;
+struct TinyEmuArgs {
+    TinyArgs t[kMaxEmu];
+    int P, g;
 };
 constexpr int kTrace = 8;
 __device__ __forceinline__ void stamp(const TinyArgs& T, long long k, int i) {
@@ -338,9 +348,10 @@ __device__ __forceinline__ void stamp(const TinyArgs& T, long long k, int i) {
     }
 }
 
-// This CTA's rows [rb, rb + R) of the rank's m rows: balanced contiguous blocks.
-__device__ __forceinline__ void my_rows(int n, int& rb, int& R) {
-    const int q = n / (int)gridDim.x, rem = n % (int)gridDim.x, b = (int)blockIdx.x;
+// This CTA's rows [rb, rb + R) of the rank's m rows: balanced contiguous blocks over
+// the rank's vg CTAs (vb = this CTA's index among them).
+__device__ __forceinline__ void my_rows(int n, int& rb, int& R, int vb, int vg) {
+    const int q = n / vg, rem = n % vg, b = vb;
     rb = b * q + min(b, rem);
     R = q + (b < rem ? 1 : 0);
 }
@@ -360,19 +371,23 @@ __device__ __forceinline__ void ll_publish(const TinyArgs& T, int64_t off, int64
 
 // ------------------------------------------------------------------ CG (A1-A5)
 template <int V, int XM>
-__global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
+__device__ __forceinline__ void cg_tiny_body(const TinyArgs& T, int vb, int vg) {
     __shared__ double wred[kRM * kTW];
     __shared__ double red[2 * 2 * kTW];
     int par = 0;
     const VecArgs& a = T.a;
     DevState* st = a.st;
     const int n = (int)a.L.n;
-    if (is_done(st)) return;
+    if (is_done(st)) {                               // 0-iteration exit: x = x0 = 0
+        if (T.xfull && vb == 0)
+            for (int j = threadIdx.x; j < n; j += kTT) a.X[j] = 0.0;
+        return;
+    }
     const int P = a.L.P, m = (int)rows_of(a.L);
     const int64_t row0 = a.L.row0[a.L.rank];
     const int wide = P > 1 ? 2 : T.wide;           // P > 1: system-scope polls of the LL words
     int rb, R;
-    my_rows(m, rb, R);
+    my_rows(m, rb, R, vb, vg);
     double Ar[kRM][V];
     load_rows_reg<V>(T.A, T.lda, rb, R, Ar);
     double x[V], r[V], p[V];
@@ -388,7 +403,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
     const double nb = st->nb, tol = st->tol;
     const long long maxit = st->maxit;
     const unsigned long long eb = st->ebase;
-    const bool lead0 = blockIdx.x == 0;
+    const bool lead0 = vb == 0;
     long long k = 1;
     int status = KS_EMAXIT, conv = 0;
     long long iters = maxit;
@@ -455,6 +470,7 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
             if (j >= row0 && j < row0 + m) a.x_loc[j - row0] = x[v];      // own rows
             if (j < n) a.p_full[j] = p[v];
             if (P == 1 && j < n) a.G_r[j] = r[v];
+            if (T.xfull && j < n) a.X[j] = x[v];                           // emulated ranks: full x
         }
         if (threadIdx.x == 0) {
             st->iters = iters; st->status = status; st->converged = conv;
@@ -466,19 +482,23 @@ __global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
 
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
 template <int V, int XM>
-__global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
+__device__ __forceinline__ void bs_tiny_body(const TinyArgs& T, int vb, int vg) {
     __shared__ double wred[(kRM + 1) * kTW];
     __shared__ double red[2 * 2 * kTW];
     int par = 0;
     const VecArgs& a = T.a;
     DevState* st = a.st;
     const int n = (int)a.L.n;
-    if (is_done(st)) return;
+    if (is_done(st)) {                               // 0-iteration exit: x = x0 = 0
+        if (T.xfull && vb == 0)
+            for (int j = threadIdx.x; j < n; j += kTT) a.X[j] = 0.0;
+        return;
+    }
     const int P = a.L.P, m = (int)rows_of(a.L);
     const int64_t row0 = a.L.row0[a.L.rank];
     const int wide = P > 1 ? 2 : T.wide;           // P > 1: system-scope polls of the LL words
     int rb, R;
-    my_rows(m, rb, R);
+    my_rows(m, rb, R, vb, vg);
     double Ar[kRM][V];
     load_rows_reg<V>(T.A, T.lda, rb, R, Ar);
     double x[V], r[V], p[V], v_[V], rh[V];
@@ -495,7 +515,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
     const double nb = st->nb, tol = st->tol;
     const long long maxit = st->maxit;
     const unsigned long long eb = st->ebase;
-    const bool lead0 = blockIdx.x == 0;
+    const bool lead0 = vb == 0;
     double rho = slot_sum(a.L, a.G_r, 0);     // rho_1 = <rhat, r0>
     double rho_old = 1.0, alpha = 1.0, omega = 1.0;
     int status = KS_EMAXIT, conv = 0, brk = 0, half = 0;
@@ -604,6 +624,7 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
             if (j >= row0 && j < row0 + m) a.x_loc[j - row0] = x[v];      // own rows
             if (j < n) { a.p_full[j] = p[v]; a.v_full[j] = v_[v]; }
             if (P == 1 && j < n) a.G_r[j] = r[v];
+            if (T.xfull && j < n) a.X[j] = x[v];                           // emulated ranks: full x
         }
         if (threadIdx.x == 0) {
             st->iters = iters; st->status = status; st->converged = conv; st->breakdown = brk;
@@ -612,6 +633,25 @@ __global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
             st->done = 1;
         }
     }
+}
+
+template <int V, int XM>
+__global__ void __launch_bounds__(kTT, 1) k_cg_tiny(TinyArgs T) {
+    cg_tiny_body<V, XM>(T, (int)blockIdx.x, (int)gridDim.x);
+}
+template <int V, int XM>
+__global__ void __launch_bounds__(kTT, 1) k_bs_tiny(TinyArgs T) {
+    bs_tiny_body<V, XM>(T, (int)blockIdx.x, (int)gridDim.x);
+}
+template <int V>
+__global__ void __launch_bounds__(kTT, 1) k_cg_tiny_emu(const __grid_constant__ TinyEmuArgs E) {
+    const int rk = (int)blockIdx.x / E.g;
+    cg_tiny_body<V, 0>(E.t[rk], (int)blockIdx.x - rk * E.g, E.g);
+}
+template <int V>
+__global__ void __launch_bounds__(kTT, 1) k_bs_tiny_emu(const __grid_constant__ TinyEmuArgs E) {
+    const int rk = (int)blockIdx.x / E.g;
+    bs_tiny_body<V, 0>(E.t[rk], (int)blockIdx.x - rk * E.g, E.g);
 }
 
 template <int V, int XM>
@@ -671,6 +711,7 @@ int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, ui
     if (const char* bo = std::getenv("KS_TINY_BACKOFF")) T.backoff = (unsigned)std::atoi(bo);   // tuning
     T.wide = 1;
     if (const char* wd = std::getenv("KS_TINY_WIDE")) T.wide = std::atoi(wd) != 0;               // tuning
+    T.xfull = 0;
     const char* tr = bicgstab ? nullptr : std::getenv("KS_TINY_TRACE");   // debug facility
     if (tr) {
         T.trace_k = std::atoll(tr);
@@ -697,6 +738,48 @@ int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, ui
             std::fclose(f);
         }
     }
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+bool tiny_emu_fits(int bicgstab, int64_t lda, int blocks, int num_sms) {
+    if (blocks < 1 || lda > 1024) return false;
+    const int V = lda <= 512 ? 2 : 4;
+    const void* k = bicgstab ? (V == 2 ? (const void*)k_bs_tiny_emu<2> : (const void*)k_bs_tiny_emu<4>)
+                             : (V == 2 ? (const void*)k_cg_tiny_emu<2> : (const void*)k_cg_tiny_emu<4>);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTT, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return (int64_t)per_sm * num_sms >= blocks;
+}
+
+int launch_tiny_emu(int bicgstab, const VecArgs* const* a, const double* const* A, int64_t lda,
+                    uint64_t* const* ll, uint64_t* const* const* llp, int P, int g, cudaStream_t st) {
+    if (P < 2 || P > kMaxEmu || g < 1) return -(int)cudaErrorInvalidValue;
+    TinyEmuArgs E;
+    std::memset(&E, 0, sizeof E);
+    for (int h = 0; h < P; ++h) {
+        TinyArgs& T = E.t[h];
+        T.a = *a[h];
+        T.A = A[h];
+        T.lda = lda;
+        T.ll = ll[h];
+        for (int q = 0; q < kMaxRanks; ++q) T.llp[q] = q < P ? llp[h][q] : nullptr;
+        T.x0f = nullptr;
+        T.trace = nullptr;
+        T.trace_k = 0;
+        T.backoff = 0;
+        T.wide = 2;
+        T.xfull = 1;
+    }
+    E.P = P;
+    E.g = g;
+    const int V = lda <= 512 ? 2 : 4;
+    const void* k = bicgstab ? (V == 2 ? (const void*)k_bs_tiny_emu<2> : (const void*)k_bs_tiny_emu<4>)
+                             : (V == 2 ? (const void*)k_cg_tiny_emu<2> : (const void*)k_cg_tiny_emu<4>);
+    void* args[] = {&E};
+    const cudaError_t e = cudaLaunchCooperativeKernel(k, dim3((unsigned)(P * g)), dim3(kTT), args, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 

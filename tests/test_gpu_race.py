@@ -86,7 +86,8 @@ def test_race_cg_bicgstab(lay, path):
     assert P >= 1
 
 
-@pytest.mark.parametrize("lay", LAYS)
+@pytest.mark.parametrize("lay", LAYS + [pytest.param(("shared", 2), id="shared2"),
+                                        pytest.param(("shared", 4), id="shared4")])
 def test_race_tiny(lay):
     need(lay)
     n = 1000
