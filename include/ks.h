@@ -185,9 +185,12 @@ ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
  * runs kernels that wait on each other (separate launches on one GPU have no
  * co-residency guarantee): its collectives are host-driven peer copies ordered by
  * events, KS_OPT_FUSED_COMM is 0 and cannot be set, and the kernels that need the
- * fused exchange at P > 1 (persistent, small-n, tiny, multi-RHS) are not used.
- * Results equal the oracle's within the same bars; they are not bitwise those of
- * the fused path.  KS_EARG for a bad device list, KS_EDIM for n < nranks.        */
+ * fused exchange at P > 1 (persistent, small-n, multi-RHS) are not used.  Exception:
+ * with every rank on one GPU, CG / BiCGSTAB at n <= 1024 with x0 = NULL run the tiny
+ * kernels of all ranks as ONE cooperative launch (rank = block / CTAs per rank), so
+ * their LL exchange between ranks runs with co-residency guaranteed -- bitwise the
+ * one-GPU result.  Otherwise results equal the oracle's within the same bars.
+ * KS_EARG for a bad device list, KS_EDIM for n < nranks.                         */
 ks_status ks_create_on(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t nranks, const int32_t* devices);
 
 /* One rank of a multi-process job (one process per GPU, e.g. torchrun) -- the
