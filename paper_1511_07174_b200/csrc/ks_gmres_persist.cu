@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(kNT, 4) k_gm_cycle(GPArgs A) {
         if (!grid_sync(A.P.bar, st)) return;
     }
     double d1, d2;
-    gemv_phase<kR, kU>(A.P, a.s_full, a.q_loc, (const double*)nullptr, d1, d2, red, a.b_full + L.row0[L.rank]);
+    gemv_phase<kR, kU>(A.P, a.s_full, a.q_loc, (const double*)nullptr, d1, d2, red, a.b_full + L.row0[L.rank],
+                       (int)blockIdx.x, (int)gridDim.x);
     if (threadIdx.x == 0) A.P.bpart[blockIdx.x * 4 + 1] = d2;
     if (!grid_sync(A.P.bar, st)) return;
     double bt[1];
@@ -183,7 +184,8 @@ __global__ void __launch_bounds__(kNT, 4) k_gm_cycle(GPArgs A) {
     for (int j = 0; j < g.mres && k < maxit; ++j) {
         const unsigned long long sj = sq0 + 3 + 4ull * (unsigned long long)j;
         const int nv = j + 1;
-        gemv_phase<kR, kU>(A.P, a.p_full, a.q_loc, (const double*)nullptr, d1, d2, red);   // w = A v_j
+        gemv_phase<kR, kU>(A.P, a.p_full, a.q_loc, (const double*)nullptr, d1, d2, red, (const double*)nullptr, (int)blockIdx.x,
+                           (int)gridDim.x);   // w = A v_j
         if (!grid_sync(A.P.bar, st)) return;
         cta_dots(g, a.q_loc, m, nv, red);                                 // CGS pass 1
         if (!grid_sync(A.P.bar, st)) return;

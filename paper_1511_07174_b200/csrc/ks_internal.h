@@ -302,6 +302,13 @@ int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_
 // P > 1 (fused exchange): the LL words go over NVLink into every rank's buffer (llp,
 // a region of the exchange allocation), x0f = the full x0 or NULL.  m = this rank's rows.
 int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t m, int64_t ld);
+// Ranks sharing one GPU: every rank's persistent CG / BiCGSTAB kernel (FP64) as one
+// cooperative launch of P * g CTAs (rank h = block / g, arguments a[h], A[h], bpart[h],
+// bar[h]); persist_emu_grid = the per-rank CTA count for num_sms / P SMs, 0 = n/a.
+int persist_emu_grid(int bicgstab, int num_sms, int P, int64_t mmax, int rows, int unroll);
+int launch_persist_emu(int bicgstab, const VecArgs* const* a, const double* const* A, int64_t lda, int64_t ncols,
+                       double* const* bpart, unsigned* const* bar, long long k0, long long k1, int P, int g,
+                       int rows, int unroll, cudaStream_t st);
 // the emulated-rank tiny launch of `blocks` CTAs is co-resident on one GPU
 bool tiny_emu_fits(int bicgstab, int64_t lda, int blocks, int num_sms);
 int launch_tiny(int bicgstab, const VecArgs& a, const double* A, int64_t lda, uint64_t* ll,

@@ -15,6 +15,7 @@
 // to every rank and flagged; v is pulled.
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <cstring>
 #include <math.h>
 #include <stdint.h>
 
@@ -30,34 +31,34 @@ namespace {
 using namespace pk;
 
 // ---------------------------------------------------------------- CG (A1-A5)
-template <class T, int kR, int kU, int kMinB = 4>
-__global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
+template <class T, int kR, int kU>
+__device__ __forceinline__ void cg_persist_body(const PersistArgs<T>& P, int vb, int vg) {
     __shared__ T red[(kR > 2 ? kR : 2) * kNW];
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
     const int64_t m = rows_of(L), r0 = L.row0[L.rank];
-    const int64_t gstride = (int64_t)gridDim.x * kNT;
-    const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
+    const int64_t gstride = (int64_t)vg * kNT;
+    const int64_t tid0 = (int64_t)vb * kNT + threadIdx.x;
     for (long long k = P.k0; k <= P.k1; ++k) {
         if (is_done(st)) break;
         // A1: q = A p, sigma_g = <p_loc, q>
         T d1, d2;
-        gemv_phase<kR, kU>(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red);
-        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
-        if (!grid_sync(P.bar, st)) return;
+        gemv_phase<kR, kU>(P, a.p_full, a.q_loc, a.p_full + r0, d1, d2, red, (const T*)nullptr, vb, vg);
+        if (threadIdx.x == 0) P.bpart[vb * 4 + 0] = d1;
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
         T sig[1];
-        grid_total<1>(P.bpart, 0, sig, red);
+        grid_total<1>(P.bpart, 0, sig, red, vg);
         T sigma = sig[0];
         if (a.peer && a.ll) {                           // A2 fused C2, LL words
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 const double v = (double)sigma;
                 ll_push_scal(a, (int)(k & 1), 0, &v, 1, ll_epoch(st, k));
             }
             if (!ll_sum_scal<1>(a, (int)(k & 1), 0, ll_epoch(st, k), sig)) return;
             sigma = sig[0];
         } else if (a.peer) {                            // A2 fused C2
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 for (int g = 0; g < L.P; ++g) a.pp.S[g][(k & 1) * a.spar + L.rank * kScalSlot] = sigma;
                 flags_out(a, kPhaseS, k);
             }
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
             sigma = scal_sum(L, par_ptr(a.S, a.spar, k), 0);
         }
         if (!(sigma > T(0))) {                           // Q9
-            if (lead()) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
+            if ((vb == 0 && threadIdx.x == 0)) { st->status = KS_ENOTSPD; st->iters = k - 1; st->done = 1; }
             break;
         }
         const T alpha = (T)st->rho[(k - 1) & 3] / sigma;
@@ -90,20 +91,20 @@ __global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
         }
         if (a.peer && !a.ll && tid0 < m) __threadfence_system();   // only threads that stored remotely
         block_sum<kNT, 1>(acc, red);
-        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = acc[0];
-        if (!grid_sync(P.bar, st)) return;
+        if (threadIdx.x == 0) P.bpart[vb * 4 + 1] = acc[0];
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
         T rr[1];
-        grid_total<1>(P.bpart, 1, rr, red);
+        grid_total<1>(P.bpart, 1, rr, red, vg);
         T rho1 = rr[0];
         if (a.peer && a.ll) {                           // rho' rank partials, LL words
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 const double v = (double)rho1;
                 ll_push_scal(a, (int)(k & 1), 1, &v, 1, ep);
             }
             if (!ll_sum_scal<1>(a, (int)(k & 1), 1, ep, rr)) return;
             rho1 = rr[0];
         } else if (a.peer) {                            // A4 fused C1 (+ partials)
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_r[g][ro + L.pslot + 1] = rho1;
                 flags_out(a, kPhaseR, k);
             }
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
         // A5: test, beta, p = r + beta p (full, replicated)
         const T rel = sqrt(rho1) / (T)st->nb;
         if (rel <= (T)st->tol) {
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 put_hist(st, a.hist, k - 1, rel);
                 st->relres = rel; st->iters = k; st->converged = 1; st->status = KS_OK; st->done = 1;
             }
@@ -137,25 +138,25 @@ __global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
                 a.p_full[j] = fma(beta, a.p_full[j], Gr[gj]);
             }
         }
-        if (lead()) {
+        if ((vb == 0 && threadIdx.x == 0)) {
             put_hist(st, a.hist, k - 1, rel);
             st->relres = rel; st->iters = k; st->rho[k & 3] = rho1; st->alpha[k & 3] = alpha;
             if (!a.peer) a.G_r[ro + L.pslot + 1] = rho1;    // for the multi-kernel path / finish
         }
-        if (!grid_sync(P.bar, st)) return;
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
     }
 }
 
 // ---------------------------------------------------------- BiCGSTAB (B1-B8)
-template <class T, int kR, int kU, int kMinB = 4>
-__global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
+template <class T, int kR, int kU>
+__device__ __forceinline__ void bs_persist_body(const PersistArgs<T>& P, int vb, int vg) {
     __shared__ T red[(kR > 2 ? kR : 2) * kNW];
     const VecArgsT<T>& a = P.a;
     const Layout& L = a.L;
     DevState* st = a.st;
     const int64_t m = rows_of(L), r0 = L.row0[L.rank];
-    const int64_t gstride = (int64_t)gridDim.x * kNT;
-    const int64_t tid0 = (int64_t)blockIdx.x * kNT + threadIdx.x;
+    const int64_t gstride = (int64_t)vg * kNT;
+    const int64_t tid0 = (int64_t)vb * kNT + threadIdx.x;
     // scalars of the previous iteration (written by the previous launch / init)
     T rho_prev = (T)st->rho[(P.k0 - 1) & 3], alpha_prev = (T)st->alpha[(P.k0 - 1) & 3];
     T omega_prev = (T)st->omega[(P.k0 - 1) & 3];
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         if (i >= 2) {
             rel = sqrt(carried ? rr_next : llx ? rv_prev[1] : slot_sum(L, Gr, 1)) / (T)st->nb;
             if (rel <= (T)st->tol) {
-                if (lead()) {
+                if ((vb == 0 && threadIdx.x == 0)) {
                     put_hist(st, a.hist, i - 2, rel);
                     st->relres = rel; st->iters = i - 1; st->converged = 1; st->status = KS_OK; st->done = 1;
                 }
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
             }
         }
         if (rho == T(0) || !isfinite(rho)) {
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
                 st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1;
             }
@@ -215,23 +216,23 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
                 a.p_full[j] = fma(beta, fma(-omega_prev, a.v_full[j], a.p_full[j]), Gr[gj]);
             }
         }
-        if (lead()) {
+        if ((vb == 0 && threadIdx.x == 0)) {
             if (i >= 2) { put_hist(st, a.hist, i - 2, rel); st->relres = rel; }
             st->rho[i & 3] = rho;
             st->iters = i - 1;
         }
-        if (!grid_sync(P.bar, st)) return;
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
         // B3: v = A p (own chunk of G_v[i&1]), <rhat, v>_g
         const int64_t vo = (i & 1) * a.gpar + (int64_t)L.rank * L.chunk;
         T d1, d2;
-        gemv_phase<kR, kU>(P, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red);
-        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 0] = d1;
-        if (!grid_sync(P.bar, st)) return;
+        gemv_phase<kR, kU>(P, a.p_full, a.G_v + vo, a.rhat_loc, d1, d2, red, (const T*)nullptr, vb, vg);
+        if (threadIdx.x == 0) P.bpart[vb * 4 + 0] = d1;
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
         T gm[1];
-        grid_total<1>(P.bpart, 0, gm, red);
+        grid_total<1>(P.bpart, 0, gm, red, vg);
         T gam = gm[0];
         if (llx) {                                      // B2/B4: v rows and the rank partial as LL words
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 const double g1 = (double)gam;
                 ll_push_scal(a, par, 0, &g1, 1, ep);
             }
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
             if (!ll_sum_scal<1>(a, par, 0, ep, gm)) return;
             gam = gm[0];
         } else if (a.peer) {                            // B2/B4: v pulled, partial pushed
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 for (int g = 0; g < L.P; ++g) a.pp.G_v[g][vo + L.pslot] = gam;
                 flags_out(a, kPhaseV, i);
             }
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
             gam = slot_sum(L, par_ptr(a.G_v, a.gpar, i), 0);
         }
         if (gam == T(0) || !isfinite(gam)) {
-            if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+            if ((vb == 0 && threadIdx.x == 0)) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
             break;
         }
         const T alpha = rho / gam;
@@ -289,14 +290,14 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
             }
         }
         block_sum<kNT, 1>(sacc, red);
-        if (threadIdx.x == 0) P.bpart[blockIdx.x * 4 + 1] = sacc[0];
-        if (!grid_sync(P.bar, st)) return;
+        if (threadIdx.x == 0) P.bpart[vb * 4 + 1] = sacc[0];
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
         T ssv[1];
-        grid_total<1>(P.bpart, 1, ssv, red);
+        grid_total<1>(P.bpart, 1, ssv, red, vg);
         const T srel = sqrt(ssv[0]) / (T)st->nb;
         if (srel <= (T)st->tol) {                          // half-step exit
             for (int64_t l = tid0; l < m; l += gstride) a.x_loc[l] = fma(alpha, a.p_full[r0 + l], a.x_loc[l]);
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 put_hist(st, a.hist, i - 1, srel);
                 st->alpha[i & 3] = alpha;
                 st->relres = srel; st->half = 1; st->half_iter = i; st->converged = 1;
@@ -305,14 +306,14 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
             break;
         }
         // B6: t = A s (q_loc), <t, s_loc>_g, <t, t>_g
-        gemv_phase<kR, kU>(P, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red);
-        if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 2] = d1; P.bpart[blockIdx.x * 4 + 3] = d2; }
-        if (!grid_sync(P.bar, st)) return;
+        gemv_phase<kR, kU>(P, a.s_full, a.q_loc, a.s_full + r0, d1, d2, red, (const T*)nullptr, vb, vg);
+        if (threadIdx.x == 0) { P.bpart[vb * 4 + 2] = d1; P.bpart[vb * 4 + 3] = d2; }
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
         T tv[2];
-        grid_total<2>(P.bpart, 2, tv, red);
+        grid_total<2>(P.bpart, 2, tv, red, vg);
         T ts = tv[0], tt = tv[1];
         if (llx) {                                      // B7 C2 as LL words
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 const double w2[2] = {(double)ts, (double)tt};
                 ll_push_scal(a, par, 2, w2, 2, ep);
             }
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
             ts = tv[0];
             tt = tv[1];
         } else if (a.peer) {                            // B7 fused C2
-            if (lead()) {
+            if ((vb == 0 && threadIdx.x == 0)) {
                 for (int g = 0; g < L.P; ++g) {
                     a.pp.S[g][(i & 1) * a.spar + L.rank * kScalSlot + 0] = ts;
                     a.pp.S[g][(i & 1) * a.spar + L.rank * kScalSlot + 1] = tt;
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         }
         const T om = ts / tt;
         if (tt == T(0) || !isfinite(tt) || om == T(0) || !isfinite(om)) {
-            if (lead()) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
+            if ((vb == 0 && threadIdx.x == 0)) { st->status = KS_EBREAKDOWN; st->breakdown = 1; st->iters = i - 1; st->done = 1; }
             break;
         }
         // B7: x += alpha p + omega s; r = s - omega t; <rhat, r>_g, <r, r>_g
@@ -357,11 +358,11 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         }
         if (a.peer && !llx && tid0 < m) __threadfence_system();   // only threads that stored remotely
         block_sum<kNT, 2>(acc, red);
-        if (threadIdx.x == 0) { P.bpart[blockIdx.x * 4 + 0] = acc[0]; P.bpart[blockIdx.x * 4 + 1] = acc[1]; }
-        if (!grid_sync(P.bar, st)) return;
+        if (threadIdx.x == 0) { P.bpart[vb * 4 + 0] = acc[0]; P.bpart[vb * 4 + 1] = acc[1]; }
+        if (!grid_sync_n(P.bar, st, (unsigned)vg)) return;
         T rv[2];
-        grid_total<2>(P.bpart, 0, rv, red);
-        if (lead()) {
+        grid_total<2>(P.bpart, 0, rv, red, vg);
+        if ((vb == 0 && threadIdx.x == 0)) {
             if (llx) {                                  // consumed at the top of i + 1
                 const double w2[2] = {(double)rv[0], (double)rv[1]};
                 ll_push_scal(a, par, 1, w2, 2, ep);
@@ -389,6 +390,36 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
         // fused: the next iteration waits on the R flags; P == 1: the values are
         // carried in registers and the lead's slots are read only by the next launch
     }
+}
+
+template <class T, int kR, int kU, int kMinB = 4>
+__global__ void __launch_bounds__(kNT, kMinB) k_cg_persist(PersistArgs<T> P) {
+    cg_persist_body<T, kR, kU>(P, (int)blockIdx.x, (int)gridDim.x);
+}
+template <class T, int kR, int kU, int kMinB = 4>
+__global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
+    bs_persist_body<T, kR, kU>(P, (int)blockIdx.x, (int)gridDim.x);
+}
+
+// Ranks sharing one GPU (ks_create_on): every rank's persistent kernel as ONE
+// cooperative launch of P * g CTAs -- CTA b serves rank b / g as its block b % g, with
+// its rank's arguments -- so the CTAs that wait on each other's exchanges are
+// co-resident by construction (separate launches on one GPU would not be).
+constexpr int kMaxEmuP = 8;
+template <class T>
+struct PersistEmuArgs {
+    PersistArgs<T> p[kMaxEmuP];
+    int P, g;
+};
+template <class T, int kR, int kU>
+__global__ void __launch_bounds__(kNT, 4) k_cg_persist_emu(const __grid_constant__ PersistEmuArgs<T> E) {
+    const int rk = (int)blockIdx.x / E.g;
+    cg_persist_body<T, kR, kU>(E.p[rk], (int)blockIdx.x - rk * E.g, E.g);
+}
+template <class T, int kR, int kU>
+__global__ void __launch_bounds__(kNT, 4) k_bs_persist_emu(const __grid_constant__ PersistEmuArgs<T> E) {
+    const int rk = (int)blockIdx.x / E.g;
+    bs_persist_body<T, kR, kU>(E.p[rk], (int)blockIdx.x - rk * E.g, E.g);
 }
 
 // Persistent GEMV shape: default R=2, U=4 (the sweep's best: CG 211.5 / BiCGSTAB
@@ -465,6 +496,51 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
     }
     e = cudaLaunchCooperativeKernel(pick<T>(bicgstab, rows, unroll), dim3((unsigned)grid),
                                                 dim3(kNT), args, 0, st);
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+// ---- emulated ranks (all on one GPU): one cooperative launch for every rank -------
+namespace {
+const void* pick_emu(int bicgstab, int rows, int unroll) {
+    const int shape = (rows == 4 && unroll == 2) ? 1 : (rows == 4 && unroll == 4) ? 2 : (rows == 1) ? 3 : 0;
+    if (bicgstab) {
+        return shape == 1 ? (const void*)k_bs_persist_emu<double, 4, 2>
+             : shape == 2 ? (const void*)k_bs_persist_emu<double, 4, 4>
+             : shape == 3 ? (const void*)k_bs_persist_emu<double, 1, 8> : (const void*)k_bs_persist_emu<double, 2, 4>;
+    }
+    return shape == 1 ? (const void*)k_cg_persist_emu<double, 4, 2>
+         : shape == 2 ? (const void*)k_cg_persist_emu<double, 4, 4>
+         : shape == 3 ? (const void*)k_cg_persist_emu<double, 1, 8> : (const void*)k_cg_persist_emu<double, 2, 4>;
+}
+}  // namespace
+
+int persist_emu_grid(int bicgstab, int num_sms, int P, int64_t mmax, int rows, int unroll) {
+    if (P < 2 || P > kMaxEmuP || num_sms < P) return 0;
+    return coop_grid(pick_emu(bicgstab, rows, unroll), num_sms / P, mmax, rows_of(rows, unroll));
+}
+
+int launch_persist_emu(int bicgstab, const VecArgs* const* a, const double* const* A, int64_t lda, int64_t ncols,
+                       double* const* bpart, unsigned* const* bar, long long k0, long long k1, int P, int g,
+                       int rows, int unroll, cudaStream_t st) {
+    if (P < 2 || P > kMaxEmuP || g < 1) return -(int)cudaErrorInvalidValue;
+    PersistEmuArgs<double> E;
+    std::memset(&E, 0, sizeof E);
+    for (int h = 0; h < P; ++h) {
+        PersistArgs<double>& Q = E.p[h];
+        Q.a = *a[h];
+        Q.A = A[h];
+        Q.lda = lda;
+        Q.ncols = ncols;
+        Q.bpart = bpart[h];
+        Q.bar = bar[h];
+        Q.k0 = k0;
+        Q.k1 = k1;
+    }
+    E.P = P;
+    E.g = g;
+    void* args[] = {&E};
+    const cudaError_t e = cudaLaunchCooperativeKernel(pick_emu(bicgstab, rows, unroll), dim3((unsigned)(P * g)),
+                                                      dim3(kNT), args, 0, st);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 

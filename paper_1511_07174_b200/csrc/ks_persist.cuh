@@ -39,7 +39,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned 
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ bool grid_sync(unsigned* bar, DevState* st) {
+// nb = the CTAs that meet (gridDim.x, or one rank's CTAs of an emulated launch).
+__device__ bool grid_sync_n(unsigned* bar, DevState* st, unsigned nb) {
     __shared__ int s_ok;
     __shared__ unsigned s_jit;
     __syncthreads();
@@ -50,7 +51,7 @@ __device__ bool grid_sync(unsigned* bar, DevState* st) {
         unsigned long long* cnt = reinterpret_cast<unsigned long long*>(bar);
         __threadfence();
         const unsigned long long old = atomicAdd(cnt, 1ull);
-        const unsigned long long target = (old / gridDim.x + 1ull) * gridDim.x;
+        const unsigned long long target = (old / nb + 1ull) * nb;
         if (old + 1ull != target) {
             const unsigned long long t0 = globaltimer_ns();
             while (ld_acquire_gpu_u64(cnt) < target) {
@@ -70,18 +71,23 @@ __device__ bool grid_sync(unsigned* bar, DevState* st) {
     jitter_at(s_jit, 2u);                         // departure order of the warps
     return s_ok != 0;
 }
+__device__ __forceinline__ bool grid_sync(unsigned* bar, DevState* st) { return grid_sync_n(bar, st, gridDim.x); }
 
 // Sum over CTAs (in CTA order, fixed tree) of slot q of the per-CTA partials;
 // every CTA computes the same value.
 template <int K, class T>
-__device__ __forceinline__ void grid_total(const T* bpart, int q0, T (&out)[K], T* red) {
+__device__ __forceinline__ void grid_total(const T* bpart, int q0, T (&out)[K], T* red, int nb) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         T acc = T(0);
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += kNT) acc += __ldcg(bpart + (int64_t)b * 4 + q0 + k);
+        for (int b = threadIdx.x; b < nb; b += kNT) acc += __ldcg(bpart + (int64_t)b * 4 + q0 + k);
         out[k] = acc;
     }
     block_sum<kNT, K>(out, red);
+}
+template <int K, class T>
+__device__ __forceinline__ void grid_total(const T* bpart, int q0, T (&out)[K], T* red) {
+    grid_total<K>(bpart, q0, out, red, (int)gridDim.x);
 }
 
 // Fused-mode wait for phase ph of iteration k from every rank (all CTAs).
@@ -183,13 +189,13 @@ struct PersistArgs {
 // accumulated in tile order.
 template <int kR, int kU, class T>
 __device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w1, T& d1, T& d2,
-                           T* red, const T* bsub = nullptr) {
+                           T* red, const T* bsub, int vb, int vg) {
     const int64_t m = rows_of(P.a.L);
     const int64_t tiles = (m + kR - 1) / kR;
     const int64_t ncb = P.ncols / (Vec16<T>::W * kNT);
     d1 = T(0);
     d2 = T(0);
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    for (int64_t tile = vb; tile < tiles; tile += vg) {
         const int64_t r0 = tile * kR;
         const int nvalid = (int)min((int64_t)kR, m - r0);
         T acc[kR];

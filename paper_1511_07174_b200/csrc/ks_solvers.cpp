@@ -402,25 +402,39 @@ void fuse_gemv(const ks_ctx* c, const Rank& r, GemvParams& p, int phase, double*
     p.ebase = &r.st->ebase;
 }
 
-// Ranks sharing one GPU, n <= 1024, x0 = 0, the whole solve in one launch: the tiny
-// kernels of all ranks as ONE cooperative launch (their LL exchange between ranks is
-// the fused exchange's; one launch makes the waiting CTAs co-resident).  Returns the
-// per-rank CTA count, 0 when not applicable (then the host-collective schedule runs);
-// depends only on context state, so every rank decides the same.
-int tiny_emu_grid(const ks_ctx* c, int bicgstab, int64_t maxit) {
-    if (!c->shared_dev || c->P < 2 || c->dtype != KS_FLOAT64) return 0;
-    if (!c->opt.tiny || c->opt.small == 0 || c->opt.persistent == 0) return 0;
-    if (c->opt.poll_batch > 0 && c->opt.poll_batch < maxit) return 0;
+// Ranks sharing one GPU (ks_create_on with every rank on the same device), x0 = 0, the
+// whole solve in one launch: every rank's kernel in ONE cooperative launch over all
+// ranks' CTAs (rank = block / g) -- the tiny kernels for n <= 1024, else the persistent
+// kernels -- so the fused exchange between ranks (LL words / peer stores + flags) runs
+// with the waiting CTAs co-resident by construction.  The plan depends only on
+// context state, so every rank decides the same; g == 0: not applicable (the
+// host-collective schedule runs).
+struct EmuPlan {
+    int tiny = 0, g = 0, rows = 0, unroll = 0;
+};
+EmuPlan emu_plan(const ks_ctx* c, int bicgstab, int64_t maxit) {
+    EmuPlan e;
+    if (!c->shared_dev || c->P < 2 || c->dtype != KS_FLOAT64 || c->opt.persistent == 0) return e;
+    if (c->opt.poll_batch > 0 && c->opt.poll_batch < maxit) return e;
     for (const auto& h : c->ranks)
-        if (h.dev != c->ranks[0].dev || !h.llx) return 0;
+        if (h.dev != c->ranks[0].dev || !h.llg) return e;
     const Rank& r0 = c->ranks[0];                  // the first ranks hold the extra rows
-    const int g = tiny_grid(bicgstab, r0.num_sms, c->n, r0.m, c->ld);
-    if (g == 0 || !tiny_emu_fits(bicgstab, c->ld, c->P * g, r0.num_sms)) return 0;
-    return g;
+    if (c->opt.tiny && c->opt.small != 0 && r0.llx) {
+        const int g = tiny_grid(bicgstab, r0.num_sms, c->n, r0.m, c->ld);
+        if (g > 0 && tiny_emu_fits(bicgstab, c->ld, c->P * g, r0.num_sms)) {
+            e.tiny = 1;
+            e.g = g;
+            return e;
+        }
+    }
+    e.rows = c->opt.gemv_rows ? (int)c->opt.gemv_rows : (r0.L.pslot <= 4096 ? 4 : 2);
+    e.unroll = c->opt.gemv_unroll ? (int)c->opt.gemv_unroll : (e.rows == 4 ? 2 : 4);
+    e.g = persist_emu_grid(bicgstab, r0.num_sms, c->P, r0.L.pslot, e.rows, e.unroll);
+    return e;
 }
 
-int64_t run_tiny_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, int64_t maxit,
-                     double* x, double* hist, int64_t hist_cap, ks_report* rep, int g) {
+int64_t run_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, int64_t maxit,
+                double* x, double* hist, int64_t hist_cap, ks_report* rep, const EmuPlan& plan) {
     const auto t_start = Clock::now();
     r.launches = 0;
     r.gemv_launches = 0;
@@ -430,9 +444,9 @@ int64_t run_tiny_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double t
     r.epoch_next += (unsigned long long)maxit + 2;
     r.x0_full = nullptr;
     KS_CUDA(cudaMemcpyAsync(r.b_full, b, (size_t)c->n * sizeof(double), cudaMemcpyDefault, r.stream));
-    // rows A0 / B0 + state init in the fused layout; no rendezvous (no cross-launch wait)
+    // rows A0 / B0 + state init in the fused layout (also zeroes the grid-barrier
+    // counter); no rendezvous (no cross-launch wait)
     r.launches += launch_start(r.vargs(true), bicgstab, tol, maxit, hist_cap, ebase, 0, r.stream);
-    r.bar_zeroed = true;
     KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
     host_launch_once(c, r, [&] {
         VecArgs va[kMaxRanks];
@@ -440,23 +454,31 @@ int64_t run_tiny_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double t
         const double* Av[kMaxRanks];
         uint64_t* llv[kMaxRanks];
         uint64_t* const* llpv[kMaxRanks];
+        double* bp[kMaxRanks];
+        unsigned* bar[kMaxRanks];
         for (int h = 0; h < c->P; ++h) {
-            const Rank& rh = c->ranks[(size_t)h];
+            Rank& rh = c->ranks[(size_t)h];
             va[h] = rh.vargs(true);
             av[h] = &va[h];
             Av[h] = rh.A;
             llv[h] = rh.llx;
             llpv[h] = rh.llpeer;
+            bp[h] = rh.scr.part + 2 * kPartStride;
+            bar[h] = rh.scr.ticket + 8;
         }
-        const int rc = launch_tiny_emu(bicgstab, av, Av, c->ld, llv, llpv, c->P, g, r.stream);
+        const int rc = plan.tiny
+            ? launch_tiny_emu(bicgstab, av, Av, c->ld, llv, llpv, c->P, plan.g, r.stream)
+            : launch_persist_emu(bicgstab, av, Av, c->ld, c->ld, bp, bar, 1, maxit, c->P, plan.g, plan.rows,
+                                 plan.unroll, r.stream);
         if (rc < 0) KS_CUDA((cudaError_t)(-rc));
         r.launches += 1;
     });
     r.bar_zeroed = false;
-    r.gemv_launches = 0;
     KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    // tiny: the kernels wrote the full x into every rank's X; persistent: x is gathered
+    // by the host collective (pack + allgather), as on the host-collective schedule
     finish_and_copy(c, r, x, hist, hist_cap, rep, bicgstab != 0, t_start, maxit, 1,
-                    ebase + (unsigned long long)maxit + 1, true);
+                    ebase + (unsigned long long)maxit + 1, plan.tiny != 0);
     r.gemv_launches = bicgstab ? 2 * r.h_state->iters - (r.h_state->half ? 1 : 0) : r.h_state->iters;
     if (rep) rep->gemv_launches = r.gemv_launches;
     return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
@@ -464,11 +486,13 @@ int64_t run_tiny_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double t
 
 int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol, int64_t maxit,
                double* x, double* hist, int64_t hist_cap, ks_report* rep) {
-    if (!x0)
-        if (const int g = tiny_emu_grid(c, 0, maxit)) {
+    if (!x0) {
+        const EmuPlan plan = emu_plan(c, 0, maxit);
+        if (plan.g > 0) {
             check_loaded(c, r);
-            return run_tiny_emu(c, r, 0, b, tol, maxit, x, hist, hist_cap, rep, g);
+            return run_emu(c, r, 0, b, tol, maxit, x, hist, hist_cap, rep, plan);
         }
+    }
     const auto t_start = Clock::now();
     check_loaded(c, r);
     r.launches = 0;
@@ -511,11 +535,13 @@ int64_t run_cg(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol
 
 int64_t run_bicgstab(ks_ctx* c, Rank& r, const double* b, const double* x0, double tol,
                      int64_t maxit, double* x, double* hist, int64_t hist_cap, ks_report* rep) {
-    if (!x0)
-        if (const int g = tiny_emu_grid(c, 1, maxit)) {
+    if (!x0) {
+        const EmuPlan plan = emu_plan(c, 1, maxit);
+        if (plan.g > 0) {
             check_loaded(c, r);
-            return run_tiny_emu(c, r, 1, b, tol, maxit, x, hist, hist_cap, rep, g);
+            return run_emu(c, r, 1, b, tol, maxit, x, hist, hist_cap, rep, plan);
         }
+    }
     const auto t_start = Clock::now();
     check_loaded(c, r);
     r.launches = 0;

@@ -210,6 +210,47 @@ def test_multi_persistent_fused(lay):
     bars(xc, hc, rc, xo, ho, ro)
 
 
+@pytest.mark.parametrize("lay", layouts(gpus=(), shared=(2, 4)))
+def test_emulated_ranks_persistent_one_gpu(lay):
+    """P ranks on ONE GPU run the fused persistent kernels (A4 / B2 over the fused
+    exchange, NEXT-1) as ONE cooperative launch over all ranks' CTAs (rank = block /
+    g): the CTAs that wait on each other's LL words / flags are co-resident by
+    construction.  CG and BiCGSTAB vs the oracle, a fixed-length BiCGSTAB (k_end's
+    last-step test), LL vs flag handovers bitwise equal, jitter at every sync point
+    bitwise equal, and the launch count of one emulated launch per solve."""
+    P = need(lay)
+    n = 4100
+    D, bd = synth.gdd(n, 16)
+    Cs, cs, bs = synth.gspd(4096, 1e4)
+    with context(n, lay) as ctx, context(4096, lay) as cc:
+        ctx.generate("dd", seed=synth.SEED, kd=16, want_b=False)
+        cc.generate("spd", seed=synth.SEED, table=cs, want_b=False)
+        res = {}
+        for ll, jit in ((1, 0), (0, 0), (1, 7), (0, 0x9E3779B1)):
+            for cx in (ctx, cc):
+                cx.set_option("ll_xchg", ll)
+                cx.set_option("jitter", jit)
+            res[(ll, jit)] = (ctx.bicgstab(bd, tol=1e-10), cc.cg(bs, tol=1e-10),
+                              ctx.bicgstab(bd, tol=0.0, maxit=9))
+        ref = res[(1, 0)]
+        for key, val in res.items():
+            for (x, h, r), (xr, hr, rr) in zip(val, ref):
+                assert r.iterations == rr.iterations and r.status == rr.status, key
+                assert np.array_equal(x, xr) and np.array_equal(h, hr), key
+        for _, _, r in ref:
+            assert r.kernel_launches <= 8, r.kernel_launches      # one emulated launch per solve
+    xo, ho, ro = oracle.bicgstab(D, bd, tol=1e-10)
+    x, h, r = ref[0]
+    bars(x, h, r, xo, ho, ro, floor=FLOOR_BS)
+    xo, ho, ro = oracle.cg(Cs, bs, tol=1e-10)
+    x, h, r = ref[1]
+    bars(x, h, r, xo, ho, ro)
+    xo, ho, ro = oracle.bicgstab(D, bd, tol=0.0, maxit=9)
+    x, h, r = ref[2]
+    assert r.status == ks.KS_EMAXIT and r.iterations == 9
+    bars(x, h, r, xo, ho, ro, iters_tol=0, floor=FLOOR_BS)
+
+
 @pytest.mark.parametrize("lay", layouts(shared=()))
 def test_ll_handovers_bitwise_equal_flags(lay):
     """KS_OPT_LL_XCHG: the persistent kernels over P GPUs hand the r / v slices and the
