@@ -185,11 +185,12 @@ ks_status ks_create(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t ngpus);
  * runs kernels that wait on each other (separate launches on one GPU have no
  * co-residency guarantee): its collectives are host-driven peer copies ordered by
  * events, KS_OPT_FUSED_COMM is 0 and cannot be set, and the kernels that need the
- * fused exchange at P > 1 (persistent, small-n, multi-RHS) are not used.  Exception:
- * with every rank on one GPU, CG / BiCGSTAB at n <= 1024 with x0 = NULL run the tiny
- * kernels of all ranks as ONE cooperative launch (rank = block / CTAs per rank), so
- * their LL exchange between ranks runs with co-residency guaranteed -- bitwise the
- * one-GPU result.  Otherwise results equal the oracle's within the same bars.
+ * fused exchange at P > 1 as separate launches are not used.  Instead, with every
+ * rank on one GPU, CG / BiCGSTAB with x0 = NULL (whole solve in one launch) run the
+ * fused persistent kernels -- or the tiny kernels for n <= 1024 -- of all ranks as
+ * ONE cooperative launch (rank = block / CTAs per rank), so their exchanges between
+ * ranks run with co-residency guaranteed.  Results equal the oracle's within the
+ * same bars (the tiny kernels: bitwise the one-GPU result).
  * KS_EARG for a bad device list, KS_EDIM for n < nranks.                         */
 ks_status ks_create_on(ks_ctx** out, int64_t n, ks_dtype dtype, int32_t nranks, const int32_t* devices);
 

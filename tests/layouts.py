@@ -5,9 +5,11 @@
 schedule -- row-block partition, allgathers of r / p / v ingredients, rank-ordered
 scalar sums, x gather -- through host-driven peer-copy collectives (no NCCL, no fused
 exchange: kernels that wait on each other are never launched separately on one GPU,
-B200_PROFILING.md).  It runs on any GPU box, so the allgather schedule of rows A4 / B2
-is checked against the oracle even where only one GPU exists; the fused NVLink kernels
-(NEXT-1) need the ("gpus", P) layouts.
+B200_PROFILING.md) -- except as ONE cooperative launch over all ranks' CTAs: CG /
+BiCGSTAB with x0 = 0 run the fused persistent / tiny kernels of all ranks that way.
+It runs on any GPU box, so rows A4 / B2 (host-collective and fused) and the fused
+exchange of NEXT-1 are checked against the oracle even where only one GPU exists;
+NVLink itself and the multi-process path need the ("gpus", P) layouts.
 """
 import pytest
 
