@@ -295,11 +295,14 @@ void setup(ks_ctx* c, Rank& r, const double* b, const double* x0, int64_t hist_c
 // call, no extra launch).  One stream synchronisation when the history is short.
 void finish_and_copy(ks_ctx* c, Rank& r, double* x, double* hist, int64_t hist_cap,
                      ks_report* rep, bool bicgstab, const Clock::time_point& t_start, int64_t maxit,
-                     int end_mode = 0, unsigned long long x_epoch = 0, bool x_ready = false) {
+                     int end_mode = 0, unsigned long long x_epoch = 0, bool x_ready = false,
+                     bool emulated = false) {
     VecArgs a = r.vargs(false);   // final x gather / true residual: NCCL, parity 0
     const bool fused_x = end_mode == 1 && c->P > 1 && c->fused();
-    if (end_mode == 1) r.launches += launch_end(r.vargs(c->fused()), bicgstab ? 1 : 0, fused_x ? 1 : 0,
-                                                x_epoch, r.stream);
+    // emulated ranks: the solve ran in the fused layout (parity-buffered slots), so
+    // k_end's last-step test reads it with the fused arguments (its flags are all set)
+    if (end_mode == 1) r.launches += launch_end(r.vargs(c->fused() || emulated), bicgstab ? 1 : 0,
+                                                fused_x ? 1 : 0, x_epoch, r.stream);
     // contiguous full x: P == 1 x_loc; fused: gathered into X by k_end; x_ready: the
     // emulated-rank tiny kernels wrote it into X
     const double* xsrc = c->P == 1 ? r.x_loc : (fused_x || x_ready) ? r.X : nullptr;
@@ -478,7 +481,7 @@ int64_t run_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     // tiny: the kernels wrote the full x into every rank's X; persistent: x is gathered
     // by the host collective (pack + allgather), as on the host-collective schedule
     finish_and_copy(c, r, x, hist, hist_cap, rep, bicgstab != 0, t_start, maxit, 1,
-                    ebase + (unsigned long long)maxit + 1, plan.tiny != 0);
+                    ebase + (unsigned long long)maxit + 1, plan.tiny != 0, true);
     r.gemv_launches = bicgstab ? 2 * r.h_state->iters - (r.h_state->half ? 1 : 0) : r.h_state->iters;
     if (rep) rep->gemv_launches = r.gemv_launches;
     return r.h_state->peer_timeout ? (int64_t)KS_ENCCL : r.h_state->status;
