@@ -450,7 +450,6 @@ int64_t run_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
     // rows A0 / B0 + state init in the fused layout (also zeroes the grid-barrier
     // counter); no rendezvous (no cross-launch wait)
     r.launches += launch_start(r.vargs(true), bicgstab, tol, maxit, hist_cap, ebase, 0, r.stream);
-    KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
     host_launch_once(c, r, [&] {
         VecArgs va[kMaxRanks];
         const VecArgs* av[kMaxRanks];
@@ -469,15 +468,21 @@ int64_t run_emu(ks_ctx* c, Rank& r, int bicgstab, const double* b, double tol, i
             bp[h] = rh.scr.part + 2 * kPartStride;
             bar[h] = rh.scr.ticket + 8;
         }
+        // loop time = the emulated launch alone (after the waits for every rank's start)
+        KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
         const int rc = plan.tiny
             ? launch_tiny_emu(bicgstab, av, Av, c->ld, llv, llpv, c->P, plan.g, r.stream)
             : launch_persist_emu(bicgstab, av, Av, c->ld, c->ld, bp, bar, 1, maxit, c->P, plan.g, plan.rows,
                                  plan.unroll, r.stream);
         if (rc < 0) KS_CUDA((cudaError_t)(-rc));
+        KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
         r.launches += 1;
     });
+    if (r.rank != 0) {                    // the launch ran on rank 0's stream
+        KS_CUDA(cudaEventRecord(r.ev_t0, r.stream));
+        KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
+    }
     r.bar_zeroed = false;
-    KS_CUDA(cudaEventRecord(r.ev_t1, r.stream));
     // tiny: the kernels wrote the full x into every rank's X; persistent: x is gathered
     // by the host collective (pack + allgather), as on the host-collective schedule
     finish_and_copy(c, r, x, hist, hist_cap, rep, bicgstab != 0, t_start, maxit, 1,
