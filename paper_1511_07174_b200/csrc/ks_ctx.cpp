@@ -533,8 +533,15 @@ GemvConfig gemv_config(const ks_ctx* c, const Rank& r) {
 }  // namespace ks
 
 void ks_ctx::for_each_rank(const std::function<void(ks::Rank&)>& fn) {
+    bool flushed = false;
+    int prev = 0;
     for (auto& r : ranks)                 // nothing of this context is in flight between calls
-        if (!r.retired.empty() && cudaSetDevice(r.dev) == cudaSuccess) ks::flush_retired(r);
+        if (!r.retired.empty()) {
+            if (!flushed && cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+            flushed = true;
+            if (cudaSetDevice(r.dev) == cudaSuccess) ks::flush_retired(r);
+        }
+    if (flushed && prev >= 0) cudaSetDevice(prev);   // the caller's current device
     if (ranks.size() == 1) {
         ks::cuda_check(cudaSetDevice(ranks[0].dev), "cudaSetDevice");
         cudaGetLastError();   // drop a stale, already-reported non-sticky error (e.g. an OOM)

@@ -302,6 +302,7 @@ int launch_small(int kind, const VecArgsT<T>& a, const T* A, int64_t lda, int64_
 // P > 1 (fused exchange): the LL words go over NVLink into every rank's buffer (llp,
 // a region of the exchange allocation), x0f = the full x0 or NULL.  m = this rank's rows.
 int tiny_grid(int bicgstab, int num_sms, int64_t n, int64_t m, int64_t ld);
+constexpr int kMaxEmuRanks = 8;     // ranks of one emulated launch (kernel-parameter budget)
 // Ranks sharing one GPU: every rank's persistent CG / BiCGSTAB kernel (FP64) as one
 // cooperative launch of P * g CTAs (rank h = block / g, arguments a[h], A[h], bpart[h],
 // bar[h]); persist_emu_grid = the per-rank CTA count for num_sms / P SMs, 0 = n/a.

@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kNT, kMinB) k_bs_persist(PersistArgs<T> P) {
 // cooperative launch of P * g CTAs -- CTA b serves rank b / g as its block b % g, with
 // its rank's arguments -- so the CTAs that wait on each other's exchanges are
 // co-resident by construction (separate launches on one GPU would not be).
-constexpr int kMaxEmuP = 8;
+constexpr int kMaxEmuP = kMaxEmuRanks;
 template <class T>
 struct PersistEmuArgs {
     PersistArgs<T> p[kMaxEmuP];

@@ -417,7 +417,8 @@ struct EmuPlan {
 };
 EmuPlan emu_plan(const ks_ctx* c, int bicgstab, int64_t maxit) {
     EmuPlan e;
-    if (!c->shared_dev || c->P < 2 || c->dtype != KS_FLOAT64 || c->opt.persistent == 0) return e;
+    if (!c->shared_dev || c->P < 2 || c->P > kMaxEmuRanks || c->dtype != KS_FLOAT64 || c->opt.persistent == 0)
+        return e;
     if (c->opt.poll_batch > 0 && c->opt.poll_batch < maxit) return e;
     for (const auto& h : c->ranks)
         if (h.dev != c->ranks[0].dev || !h.llg) return e;

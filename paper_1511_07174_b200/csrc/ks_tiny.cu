@@ -333,7 +333,7 @@ struct TinyArgs {
 // Ranks sharing one GPU (ks_create_on): all ranks' CTAs in ONE cooperative launch --
 // CTA b serves rank b / g as its block b % g -- so the CTAs that wait on each other's
 // LL words are co-resident by construction (separate launches would not be).
-constexpr int kMaxEmu = 8;
+constexpr int kMaxEmu = kMaxEmuRanks;
 struct TinyEmuArgs {
     TinyArgs t[kMaxEmu];
     int P, g;
