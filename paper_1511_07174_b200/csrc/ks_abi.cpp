@@ -576,7 +576,8 @@ ks_status ks_set_option(ks_ctx* c, ks_option opt, int64_t v) {
             if (v < 0 || v > 4096) return fail(c, KS_EARG, "poll batch must be in [0, 4096]");
             o.poll_batch = v; break;
         case KS_OPT_GEMV_ROWS:
-            if (v != 0 && v != 2 && v != 4 && v != 8 && v != 16) return fail(c, KS_EARG, "rows must be 0, 2, 4, 8 or 16");
+            if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8 && v != 16)
+                return fail(c, KS_EARG, "rows must be 0, 1 (persistent kernels only), 2, 4, 8 or 16");
             o.gemv_rows = v; break;
         case KS_OPT_GEMV_SPLIT:
             if (v < 0 || v > 64) return fail(c, KS_EARG, "split must be in [0, 64]");

@@ -427,6 +427,14 @@ __global__ void __launch_bounds__(kNT, 4) k_bs_persist_emu(const __grid_constant
 // (4,2) and (4,4) selectable through KS_OPT_GEMV_ROWS / KS_OPT_GEMV_UNROLL.
 // (1, 8): one-row tiles for shards whose 2-row tile count would leave a badly filled
 // last wave over the resident CTAs (ks_solvers.cpp persist_shape).
+// KS_GEMV_DEFER=1 (tuning): deferred row reductions in the persistent GEMV phase.
+int defer_gemv() {
+    static const int v = [] {
+        const char* e = std::getenv("KS_GEMV_DEFER");
+        return e && std::atoi(e) == 1 ? 1 : 0;
+    }();
+    return v;
+}
 // KS_PERSIST_OCC=5 (tuning): the default (2, 4) shape compiled for 5 CTAs per SM
 // (48 registers; the GEMV loop stays spill-free) instead of 4 (64 registers).
 bool occ5() {
@@ -488,6 +496,7 @@ int launch_persist(int bicgstab, const VecArgsT<T>& a, const T* A, int64_t lda, 
     P.bar = bar;
     P.k0 = k0;
     P.k1 = k1;
+    P.defer = defer_gemv();
     void* args[] = {&P};
     cudaError_t e = cudaSuccess;
     if (!bar_zeroed) {
@@ -535,6 +544,7 @@ int launch_persist_emu(int bicgstab, const VecArgs* const* a, const double* cons
         Q.bar = bar[h];
         Q.k0 = k0;
         Q.k1 = k1;
+        Q.defer = defer_gemv();
     }
     E.P = P;
     E.g = g;

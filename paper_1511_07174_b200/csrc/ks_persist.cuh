@@ -182,6 +182,7 @@ struct PersistArgs {
     T* bpart;           // gridDim.x * 4
     unsigned* bar;      // {count, generation}
     long long k0, k1;   // iteration range of this launch (inclusive)
+    int defer = 0;      // 1: deferred row reductions in the GEMV phase (gemv_phase)
 };
 
 // GEMV phase: y = A_loc x (or bsub - A_loc x) over the tiles of this CTA
@@ -195,6 +196,48 @@ __device__ void gemv_phase(const PersistArgs<T>& P, const T* x, T* y, const T* w
     const int64_t ncb = P.ncols / (Vec16<T>::W * kNT);
     d1 = T(0);
     d2 = T(0);
+    // Deferred row reductions (P.defer): each warp parks its row partials of every tile
+    // in shared memory and streams on -- no CTA barrier between tiles, so a CTA's loads
+    // never drain at a tile boundary (a tile of a 16384-column row is only 4 load steps).
+    // One barrier at the end; then each row's warp partials are added in warp order and
+    // the dot partials are a fixed-tree block sum (every thread returns them).
+    constexpr int kDeferRows = 256;
+    __shared__ T wp[kDeferRows * kNW];
+    const int64_t mine = tiles > vb ? (tiles - vb + vg - 1) / vg : 0;
+    if (P.defer && mine * kR <= kDeferRows) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        int nt = 0;
+        for (int64_t tile = vb; tile < tiles; tile += vg, ++nt) {
+            const int64_t r0 = tile * kR;
+            const int nvalid = (int)min((int64_t)kR, m - r0);
+            T acc[kR];
+            stream_rows<kR, kU, kNT>(P.A, P.lda, r0, nvalid, x, 0, ncb, acc);
+#pragma unroll
+            for (int r = 0; r < kR; ++r) acc[r] = warp_sum(acc[r]);
+            if (lane == 0) {
+#pragma unroll
+                for (int r = 0; r < kR; ++r) wp[(nt * kR + r) * kNW + w] = acc[r];
+            }
+        }
+        __syncthreads();
+        T v2[2] = {T(0), T(0)};
+        for (int j = threadIdx.x; j < nt * kR; j += kNT) {
+            const int64_t row = ((int64_t)vb + (int64_t)(j / kR) * vg) * kR + (j % kR);
+            if (row < m) {
+                T sum = T(0);
+#pragma unroll
+                for (int ww = 0; ww < kNW; ++ww) sum += wp[j * kNW + ww];
+                const T yv = bsub ? bsub[row] - sum : sum;
+                y[row] = yv;
+                if (w1) v2[0] = fma(w1[row], yv, v2[0]);
+                v2[1] = fma(yv, yv, v2[1]);
+            }
+        }
+        block_sum<kNT, 2>(v2, red);
+        d1 = v2[0];
+        d2 = v2[1];
+        return;
+    }
     for (int64_t tile = vb; tile < tiles; tile += vg) {
         const int64_t r0 = tile * kR;
         const int nvalid = (int)min((int64_t)kR, m - r0);
