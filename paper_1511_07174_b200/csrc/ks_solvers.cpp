@@ -36,9 +36,12 @@ void persist_shape(const ks_ctx* c, const Rank& r, int* rows, int* unroll) {
         const int64_t waves = (tiles + G - 1) / G;
         return (double)tiles / (double)(waves * G);
     };
-    const int def_r = m <= 4096 ? 4 : 2;
+    // rows of <= 16384 columns (128 KiB): one-row tiles stream faster on one B200 --
+    // n = 16384: CG 320.1 -> 313.8 us, BiCGSTAB 646.2 -> 630.7 us; n = 8192: 92.3 ->
+    // 87.1 / 183.4 -> 176.7 us per iteration (profiles/r02_defer_ab.jsonl, rows 0 vs 1)
+    const int def_r = m <= 4096 ? 4 : (c->ld <= 16384 ? 1 : 2);
     *rows = def_r;
-    *unroll = def_r == 4 ? 2 : 4;
+    *unroll = def_r == 4 ? 2 : def_r == 1 ? 8 : 4;
     double best = fill(def_r);
     for (int R : {2, 1}) {
         if (R == def_r) continue;
