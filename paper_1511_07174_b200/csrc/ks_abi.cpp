@@ -666,7 +666,7 @@ ks_status ks_get_option(const ks_ctx* c, ks_option opt, int64_t* v) {
         case KS_OPT_JOIN_TIMEOUT_MS: *v = o.join_timeout_ms; break;
         case KS_OPT_TINY: *v = o.tiny; break;
         case KS_OPT_JITTER: *v = o.jitter; break;
-        case KS_OPT_LL_XCHG: *v = (o.ll_xchg && c->fused()) ? 1 : 0; break;   // effective value
+        case KS_OPT_LL_XCHG: *v = (o.ll_xchg && (c->fused() || c->shared_dev)) ? 1 : 0; break;   // effective
         default: return fail(const_cast<ks_ctx*>(c), KS_EARG, "unknown option");
     }
     return KS_OK;
